@@ -1,0 +1,233 @@
+/*
+ * mgx.h — C-ABI of the B200-native data-parallel training step.
+ *
+ * This is the drop-in boundary for the reference's hot path (minigraph, the
+ * Python restatement of arXiv 1512.01274 under /root/reference/pkg/src).  The
+ * reference exposes its flat foreign-call surface in capi.py; every function
+ * here follows the same conventions (capi.py:26-29, 102-116):
+ *   - return an int status: 0 OK, 1 BAD_HANDLE, 2 BAD_ARGUMENT, 3 INTERNAL;
+ *   - results go through out-parameters;
+ *   - a thread-local last-error string explains any non-zero status.
+ * Pointers are CUDA device pointers (plain addresses, no torch types); streams
+ * are cudaStream_t values passed as uintptr_t (0 = legacy default stream).
+ *
+ * Each entry point cites the reference interface it replaces (file:line,
+ * paths relative to /root/reference/pkg/src/minigraph/).
+ */
+#ifndef MGX_H_
+#define MGX_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------ status codes
+ * capi.py:26-29 */
+#define MGX_OK 0
+#define MGX_BAD_HANDLE 1
+#define MGX_BAD_ARGUMENT 2
+#define MGX_INTERNAL 3
+
+/* Thread-local message for the last failing call (capi.py:95-97). */
+const char* mgx_last_error_message(void);
+/* ABI version (bumped on any signature change). */
+int mgx_abi_version(int* out);
+
+/* ------------------------------------------------------- device & memory
+ * Replaces tensor.py Buffer (tensor.py:42-52) and the engine's tags
+ * (engine.py:89-92): storage is device memory, ordering is a CUDA stream. */
+int mgx_device_count(int* out);
+int mgx_set_device(int device);
+int mgx_malloc(size_t nbytes, void** out);          /* cudaMalloc: IPC-exportable */
+int mgx_free(void* ptr);
+int mgx_host_alloc(size_t nbytes, void** out);      /* pinned host memory */
+int mgx_host_free(void* ptr);
+int mgx_stream_create(uintptr_t* out);
+int mgx_stream_destroy(uintptr_t stream);
+int mgx_stream_sync(uintptr_t stream);              /* to_host / wait_for sync point (tensor.py:132-137, engine.py:200-209) */
+int mgx_memcpy_async(void* dst, const void* src, size_t nbytes, uintptr_t stream); /* load_host / to_host copies (tensor.py:140-147) */
+int mgx_memset_async(void* dst, int value, size_t nbytes, uintptr_t stream);
+int mgx_event_create(uintptr_t* out);               /* timing-enabled event */
+int mgx_event_destroy(uintptr_t ev);
+int mgx_event_record(uintptr_t ev, uintptr_t stream);
+int mgx_event_elapsed_ms(uintptr_t start, uintptr_t end, float* out);
+int mgx_stream_wait_event(uintptr_t stream, uintptr_t ev);
+
+/* CUDA IPC for the multi-process KVStore: peer replicas and barrier flags are
+ * mapped into every rank (replaces the L1/L2 queues, kvstore.py:52-82). */
+#define MGX_IPC_HANDLE_BYTES 64
+int mgx_ipc_get_handle(void* dev_ptr, void* handle_out /* 64 bytes */);
+int mgx_ipc_open_handle(const void* handle /* 64 bytes */, void** out);
+int mgx_ipc_close_handle(void* dev_ptr);
+
+/* ------------------------------------------------------ tensor primitives
+ * tensor.py:103-231 and kernels.py:50-53.  n = element count, fp32. */
+int mgx_fill(float* y, int64_t n, float value, uintptr_t stream);             /* zeros/ones, ZerosLike (ops.py:362-373) */
+int mgx_copy(const float* x, float* y, int64_t n, uintptr_t stream);          /* copy_to (tensor.py:223-231), Flatten (ops.py:335-357) */
+int mgx_axpy(float alpha, const float* x, float* y, int64_t n, uintptr_t stream); /* y = y + x*alpha (kernels.py:50-53) */
+/* op: 0 add, 1 sub, 2 mul, 3 div (tensor.py:169-190, ops.py:222-250) */
+int mgx_elementwise(int op, const float* a, const float* b, float* out, int64_t n, uintptr_t stream);
+/* op: 0 add, 1 mul (tensor.py:193-203, ops.py:281-318) */
+int mgx_scalar_op(int op, const float* a, float c, float* out, int64_t n, uintptr_t stream);
+
+/* ------------------------------------------------------- dense operators
+ * Exact-order fp32 kernels: they reproduce the reference's numpy reduction
+ * orders with separately rounded mul/add. */
+
+/* act: 0 none, 1 relu, 2 sigmoid, 3 tanh (ops.py:138-171). */
+#define MGX_ACT_NONE 0
+#define MGX_ACT_RELU 1
+#define MGX_ACT_SIGMOID 2
+#define MGX_ACT_TANH 3
+
+/* C[m,n] = pairwise_k(A[m,k]*B[n,k]) (+ bias[n]) then act.  numpy pairwise
+ * summation over k (kernels.py:20-29 via ops.py:102-106: FC forward).
+ * lda/ldb/ldc are row strides in elements; bias may be NULL. */
+int mgx_gemm_pairwise(const float* A, int64_t lda, const float* B, int64_t ldb,
+                      const float* bias, float* C, int64_t ldc,
+                      int64_t M, int64_t N, int64_t K, int act, uintptr_t stream);
+
+/* C[m,n] = sequential_k(A[m,k]*B[k,n]); then, if act != NONE, the activation
+ * backward against Y (the activation's forward output) is fused:
+ * C = C * act'(Y).  (ops.py:111-112 FC dX; ops.py:302-303 MatMul forward;
+ * ops.py:164-166 activation backward).  Strides: A[m*sam + k*sak],
+ * B[k*sbk + n*sbn], C/Y row stride ldc. */
+int mgx_gemm_sequential(const float* A, int64_t sam, int64_t sak,
+                        const float* B, int64_t sbk, int64_t sbn,
+                        float* C, int64_t ldc, const float* Y, int act,
+                        int64_t M, int64_t N, int64_t K, uintptr_t stream);
+
+/* dW[h,f] = tree_b(og[b,h]*x[b,f]); db[h] = tree_b(og[b,h]).  Balanced
+ * power-of-two tree over the batch (kernels.py:32-47, ops.py:113-116).
+ * dw or db may be NULL. */
+int mgx_fc_dw_db(const float* og, const float* x, float* dw, float* db,
+                 int64_t B, int64_t H, int64_t F, uintptr_t stream);
+
+/* out[c] = tree_r(a[r, c]) (kernels.py:32-42) over `rows` rows of `cols`. */
+int mgx_tree_sum_rows(const float* a, float* out, int64_t rows, int64_t cols, uintptr_t stream);
+
+int mgx_act_forward(int act, const float* x, float* y, int64_t n, uintptr_t stream);          /* ops.py:154-156 */
+int mgx_act_backward(int act, const float* y, const float* og, float* g, int64_t n, uintptr_t stream); /* ops.py:159-161 */
+
+/* SoftmaxOutput (ops.py:176-207, kernels.py:68-83).  label holds class ids
+ * as fp32 (truncated to int64 like one_hot).  grad = (p - onehot) / f32(B). */
+int mgx_softmax_forward(const float* x, float* p, int64_t B, int64_t C, uintptr_t stream);
+int mgx_softmax_backward(const float* p, const float* label, float* g, int64_t B, int64_t C, uintptr_t stream);
+
+/* Momentum SGD, tensor path (optim.py:39-50): 5 separately rounded steps. */
+int mgx_sgd_step(float* w, const float* g, float* v, int64_t n,
+                 float eta, float momentum, float weight_decay, uintptr_t stream);
+
+/* ---------------------------------------------------------- memory planner
+ * plan_memory/_plan_view/_longest_path_order (planner.py:205-348) over a flat
+ * index view of the graph (planner.py:164-200).  Node arrays are in topo
+ * order.  strategy: 0 none, 1 inplace, 2 coshare, 3 both.
+ *   in_ptr/in_idx      CSR of each node's input node indices (with repeats)
+ *   ip_ptr/ip_pos      CSR of each node's in-place input positions
+ * Outputs: slot_of[n]; slot_bytes/slot_dedicated[*n_slots] (capacity n);
+ * edges[2*k] pairs sorted ascending (capacity edge_cap pairs). */
+int mgx_plan_memory(int32_t n, const uint8_t* is_var, const int64_t* nbytes,
+                    const uint8_t* dedicated, const int32_t* in_ptr,
+                    const int32_t* in_idx, const int32_t* ip_ptr,
+                    const int32_t* ip_pos, const int32_t* phase, int32_t strategy,
+                    int32_t* slot_of, int64_t* slot_bytes, uint8_t* slot_dedicated,
+                    int32_t* n_slots, int32_t* edges, int32_t edge_cap,
+                    int32_t* n_edges, int64_t* total_internal_bytes,
+                    int64_t* visits);
+/* Iteration order of CPython's set() over a list of small non-negative ints
+ * (the order planner.py:298 frees inputs in); exposed for testing. */
+int mgx_py_set_order(const int64_t* keys, int32_t n, int64_t* out, int32_t* n_out);
+
+/* ------------------------------------------------------ executor program
+ * The bound graph's push lists (executor.py:143-185) compiled into a native
+ * instruction list; forward()/backward() (executor.py:198-215) replay a
+ * range of it on a stream, optionally as one captured CUDA graph. */
+typedef struct mgx_instr {
+  int32_t op;          /* MGX_OP_* */
+  int32_t act;         /* activation code for fused epilogues */
+  int64_t dims[8];
+  float fattr[4];
+  void* ptr[6];
+} mgx_instr;
+
+#define MGX_OP_FILL 1         /* ptr0=y dims0=n fattr0=value                      */
+#define MGX_OP_COPY 2         /* ptr0=x ptr1=y dims0=n                            */
+#define MGX_OP_EW 3           /* ptr0=a ptr1=b ptr2=out dims0=n dims1=op          */
+#define MGX_OP_SCALAR 4       /* ptr0=a ptr1=out dims0=n dims1=op fattr0=c        */
+#define MGX_OP_GEMM_PW 5      /* ptr0=A ptr1=B ptr2=bias ptr3=C act               */
+                              /* dims=M,N,K,lda,ldb,ldc                           */
+#define MGX_OP_GEMM_SEQ 6     /* ptr0=A ptr1=B ptr2=C ptr3=Y act                  */
+                              /* dims=M,N,K,sam,sak,sbk,sbn,ldc                   */
+#define MGX_OP_DW_DB 7        /* ptr0=og ptr1=x ptr2=dw ptr3=db dims=B,H,F        */
+#define MGX_OP_ACT_FWD 8      /* ptr0=x ptr1=y dims0=n act                        */
+#define MGX_OP_ACT_BWD 9      /* ptr0=y ptr1=og ptr2=g dims0=n act                */
+#define MGX_OP_SOFTMAX_FWD 10 /* ptr0=x ptr1=p dims=B,C                           */
+#define MGX_OP_SOFTMAX_BWD 11 /* ptr0=p ptr1=label ptr2=g dims=B,C                */
+#define MGX_OP_AXPY 12        /* ptr0=x ptr1=y dims0=n fattr0=alpha               */
+
+/* Run instructions eagerly, in order, on stream (no program object). */
+int mgx_instr_run(const mgx_instr* instrs, int32_t count, uintptr_t stream);
+int mgx_prog_create(const mgx_instr* instrs, int32_t count, uint64_t* out);
+/* Launch instructions [begin, end) on stream.  use_graph=1 captures the range
+ * once into a CUDA graph and replays it on later calls. */
+int mgx_prog_run(uint64_t prog, int32_t begin, int32_t end, uintptr_t stream, int32_t use_graph);
+/* Per-instruction device time of one eager run of [begin,end) (profiling). */
+int mgx_prog_profile(uint64_t prog, int32_t begin, int32_t end, uintptr_t stream, float* ms_out);
+int mgx_prog_destroy(uint64_t prog);
+
+/* ------------------------------------------------------------- KVStore
+ * Device KVStore (kvstore.py:84-409): push -> level-1 tree aggregate over the
+ * W workers of a machine -> level-2 tree over M machines -> updater -> pull.
+ * One fused kernel per flushed round: the owner of each element range
+ * tree-sums every worker's gradient, applies the updater on its momentum
+ * shard, and stores the new weight into every worker replica.
+ *
+ * Segments are element ranges of the flat key arena this process owns:
+ * {arena offset, length, offset into this process's momentum buffer}. */
+typedef struct mgx_kv_seg {
+  int64_t off;
+  int64_t len;
+  int64_t voff;
+} mgx_kv_seg;
+
+/* updater: 0 = add (kvstore.py:47-49), 1 = fused momentum SGD
+ * (optim.py:64-78), 2 = aggregate only (result written to the gradient
+ * buffer of worker 0, for custom updaters). */
+#define MGX_KV_ADD 0
+#define MGX_KV_SGD 1
+#define MGX_KV_AGG 2
+
+typedef struct mgx_kv_round_args {
+  const mgx_kv_seg* segs;     /* HOST array, nseg <= 256 (copied into the launch) */
+  int32_t nseg;
+  int32_t machines, workers;  /* M x W gradient sources, ascending worker id */
+  float* const* grads;        /* HOST array of M*W device pointers (local or IPC-mapped) */
+  float* const* weights;      /* HOST array of M*W replica pointers */
+  int32_t self_replica;       /* replica this process reads w from */
+  float* velocity;            /* this process's momentum shard (SGD) */
+  float* agg_out;             /* AGG: where this process's totals go */
+  int32_t updater;
+  float rescale, neg_eta, momentum, weight_decay;
+  /* cross-process barrier (NULL flags = single process, no barrier):
+   * flag arrays are 2 * 1024 * (M*W) uint32 words, zero-initialised once */
+  uint32_t* const* flags;     /* HOST array of M*W flag-array pointers */
+  int32_t rank;               /* this process's worker id when flags != NULL */
+  uint32_t* epoch_ctr;        /* device, 2 words, zero-initialised: the kernel
+                                 derives its barrier epoch from it and advances
+                                 it, so captured launches replay correctly */
+  uint32_t* error_word;       /* device word set non-zero on barrier timeout */
+  int32_t grid;               /* 0 = auto; required (same on all ranks) with flags */
+} mgx_kv_round_args;
+
+int mgx_kv_round(const mgx_kv_round_args* args, uintptr_t stream);
+/* Largest grid mgx_kv_round will use (flag arrays need grid * M*W words). */
+int mgx_kv_max_grid(int32_t machines, int32_t workers, int32_t* out);
+#define MGX_KV_FLAG_WORDS_PER_WORKER 2048  /* 2 phases x 1024 blocks */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MGX_H_ */

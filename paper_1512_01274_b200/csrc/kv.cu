@@ -1,0 +1,357 @@
+// Device KVStore round: fused reduce -> update -> broadcast.
+//
+// Reference data path (kvstore.py):
+//   push        worker copies its gradient to its level-1 server     (:190-211)
+//   level 1     tree_sum over the machine's W workers, ascending id   (:328-338)
+//   level 2     tree_sum over the M machine aggregates, ascending id  (:390-402)
+//   updater     make_sgd_updater -> sgd_arrays (optim.py:53-78), or add (:47-49)
+//   broadcast   snapshot copied to every level-1 server, pulls copy   (:373-375, :233-238)
+//
+// Here all of that is one pass over HBM/NVLink.  The element range of a key
+// (or a bucket of small keys) is split into contiguous owner shards; the
+// owner reads every worker's gradient for its shard (local HBM or a peer's
+// over NVLink via CUDA IPC mappings), sums them with the reference's exact
+// two-level balanced tree, applies the updater with its momentum shard, and
+// stores the new weight into every worker's replica.  Per element this is the
+// reference's float-op sequence, so the result is bitwise identical no matter
+// how the range is sharded.
+//
+// Cross-process ordering: when `flags` is set, each block does a
+// release/acquire flag barrier with the same-index block of every peer before
+// reading (all gradients final, all peers done reading the previous weights)
+// and after writing (all replicas final before anyone's next forward).  The
+// grid is at most one resident wave, so every block of every peer is running.
+
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <utility>
+
+#include "common.cuh"
+
+namespace mgx {
+
+constexpr int kKvThreads = 512;
+constexpr int kKvMaxNW = 16;
+constexpr int kKvMaxSegs = 256;
+constexpr int kKvFlagBlocks = 1024;  // flag-array stride per phase
+
+struct KvParams {
+  float* grads[kKvMaxNW];
+  float* weights[kKvMaxNW];
+  uint32_t* flags[kKvMaxNW];
+  float* velocity;
+  float* agg_out;
+  uint32_t* error_word;
+  int32_t nseg;
+  int32_t self_replica;
+  int32_t updater;
+  int32_t rank;
+  uint32_t* epoch_ctr;  // device: [completed launches, blocks finished]
+  float rescale, neg_eta, momentum, weight_decay;
+  mgx_kv_seg segs[kKvMaxSegs];
+};
+
+// largest power of two strictly below n (n >= 2): kernels.py:39
+__host__ __device__ constexpr int hpow2(int n) {
+  int h = 1;
+  while (h * 2 < n) h *= 2;
+  return h;
+}
+
+template <int N>
+__device__ __forceinline__ float tree(const float* v) {
+  if constexpr (N == 1) {
+    return v[0];
+  } else {
+    constexpr int H = hpow2(N);
+    return fadd(tree<H>(v), tree<N - H>(v + H));
+  }
+}
+
+// level-1 tree per machine over its W workers, then level-2 tree over machines
+template <int M, int W>
+__device__ __forceinline__ float two_level(const float* v) {
+  if constexpr (M == 1) {
+    return tree<W>(v);
+  } else {
+    float agg[M];
+#pragma unroll
+    for (int m = 0; m < M; ++m) agg[m] = tree<W>(v + m * W);
+    return tree<M>(agg);
+  }
+}
+
+__device__ __forceinline__ float4 ld_nc_v4(const float* p) {
+  float4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ void st_v4(float* p, float4 v) {
+  asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y),
+               "f"(v.z), "f"(v.w)
+               : "memory");
+}
+
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Flag barrier with the same-index block of every peer.  Returns false (for
+// the whole block) if a peer did not arrive within 30 s.
+template <int NW>
+__device__ bool block_barrier(const KvParams& p, int phase, uint32_t epoch) {
+  __shared__ int ok;
+  __syncthreads();
+  if (threadIdx.x == 0) ok = 1;
+  __syncthreads();
+  if (threadIdx.x < NW) {
+    const size_t base = (size_t(phase) * kKvFlagBlocks + blockIdx.x) * NW;
+    __threadfence_system();
+    st_release_sys(p.flags[threadIdx.x] + base + p.rank, epoch);
+    const uint32_t* mine = p.flags[p.rank] + base + threadIdx.x;
+    const uint64_t t0 = global_ns();
+    while (static_cast<int32_t>(ld_acquire_sys(mine) - epoch) < 0) {
+      if (global_ns() - t0 > 30ull * 1000 * 1000 * 1000) {
+        atomicExch(p.error_word, 1u);
+        ok = 0;
+        break;
+      }
+    }
+  }
+  __syncthreads();
+  return ok != 0;
+}
+
+template <int M, int W, int UNROLL>
+__global__ void __launch_bounds__(kKvThreads) kv_round_kernel(const __grid_constant__ KvParams p) {
+  constexpr int NW = M * W;
+  const bool barrier = p.flags[0] != nullptr;
+  // The barrier epoch lives on the device (launch count + 1), so a captured
+  // launch replays correctly; the last block to finish advances it.
+  __shared__ uint32_t s_epoch;
+  if (barrier) {
+    if (threadIdx.x == 0) s_epoch = *reinterpret_cast<volatile uint32_t*>(p.epoch_ctr) + 1;
+    __syncthreads();
+  }
+  const bool live = !barrier || block_barrier<NW>(p, 0, s_epoch);
+
+  const int64_t stride = int64_t(gridDim.x) * kKvThreads;
+  const float* wsrc = p.weights[p.self_replica];
+  for (int s = 0; live && s < p.nseg; ++s) {
+    const int64_t off = p.segs[s].off;
+    const int64_t n4 = (p.segs[s].len + 3) >> 2;
+    const int64_t voff = p.segs[s].voff;
+    for (int64_t base = int64_t(blockIdx.x) * kKvThreads + threadIdx.x; base < n4;
+         base += stride * UNROLL) {
+      float4 g[UNROLL][NW];
+      float4 w[UNROLL];
+      float4 v[UNROLL];
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) {
+        const int64_t i = base + u * stride;
+        if (i < n4) {
+#pragma unroll
+          for (int j = 0; j < NW; ++j) g[u][j] = ld_nc_v4(p.grads[j] + off + 4 * i);
+          if (p.updater != MGX_KV_AGG) w[u] = ld_nc_v4(wsrc + off + 4 * i);
+          if (p.updater == MGX_KV_SGD)
+            v[u] = *reinterpret_cast<const float4*>(p.velocity + voff + 4 * i);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < UNROLL; ++u) {
+        const int64_t i = base + u * stride;
+        if (i >= n4) continue;
+        float tot[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          float vals[NW];
+#pragma unroll
+          for (int j = 0; j < NW; ++j) vals[j] = reinterpret_cast<const float*>(&g[u][j])[c];
+          tot[c] = two_level<M, W>(vals);
+        }
+        if (p.updater == MGX_KV_AGG) {
+          *reinterpret_cast<float4*>(p.agg_out + off + 4 * i) = make_float4(tot[0], tot[1], tot[2], tot[3]);
+          continue;
+        }
+        float* wc = reinterpret_cast<float*>(&w[u]);
+        if (p.updater == MGX_KV_SGD) {
+          // make_sgd_updater (optim.py:72-76) -> sgd_arrays (optim.py:53-61):
+          //   g = incoming * f32(1/scale); tmp = g + w*wd; v = v*mom;
+          //   v = v + tmp*(-eta); w = w + v*1
+          float* vc = reinterpret_cast<float*>(&v[u]);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const float gg = fmul(tot[c], p.rescale);
+            const float tmp = fadd(gg, fmul(wc[c], p.weight_decay));
+            vc[c] = fmul(vc[c], p.momentum);
+            vc[c] = fadd(vc[c], fmul(tmp, p.neg_eta));
+            wc[c] = fadd(wc[c], fmul(vc[c], 1.0f));
+          }
+          *reinterpret_cast<float4*>(p.velocity + voff + 4 * i) = v[u];
+        } else {
+          // add_updater (kvstore.py:47-49): stored += incoming
+#pragma unroll
+          for (int c = 0; c < 4; ++c) wc[c] = fadd(wc[c], tot[c]);
+        }
+#pragma unroll
+        for (int j = 0; j < NW; ++j) st_v4(p.weights[j] + off + 4 * i, w[u]);
+      }
+    }
+  }
+  if (barrier) {
+    if (live) block_barrier<NW>(p, 1, s_epoch);
+    if (threadIdx.x == 0) {
+      __threadfence();
+      const uint32_t prev = atomicAdd(p.epoch_ctr + 1, 1u);
+      if (prev == gridDim.x - 1) {
+        p.epoch_ctr[1] = 0;
+        __threadfence();
+        atomicAdd(p.epoch_ctr, 1u);
+      }
+    }
+  }
+}
+
+using KvKernel = void (*)(const KvParams);
+
+template <int M, int W>
+KvKernel pick_unroll(int64_t) {
+  if constexpr (M * W <= 4) return kv_round_kernel<M, W, 2>;
+  else return kv_round_kernel<M, W, 1>;
+}
+
+static KvKernel select_kernel(int M, int W) {
+#define MGX_KV_CASE(m, w) \
+  if (M == m && W == w) return pick_unroll<m, w>(0);
+  MGX_KV_CASE(1, 1) MGX_KV_CASE(1, 2) MGX_KV_CASE(1, 3) MGX_KV_CASE(1, 4)
+  MGX_KV_CASE(1, 5) MGX_KV_CASE(1, 6) MGX_KV_CASE(1, 7) MGX_KV_CASE(1, 8)
+  MGX_KV_CASE(1, 16)
+  MGX_KV_CASE(2, 1) MGX_KV_CASE(2, 2) MGX_KV_CASE(2, 3) MGX_KV_CASE(2, 4) MGX_KV_CASE(2, 8)
+  MGX_KV_CASE(3, 1) MGX_KV_CASE(3, 2)
+  MGX_KV_CASE(4, 1) MGX_KV_CASE(4, 2) MGX_KV_CASE(4, 4)
+  MGX_KV_CASE(8, 1) MGX_KV_CASE(8, 2)
+#undef MGX_KV_CASE
+  return nullptr;
+}
+
+static int kv_capacity(KvKernel k, int* out) {
+  // cached per (kernel, device): no runtime API calls on the launch path,
+  // which matters inside stream capture
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> cache;
+  int dev0 = 0;
+  MGX_CUDA(cudaGetDevice(&dev0));
+  const auto key = std::make_pair(reinterpret_cast<const void*>(k), dev0);
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+      *out = it->second;
+      return MGX_OK;
+    }
+  }
+  int per_sm = 0;
+  MGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kKvThreads, 0));
+  int dev = 0, sms = kNumSMs;
+  MGX_CUDA(cudaGetDevice(&dev));
+  MGX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  int cap = per_sm * sms;
+  if (cap > kKvFlagBlocks) cap = kKvFlagBlocks;
+  *out = cap < 1 ? 1 : cap;
+  std::lock_guard<std::mutex> lock(mu);
+  cache[key] = *out;
+  return MGX_OK;
+}
+
+}  // namespace mgx
+
+extern "C" int mgx_kv_max_grid(int32_t machines, int32_t workers, int32_t* out) {
+  MGX_REQUIRE(out, "mgx_kv_max_grid: null out");
+  mgx::KvKernel k = mgx::select_kernel(machines, workers);
+  MGX_REQUIRE(k, "mgx_kv_max_grid: unsupported topology %d x %d", machines, workers);
+  int cap = 0;
+  MGX_TRY(mgx::kv_capacity(k, &cap));
+  *out = cap;
+  return MGX_OK;
+}
+
+extern "C" int mgx_kv_round(const mgx_kv_round_args* a, uintptr_t stream) {
+  MGX_REQUIRE(a && a->segs && a->grads, "mgx_kv_round: null arguments");
+  const int M = a->machines, W = a->workers, NW = M * W;
+  MGX_REQUIRE(M >= 1 && W >= 1 && NW <= mgx::kKvMaxNW, "mgx_kv_round: bad topology %d x %d", M, W);
+  MGX_REQUIRE(a->nseg >= 0 && a->nseg <= mgx::kKvMaxSegs, "mgx_kv_round: nseg %d outside [0, %d]",
+              a->nseg, mgx::kKvMaxSegs);
+  MGX_REQUIRE(a->updater >= 0 && a->updater <= 2, "mgx_kv_round: unknown updater %d", a->updater);
+  MGX_REQUIRE(a->updater == MGX_KV_AGG || a->weights, "mgx_kv_round: weights required");
+  MGX_REQUIRE(a->updater != MGX_KV_SGD || a->velocity, "mgx_kv_round: SGD needs velocity");
+  MGX_REQUIRE(a->updater != MGX_KV_AGG || a->agg_out, "mgx_kv_round: AGG needs agg_out");
+  MGX_REQUIRE(a->self_replica >= 0 && a->self_replica < NW, "mgx_kv_round: bad self_replica");
+  mgx::KvKernel k = mgx::select_kernel(M, W);
+  MGX_REQUIRE(k, "mgx_kv_round: unsupported topology %d x %d", M, W);
+
+  mgx::KvParams p;
+  std::memset(&p, 0, sizeof(p));
+  int64_t total4 = 0;
+  for (int s = 0; s < a->nseg; ++s) {
+    const mgx_kv_seg& sg = a->segs[s];
+    MGX_REQUIRE(sg.off % 4 == 0 && sg.len >= 0 && sg.voff % 4 == 0,
+                "mgx_kv_round: segment %d not 16-byte aligned", s);
+    p.segs[s] = sg;
+    total4 += (sg.len + 3) / 4;
+  }
+  for (int j = 0; j < NW; ++j) {
+    p.grads[j] = a->grads[j];
+    p.weights[j] = a->weights ? a->weights[j] : nullptr;
+    p.flags[j] = a->flags ? a->flags[j] : nullptr;
+    MGX_REQUIRE(p.grads[j], "mgx_kv_round: null gradient pointer %d", j);
+  }
+  p.velocity = a->velocity;
+  p.agg_out = a->agg_out;
+  p.error_word = a->error_word;
+  p.nseg = a->nseg;
+  p.self_replica = a->self_replica;
+  p.updater = a->updater;
+  p.rank = a->rank;
+  p.epoch_ctr = a->epoch_ctr;
+  p.rescale = a->rescale;
+  p.neg_eta = a->neg_eta;
+  p.momentum = a->momentum;
+  p.weight_decay = a->weight_decay;
+
+  int cap = 0;
+  MGX_TRY(mgx::kv_capacity(k, &cap));
+  int grid = a->grid;
+  const bool barrier = a->flags != nullptr;
+  if (barrier) {
+    MGX_REQUIRE(a->error_word && a->epoch_ctr, "mgx_kv_round: barrier needs error_word and epoch_ctr");
+    MGX_REQUIRE(a->rank >= 0 && a->rank < NW, "mgx_kv_round: bad rank");
+    MGX_REQUIRE(grid >= 1 && grid <= cap,
+                "mgx_kv_round: barrier mode needs an explicit grid in [1, %d], got %d", cap, grid);
+  } else {
+    if (total4 == 0) return MGX_OK;
+    if (grid <= 0) {
+      int64_t want = mgx::ceil_div(total4, mgx::kKvThreads * 2);
+      grid = static_cast<int>(want < cap ? want : cap);
+      if (grid < 1) grid = 1;
+    }
+  }
+  k<<<grid, mgx::kKvThreads, 0, mgx::as_stream(stream)>>>(p);
+  MGX_LAUNCHED();
+  return MGX_OK;
+}

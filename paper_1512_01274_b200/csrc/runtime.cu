@@ -1,0 +1,356 @@
+// Runtime pieces of the C-ABI: error reporting, device memory, streams,
+// events, CUDA IPC, and the native executor program.
+//
+// The reference schedules every operator closure on a host thread pool with
+// read/write tags (engine.py:94-196) and the executor pushes one closure per
+// graph node in a fixed heap order (executor.py:143-185, 198-215).  Here the
+// bound graph becomes a flat instruction list replayed on one CUDA stream
+// (stream order == the reference's per-tag FIFO order for a single writer
+// chain); a replayed range can be captured once into a CUDA graph so a whole
+// forward or backward pass is one launch from the host.
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "common.cuh"
+
+namespace mgx {
+
+static thread_local std::string g_last_error;
+
+void set_error(const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+}
+
+cudaStream_t as_stream(uintptr_t s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// launchers defined in dense.cu / pointwise.cu
+int launch_gemm_pairwise(const float* A, int64_t lda, const float* B, int64_t ldb,
+                         const float* bias, float* C, int64_t ldc, int64_t M, int64_t N,
+                         int64_t K, int act, cudaStream_t st);
+int launch_gemm_sequential(const float* A, int64_t sam, int64_t sak, const float* B, int64_t sbk,
+                           int64_t sbn, float* C, int64_t ldc, const float* Y, int act, int64_t M,
+                           int64_t N, int64_t K, cudaStream_t st);
+int launch_dw_db(const float* og, const float* x, float* dw, float* db, int64_t Bn, int64_t H,
+                 int64_t F, cudaStream_t st);
+
+}  // namespace mgx
+
+using mgx::as_stream;
+
+extern "C" const char* mgx_last_error_message(void) { return mgx::g_last_error.c_str(); }
+
+extern "C" int mgx_abi_version(int* out) {
+  MGX_REQUIRE(out, "mgx_abi_version: null out");
+  *out = 1;
+  return MGX_OK;
+}
+
+extern "C" int mgx_device_count(int* out) {
+  MGX_REQUIRE(out, "mgx_device_count: null out");
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    n = 0;
+  }
+  *out = n;
+  return MGX_OK;
+}
+
+extern "C" int mgx_set_device(int device) {
+  MGX_CUDA(cudaSetDevice(device));
+  return MGX_OK;
+}
+
+extern "C" int mgx_malloc(size_t nbytes, void** out) {
+  MGX_REQUIRE(out, "mgx_malloc: null out");
+  MGX_CUDA(cudaMalloc(out, nbytes ? nbytes : 256));
+  return MGX_OK;
+}
+
+extern "C" int mgx_free(void* ptr) {
+  if (ptr) MGX_CUDA(cudaFree(ptr));
+  return MGX_OK;
+}
+
+extern "C" int mgx_host_alloc(size_t nbytes, void** out) {
+  MGX_REQUIRE(out, "mgx_host_alloc: null out");
+  MGX_CUDA(cudaHostAlloc(out, nbytes ? nbytes : 256, cudaHostAllocPortable));
+  return MGX_OK;
+}
+
+extern "C" int mgx_host_free(void* ptr) {
+  if (ptr) MGX_CUDA(cudaFreeHost(ptr));
+  return MGX_OK;
+}
+
+extern "C" int mgx_stream_create(uintptr_t* out) {
+  MGX_REQUIRE(out, "mgx_stream_create: null out");
+  cudaStream_t s;
+  MGX_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  *out = reinterpret_cast<uintptr_t>(s);
+  return MGX_OK;
+}
+
+extern "C" int mgx_stream_destroy(uintptr_t stream) {
+  if (stream) MGX_CUDA(cudaStreamDestroy(as_stream(stream)));
+  return MGX_OK;
+}
+
+extern "C" int mgx_stream_sync(uintptr_t stream) {
+  MGX_CUDA(cudaStreamSynchronize(as_stream(stream)));
+  return MGX_OK;
+}
+
+extern "C" int mgx_memcpy_async(void* dst, const void* src, size_t nbytes, uintptr_t stream) {
+  MGX_REQUIRE(nbytes == 0 || (dst && src), "mgx_memcpy_async: null pointer");
+  if (nbytes) MGX_CUDA(cudaMemcpyAsync(dst, src, nbytes, cudaMemcpyDefault, as_stream(stream)));
+  return MGX_OK;
+}
+
+extern "C" int mgx_memset_async(void* dst, int value, size_t nbytes, uintptr_t stream) {
+  MGX_REQUIRE(nbytes == 0 || dst, "mgx_memset_async: null pointer");
+  if (nbytes) MGX_CUDA(cudaMemsetAsync(dst, value, nbytes, as_stream(stream)));
+  return MGX_OK;
+}
+
+extern "C" int mgx_event_create(uintptr_t* out) {
+  MGX_REQUIRE(out, "mgx_event_create: null out");
+  cudaEvent_t e;
+  MGX_CUDA(cudaEventCreate(&e));
+  *out = reinterpret_cast<uintptr_t>(e);
+  return MGX_OK;
+}
+
+extern "C" int mgx_event_destroy(uintptr_t ev) {
+  if (ev) MGX_CUDA(cudaEventDestroy(reinterpret_cast<cudaEvent_t>(ev)));
+  return MGX_OK;
+}
+
+extern "C" int mgx_event_record(uintptr_t ev, uintptr_t stream) {
+  MGX_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(ev), as_stream(stream)));
+  return MGX_OK;
+}
+
+extern "C" int mgx_event_elapsed_ms(uintptr_t start, uintptr_t end, float* out) {
+  MGX_REQUIRE(out, "mgx_event_elapsed_ms: null out");
+  MGX_CUDA(cudaEventSynchronize(reinterpret_cast<cudaEvent_t>(end)));
+  MGX_CUDA(cudaEventElapsedTime(out, reinterpret_cast<cudaEvent_t>(start),
+                                reinterpret_cast<cudaEvent_t>(end)));
+  return MGX_OK;
+}
+
+extern "C" int mgx_stream_wait_event(uintptr_t stream, uintptr_t ev) {
+  MGX_CUDA(cudaStreamWaitEvent(as_stream(stream), reinterpret_cast<cudaEvent_t>(ev), 0));
+  return MGX_OK;
+}
+
+// ------------------------------------------------------------------- IPC
+
+static_assert(sizeof(cudaIpcMemHandle_t) == MGX_IPC_HANDLE_BYTES, "IPC handle size");
+
+extern "C" int mgx_ipc_get_handle(void* dev_ptr, void* handle_out) {
+  MGX_REQUIRE(dev_ptr && handle_out, "mgx_ipc_get_handle: null pointer");
+  cudaIpcMemHandle_t h;
+  MGX_CUDA(cudaIpcGetMemHandle(&h, dev_ptr));
+  std::memcpy(handle_out, &h, sizeof(h));
+  return MGX_OK;
+}
+
+extern "C" int mgx_ipc_open_handle(const void* handle, void** out) {
+  MGX_REQUIRE(handle && out, "mgx_ipc_open_handle: null pointer");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  MGX_CUDA(cudaIpcOpenMemHandle(out, h, cudaIpcMemLazyEnablePeerAccess));
+  return MGX_OK;
+}
+
+extern "C" int mgx_ipc_close_handle(void* dev_ptr) {
+  if (dev_ptr) MGX_CUDA(cudaIpcCloseMemHandle(dev_ptr));
+  return MGX_OK;
+}
+
+// -------------------------------------------------------- executor program
+
+namespace mgx {
+
+struct Program {
+  std::vector<mgx_instr> instrs;
+  std::map<std::pair<int32_t, int32_t>, cudaGraphExec_t> graphs;
+  std::mutex mu;
+};
+
+static std::mutex g_prog_mu;
+static std::map<uint64_t, Program*> g_progs;
+static uint64_t g_next_prog = 1;
+
+static Program* find_prog(uint64_t h) {
+  std::lock_guard<std::mutex> lock(g_prog_mu);
+  auto it = g_progs.find(h);
+  return it == g_progs.end() ? nullptr : it->second;
+}
+
+static int run_instr(const mgx_instr& in, cudaStream_t st) {
+  const uintptr_t s = reinterpret_cast<uintptr_t>(st);
+  float* p0 = static_cast<float*>(in.ptr[0]);
+  float* p1 = static_cast<float*>(in.ptr[1]);
+  float* p2 = static_cast<float*>(in.ptr[2]);
+  float* p3 = static_cast<float*>(in.ptr[3]);
+  const int64_t* d = in.dims;
+  switch (in.op) {
+    case MGX_OP_FILL: return mgx_fill(p0, d[0], in.fattr[0], s);
+    case MGX_OP_COPY: return mgx_copy(p0, p1, d[0], s);
+    case MGX_OP_EW: return mgx_elementwise(static_cast<int>(d[1]), p0, p1, p2, d[0], s);
+    case MGX_OP_SCALAR: return mgx_scalar_op(static_cast<int>(d[1]), p0, in.fattr[0], p1, d[0], s);
+    case MGX_OP_GEMM_PW:
+      return launch_gemm_pairwise(p0, d[3], p1, d[4], p2, p3, d[5], d[0], d[1], d[2], in.act, st);
+    case MGX_OP_GEMM_SEQ:
+      return launch_gemm_sequential(p0, d[3], d[4], p1, d[5], d[6], p2, d[7], p3, in.act, d[0],
+                                    d[1], d[2], st);
+    case MGX_OP_DW_DB: {
+      if (!p2 && !p3) return MGX_OK;
+      return launch_dw_db(p0, p1, p2, p3, d[0], d[1], p2 ? d[2] : 1, st);
+    }
+    case MGX_OP_ACT_FWD: return mgx_act_forward(in.act, p0, p1, d[0], s);
+    case MGX_OP_ACT_BWD: return mgx_act_backward(in.act, p0, p1, p2, d[0], s);
+    case MGX_OP_SOFTMAX_FWD: return mgx_softmax_forward(p0, p1, d[0], d[1], s);
+    case MGX_OP_SOFTMAX_BWD: return mgx_softmax_backward(p0, p1, p2, d[0], d[1], s);
+    case MGX_OP_AXPY: return mgx_axpy(in.fattr[0], p0, p1, d[0], s);
+    default:
+      set_error("program: unknown opcode %d", in.op);
+      return MGX_BAD_ARGUMENT;
+  }
+}
+
+static int run_range(Program* p, int32_t begin, int32_t end, cudaStream_t st) {
+  for (int32_t i = begin; i < end; ++i) {
+    int rc = run_instr(p->instrs[i], st);
+    if (rc != MGX_OK) return rc;
+  }
+  return MGX_OK;
+}
+
+}  // namespace mgx
+
+extern "C" int mgx_instr_run(const mgx_instr* instrs, int32_t count, uintptr_t stream) {
+  MGX_REQUIRE(count >= 0 && (count == 0 || instrs), "mgx_instr_run: bad arguments");
+  for (int32_t i = 0; i < count; ++i) {
+    int rc = mgx::run_instr(instrs[i], as_stream(stream));
+    if (rc != MGX_OK) return rc;
+  }
+  return MGX_OK;
+}
+
+extern "C" int mgx_prog_create(const mgx_instr* instrs, int32_t count, uint64_t* out) {
+  MGX_REQUIRE(out && count >= 0 && (count == 0 || instrs), "mgx_prog_create: bad arguments");
+  auto* p = new mgx::Program();
+  p->instrs.assign(instrs, instrs + count);
+  // Materialise per-K pairwise leaf tables now: they allocate, which is not
+  // allowed while a range is being captured into a graph.
+  for (const auto& in : p->instrs) {
+    const mgx::PwLeaf* t;
+    int nl, dp;
+    int rc = MGX_OK;
+    if (in.op == MGX_OP_GEMM_PW) rc = mgx::pw_leaf_table(in.dims[2], &t, &nl, &dp);
+    if (in.op == MGX_OP_SOFTMAX_FWD) rc = mgx::pw_leaf_table(in.dims[1], &t, &nl, &dp);
+    if (rc != MGX_OK) {
+      delete p;
+      return rc;
+    }
+  }
+  std::lock_guard<std::mutex> lock(mgx::g_prog_mu);
+  uint64_t h = mgx::g_next_prog++;
+  mgx::g_progs[h] = p;
+  *out = h;
+  return MGX_OK;
+}
+
+extern "C" int mgx_prog_run(uint64_t prog, int32_t begin, int32_t end, uintptr_t stream,
+                            int32_t use_graph) {
+  mgx::Program* p = mgx::find_prog(prog);
+  if (!p) {
+    mgx::set_error("mgx_prog_run: unknown program handle %llu", (unsigned long long)prog);
+    return MGX_BAD_HANDLE;
+  }
+  MGX_REQUIRE(0 <= begin && begin <= end && end <= static_cast<int32_t>(p->instrs.size()),
+              "mgx_prog_run: bad range [%d, %d)", begin, end);
+  if (begin == end) return MGX_OK;
+  cudaStream_t st = as_stream(stream);
+  if (!use_graph || stream == 0) return mgx::run_range(p, begin, end, st);
+
+  std::lock_guard<std::mutex> lock(p->mu);
+  auto key = std::make_pair(begin, end);
+  auto it = p->graphs.find(key);
+  if (it == p->graphs.end()) {
+    cudaGraph_t graph;
+    MGX_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    int rc = mgx::run_range(p, begin, end, st);
+    cudaError_t ce = cudaStreamEndCapture(st, &graph);
+    if (rc != MGX_OK) {
+      if (ce == cudaSuccess) cudaGraphDestroy(graph);
+      return rc;
+    }
+    MGX_CUDA(ce);
+    cudaGraphExec_t exec;
+    cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    MGX_CUDA(ie);
+    it = p->graphs.emplace(key, exec).first;
+  }
+  MGX_CUDA(cudaGraphLaunch(it->second, st));
+  return MGX_OK;
+}
+
+extern "C" int mgx_prog_profile(uint64_t prog, int32_t begin, int32_t end, uintptr_t stream,
+                                float* ms_out) {
+  mgx::Program* p = mgx::find_prog(prog);
+  if (!p) {
+    mgx::set_error("mgx_prog_profile: unknown program handle");
+    return MGX_BAD_HANDLE;
+  }
+  MGX_REQUIRE(ms_out && 0 <= begin && begin <= end && end <= static_cast<int32_t>(p->instrs.size()),
+              "mgx_prog_profile: bad arguments");
+  cudaStream_t st = as_stream(stream);
+  const int n = end - begin;
+  std::vector<cudaEvent_t> ev(n + 1);
+  for (auto& e : ev) MGX_CUDA(cudaEventCreate(&e));
+  int rc = MGX_OK;
+  MGX_CUDA(cudaEventRecord(ev[0], st));
+  for (int i = 0; i < n && rc == MGX_OK; ++i) {
+    rc = mgx::run_instr(p->instrs[begin + i], st);
+    cudaEventRecord(ev[i + 1], st);
+  }
+  cudaEventSynchronize(ev[n]);
+  for (int i = 0; i < n; ++i) cudaEventElapsedTime(&ms_out[i], ev[i], ev[i + 1]);
+  for (auto& e : ev) cudaEventDestroy(e);
+  return rc;
+}
+
+extern "C" int mgx_prog_destroy(uint64_t prog) {
+  mgx::Program* p = nullptr;
+  {
+    std::lock_guard<std::mutex> lock(mgx::g_prog_mu);
+    auto it = mgx::g_progs.find(prog);
+    if (it == mgx::g_progs.end()) {
+      mgx::set_error("mgx_prog_destroy: unknown program handle");
+      return MGX_BAD_HANDLE;
+    }
+    p = it->second;
+    mgx::g_progs.erase(it);
+  }
+  for (auto& kv : p->graphs) cudaGraphExecDestroy(kv.second);
+  delete p;
+  return MGX_OK;
+}

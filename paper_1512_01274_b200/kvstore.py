@@ -1,0 +1,634 @@
+"""Device key-value store for data-parallel training.
+
+Drop-in for the reference KVStore (kvstore.py:84-409): ``KVStore(machines,
+workers, mode, etype, engine, tcp)`` with ``init / set_updater / push /
+pull / round_barrier / quiesce / stats / close``.  Instead of level-1 and
+level-2 server threads exchanging copies through queues, one fused kernel
+per flush (csrc/kv.cu) does, for every pushed key:
+
+    level-1 tree over each machine's W workers (ascending worker id)
+    -> level-2 tree over the M machine aggregates (ascending machine id)
+    -> updater (fused momentum SGD, add, or a plugin callable)
+    -> the new value stored into every worker's replica (the pull source)
+
+Bit-exactness with the reference's per-element float sequence is kept for
+every sharding, so the placement rule below is a free choice:
+
+* keys are laid out in init order in a flat arena, each key starting on a
+  256-byte boundary and padded to 64 elements (padding stays zero);
+* consecutive keys are grouped into buckets of at least ``bucket_bytes``
+  (4 MB default; a key of that size or more is a bucket of its own);
+* each bucket range of L elements is split into ``M*W`` contiguous owner
+  shards: owner r gets [floor32(r*L/N), floor32((r+1)*L/N)), the last owner
+  ending at L (``shard_ranges``); the owner keeps the momentum state for
+  its shard only.
+
+Two placements of the workers:
+
+* single process (the reference's own model, kvstore.py:84-135): every
+  worker's gradient buffer and weight replica live on this engine's device;
+  one kernel reduces all of them;
+* ``distributed=True`` (one process per GPU under torch.distributed, world
+  size == machines*workers, worker id == rank): replicas are exchanged once
+  as CUDA IPC mappings; each rank's kernel reads its shard from every peer
+  over NVLink, updates it, and stores it into every peer's replica, with a
+  device-side flag barrier at both ends of the kernel (no NCCL on the data
+  path).
+
+Consistency (kvstore.py:8-17): "sequential" = a key is reduced when every
+worker of this process has pushed it for the round; a pull of a key whose
+round is complete but not yet reduced flushes all pending keys in one launch.
+"eventual" = every push is applied at once (single process only).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from dataclasses import dataclass, field
+from typing import Callable, Dict, List, Optional, Tuple
+
+import numpy as np
+
+from . import _lib as L
+from . import tensor as tmod
+from .engine import Engine, default_engine
+from .errors import ArgumentError, KVStoreError, StateError
+from .tensor import Tensor
+
+MODES = ("sequential", "eventual")
+KEY_ALIGN = 64            # elements (256 bytes)
+SHARD_ALIGN = 32          # elements (128 bytes)
+DEFAULT_BUCKET_BYTES = 4 << 20
+
+
+def add_updater(key: int, stored, incoming) -> None:
+    """Default updater (kvstore.py:47-49): stored += incoming, on device."""
+    stored.add_(incoming)
+
+
+def padded(n: int) -> int:
+    return -(-n // KEY_ALIGN) * KEY_ALIGN
+
+
+def shard_ranges(length: int, owners: int) -> List[Tuple[int, int]]:
+    """Owner shards of a bucket of ``length`` elements (the sharding rule)."""
+    bounds = [(r * length // owners) // SHARD_ALIGN * SHARD_ALIGN for r in range(owners)]
+    bounds.append(length)
+    return [(bounds[r], bounds[r + 1]) for r in range(owners)]
+
+
+def plan_buckets(numels: List[int], bucket_bytes: int = DEFAULT_BUCKET_BYTES
+                 ) -> Tuple[List[int], List[Tuple[int, int]], List[int]]:
+    """Arena layout for keys in init order: (key offsets, bucket ranges,
+    bucket of each key).  Offsets/lengths in elements."""
+    offs, key_bucket, buckets = [], [], []
+    pos = 0
+    start = 0
+    for n in numels:
+        if pos > start and ((pos - start) * 4 >= bucket_bytes or n * 4 >= bucket_bytes):
+            buckets.append((start, pos))
+            start = pos
+        offs.append(pos)
+        key_bucket.append(len(buckets))
+        pos += padded(n)
+    if pos > start or not buckets:
+        buckets.append((start, pos))
+    return offs, buckets, key_bucket
+
+
+@dataclass
+class _Key:
+    key: int
+    shape: tuple
+    numel: int
+    init: object                      # host float32 array until materialised
+    off: int = -1
+    bucket: int = -1
+    arena: int = -1
+
+
+@dataclass
+class _Arena:
+    """One materialised group of keys (keys inited after the first push or
+    pull go into a new arena)."""
+    keys: List[int]
+    length: int
+    buckets: List[Tuple[int, int]]
+    weights: List[int] = field(default_factory=list)   # per-worker device pointers
+    grads: List[int] = field(default_factory=list)
+    flags: List[int] = field(default_factory=list)
+    velocity: int = 0
+    vlen: int = 0
+    voff: Dict[Tuple[int, int], int] = field(default_factory=dict)  # (bucket, owner)
+    agg: int = 0
+    epoch_ctr: int = 0
+    owned_local: List[int] = field(default_factory=list)  # pointers this process allocated
+    opened: List[int] = field(default_factory=list)       # IPC-mapped pointers
+    torch_views: Dict[Tuple[str, int], object] = field(default_factory=dict)
+
+
+class _RawBuffer:
+    """__cuda_array_interface__ over a device pointer so torch can view it."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f4", "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+class KVStore:
+    def __init__(self, machines: int = 1, workers: int = 1, mode: str = "sequential",
+                 etype: str = "float32", engine: Optional[Engine] = None,
+                 tcp: Optional[str] = None, distributed: bool = False,
+                 bucket_bytes: int = DEFAULT_BUCKET_BYTES, timeout: float = 120.0):
+        if machines < 1 or workers < 1:
+            raise ArgumentError("topology needs machines >= 1 and workers >= 1")
+        if mode not in MODES:
+            raise ArgumentError(f"unknown consistency mode {mode!r}")
+        if etype != "float32":
+            raise ArgumentError(f"unsupported etype {etype!r} (the device store is fp32)")
+        if tcp is not None:
+            raise ArgumentError("the TCP level-1/level-2 link is out of scope on one box "
+                                "(kvstore.py:139-158); all workers share NVLink")
+        self.machines, self.workers, self.mode, self.etype = machines, workers, mode, etype
+        self.nw = machines * workers
+        self.engine = engine or default_engine()
+        self.distributed = distributed
+        self.bucket_bytes = int(bucket_bytes)
+        self.timeout = timeout
+        if distributed:
+            import torch.distributed as dist
+            if not dist.is_initialized():
+                raise ArgumentError("distributed KVStore needs torch.distributed initialised")
+            if dist.get_world_size() != self.nw:
+                raise ArgumentError(f"world size {dist.get_world_size()} != machines*workers "
+                                    f"{self.nw}")
+            if mode != "sequential":
+                raise ArgumentError("eventual mode is single-process only")
+            self.rank = dist.get_rank()
+            self.local_workers = [self.rank]
+        else:
+            self.rank = 0
+            self.local_workers = list(range(self.nw))
+        self._lock = threading.RLock()
+        self._cv = threading.Condition(self._lock)
+        self._keys: Dict[int, _Key] = {}
+        self._order: List[int] = []          # init order
+        self._arenas: List[_Arena] = []
+        self._rounds: Dict[Tuple[int, int], int] = {}
+        self._pushed: Dict[int, set] = {}    # key -> local workers pushed this round
+        self._pending: List[int] = []        # keys whose round is complete, not reduced
+        self._stats = {"level2_messages": 0, "level2_updates": 0, "level1_aggregates": 0,
+                       "pushes": 0, "pulls": 0, "flushes": 0, "launches": 0}
+        self._updater: Callable = add_updater
+        self._native = L.KV_ADD
+        self._sgd = None                      # (eta, momentum, wd, scale)
+        self._epoch = 0
+        self._err = None
+        self._closed = False
+        self._grid_cap = None
+
+    # ------------------------------------------------------------ public API
+
+    def init(self, key: int, value) -> None:
+        """Register ``key`` with its initial value (kvstore.py:162-181)."""
+        if not isinstance(key, (int, np.integer)) or key < 0:
+            raise ArgumentError("keys are non-negative integers")
+        key = int(key)
+        if isinstance(value, Tensor):
+            arr = tmod.to_numpy(value)
+        else:
+            import torch
+            if isinstance(value, torch.Tensor):
+                arr = value.detach().float().cpu().numpy()
+            else:
+                arr = np.array(value, dtype=np.float32)
+        arr = np.ascontiguousarray(arr, dtype=np.float32)
+        with self._lock:
+            if key in self._keys:
+                raise KVStoreError(f"double init of key {key}")
+            self._keys[key] = _Key(key, tuple(arr.shape), int(arr.size), arr.ravel().copy())
+            self._order.append(key)
+
+    def set_updater(self, fn: Callable) -> None:
+        """Install the level-2 merge function (kvstore.py:183-188).  The
+        momentum-SGD updater from ``optim.make_sgd_updater`` and the default
+        add run fused in the reduce kernel; any other callable runs on
+        device tensors after an aggregate-only reduction."""
+        with self._lock:
+            self._flush_locked()
+            sgd = getattr(fn, "_mgx_sgd", None)
+            if sgd is not None:
+                cfg, scale = sgd
+                self._native = L.KV_SGD
+                self._sgd = (float(np.float32(cfg.eta)), float(np.float32(cfg.momentum)),
+                             float(np.float32(cfg.weight_decay)),
+                             float(np.float32(1.0 / scale)))
+            elif fn is add_updater:
+                self._native = L.KV_ADD
+            else:
+                self._native = L.KV_AGG
+            self._updater = fn
+
+    def push(self, key: int, value: Tensor, worker: int) -> None:
+        """Join this worker's next round for ``key`` (kvstore.py:190-211)."""
+        self._check_worker(worker)
+        k = self._key(key)
+        if value.shape != k.shape:
+            raise KVStoreError(f"push shape {value.shape} != init shape {k.shape}")
+        if value.engine is not self.engine:
+            raise ArgumentError("pushed tensor is on another engine")
+        with self._lock:
+            ar = self._materialize_locked(k)
+            r = self._rounds.get((worker, key), 0) + 1
+            self._rounds[(worker, key)] = r
+            self._stats["pushes"] += 1
+            dst = ar.grads[self._slot(worker)] + 4 * k.off
+            if value.ptr != dst:
+                self.engine.push(lambda: L.call("mgx_copy", value.ptr, dst, k.numel,
+                                                self.engine.stream_handle),
+                                 reads=[value.tag], label=f"kv-push:{key}")
+            if self.mode == "eventual":
+                self._launch_locked([key], single_worker=self._slot(worker))
+                return
+            done = self._pushed.setdefault(key, set())
+            if worker in done:
+                raise StateError(f"worker {worker} pushed key {key} twice in one round")
+            done.add(worker)
+            if len(done) == len(self.local_workers):
+                self._pushed[key] = set()
+                self._pending.append(key)
+                self._cv.notify_all()
+                if self._bucket_complete_locked(k):
+                    self._flush_locked()
+
+    def pull(self, key: int, out: Tensor, worker: int) -> None:
+        """Copy this worker's round value of ``key`` into ``out``
+        (kvstore.py:213-241)."""
+        self._check_worker(worker)
+        k = self._key(key)
+        if out.shape != k.shape:
+            raise KVStoreError(f"pull shape {out.shape} != init shape {k.shape}")
+        if out.engine is not self.engine:
+            raise ArgumentError("pulled tensor is on another engine")
+        with self._lock:
+            ar = self._materialize_locked(k)
+            self._stats["pulls"] += 1
+            if self.mode == "sequential":
+                want = self._rounds.get((worker, key), 0)
+                self._wait_round_locked(key, want)
+                if key in self._pending:
+                    self._flush_locked()
+            src = ar.weights[self._slot(worker)] + 4 * k.off
+            if out.ptr != src:
+                self.engine.push(lambda: L.call("mgx_copy", src, out.ptr, k.numel,
+                                                self.engine.stream_handle),
+                                 writes=[out.tag], label=f"kv-pull:{key}")
+
+    def round_barrier(self) -> None:
+        """Reduce everything pushed so far and wait for the device."""
+        with self._lock:
+            self._flush_locked()
+        self.engine.wait_all()
+        self._check_error()
+
+    def quiesce(self) -> None:
+        self.round_barrier()
+
+    def stats(self) -> Dict[str, int]:
+        with self._lock:
+            return dict(self._stats)
+
+    def close(self) -> None:
+        if self._closed:
+            return
+        with self._lock:
+            self._flush_locked()
+        try:
+            self.engine.synchronize()
+        except Exception:  # noqa: BLE001
+            pass
+        if self.distributed:
+            import torch.distributed as dist
+            dist.barrier()
+        for ar in self._arenas:
+            for p in ar.opened:
+                L.lib().mgx_ipc_close_handle(p)
+            for p in ar.owned_local:
+                L.lib().mgx_free(p)
+        if self._err is not None:
+            L.lib().mgx_host_free(self._err)
+        self._arenas = []
+        self._closed = True
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # -------------------------------------------------- zero-copy endpoints
+
+    def weight_tensor(self, key: int, worker: int) -> Tensor:
+        """The replica ``pull`` reads for ``worker``, as a bindable Tensor
+        (binding it as the executor argument makes pull a no-op)."""
+        return self._view("w", key, worker)
+
+    def grad_tensor(self, key: int, worker: int) -> Tensor:
+        """The buffer ``push`` reduces from for ``worker``; binding it as the
+        executor's gradient makes push copy-free."""
+        return self._view("g", key, worker)
+
+    def _view(self, kind: str, key: int, worker: int) -> Tensor:
+        self._check_worker(worker)
+        k = self._key(key)
+        with self._lock:
+            ar = self._materialize_locked(k)
+            base = (ar.weights if kind == "w" else ar.grads)[self._slot(worker)]
+            import torch
+            full = ar.torch_views.get((kind, worker))
+            if full is None:
+                full = torch.as_tensor(_RawBuffer(base, ar.length), device=f"cuda:{self.engine.device}")
+                ar.torch_views[(kind, worker)] = full
+            return Tensor(k.shape, "float32", engine=self.engine,
+                          _storage=full[k.off: k.off + k.numel].view(k.shape))
+
+    # --------------------------------------------------------------- helpers
+
+    def _check_worker(self, worker: int) -> None:
+        if not 0 <= worker < self.nw:
+            raise ArgumentError(f"no worker {worker} in this topology")
+        if worker not in self.local_workers:
+            raise ArgumentError(f"worker {worker} belongs to another process (rank {worker})")
+
+    def _key(self, key: int) -> _Key:
+        k = self._keys.get(key)
+        if k is None:
+            raise KVStoreError(f"key {key} used before init")
+        return k
+
+    def _slot(self, worker: int) -> int:
+        return worker  # replica / gradient pointer index == worker id
+
+    def _wait_round_locked(self, key: int, want: int) -> None:
+        """Sequential mode: block until every local worker reached round
+        ``want`` for key (other threads may still be pushing)."""
+        def ready():
+            return all(self._rounds.get((w, key), 0) >= want for w in self.local_workers)
+        if not self._cv.wait_for(ready, timeout=self.timeout):
+            raise KVStoreError(f"timed out waiting for round {want} of key {key}")
+
+    def _bucket_complete_locked(self, k: _Key) -> bool:
+        ar = self._arenas[k.arena]
+        members = [kk for kk in ar.keys if self._keys[kk].bucket == k.bucket]
+        return all(m in self._pending for m in members)
+
+    # ------------------------------------------------------------ materialise
+
+    def _materialize_locked(self, k: _Key) -> _Arena:
+        if k.arena >= 0:
+            return self._arenas[k.arena]
+        new = [kk for kk in self._order if self._keys[kk].arena < 0]
+        numels = [self._keys[kk].numel for kk in new]
+        offs, buckets, kb = plan_buckets(numels, self.bucket_bytes)
+        length = sum(padded(n) for n in numels)
+        ar = _Arena(keys=new, length=length, buckets=buckets)
+        aid = len(self._arenas)
+        for kk, off, b in zip(new, offs, kb):
+            self._keys[kk].off, self._keys[kk].bucket, self._keys[kk].arena = off, b, aid
+        self.engine.activate()
+        nbytes = 4 * length
+        st = self.engine.stream_handle
+
+        def alloc(n):
+            p = ctypes.c_void_p()
+            L.call("mgx_malloc", n, ctypes.byref(p))
+            ar.owned_local.append(p.value)
+            L.call("mgx_memset_async", p.value, 0, n, st)
+            return p.value
+
+        if self._err is None:
+            p = ctypes.c_void_p()
+            L.call("mgx_host_alloc", 64, ctypes.byref(p))
+            ctypes.memset(p.value, 0, 64)
+            self._err = p.value
+        if self.distributed:
+            self._materialize_distributed(ar, alloc, nbytes)
+        else:
+            ar.weights = [alloc(nbytes) for _ in range(self.nw)]
+            ar.grads = [alloc(nbytes) for _ in range(self.nw)]
+            ar.velocity = alloc(nbytes)
+            ar.vlen = length
+            for b, (lo, _hi) in enumerate(buckets):
+                for r in range(self.nw):
+                    ar.voff[(b, r)] = lo  # full layout: velocity offset == arena offset
+            for kk in new:
+                key = self._keys[kk]
+                host = key.init
+                for w in range(self.nw):
+                    dst = ar.weights[w] + 4 * key.off
+                    L.call("mgx_memcpy_async", dst, host.ctypes.data, 4 * key.numel, st)
+            L.call("mgx_stream_sync", st)
+        for kk in new:
+            self._keys[kk].init = None
+        self._arenas.append(ar)
+        return ar
+
+    def _materialize_distributed(self, ar: _Arena, alloc, nbytes: int) -> None:
+        import torch.distributed as dist
+        st = self.engine.stream_handle
+        own_w = alloc(nbytes)
+        own_g = alloc(nbytes)
+        flag_bytes = 4 * L.KV_FLAG_WORDS_PER_WORKER * self.nw
+        own_f = alloc(flag_bytes)
+        ar.epoch_ctr = alloc(256)
+        # compact momentum layout: this rank's shard of every bucket
+        vpos = 0
+        for b, (lo, hi) in enumerate(ar.buckets):
+            s0, s1 = shard_ranges(hi - lo, self.nw)[self.rank]
+            ar.voff[(b, self.rank)] = vpos
+            vpos += s1 - s0
+        ar.vlen = vpos
+        ar.velocity = alloc(max(4 * vpos, 256))
+        for kk in ar.keys:
+            key = self._keys[kk]
+            L.call("mgx_memcpy_async", own_w + 4 * key.off, key.init.ctypes.data,
+                   4 * key.numel, st)
+        L.call("mgx_stream_sync", st)
+
+        def handle(p):
+            buf = ctypes.create_string_buffer(L.IPC_HANDLE_BYTES)
+            L.call("mgx_ipc_get_handle", p, buf)
+            return buf.raw
+
+        mine = (handle(own_w), handle(own_g), handle(own_f))
+        everyone: List = [None] * self.nw
+        dist.all_gather_object(everyone, mine)
+
+        def open_(h, own):
+            if h == mine[0] or h == mine[1] or h == mine[2]:
+                return own
+            p = ctypes.c_void_p()
+            L.call("mgx_ipc_open_handle", ctypes.create_string_buffer(h, L.IPC_HANDLE_BYTES),
+                   ctypes.byref(p))
+            ar.opened.append(p.value)
+            return p.value
+
+        for r in range(self.nw):
+            hw, hg, hf = everyone[r]
+            ar.weights.append(own_w if r == self.rank else open_(hw, own_w))
+            ar.grads.append(own_g if r == self.rank else open_(hg, own_g))
+            ar.flags.append(own_f if r == self.rank else open_(hf, own_f))
+        dist.barrier()
+        # every replica starts from worker 0's init value (kvstore init
+        # broadcasts one value, kvstore.py:177-181)
+        if self.rank != 0:
+            L.call("mgx_memcpy_async", own_w, ar.weights[0], nbytes, st)
+            L.call("mgx_stream_sync", st)
+        dist.barrier()
+
+    # -------------------------------------------------------------- reduce
+
+    def _flush_locked(self) -> None:
+        if not self._pending:
+            return
+        pending, self._pending = self._pending, []
+        by_arena: Dict[int, List[int]] = {}
+        for key in pending:
+            by_arena.setdefault(self._keys[key].arena, []).append(key)
+        for aid in sorted(by_arena):
+            self._launch_locked(by_arena[aid])
+        self._stats["flushes"] += 1
+        for key in pending:
+            self._stats["level1_aggregates"] += self.machines
+            self._stats["level2_messages"] += self.machines
+            self._stats["level2_updates"] += 1
+
+    def _segments(self, ar: _Arena, keys: List[int], owners: List[int],
+                  whole_keys: bool = False) -> List[Tuple[int, int, int]]:
+        segs = []
+        for key in sorted(keys, key=lambda kk: self._keys[kk].off):
+            k = self._keys[key]
+            klo, khi = k.off, k.off + padded(k.numel)
+            if whole_keys:
+                segs.append((klo, khi - klo, klo))
+                continue
+            blo, bhi = ar.buckets[k.bucket]
+            shards = shard_ranges(bhi - blo, self.nw)
+            for r in owners:
+                s0, s1 = shards[r]
+                lo, hi = max(klo, blo + s0), min(khi, blo + s1)
+                if lo < hi:
+                    segs.append((lo, hi - lo, ar.voff[(k.bucket, r)] + (lo - blo - s0)
+                                 if self.distributed else lo))
+        return segs
+
+    def _grid_locked(self, total_elems: int) -> int:
+        if self._grid_cap is None:
+            cap = ctypes.c_int32()
+            L.call("mgx_kv_max_grid", self.machines, self.workers, ctypes.byref(cap))
+            self._grid_cap = cap.value
+        per_rank4 = -(-total_elems // (4 * self.nw))
+        want = -(-per_rank4 // 1024)
+        return max(1, min(self._grid_cap, want))
+
+    def _launch_locked(self, keys: List[int], single_worker: Optional[int] = None) -> None:
+        ar = self._arenas[self._keys[keys[0]].arena]
+        updater = self._native
+        custom = updater == L.KV_AGG
+        if custom and ar.agg == 0:
+            p = ctypes.c_void_p()
+            L.call("mgx_malloc", 4 * ar.length, ctypes.byref(p))
+            ar.owned_local.append(p.value)
+            ar.agg = p.value
+        if single_worker is not None:
+            # eventual mode: apply this worker's push alone
+            segs = self._segments(ar, keys, [], whole_keys=True)
+            machines, workers = 1, 1
+            grads = [ar.grads[single_worker]]
+            weights = list(ar.weights)
+        else:
+            owners = self.local_workers if self.distributed else list(range(self.nw))
+            segs = self._segments(ar, keys, owners, whole_keys=custom)
+            machines, workers = self.machines, self.workers
+            grads, weights = ar.grads, ar.weights
+        total = sum(padded(self._keys[kk].numel) for kk in keys)
+        barrier = self.distributed and single_worker is None
+        nchunks = -(-max(len(segs), 1) // L.KV_MAX_SEGS)
+        if barrier and not custom:
+            # every rank must launch the same number of kernels so the
+            # device barrier epochs line up: use the largest owner's count
+            most = max(len(self._segments(ar, keys, [r])) for r in range(self.nw))
+            nchunks = -(-max(most, 1) // L.KV_MAX_SEGS)
+        for c in range(nchunks):
+            chunk = segs[c * L.KV_MAX_SEGS: (c + 1) * L.KV_MAX_SEGS]
+            self._launch_one(ar, chunk, machines, workers, grads, weights, updater, total,
+                             barrier=barrier)
+        if custom:
+            self._run_custom_updater(ar, keys)
+
+    def _launch_one(self, ar, segs, machines, workers, grads, weights, updater, total,
+                    barrier: bool) -> None:
+        nw = machines * workers
+        a = L.KvRoundArgs()
+        seg_arr = (L.KvSeg * max(len(segs), 1))()
+        for i, (off, ln, voff) in enumerate(segs):
+            seg_arr[i].off, seg_arr[i].len, seg_arr[i].voff = off, ln, voff
+        g_arr = (ctypes.c_void_p * nw)(*grads[:nw])
+        w_arr = (ctypes.c_void_p * len(weights))(*weights)
+        a.segs = seg_arr
+        a.nseg = len(segs)
+        a.machines, a.workers = machines, workers
+        a.grads = ctypes.cast(g_arr, ctypes.POINTER(ctypes.c_void_p))
+        a.weights = ctypes.cast(w_arr, ctypes.POINTER(ctypes.c_void_p))
+        a.self_replica = self.rank if self.distributed else 0
+        a.velocity = ar.velocity
+        a.agg_out = ar.agg or None
+        a.updater = updater
+        if self._sgd is not None:
+            eta, mom, wd, rescale = self._sgd
+            a.rescale, a.neg_eta, a.momentum, a.weight_decay = rescale, -eta, mom, wd
+        f_arr = None
+        if barrier:
+            self._epoch += 1
+            f_arr = (ctypes.c_void_p * nw)(*ar.flags)
+            a.flags = ctypes.cast(f_arr, ctypes.POINTER(ctypes.c_void_p))
+            a.rank = self.rank
+            a.epoch_ctr = ar.epoch_ctr
+            a.error_word = self._err
+            a.grid = self._grid_locked(total)
+        else:
+            a.flags = None
+            a.grid = 0
+        # an eventual-mode push reduces one source; the kernel stores into
+        # that many replicas, the rest are refreshed by a copy below
+        broadcast_rest = nw == 1 and len(weights) > 1
+        self.engine.activate()
+        L.call("mgx_kv_round", ctypes.byref(a), self.engine.stream_handle)
+        self._stats["launches"] += 1
+        if broadcast_rest and updater != L.KV_AGG:
+            for off, ln, _ in segs:
+                for w in weights[1:]:
+                    L.call("mgx_copy", weights[0] + 4 * off, w + 4 * off, ln,
+                           self.engine.stream_handle)
+
+    def _run_custom_updater(self, ar: _Arena, keys: List[int]) -> None:
+        import torch
+        dev = f"cuda:{self.engine.device}"
+        own = self.rank if self.distributed else 0
+        stored_full = torch.as_tensor(_RawBuffer(ar.weights[own], ar.length), device=dev)
+        agg_full = torch.as_tensor(_RawBuffer(ar.agg, ar.length), device=dev)
+        with torch.cuda.stream(self.engine.stream):
+            for key in keys:
+                k = self._keys[key]
+                stored = stored_full[k.off: k.off + k.numel].view(k.shape)
+                incoming = agg_full[k.off: k.off + k.numel].view(k.shape)
+                self._updater(key, stored, incoming)
+                if not self.distributed:
+                    for w in range(1, self.nw):
+                        L.call("mgx_copy", ar.weights[0] + 4 * k.off, ar.weights[w] + 4 * k.off,
+                               k.numel, self.engine.stream_handle)
+
+    def _check_error(self) -> None:
+        if self._err is not None and ctypes.c_uint32.from_address(self._err).value:
+            raise KVStoreError("a peer did not reach the device barrier within 30 s")

@@ -1,0 +1,299 @@
+"""Training drivers: the data-parallel step over the device KVStore.
+
+Mirrors the reference's train.py (mlp/param_names/init_params/TrainReport,
+train_local, train_distributed; train.py:57-270) with the per-worker step
+
+    pull every key -> load the worker's row shard -> forward -> backward
+    -> push every key -> read the outputs
+
+Worker g takes rows [g*B/N, (g+1)*B/N) of every global batch and every
+worker walks the same shuffled batch order (train.py:166-168, 195, 206).
+Executors are bound zero-copy to the store: a worker's parameter arguments
+ARE its KVStore replica and its gradient outputs ARE its KVStore gradient
+buffer, so push/pull move no bytes and the only data-path kernels are the
+graph's and the store's fused reduce+update+broadcast.
+
+``DataParallelStep`` is the reusable core; it can also capture one whole
+step (forward, backward, store round) into a single CUDA graph.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import _lib as L
+from . import symbol
+from . import tensor as tmod
+from .data import BatchOrder, read_examples
+from .engine import Engine, default_engine
+from .errors import ArgumentError
+from .executor import bind
+from .kvstore import KVStore
+from .optim import SGDConfig, make_sgd_updater, sgd_step
+from .symbol import SymbolGraph, infer_shape
+
+RESERVED_ARGS = ("data", "label")
+CSV_HEADER = "epoch,loss,acc,seconds,planner_bytes,engine_ops"
+
+
+@dataclass
+class TrainReport:
+    rows: List[tuple] = field(default_factory=list)
+
+    def append(self, epoch, loss, acc, seconds, planner_bytes, engine_ops) -> None:
+        self.rows.append((epoch, loss, acc, seconds, planner_bytes, engine_ops))
+
+    def to_csv(self) -> str:
+        out = [CSV_HEADER]
+        for e, loss, acc, sec, pb, ops in self.rows:
+            out.append(f"{e},{loss!r},{acc!r},{sec:.3f},{pb},{ops}")
+        return "\n".join(out) + "\n"
+
+    def save(self, path: str) -> None:
+        with open(path, "w") as f:
+            f.write(self.to_csv())
+
+
+def mlp(hidden: Sequence[int], classes: int) -> SymbolGraph:
+    """relu MLP ending in a softmax loss head (train.py:57-67)."""
+    net = symbol.variable("data")
+    for i, h in enumerate(hidden, 1):
+        net = symbol.apply("FullyConnected", {"num_hidden": int(h)}, [net], name=f"fc{i}")
+        net = symbol.apply("Activation", {"act_type": "relu"}, [net], name=f"act{i}")
+    net = symbol.apply("FullyConnected", {"num_hidden": int(classes)}, [net], name="out")
+    return symbol.apply("SoftmaxOutput", {}, [net], name="softmax")
+
+
+def param_names(g: SymbolGraph) -> List[str]:
+    return [n for n in g.list_arguments() if n not in RESERVED_ARGS]
+
+
+def init_params(g: SymbolGraph, arg_shapes: Dict[str, tuple], seed: int) -> Dict[str, np.ndarray]:
+    """randn*0.1 weights in parameter order, zero biases (train.py:74-85)."""
+    rs = np.random.RandomState(seed)
+    out = {}
+    for name in param_names(g):
+        shape = arg_shapes[name]
+        if name.endswith("_bias"):
+            out[name] = np.zeros(shape, dtype=np.float32)
+        else:
+            out[name] = (rs.randn(*shape) * 0.1).astype(np.float32)
+    return out
+
+
+def cross_entropy_mean(probs: np.ndarray, labels: np.ndarray, eps: float = 1e-12) -> float:
+    """Host-side metric only (kernels.py:86-89)."""
+    idx = labels.astype(np.int64)
+    picked = probs[np.arange(idx.shape[0]), idx]
+    return float(np.mean(-np.log(np.maximum(picked, eps))))
+
+
+def _check_graph(g: SymbolGraph):
+    args = g.list_arguments()
+    for need in RESERVED_ARGS:
+        if need not in args:
+            raise ArgumentError(f"training graph needs a {need!r} argument")
+
+
+def _load(data) -> Tuple[np.ndarray, np.ndarray]:
+    if isinstance(data, str):
+        return read_examples(data)
+    feats, labels = data
+    return np.asarray(feats, np.float32), np.asarray(labels, np.float32)
+
+
+class DataParallelStep:
+    """One data-parallel training step over a device KVStore.
+
+    Binds one executor per local worker (all workers in a single-process
+    store, the rank's own worker in a distributed one) against the store's
+    replicas and gradient buffers.
+    """
+
+    def __init__(self, g: SymbolGraph, kv: KVStore, shard_shapes: Dict[str, tuple],
+                 params0: Dict[str, np.ndarray], strategy: str = "both",
+                 engine: Optional[Engine] = None, use_graph: bool = True):
+        _check_graph(g)
+        self.g, self.kv = g, kv
+        self.engine = engine or kv.engine
+        self.names = param_names(g)
+        for i, n in enumerate(self.names):
+            kv.init(i, params0[n])
+        self.workers = list(kv.local_workers)
+        self.args: Dict[int, Dict[str, tmod.Tensor]] = {}
+        self.grads: Dict[int, Dict[str, tmod.Tensor]] = {}
+        self.execs = {}
+        for w in self.workers:
+            args = {"data": tmod.zeros(shard_shapes["data"], engine=self.engine),
+                    "label": tmod.zeros(shard_shapes["label"], engine=self.engine)}
+            grads = {}
+            for i, n in enumerate(self.names):
+                args[n] = kv.weight_tensor(i, w)
+                grads[n] = kv.grad_tensor(i, w)
+            self.args[w], self.grads[w] = args, grads
+            self.execs[w] = bind(g, args, {n: "write" for n in self.names}, grads,
+                                 strategy=strategy, engine=self.engine, use_graph=use_graph)
+        self.plan_bytes = self.execs[self.workers[0]].plan.total_internal_bytes
+        self._graph_exec = None
+
+    # host-staged step (the reference's per-step sequence)
+    def load(self, w: int, feats, labels) -> None:
+        tmod.load_host(self.args[w]["data"], feats)
+        tmod.load_host(self.args[w]["label"], labels)
+
+    def run_worker(self, w: int, pull: bool = True) -> None:
+        kv, ex = self.kv, self.execs[w]
+        if pull:
+            for i, n in enumerate(self.names):
+                kv.pull(i, self.args[w][n], w)
+        ex.forward()
+        ex.backward()
+        for i, n in enumerate(self.names):
+            kv.push(i, self.grads[w][n], w)
+
+    def step(self, shards: Optional[Dict[int, Tuple[np.ndarray, np.ndarray]]] = None) -> None:
+        """pull -> (load) -> forward -> backward -> push, for every local worker."""
+        for w in self.workers:
+            for i, n in enumerate(self.names):
+                self.kv.pull(i, self.args[w][n], w)
+            if shards is not None:
+                self.load(w, *shards[w])
+            ex = self.execs[w]
+            ex.forward()
+            ex.backward()
+            for i, n in enumerate(self.names):
+                self.kv.push(i, self.grads[w][n], w)
+
+    def outputs(self, w: int) -> np.ndarray:
+        return tmod.to_numpy(self.execs[w].outputs[0])
+
+    # ---------------------------------------------------- whole-step graph
+
+    def capture(self) -> None:
+        """Capture one device-resident step (all workers) as a CUDA graph.
+        Executors run eagerly inside the capture; the store's launches use a
+        device-side barrier epoch, so replays stay correct."""
+        for ex in self.execs.values():
+            ex._use_graph = False
+        self.engine.activate()
+        self.engine.synchronize()
+        import torch
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=self.engine.stream, capture_error_mode="thread_local"):
+            self.step()
+            with self.kv._lock:
+                self.kv._flush_locked()
+        self._graph_exec = g
+
+    def replay(self) -> None:
+        if self._graph_exec is None:
+            raise ArgumentError("capture() first")
+        self._graph_exec.replay()
+
+
+# ----------------------------------------------------------------- drivers
+
+def train_local(g: SymbolGraph, data, cfg: SGDConfig, epochs: int, batch: int,
+                strategy: str = "both", param_seed: int = 0, shuffle_seed: int = 0,
+                prefetch: int = 2, engine: Optional[Engine] = None
+                ) -> Tuple[TrainReport, Dict[str, np.ndarray]]:
+    """Single-device SGD (train.py:97-153): forward, backward, then one
+    fused SGD kernel per parameter."""
+    _check_graph(g)
+    engine = engine or default_engine()
+    feats, labels = _load(data)
+    it = BatchOrder(feats, labels, batch, seed=shuffle_seed)
+    if it.batches_per_epoch < 1:
+        raise ArgumentError("batch size exceeds the dataset")
+    given = {"data": (batch, feats.shape[1]), "label": (batch,)}
+    arg_shapes, _ = infer_shape(g, given)
+    params0 = init_params(g, arg_shapes, param_seed)
+    names = param_names(g)
+    args = {"data": tmod.zeros(given["data"], engine=engine),
+            "label": tmod.zeros(given["label"], engine=engine)}
+    for n in names:
+        args[n] = tmod.from_host(arg_shapes[n], "float32", params0[n], engine=engine)
+    grads = {n: tmod.zeros(arg_shapes[n], engine=engine) for n in names}
+    vel = {n: tmod.zeros(arg_shapes[n], engine=engine) for n in names}
+    ex = bind(g, args, {n: "write" for n in names}, grads, strategy=strategy, engine=engine)
+    report = TrainReport()
+    last = engine.executed
+    for epoch in range(epochs):
+        t0 = time.perf_counter()
+        losses, correct, seen = [], 0, 0
+        for fb, lb in it.epoch(epoch):
+            tmod.load_host(args["data"], fb)
+            tmod.load_host(args["label"], lb)
+            ex.forward()
+            ex.backward()
+            for n in names:
+                sgd_step(args[n], grads[n], vel[n], vel[n], cfg)
+            probs = tmod.to_numpy(ex.outputs[0]).astype(np.float64).reshape(batch, -1)
+            losses.append(cross_entropy_mean(probs, lb))
+            correct += int((probs.argmax(axis=1) == lb).sum())
+            seen += batch
+        engine.wait_all()
+        report.append(epoch, float(np.mean(losses)), correct / seen, time.perf_counter() - t0,
+                      ex.plan.total_internal_bytes, engine.executed - last)
+        last = engine.executed
+    params = {n: tmod.to_numpy(args[n]) for n in names}
+    return report, params
+
+
+def train_distributed(g: SymbolGraph, data, cfg: SGDConfig, epochs: int, batch: int,
+                      machines: int = 1, workers: int = 1, mode: str = "sequential",
+                      strategy: str = "both", param_seed: int = 0, shuffle_seed: int = 0,
+                      tcp: Optional[str] = None, distributed: bool = False,
+                      engine: Optional[Engine] = None
+                      ) -> Tuple[TrainReport, Dict[str, np.ndarray]]:
+    """Data-parallel SGD through the device KVStore (train.py:158-270).
+
+    ``distributed=False``: all M*W workers in this process on one device (the
+    reference's threading model).  ``distributed=True``: one worker per
+    torch.distributed rank (launch with torchrun, world size M*W)."""
+    _check_graph(g)
+    nworkers = machines * workers
+    if batch % nworkers:
+        raise ArgumentError(f"batch {batch} not divisible by {nworkers} workers")
+    shard = batch // nworkers
+    feats, labels = _load(data)
+    it = BatchOrder(feats, labels, batch, seed=shuffle_seed)
+    if it.batches_per_epoch < 1:
+        raise ArgumentError("batch size exceeds the dataset")
+    given = {"data": (shard, feats.shape[1]), "label": (shard,)}
+    arg_shapes, _ = infer_shape(g, given)
+    params0 = init_params(g, arg_shapes, param_seed)
+    engine = engine or default_engine()
+    kv = KVStore(machines, workers, mode, engine=engine, tcp=tcp, distributed=distributed)
+    try:
+        step = DataParallelStep(g, kv, given, params0, strategy=strategy, engine=engine)
+        kv.set_updater(make_sgd_updater(cfg, scale=nworkers))
+        report = TrainReport()
+        last = engine.executed
+        for epoch in range(epochs):
+            t0 = time.perf_counter()
+            losses, correct, seen = [], 0, 0
+            for fb, lb in it.epoch(epoch):
+                shards = {w: (fb[w * shard:(w + 1) * shard], lb[w * shard:(w + 1) * shard])
+                          for w in step.workers}
+                step.step(shards)
+                for w in step.workers:
+                    probs = step.outputs(w).astype(np.float64).reshape(shard, -1)
+                    lw = shards[w][1]
+                    losses.append(cross_entropy_mean(probs, lw))
+                    correct += int((probs.argmax(axis=1) == lw).sum())
+                    seen += shard
+            kv.round_barrier()
+            report.append(epoch, float(np.mean(losses)), correct / seen,
+                          time.perf_counter() - t0, step.plan_bytes, engine.executed - last)
+            last = engine.executed
+        w0 = step.workers[0]
+        params = {n: tmod.to_numpy(step.args[w0][n]) for n in step.names}
+    finally:
+        kv.close()
+    return report, params

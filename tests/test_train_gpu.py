@@ -1,0 +1,158 @@
+"""End-to-end data-parallel training on the GPU vs the reference.
+
+Parity bar (BASELINE.json north_star): fp32 weights after N steps within
+rtol 1e-5 / atol 1e-6 of the reference's train_distributed.  The only
+non-reproducible op is numpy's SIMD float32 exp in the softmax (ulp-level);
+every other reduction order is the reference's."""
+
+import numpy as np
+import pytest
+
+from oracle import step as ostep
+
+pytestmark = pytest.mark.gpu
+F32 = np.float32
+RTOL, ATOL = 1e-5, 1e-6
+
+
+def run_dist(engine, n, batch, machines, workers, **kw):
+    from paper_1512_01274_b200 import symbol
+    from paper_1512_01274_b200.optim import SGDConfig
+    from paper_1512_01274_b200.train import mlp, train_distributed
+    symbol.reset_names()
+    feats, labels = ostep.cfg1_data(n)
+    return train_distributed(mlp([128, 64], 10), (feats, labels), SGDConfig(0.05, 0.9, 1e-4),
+                             epochs=1, batch=batch, machines=machines, workers=workers,
+                             engine=engine, **kw)
+
+
+@pytest.mark.parametrize("tag,batch,machines,workers,n", [
+    ("w2b100", 100, 1, 2, 500), ("w2b100", 100, 1, 2, 2000),
+    ("w8b128", 128, 1, 8, 500), ("m2w2b128", 128, 2, 2, 500)])
+def test_config1_weights_match_reference(engine, train_golden, tag, batch, machines, workers, n):
+    _rep, params = run_dist(engine, n, batch, machines, workers)
+    for k, v in params.items():
+        np.testing.assert_allclose(v, train_golden[f"dist_{tag}_n{n}_{k}"], rtol=RTOL, atol=ATOL,
+                                   err_msg=k)
+
+
+def test_train_local_matches_reference(engine, train_golden):
+    from paper_1512_01274_b200 import symbol
+    from paper_1512_01274_b200.optim import SGDConfig
+    from paper_1512_01274_b200.train import mlp, train_local
+    feats, labels = ostep.cfg1_data(500)
+    symbol.reset_names()
+    _rep, params = train_local(mlp([128, 64], 10), (feats, labels), SGDConfig(0.05, 0.9, 1e-4),
+                               epochs=1, batch=100, engine=engine)
+    for k, v in params.items():
+        np.testing.assert_allclose(v, train_golden[f"local_b100_n500_{k}"], rtol=RTOL, atol=ATOL)
+
+
+def test_loss_matches_reference_report(engine, train_golden):
+    rep, _ = run_dist(engine, 500, 100, 1, 2)
+    np.testing.assert_allclose([r[1] for r in rep.rows], train_golden["dist_w2b100_n500_loss"],
+                               rtol=1e-6)
+
+
+def test_power_of_two_sharding_equals_local_on_device(engine):
+    """Reference property (test_train.py:89-96): W=4 of batch 128 equals
+    W=1 of batch 128 bit for bit; on device both paths share kernels."""
+    _r, p4 = run_dist(engine, 512, 128, 1, 4)
+    _r, p1 = run_dist(engine, 512, 128, 1, 1)
+    for k in p4:
+        assert np.array_equal(p4[k], p1[k]), k
+
+
+def test_strategies_and_fusion_do_not_change_numbers(engine):
+    """All planner strategies and the fused/unfused programs agree bitwise
+    (test_executor.py:37-46, test_train.py:58-64)."""
+    from paper_1512_01274_b200 import symbol
+    from paper_1512_01274_b200 import tensor as tmod
+    from paper_1512_01274_b200.executor import bind
+    from paper_1512_01274_b200.train import init_params, mlp, param_names
+    feats, labels = ostep.cfg1_data(50)
+    results = []
+    for strategy in ("none", "inplace", "coshare", "both"):
+        for fuse in (True, False):
+            symbol.reset_names()
+            g = mlp([128, 64], 10)
+            shapes, _ = symbol.infer_shape(g, {"data": (50, 784), "label": (50,)})
+            p0 = init_params(g, shapes, 0)
+            names = param_names(g)
+            args = {"data": tmod.from_host((50, 784), "float32", feats, engine=engine),
+                    "label": tmod.from_host((50,), "float32", labels, engine=engine)}
+            for n in names:
+                args[n] = tmod.from_host(shapes[n], "float32", p0[n], engine=engine)
+            grads = {n: tmod.zeros(shapes[n], engine=engine) for n in names}
+            ex = bind(g, args, {n: "write" for n in names}, grads, strategy=strategy,
+                      engine=engine, fuse=fuse)
+            ex.forward()
+            ex.backward()
+            results.append([tmod.to_numpy(ex.outputs[0])] + [tmod.to_numpy(grads[n]) for n in names])
+    for other in results[1:]:
+        for a, b in zip(results[0], other):
+            assert np.array_equal(a, b)
+
+
+def test_single_step_gradients_vs_oracle(engine):
+    """One worker's gradients: bitwise for everything upstream of nothing
+    but the softmax; tolerance for the rest."""
+    from paper_1512_01274_b200 import symbol
+    from paper_1512_01274_b200 import tensor as tmod
+    from paper_1512_01274_b200.executor import bind
+    from paper_1512_01274_b200.train import init_params, mlp, param_names
+    feats, labels = ostep.cfg1_data(100)
+    g = mlp([128, 64], 10)
+    shapes, _ = symbol.infer_shape(g, {"data": (100, 784), "label": (100,)})
+    p0 = init_params(g, shapes, 0)
+    names = param_names(g)
+    args = {"data": tmod.from_host((100, 784), "float32", feats, engine=engine),
+            "label": tmod.from_host((100,), "float32", labels, engine=engine)}
+    for n in names:
+        args[n] = tmod.from_host(shapes[n], "float32", p0[n], engine=engine)
+    grads = {n: tmod.zeros(shapes[n], engine=engine) for n in names}
+    ex = bind(g, args, {n: "write" for n in names}, grads, engine=engine)
+    assert ex.num_instructions == 10  # 4 forward + 6 backward after fusion
+    ex.forward()
+    ex.backward()
+    p_want, g_want = ostep.mlp_forward_backward(p0, [128, 64], feats, labels)
+    np.testing.assert_allclose(tmod.to_numpy(ex.outputs[0]), p_want, rtol=1e-6, atol=1e-9)
+    for n in names:
+        np.testing.assert_allclose(tmod.to_numpy(grads[n]), g_want[n], rtol=1e-5, atol=1e-7,
+                                   err_msg=n)
+
+
+def test_whole_step_graph_capture_matches_eager(engine):
+    from paper_1512_01274_b200 import symbol
+    from paper_1512_01274_b200 import tensor as tmod
+    from paper_1512_01274_b200.engine import Engine
+    from paper_1512_01274_b200.kvstore import KVStore
+    from paper_1512_01274_b200.optim import SGDConfig, make_sgd_updater
+    from paper_1512_01274_b200.train import DataParallelStep, init_params, mlp
+    feats, labels = ostep.cfg1_data(100)
+    outs = []
+    for captured in (False, True):
+        eng = Engine(device=0)
+        symbol.reset_names()
+        g = mlp([128, 64], 10)
+        given = {"data": (50, 784), "label": (50,)}
+        shapes, _ = symbol.infer_shape(g, given)
+        kv = KVStore(1, 2, engine=eng)
+        st = DataParallelStep(g, kv, given, init_params(g, shapes, 0), engine=eng)
+        kv.set_updater(make_sgd_updater(SGDConfig(0.05, 0.9, 1e-4), scale=2))
+        for w in st.workers:
+            st.load(w, feats[w * 50:(w + 1) * 50], labels[w * 50:(w + 1) * 50])
+        if captured:
+            st.step()  # warm: first real step outside the graph
+            st.capture()
+            for _ in range(4):
+                st.replay()
+        else:
+            for _ in range(5):
+                st.step()
+        kv.round_barrier()
+        outs.append({n: tmod.to_numpy(st.args[0][n]) for n in st.names})
+        kv.close()
+        eng.close()
+    for n in outs[0]:
+        assert np.array_equal(outs[0][n], outs[1][n]), n
