@@ -193,7 +193,10 @@ class DataParallelStep:
     def replay(self) -> None:
         if self._graph_exec is None:
             raise ArgumentError("capture() first")
-        self._graph_exec.replay()
+        import torch
+        # CUDAGraph.replay launches on torch's current stream: make it ours
+        with torch.cuda.stream(self.engine.stream):
+            self._graph_exec.replay()
 
 
 # ----------------------------------------------------------------- drivers
