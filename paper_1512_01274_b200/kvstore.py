@@ -97,6 +97,45 @@ def plan_buckets(numels: List[int], bucket_bytes: int = DEFAULT_BUCKET_BYTES
     return offs, buckets, key_bucket
 
 
+def compact_velocity_layout(buckets: List[Tuple[int, int]], owners: int, owner: int
+                            ) -> Tuple[Dict[int, int], int]:
+    """Momentum layout of one owner: its shard of every bucket, packed in
+    bucket order.  Returns (bucket -> offset, total length)."""
+    offs, pos = {}, 0
+    for b, (lo, hi) in enumerate(buckets):
+        s0, s1 = shard_ranges(hi - lo, owners)[owner]
+        offs[b] = pos
+        pos += s1 - s0
+    return offs, pos
+
+
+def owner_segments(keys: List[Tuple[int, int, int]], buckets: List[Tuple[int, int]],
+                   owners: int, owner: int, vbase: Optional[Dict[int, int]] = None
+                   ) -> List[Tuple[int, int, int]]:
+    """Element ranges ``owner`` reduces for the given keys.
+
+    keys: (arena offset, padded length, bucket) per key, any order.
+    Returns (arena offset, length, momentum offset) segments in arena order;
+    momentum offsets use the compact layout ``vbase`` (bucket -> offset) or,
+    when None, the full layout (momentum offset == arena offset).
+    """
+    segs = []
+    for off, plen, b in sorted(keys):
+        blo, bhi = buckets[b]
+        s0, s1 = shard_ranges(bhi - blo, owners)[owner]
+        lo, hi = max(off, blo + s0), min(off + plen, blo + s1)
+        if lo < hi:
+            voff = lo if vbase is None else vbase[b] + (lo - blo - s0)
+            segs.append((lo, hi - lo, voff))
+    return segs
+
+
+def launches_for(segment_counts: List[int], max_segs: int) -> int:
+    """Kernel launches a flush needs so every rank launches the same number
+    (their device barriers pair up launch by launch)."""
+    return -(-max(max(segment_counts), 1) // max_segs)
+
+
 @dataclass
 class _Key:
     key: int
@@ -443,11 +482,9 @@ class KVStore:
         own_f = alloc(flag_bytes)
         ar.epoch_ctr = alloc(256)
         # compact momentum layout: this rank's shard of every bucket
-        vpos = 0
-        for b, (lo, hi) in enumerate(ar.buckets):
-            s0, s1 = shard_ranges(hi - lo, self.nw)[self.rank]
-            ar.voff[(b, self.rank)] = vpos
-            vpos += s1 - s0
+        vb, vpos = compact_velocity_layout(ar.buckets, self.nw, self.rank)
+        for b, off in vb.items():
+            ar.voff[(b, self.rank)] = off
         ar.vlen = vpos
         ar.velocity = alloc(max(4 * vpos, 256))
         for kk in ar.keys:
@@ -506,22 +543,16 @@ class KVStore:
 
     def _segments(self, ar: _Arena, keys: List[int], owners: List[int],
                   whole_keys: bool = False) -> List[Tuple[int, int, int]]:
+        spans = [(self._keys[kk].off, padded(self._keys[kk].numel), self._keys[kk].bucket)
+                 for kk in keys]
+        if whole_keys:
+            return [(off, plen, off) for off, plen, _b in sorted(spans)]
         segs = []
-        for key in sorted(keys, key=lambda kk: self._keys[kk].off):
-            k = self._keys[key]
-            klo, khi = k.off, k.off + padded(k.numel)
-            if whole_keys:
-                segs.append((klo, khi - klo, klo))
-                continue
-            blo, bhi = ar.buckets[k.bucket]
-            shards = shard_ranges(bhi - blo, self.nw)
-            for r in owners:
-                s0, s1 = shards[r]
-                lo, hi = max(klo, blo + s0), min(khi, blo + s1)
-                if lo < hi:
-                    segs.append((lo, hi - lo, ar.voff[(k.bucket, r)] + (lo - blo - s0)
-                                 if self.distributed else lo))
-        return segs
+        for r in owners:
+            vbase = ({b: ar.voff[(b, r)] for b in range(len(ar.buckets))}
+                     if self.distributed else None)
+            segs += owner_segments(spans, ar.buckets, self.nw, r, vbase)
+        return sorted(segs)
 
     def _grid_locked(self, total_elems: int) -> int:
         if self._grid_cap is None:
@@ -558,8 +589,10 @@ class KVStore:
         if barrier and not custom:
             # every rank must launch the same number of kernels so the
             # device barrier epochs line up: use the largest owner's count
-            most = max(len(self._segments(ar, keys, [r])) for r in range(self.nw))
-            nchunks = -(-max(most, 1) // L.KV_MAX_SEGS)
+            spans = [(self._keys[kk].off, padded(self._keys[kk].numel), self._keys[kk].bucket)
+                     for kk in keys]
+            counts = [len(owner_segments(spans, ar.buckets, self.nw, r)) for r in range(self.nw)]
+            nchunks = launches_for(counts, L.KV_MAX_SEGS)
         for c in range(nchunks):
             chunk = segs[c * L.KV_MAX_SEGS: (c + 1) * L.KV_MAX_SEGS]
             self._launch_one(ar, chunk, machines, workers, grads, weights, updater, total,

@@ -1,0 +1,122 @@
+"""One rank of the multi-GPU KVStore checks (launched by test_kv_dist_gpu.py
+under torchrun; one process per GPU, worker id == rank)."""
+
+import os
+import sys
+import traceback
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+F32 = np.float32
+
+
+def check_kv_golden(eng, world, rank, failures):
+    from paper_1512_01274_b200 import tensor as tmod
+    from paper_1512_01274_b200.kvstore import KVStore
+    from paper_1512_01274_b200.optim import SGDConfig, make_sgd_updater
+    golden = np.load(os.path.join(ROOT, "tests", "golden", "kv_golden.npz"))
+    numels = [1000, 10, 5003]
+    for bucket in (4 << 20, 4096):
+        for upd in ("sgd", "add"):
+            kv = KVStore(1, world, engine=eng, distributed=True, bucket_bytes=bucket)
+            for key, n in enumerate(numels):
+                kv.init(key, (np.random.RandomState(key).randn(n) * 0.1).astype(F32))
+            if upd == "sgd":
+                kv.set_updater(make_sgd_updater(SGDConfig(0.05, 0.9, 1e-4), scale=world))
+            for r in range(3):
+                for key, n in enumerate(numels):
+                    g = np.random.RandomState(1000 + rank + 100 * r + 10000 * key).randn(n)
+                    kv.push(key, tmod.from_host((n,), "float32", g.astype(F32), engine=eng), rank)
+            for key, n in enumerate(numels):
+                o = tmod.zeros((n,), engine=eng)
+                kv.pull(key, o, rank)
+                got = tmod.to_numpy(o)
+                want = golden[f"m1w{world}_{upd}_k{key}"]
+                if not np.array_equal(got, want):
+                    failures.append(f"kv {upd} bucket={bucket} key={key}: "
+                                    f"max diff {np.abs(got - want).max()}")
+            kv.round_barrier()
+            kv.close()
+
+
+def check_training(eng, world, rank, failures):
+    from oracle import step as ostep
+    from paper_1512_01274_b200 import symbol
+    from paper_1512_01274_b200.optim import SGDConfig
+    from paper_1512_01274_b200.train import mlp, train_distributed
+    batch = 100 if 100 % world == 0 else 128
+    feats, labels = ostep.cfg1_data(5 * batch)
+    symbol.reset_names()
+    _rep, params = train_distributed(mlp([128, 64], 10), (feats, labels),
+                                     SGDConfig(0.05, 0.9, 1e-4), epochs=1, batch=batch,
+                                     machines=1, workers=world, distributed=True, engine=eng)
+    want, _ = ostep.train_distributed([128, 64], 10, feats, labels, 0.05, 0.9, 1e-4, epochs=1,
+                                      batch=batch, machines=1, workers=world)
+    for k, v in want.items():
+        if not np.allclose(params[k], v, rtol=1e-5, atol=1e-6):
+            failures.append(f"train {k}: max diff {np.abs(params[k] - v).max()}")
+
+
+def check_capture(eng, world, rank, failures):
+    import torch
+    from oracle import step as ostep
+    from paper_1512_01274_b200 import symbol
+    from paper_1512_01274_b200 import tensor as tmod
+    from paper_1512_01274_b200.engine import Engine
+    from paper_1512_01274_b200.kvstore import KVStore
+    from paper_1512_01274_b200.optim import SGDConfig, make_sgd_updater
+    from paper_1512_01274_b200.train import DataParallelStep, init_params, mlp
+    feats, labels = ostep.cfg1_data(100 * world)
+    outs = []
+    for captured in (False, True):
+        symbol.reset_names()
+        g = mlp([128, 64], 10)
+        given = {"data": (100, 784), "label": (100,)}
+        shapes, _ = symbol.infer_shape(g, given)
+        kv = KVStore(1, world, engine=eng, distributed=True)
+        st = DataParallelStep(g, kv, given, init_params(g, shapes, 0), engine=eng)
+        kv.set_updater(make_sgd_updater(SGDConfig(0.05, 0.9, 1e-4), scale=world))
+        st.load(rank, feats[rank * 100:(rank + 1) * 100], labels[rank * 100:(rank + 1) * 100])
+        if captured:
+            st.step()
+            st.capture()
+            for _ in range(9):
+                st.replay()
+        else:
+            for _ in range(10):
+                st.step()
+        kv.round_barrier()
+        outs.append({n: tmod.to_numpy(st.args[rank][n]) for n in st.names})
+        kv.close()
+    for n in outs[0]:
+        if not np.array_equal(outs[0][n], outs[1][n]):
+            failures.append(f"capture {n} differs from eager")
+
+
+def main():
+    import torch
+    import torch.distributed as dist
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    from paper_1512_01274_b200.engine import Engine
+    eng = Engine(device=local)
+    failures = []
+    for check in (check_kv_golden, check_training, check_capture):
+        try:
+            check(eng, world, rank, failures)
+        except Exception:  # noqa: BLE001
+            failures.append(f"{check.__name__} raised:\n{traceback.format_exc()}")
+        dist.barrier()
+    out = os.environ.get("DIST_RESULT_DIR", ".")
+    with open(os.path.join(out, f"rank{rank}.txt"), "w") as f:
+        f.write("\n".join(failures) if failures else "OK")
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
