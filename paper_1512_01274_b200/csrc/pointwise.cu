@@ -21,8 +21,6 @@ inline unsigned grid_for(int64_t n_vec) {
   return static_cast<unsigned>(blocks);
 }
 
-inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
-
 // Generic vectorised map: out[i] = f(i, in...) over n elements.  Uses float4
 // when every pointer is 16-byte aligned, scalar otherwise.
 template <typename F>
