@@ -86,103 +86,168 @@ int pw_leaf_table(int64_t K, const PwLeaf** out, int* nleaves, int* max_depth) {
   return MGX_OK;
 }
 
-// ----------------------------------------------------- pairwise GEMM kernel
+// --------------------------------------------------------- tile staging
+// Copy rows [r0, r0+R) x cols [c0, c0+kc) of a row-major matrix (row stride
+// ld, K valid columns, nrows valid rows) into smem S[R][kcp] with cp.async.
+// Out-of-range elements are zero-filled.  `vec` = 16-byte copies (needs ld,
+// c0, K multiples of 4 and an aligned base).
+__device__ __forceinline__ void stage_rows(float* S, int kcp, const float* G, int64_t ld,
+                                           int64_t r0, int R, int64_t nrows, int64_t c0, int kc,
+                                           int64_t K, bool vec) {
+  if (vec) {
+    const int per_row = kc >> 2;
+    for (int e = threadIdx.x; e < R * per_row; e += blockDim.x) {
+      const int r = e / per_row, c = (e - r * per_row) << 2;
+      const int64_t gr = r0 + r, gc = c0 + c;
+      const bool ok = gr < nrows && gc < K;
+      cp_async16(S + r * kcp + c, ok ? G + gr * ld + gc : G, ok);
+    }
+  } else {
+    for (int e = threadIdx.x; e < R * kc; e += blockDim.x) {
+      const int r = e / kc, c = e - r * kc;
+      const int64_t gr = r0 + r, gc = c0 + c;
+      const bool ok = gr < nrows && gc < K;
+      cp_async4(S + r * kcp + c, ok ? G + gr * ld + gc : G, ok);
+    }
+  }
+}
 
-constexpr int kPwThreads = 256;  // 32 groups of 8 lanes
+// ----------------------------------------------------- pairwise GEMM kernel
+// Block tile (4*TM) x (8*TN) outputs; 32 groups of 8 lanes, group (gm, gn)
+// owns a TM x TN micro-tile and lane j of the group is numpy's accumulator
+// r[j].  K is streamed through shared memory in chunks of kc (a multiple of
+// 8), double-buffered with cp.async; the leaf walk is a state machine over
+// 8-element blocks so leaves may straddle chunks.
+
+constexpr int kPwThreads = 256;
 constexpr int kPwMaxDepth = 24;
+constexpr int kPwMaxKc = 512;
 
 template <int TM, int TN, bool kStack>
 __global__ void __launch_bounds__(kPwThreads)
 gemm_pairwise_kernel(const float* __restrict__ A, int64_t lda, const float* __restrict__ B,
                      int64_t ldb, const float* __restrict__ bias, float* __restrict__ C,
-                     int64_t ldc, int64_t M, int64_t N, const PwLeaf* __restrict__ leaves,
-                     int nleaves, int act) {
+                     int64_t ldc, int64_t M, int64_t N, int64_t K,
+                     const PwLeaf* __restrict__ leaves, int nleaves, int act, int kc,
+                     bool vecA, bool vecB) {
+  extern __shared__ float4 smem_f4[];
+  float* smem = reinterpret_cast<float*>(smem_f4);
+  constexpr int BM = 4 * TM, BN = 8 * TN;
+  const int kcp = kc + 4;
+  float* As[2] = {smem, smem + (BM + BN) * kcp};
+  float* Bs[2] = {As[0] + BM * kcp, As[1] + BM * kcp};
+
   const int lane8 = threadIdx.x & 7;
-  const int group = threadIdx.x >> 3;  // 0..31: 4 (m) x 8 (n)
-  const int gm = group >> 3;
-  const int gn = group & 7;
-  const int64_t m0 = static_cast<int64_t>(blockIdx.y) * (4 * TM) + gm * TM;
-  const int64_t n0 = static_cast<int64_t>(blockIdx.x) * (8 * TN) + gn * TN;
+  const int group = threadIdx.x >> 3;
+  const int gm = group >> 3, gn = group & 7;
+  const int64_t mb = int64_t(blockIdx.y) * BM, nb = int64_t(blockIdx.x) * BN;
+  const int nchunks = static_cast<int>((K + kc - 1) / kc);
+  const int64_t nblocks = (K + 7) >> 3;
 
-  const float* arow[TM];
-  const float* brow[TN];
-#pragma unroll
-  for (int i = 0; i < TM; ++i) arow[i] = A + (m0 + i < M ? m0 + i : M - 1) * lda;
-#pragma unroll
-  for (int j = 0; j < TN; ++j) brow[j] = B + (n0 + j < N ? n0 + j : N - 1) * ldb;
+  stage_rows(As[0], kcp, A, lda, mb, BM, M, 0, kc, K, vecA);
+  stage_rows(Bs[0], kcp, B, ldb, nb, BN, N, 0, kc, K, vecB);
+  cp_async_commit();
 
+  int leaf = 0;
+  PwLeaf lf = leaves[0];
+  int64_t lb0 = lf.start >> 3;
+  int lnb = lf.len >> 3, ltail = lf.len & 7;
+  int last_rel = ltail ? lnb : lnb - 1;
+
+  float acc[TM][TN], res[TM][TN];
   float stk[kStack ? kPwMaxDepth : 1][TM][TN];
-  float res[TM][TN];
   int sp = 0;
 
-  for (int l = 0; l < nleaves; ++l) {
-    const PwLeaf lf = leaves[l];
-    const int nb = lf.len >> 3;
-    const int tail = lf.len & 7;
-    float acc[TM][TN];
-    if (nb > 0) {
-      int k = lf.start + lane8;
-      float a[TM], b[TN];
-#pragma unroll
-      for (int i = 0; i < TM; ++i) a[i] = __ldg(arow[i] + k);
-#pragma unroll
-      for (int j = 0; j < TN; ++j) b[j] = __ldg(brow[j] + k);
-#pragma unroll
-      for (int i = 0; i < TM; ++i)
-#pragma unroll
-        for (int j = 0; j < TN; ++j) acc[i][j] = fmul(a[i], b[j]);
-      for (int bb = 1; bb < nb; ++bb) {
-        k += 8;
-#pragma unroll
-        for (int i = 0; i < TM; ++i) a[i] = __ldg(arow[i] + k);
-#pragma unroll
-        for (int j = 0; j < TN; ++j) b[j] = __ldg(brow[j] + k);
-#pragma unroll
-        for (int i = 0; i < TM; ++i)
-#pragma unroll
-          for (int j = 0; j < TN; ++j) acc[i][j] = fadd(acc[i][j], fmul(a[i], b[j]));
-      }
-#pragma unroll
-      for (int mask = 1; mask < 8; mask <<= 1)
-#pragma unroll
-        for (int i = 0; i < TM; ++i)
-#pragma unroll
-          for (int j = 0; j < TN; ++j)
-            acc[i][j] = fadd(acc[i][j], __shfl_xor_sync(0xffffffffu, acc[i][j], mask));
+  for (int c = 0; c < nchunks; ++c) {
+    if (c + 1 < nchunks) {
+      const int64_t c0 = int64_t(c + 1) * kc;
+      stage_rows(As[(c + 1) & 1], kcp, A, lda, mb, BM, M, c0, kc, K, vecA);
+      stage_rows(Bs[(c + 1) & 1], kcp, B, ldb, nb, BN, N, c0, kc, K, vecB);
+      cp_async_commit();
+      cp_async_wait<1>();
     } else {
-#pragma unroll
-      for (int i = 0; i < TM; ++i)
-#pragma unroll
-        for (int j = 0; j < TN; ++j) acc[i][j] = 0.0f;  // n < 8: res = 0. then +=
+      cp_async_wait<0>();
     }
-    for (int t = 0; t < tail; ++t) {
-      const int k = lf.start + 8 * nb + t;
+    __syncthreads();
+    const float* a_s = As[c & 1] + gm * TM * kcp;
+    const float* b_s = Bs[c & 1] + gn * TN * kcp;
+    const int64_t jb0 = int64_t(c) * (kc >> 3);
+    const int64_t jb1 = jb0 + (kc >> 3) < nblocks ? jb0 + (kc >> 3) : nblocks;
+    for (int64_t jb = jb0; jb < jb1; ++jb) {
+      const int kk = static_cast<int>(jb - jb0) << 3;
+      const int rel = static_cast<int>(jb - lb0);
+      if (rel < lnb) {
+        float a[TM], b[TN];
 #pragma unroll
-      for (int i = 0; i < TM; ++i) {
-        const float a = __ldg(arow[i] + k);
+        for (int i = 0; i < TM; ++i) a[i] = a_s[i * kcp + kk + lane8];
 #pragma unroll
-        for (int j = 0; j < TN; ++j) acc[i][j] = fadd(acc[i][j], fmul(a, __ldg(brow[j] + k)));
+        for (int j = 0; j < TN; ++j) b[j] = b_s[j * kcp + kk + lane8];
+        if (rel == 0) {
+#pragma unroll
+          for (int i = 0; i < TM; ++i)
+#pragma unroll
+            for (int j = 0; j < TN; ++j) acc[i][j] = fmul(a[i], b[j]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < TM; ++i)
+#pragma unroll
+            for (int j = 0; j < TN; ++j) acc[i][j] = fadd(acc[i][j], fmul(a[i], b[j]));
+        }
+        if (rel == lnb - 1) {
+#pragma unroll
+          for (int mask = 1; mask < 8; mask <<= 1)
+#pragma unroll
+            for (int i = 0; i < TM; ++i)
+#pragma unroll
+              for (int j = 0; j < TN; ++j)
+                acc[i][j] = fadd(acc[i][j], __shfl_xor_sync(0xffffffffu, acc[i][j], mask));
+#pragma unroll
+          for (int i = 0; i < TM; ++i)
+#pragma unroll
+            for (int j = 0; j < TN; ++j) res[i][j] = acc[i][j];
+        }
+      } else {
+        // tail block of the leaf: elements added in order (n < 8 starts at +0)
+        if (lnb == 0) {
+#pragma unroll
+          for (int i = 0; i < TM; ++i)
+#pragma unroll
+            for (int j = 0; j < TN; ++j) res[i][j] = 0.0f;
+        }
+        for (int t = 0; t < ltail; ++t) {
+#pragma unroll
+          for (int i = 0; i < TM; ++i) {
+            const float a = a_s[i * kcp + kk + t];
+#pragma unroll
+            for (int j = 0; j < TN; ++j) res[i][j] = fadd(res[i][j], fmul(a, b_s[j * kcp + kk + t]));
+          }
+        }
+      }
+      if (rel == last_rel) {
+        if constexpr (kStack) {
+#pragma unroll
+          for (int i = 0; i < TM; ++i)
+#pragma unroll
+            for (int j = 0; j < TN; ++j) stk[sp][i][j] = res[i][j];
+          ++sp;
+          for (int q = 0; q < lf.merges; ++q) {
+            --sp;
+#pragma unroll
+            for (int i = 0; i < TM; ++i)
+#pragma unroll
+              for (int j = 0; j < TN; ++j) stk[sp - 1][i][j] = fadd(stk[sp - 1][i][j], stk[sp][i][j]);
+          }
+        }
+        if (++leaf < nleaves) {
+          lf = leaves[leaf];
+          lb0 = lf.start >> 3;
+          lnb = lf.len >> 3;
+          ltail = lf.len & 7;
+          last_rel = ltail ? lnb : lnb - 1;
+        }
       }
     }
-    if constexpr (kStack) {
-#pragma unroll
-      for (int i = 0; i < TM; ++i)
-#pragma unroll
-        for (int j = 0; j < TN; ++j) stk[sp][i][j] = acc[i][j];
-      ++sp;
-      for (int q = 0; q < lf.merges; ++q) {
-        --sp;
-#pragma unroll
-        for (int i = 0; i < TM; ++i)
-#pragma unroll
-          for (int j = 0; j < TN; ++j) stk[sp - 1][i][j] = fadd(stk[sp - 1][i][j], stk[sp][i][j]);
-      }
-    } else {
-#pragma unroll
-      for (int i = 0; i < TM; ++i)
-#pragma unroll
-        for (int j = 0; j < TN; ++j) res[i][j] = acc[i][j];
-    }
+    __syncthreads();
   }
   if constexpr (kStack) {
 #pragma unroll
@@ -190,15 +255,14 @@ gemm_pairwise_kernel(const float* __restrict__ A, int64_t lda, const float* __re
 #pragma unroll
       for (int j = 0; j < TN; ++j) res[i][j] = stk[0][i][j];
   }
-
-  // Epilogue: lane j of the group stores column j of the micro-tile rows,
-  // bias added separately (np.add(res, b), ops.py:106), then activation.
+  // lane j of the group stores outputs (i*TN + j) % 8 == j: bias added
+  // separately (np.add(res, b), ops.py:106), then the activation
 #pragma unroll
   for (int i = 0; i < TM; ++i) {
 #pragma unroll
     for (int j = 0; j < TN; ++j) {
       if ((i * TN + j) % 8 != lane8) continue;
-      const int64_t m = m0 + i, n = n0 + j;
+      const int64_t m = mb + gm * TM + i, n = nb + gn * TN + j;
       if (m >= M || n >= N) continue;
       float v = res[i][j];
       if (bias) v = fadd(v, __ldg(bias + n));
@@ -208,64 +272,82 @@ gemm_pairwise_kernel(const float* __restrict__ A, int64_t lda, const float* __re
 }
 
 // --------------------------------------------------- sequential GEMM kernel
-// Classic shared-memory tiled SIMT GEMM; each output accumulates its K
-// products strictly in order k = 0..K-1, starting from -0.0 (the additive
-// identity, so the first step yields the first product exactly).
+// 32x32 output tile, 16x16 threads with 2x2 outputs; A and B chunks of K
+// staged in smem with cp.async (double-buffered); every output accumulates
+// strictly in k order from -0.0 (the additive identity, so the first step
+// yields the first product exactly).
 
-constexpr int kSeqBM = 64, kSeqBN = 64, kSeqBK = 16, kSeqTM = 4, kSeqTN = 4;
+constexpr int kSeqBM = 32, kSeqBN = 32, kSeqKC = 64;
+
+__device__ __forceinline__ void stage_a_seq(float* As, const float* A, int64_t sam, int64_t sak,
+                                            int64_t mb, int64_t M, int64_t k0, int64_t K) {
+  // As[m][k], row pitch kSeqKC + 1
+  for (int e = threadIdx.x; e < kSeqBM * kSeqKC; e += 256) {
+    const int kk = sak == 1 ? e % kSeqKC : e / kSeqBM;
+    const int mm = sak == 1 ? e / kSeqKC : e % kSeqBM;
+    const int64_t m = mb + mm, k = k0 + kk;
+    const bool ok = m < M && k < K;
+    cp_async4(As + mm * (kSeqKC + 1) + kk, ok ? A + m * sam + k * sak : A, ok);
+  }
+}
+
+__device__ __forceinline__ void stage_b_seq(float* Bs, const float* B, int64_t sbk, int64_t sbn,
+                                            int64_t nb, int64_t N, int64_t k0, int64_t K) {
+  // Bs[k][n], row pitch kSeqBN + 1
+  for (int e = threadIdx.x; e < kSeqKC * kSeqBN; e += 256) {
+    const int nn = sbn == 1 ? e % kSeqBN : e / kSeqKC;
+    const int kk = sbn == 1 ? e / kSeqBN : e % kSeqKC;
+    const int64_t n = nb + nn, k = k0 + kk;
+    const bool ok = n < N && k < K;
+    cp_async4(Bs + kk * (kSeqBN + 1) + nn, ok ? B + k * sbk + n * sbn : B, ok);
+  }
+}
 
 __global__ void __launch_bounds__(256)
 gemm_sequential_kernel(const float* __restrict__ A, int64_t sam, int64_t sak,
                        const float* __restrict__ B, int64_t sbk, int64_t sbn,
                        float* __restrict__ C, int64_t ldc, const float* __restrict__ Y,
                        int act, int64_t M, int64_t N, int64_t K) {
-  __shared__ float As[kSeqBK][kSeqBM + 1];
-  __shared__ float Bs[kSeqBK][kSeqBN + 1];
-  const int tx = threadIdx.x & 15;  // n
-  const int ty = threadIdx.x >> 4;  // m
-  const int64_t mb = static_cast<int64_t>(blockIdx.y) * kSeqBM;
-  const int64_t nb = static_cast<int64_t>(blockIdx.x) * kSeqBN;
-  float acc[kSeqTM][kSeqTN];
-#pragma unroll
-  for (int i = 0; i < kSeqTM; ++i)
-#pragma unroll
-    for (int j = 0; j < kSeqTN; ++j) acc[i][j] = -0.0f;
-
-  for (int64_t k0 = 0; k0 < K; k0 += kSeqBK) {
-    for (int e = threadIdx.x; e < kSeqBK * kSeqBM; e += 256) {
-      // coalesce along whichever of A's axes is contiguous
-      const int kk = sak == 1 ? e % kSeqBK : e / kSeqBM;
-      const int mm = sak == 1 ? e / kSeqBK : e % kSeqBM;
-      const int64_t m = mb + mm, k = k0 + kk;
-      As[kk][mm] = (m < M && k < K) ? __ldg(A + m * sam + k * sak) : 0.0f;
-    }
-    for (int e = threadIdx.x; e < kSeqBK * kSeqBN; e += 256) {
-      const int kk = sbn == 1 ? e / kSeqBN : e % kSeqBK;
-      const int nn = sbn == 1 ? e % kSeqBN : e / kSeqBK;
-      const int64_t n = nb + nn, k = k0 + kk;
-      Bs[kk][nn] = (n < N && k < K) ? __ldg(B + k * sbk + n * sbn) : 0.0f;
+  __shared__ float As[2][kSeqBM * (kSeqKC + 1)];
+  __shared__ float Bs[2][kSeqKC * (kSeqBN + 1)];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int64_t mb = int64_t(blockIdx.y) * kSeqBM, nb = int64_t(blockIdx.x) * kSeqBN;
+  float acc[2][2] = {{-0.0f, -0.0f}, {-0.0f, -0.0f}};
+  const int nchunks = static_cast<int>((K + kSeqKC - 1) / kSeqKC);
+  stage_a_seq(As[0], A, sam, sak, mb, M, 0, K);
+  stage_b_seq(Bs[0], B, sbk, sbn, nb, N, 0, K);
+  cp_async_commit();
+  for (int c = 0; c < nchunks; ++c) {
+    if (c + 1 < nchunks) {
+      stage_a_seq(As[(c + 1) & 1], A, sam, sak, mb, M, int64_t(c + 1) * kSeqKC, K);
+      stage_b_seq(Bs[(c + 1) & 1], B, sbk, sbn, nb, N, int64_t(c + 1) * kSeqKC, K);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
     __syncthreads();
-    const int kmax = static_cast<int>(K - k0 < kSeqBK ? K - k0 : kSeqBK);
+    const float* a_s = As[c & 1];
+    const float* b_s = Bs[c & 1];
+    const int kmax = static_cast<int>(K - int64_t(c) * kSeqKC < kSeqKC ? K - int64_t(c) * kSeqKC
+                                                                       : kSeqKC);
+#pragma unroll 4
     for (int kk = 0; kk < kmax; ++kk) {
-      float a[kSeqTM], b[kSeqTN];
-#pragma unroll
-      for (int i = 0; i < kSeqTM; ++i) a[i] = As[kk][ty + 16 * i];
-#pragma unroll
-      for (int j = 0; j < kSeqTN; ++j) b[j] = Bs[kk][tx + 16 * j];
-#pragma unroll
-      for (int i = 0; i < kSeqTM; ++i)
-#pragma unroll
-        for (int j = 0; j < kSeqTN; ++j) acc[i][j] = fadd(acc[i][j], fmul(a[i], b[j]));
+      const float a0 = a_s[ty * (kSeqKC + 1) + kk], a1 = a_s[(ty + 16) * (kSeqKC + 1) + kk];
+      const float b0 = b_s[kk * (kSeqBN + 1) + tx], b1 = b_s[kk * (kSeqBN + 1) + tx + 16];
+      acc[0][0] = fadd(acc[0][0], fmul(a0, b0));
+      acc[0][1] = fadd(acc[0][1], fmul(a0, b1));
+      acc[1][0] = fadd(acc[1][0], fmul(a1, b0));
+      acc[1][1] = fadd(acc[1][1], fmul(a1, b1));
     }
     __syncthreads();
   }
 #pragma unroll
-  for (int i = 0; i < kSeqTM; ++i) {
+  for (int i = 0; i < 2; ++i) {
     const int64_t m = mb + ty + 16 * i;
     if (m >= M) continue;
 #pragma unroll
-    for (int j = 0; j < kSeqTN; ++j) {
+    for (int j = 0; j < 2; ++j) {
       const int64_t n = nb + tx + 16 * j;
       if (n >= N) continue;
       float v = acc[i][j];
@@ -282,6 +364,8 @@ gemm_sequential_kernel(const float* __restrict__ A, int64_t sam, int64_t sak,
 // of 8 (a perfect T8 in registers), chunk trees go through a binary counter
 // (slot a holds a perfect T(8*2^a)); the n%8 tail rows form T4/T2/T1 by its
 // bits; the pieces are then folded right-associatively, smallest first.
+// The og and x tiles for up to kDwRows batch rows are staged in smem with
+// cp.async (double-buffered over row chunks).
 
 template <int LV, int T>
 struct BatchTree {
@@ -305,8 +389,6 @@ struct BatchTree {
       }
     }
   }
-  // Fold: tail pieces (already combined, smallest-first into `acc`, valid if
-  // have_acc) then slots a = 0..LV-1 for the set bits of nch.
   __device__ __forceinline__ void finish(int nch, bool have_acc, float (&acc)[T]) {
 #pragma unroll
     for (int a = 0; a < LV; ++a) {
@@ -324,7 +406,6 @@ struct BatchTree {
   }
 };
 
-// perfect pairwise tree over v[0..2^L) in registers
 template <int N>
 __device__ __forceinline__ float perfect_tree(const float* v) {
   if constexpr (N == 1) {
@@ -334,110 +415,97 @@ __device__ __forceinline__ float perfect_tree(const float* v) {
   }
 }
 
-constexpr int kDwTH = 2, kDwTF = 2;            // outputs per thread
-constexpr int kDwBH = 16 * kDwTH, kDwBF = 16 * kDwTF;  // 32 x 32 tile
-constexpr int kDwRows = 32;                    // batch rows staged per pass
+constexpr int kDwTH = 2, kDwTF = 2;
+constexpr int kDwBH = 16 * kDwTH, kDwBF = 16 * kDwTF;
+constexpr int kDwRows = 64;  // rows per staged chunk (multiple of 8)
 
 template <int LV>
 __global__ void __launch_bounds__(256)
 fc_dw_db_kernel(const float* __restrict__ og, const float* __restrict__ x, float* __restrict__ dw,
-                float* __restrict__ db, int64_t Bn, int64_t H, int64_t F) {
-  __shared__ float Os[kDwRows][kDwBH];
-  __shared__ float Xs[kDwRows][kDwBF + 1];
-  const int tf = threadIdx.x & 15;
-  const int th = threadIdx.x >> 4;
-  const int64_t hb = static_cast<int64_t>(blockIdx.y) * kDwBH;
-  const int64_t fb = static_cast<int64_t>(blockIdx.x) * kDwBF;
+                float* __restrict__ db, int64_t Bn, int64_t H, int64_t F, bool vecO, bool vecX) {
+  __shared__ __align__(16) float Os[2][kDwRows][kDwBH + 4];
+  __shared__ __align__(16) float Xs[2][kDwRows][kDwBF + 4];
+  const int tf = threadIdx.x & 15, th = threadIdx.x >> 4;
+  const int64_t hb = int64_t(blockIdx.y) * kDwBH, fb = int64_t(blockIdx.x) * kDwBF;
   const bool do_db = db != nullptr && blockIdx.x == 0 && tf == 0;
   const bool do_dw = dw != nullptr;
-
   constexpr int T = kDwTH * kDwTF;
   BatchTree<LV, T> tw;
   BatchTree<LV, kDwTH> tb;
-  const int64_t nch = Bn >> 3;
-  const int tail = static_cast<int>(Bn & 7);
-  float tailv[7][T];
-  float tailb[7][kDwTH];
+  const int nrc = static_cast<int>((Bn + kDwRows - 1) / kDwRows);
 
-  for (int64_t r0 = 0; r0 < Bn; r0 += kDwRows) {
-    const int rows = static_cast<int>(Bn - r0 < kDwRows ? Bn - r0 : kDwRows);
-    for (int e = threadIdx.x; e < kDwRows * kDwBH; e += 256) {
-      const int rr = e / kDwBH, hh = e % kDwBH;
-      const int64_t h = hb + hh;
-      Os[rr][hh] = (rr < rows && h < H) ? __ldg(og + (r0 + rr) * H + h) : 0.0f;
-    }
-    for (int e = threadIdx.x; e < kDwRows * kDwBF; e += 256) {
-      const int rr = e / kDwBF, ff = e % kDwBF;
-      const int64_t f = fb + ff;
-      Xs[rr][ff] = (x != nullptr && rr < rows && f < F) ? __ldg(x + (r0 + rr) * F + f) : 0.0f;
+  auto stage = [&](int buf, int64_t r0) {
+    // og rows r0.. (row stride H), columns hb..hb+32; x rows, columns fb..
+    stage_rows(&Os[buf][0][0], kDwBH + 4, og - 0, H, r0, kDwRows, Bn, hb, kDwBH, H, vecO);
+    if (do_dw) stage_rows(&Xs[buf][0][0], kDwBF + 4, x, F, r0, kDwRows, Bn, fb, kDwBF, F, vecX);
+    cp_async_commit();
+  };
+  // stage_rows indexes columns from c0 = hb; it expects (r0, c0) semantics
+  stage(0, 0);
+  int buf = 0;
+  for (int rc = 0; rc < nrc; ++rc, buf ^= 1) {
+    const int64_t r0 = int64_t(rc) * kDwRows;
+    if (rc + 1 < nrc) {
+      stage(buf ^ 1, r0 + kDwRows);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
     }
     __syncthreads();
-    for (int c8 = 0; c8 < rows; c8 += 8) {
-      const int64_t chunk = (r0 + c8) >> 3;
-      const int nr = rows - c8 < 8 ? rows - c8 : 8;
-      float p[T][8];
-      float q[kDwTH][8];
+    const int rows = static_cast<int>(Bn - r0 < kDwRows ? Bn - r0 : kDwRows);
+    for (int c8 = 0; c8 + 8 <= rows; c8 += 8) {
+      const int c = static_cast<int>((r0 + c8) >> 3);
+      float p[T][8], q[kDwTH][8];
 #pragma unroll
       for (int r = 0; r < 8; ++r) {
-        if (r < nr) {
 #pragma unroll
-          for (int i = 0; i < kDwTH; ++i) {
-            const float o = Os[c8 + r][th + 16 * i];
-            q[i][r] = o;
+        for (int i = 0; i < kDwTH; ++i) {
+          const float o = Os[buf][c8 + r][th + 16 * i];
+          q[i][r] = o;
 #pragma unroll
-            for (int j = 0; j < kDwTF; ++j) p[i * kDwTF + j][r] = fmul(o, Xs[c8 + r][tf + 16 * j]);
-          }
+          for (int j = 0; j < kDwTF; ++j) p[i * kDwTF + j][r] = fmul(o, Xs[buf][c8 + r][tf + 16 * j]);
         }
       }
-      if (nr == 8) {
-        float t8[T], b8[kDwTH];
+      float t8[T], b8[kDwTH];
 #pragma unroll
-        for (int o = 0; o < T; ++o) t8[o] = perfect_tree<8>(p[o]);
+      for (int o = 0; o < T; ++o) t8[o] = perfect_tree<8>(p[o]);
 #pragma unroll
-        for (int i = 0; i < kDwTH; ++i) b8[i] = perfect_tree<8>(q[i]);
-        const int c = static_cast<int>(chunk);
-        if (do_dw) tw.push(c, t8);
-        if (do_db) tb.push(c, b8);
-      } else {
-#pragma unroll
-        for (int r = 0; r < 7; ++r) {
-          if (r < nr) {
-#pragma unroll
-            for (int o = 0; o < T; ++o) tailv[r][o] = p[o][r];
-#pragma unroll
-            for (int i = 0; i < kDwTH; ++i) tailb[r][i] = q[i][r];
-          }
-        }
-      }
+      for (int i = 0; i < kDwTH; ++i) b8[i] = perfect_tree<8>(q[i]);
+      if (do_dw) tw.push(c, t8);
+      if (do_db) tb.push(c, b8);
     }
-    __syncthreads();
+    if (rc + 1 < nrc) __syncthreads();
   }
-
-  // Tail pieces by the bits of `tail` (descending sizes from the front):
-  // rows [0, 4) if bit 2, then [.., +2) if bit 1, then 1 if bit 0.  Fold
-  // smallest first: acc = T1; acc = T2 + acc; acc = T4 + acc.
+  // tail rows (Bn % 8 of them, all in the last staged chunk, buffer buf^1)
+  const int tail = static_cast<int>(Bn & 7);
+  const int lbuf = buf ^ 1;
+  const int tr0 = static_cast<int>((Bn - tail) - int64_t(nrc - 1) * kDwRows);
   float acc[T], accb[kDwTH];
   bool have = false;
+  auto prod = [&](int r, int o) {
+    const int i = o / kDwTF, j = o % kDwTF;
+    return fmul(Os[lbuf][tr0 + r][th + 16 * i], Xs[lbuf][tr0 + r][tf + 16 * j]);
+  };
+  auto ogv = [&](int r, int i) { return Os[lbuf][tr0 + r][th + 16 * i]; };
   {
-    const int o4 = 0;
     const int o2 = (tail & 4) ? 4 : 0;
     const int o1 = o2 + ((tail & 2) ? 2 : 0);
     if (tail & 1) {
 #pragma unroll
-      for (int o = 0; o < T; ++o) acc[o] = tailv[o1][o];
+      for (int o = 0; o < T; ++o) acc[o] = do_dw ? prod(o1, o) : 0.0f;
 #pragma unroll
-      for (int i = 0; i < kDwTH; ++i) accb[i] = tailb[o1][i];
+      for (int i = 0; i < kDwTH; ++i) accb[i] = ogv(o1, i);
       have = true;
     }
     if (tail & 2) {
 #pragma unroll
       for (int o = 0; o < T; ++o) {
-        const float t2 = fadd(tailv[o2][o], tailv[o2 + 1][o]);
+        const float t2 = do_dw ? fadd(prod(o2, o), prod(o2 + 1, o)) : 0.0f;
         acc[o] = have ? fadd(t2, acc[o]) : t2;
       }
 #pragma unroll
       for (int i = 0; i < kDwTH; ++i) {
-        const float t2 = fadd(tailb[o2][i], tailb[o2 + 1][i]);
+        const float t2 = fadd(ogv(o2, i), ogv(o2 + 1, i));
         accb[i] = have ? fadd(t2, accb[i]) : t2;
       }
       have = true;
@@ -445,22 +513,21 @@ fc_dw_db_kernel(const float* __restrict__ og, const float* __restrict__ x, float
     if (tail & 4) {
 #pragma unroll
       for (int o = 0; o < T; ++o) {
-        const float t4 = fadd(fadd(tailv[o4][o], tailv[o4 + 1][o]),
-                              fadd(tailv[o4 + 2][o], tailv[o4 + 3][o]));
+        const float t4 = do_dw ? fadd(fadd(prod(0, o), prod(1, o)), fadd(prod(2, o), prod(3, o)))
+                               : 0.0f;
         acc[o] = have ? fadd(t4, acc[o]) : t4;
       }
 #pragma unroll
       for (int i = 0; i < kDwTH; ++i) {
-        const float t4 = fadd(fadd(tailb[o4][i], tailb[o4 + 1][i]),
-                              fadd(tailb[o4 + 2][i], tailb[o4 + 3][i]));
+        const float t4 = fadd(fadd(ogv(0, i), ogv(1, i)), fadd(ogv(2, i), ogv(3, i)));
         accb[i] = have ? fadd(t4, accb[i]) : t4;
       }
       have = true;
     }
   }
-  const int nchi = static_cast<int>(nch);
+  const int nch = static_cast<int>(Bn >> 3);
   if (do_dw) {
-    tw.finish(nchi, have, acc);
+    tw.finish(nch, have, acc);
 #pragma unroll
     for (int i = 0; i < kDwTH; ++i) {
       const int64_t h = hb + th + 16 * i;
@@ -473,7 +540,7 @@ fc_dw_db_kernel(const float* __restrict__ og, const float* __restrict__ x, float
     }
   }
   if (do_db) {
-    tb.finish(nchi, have, accb);
+    tb.finish(nch, have, accb);
 #pragma unroll
     for (int i = 0; i < kDwTH; ++i) {
       const int64_t h = hb + th + 16 * i;
@@ -482,22 +549,43 @@ fc_dw_db_kernel(const float* __restrict__ og, const float* __restrict__ x, float
   }
 }
 
-// tree over rows for a plain column reduction: treat it as db with og=a.
 int launch_dw_db(const float* og, const float* x, float* dw, float* db, int64_t Bn, int64_t H,
                  int64_t F, cudaStream_t st) {
   const int64_t nch = Bn >> 3;
   dim3 grid(static_cast<unsigned>(dw ? ceil_div(F, kDwBF) : 1),
             static_cast<unsigned>(ceil_div(H, kDwBH)));
+  const bool vecO = (H % 4 == 0) && aligned16(og);
+  const bool vecX = dw && (F % 4 == 0) && aligned16(x);
   if (nch < (1 << 4)) {
-    fc_dw_db_kernel<4><<<grid, 256, 0, st>>>(og, x, dw, db, Bn, H, F);
+    fc_dw_db_kernel<4><<<grid, 256, 0, st>>>(og, x, dw, db, Bn, H, F, vecO, vecX);
   } else if (nch < (1 << 10)) {
-    fc_dw_db_kernel<10><<<grid, 256, 0, st>>>(og, x, dw, db, Bn, H, F);
+    fc_dw_db_kernel<10><<<grid, 256, 0, st>>>(og, x, dw, db, Bn, H, F, vecO, vecX);
   } else if (nch < (1 << 20)) {
-    fc_dw_db_kernel<20><<<grid, 256, 0, st>>>(og, x, dw, db, Bn, H, F);
+    fc_dw_db_kernel<20><<<grid, 256, 0, st>>>(og, x, dw, db, Bn, H, F, vecO, vecX);
   } else {
     set_error("batch tree: %lld rows exceed the supported 2^23", static_cast<long long>(Bn));
     return MGX_BAD_ARGUMENT;
   }
+  MGX_LAUNCHED();
+  return MGX_OK;
+}
+
+template <int TM, int TN, bool S>
+static int pw_launch(dim3 grid, size_t smem, cudaStream_t st, const float* A, int64_t lda,
+                     const float* B, int64_t ldb, const float* bias, float* C, int64_t ldc,
+                     int64_t M, int64_t N, int64_t K, const PwLeaf* leaves, int nleaves, int act,
+                     int kc, bool vecA, bool vecB) {
+  static bool configured[8] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!configured[dev & 7]) {
+    MGX_CUDA(cudaFuncSetAttribute(gemm_pairwise_kernel<TM, TN, S>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  2 * (4 * TM + 8 * TN) * (kPwMaxKc + 4) * 4));
+    configured[dev & 7] = true;
+  }
+  gemm_pairwise_kernel<TM, TN, S><<<grid, kPwThreads, smem, st>>>(
+      A, lda, B, ldb, bias, C, ldc, M, N, K, leaves, nleaves, act, kc, vecA, vecB);
   MGX_LAUNCHED();
   return MGX_OK;
 }
@@ -513,16 +601,16 @@ int launch_gemm_pairwise(const float* A, int64_t lda, const float* B, int64_t ld
     return MGX_BAD_ARGUMENT;
   }
   constexpr int TM = 2, TN = 2;
+  const int kc = static_cast<int>(K >= kPwMaxKc ? kPwMaxKc : ((K + 7) / 8) * 8);
+  const bool vecA = (lda % 4 == 0) && (K % 4 == 0) && aligned16(A);
+  const bool vecB = (ldb % 4 == 0) && (K % 4 == 0) && aligned16(B);
+  const size_t smem = size_t(2) * (4 * TM + 8 * TN) * (kc + 4) * sizeof(float);
   dim3 grid(static_cast<unsigned>(ceil_div(N, 8 * TN)), static_cast<unsigned>(ceil_div(M, 4 * TM)));
-  if (nleaves == 1) {
-    gemm_pairwise_kernel<TM, TN, false><<<grid, kPwThreads, 0, st>>>(A, lda, B, ldb, bias, C, ldc,
-                                                                     M, N, leaves, nleaves, act);
-  } else {
-    gemm_pairwise_kernel<TM, TN, true><<<grid, kPwThreads, 0, st>>>(A, lda, B, ldb, bias, C, ldc,
-                                                                    M, N, leaves, nleaves, act);
-  }
-  MGX_LAUNCHED();
-  return MGX_OK;
+  if (nleaves == 1)
+    return pw_launch<TM, TN, false>(grid, smem, st, A, lda, B, ldb, bias, C, ldc, M, N, K, leaves,
+                                    nleaves, act, kc, vecA, vecB);
+  return pw_launch<TM, TN, true>(grid, smem, st, A, lda, B, ldb, bias, C, ldc, M, N, K, leaves,
+                                 nleaves, act, kc, vecA, vecB);
 }
 
 int launch_gemm_sequential(const float* A, int64_t sam, int64_t sak, const float* B, int64_t sbk,
