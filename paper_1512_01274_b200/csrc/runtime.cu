@@ -322,20 +322,35 @@ extern "C" int mgx_prog_profile(uint64_t prog, int32_t begin, int32_t end, uintp
   }
   MGX_REQUIRE(ms_out && 0 <= begin && begin <= end && end <= static_cast<int32_t>(p->instrs.size()),
               "mgx_prog_profile: bad arguments");
+  MGX_REQUIRE(stream != 0, "mgx_prog_profile: needs a non-default stream");
+  // Capture the range with an event-record node between instructions, so
+  // the deltas are back-to-back device times, not host launch gaps.
   cudaStream_t st = as_stream(stream);
   const int n = end - begin;
   std::vector<cudaEvent_t> ev(n + 1);
   for (auto& e : ev) MGX_CUDA(cudaEventCreate(&e));
   int rc = MGX_OK;
-  MGX_CUDA(cudaEventRecord(ev[0], st));
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  MGX_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+  cudaEventRecordWithFlags(ev[0], st, cudaEventRecordExternal);
   for (int i = 0; i < n && rc == MGX_OK; ++i) {
     rc = mgx::run_instr(p->instrs[begin + i], st);
-    cudaEventRecord(ev[i + 1], st);
+    cudaEventRecordWithFlags(ev[i + 1], st, cudaEventRecordExternal);
   }
-  cudaEventSynchronize(ev[n]);
-  for (int i = 0; i < n; ++i) cudaEventElapsedTime(&ms_out[i], ev[i], ev[i + 1]);
+  cudaError_t ce = cudaStreamEndCapture(st, &graph);
+  if (rc == MGX_OK && ce == cudaSuccess) ce = cudaGraphInstantiate(&exec, graph, 0);
+  if (rc == MGX_OK && ce == cudaSuccess) {
+    for (int rep = 0; rep < 2 && ce == cudaSuccess; ++rep) ce = cudaGraphLaunch(exec, st);
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
+    for (int i = 0; i < n && ce == cudaSuccess; ++i) ce = cudaEventElapsedTime(&ms_out[i], ev[i], ev[i + 1]);
+  }
+  if (exec) cudaGraphExecDestroy(exec);
+  if (graph) cudaGraphDestroy(graph);
   for (auto& e : ev) cudaEventDestroy(e);
-  return rc;
+  if (rc != MGX_OK) return rc;
+  MGX_CUDA(ce);
+  return MGX_OK;
 }
 
 extern "C" int mgx_prog_destroy(uint64_t prog) {
