@@ -96,7 +96,10 @@ struct PwLeaf {
   int32_t pad;
 };
 // Device-resident leaf table for length K (cached per device and K).
-int pw_leaf_table(int64_t K, const PwLeaf** out, int* nleaves, int* max_depth);
+// The table holds the leaves followed by `nchunks` chunk records
+// {k0, klen, leaf_begin, leaf_end} (runs of whole leaves of <= 512 elements).
+int pw_leaf_table(int64_t K, const PwLeaf** out, int* nleaves, int* max_depth,
+                  int* nchunks = nullptr);
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 

@@ -57,8 +57,28 @@ std::vector<PwLeaf> pairwise_leaves(int64_t n) {
 static std::mutex g_leaf_mu;
 static std::unordered_map<int64_t, PwLeaf*> g_leaf_tables;
 
-int pw_leaf_table(int64_t K, const PwLeaf** out, int* nleaves, int* max_depth) {
+// Chunks of consecutive whole leaves spanning at most kPwChunk elements
+// (the pairwise GEMM stages one chunk of K in shared memory at a time).
+constexpr int kPwChunk = 512;
+
+static std::vector<PwLeaf> pairwise_chunks(const std::vector<PwLeaf>& leaves) {
+  std::vector<PwLeaf> chunks;  // {k0, klen, leaf_begin, leaf_end}
+  size_t l = 0;
+  while (l < leaves.size()) {
+    const int32_t k0 = leaves[l].start;
+    size_t e = l;
+    while (e < leaves.size() && leaves[e].start + leaves[e].len - k0 <= kPwChunk) ++e;
+    if (e == l) ++e;  // a single leaf is at most 128 elements
+    chunks.push_back(PwLeaf{k0, leaves[e - 1].start + leaves[e - 1].len - k0,
+                            static_cast<int32_t>(l), static_cast<int32_t>(e)});
+    l = e;
+  }
+  return chunks;
+}
+
+int pw_leaf_table(int64_t K, const PwLeaf** out, int* nleaves, int* max_depth, int* nchunks) {
   auto leaves = pairwise_leaves(K);
+  auto chunks = pairwise_chunks(leaves);
   int depth = 0, cur = 0;
   for (auto& l : leaves) {
     ++cur;
@@ -67,6 +87,7 @@ int pw_leaf_table(int64_t K, const PwLeaf** out, int* nleaves, int* max_depth) {
   }
   *nleaves = static_cast<int>(leaves.size());
   *max_depth = depth;
+  if (nchunks) *nchunks = static_cast<int>(chunks.size());
   int dev = 0;
   MGX_CUDA(cudaGetDevice(&dev));
   int64_t key = (static_cast<int64_t>(dev) << 48) | K;
@@ -76,11 +97,13 @@ int pw_leaf_table(int64_t K, const PwLeaf** out, int* nleaves, int* max_depth) {
     *out = it->second;
     return MGX_OK;
   }
+  std::vector<PwLeaf> table(leaves);
+  table.insert(table.end(), chunks.begin(), chunks.end());
   PwLeaf* d = nullptr;
-  size_t bytes = leaves.size() * sizeof(PwLeaf);
+  size_t bytes = table.size() * sizeof(PwLeaf);
   MGX_CUDA(cudaMalloc(&d, bytes > 0 ? bytes : sizeof(PwLeaf)));
   // Plain synchronous copy: done once per (device, K), before any capture.
-  MGX_CUDA(cudaMemcpy(d, leaves.data(), bytes, cudaMemcpyHostToDevice));
+  MGX_CUDA(cudaMemcpy(d, table.data(), bytes, cudaMemcpyHostToDevice));
   g_leaf_tables[key] = d;
   *out = d;
   return MGX_OK;
@@ -115,145 +138,134 @@ __device__ __forceinline__ void stage_rows(float* S, int kcp, const float* G, in
 // ----------------------------------------------------- pairwise GEMM kernel
 // Block tile (4*TM) x (8*TN) outputs; 32 groups of 8 lanes, group (gm, gn)
 // owns a TM x TN micro-tile and lane j of the group is numpy's accumulator
-// r[j].  K is streamed through shared memory in chunks of kc (a multiple of
-// 8), double-buffered with cp.async; the leaf walk is a state machine over
-// 8-element blocks so leaves may straddle chunks.
+// r[j].  K is staged through shared memory one chunk of whole leaves at a
+// time (<= 512 elements, cp.async, double-buffered).  Per leaf the 8-block
+// loop is branch-free; leaf results merge on a D-deep stack held in
+// registers (predicated updates, no local memory) per the split tree.
 
 constexpr int kPwThreads = 256;
 constexpr int kPwMaxDepth = 24;
-constexpr int kPwMaxKc = 512;
 
-template <int TM, int TN, bool kStack>
+template <int D, int T>
+struct LeafStack {
+  // shift register: v[0] is the top; every index is static, so the stack
+  // lives in registers
+  float v[D][T];
+  __device__ __forceinline__ void push(const float (&x)[T]) {
+#pragma unroll
+    for (int d = D - 1; d > 0; --d)
+#pragma unroll
+      for (int o = 0; o < T; ++o) v[d][o] = v[d - 1][o];
+#pragma unroll
+    for (int o = 0; o < T; ++o) v[0][o] = x[o];
+  }
+  __device__ __forceinline__ void merge() {  // (second + top), popped into one entry
+#pragma unroll
+    for (int o = 0; o < T; ++o) v[0][o] = fadd(v[1][o], v[0][o]);
+#pragma unroll
+    for (int d = 1; d + 1 < D; ++d)
+#pragma unroll
+      for (int o = 0; o < T; ++o) v[d][o] = v[d + 1][o];
+  }
+};
+
+template <int TM, int TN, int D>
 __global__ void __launch_bounds__(kPwThreads)
-gemm_pairwise_kernel(const float* __restrict__ A, int64_t lda, const float* __restrict__ B,
-                     int64_t ldb, const float* __restrict__ bias, float* __restrict__ C,
-                     int64_t ldc, int64_t M, int64_t N, int64_t K,
-                     const PwLeaf* __restrict__ leaves, int nleaves, int act, int kc,
-                     bool vecA, bool vecB) {
+gemm_pairwise_kernel(const float* __restrict__ A, int lda, const float* __restrict__ B, int ldb,
+                     const float* __restrict__ bias, float* __restrict__ C, int ldc, int M, int N,
+                     int K, const PwLeaf* __restrict__ leaves, int nleaves, int nchunks, int act,
+                     int kc, bool vecA, bool vecB) {
   extern __shared__ float4 smem_f4[];
   float* smem = reinterpret_cast<float*>(smem_f4);
-  constexpr int BM = 4 * TM, BN = 8 * TN;
+  constexpr int BM = 4 * TM, BN = 8 * TN, T = TM * TN;
   const int kcp = kc + 4;
-  float* As[2] = {smem, smem + (BM + BN) * kcp};
-  float* Bs[2] = {As[0] + BM * kcp, As[1] + BM * kcp};
+  // stage s: A rows at smem + s*(BM+BN)*kcp, B rows right after them
+  const int stage_floats = (BM + BN) * kcp;
+  const PwLeaf* chunks = leaves + nleaves;
 
   const int lane8 = threadIdx.x & 7;
   const int group = threadIdx.x >> 3;
   const int gm = group >> 3, gn = group & 7;
-  const int64_t mb = int64_t(blockIdx.y) * BM, nb = int64_t(blockIdx.x) * BN;
-  const int nchunks = static_cast<int>((K + kc - 1) / kc);
-  const int64_t nblocks = (K + 7) >> 3;
+  const int mb = blockIdx.y * BM, nb = blockIdx.x * BN;
 
-  stage_rows(As[0], kcp, A, lda, mb, BM, M, 0, kc, K, vecA);
-  stage_rows(Bs[0], kcp, B, ldb, nb, BN, N, 0, kc, K, vecB);
-  cp_async_commit();
-
-  int leaf = 0;
-  PwLeaf lf = leaves[0];
-  int64_t lb0 = lf.start >> 3;
-  int lnb = lf.len >> 3, ltail = lf.len & 7;
-  int last_rel = ltail ? lnb : lnb - 1;
-
-  float acc[TM][TN], res[TM][TN];
-  float stk[kStack ? kPwMaxDepth : 1][TM][TN];
-  int sp = 0;
+  {
+    const PwLeaf c0 = chunks[0];
+    stage_rows(smem, kcp, A, lda, mb, BM, M, c0.start, c0.len, K, vecA);
+    stage_rows(smem + BM * kcp, kcp, B, ldb, nb, BN, N, c0.start, c0.len, K, vecB);
+    cp_async_commit();
+  }
+  LeafStack<D, T> stk;
+  float res[T];
 
   for (int c = 0; c < nchunks; ++c) {
+    const PwLeaf ch = chunks[c];
     if (c + 1 < nchunks) {
-      const int64_t c0 = int64_t(c + 1) * kc;
-      stage_rows(As[(c + 1) & 1], kcp, A, lda, mb, BM, M, c0, kc, K, vecA);
-      stage_rows(Bs[(c + 1) & 1], kcp, B, ldb, nb, BN, N, c0, kc, K, vecB);
+      const PwLeaf cn = chunks[c + 1];
+      float* nxt = smem + ((c + 1) & 1) * stage_floats;
+      stage_rows(nxt, kcp, A, lda, mb, BM, M, cn.start, cn.len, K, vecA);
+      stage_rows(nxt + BM * kcp, kcp, B, ldb, nb, BN, N, cn.start, cn.len, K, vecB);
       cp_async_commit();
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
     }
     __syncthreads();
-    const float* a_s = As[c & 1] + gm * TM * kcp;
-    const float* b_s = Bs[c & 1] + gn * TN * kcp;
-    const int64_t jb0 = int64_t(c) * (kc >> 3);
-    const int64_t jb1 = jb0 + (kc >> 3) < nblocks ? jb0 + (kc >> 3) : nblocks;
-    for (int64_t jb = jb0; jb < jb1; ++jb) {
-      const int kk = static_cast<int>(jb - jb0) << 3;
-      const int rel = static_cast<int>(jb - lb0);
-      if (rel < lnb) {
-        float a[TM], b[TN];
+    const float* cur = smem + (c & 1) * stage_floats;
+    const float* a_s = cur + gm * TM * kcp;
+    const float* b_s = cur + BM * kcp + gn * TN * kcp;
+    for (int l = ch.merges; l < ch.pad; ++l) {  // leaves [leaf_begin, leaf_end)
+      const PwLeaf lf = leaves[l];
+      const int base = lf.start - ch.start;
+      const int nblk = lf.len >> 3, tail = lf.len & 7;
+      float acc[T];
+      if (nblk > 0) {
+        const float* ap = a_s + base + lane8;
+        const float* bp = b_s + base + lane8;
 #pragma unroll
-        for (int i = 0; i < TM; ++i) a[i] = a_s[i * kcp + kk + lane8];
+        for (int i = 0; i < TM; ++i)
 #pragma unroll
-        for (int j = 0; j < TN; ++j) b[j] = b_s[j * kcp + kk + lane8];
-        if (rel == 0) {
+          for (int j = 0; j < TN; ++j) acc[i * TN + j] = fmul(ap[i * kcp], bp[j * kcp]);
+#pragma unroll 4
+        for (int q = 1; q < nblk; ++q) {
+          float a[TM], b[TN];
+#pragma unroll
+          for (int i = 0; i < TM; ++i) a[i] = ap[i * kcp + 8 * q];
+#pragma unroll
+          for (int j = 0; j < TN; ++j) b[j] = bp[j * kcp + 8 * q];
 #pragma unroll
           for (int i = 0; i < TM; ++i)
 #pragma unroll
-            for (int j = 0; j < TN; ++j) acc[i][j] = fmul(a[i], b[j]);
-        } else {
-#pragma unroll
-          for (int i = 0; i < TM; ++i)
-#pragma unroll
-            for (int j = 0; j < TN; ++j) acc[i][j] = fadd(acc[i][j], fmul(a[i], b[j]));
+            for (int j = 0; j < TN; ++j) acc[i * TN + j] = fadd(acc[i * TN + j], fmul(a[i], b[j]));
         }
-        if (rel == lnb - 1) {
 #pragma unroll
-          for (int mask = 1; mask < 8; mask <<= 1)
+        for (int mask = 1; mask < 8; mask <<= 1)
 #pragma unroll
-            for (int i = 0; i < TM; ++i)
-#pragma unroll
-              for (int j = 0; j < TN; ++j)
-                acc[i][j] = fadd(acc[i][j], __shfl_xor_sync(0xffffffffu, acc[i][j], mask));
-#pragma unroll
-          for (int i = 0; i < TM; ++i)
-#pragma unroll
-            for (int j = 0; j < TN; ++j) res[i][j] = acc[i][j];
-        }
+          for (int o = 0; o < T; ++o) acc[o] = fadd(acc[o], __shfl_xor_sync(0xffffffffu, acc[o], mask));
       } else {
-        // tail block of the leaf: elements added in order (n < 8 starts at +0)
-        if (lnb == 0) {
 #pragma unroll
-          for (int i = 0; i < TM; ++i)
-#pragma unroll
-            for (int j = 0; j < TN; ++j) res[i][j] = 0.0f;
-        }
-        for (int t = 0; t < ltail; ++t) {
-#pragma unroll
-          for (int i = 0; i < TM; ++i) {
-            const float a = a_s[i * kcp + kk + t];
-#pragma unroll
-            for (int j = 0; j < TN; ++j) res[i][j] = fadd(res[i][j], fmul(a, b_s[j * kcp + kk + t]));
-          }
-        }
+        for (int o = 0; o < T; ++o) acc[o] = 0.0f;  // n < 8: res = 0. then +=
       }
-      if (rel == last_rel) {
-        if constexpr (kStack) {
+      for (int t = 0; t < tail; ++t) {
+        const int k = base + 8 * nblk + t;
 #pragma unroll
-          for (int i = 0; i < TM; ++i)
+        for (int i = 0; i < TM; ++i)
 #pragma unroll
-            for (int j = 0; j < TN; ++j) stk[sp][i][j] = res[i][j];
-          ++sp;
-          for (int q = 0; q < lf.merges; ++q) {
-            --sp;
+          for (int j = 0; j < TN; ++j)
+            acc[i * TN + j] = fadd(acc[i * TN + j], fmul(a_s[i * kcp + k], b_s[j * kcp + k]));
+      }
+      if constexpr (D == 1) {
 #pragma unroll
-            for (int i = 0; i < TM; ++i)
-#pragma unroll
-              for (int j = 0; j < TN; ++j) stk[sp - 1][i][j] = fadd(stk[sp - 1][i][j], stk[sp][i][j]);
-          }
-        }
-        if (++leaf < nleaves) {
-          lf = leaves[leaf];
-          lb0 = lf.start >> 3;
-          lnb = lf.len >> 3;
-          ltail = lf.len & 7;
-          last_rel = ltail ? lnb : lnb - 1;
-        }
+        for (int o = 0; o < T; ++o) res[o] = acc[o];
+      } else {
+        stk.push(acc);
+        for (int q = 0; q < lf.merges; ++q) stk.merge();
       }
     }
     __syncthreads();
   }
-  if constexpr (kStack) {
+  if constexpr (D > 1) {
 #pragma unroll
-    for (int i = 0; i < TM; ++i)
-#pragma unroll
-      for (int j = 0; j < TN; ++j) res[i][j] = stk[0][i][j];
+    for (int o = 0; o < T; ++o) res[o] = stk.v[0][o];
   }
   // lane j of the group stores outputs (i*TN + j) % 8 == j: bias added
   // separately (np.add(res, b), ops.py:106), then the activation
@@ -262,11 +274,11 @@ gemm_pairwise_kernel(const float* __restrict__ A, int64_t lda, const float* __re
 #pragma unroll
     for (int j = 0; j < TN; ++j) {
       if ((i * TN + j) % 8 != lane8) continue;
-      const int64_t m = mb + gm * TM + i, n = nb + gn * TN + j;
+      const int m = mb + gm * TM + i, n = nb + gn * TN + j;
       if (m >= M || n >= N) continue;
-      float v = res[i][j];
+      float v = res[i * TN + j];
       if (bias) v = fadd(v, __ldg(bias + n));
-      C[m * ldc + n] = act_forward(act, v);
+      C[int64_t(m) * ldc + n] = act_forward(act, v);
     }
   }
 }
@@ -570,22 +582,24 @@ int launch_dw_db(const float* og, const float* x, float* dw, float* db, int64_t 
   return MGX_OK;
 }
 
-template <int TM, int TN, bool S>
+template <int TM, int TN, int D>
 static int pw_launch(dim3 grid, size_t smem, cudaStream_t st, const float* A, int64_t lda,
                      const float* B, int64_t ldb, const float* bias, float* C, int64_t ldc,
-                     int64_t M, int64_t N, int64_t K, const PwLeaf* leaves, int nleaves, int act,
-                     int kc, bool vecA, bool vecB) {
+                     int64_t M, int64_t N, int64_t K, const PwLeaf* leaves, int nleaves,
+                     int nchunks, int act, int kc, bool vecA, bool vecB) {
   static bool configured[8] = {false};
   int dev = 0;
   cudaGetDevice(&dev);
   if (!configured[dev & 7]) {
-    MGX_CUDA(cudaFuncSetAttribute(gemm_pairwise_kernel<TM, TN, S>,
+    MGX_CUDA(cudaFuncSetAttribute(gemm_pairwise_kernel<TM, TN, D>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  2 * (4 * TM + 8 * TN) * (kPwMaxKc + 4) * 4));
+                                  2 * (4 * TM + 8 * TN) * (kPwChunk + 4) * 4));
     configured[dev & 7] = true;
   }
-  gemm_pairwise_kernel<TM, TN, S><<<grid, kPwThreads, smem, st>>>(
-      A, lda, B, ldb, bias, C, ldc, M, N, K, leaves, nleaves, act, kc, vecA, vecB);
+  gemm_pairwise_kernel<TM, TN, D><<<grid, kPwThreads, smem, st>>>(
+      A, static_cast<int>(lda), B, static_cast<int>(ldb), bias, C, static_cast<int>(ldc),
+      static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), leaves, nleaves, nchunks,
+      act, kc, vecA, vecB);
   MGX_LAUNCHED();
   return MGX_OK;
 }
@@ -594,23 +608,27 @@ int launch_gemm_pairwise(const float* A, int64_t lda, const float* B, int64_t ld
                          const float* bias, float* C, int64_t ldc, int64_t M, int64_t N,
                          int64_t K, int act, cudaStream_t st) {
   const PwLeaf* leaves = nullptr;
-  int nleaves = 0, depth = 0;
-  MGX_TRY(pw_leaf_table(K, &leaves, &nleaves, &depth));
-  if (depth > kPwMaxDepth) {
-    set_error("pairwise GEMM: K=%lld too deep", static_cast<long long>(K));
-    return MGX_BAD_ARGUMENT;
-  }
+  int nleaves = 0, depth = 0, nchunks = 0;
+  MGX_TRY(pw_leaf_table(K, &leaves, &nleaves, &depth, &nchunks));
+  MGX_REQUIRE(M < (int64_t(1) << 31) && N < (int64_t(1) << 31) && K < (int64_t(1) << 31) &&
+                  lda < (int64_t(1) << 31) && ldb < (int64_t(1) << 31) && ldc < (int64_t(1) << 31),
+              "pairwise GEMM: dimensions exceed 2^31");
   constexpr int TM = 2, TN = 2;
-  const int kc = static_cast<int>(K >= kPwMaxKc ? kPwMaxKc : ((K + 7) / 8) * 8);
+  const int kc = static_cast<int>(K >= kPwChunk ? kPwChunk : ((K + 7) / 8) * 8);
   const bool vecA = (lda % 4 == 0) && (K % 4 == 0) && aligned16(A);
   const bool vecB = (ldb % 4 == 0) && (K % 4 == 0) && aligned16(B);
   const size_t smem = size_t(2) * (4 * TM + 8 * TN) * (kc + 4) * sizeof(float);
   dim3 grid(static_cast<unsigned>(ceil_div(N, 8 * TN)), static_cast<unsigned>(ceil_div(M, 4 * TM)));
-  if (nleaves == 1)
-    return pw_launch<TM, TN, false>(grid, smem, st, A, lda, B, ldb, bias, C, ldc, M, N, K, leaves,
-                                    nleaves, act, kc, vecA, vecB);
-  return pw_launch<TM, TN, true>(grid, smem, st, A, lda, B, ldb, bias, C, ldc, M, N, K, leaves,
-                                 nleaves, act, kc, vecA, vecB);
+#define MGX_PW(Dd) \
+  return pw_launch<TM, TN, Dd>(grid, smem, st, A, lda, B, ldb, bias, C, ldc, M, N, K, leaves, \
+                               nleaves, nchunks, act, kc, vecA, vecB)
+  if (depth <= 1) MGX_PW(1);
+  if (depth <= 6) MGX_PW(6);
+  if (depth <= 12) MGX_PW(12);
+  if (depth <= kPwMaxDepth) MGX_PW(kPwMaxDepth);
+#undef MGX_PW
+  set_error("pairwise GEMM: K=%lld too deep", static_cast<long long>(K));
+  return MGX_BAD_ARGUMENT;
 }
 
 int launch_gemm_sequential(const float* A, int64_t sam, int64_t sak, const float* B, int64_t sbk,
