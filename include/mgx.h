@@ -117,6 +117,17 @@ int mgx_act_backward(int act, const float* y, const float* og, float* g, int64_t
 int mgx_softmax_forward(const float* x, float* p, int64_t B, int64_t C, uintptr_t stream);
 int mgx_softmax_backward(const float* p, const float* label, float* g, int64_t B, int64_t C, uintptr_t stream);
 
+/* Tensor-core dense path (tolerance, not exact order): C[M,N] fp32 =
+ * A[M,K] . B[N,K]^T (+bias) then act, A/B bf16 K-major ("TN"), fp32
+ * accumulation in TMEM via tcgen05.mma, operands by TMA.  Replaces the
+ * reference's FC forward contraction (ops.py:102-106) for the large FC
+ * layers of configs 3-5.  K, lda, ldb multiples of 8; 16-byte aligned. */
+int mgx_gemm_bf16_tc(const void* A, int64_t lda, const void* B, int64_t ldb,
+                     const float* bias, float* C, int64_t ldc,
+                     int64_t M, int64_t N, int64_t K, int act, uintptr_t stream);
+/* y(bf16) = round-to-nearest-even(x(fp32)) */
+int mgx_cast_f32_bf16(const float* x, void* y, int64_t n, uintptr_t stream);
+
 /* Momentum SGD, tensor path (optim.py:39-50): 5 separately rounded steps. */
 int mgx_sgd_step(float* w, const float* g, float* v, int64_t n,
                  float eta, float momentum, float weight_decay, uintptr_t stream);

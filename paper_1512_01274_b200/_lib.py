@@ -106,6 +106,9 @@ _SIGNATURES = {
     "mgx_act_backward": ([ctypes.c_int, c_vp, c_vp, c_vp, c_i64, c_uptr], ctypes.c_int),
     "mgx_softmax_forward": ([c_vp, c_vp, c_i64, c_i64, c_uptr], ctypes.c_int),
     "mgx_softmax_backward": ([c_vp, c_vp, c_vp, c_i64, c_i64, c_uptr], ctypes.c_int),
+    "mgx_gemm_bf16_tc": ([c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64,
+                          ctypes.c_int, c_uptr], ctypes.c_int),
+    "mgx_cast_f32_bf16": ([c_vp, c_vp, c_i64, c_uptr], ctypes.c_int),
     "mgx_sgd_step": ([c_vp, c_vp, c_vp, c_i64, c_f32, c_f32, c_f32, c_uptr], ctypes.c_int),
     "mgx_plan_memory": ([c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32,
                          c_vp, c_vp, c_vp, ctypes.POINTER(c_i32), c_vp, c_i32,
