@@ -182,9 +182,15 @@ typedef struct mgx_instr {
 /* Run instructions eagerly, in order, on stream (no program object). */
 int mgx_instr_run(const mgx_instr* instrs, int32_t count, uintptr_t stream);
 int mgx_prog_create(const mgx_instr* instrs, int32_t count, uint64_t* out);
-/* Launch instructions [begin, end) on stream.  use_graph=1 captures the range
- * once into a CUDA graph and replays it on later calls. */
-int mgx_prog_run(uint64_t prog, int32_t begin, int32_t end, uintptr_t stream, int32_t use_graph);
+/* Launch instructions [begin, end) on stream.  mode 0: one kernel per
+ * instruction; 1: those kernels captured once into a CUDA graph and
+ * replayed; 2: ONE cooperative program kernel that runs the range as
+ * dependency levels separated by grid barriers; 3: mode 2 inside a graph. */
+int mgx_prog_run(uint64_t prog, int32_t begin, int32_t end, uintptr_t stream, int32_t mode);
+/* Dependency levels the program kernel uses for [begin, end): level count,
+ * grid size, and (optional, capacity end-begin) the level of each instruction. */
+int mgx_prog_levels(uint64_t prog, int32_t begin, int32_t end, int32_t* nlevels,
+                    int32_t* grid, int32_t* level_of);
 /* Per-instruction device time of one eager run of [begin,end) (profiling). */
 int mgx_prog_profile(uint64_t prog, int32_t begin, int32_t end, uintptr_t stream, float* ms_out);
 int mgx_prog_destroy(uint64_t prog);

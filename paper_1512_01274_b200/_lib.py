@@ -118,6 +118,8 @@ _SIGNATURES = {
     "mgx_instr_run": ([ctypes.POINTER(Instr), c_i32, c_uptr], ctypes.c_int),
     "mgx_prog_create": ([ctypes.POINTER(Instr), c_i32, ctypes.POINTER(c_u64)], ctypes.c_int),
     "mgx_prog_run": ([c_u64, c_i32, c_i32, c_uptr, c_i32], ctypes.c_int),
+    "mgx_prog_levels": ([c_u64, c_i32, c_i32, ctypes.POINTER(c_i32), ctypes.POINTER(c_i32),
+                         c_vp], ctypes.c_int),
     "mgx_prog_profile": ([c_u64, c_i32, c_i32, c_uptr, ctypes.POINTER(c_f32)], ctypes.c_int),
     "mgx_prog_destroy": ([c_u64], ctypes.c_int),
     "mgx_kv_round": ([ctypes.POINTER(KvRoundArgs), c_uptr], ctypes.c_int),

@@ -1,0 +1,27 @@
+// Fused (single-launch) execution of a program range; see megakernel.cu.
+#pragma once
+
+#include <vector>
+
+#include "common.cuh"
+
+namespace mgx {
+
+struct MegaOp;
+struct MegaLevel;
+
+struct FusedRange {
+  MegaOp* d_ops = nullptr;
+  MegaLevel* d_levels = nullptr;
+  uint32_t* d_barrier = nullptr;
+  int nlevels = 0;
+  int grid = 0;
+  size_t smem = 0;
+  std::vector<int> level_of;  // diagnostics
+};
+
+int build_fused(const mgx_instr* instrs, int n, FusedRange* out);
+int launch_fused(const FusedRange& f, cudaStream_t st);
+void free_fused(FusedRange& f);
+
+}  // namespace mgx

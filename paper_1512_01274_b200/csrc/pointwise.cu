@@ -5,7 +5,7 @@
 // fp32 op in the reference's order (tensor.py:169-231, ops.py:138-207,
 // optim.py:39-50).
 
-#include "common.cuh"
+#include "tiles.cuh"
 
 namespace mgx {
 
@@ -52,125 +52,6 @@ int launch_map(int64_t n, bool vec_ok, F f, cudaStream_t st) {
   return MGX_OK;
 }
 
-struct FillOp {
-  float* y;
-  float v;
-  __device__ void vec(int64_t i) const { reinterpret_cast<float4*>(y)[i] = make_float4(v, v, v, v); }
-  __device__ void scalar(int64_t i) const { y[i] = v; }
-};
-
-struct CopyOp {
-  const float* x;
-  float* y;
-  __device__ void vec(int64_t i) const {
-    reinterpret_cast<float4*>(y)[i] = __ldg(reinterpret_cast<const float4*>(x) + i);
-  }
-  __device__ void scalar(int64_t i) const { y[i] = x[i]; }
-};
-
-// y = y + x*alpha (kernels.py:50-53)
-struct AxpyOp {
-  const float* x;
-  float* y;
-  float alpha;
-  __device__ float f(float xv, float yv) const { return fadd(yv, fmul(xv, alpha)); }
-  __device__ void vec(int64_t i) const {
-    const float4 a = reinterpret_cast<const float4*>(x)[i];
-    float4 b = reinterpret_cast<float4*>(y)[i];
-    b = make_float4(f(a.x, b.x), f(a.y, b.y), f(a.z, b.z), f(a.w, b.w));
-    reinterpret_cast<float4*>(y)[i] = b;
-  }
-  __device__ void scalar(int64_t i) const { y[i] = f(x[i], y[i]); }
-};
-
-struct EwOp {
-  const float* a;
-  const float* b;
-  float* out;
-  int op;
-  __device__ float f(float x, float z) const {
-    switch (op) {
-      case 0: return fadd(x, z);
-      case 1: return fsub(x, z);
-      case 2: return fmul(x, z);
-      default: return fdiv(x, z);
-    }
-  }
-  __device__ void vec(int64_t i) const {
-    const float4 x = reinterpret_cast<const float4*>(a)[i];
-    const float4 z = reinterpret_cast<const float4*>(b)[i];
-    reinterpret_cast<float4*>(out)[i] = make_float4(f(x.x, z.x), f(x.y, z.y), f(x.z, z.z), f(x.w, z.w));
-  }
-  __device__ void scalar(int64_t i) const { out[i] = f(a[i], b[i]); }
-};
-
-struct ScalarOp {
-  const float* a;
-  float* out;
-  float c;
-  int op;
-  __device__ float f(float x) const { return op == 0 ? fadd(x, c) : fmul(x, c); }
-  __device__ void vec(int64_t i) const {
-    const float4 x = reinterpret_cast<const float4*>(a)[i];
-    reinterpret_cast<float4*>(out)[i] = make_float4(f(x.x), f(x.y), f(x.z), f(x.w));
-  }
-  __device__ void scalar(int64_t i) const { out[i] = f(a[i]); }
-};
-
-struct ActFwdOp {
-  const float* x;
-  float* y;
-  int act;
-  __device__ void vec(int64_t i) const {
-    const float4 v = reinterpret_cast<const float4*>(x)[i];
-    reinterpret_cast<float4*>(y)[i] = make_float4(act_forward(act, v.x), act_forward(act, v.y),
-                                                  act_forward(act, v.z), act_forward(act, v.w));
-  }
-  __device__ void scalar(int64_t i) const { y[i] = act_forward(act, x[i]); }
-};
-
-struct ActBwdOp {
-  const float* y;
-  const float* og;
-  float* g;
-  int act;
-  __device__ void vec(int64_t i) const {
-    const float4 a = reinterpret_cast<const float4*>(y)[i];
-    const float4 o = reinterpret_cast<const float4*>(og)[i];
-    reinterpret_cast<float4*>(g)[i] =
-        make_float4(act_backward(act, a.x, o.x), act_backward(act, a.y, o.y),
-                    act_backward(act, a.z, o.z), act_backward(act, a.w, o.w));
-  }
-  __device__ void scalar(int64_t i) const { g[i] = act_backward(act, y[i], og[i]); }
-};
-
-// Momentum SGD tensor path (optim.py:39-50):
-//   tmp = g; tmp = tmp + w*wd; v = v*mom; v = v + tmp*(-eta); w = w + v*1
-struct SgdOp {
-  float* w;
-  const float* g;
-  float* v;
-  float neg_eta, mom, wd;
-  __device__ void step(float& wv, float gv, float& vv) const {
-    const float tmp = fadd(gv, fmul(wv, wd));
-    vv = fmul(vv, mom);
-    vv = fadd(vv, fmul(tmp, neg_eta));
-    wv = fadd(wv, fmul(vv, 1.0f));
-  }
-  __device__ void vec(int64_t i) const {
-    float4 a = reinterpret_cast<float4*>(w)[i];
-    const float4 b = reinterpret_cast<const float4*>(g)[i];
-    float4 c = reinterpret_cast<float4*>(v)[i];
-    step(a.x, b.x, c.x);
-    step(a.y, b.y, c.y);
-    step(a.z, b.z, c.z);
-    step(a.w, b.w, c.w);
-    reinterpret_cast<float4*>(w)[i] = a;
-    reinterpret_cast<float4*>(v)[i] = c;
-  }
-  __device__ void scalar(int64_t i) const { step(w[i], g[i], v[i]); }
-};
-
 // --------------------------------------------------------------- softmax
 // One group of 8 lanes per row.  shifted = x - rowmax; e = exp(shifted);
 // p = e / pairwise_sum(e) (kernels.py:68-76).  The row sum follows numpy's
@@ -179,78 +60,10 @@ struct SgdOp {
 // 8 lanes, the tail is added in order, and leaves are merged per the split
 // tree (for C <= 128 there is exactly one leaf).
 
-__device__ __forceinline__ float max_nan(float a, float b) {
-  if (a != a) return a;
-  if (b != b) return b;
-  return a > b ? a : b;
-}
-
 __global__ void __launch_bounds__(256)
 softmax_fwd_kernel(const float* __restrict__ x, float* __restrict__ p, int64_t Bn, int64_t C,
                    const PwLeaf* __restrict__ leaves, int nleaves) {
-  const int lane8 = threadIdx.x & 7;
-  const int64_t row = int64_t(blockIdx.x) * 32 + (threadIdx.x >> 3);
-  const bool live = row < Bn;
-  const float* xr = x + (live ? row : 0) * C;
-  float* pr = p + (live ? row : 0) * C;
-
-  float mx = -INFINITY;
-  for (int64_t c = lane8; c < C; c += 8) mx = max_nan(mx, xr[c]);
-#pragma unroll
-  for (int mask = 1; mask < 8; mask <<= 1) mx = max_nan(mx, __shfl_xor_sync(0xffffffffu, mx, mask));
-  if (live)
-    for (int64_t c = lane8; c < C; c += 8) pr[c] = exp_rn(fsub(xr[c], mx));
-  __syncwarp();
-
-  float stk[32];
-  int sp = 0;
-  float res = 0.0f;
-  for (int l = 0; l < nleaves; ++l) {
-    const PwLeaf lf = leaves[l];
-    const int nb = lf.len >> 3, tail = lf.len & 7;
-    float acc;
-    if (nb > 0) {
-      int64_t c = lf.start + lane8;
-      acc = live ? pr[c] : 0.0f;
-      for (int bb = 1; bb < nb; ++bb) {
-        c += 8;
-        acc = fadd(acc, live ? pr[c] : 0.0f);
-      }
-#pragma unroll
-      for (int mask = 1; mask < 8; mask <<= 1) acc = fadd(acc, __shfl_xor_sync(0xffffffffu, acc, mask));
-    } else {
-      acc = 0.0f;
-    }
-    for (int t = 0; t < tail; ++t) acc = fadd(acc, live ? pr[lf.start + 8 * nb + t] : 0.0f);
-    if (nleaves == 1) {
-      res = acc;
-    } else {
-      stk[sp++] = acc;
-      for (int q = 0; q < lf.merges; ++q) {
-        --sp;
-        stk[sp - 1] = fadd(stk[sp - 1], stk[sp]);
-      }
-    }
-  }
-  if (nleaves > 1) res = stk[0];
-  __syncwarp();
-  if (live)
-    for (int64_t c = lane8; c < C; c += 8) pr[c] = fdiv(pr[c], res);
-}
-
-// grad = (p - onehot(int64(label))) / f32(B)   (ops.py:188-196)
-__global__ void softmax_bwd_kernel(const float* __restrict__ p, const float* __restrict__ label,
-                                   float* __restrict__ g, int64_t Bn, int64_t C) {
-  const int64_t n = Bn * C;
-  const float denom = static_cast<float>(Bn);
-  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const int64_t b = i / C, c = i % C;
-    int64_t cls = static_cast<int64_t>(label[b]);  // astype(int64): truncation
-    if (cls < 0) cls += C;                         // numpy negative indexing
-    const float hot = (c == cls) ? 1.0f : 0.0f;
-    g[i] = fdiv(fsub(p[i], hot), denom);
-  }
+  softmax_fwd_tile(blockIdx.x, x, p, Bn, C, leaves, nleaves);
 }
 
 }  // namespace
@@ -329,10 +142,8 @@ extern "C" int mgx_softmax_forward(const float* x, float* p, int64_t B, int64_t 
 extern "C" int mgx_softmax_backward(const float* p, const float* label, float* g, int64_t B,
                                     int64_t C, uintptr_t stream) {
   MGX_REQUIRE(p && label && g && B > 0 && C > 0, "mgx_softmax_backward: bad arguments");
-  const unsigned blocks = static_cast<unsigned>(mgx::ceil_div(B * C, 256) < 1184 ? mgx::ceil_div(B * C, 256) : 1184);
-  mgx::softmax_bwd_kernel<<<blocks, 256, 0, as_stream(stream)>>>(p, label, g, B, C);
-  MGX_LAUNCHED();
-  return MGX_OK;
+  return mgx::launch_map(B * C, false, mgx::SoftmaxBwdOp{p, label, g, C, static_cast<float>(B)},
+                         as_stream(stream));
 }
 
 extern "C" int mgx_sgd_step(float* w, const float* g, float* v, int64_t n, float eta,

@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "fused.cuh"
 
 namespace mgx {
 
@@ -188,9 +189,27 @@ namespace mgx {
 
 struct Program {
   std::vector<mgx_instr> instrs;
-  std::map<std::pair<int32_t, int32_t>, cudaGraphExec_t> graphs;
+  std::map<std::pair<int32_t, int32_t>, cudaGraphExec_t> graphs;   // mode 1
+  std::map<std::pair<int32_t, int32_t>, cudaGraphExec_t> fgraphs;  // mode 3
+  std::map<std::pair<int32_t, int32_t>, FusedRange> fused;         // modes 2, 3
   std::mutex mu;
 };
+
+static int get_fused(Program* p, int32_t begin, int32_t end, FusedRange** out) {
+  auto key = std::make_pair(begin, end);
+  auto it = p->fused.find(key);
+  if (it == p->fused.end()) {
+    FusedRange f;
+    int rc = build_fused(p->instrs.data() + begin, end - begin, &f);
+    if (rc != MGX_OK) {
+      free_fused(f);
+      return rc;
+    }
+    it = p->fused.emplace(key, f).first;
+  }
+  *out = &it->second;
+  return MGX_OK;
+}
 
 static std::mutex g_prog_mu;
 static std::map<uint64_t, Program*> g_progs;
@@ -278,7 +297,9 @@ extern "C" int mgx_prog_create(const mgx_instr* instrs, int32_t count, uint64_t*
 }
 
 extern "C" int mgx_prog_run(uint64_t prog, int32_t begin, int32_t end, uintptr_t stream,
-                            int32_t use_graph) {
+                            int32_t mode) {
+  // mode 0: eager launches; 1: captured CUDA graph of the per-instruction
+  // kernels; 2: one cooperative program kernel; 3: that kernel in a graph
   mgx::Program* p = mgx::find_prog(prog);
   if (!p) {
     mgx::set_error("mgx_prog_run: unknown program handle %llu", (unsigned long long)prog);
@@ -286,17 +307,25 @@ extern "C" int mgx_prog_run(uint64_t prog, int32_t begin, int32_t end, uintptr_t
   }
   MGX_REQUIRE(0 <= begin && begin <= end && end <= static_cast<int32_t>(p->instrs.size()),
               "mgx_prog_run: bad range [%d, %d)", begin, end);
+  MGX_REQUIRE(mode >= 0 && mode <= 3, "mgx_prog_run: unknown mode %d", mode);
   if (begin == end) return MGX_OK;
   cudaStream_t st = as_stream(stream);
-  if (!use_graph || stream == 0) return mgx::run_range(p, begin, end, st);
-
+  if (mode == 0 || (stream == 0 && mode == 1)) return mgx::run_range(p, begin, end, st);
   std::lock_guard<std::mutex> lock(p->mu);
   auto key = std::make_pair(begin, end);
-  auto it = p->graphs.find(key);
-  if (it == p->graphs.end()) {
+  if (mode == 2 || (mode == 3 && stream == 0)) {
+    mgx::FusedRange* f = nullptr;
+    MGX_TRY(mgx::get_fused(p, begin, end, &f));
+    return mgx::launch_fused(*f, st);
+  }
+  auto& cache = mode == 1 ? p->graphs : p->fgraphs;
+  auto it = cache.find(key);
+  if (it == cache.end()) {
+    mgx::FusedRange* f = nullptr;
+    if (mode == 3) MGX_TRY(mgx::get_fused(p, begin, end, &f));
     cudaGraph_t graph;
     MGX_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-    int rc = mgx::run_range(p, begin, end, st);
+    int rc = mode == 1 ? mgx::run_range(p, begin, end, st) : mgx::launch_fused(*f, st);
     cudaError_t ce = cudaStreamEndCapture(st, &graph);
     if (rc != MGX_OK) {
       if (ce == cudaSuccess) cudaGraphDestroy(graph);
@@ -307,9 +336,29 @@ extern "C" int mgx_prog_run(uint64_t prog, int32_t begin, int32_t end, uintptr_t
     cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
     cudaGraphDestroy(graph);
     MGX_CUDA(ie);
-    it = p->graphs.emplace(key, exec).first;
+    it = cache.emplace(key, exec).first;
   }
   MGX_CUDA(cudaGraphLaunch(it->second, st));
+  return MGX_OK;
+}
+
+extern "C" int mgx_prog_levels(uint64_t prog, int32_t begin, int32_t end, int32_t* nlevels,
+                               int32_t* grid, int32_t* level_of) {
+  mgx::Program* p = mgx::find_prog(prog);
+  if (!p) {
+    mgx::set_error("mgx_prog_levels: unknown program handle");
+    return MGX_BAD_HANDLE;
+  }
+  MGX_REQUIRE(nlevels && grid && 0 <= begin && begin <= end &&
+                  end <= static_cast<int32_t>(p->instrs.size()),
+              "mgx_prog_levels: bad arguments");
+  std::lock_guard<std::mutex> lock(p->mu);
+  mgx::FusedRange* f = nullptr;
+  MGX_TRY(mgx::get_fused(p, begin, end, &f));
+  *nlevels = f->nlevels;
+  *grid = f->grid;
+  if (level_of)
+    for (size_t i = 0; i < f->level_of.size(); ++i) level_of[i] = f->level_of[i];
   return MGX_OK;
 }
 
@@ -366,6 +415,8 @@ extern "C" int mgx_prog_destroy(uint64_t prog) {
     mgx::g_progs.erase(it);
   }
   for (auto& kv : p->graphs) cudaGraphExecDestroy(kv.second);
+  for (auto& kv : p->fgraphs) cudaGraphExecDestroy(kv.second);
+  for (auto& kv : p->fused) mgx::free_fused(kv.second);
   delete p;
   return MGX_OK;
 }
