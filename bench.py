@@ -328,7 +328,8 @@ def run_ours(args, world, rank, local):
             "config": {"workload": WORKLOAD, "global_batch": PER_GPU_BATCH * world,
                        "per_gpu_batch": PER_GPU_BATCH, "parallelism": f"dp{world}",
                        "l2": "flushed between timed steps (256 MB device write, untimed)",
-                       "step": "forward+backward+KVStore round captured as one CUDA graph"},
+                       "step": "forward+backward+KVStore round captured as one CUDA graph",
+                       "program_kernel": step.execs[w].uses_program_kernel},
             "e2e": {"value": e2e_value, "unit": "images/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h,
                     "path": "DataParallelStep.step(host pinned batch) + D2H softmax output + sync"},

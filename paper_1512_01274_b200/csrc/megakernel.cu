@@ -366,10 +366,20 @@ int build_fused(const mgx_instr* instrs, int n, FusedRange* out) {
 
 int launch_fused(const FusedRange& f, cudaStream_t st) {
   if (f.nlevels == 0) return MGX_OK;
-  void* args[] = {const_cast<MegaOp**>(&f.d_ops), const_cast<MegaLevel**>(&f.d_levels),
-                  const_cast<int*>(&f.nlevels), const_cast<uint32_t**>(&f.d_barrier)};
-  MGX_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(program_kernel), dim3(f.grid),
-                                       dim3(256), args, f.smem, st));
+  // cudaLaunchKernelEx + the cooperative attribute (co-residency guaranteed)
+  // is capturable into CUDA graphs, unlike cudaLaunchCooperativeKernel
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(f.grid);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = f.smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  MGX_CUDA(cudaLaunchKernelEx(&cfg, program_kernel, static_cast<const MegaOp*>(f.d_ops),
+                              static_cast<const MegaLevel*>(f.d_levels), f.nlevels, f.d_barrier));
   return MGX_OK;
 }
 

@@ -147,6 +147,7 @@ def test_whole_step_graph_capture_matches_eager(engine):
             st.capture()
             for _ in range(4):
                 st.replay()
+            assert all(ex.uses_program_kernel for ex in st.execs.values())
         else:
             for _ in range(5):
                 st.step()
@@ -188,6 +189,8 @@ def test_program_kernel_levels_and_bits(engine):
             for _ in range(3):
                 ex.forward()
                 ex.backward()
+            engine.wait_all()
+            assert ex.uses_program_kernel == fused_kernel, getattr(ex, "fused_fallback_reason", "")
             results.append([tmod.to_numpy(ex.outputs[0])] + [tmod.to_numpy(grads[n]) for n in names])
     for other in results[1:]:
         for a, b in zip(results[0], other):
