@@ -243,6 +243,10 @@ int mgx_kv_round(const mgx_kv_round_args* args, uintptr_t stream);
 /* Largest grid mgx_kv_round will use (flag arrays need grid * M*W words). */
 int mgx_kv_max_grid(int32_t machines, int32_t workers, int32_t* out);
 #define MGX_KV_FLAG_WORDS_PER_WORKER 2048  /* 2 phases x 1024 blocks */
+/* Launch shape of the round kernel for a topology: largest resident grid,
+ * threads per block, float4 vectors per thread per iteration. */
+int mgx_kv_config(int32_t machines, int32_t workers, int32_t* max_grid, int32_t* threads,
+                  int32_t* unroll);
 
 #ifdef __cplusplus
 }

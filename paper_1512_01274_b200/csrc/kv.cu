@@ -22,6 +22,8 @@
 // and after writing (all replicas final before anyone's next forward).  The
 // grid is at most one resident wave, so every block of every peer is running.
 
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -138,8 +140,8 @@ __device__ bool block_barrier(const KvParams& p, int phase, uint32_t epoch) {
   return ok != 0;
 }
 
-template <int M, int W, int UNROLL>
-__global__ void __launch_bounds__(kKvThreads) kv_round_kernel(const __grid_constant__ KvParams p) {
+template <int M, int W, int UNROLL, int THREADS>
+__global__ void __launch_bounds__(THREADS) kv_round_kernel(const __grid_constant__ KvParams p) {
   constexpr int NW = M * W;
   const bool barrier = p.flags[0] != nullptr;
   // The barrier epoch lives on the device (launch count + 1), so a captured
@@ -151,13 +153,13 @@ __global__ void __launch_bounds__(kKvThreads) kv_round_kernel(const __grid_const
   }
   const bool live = !barrier || block_barrier<NW>(p, 0, s_epoch);
 
-  const int64_t stride = int64_t(gridDim.x) * kKvThreads;
+  const int64_t stride = int64_t(gridDim.x) * THREADS;
   const float* wsrc = p.weights[p.self_replica];
   for (int s = 0; live && s < p.nseg; ++s) {
     const int64_t off = p.segs[s].off;
     const int64_t n4 = (p.segs[s].len + 3) >> 2;
     const int64_t voff = p.segs[s].voff;
-    for (int64_t base = int64_t(blockIdx.x) * kKvThreads + threadIdx.x; base < n4;
+    for (int64_t base = int64_t(blockIdx.x) * THREADS + threadIdx.x; base < n4;
          base += stride * UNROLL) {
       float4 g[UNROLL][NW];
       float4 w[UNROLL];
@@ -230,15 +232,42 @@ __global__ void __launch_bounds__(kKvThreads) kv_round_kernel(const __grid_const
 
 using KvKernel = void (*)(const KvParams);
 
-template <int M, int W>
-KvKernel pick_unroll(int64_t) {
-  if constexpr (M * W <= 4) return kv_round_kernel<M, W, 2>;
-  else return kv_round_kernel<M, W, 1>;
+struct KvVariant {
+  KvKernel k;
+  int threads, unroll;
+};
+
+template <int M, int W, int U, int T>
+constexpr KvVariant variant() {
+  return KvVariant{kv_round_kernel<M, W, U, T>, T, U};
 }
 
-static KvKernel select_kernel(int M, int W) {
+// Launch shape per topology.  For the one-machine topologies the shape can
+// be overridden with MGX_KV_VARIANT="<unroll>,<threads>" (unroll 1|2|4,
+// threads 256|512|1024) for tuning sweeps.
+template <int M, int W>
+KvVariant pick_variant() {
+  if constexpr (M == 1 && (W == 2 || W == 4 || W == 8)) {
+    static const char* env = getenv("MGX_KV_VARIANT");
+    if (env) {
+      int u = 0, t = 0;
+      if (sscanf(env, "%d,%d", &u, &t) == 2) {
+#define MGX_KV_V(uu, tt) \
+  if (u == uu && t == tt) return variant<M, W, uu, tt>();
+        MGX_KV_V(1, 256) MGX_KV_V(1, 512) MGX_KV_V(1, 1024)
+        MGX_KV_V(2, 256) MGX_KV_V(2, 512) MGX_KV_V(2, 1024)
+        MGX_KV_V(4, 256) MGX_KV_V(4, 512)
+#undef MGX_KV_V
+      }
+    }
+  }
+  if constexpr (M * W <= 4) return variant<M, W, 2, kKvThreads>();
+  else return variant<M, W, 1, kKvThreads>();
+}
+
+static KvVariant select_kernel(int M, int W) {
 #define MGX_KV_CASE(m, w) \
-  if (M == m && W == w) return pick_unroll<m, w>(0);
+  if (M == m && W == w) return pick_variant<m, w>();
   MGX_KV_CASE(1, 1) MGX_KV_CASE(1, 2) MGX_KV_CASE(1, 3) MGX_KV_CASE(1, 4)
   MGX_KV_CASE(1, 5) MGX_KV_CASE(1, 6) MGX_KV_CASE(1, 7) MGX_KV_CASE(1, 8)
   MGX_KV_CASE(1, 16)
@@ -247,10 +276,11 @@ static KvKernel select_kernel(int M, int W) {
   MGX_KV_CASE(4, 1) MGX_KV_CASE(4, 2) MGX_KV_CASE(4, 4)
   MGX_KV_CASE(8, 1) MGX_KV_CASE(8, 2)
 #undef MGX_KV_CASE
-  return nullptr;
+  return KvVariant{nullptr, 0, 0};
 }
 
-static int kv_capacity(KvKernel k, int* out) {
+static int kv_capacity(const KvVariant& v, int* out) {
+  const KvKernel k = v.k;
   // cached per (kernel, device): no runtime API calls on the launch path,
   // which matters inside stream capture
   static std::mutex mu;
@@ -267,7 +297,7 @@ static int kv_capacity(KvKernel k, int* out) {
     }
   }
   int per_sm = 0;
-  MGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kKvThreads, 0));
+  MGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, v.threads, 0));
   int dev = 0, sms = kNumSMs;
   MGX_CUDA(cudaGetDevice(&dev));
   MGX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -283,11 +313,24 @@ static int kv_capacity(KvKernel k, int* out) {
 
 extern "C" int mgx_kv_max_grid(int32_t machines, int32_t workers, int32_t* out) {
   MGX_REQUIRE(out, "mgx_kv_max_grid: null out");
-  mgx::KvKernel k = mgx::select_kernel(machines, workers);
-  MGX_REQUIRE(k, "mgx_kv_max_grid: unsupported topology %d x %d", machines, workers);
+  mgx::KvVariant v = mgx::select_kernel(machines, workers);
+  MGX_REQUIRE(v.k, "mgx_kv_max_grid: unsupported topology %d x %d", machines, workers);
   int cap = 0;
-  MGX_TRY(mgx::kv_capacity(k, &cap));
+  MGX_TRY(mgx::kv_capacity(v, &cap));
   *out = cap;
+  return MGX_OK;
+}
+
+extern "C" int mgx_kv_config(int32_t machines, int32_t workers, int32_t* max_grid,
+                             int32_t* threads, int32_t* unroll) {
+  MGX_REQUIRE(max_grid && threads && unroll, "mgx_kv_config: null out");
+  mgx::KvVariant v = mgx::select_kernel(machines, workers);
+  MGX_REQUIRE(v.k, "mgx_kv_config: unsupported topology %d x %d", machines, workers);
+  int cap = 0;
+  MGX_TRY(mgx::kv_capacity(v, &cap));
+  *max_grid = cap;
+  *threads = v.threads;
+  *unroll = v.unroll;
   return MGX_OK;
 }
 
@@ -302,8 +345,8 @@ extern "C" int mgx_kv_round(const mgx_kv_round_args* a, uintptr_t stream) {
   MGX_REQUIRE(a->updater != MGX_KV_SGD || a->velocity, "mgx_kv_round: SGD needs velocity");
   MGX_REQUIRE(a->updater != MGX_KV_AGG || a->agg_out, "mgx_kv_round: AGG needs agg_out");
   MGX_REQUIRE(a->self_replica >= 0 && a->self_replica < NW, "mgx_kv_round: bad self_replica");
-  mgx::KvKernel k = mgx::select_kernel(M, W);
-  MGX_REQUIRE(k, "mgx_kv_round: unsupported topology %d x %d", M, W);
+  mgx::KvVariant var = mgx::select_kernel(M, W);
+  MGX_REQUIRE(var.k, "mgx_kv_round: unsupported topology %d x %d", M, W);
 
   mgx::KvParams p;
   std::memset(&p, 0, sizeof(p));
@@ -335,7 +378,7 @@ extern "C" int mgx_kv_round(const mgx_kv_round_args* a, uintptr_t stream) {
   p.weight_decay = a->weight_decay;
 
   int cap = 0;
-  MGX_TRY(mgx::kv_capacity(k, &cap));
+  MGX_TRY(mgx::kv_capacity(var, &cap));
   int grid = a->grid;
   const bool barrier = a->flags != nullptr;
   if (barrier) {
@@ -346,12 +389,12 @@ extern "C" int mgx_kv_round(const mgx_kv_round_args* a, uintptr_t stream) {
   } else {
     if (total4 == 0) return MGX_OK;
     if (grid <= 0) {
-      int64_t want = mgx::ceil_div(total4, mgx::kKvThreads * 2);
+      int64_t want = mgx::ceil_div(total4, int64_t(var.threads) * var.unroll);
       grid = static_cast<int>(want < cap ? want : cap);
       if (grid < 1) grid = 1;
     }
   }
-  k<<<grid, mgx::kKvThreads, 0, mgx::as_stream(stream)>>>(p);
+  var.k<<<grid, var.threads, 0, mgx::as_stream(stream)>>>(p);
   MGX_LAUNCHED();
   return MGX_OK;
 }

@@ -556,11 +556,13 @@ class KVStore:
 
     def _grid_locked(self, total_elems: int) -> int:
         if self._grid_cap is None:
-            cap = ctypes.c_int32()
-            L.call("mgx_kv_max_grid", self.machines, self.workers, ctypes.byref(cap))
-            self._grid_cap = cap.value
+            cap, thr, unr = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+            L.call("mgx_kv_config", self.machines, self.workers, ctypes.byref(cap),
+                   ctypes.byref(thr), ctypes.byref(unr))
+            self._grid_cap, self._per_block = cap.value, thr.value * unr.value
+        # identical on every rank: derived from the flush size only
         per_rank4 = -(-total_elems // (4 * self.nw))
-        want = -(-per_rank4 // 1024)
+        want = -(-per_rank4 // self._per_block)
         return max(1, min(self._grid_cap, want))
 
     def _launch_locked(self, keys: List[int], single_worker: Optional[int] = None) -> None:
