@@ -191,6 +191,9 @@ int mgx_prog_run(uint64_t prog, int32_t begin, int32_t end, uintptr_t stream, in
  * grid size, and (optional, capacity end-begin) the level of each instruction. */
 int mgx_prog_levels(uint64_t prog, int32_t begin, int32_t end, int32_t* nlevels,
                     int32_t* grid, int32_t* level_of);
+/* Non-zero if a program kernel's grid barrier timed out since the last
+ * call (its blocks could not all be resident); clears the flag. */
+int mgx_prog_error(uint32_t* out);
 /* Per-instruction device time of one eager run of [begin,end) (profiling). */
 int mgx_prog_profile(uint64_t prog, int32_t begin, int32_t end, uintptr_t stream, float* ms_out);
 int mgx_prog_destroy(uint64_t prog);

@@ -48,12 +48,28 @@ __device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
 // Grid barrier on a monotonically increasing arrival counter: level k ends
 // when (k+1)*gridDim.x blocks have arrived.  The fences make the level's
 // global writes visible and drop stale L1 lines before the next level.
-__device__ __forceinline__ void grid_barrier(uint32_t* counter, uint32_t target) {
+__device__ __forceinline__ uint64_t now_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// A block that waits more than 10 s (another kernel holding SMs, so not
+// every block became resident) records the failure in host-mapped memory
+// and continues instead of hanging the device.
+__device__ __forceinline__ void grid_barrier(uint32_t* counter, uint32_t target, uint32_t* err) {
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
     atomicAdd(counter, 1u);
-    while (ld_acquire_gpu(counter) < target) __nanosleep(20);
+    const uint64_t t0 = now_ns();
+    while (ld_acquire_gpu(counter) < target) {
+      __nanosleep(20);
+      if (now_ns() - t0 > 10ull * 1000 * 1000 * 1000) {
+        atomicExch(err, 1u);
+        break;
+      }
+    }
     __threadfence();
   }
   __syncthreads();
@@ -111,7 +127,7 @@ __device__ void run_tile(const MegaOp& o, int t, float* smem) {
 
 __global__ void __launch_bounds__(256, 2)
 program_kernel(const MegaOp* __restrict__ ops, const MegaLevel* __restrict__ levels, int nlevels,
-               uint32_t* barrier) {
+               uint32_t* barrier, uint32_t* err) {
   extern __shared__ float4 smem_f4[];
   float* smem = reinterpret_cast<float*>(smem_f4);
   for (int lv = 0; lv < nlevels; ++lv) {
@@ -125,7 +141,7 @@ program_kernel(const MegaOp* __restrict__ ops, const MegaLevel* __restrict__ lev
       run_tile(ops[j], t - base, smem);
       __syncthreads();
     }
-    if (lv + 1 < nlevels) grid_barrier(barrier, uint32_t(lv + 1) * gridDim.x);
+    if (lv + 1 < nlevels) grid_barrier(barrier, uint32_t(lv + 1) * gridDim.x, err);
   }
   // last block out resets the counters for the next launch
   __syncthreads();
@@ -140,6 +156,20 @@ program_kernel(const MegaOp* __restrict__ ops, const MegaLevel* __restrict__ lev
 }
 
 // ------------------------------------------------------------------ host
+
+// process-wide error word in host-mapped pinned memory (barrier timeouts)
+uint32_t* program_error_word() {
+  static uint32_t* word = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, 64, cudaHostAllocMapped | cudaHostAllocPortable) == cudaSuccess) {
+      std::memset(p, 0, 64);
+      word = static_cast<uint32_t*>(p);
+    }
+  });
+  return word;
+}
 
 struct Range {
   uintptr_t lo, hi;
@@ -350,7 +380,7 @@ int build_fused(const mgx_instr* instrs, int n, FusedRange* out) {
     set_error("program kernel does not fit on an SM (smem %zu)", smem);
     return MGX_INTERNAL;
   }
-  out->grid = std::min(per_sm * sms, max_tiles);
+  out->grid = std::min(sms, max_tiles);
   out->smem = std::max<size_t>(smem, 16);
   out->nlevels = static_cast<int>(levels.size());
   out->level_of = level;
@@ -366,20 +396,12 @@ int build_fused(const mgx_instr* instrs, int n, FusedRange* out) {
 
 int launch_fused(const FusedRange& f, cudaStream_t st) {
   if (f.nlevels == 0) return MGX_OK;
-  // cudaLaunchKernelEx + the cooperative attribute (co-residency guaranteed)
-  // is capturable into CUDA graphs, unlike cudaLaunchCooperativeKernel
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(f.grid);
-  cfg.blockDim = dim3(256);
-  cfg.dynamicSmemBytes = f.smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  MGX_CUDA(cudaLaunchKernelEx(&cfg, program_kernel, static_cast<const MegaOp*>(f.d_ops),
-                              static_cast<const MegaLevel*>(f.d_levels), f.nlevels, f.d_barrier));
+  // Plain launch, one block per SM: every block is resident when the stream
+  // owns the device (cooperative launches were rejected for this kernel and
+  // are not capturable here); the barrier times out instead of hanging.
+  program_kernel<<<f.grid, 256, f.smem, st>>>(f.d_ops, f.d_levels, f.nlevels, f.d_barrier,
+                                              program_error_word());
+  MGX_LAUNCHED();
   return MGX_OK;
 }
 

@@ -342,6 +342,14 @@ extern "C" int mgx_prog_run(uint64_t prog, int32_t begin, int32_t end, uintptr_t
   return MGX_OK;
 }
 
+extern "C" int mgx_prog_error(uint32_t* out) {
+  MGX_REQUIRE(out, "mgx_prog_error: null out");
+  uint32_t* w = mgx::program_error_word();
+  *out = w ? *reinterpret_cast<volatile uint32_t*>(w) : 0;
+  if (w) *w = 0;
+  return MGX_OK;
+}
+
 extern "C" int mgx_prog_levels(uint64_t prog, int32_t begin, int32_t end, int32_t* nlevels,
                                int32_t* grid, int32_t* level_of) {
   mgx::Program* p = mgx::find_prog(prog);
