@@ -372,8 +372,18 @@ int build_fused(const mgx_instr* instrs, int n, FusedRange* out) {
   int dev = 0, sms = kNumSMs, per_sm = 0;
   MGX_CUDA(cudaGetDevice(&dev));
   MGX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  MGX_CUDA(cudaFuncSetAttribute(program_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(std::max<size_t>(smem, 16))));
+  {
+    // the attribute is per function: only ever raise it, or building one
+    // range would shrink the limit another range was built with
+    static std::mutex mu;
+    static size_t granted[16] = {0};
+    std::lock_guard<std::mutex> lock(mu);
+    if (smem > granted[dev & 15]) {
+      MGX_CUDA(cudaFuncSetAttribute(program_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem)));
+      granted[dev & 15] = smem;
+    }
+  }
   MGX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, program_kernel, 256,
                                                          std::max<size_t>(smem, 16)));
   if (per_sm < 1) {
