@@ -104,6 +104,9 @@ int pw_leaf_table(int64_t K, const PwLeaf** out, int* nleaves, int* max_depth, i
   MGX_CUDA(cudaMalloc(&d, bytes > 0 ? bytes : sizeof(PwLeaf)));
   // Plain synchronous copy: done once per (device, K), before any capture.
   MGX_CUDA(cudaMemcpy(d, table.data(), bytes, cudaMemcpyHostToDevice));
+  // a pageable H2D copy may return before the DMA lands; kernels read the
+  // table from non-blocking streams
+  MGX_CUDA(cudaDeviceSynchronize());
   g_leaf_tables[key] = d;
   *out = d;
   return MGX_OK;

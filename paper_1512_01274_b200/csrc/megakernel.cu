@@ -401,6 +401,9 @@ int build_fused(const mgx_instr* instrs, int n, FusedRange* out) {
   MGX_CUDA(cudaMemcpy(out->d_levels, levels.data(), levels.size() * sizeof(MegaLevel),
                       cudaMemcpyHostToDevice));
   MGX_CUDA(cudaMemset(out->d_barrier, 0, 2 * sizeof(uint32_t)));
+  // the uploads above ride the legacy stream and may still be in flight; the
+  // program kernel launches on a non-blocking stream, so finish them first
+  MGX_CUDA(cudaDeviceSynchronize());
   return MGX_OK;
 }
 
