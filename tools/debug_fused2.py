@@ -10,12 +10,13 @@ from paper_1512_01274_b200.executor import bind
 from paper_1512_01274_b200.train import init_params, mlp, param_names
 
 eng = Engine(device=0)
-feats, labels = ostep.cfg1_data(100)
+B = int(sys.argv[1]) if len(sys.argv) > 1 else 100
+feats, labels = ostep.cfg1_data(B)
 g = mlp([128, 64], 10)
-shapes, _ = symbol.infer_shape(g, {"data": (100, 784), "label": (100,)})
+shapes, _ = symbol.infer_shape(g, {"data": (B, 784), "label": (B,)})
 p0 = init_params(g, shapes, 0); names = param_names(g)
-args = {"data": tmod.from_host((100, 784), "float32", feats, engine=eng),
-        "label": tmod.from_host((100,), "float32", labels, engine=eng)}
+args = {"data": tmod.from_host((B, 784), "float32", feats, engine=eng),
+        "label": tmod.from_host((B,), "float32", labels, engine=eng)}
 for n in names: args[n] = tmod.from_host(shapes[n], "float32", p0[n], engine=eng)
 grads = {n: tmod.zeros(shapes[n], engine=eng) for n in names}
 ex = bind(g, args, {n: "write" for n in names}, grads, engine=eng)
