@@ -41,7 +41,7 @@ def reset():
 
 
 n = ex._n_all
-for mode in (2,):
+for mode in (2, 3):
     # per instruction: state from eager prefix, then instruction i in mode
     for i in range(n):
         reset(); run(0, i, 0); run(i, i + 1, 0); want = snap()
@@ -54,3 +54,17 @@ for mode in (2,):
         print("whole", k, torch.equal(torch.nan_to_num(a, 7.0), torch.nan_to_num(b, 7.0)),
               int(torch.isnan(b).sum()))
 print("err word", L.lib().mgx_prog_error)
+
+# two executors on one engine, alternating, mode 3 vs mode 0
+ex2 = bind(g, {k: (tmod.from_host(v.shape, "float32", tmod.to_numpy(v), engine=eng)) for k, v in args.items()},
+           {n: "write" for n in names}, {n: tmod.zeros(shapes[n], engine=eng) for n in names}, engine=eng)
+for mode in (0, 3):
+    outs = []
+    for e in (ex, ex2):
+        e.engine.synchronize()
+    for _ in range(3):
+        for e in (ex, ex2):
+            L.lib().mgx_prog_run(e._prog, 0, e._n_fwd, eng.stream_handle, mode)
+            L.lib().mgx_prog_run(e._prog, e._n_fwd, e._n_all, eng.stream_handle, mode)
+    torch.cuda.synchronize()
+    print("two executors mode", mode, [float(e.outputs[0].arr.sum()) for e in (ex, ex2)])
