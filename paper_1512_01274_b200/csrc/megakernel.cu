@@ -333,6 +333,12 @@ static int build_op(const mgx_instr& in, MegaOp* o, size_t* smem_need) {
 }
 
 int build_fused(const mgx_instr* instrs, int n, FusedRange* out) {
+  // allocate the error word now: a first use inside a stream capture would
+  // allocate during capture and invalidate it
+  if (!program_error_word()) {
+    set_error("program kernel: cannot allocate the host-mapped error word");
+    return MGX_INTERNAL;
+  }
   std::vector<std::vector<Range>> rd(n), wr(n);
   for (int i = 0; i < n; ++i) extents(instrs[i], rd[i], wr[i]);
   std::vector<int> level(n, 0);
