@@ -7,12 +7,10 @@
 
 namespace mgx {
 
-struct MegaOp;
-struct MegaLevel;
+struct ProgramParams;
 
 struct FusedRange {
-  MegaOp* d_ops = nullptr;
-  MegaLevel* d_levels = nullptr;
+  ProgramParams* params = nullptr;  // host copy, passed by value at launch
   uint32_t* d_barrier = nullptr;
   int nlevels = 0;
   int grid = 0;

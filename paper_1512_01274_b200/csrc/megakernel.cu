@@ -64,7 +64,6 @@ __device__ __forceinline__ void grid_barrier(uint32_t* counter, uint32_t target,
     atomicAdd(counter, 1u);
     const uint64_t t0 = now_ns();
     while (ld_acquire_gpu(counter) < target) {
-      __nanosleep(20);
       if (now_ns() - t0 > 10ull * 1000 * 1000 * 1000) {
         atomicExch(err, 1u);
         break;
@@ -125,23 +124,37 @@ __device__ void run_tile(const MegaOp& o, int t, float* smem) {
   }
 }
 
-__global__ void __launch_bounds__(256, 2)
-program_kernel(const MegaOp* __restrict__ ops, const MegaLevel* __restrict__ levels, int nlevels,
-               uint32_t* barrier, uint32_t* err) {
+// The whole op/level table travels as one __grid_constant__ kernel
+// parameter: tiles read their descriptors through the constant cache
+// (uniform broadcast) instead of dependent global loads.
+constexpr int kMaxProgramOps = 48;
+constexpr int kMaxProgramLevels = 48;
+
+struct ProgramParams {
+  uint32_t* barrier;
+  uint32_t* err;
+  int32_t nlevels, nops;
+  MegaLevel levels[kMaxProgramLevels];
+  MegaOp ops[kMaxProgramOps];
+};
+
+__global__ void __launch_bounds__(256, 1)
+program_kernel(const __grid_constant__ ProgramParams p) {
   extern __shared__ float4 smem_f4[];
   float* smem = reinterpret_cast<float*>(smem_f4);
-  for (int lv = 0; lv < nlevels; ++lv) {
-    const MegaLevel L = levels[lv];
+  uint32_t* barrier = p.barrier;
+  for (int lv = 0; lv < p.nlevels; ++lv) {
+    const MegaLevel L = p.levels[lv];
     for (int t = blockIdx.x; t < L.tiles; t += gridDim.x) {
       int j = L.first, base = 0;
-      while (t - base >= ops[j].ntiles) {
-        base += ops[j].ntiles;
+      while (t - base >= p.ops[j].ntiles) {
+        base += p.ops[j].ntiles;
         ++j;
       }
-      run_tile(ops[j], t - base, smem);
+      run_tile(p.ops[j], t - base, smem);
       __syncthreads();
     }
-    if (lv + 1 < nlevels) grid_barrier(barrier, uint32_t(lv + 1) * gridDim.x, err);
+    if (lv + 1 < p.nlevels) grid_barrier(barrier, uint32_t(lv + 1) * gridDim.x, p.err);
   }
   // last block out resets the counters for the next launch
   __syncthreads();
@@ -396,20 +409,29 @@ int build_fused(const mgx_instr* instrs, int n, FusedRange* out) {
     set_error("program kernel does not fit on an SM (smem %zu)", smem);
     return MGX_INTERNAL;
   }
+  if (ops.size() > size_t(kMaxProgramOps) || levels.size() > size_t(kMaxProgramLevels)) {
+    set_error("program kernel: %zu ops / %zu levels exceed %d / %d", ops.size(), levels.size(),
+              kMaxProgramOps, kMaxProgramLevels);
+    return MGX_BAD_ARGUMENT;
+  }
   out->grid = std::min(sms, max_tiles);
   out->smem = std::max<size_t>(smem, 16);
   out->nlevels = static_cast<int>(levels.size());
   out->level_of = level;
-  MGX_CUDA(cudaMalloc(&out->d_ops, ops.size() * sizeof(MegaOp)));
-  MGX_CUDA(cudaMalloc(&out->d_levels, levels.size() * sizeof(MegaLevel)));
   MGX_CUDA(cudaMalloc(&out->d_barrier, 2 * sizeof(uint32_t)));
-  MGX_CUDA(cudaMemcpy(out->d_ops, ops.data(), ops.size() * sizeof(MegaOp), cudaMemcpyHostToDevice));
-  MGX_CUDA(cudaMemcpy(out->d_levels, levels.data(), levels.size() * sizeof(MegaLevel),
-                      cudaMemcpyHostToDevice));
   MGX_CUDA(cudaMemset(out->d_barrier, 0, 2 * sizeof(uint32_t)));
-  // the uploads above ride the legacy stream and may still be in flight; the
-  // program kernel launches on a non-blocking stream, so finish them first
+  // the memset rides the legacy stream and may still be in flight; the
+  // program kernel launches on a non-blocking stream, so finish it first
   MGX_CUDA(cudaDeviceSynchronize());
+  auto* prm = new ProgramParams();
+  std::memset(prm, 0, sizeof(*prm));
+  prm->barrier = out->d_barrier;
+  prm->err = program_error_word();
+  prm->nlevels = static_cast<int32_t>(levels.size());
+  prm->nops = static_cast<int32_t>(ops.size());
+  std::copy(levels.begin(), levels.end(), prm->levels);
+  std::copy(ops.begin(), ops.end(), prm->ops);
+  out->params = prm;
   return MGX_OK;
 }
 
@@ -418,16 +440,14 @@ int launch_fused(const FusedRange& f, cudaStream_t st) {
   // Plain launch, one block per SM: every block is resident when the stream
   // owns the device (cooperative launches were rejected for this kernel and
   // are not capturable here); the barrier times out instead of hanging.
-  program_kernel<<<f.grid, 256, f.smem, st>>>(f.d_ops, f.d_levels, f.nlevels, f.d_barrier,
-                                              program_error_word());
+  program_kernel<<<f.grid, 256, f.smem, st>>>(*f.params);
   MGX_LAUNCHED();
   return MGX_OK;
 }
 
 void free_fused(FusedRange& f) {
-  if (f.d_ops) cudaFree(f.d_ops);
-  if (f.d_levels) cudaFree(f.d_levels);
   if (f.d_barrier) cudaFree(f.d_barrier);
+  delete f.params;
   f = FusedRange();
 }
 
