@@ -21,6 +21,7 @@ struct FusedRange {
 int build_fused(const mgx_instr* instrs, int n, FusedRange* out);
 uint32_t* program_error_word();
 int launch_fused(const FusedRange& f, cudaStream_t st);
+int time_fused(const FusedRange& f, cudaStream_t st, double* ns_out);
 void free_fused(FusedRange& f);
 
 }  // namespace mgx

@@ -133,6 +133,7 @@ constexpr int kMaxProgramLevels = 48;
 struct ProgramParams {
   uint32_t* barrier;
   uint32_t* err;
+  unsigned long long* times;  // optional: [0] launch start, [1+lv] last block done with level lv
   int32_t nlevels, nops;
   MegaLevel levels[kMaxProgramLevels];
   MegaOp ops[kMaxProgramOps];
@@ -143,6 +144,7 @@ program_kernel(const __grid_constant__ ProgramParams p) {
   extern __shared__ float4 smem_f4[];
   float* smem = reinterpret_cast<float*>(smem_f4);
   uint32_t* barrier = p.barrier;
+  if (p.times && threadIdx.x == 0) atomicMin(&p.times[0], static_cast<unsigned long long>(now_ns()));
   for (int lv = 0; lv < p.nlevels; ++lv) {
     const MegaLevel L = p.levels[lv];
     for (int t = blockIdx.x; t < L.tiles; t += gridDim.x) {
@@ -154,6 +156,8 @@ program_kernel(const __grid_constant__ ProgramParams p) {
       run_tile(p.ops[j], t - base, smem);
       __syncthreads();
     }
+    if (p.times && threadIdx.x == 0)
+      atomicMax(&p.times[1 + lv], static_cast<unsigned long long>(now_ns()));
     if (lv + 1 < p.nlevels) grid_barrier(barrier, uint32_t(lv + 1) * gridDim.x, p.err);
   }
   // last block out resets the counters for the next launch
@@ -442,6 +446,26 @@ int launch_fused(const FusedRange& f, cudaStream_t st) {
   // are not capturable here); the barrier times out instead of hanging.
   program_kernel<<<f.grid, 256, f.smem, st>>>(*f.params);
   MGX_LAUNCHED();
+  return MGX_OK;
+}
+
+// One instrumented launch: ns from the first block's start to the last block
+// finishing each level (includes that level's barrier wait of the previous).
+int time_fused(const FusedRange& f, cudaStream_t st, double* ns_out) {
+  if (f.nlevels == 0) return MGX_OK;
+  unsigned long long* buf = nullptr;
+  MGX_CUDA(cudaHostAlloc(&buf, (f.nlevels + 1) * sizeof(unsigned long long), cudaHostAllocMapped));
+  buf[0] = ~0ull;
+  for (int i = 1; i <= f.nlevels; ++i) buf[i] = 0;
+  ProgramParams prm = *f.params;
+  prm.times = buf;
+  program_kernel<<<f.grid, 256, f.smem, st>>>(prm);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e == cudaSuccess)
+    for (int i = 0; i < f.nlevels; ++i) ns_out[i] = double(buf[1 + i] - buf[0]);
+  cudaFreeHost(buf);
+  MGX_CUDA(e);
   return MGX_OK;
 }
 

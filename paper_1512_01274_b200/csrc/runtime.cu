@@ -342,6 +342,22 @@ extern "C" int mgx_prog_run(uint64_t prog, int32_t begin, int32_t end, uintptr_t
   return MGX_OK;
 }
 
+extern "C" int mgx_prog_time_levels(uint64_t prog, int32_t begin, int32_t end, uintptr_t stream,
+                                    double* ns_out) {
+  mgx::Program* p = mgx::find_prog(prog);
+  if (!p) {
+    mgx::set_error("mgx_prog_time_levels: unknown program handle");
+    return MGX_BAD_HANDLE;
+  }
+  MGX_REQUIRE(ns_out && stream && 0 <= begin && begin <= end &&
+                  end <= static_cast<int32_t>(p->instrs.size()),
+              "mgx_prog_time_levels: bad arguments");
+  std::lock_guard<std::mutex> lock(p->mu);
+  mgx::FusedRange* f = nullptr;
+  MGX_TRY(mgx::get_fused(p, begin, end, &f));
+  return mgx::time_fused(*f, as_stream(stream), ns_out);
+}
+
 extern "C" int mgx_prog_error(uint32_t* out) {
   MGX_REQUIRE(out, "mgx_prog_error: null out");
   uint32_t* w = mgx::program_error_word();
