@@ -194,6 +194,11 @@ int mgx_prog_levels(uint64_t prog, int32_t begin, int32_t end, int32_t* nlevels,
 /* Non-zero if a program kernel's grid barrier timed out since the last
  * call (its blocks could not all be resident); clears the flag. */
 int mgx_prog_error(uint32_t* out);
+/* Diagnostics: one instrumented program-kernel launch of [begin, end);
+ * ns_out[l] = ns from the first block's start until the last block finished
+ * level l (capacity = level count). */
+int mgx_prog_time_levels(uint64_t prog, int32_t begin, int32_t end, uintptr_t stream,
+                         double* ns_out);
 /* Per-instruction device time of one eager run of [begin,end) (profiling). */
 int mgx_prog_profile(uint64_t prog, int32_t begin, int32_t end, uintptr_t stream, float* ms_out);
 int mgx_prog_destroy(uint64_t prog);

@@ -124,6 +124,7 @@ _SIGNATURES = {
     "mgx_prog_destroy": ([c_u64], ctypes.c_int),
     "mgx_kv_round": ([ctypes.POINTER(KvRoundArgs), c_uptr], ctypes.c_int),
     "mgx_prog_error": ([ctypes.POINTER(c_u32)], ctypes.c_int),
+    "mgx_prog_time_levels": ([c_u64, c_i32, c_i32, c_uptr, c_vp], ctypes.c_int),
     "mgx_kv_max_grid": ([c_i32, c_i32, ctypes.POINTER(c_i32)], ctypes.c_int),
     "mgx_kv_config": ([c_i32, c_i32, ctypes.POINTER(c_i32), ctypes.POINTER(c_i32),
                        ctypes.POINTER(c_i32)], ctypes.c_int),
