@@ -58,10 +58,11 @@ __device__ __forceinline__ uint64_t now_ns() {
 // every block became resident) records the failure in host-mapped memory
 // and continues instead of hanging the device.
 __device__ __forceinline__ void grid_barrier(uint32_t* counter, uint32_t target, uint32_t* err) {
+  // release-add publishes this block's writes (ordered before it by the
+  // bar.sync), acquire-polling makes the other blocks' writes visible
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(counter, 1u);
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(counter) : "memory");
     const uint64_t t0 = now_ns();
     while (ld_acquire_gpu(counter) < target) {
       if (now_ns() - t0 > 10ull * 1000 * 1000 * 1000) {
@@ -69,7 +70,6 @@ __device__ __forceinline__ void grid_barrier(uint32_t* counter, uint32_t target,
         break;
       }
     }
-    __threadfence();
   }
   __syncthreads();
 }
@@ -453,18 +453,24 @@ int launch_fused(const FusedRange& f, cudaStream_t st) {
 // finishing each level (includes that level's barrier wait of the previous).
 int time_fused(const FusedRange& f, cudaStream_t st, double* ns_out) {
   if (f.nlevels == 0) return MGX_OK;
+  // device-resident timestamps (host-mapped atomics would dominate the timing)
+  std::vector<unsigned long long> host(f.nlevels + 1, 0);
+  host[0] = ~0ull;
   unsigned long long* buf = nullptr;
-  MGX_CUDA(cudaHostAlloc(&buf, (f.nlevels + 1) * sizeof(unsigned long long), cudaHostAllocMapped));
-  buf[0] = ~0ull;
-  for (int i = 1; i <= f.nlevels; ++i) buf[i] = 0;
+  MGX_CUDA(cudaMalloc(&buf, host.size() * sizeof(unsigned long long)));
+  cudaError_t e = cudaMemcpyAsync(buf, host.data(), host.size() * 8, cudaMemcpyHostToDevice, st);
   ProgramParams prm = *f.params;
   prm.times = buf;
-  program_kernel<<<f.grid, 256, f.smem, st>>>(prm);
-  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) {
+    program_kernel<<<f.grid, 256, f.smem, st>>>(prm);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(host.data(), buf, host.size() * 8, cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e == cudaSuccess)
-    for (int i = 0; i < f.nlevels; ++i) ns_out[i] = double(buf[1 + i] - buf[0]);
-  cudaFreeHost(buf);
+    for (int i = 0; i < f.nlevels; ++i) ns_out[i] = double(host[1 + i] - host[0]);
+  cudaFree(buf);
   MGX_CUDA(e);
   return MGX_OK;
 }
