@@ -127,6 +127,11 @@ int mgx_gemm_bf16_tc(const void* A, int64_t lda, const void* B, int64_t ldb,
                      int64_t M, int64_t N, int64_t K, int act, uintptr_t stream);
 /* y(bf16) = round-to-nearest-even(x(fp32)) */
 int mgx_cast_f32_bf16(const float* x, void* y, int64_t n, uintptr_t stream);
+/* y (bf16, rows x ldo) = x (fp32, R x C, row stride ldi), transposed if
+ * transpose != 0 (y then holds x^T), zero-filled beyond the source extent
+ * (the K padding of a tensor-core operand). */
+int mgx_cast_bf16_2d(const float* x, int64_t R, int64_t C, int64_t ldi, void* y,
+                     int64_t rows, int64_t ldo, int transpose, uintptr_t stream);
 
 /* Momentum SGD, tensor path (optim.py:39-50): 5 separately rounded steps. */
 int mgx_sgd_step(float* w, const float* g, float* v, int64_t n,
@@ -178,6 +183,9 @@ typedef struct mgx_instr {
 #define MGX_OP_SOFTMAX_FWD 10 /* ptr0=x ptr1=p dims=B,C                           */
 #define MGX_OP_SOFTMAX_BWD 11 /* ptr0=p ptr1=label ptr2=g dims=B,C                */
 #define MGX_OP_AXPY 12        /* ptr0=x ptr1=y dims0=n fattr0=alpha               */
+#define MGX_OP_CAST_BF16 13   /* ptr0=x(f32) ptr1=y(bf16) dims=R,C,ldi,rows,ldo,T */
+#define MGX_OP_GEMM_TC 14     /* ptr0=A ptr1=B ptr2=bias ptr3=C act (bf16 TN)     */
+                              /* dims=M,N,K,lda,ldb,ldc                           */
 
 /* Run instructions eagerly, in order, on stream (no program object). */
 int mgx_instr_run(const mgx_instr* instrs, int32_t count, uintptr_t stream);

@@ -27,6 +27,7 @@ ACT_CODES = {"relu": 1, "sigmoid": 2, "tanh": 3}
 # instruction opcodes (include/mgx.h MGX_OP_*)
 OP_FILL, OP_COPY, OP_EW, OP_SCALAR, OP_GEMM_PW, OP_GEMM_SEQ, OP_DW_DB = 1, 2, 3, 4, 5, 6, 7
 OP_ACT_FWD, OP_ACT_BWD, OP_SOFTMAX_FWD, OP_SOFTMAX_BWD, OP_AXPY = 8, 9, 10, 11, 12
+OP_CAST_BF16, OP_GEMM_TC = 13, 14
 
 KV_ADD, KV_SGD, KV_AGG = 0, 1, 2
 KV_MAX_SEGS = 256
@@ -109,6 +110,8 @@ _SIGNATURES = {
     "mgx_gemm_bf16_tc": ([c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, c_i64, c_i64, c_i64, c_i64,
                           ctypes.c_int, c_uptr], ctypes.c_int),
     "mgx_cast_f32_bf16": ([c_vp, c_vp, c_i64, c_uptr], ctypes.c_int),
+    "mgx_cast_bf16_2d": ([c_vp, c_i64, c_i64, c_i64, c_vp, c_i64, c_i64, ctypes.c_int, c_uptr],
+                         ctypes.c_int),
     "mgx_sgd_step": ([c_vp, c_vp, c_vp, c_i64, c_f32, c_f32, c_f32, c_uptr], ctypes.c_int),
     "mgx_plan_memory": ([c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32,
                          c_vp, c_vp, c_vp, ctypes.POINTER(c_i32), c_vp, c_i32,

@@ -191,6 +191,26 @@ tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
   }
 }
 
+// y (bf16, rows x ldo) = x (fp32, R x C, row stride ldi), optionally
+// transposed (y is C x ldo then), zero-filled beyond the source extent so the
+// padded K columns contribute nothing to the tensor-core contraction.
+__global__ void cast_2d_kernel(const float* __restrict__ x, int64_t R, int64_t C, int64_t ldi,
+                               __nv_bfloat16* __restrict__ y, int64_t rows, int64_t ldo,
+                               int transpose) {
+  const int64_t n = rows * ldo;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const int64_t r = i / ldo, c = i - r * ldo;
+    float v = 0.0f;
+    if (!transpose) {
+      if (r < R && c < C) v = x[r * ldi + c];
+    } else {
+      if (c < R && r < C) v = x[c * ldi + r];
+    }
+    y[i] = __float2bfloat16_rn(v);
+  }
+}
+
 __global__ void cast_f32_bf16_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ y,
                                      int64_t n) {
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
@@ -262,6 +282,19 @@ extern "C" int mgx_gemm_bf16_tc(const void* A, int64_t lda, const void* B, int64
   tc_gemm_bf16_kernel<<<grid, 128, kSmemBytes, mgx::as_stream(stream)>>>(
       ma, mb, bias, C, static_cast<int>(ldc), static_cast<int>(M), static_cast<int>(N),
       static_cast<int>(K), act);
+  MGX_LAUNCHED();
+  return MGX_OK;
+}
+
+extern "C" int mgx_cast_bf16_2d(const float* x, int64_t R, int64_t C, int64_t ldi, void* y,
+                                int64_t rows, int64_t ldo, int transpose, uintptr_t stream) {
+  MGX_REQUIRE(x && y && R > 0 && C > 0 && rows > 0 && ldo > 0, "mgx_cast_bf16_2d: bad arguments");
+  MGX_REQUIRE(transpose ? (rows >= C && ldo >= R) : (rows >= R && ldo >= C),
+              "mgx_cast_bf16_2d: destination smaller than the source");
+  int64_t blocks = mgx::ceil_div(rows * ldo, 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  mgx::tc::cast_2d_kernel<<<static_cast<unsigned>(blocks), 256, 0, mgx::as_stream(stream)>>>(
+      x, R, C, ldi, static_cast<__nv_bfloat16*>(y), rows, ldo, transpose);
   MGX_LAUNCHED();
   return MGX_OK;
 }

@@ -127,6 +127,11 @@ def instr_cost(ins: L.Instr) -> tuple:
         b, h, f = d[0], d[1], d[2]
         byt = 4 * (b * h + ((b * f + h * f) if has[2] else 0) + (h if has[3] else 0))
         return byt, (2 * b * h * f if has[2] else 0) + (b * h if has[3] else 0)
+    if op == L.OP_GEMM_TC:
+        m, n, k = d[0], d[1], d[2]
+        return 2 * (m * k + n * k) + 4 * m * n + (4 * n if has[2] else 0), 2 * m * n * k
+    if op == L.OP_CAST_BF16:
+        return 4 * d[0] * d[1] + 2 * d[3] * d[4], d[3] * d[4]
     if op == L.OP_SOFTMAX_FWD:
         return 4 * 2 * d[0] * d[1], 4 * d[0] * d[1]
     if op == L.OP_SOFTMAX_BWD:
@@ -207,6 +212,49 @@ def fc_forward_instr(x: View, w: View, b: Optional[View], out: View, act: int = 
     h = w.shape[0]
     return instr(L.OP_GEMM_PW, [x.ptr, w.ptr, b.ptr if b else None, out.ptr],
                  [bsz, h, f, f, f, h], act=act)
+
+
+# ---- bf16 tensor-core lowering (executor dense="bf16"): tolerance path.
+# Operands are cast (and transposed where the contraction needs K-major
+# operands) into bf16 scratch with K padded to a multiple of 8, then one
+# tcgen05 GEMM with fp32 accumulation in TMEM (csrc/tc_gemm.cu).
+
+def _pad8(n: int) -> int:
+    return -(-n // 8) * 8
+
+
+def _cast(src: View, rows_in: int, cols_in: int, dst: int, rows_out: int, ld_out: int,
+          transpose: bool):
+    return instr(L.OP_CAST_BF16, [src.ptr, dst],
+                 [rows_in, cols_in, cols_in, rows_out, ld_out, 1 if transpose else 0])
+
+
+def fc_forward_tc(x: View, w: View, b: Optional[View], out: View, act: int, alloc) -> list:
+    bsz, f = _flat2(x.shape)
+    h = w.shape[0]
+    fp = _pad8(f)
+    xb, wb = alloc(bsz * fp), alloc(h * fp)
+    return [_cast(x, bsz, f, xb, bsz, fp, False), _cast(w, h, f, wb, h, fp, False),
+            instr(L.OP_GEMM_TC, [xb, wb, b.ptr if b else None, out.ptr], [bsz, h, fp, fp, fp, h],
+                  act=act)]
+
+
+def fc_dx_tc(og: View, w: View, dx: View, alloc) -> list:
+    bsz, h = og.shape
+    f = w.shape[1]
+    hp = _pad8(h)
+    ogb, wtb = alloc(bsz * hp), alloc(f * hp)
+    return [_cast(og, bsz, h, ogb, bsz, hp, False), _cast(w, h, f, wtb, f, hp, True),
+            instr(L.OP_GEMM_TC, [ogb, wtb, None, dx.ptr], [bsz, f, hp, hp, hp, f])]
+
+
+def fc_dw_tc(og: View, x: View, dw: View, alloc) -> list:
+    bsz, h = og.shape
+    f = _flat2(x.shape)[1]
+    bp = _pad8(bsz)
+    ogt, xt = alloc(h * bp), alloc(f * bp)
+    return [_cast(og, bsz, h, ogt, h, bp, True), _cast(x, bsz, f, xt, f, bp, True),
+            instr(L.OP_GEMM_TC, [ogt, xt, None, dw.ptr], [h, f, bp, bp, bp, f])]
 
 
 def _fc_lower_fwd(ins, out, attrs):

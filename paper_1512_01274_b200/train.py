@@ -117,7 +117,7 @@ class DataParallelStep:
 
     def __init__(self, g: SymbolGraph, kv: KVStore, shard_shapes: Dict[str, tuple],
                  params0: Dict[str, np.ndarray], strategy: str = "both",
-                 engine: Optional[Engine] = None, use_graph: bool = True):
+                 engine: Optional[Engine] = None, use_graph: bool = True, dense: str = "fp32"):
         _check_graph(g)
         self.g, self.kv = g, kv
         self.engine = engine or kv.engine
@@ -137,7 +137,8 @@ class DataParallelStep:
                 grads[n] = kv.grad_tensor(i, w)
             self.args[w], self.grads[w] = args, grads
             self.execs[w] = bind(g, args, {n: "write" for n in self.names}, grads,
-                                 strategy=strategy, engine=self.engine, use_graph=use_graph)
+                                 strategy=strategy, engine=self.engine, use_graph=use_graph,
+                                 dense=dense)
         self.plan_bytes = self.execs[self.workers[0]].plan.total_internal_bytes
         self._graph_exec = None
 
@@ -252,13 +253,15 @@ def train_distributed(g: SymbolGraph, data, cfg: SGDConfig, epochs: int, batch: 
                       machines: int = 1, workers: int = 1, mode: str = "sequential",
                       strategy: str = "both", param_seed: int = 0, shuffle_seed: int = 0,
                       tcp: Optional[str] = None, distributed: bool = False,
-                      engine: Optional[Engine] = None
+                      engine: Optional[Engine] = None, dense: str = "fp32"
                       ) -> Tuple[TrainReport, Dict[str, np.ndarray]]:
     """Data-parallel SGD through the device KVStore (train.py:158-270).
 
     ``distributed=False``: all M*W workers in this process on one device (the
     reference's threading model).  ``distributed=True``: one worker per
-    torch.distributed rank (launch with torchrun, world size M*W)."""
+    torch.distributed rank (launch with torchrun, world size M*W).
+    ``dense="bf16"`` runs the FC contractions on the tcgen05 tensor cores
+    (bf16 operands, fp32 accumulation; tolerance-matched, not exact order)."""
     _check_graph(g)
     nworkers = machines * workers
     if batch % nworkers:
@@ -274,7 +277,8 @@ def train_distributed(g: SymbolGraph, data, cfg: SGDConfig, epochs: int, batch: 
     engine = engine or default_engine()
     kv = KVStore(machines, workers, mode, engine=engine, tcp=tcp, distributed=distributed)
     try:
-        step = DataParallelStep(g, kv, given, params0, strategy=strategy, engine=engine)
+        step = DataParallelStep(g, kv, given, params0, strategy=strategy, engine=engine,
+                                dense=dense)
         kv.set_updater(make_sgd_updater(cfg, scale=nworkers))
         report = TrainReport()
         last = engine.executed
