@@ -394,16 +394,18 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     args = ap.parse_args()
     world, rank, local = dist_env()
+    if args.impl == "reference":
+        # CPU reference arm: rank 0 alone times the oracle port; the other
+        # ranks have no work and exit immediately
+        run_reference(args, world, rank)
+        return
     if world > 1:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     try:
-        if args.impl == "reference":
-            run_reference(args, world, rank)
-        else:
-            run_ours(args, world, rank, local)
+        run_ours(args, world, rank, local)
     finally:
         if world > 1:
             import torch.distributed as dist

@@ -36,8 +36,10 @@ def test_bf16_executor_uses_tensor_core_program(engine):
     p_want, g_want = ostep.mlp_forward_backward(p0, [128, 64], feats, labels)
     np.testing.assert_allclose(tmod.to_numpy(ex.outputs[0]), p_want, rtol=1e-2, atol=1e-3)
     for n in names:
-        np.testing.assert_allclose(tmod.to_numpy(grads[n]), g_want[n], rtol=1e-2, atol=1e-3,
-                                   err_msg=n)
+        # gradients: bf16 operand rounding relative to the gradient's scale
+        scale = float(np.abs(g_want[n]).max())
+        np.testing.assert_allclose(tmod.to_numpy(grads[n]), g_want[n], rtol=2e-2,
+                                   atol=2e-2 * scale, err_msg=n)
 
 
 @pytest.mark.parametrize("n,rtol,atol", [(100, 1e-2, 1e-3), (500, 5e-2, 5e-3)])
