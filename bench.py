@@ -231,8 +231,15 @@ def run_ours(args, world, rank, local):
     with ClockSampler(local) as clocks:
         torch.cuda.synchronize()
         barrier(world)
+        align = torch.zeros(1, device=f"cuda:{local}") if world > 1 else None
         for i in range(args.steps):
             L.call("mgx_fill", flush.data_ptr(), flush.numel(), float(i), eng.stream_handle)
+            if align is not None:
+                # untimed: re-align the ranks on-device after their independent
+                # L2 flushes, so the step's in-kernel barrier does not charge
+                # flush skew to the timed region
+                with torch.cuda.stream(eng.stream):
+                    torch.distributed.all_reduce(align)
             starts[i].record(eng.stream)
             step.replay()
             ends[i].record(eng.stream)
