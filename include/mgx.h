@@ -121,7 +121,7 @@ int mgx_softmax_backward(const float* p, const float* label, float* g, int64_t B
  * A[M,K] . B[N,K]^T (+bias) then act, A/B bf16 K-major ("TN"), fp32
  * accumulation in TMEM via tcgen05.mma, operands by TMA.  Replaces the
  * reference's FC forward contraction (ops.py:102-106) for the large FC
- * layers of configs 3-5.  K, lda, ldb multiples of 8; 16-byte aligned. */
+ * layers of configs 3-5.  lda, ldb multiples of 8; 16-byte aligned. */
 int mgx_gemm_bf16_tc(const void* A, int64_t lda, const void* B, int64_t ldb,
                      const float* bias, float* C, int64_t ldc,
                      int64_t M, int64_t N, int64_t K, int act, uintptr_t stream);
@@ -132,6 +132,53 @@ int mgx_cast_f32_bf16(const float* x, void* y, int64_t n, uintptr_t stream);
  * (the K padding of a tensor-core operand). */
 int mgx_cast_bf16_2d(const float* x, int64_t R, int64_t C, int64_t ldi, void* y,
                      int64_t rows, int64_t ldo, int transpose, uintptr_t stream);
+
+/* General tensor-core GEMM: C[M,N] = sum_k A(m,k) B(n,k) (+bias[n]) then
+ * act.  a_mn == 0: A[m*lda + k] (K-major), else A[k*lda + m] (MN-major);
+ * same for B.  splits: K split count (0 = auto when a workspace is given,
+ * 1 = none); partial tiles go to workspace (splits*M*N floats) and are
+ * summed in ascending split order (deterministic).  lda/ldb multiples of 8. */
+int mgx_gemm_bf16_tc_ex(const void* A, int64_t lda, int a_mn, const void* B, int64_t ldb,
+                        int b_mn, const float* bias, float* C, int64_t ldc, int64_t M,
+                        int64_t N, int64_t K, int act, int splits, float* workspace,
+                        uintptr_t stream);
+/* Workspace (floats) the auto split-K choice needs for an M x N x K GEMM. */
+int mgx_gemm_splitk_workspace(int64_t M, int64_t N, int64_t K, int64_t* out_floats);
+
+/* ------------------------------------------------ convolution-net kernels
+ * geom = int64[7] {B, H, W, C, kh<<16|kw, sh<<16|sw, ph<<16|pw}. */
+/* col[m, k] (bf16, row stride ldk % 8 == 0) = x(NHWC) at tap k = (i, j, c) of
+ * output pixel m; zero in the padding and for k >= kh*kw*C. */
+int mgx_im2col_bf16(const float* x, void* col, const int64_t* geom, int64_t ldk, uintptr_t stream);
+/* dx(NHWC) = adjoint of im2col applied to dcol (fp32, row stride ldk). */
+int mgx_col2im(const float* dcol, int64_t ldk, float* dx, const int64_t* geom, uintptr_t stream);
+/* fp64 workspace bytes for the per-channel reductions of an M x C matrix. */
+int mgx_reduce_workspace_bytes(int64_t M, int64_t C, int64_t* out);
+/* BatchNorm (MXNet semantics, axis = channels): stats = [mean C | rstd C]
+ * from the batch (biased variance) with moving-average update, or from the
+ * moving averages when use_global. */
+int mgx_bn_stats(const float* x, int64_t M, int64_t C, void* ws, float* stats, float* moving_mean,
+                 float* moving_var, float eps, float momentum, int use_global, uintptr_t stream);
+/* y = act((x - mean) * rstd * gamma + beta); gamma NULL = fix_gamma (1). */
+int mgx_bn_apply(const float* x, const float* stats, const float* gamma, const float* beta,
+                 float* y, int64_t M, int64_t C, int act, uintptr_t stream);
+/* sums = [sum dy | sum dy*xhat] per channel (dbeta, dgamma). */
+int mgx_bn_bwd_reduce(const float* dy, const float* x, const float* stats, int64_t M, int64_t C,
+                      void* ws, float* sums, uintptr_t stream);
+/* dx = gamma * rstd * (dy - (sum dy + xhat * sum dy*xhat) / M). */
+int mgx_bn_bwd_dx(const float* dy, const float* x, const float* stats, const float* sums,
+                  const float* gamma, float* dx, int64_t M, int64_t C, uintptr_t stream);
+/* out[c] = sum over rows of x[r, c] (conv bias gradient). */
+int mgx_colsum(const float* x, int64_t M, int64_t C, void* ws, float* out, uintptr_t stream);
+/* Pooling, NHWC.  type 0 max (padding ignored), 1 avg (count_include_pad);
+ * full != 0: 'full' convention (output size rounded up). */
+int mgx_pool_forward(const float* x, float* y, const int64_t* geom, int full, int type,
+                     uintptr_t stream);
+int mgx_pool_backward(const float* x, const float* y, const float* dy, float* dx,
+                      const int64_t* geom, int full, int type, uintptr_t stream);
+/* dst[r, doff + c] = src[r, soff + c] for r < rows, c < cols (Concat). */
+int mgx_chan_copy(const float* src, int64_t lds, int64_t soff, float* dst, int64_t ldd,
+                  int64_t doff, int64_t rows, int64_t cols, uintptr_t stream);
 
 /* Momentum SGD, tensor path (optim.py:39-50): 5 separately rounded steps. */
 int mgx_sgd_step(float* w, const float* g, float* v, int64_t n,
@@ -186,6 +233,25 @@ typedef struct mgx_instr {
 #define MGX_OP_CAST_BF16 13   /* ptr0=x(f32) ptr1=y(bf16) dims=R,C,ldi,rows,ldo,T */
 #define MGX_OP_GEMM_TC 14     /* ptr0=A ptr1=B ptr2=bias ptr3=C act (bf16 TN)     */
                               /* dims=M,N,K,lda,ldb,ldc                           */
+
+/* Convolution-net instructions (configs 3-5; no reference oracle: MXNet
+ * semantics, NHWC).  "geom" = dims[0..6] = B, H, W, C, kh<<16|kw, sh<<16|sw,
+ * ph<<16|pw (input extent and window). */
+#define MGX_OP_IM2COL 15      /* ptr0=x ptr1=col(bf16) dims=geom,ldk               */
+#define MGX_OP_COL2IM 16      /* ptr0=dcol ptr1=dx dims=geom,ldk                   */
+#define MGX_OP_BN_STATS 17    /* ptr0=x ptr1=ws ptr2=stats ptr3=mmean ptr4=mvar    */
+                              /* dims=M,C,use_global fattr=eps,momentum            */
+#define MGX_OP_BN_APPLY 18    /* ptr0=x ptr1=stats ptr2=gamma ptr3=beta ptr4=y     */
+                              /* dims=M,C act                                      */
+#define MGX_OP_BN_BWD_REDUCE 19 /* ptr0=dy ptr1=x ptr2=stats ptr3=ws ptr4=sums dims=M,C */
+#define MGX_OP_BN_BWD_DX 20   /* ptr0=dy ptr1=x ptr2=stats ptr3=sums ptr4=gamma    */
+                              /* ptr5=dx dims=M,C                                  */
+#define MGX_OP_POOL_FWD 21    /* ptr0=x ptr1=y dims=geom,full act=type(0 max 1 avg) */
+#define MGX_OP_POOL_BWD 22    /* ptr0=x ptr1=y ptr2=dy ptr3=dx dims=geom,full act  */
+#define MGX_OP_CHAN_COPY 23   /* ptr0=src ptr1=dst dims=rows,cols,lds,soff,ldd,doff */
+#define MGX_OP_COLSUM 24      /* ptr0=x ptr1=ws ptr2=out dims=M,C                  */
+#define MGX_OP_GEMM_TC_EX 25  /* ptr0=A ptr1=B ptr2=bias ptr3=C ptr4=workspace act */
+                              /* dims=M,N,K,lda,ldb,ldc,(a_mn|b_mn<<1),splits      */
 
 /* Run instructions eagerly, in order, on stream (no program object). */
 int mgx_instr_run(const mgx_instr* instrs, int32_t count, uintptr_t stream);

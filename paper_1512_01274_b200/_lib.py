@@ -28,6 +28,8 @@ ACT_CODES = {"relu": 1, "sigmoid": 2, "tanh": 3}
 OP_FILL, OP_COPY, OP_EW, OP_SCALAR, OP_GEMM_PW, OP_GEMM_SEQ, OP_DW_DB = 1, 2, 3, 4, 5, 6, 7
 OP_ACT_FWD, OP_ACT_BWD, OP_SOFTMAX_FWD, OP_SOFTMAX_BWD, OP_AXPY = 8, 9, 10, 11, 12
 OP_CAST_BF16, OP_GEMM_TC = 13, 14
+OP_IM2COL, OP_COL2IM, OP_BN_STATS, OP_BN_APPLY, OP_BN_BWD_REDUCE, OP_BN_BWD_DX = 15, 16, 17, 18, 19, 20
+OP_POOL_FWD, OP_POOL_BWD, OP_CHAN_COPY, OP_COLSUM, OP_GEMM_TC_EX = 21, 22, 23, 24, 25
 
 KV_ADD, KV_SGD, KV_AGG = 0, 1, 2
 KV_MAX_SEGS = 256
@@ -128,6 +130,24 @@ _SIGNATURES = {
     "mgx_kv_round": ([ctypes.POINTER(KvRoundArgs), c_uptr], ctypes.c_int),
     "mgx_prog_error": ([ctypes.POINTER(c_u32)], ctypes.c_int),
     "mgx_prog_time_levels": ([c_u64, c_i32, c_i32, c_uptr, c_vp], ctypes.c_int),
+    "mgx_gemm_bf16_tc_ex": ([c_vp, c_i64, ctypes.c_int, c_vp, c_i64, ctypes.c_int, c_vp, c_vp,
+                             c_i64, c_i64, c_i64, c_i64, ctypes.c_int, ctypes.c_int, c_vp, c_uptr],
+                            ctypes.c_int),
+    "mgx_gemm_splitk_workspace": ([c_i64, c_i64, c_i64, ctypes.POINTER(c_i64)], ctypes.c_int),
+    "mgx_im2col_bf16": ([c_vp, c_vp, c_vp, c_i64, c_uptr], ctypes.c_int),
+    "mgx_col2im": ([c_vp, c_i64, c_vp, c_vp, c_uptr], ctypes.c_int),
+    "mgx_reduce_workspace_bytes": ([c_i64, c_i64, ctypes.POINTER(c_i64)], ctypes.c_int),
+    "mgx_bn_stats": ([c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_f32, c_f32, ctypes.c_int,
+                      c_uptr], ctypes.c_int),
+    "mgx_bn_apply": ([c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, ctypes.c_int, c_uptr],
+                     ctypes.c_int),
+    "mgx_bn_bwd_reduce": ([c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_uptr], ctypes.c_int),
+    "mgx_bn_bwd_dx": ([c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_uptr], ctypes.c_int),
+    "mgx_colsum": ([c_vp, c_i64, c_i64, c_vp, c_vp, c_uptr], ctypes.c_int),
+    "mgx_pool_forward": ([c_vp, c_vp, c_vp, ctypes.c_int, ctypes.c_int, c_uptr], ctypes.c_int),
+    "mgx_pool_backward": ([c_vp, c_vp, c_vp, c_vp, c_vp, ctypes.c_int, ctypes.c_int, c_uptr],
+                          ctypes.c_int),
+    "mgx_chan_copy": ([c_vp, c_i64, c_i64, c_vp, c_i64, c_i64, c_i64, c_i64, c_uptr], ctypes.c_int),
     "mgx_kv_max_grid": ([c_i32, c_i32, ctypes.POINTER(c_i32)], ctypes.c_int),
     "mgx_kv_config": ([c_i32, c_i32, ctypes.POINTER(c_i32), ctypes.POINTER(c_i32),
                        ctypes.POINTER(c_i32)], ctypes.c_int),

@@ -1,0 +1,434 @@
+"""Convolution-net operators: Convolution, Pooling, BatchNorm, Concat.
+
+The reference registers no such operators (ops.py:127-527),
+so these follow MXNet's operator semantics (arXiv 1512.01274 §2, the paper's
+Inception-BN/AlexNet experiments) behind the reference's plugin surface
+(``OperatorDef``, ops.py:23-41): shape inference, ``forward``/``backward``,
+``backward_uses`` roles, plus native lowerings to ``mgx_instr`` records.
+
+Layout is channels-last (MXNet's ``layout='NHWC'``): data (B, H, W, C),
+convolution weight (num_filter, kh, kw, C), per-channel parameters (C,).
+Every 4-D activation is therefore an [B*H*W, C] row-major matrix, which is
+what the tensor-core GEMMs and the per-channel reductions want.
+
+Convolutions always run on the tcgen05 tensor cores with bf16 operand copies
+and fp32 accumulation (tolerance path; there is no exact-order reference to
+match).  The bf16 copies a backward pass needs (im2col of the input, the
+weight, the output gradient) are made once per step and shared between the
+forward and the sibling backward nodes through the lowering context memo.
+"""
+
+from __future__ import annotations
+
+from math import prod
+from typing import Optional
+
+from . import _lib as L
+from .errors import ArgumentError, InferenceError
+from .ops import OperatorDef, View, _fill, _native_backward, _native_forward, _need, current_ctx
+from .ops import instr, register
+
+
+def _pair(v, what: str) -> tuple:
+    if isinstance(v, int):
+        return (v, v)
+    if isinstance(v, (tuple, list)) and len(v) == 2 and all(isinstance(x, int) for x in v):
+        return (int(v[0]), int(v[1]))
+    raise InferenceError(f"{what} must be an int or a pair of ints, got {v!r}")
+
+
+def _pad8(n: int) -> int:
+    return -(-int(n) // 8) * 8
+
+
+def _check_layout(attrs, op):
+    lay = attrs.get("layout", "NHWC")
+    if lay != "NHWC":
+        raise InferenceError(f"{op}: only layout='NHWC' is implemented (channels-last), got {lay!r}")
+
+
+def _geom(shape, kernel, stride, pad) -> list:
+    b, h, w, c = shape
+    return [b, h, w, c, (kernel[0] << 16) | kernel[1], (stride[0] << 16) | stride[1],
+            (pad[0] << 16) | pad[1]]
+
+
+_PAIR = ((int, tuple, list), False)
+
+# ------------------------------------------------------------- Convolution
+
+
+def _conv_params(attrs):
+    k = _pair(attrs["kernel"], "kernel")
+    s = _pair(attrs.get("stride", 1), "stride")
+    p = _pair(attrs.get("pad", 0), "pad")
+    if attrs.get("num_group", 1) != 1:
+        raise InferenceError("Convolution: num_group != 1 is not implemented")
+    if _pair(attrs.get("dilate", 1), "dilate") != (1, 1):
+        raise InferenceError("Convolution: dilation is not implemented")
+    return k, s, p
+
+
+def _conv_out(h, w, k, s, p):
+    ho, wo = (h + 2 * p[0] - k[0]) // s[0] + 1, (w + 2 * p[1] - k[1]) // s[1] + 1
+    if ho <= 0 or wo <= 0:
+        raise InferenceError(f"Convolution: window {k} larger than padded input {(h, w)}")
+    return ho, wo
+
+
+def _conv_infer(shapes, attrs):
+    _check_layout(attrs, "Convolution")
+    data = _need(shapes[0], "Convolution", "data")
+    if len(data) != 4:
+        raise InferenceError("Convolution: data must be (batch, height, width, channels)")
+    b, h, w, c = data
+    k, s, p = _conv_params(attrs)
+    f = attrs["num_filter"]
+    ho, wo = _conv_out(h, w, k, s, p)
+    filled = [tuple(data), _fill(shapes[1], (f, k[0], k[1], c), "weight")]
+    if not attrs.get("no_bias", False):
+        filled.append(_fill(shapes[2], (f,), "bias"))
+    return filled, [(b, ho, wo, f)]
+
+
+def _conv_inputs(attrs):
+    return ("data", "weight") if attrs.get("no_bias", False) else ("data", "weight", "bias")
+
+
+def _cast_rows(src: View, rows: int, cols: int, dst: int, ld: int):
+    return instr(L.OP_CAST_BF16, [src.ptr, dst], [rows, cols, cols, rows, ld, 0])
+
+
+def _gemm(a: int, lda: int, a_mn: bool, b: int, ldb: int, b_mn: bool, c: int, ldc: int,
+          m: int, n: int, k: int, bias: Optional[int] = None, act: int = 0, splits: int = 1,
+          ws: Optional[int] = None):
+    flags = (1 if a_mn else 0) | (2 if b_mn else 0)
+    return instr(L.OP_GEMM_TC_EX, [a, b, bias, c, ws], [m, n, k, lda, ldb, ldc, flags, splits],
+                 act=act)
+
+
+def _splitk_ws(m: int, n: int, k: int) -> int:
+    import ctypes
+    out = ctypes.c_int64()
+    L.call("mgx_gemm_splitk_workspace", m, n, k, ctypes.byref(out))
+    return out.value
+
+
+def _conv_operands(x: View, w: View, attrs, ctx, code: list):
+    """bf16 operand copies shared by the forward and the backward of one
+    convolution: col = im2col(x) [M, ldk], wb = w [F, ldk].  Emitted once
+    per step (memo on the source nodes)."""
+    k, s, p = _conv_params(attrs)
+    b, h, wd, c = x.shape
+    ho, wo = _conv_out(h, wd, k, s, p)
+    m, kk = b * ho * wo, k[0] * k[1] * c
+    ldk = _pad8(kk)
+    f = w.shape[0]
+    xn, wn = ctx.input_node("in0"), ctx.input_node("in1")
+    key_c = ("col", id(xn), x.ptr, tuple(k), tuple(s), tuple(p))
+    col = ctx.memo.get(key_c)
+    if col is None:
+        col = ctx.persistent(2 * m * ldk)
+        ctx.memo[key_c] = col
+        code.append(instr(L.OP_IM2COL, [x.ptr, col], _geom(x.shape, k, s, p) + [ldk]))
+    key_w = ("wb", id(wn), w.ptr)
+    wb = ctx.memo.get(key_w)
+    if wb is None:
+        wb = ctx.persistent(2 * f * ldk)
+        ctx.memo[key_w] = wb
+        code.append(_cast_rows(w, f, kk, wb, ldk))
+    return col, wb, (m, kk, ldk, f, k, s, p, ho, wo)
+
+
+def _conv_lower_fwd(ins, out, attrs):
+    ctx = current_ctx()
+    code = []
+    col, wb, (m, kk, ldk, f, *_r) = _conv_operands(ins[0], ins[1], attrs, ctx, code)
+    bias = ins[2].ptr if len(ins) > 2 else None
+    code.append(_gemm(col, ldk, False, wb, ldk, False, out.ptr, f, m, f, kk, bias=bias))
+    return code
+
+
+def _conv_dy(og: View, f: int, ctx, code: list):
+    m = prod(og.shape[:-1])
+    ldf = _pad8(f)
+    key = ("dyb", id(ctx.input_node("og")), og.ptr)
+    dyb = ctx.memo.get(key)
+    if dyb is None:
+        dyb = ctx.persistent(2 * m * ldf)
+        ctx.memo[key] = dyb
+        code.append(_cast_rows(og, m, f, dyb, ldf))
+    return dyb, ldf
+
+
+def _conv_lower_bwd(slot, env, out, attrs):
+    ctx = current_ctx()
+    og = env["og"]
+    code = []
+    if slot == 2:
+        m, f = prod(og.shape[:-1]), og.shape[-1]
+        ws = ctx.scratch(_reduce_ws(m, f))
+        return [instr(L.OP_COLSUM, [og.ptr, ws, out.ptr], [m, f])]
+    x, w = env["in0"], env["in1"]
+    col, wb, (m, kk, ldk, f, k, s, p, ho, wo) = _conv_operands(x, w, attrs, ctx, code)
+    dyb, ldf = _conv_dy(og, f, ctx, code)
+    if slot == 1:
+        # dW[f, kk] = sum_m dY[m, f] col[m, kk]: both operands MN-major, split-K
+        nws = _splitk_ws(f, kk, m)
+        ws = ctx.scratch(4 * nws) if nws else None
+        code.append(_gemm(dyb, ldf, True, col, ldk, True, out.ptr, kk, f, kk, m,
+                          splits=0 if ws else 1, ws=ws))
+        return code
+    # dX: dcol[m, kk] = dY[m, f] . W[f, kk] (W MN-major), then col2im
+    c = x.shape[3]
+    if k == (1, 1) and s == (1, 1) and p == (0, 0):
+        code.append(_gemm(dyb, ldf, False, wb, ldk, True, out.ptr, c, m, c, f))
+        return code
+    dcol = ctx.scratch(4 * m * kk)
+    code.append(_gemm(dyb, ldf, False, wb, ldk, True, dcol, kk, m, kk, f))
+    code.append(instr(L.OP_COL2IM, [dcol, out.ptr], _geom(x.shape, k, s, p) + [kk]))
+    return code
+
+
+def _conv_uses(slot, nin):
+    return {0: (("og", "in0", "in1"), "in0"),
+            1: (("og", "in0", "in1"), "in1"),
+            2: (("og", "in2"), "in2")}[slot]
+
+
+register(OperatorDef(
+    name="Convolution", prefix="conv", input_names=("data", "weight", "bias"),
+    attr_schema={"kernel": ((int, tuple, list), True), "num_filter": (int, True),
+                 "stride": _PAIR, "pad": _PAIR, "dilate": _PAIR, "no_bias": (bool, False),
+                 "num_group": (int, False), "layout": (str, False), "workspace": (int, False)},
+    infer_shape=_conv_infer, forward=_native_forward(_conv_lower_fwd),
+    backward=_native_backward("Convolution"), backward_uses=_conv_uses,
+    lower_forward=_conv_lower_fwd, lower_backward=_conv_lower_bwd, inputs_for=_conv_inputs,
+))
+
+
+# ---------------------------------------------------------------- BatchNorm
+# MXNet BatchNorm over the channel axis: training normalises with the batch
+# mean and biased variance and updates moving_mean/moving_var with
+# `momentum`; inference (no gradients requested, or use_global_stats) uses
+# the moving averages.  fix_gamma=True (MXNet's default) pins gamma to 1 and
+# its gradient to 0.  Inputs 3/4 are the auxiliary moving statistics.
+
+def _reduce_ws(m: int, c: int) -> int:
+    import ctypes
+    out = ctypes.c_int64()
+    L.call("mgx_reduce_workspace_bytes", max(m, 1), max(c, 1), ctypes.byref(out))
+    return out.value
+
+
+def _bn_infer(shapes, attrs):
+    data = _need(shapes[0], "BatchNorm", "data")
+    if len(data) < 2:
+        raise InferenceError("BatchNorm: data must have rank >= 2")
+    c = data[-1]
+    return ([tuple(data)] + [_fill(shapes[i], (c,), n) for i, n in
+                             ((1, "gamma"), (2, "beta"), (3, "moving_mean"), (4, "moving_var"))],
+            [tuple(data)])
+
+
+def _bn_stats(x: View, attrs, ctx, code: list, update: bool, mm=None, mv=None) -> int:
+    m, c = prod(x.shape[:-1]), x.shape[-1]
+    eps = float(attrs.get("eps", 1e-3))
+    key = ("bnstats", id(ctx.input_node("in0")), x.ptr, eps)
+    st = ctx.memo.get(key)
+    if st is None:
+        st = ctx.persistent(8 * c)
+        ctx.memo[key] = st
+        use_global = (not ctx.training) or bool(attrs.get("use_global_stats", False))
+        ws = ctx.scratch(_reduce_ws(m, c))
+        code.append(instr(L.OP_BN_STATS,
+                          [x.ptr, ws, st, mm.ptr if (update or use_global) and mm else None,
+                           mv.ptr if (update or use_global) and mv else None],
+                          [m, c, 1 if use_global else 0],
+                          [eps, float(attrs.get("momentum", 0.9))]))
+    return st
+
+
+def bn_forward_instrs(ins, out: View, attrs, act: int = 0) -> list:
+    ctx = current_ctx()
+    x = ins[0]
+    m, c = prod(x.shape[:-1]), x.shape[-1]
+    code = []
+    st = _bn_stats(x, attrs, ctx, code, update=True, mm=ins[3], mv=ins[4])
+    gamma = None if attrs.get("fix_gamma", True) else ins[1].ptr
+    code.append(instr(L.OP_BN_APPLY, [x.ptr, st, gamma, ins[2].ptr, out.ptr], [m, c], act=act))
+    return code
+
+
+def _bn_lower_fwd(ins, out, attrs):
+    return bn_forward_instrs(ins, out, attrs)
+
+
+def _bn_lower_bwd(slot, env, out, attrs):
+    ctx = current_ctx()
+    if slot >= 3:
+        return [instr(L.OP_FILL, [out.ptr], [out.size], [0.0])]
+    og, x = env["og"], env["in0"]
+    m, c = prod(x.shape[:-1]), x.shape[-1]
+    code = []
+    st = _bn_stats(x, attrs, ctx, code, update=False)
+    key = ("bnsums", id(ctx.input_node("og")), id(ctx.input_node("in0")), og.ptr, x.ptr)
+    sums = ctx.memo.get(key)
+    if sums is None:
+        sums = ctx.persistent(8 * c)
+        ctx.memo[key] = sums
+        ws = ctx.scratch(_reduce_ws(m, c))
+        code.append(instr(L.OP_BN_BWD_REDUCE, [og.ptr, x.ptr, st, ws, sums], [m, c]))
+    fix = attrs.get("fix_gamma", True)
+    if slot == 0:
+        gamma = None if fix else env["in1"].ptr
+        code.append(instr(L.OP_BN_BWD_DX, [og.ptr, x.ptr, st, sums, gamma, out.ptr], [m, c]))
+    elif slot == 1:
+        code.append(instr(L.OP_FILL, [out.ptr], [c], [0.0]) if fix else
+                    instr(L.OP_COPY, [sums + 4 * c, out.ptr], [c]))
+    else:
+        code.append(instr(L.OP_COPY, [sums, out.ptr], [c]))
+    return code
+
+
+def _bn_uses(slot, nin):
+    if slot >= 3:
+        return ((f"in{slot}",), f"in{slot}")
+    return (("og", "in0", "in1", "in2"), f"in{slot}")
+
+
+register(OperatorDef(
+    name="BatchNorm", prefix="bn",
+    input_names=("data", "gamma", "beta", "moving_mean", "moving_var"),
+    attr_schema={"eps": ((int, float), False), "momentum": ((int, float), False),
+                 "fix_gamma": (bool, False), "use_global_stats": (bool, False),
+                 "axis": (int, False), "output_mean_var": (bool, False)},
+    infer_shape=_bn_infer, forward=_native_forward(_bn_lower_fwd),
+    backward=_native_backward("BatchNorm"), backward_uses=_bn_uses,
+    lower_forward=_bn_lower_fwd, lower_backward=_bn_lower_bwd,
+))
+
+AUX_SUFFIXES = ("_moving_mean", "_moving_var")
+
+
+# ------------------------------------------------------------------ Pooling
+
+_POOL_TYPES = {"max": 0, "avg": 1}
+
+
+def _pool_params(attrs, shape):
+    _check_layout(attrs, "Pooling")
+    if attrs.get("pool_type", "max") not in _POOL_TYPES:
+        raise InferenceError(f"Pooling: pool_type must be max or avg, got {attrs.get('pool_type')!r}")
+    conv = attrs.get("pooling_convention", "valid")
+    if conv not in ("valid", "full"):
+        raise InferenceError(f"Pooling: unknown pooling_convention {conv!r}")
+    if attrs.get("global_pool", False):
+        return (shape[1], shape[2]), (1, 1), (0, 0), False
+    k = _pair(attrs["kernel"], "kernel")
+    s = _pair(attrs.get("stride", 1), "stride")
+    p = _pair(attrs.get("pad", 0), "pad")
+    return k, s, p, conv == "full"
+
+
+def _pool_out(h, w, k, s, p, full):
+    def one(n, kk, ss, pp):
+        span = n + 2 * pp - kk
+        return (-(-span // ss) if full else span // ss) + 1
+    return one(h, k[0], s[0], p[0]), one(w, k[1], s[1], p[1])
+
+
+def _pool_infer(shapes, attrs):
+    data = _need(shapes[0], "Pooling", "data")
+    if len(data) != 4:
+        raise InferenceError("Pooling: data must be (batch, height, width, channels)")
+    if not attrs.get("global_pool", False) and "kernel" not in attrs:
+        raise InferenceError("Pooling: kernel is required unless global_pool")
+    k, s, p, full = _pool_params(attrs, data)
+    ho, wo = _pool_out(data[1], data[2], k, s, p, full)
+    if ho <= 0 or wo <= 0:
+        raise InferenceError("Pooling: window larger than the padded input")
+    return [tuple(data)], [(data[0], ho, wo, data[3])]
+
+
+def _pool_lower_fwd(ins, out, attrs):
+    x = ins[0]
+    k, s, p, full = _pool_params(attrs, x.shape)
+    return [instr(L.OP_POOL_FWD, [x.ptr, out.ptr], _geom(x.shape, k, s, p) + [int(full)],
+                  act=_POOL_TYPES[attrs.get("pool_type", "max")])]
+
+
+def _pool_lower_bwd(slot, env, out, attrs):
+    x = env["in0"]
+    k, s, p, full = _pool_params(attrs, x.shape)
+    return [instr(L.OP_POOL_BWD, [x.ptr, env["out"].ptr, env["og"].ptr, out.ptr],
+                  _geom(x.shape, k, s, p) + [int(full)],
+                  act=_POOL_TYPES[attrs.get("pool_type", "max")])]
+
+
+register(OperatorDef(
+    name="Pooling", prefix="pool", input_names=("data",),
+    attr_schema={"kernel": ((int, tuple, list), False), "pool_type": (str, False),
+                 "stride": _PAIR, "pad": _PAIR, "global_pool": (bool, False),
+                 "pooling_convention": (str, False), "layout": (str, False)},
+    infer_shape=_pool_infer, forward=_native_forward(_pool_lower_fwd),
+    backward=_native_backward("Pooling"),
+    backward_uses=lambda slot, nin: (("og", "in0", "out"), "in0"),
+    lower_forward=_pool_lower_fwd, lower_backward=_pool_lower_bwd,
+))
+
+
+# ------------------------------------------------------------------- Concat
+# Concatenation along the channel (last) axis: one channel-offset copy per
+# input; the backward slices the output gradient.
+
+def _concat_axis(attrs, rank):
+    d = attrs.get("dim", -1)
+    if d not in (-1, rank - 1):
+        raise InferenceError(f"Concat: only the channel (last) axis is implemented, got dim={d}")
+
+
+def _concat_infer(shapes, attrs):
+    known = [s for s in shapes if s is not None]
+    if len(known) != len(shapes) or not known:
+        raise InferenceError("Concat: every input shape must be known")
+    rank = len(known[0])
+    _concat_axis(attrs, rank)
+    lead = tuple(known[0][:-1])
+    for s in known:
+        if len(s) != rank or tuple(s[:-1]) != lead:
+            raise InferenceError(f"Concat: incompatible shapes {known}")
+    return [tuple(s) for s in shapes], [lead + (sum(s[-1] for s in shapes),)]
+
+
+def _concat_lower_fwd(ins, out, attrs):
+    rows, tot = prod(out.shape[:-1]), out.shape[-1]
+    code, off = [], 0
+    for x in ins:
+        c = x.shape[-1]
+        code.append(instr(L.OP_CHAN_COPY, [x.ptr, out.ptr], [rows, c, c, 0, tot, off]))
+        off += c
+    return code
+
+
+def _concat_lower_bwd(slot, env, out, attrs):
+    og = env["og"]
+    rows, tot = prod(og.shape[:-1]), og.shape[-1]
+    off = sum(env[f"in{i}"].shape[-1] for i in range(slot))
+    c = out.shape[-1]
+    return [instr(L.OP_CHAN_COPY, [og.ptr, out.ptr], [rows, c, tot, off, c, 0])]
+
+
+register(OperatorDef(
+    name="Concat", prefix="concat", input_names=(),
+    attr_schema={"dim": (int, False), "num_args": (int, False)},
+    infer_shape=_concat_infer, forward=_native_forward(_concat_lower_fwd),
+    backward=_native_backward("Concat"), variadic=True,
+    backward_uses=lambda slot, nin: (("og",) + tuple(f"in{i}" for i in range(nin)), f"in{slot}"),
+    lower_forward=_concat_lower_fwd, lower_backward=_concat_lower_bwd,
+))
+
+
+def validate_concat_inputs(n: int) -> None:
+    if n < 1:
+        raise ArgumentError("Concat needs at least one input")

@@ -1,0 +1,578 @@
+// Convolution-net kernels (configs 3-5: LeNet, AlexNet-style, Inception-BN).
+//
+// The reference has no Convolution/Pooling/BatchNorm/Concat (SURVEY.md §0
+// fact 7); these follow MXNet's operator semantics (arXiv
+// 1512.01274 §2) in the channels-last layout: activations are NHWC fp32
+// [B*H*W rows, C contiguous], convolution weights OHWI [Cout, kh*kw*Cin].
+// Convolutions run as tcgen05 GEMMs (tc_gemm.cu) on bf16 operand copies:
+//
+//   forward  out[M=B*Ho*Wo, Cout] = col[M, K] . W[Cout, K]^T      (both K-major)
+//   dgrad    dcol[M, K]           = dY[M, Cout] . W[Cout, K]        (W MN-major)
+//   wgrad    dW[Cout, K]          = dY[M, Cout]^T . col[M, K]       (both MN-major)
+//
+// with K = kh*kw*Cin in (kh, kw, c) order.  The kernels here produce the
+// operands (im2col + bf16 cast), scatter dcol back (col2im, a gather with a
+// fixed tap order, no atomics), and do the bandwidth-bound work: BatchNorm
+// statistics/apply/backward, pooling, channel-offset copies (Concat), and
+// per-channel sums (conv bias gradient).  Every reduction has a fixed order
+// (row chunks -> fixed-order merge), so results are run-to-run
+// deterministic.
+
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+
+namespace mgx {
+namespace conv {
+
+struct Geom {
+  int B, H, W, C, kh, kw, sh, sw, ph, pw, Ho, Wo;
+};
+
+// dims: B, H, W, C, (kh<<16|kw), (sh<<16|sw), (ph<<16|pw), then op-specific
+__host__ __device__ inline Geom decode(const int64_t* d, bool full = false) {
+  Geom g;
+  g.B = static_cast<int>(d[0]);
+  g.H = static_cast<int>(d[1]);
+  g.W = static_cast<int>(d[2]);
+  g.C = static_cast<int>(d[3]);
+  g.kh = static_cast<int>(d[4] >> 16);
+  g.kw = static_cast<int>(d[4] & 0xFFFF);
+  g.sh = static_cast<int>(d[5] >> 16);
+  g.sw = static_cast<int>(d[5] & 0xFFFF);
+  g.ph = static_cast<int>(d[6] >> 16);
+  g.pw = static_cast<int>(d[6] & 0xFFFF);
+  if (!full) {
+    g.Ho = (g.H + 2 * g.ph - g.kh) / g.sh + 1;
+    g.Wo = (g.W + 2 * g.pw - g.kw) / g.sw + 1;
+  } else {
+    g.Ho = (g.H + 2 * g.ph - g.kh + g.sh - 1) / g.sh + 1;
+    g.Wo = (g.W + 2 * g.pw - g.kw + g.sw - 1) / g.sw + 1;
+  }
+  return g;
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// col[m, k] (bf16, row stride ldk >= K, zero beyond K) = x at tap k of output
+// pixel m (zero in the padding).  8 consecutive k per thread (one 16-byte
+// store); when C % 8 == 0 they are 8 channels of one tap (two float4 loads).
+__global__ void im2col_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ col, Geom g,
+                              int64_t ldk) {
+  const int K = g.kh * g.kw * g.C;
+  const int64_t per_row = ldk / 8;
+  const int64_t M = int64_t(g.B) * g.Ho * g.Wo;
+  const int64_t total = M * per_row;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  const bool vec = (g.C % 8) == 0;
+  for (int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < total; idx += stride) {
+    const int64_t m = idx / per_row;
+    const int k0 = static_cast<int>(idx - m * per_row) * 8;
+    const int b = static_cast<int>(m / (g.Ho * g.Wo));
+    const int rem = static_cast<int>(m - int64_t(b) * g.Ho * g.Wo);
+    const int oh = rem / g.Wo, ow = rem - (rem / g.Wo) * g.Wo;
+    float v[8];
+    if (vec) {
+      if (k0 < K) {
+        const int tap = k0 / g.C, c0 = k0 - tap * g.C;
+        const int i = tap / g.kw, j = tap - (tap / g.kw) * g.kw;
+        const int h = oh * g.sh - g.ph + i, w = ow * g.sw - g.pw + j;
+        if (h >= 0 && h < g.H && w >= 0 && w < g.W) {
+          const float4* src =
+              reinterpret_cast<const float4*>(x + ((int64_t(b) * g.H + h) * g.W + w) * g.C + c0);
+          const float4 a = __ldg(src), c = __ldg(src + 1);
+          v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+          v[4] = c.x; v[5] = c.y; v[6] = c.z; v[7] = c.w;
+        } else {
+#pragma unroll
+          for (int t = 0; t < 8; ++t) v[t] = 0.0f;
+        }
+      } else {
+#pragma unroll
+        for (int t = 0; t < 8; ++t) v[t] = 0.0f;
+      }
+    } else {
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const int k = k0 + t;
+        float val = 0.0f;
+        if (k < K) {
+          const int tap = k / g.C, c = k - tap * g.C;
+          const int i = tap / g.kw, j = tap - (tap / g.kw) * g.kw;
+          const int h = oh * g.sh - g.ph + i, w = ow * g.sw - g.pw + j;
+          if (h >= 0 && h < g.H && w >= 0 && w < g.W)
+            val = __ldg(x + ((int64_t(b) * g.H + h) * g.W + w) * g.C + c);
+        }
+        v[t] = val;
+      }
+    }
+    uint4 o;
+    o.x = pack_bf16(v[0], v[1]);
+    o.y = pack_bf16(v[2], v[3]);
+    o.z = pack_bf16(v[4], v[5]);
+    o.w = pack_bf16(v[6], v[7]);
+    *reinterpret_cast<uint4*>(col + m * ldk + k0) = o;
+  }
+}
+
+// dx[b,h,w,c] = sum over taps (i, j) ascending of dcol[pixel(oh,ow), (i,j,c)]
+// for every output pixel whose window covers (h, w): the adjoint of im2col
+// as a gather (deterministic, no atomics).
+__global__ void col2im_kernel(const float* __restrict__ dcol, int64_t ldk, float* __restrict__ dx,
+                              Geom g) {
+  const int64_t total = int64_t(g.B) * g.H * g.W * g.C;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < total; idx += stride) {
+    const int c = static_cast<int>(idx % g.C);
+    int64_t p = idx / g.C;
+    const int w = static_cast<int>(p % g.W);
+    p /= g.W;
+    const int h = static_cast<int>(p % g.H);
+    const int b = static_cast<int>(p / g.H);
+    float acc = 0.0f;
+    for (int i = 0; i < g.kh; ++i) {
+      const int hn = h + g.ph - i;
+      if (hn < 0 || hn % g.sh) continue;
+      const int oh = hn / g.sh;
+      if (oh >= g.Ho) continue;
+      for (int j = 0; j < g.kw; ++j) {
+        const int wn = w + g.pw - j;
+        if (wn < 0 || wn % g.sw) continue;
+        const int ow = wn / g.sw;
+        if (ow >= g.Wo) continue;
+        const int64_t m = (int64_t(b) * g.Ho + oh) * g.Wo + ow;
+        acc = fadd(acc, __ldg(dcol + m * ldk + (i * g.kw + j) * g.C + c));
+      }
+    }
+    dx[idx] = acc;
+  }
+}
+
+// ------------------------------------------------------- column reductions
+// Per-channel sums over the M rows of an [M, C] matrix, in two fixed-order
+// stages: block z reduces rows [z*rpc, (z+1)*rpc) into ws[z][*] (fp64), then
+// one thread per channel merges the chunks in ascending z.
+//   MODE 0: (sum x, sum x^2)             BatchNorm statistics
+//   MODE 1: (sum dy, sum dy*xhat)         BatchNorm backward
+//   MODE 2: (sum x)                       conv bias gradient
+// xhat = (x - mean) * rstd with stats = [mean C | rstd C].
+
+constexpr int kRedThreads = 256;
+constexpr int kMaxChunks = 2 * kNumSMs;
+
+template <int MODE>
+__global__ void __launch_bounds__(kRedThreads)
+colreduce_partial_kernel(const float* __restrict__ a, const float* __restrict__ xs,
+                         const float* __restrict__ stats, int64_t M, int C, int64_t rpc,
+                         double* __restrict__ ws) {
+  extern __shared__ double red[];  // [rpp][2*C]
+  const int tpr = C < kRedThreads ? C : kRedThreads;  // threads per row
+  const int rpp = kRedThreads / tpr;                  // rows per pass
+  const int t = threadIdx.x;
+  const int r_in = t / tpr, c_in = t - (t / tpr) * tpr;
+  const int64_t r0 = int64_t(blockIdx.x) * rpc;
+  const int64_t r1 = min(M, r0 + rpc);
+  const int nchunk = gridDim.x;
+  for (int cb = 0; cb < C; cb += tpr) {
+    const int c = cb + c_in;
+    double s0 = 0.0, s1 = 0.0;
+    if (r_in < rpp && c < C) {
+      float mean = 0.0f, rstd = 0.0f;
+      if (MODE == 1) {
+        mean = __ldg(stats + c);
+        rstd = __ldg(stats + C + c);
+      }
+      for (int64_t r = r0 + r_in; r < r1; r += rpp) {
+        const float v = __ldg(a + r * C + c);
+        s0 += v;
+        if (MODE == 0) s1 += double(v) * double(v);
+        if (MODE == 1) s1 += double(v) * double((__ldg(xs + r * C + c) - mean) * rstd);
+      }
+    }
+    if (r_in < rpp) {
+      red[r_in * 2 * tpr + c_in] = s0;
+      red[r_in * 2 * tpr + tpr + c_in] = s1;
+    }
+    __syncthreads();
+    if (t < tpr && cb + t < C) {
+      double u0 = 0.0, u1 = 0.0;
+      for (int r = 0; r < rpp; ++r) {
+        u0 += red[r * 2 * tpr + t];
+        u1 += red[r * 2 * tpr + tpr + t];
+      }
+      ws[int64_t(blockIdx.x) * C + cb + t] = u0;
+      ws[int64_t(nchunk + blockIdx.x) * C + cb + t] = u1;
+    }
+    __syncthreads();
+  }
+}
+
+// MODE 0 finalize: stats = [mean | rstd] (batch statistics, biased variance
+// like MXNet), moving averages updated when given.
+// use_global: stats from the moving averages (inference).
+__global__ void bn_stats_finalize_kernel(const double* __restrict__ ws, int nchunk, int64_t M, int C,
+                                         float eps, float momentum, int use_global,
+                                         float* __restrict__ stats, float* __restrict__ mmean,
+                                         float* __restrict__ mvar) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  if (use_global) {
+    stats[c] = mmean[c];
+    stats[C + c] = static_cast<float>(1.0 / sqrt(double(mvar[c]) + double(eps)));
+    return;
+  }
+  double s = 0.0, q = 0.0;
+  for (int z = 0; z < nchunk; ++z) {
+    s += ws[int64_t(z) * C + c];
+    q += ws[int64_t(nchunk + z) * C + c];
+  }
+  const double mean = s / double(M);
+  double var = q / double(M) - mean * mean;
+  if (var < 0.0) var = 0.0;
+  stats[c] = static_cast<float>(mean);
+  stats[C + c] = static_cast<float>(1.0 / sqrt(var + double(eps)));
+  if (mmean) mmean[c] = static_cast<float>(double(mmean[c]) * momentum + mean * (1.0 - momentum));
+  if (mvar) mvar[c] = static_cast<float>(double(mvar[c]) * momentum + var * (1.0 - momentum));
+}
+
+// MODE 1/2 finalize: out[c] = sum0, out[C + c] = sum1 (MODE 1) as fp32
+__global__ void colsum_finalize_kernel(const double* __restrict__ ws, int nchunk, int C, int two,
+                                       float* __restrict__ out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  double s = 0.0, q = 0.0;
+  for (int z = 0; z < nchunk; ++z) {
+    s += ws[int64_t(z) * C + c];
+    if (two) q += ws[int64_t(nchunk + z) * C + c];
+  }
+  out[c] = static_cast<float>(s);
+  if (two) out[C + c] = static_cast<float>(q);
+}
+
+// y = (x - mean) * rstd * gamma + beta, then act; gamma == nullptr: fixed 1
+__global__ void bn_apply_kernel(const float* __restrict__ x, const float* __restrict__ stats,
+                                const float* __restrict__ gamma, const float* __restrict__ beta,
+                                float* __restrict__ y, int64_t M, int C, int act) {
+  const int64_t total = M * C;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  if ((C & 3) == 0) {
+    const int64_t t4 = total / 4;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < t4; i += stride) {
+      const int c = static_cast<int>((i * 4) % C);
+      float4 v = reinterpret_cast<const float4*>(x)[i];
+      float* pv = &v.x;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int cc = c + u;
+        const float g = gamma ? __ldg(gamma + cc) : 1.0f;
+        float r = (pv[u] - __ldg(stats + cc)) * __ldg(stats + C + cc) * g + __ldg(beta + cc);
+        pv[u] = act_forward(act, r);
+      }
+      reinterpret_cast<float4*>(y)[i] = v;
+    }
+  } else {
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
+      const int c = static_cast<int>(i % C);
+      const float g = gamma ? __ldg(gamma + c) : 1.0f;
+      y[i] = act_forward(act, (x[i] - __ldg(stats + c)) * __ldg(stats + C + c) * g + __ldg(beta + c));
+    }
+  }
+}
+
+// dx = gamma * rstd * (dy - (sum_dy + xhat * sum_dyxhat) / M)
+__global__ void bn_bwd_dx_kernel(const float* __restrict__ dy, const float* __restrict__ x,
+                                 const float* __restrict__ stats, const float* __restrict__ sums,
+                                 const float* __restrict__ gamma, float* __restrict__ dx, int64_t M,
+                                 int C) {
+  const int64_t total = M * C;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  const float invm = static_cast<float>(1.0 / double(M));
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
+    const int c = static_cast<int>(i % C);
+    const float rstd = __ldg(stats + C + c);
+    const float xhat = (x[i] - __ldg(stats + c)) * rstd;
+    const float g = gamma ? __ldg(gamma + c) : 1.0f;
+    dx[i] = g * rstd * (dy[i] - (__ldg(sums + c) + xhat * __ldg(sums + C + c)) * invm);
+  }
+}
+
+// ------------------------------------------------------------------ pooling
+// MXNet pooling semantics: max ignores padding; avg divides by the window
+// area clipped to the padded extent (count_include_pad); 'full' convention
+// rounds the output size up.
+
+__device__ __forceinline__ float pool_area(const Geom& g, int oh, int ow) {
+  const int hs = oh * g.sh - g.ph, ws = ow * g.sw - g.pw;
+  const int he = min(hs + g.kh, g.H + g.ph), we = min(ws + g.kw, g.W + g.pw);
+  return static_cast<float>((he - hs) * (we - ws));
+}
+
+__global__ void pool_fwd_kernel(const float* __restrict__ x, float* __restrict__ y, Geom g,
+                                int type) {
+  const int64_t total = int64_t(g.B) * g.Ho * g.Wo * g.C;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < total; idx += stride) {
+    const int c = static_cast<int>(idx % g.C);
+    int64_t p = idx / g.C;
+    const int ow = static_cast<int>(p % g.Wo);
+    p /= g.Wo;
+    const int oh = static_cast<int>(p % g.Ho);
+    const int b = static_cast<int>(p / g.Ho);
+    const int hs = oh * g.sh - g.ph, ws = ow * g.sw - g.pw;
+    const int h0 = max(hs, 0), w0 = max(ws, 0);
+    const int h1 = min(hs + g.kh, g.H), w1 = min(ws + g.kw, g.W);
+    float acc = type == 0 ? -INFINITY : 0.0f;
+    for (int h = h0; h < h1; ++h)
+      for (int w = w0; w < w1; ++w) {
+        const float v = __ldg(x + ((int64_t(b) * g.H + h) * g.W + w) * g.C + c);
+        acc = type == 0 ? (v > acc ? v : acc) : fadd(acc, v);
+      }
+    y[idx] = type == 0 ? acc : fdiv(acc, pool_area(g, oh, ow));
+  }
+}
+
+// dx gathered from every window covering the input position.  Max: the
+// gradient goes to the FIRST position (row-major window scan, strict >)
+// holding the window maximum, like MXNet's unpool; avg: dy / area.
+__global__ void pool_bwd_kernel(const float* __restrict__ x, const float* __restrict__ y,
+                                const float* __restrict__ dy, float* __restrict__ dx, Geom g,
+                                int type) {
+  const int64_t total = int64_t(g.B) * g.H * g.W * g.C;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < total; idx += stride) {
+    const int c = static_cast<int>(idx % g.C);
+    int64_t p = idx / g.C;
+    const int w = static_cast<int>(p % g.W);
+    p /= g.W;
+    const int h = static_cast<int>(p % g.H);
+    const int b = static_cast<int>(p / g.H);
+    const float xv = type == 0 ? x[idx] : 0.0f;
+    // output windows covering h: oh*sh - ph <= h < oh*sh - ph + kh
+    const int nh = h + g.ph - g.kh + 1, nw = w + g.pw - g.kw + 1;
+    const int oh_lo = nh <= 0 ? 0 : (nh + g.sh - 1) / g.sh;
+    const int oh_hi = min(g.Ho - 1, (h + g.ph) / g.sh);
+    const int ow_lo = nw <= 0 ? 0 : (nw + g.sw - 1) / g.sw;
+    const int ow_hi = min(g.Wo - 1, (w + g.pw) / g.sw);
+    float acc = 0.0f;
+    for (int oh = oh_lo; oh <= oh_hi; ++oh) {
+      const int hs = oh * g.sh - g.ph;
+      if (h < hs || h >= hs + g.kh) continue;
+      for (int ow = ow_lo; ow <= ow_hi; ++ow) {
+        const int ws = ow * g.sw - g.pw;
+        if (w < ws || w >= ws + g.kw) continue;
+        const int64_t o = ((int64_t(b) * g.Ho + oh) * g.Wo + ow) * g.C + c;
+        if (type == 0) {
+          const float yv = __ldg(y + o);
+          if (xv != yv) continue;
+          // first max: no earlier valid window position holds yv
+          bool first = true;
+          const int h0 = max(hs, 0), w0 = max(ws, 0), w1 = min(ws + g.kw, g.W);
+          for (int hh = h0; hh <= h && first; ++hh) {
+            const int wend = hh < h ? w1 : w;
+            for (int ww = w0; ww < wend; ++ww)
+              if (__ldg(x + ((int64_t(b) * g.H + hh) * g.W + ww) * g.C + c) == yv) {
+                first = false;
+                break;
+              }
+          }
+          if (first) acc = fadd(acc, __ldg(dy + o));
+        } else {
+          acc = fadd(acc, fdiv(__ldg(dy + o), pool_area(g, oh, ow)));
+        }
+      }
+    }
+    dx[idx] = acc;
+  }
+}
+
+// dst[r, doff + c] = src[r, soff + c] (Concat forward / backward slices)
+__global__ void chan_copy_kernel(const float* __restrict__ src, int64_t lds, int64_t soff,
+                                 float* __restrict__ dst, int64_t ldd, int64_t doff, int64_t rows,
+                                 int64_t cols) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  if (((cols | lds | soff | ldd | doff) & 3) == 0) {
+    const int64_t c4 = cols / 4, total = rows * c4;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
+      const int64_t r = i / c4, c = (i - r * c4) * 4;
+      *reinterpret_cast<float4*>(dst + r * ldd + doff + c) =
+          __ldg(reinterpret_cast<const float4*>(src + r * lds + soff + c));
+    }
+  } else {
+    const int64_t total = rows * cols;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
+      const int64_t r = i / cols, c = i - r * cols;
+      dst[r * ldd + doff + c] = src[r * lds + soff + c];
+    }
+  }
+}
+
+inline unsigned grid_for(int64_t n, int threads = 256, int64_t cap = int64_t(kNumSMs) * 16) {
+  int64_t b = ceil_div(n, threads);
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return static_cast<unsigned>(b);
+}
+
+// chunking of M rows for the column reductions
+inline void chunks_for(int64_t M, int64_t* rpc, int* nchunk) {
+  int64_t n = M < kMaxChunks ? M : kMaxChunks;
+  if (n < 1) n = 1;
+  *rpc = ceil_div(M, n);
+  *nchunk = static_cast<int>(ceil_div(M, *rpc));
+}
+
+template <int MODE>
+int launch_partial(const float* a, const float* xs, const float* stats, int64_t M, int C,
+                   double* ws, int* nchunk_out, cudaStream_t st) {
+  int64_t rpc;
+  int nchunk;
+  chunks_for(M, &rpc, &nchunk);
+  const int tpr = C < kRedThreads ? C : kRedThreads;
+  const int rpp = kRedThreads / tpr;
+  const size_t smem = size_t(rpp) * 2 * tpr * sizeof(double);
+  colreduce_partial_kernel<MODE><<<nchunk, kRedThreads, smem, st>>>(a, xs, stats, M, C, rpc, ws);
+  *nchunk_out = nchunk;
+  MGX_LAUNCHED();
+  return MGX_OK;
+}
+
+}  // namespace conv
+}  // namespace mgx
+
+using mgx::conv::Geom;
+using mgx::conv::grid_for;
+
+// ------------------------------------------------------------------ C-ABI
+
+extern "C" int mgx_reduce_workspace_bytes(int64_t M, int64_t C, int64_t* out) {
+  MGX_REQUIRE(out && M > 0 && C > 0, "mgx_reduce_workspace_bytes: bad arguments");
+  int64_t rpc;
+  int nchunk;
+  mgx::conv::chunks_for(M, &rpc, &nchunk);
+  *out = int64_t(2) * nchunk * C * 8;
+  return MGX_OK;
+}
+
+extern "C" int mgx_im2col_bf16(const float* x, void* col, const int64_t* geom, int64_t ldk,
+                               uintptr_t stream) {
+  MGX_REQUIRE(x && col && geom, "mgx_im2col_bf16: bad arguments");
+  Geom g = mgx::conv::decode(geom);
+  MGX_REQUIRE(g.B > 0 && g.C > 0 && g.kh > 0 && g.kw > 0 && g.sh > 0 && g.sw > 0 && g.Ho > 0 &&
+                  g.Wo > 0, "mgx_im2col_bf16: bad geometry");
+  MGX_REQUIRE(ldk % 8 == 0 && ldk >= int64_t(g.kh) * g.kw * g.C, "mgx_im2col_bf16: bad ldk");
+  MGX_REQUIRE(mgx::aligned16(x) && mgx::aligned16(col), "mgx_im2col_bf16: unaligned");
+  const int64_t n = int64_t(g.B) * g.Ho * g.Wo * (ldk / 8);
+  mgx::conv::im2col_kernel<<<grid_for(n), 256, 0, mgx::as_stream(stream)>>>(
+      x, static_cast<__nv_bfloat16*>(col), g, ldk);
+  MGX_LAUNCHED();
+  return MGX_OK;
+}
+
+extern "C" int mgx_col2im(const float* dcol, int64_t ldk, float* dx, const int64_t* geom,
+                          uintptr_t stream) {
+  MGX_REQUIRE(dcol && dx && geom, "mgx_col2im: bad arguments");
+  Geom g = mgx::conv::decode(geom);
+  MGX_REQUIRE(g.Ho > 0 && g.Wo > 0 && ldk >= int64_t(g.kh) * g.kw * g.C, "mgx_col2im: bad geometry");
+  const int64_t n = int64_t(g.B) * g.H * g.W * g.C;
+  mgx::conv::col2im_kernel<<<grid_for(n), 256, 0, mgx::as_stream(stream)>>>(dcol, ldk, dx, g);
+  MGX_LAUNCHED();
+  return MGX_OK;
+}
+
+extern "C" int mgx_bn_stats(const float* x, int64_t M, int64_t C, void* ws, float* stats,
+                            float* moving_mean, float* moving_var, float eps, float momentum,
+                            int use_global, uintptr_t stream) {
+  MGX_REQUIRE(stats && M > 0 && C > 0 && C <= 65536, "mgx_bn_stats: bad arguments");
+  MGX_REQUIRE(!use_global || (moving_mean && moving_var), "mgx_bn_stats: global stats need moving_*");
+  cudaStream_t st = mgx::as_stream(stream);
+  int nchunk = 0;
+  if (!use_global) {
+    MGX_REQUIRE(x && ws, "mgx_bn_stats: bad arguments");
+    MGX_TRY(mgx::conv::launch_partial<0>(x, nullptr, nullptr, M, static_cast<int>(C),
+                                         static_cast<double*>(ws), &nchunk, st));
+  }
+  mgx::conv::bn_stats_finalize_kernel<<<static_cast<unsigned>(mgx::ceil_div(C, 128)), 128, 0, st>>>(
+      static_cast<const double*>(ws), nchunk, M, static_cast<int>(C), eps, momentum, use_global,
+      stats, moving_mean, moving_var);
+  MGX_LAUNCHED();
+  return MGX_OK;
+}
+
+extern "C" int mgx_bn_apply(const float* x, const float* stats, const float* gamma,
+                            const float* beta, float* y, int64_t M, int64_t C, int act,
+                            uintptr_t stream) {
+  MGX_REQUIRE(x && stats && beta && y && M > 0 && C > 0, "mgx_bn_apply: bad arguments");
+  mgx::conv::bn_apply_kernel<<<grid_for(M * C / ((C & 3) ? 1 : 4)), 256, 0, mgx::as_stream(stream)>>>(
+      x, stats, gamma, beta, y, M, static_cast<int>(C), act);
+  MGX_LAUNCHED();
+  return MGX_OK;
+}
+
+extern "C" int mgx_bn_bwd_reduce(const float* dy, const float* x, const float* stats, int64_t M,
+                                 int64_t C, void* ws, float* sums, uintptr_t stream) {
+  MGX_REQUIRE(dy && x && stats && ws && sums && M > 0 && C > 0, "mgx_bn_bwd_reduce: bad arguments");
+  cudaStream_t st = mgx::as_stream(stream);
+  int nchunk = 0;
+  MGX_TRY(mgx::conv::launch_partial<1>(dy, x, stats, M, static_cast<int>(C), static_cast<double*>(ws),
+                                       &nchunk, st));
+  mgx::conv::colsum_finalize_kernel<<<static_cast<unsigned>(mgx::ceil_div(C, 128)), 128, 0, st>>>(
+      static_cast<const double*>(ws), nchunk, static_cast<int>(C), 1, sums);
+  MGX_LAUNCHED();
+  return MGX_OK;
+}
+
+extern "C" int mgx_bn_bwd_dx(const float* dy, const float* x, const float* stats, const float* sums,
+                             const float* gamma, float* dx, int64_t M, int64_t C, uintptr_t stream) {
+  MGX_REQUIRE(dy && x && stats && sums && dx && M > 0 && C > 0, "mgx_bn_bwd_dx: bad arguments");
+  mgx::conv::bn_bwd_dx_kernel<<<grid_for(M * C), 256, 0, mgx::as_stream(stream)>>>(
+      dy, x, stats, sums, gamma, dx, M, static_cast<int>(C));
+  MGX_LAUNCHED();
+  return MGX_OK;
+}
+
+extern "C" int mgx_colsum(const float* x, int64_t M, int64_t C, void* ws, float* out,
+                          uintptr_t stream) {
+  MGX_REQUIRE(x && ws && out && M > 0 && C > 0, "mgx_colsum: bad arguments");
+  cudaStream_t st = mgx::as_stream(stream);
+  int nchunk = 0;
+  MGX_TRY(mgx::conv::launch_partial<2>(x, nullptr, nullptr, M, static_cast<int>(C),
+                                       static_cast<double*>(ws), &nchunk, st));
+  mgx::conv::colsum_finalize_kernel<<<static_cast<unsigned>(mgx::ceil_div(C, 128)), 128, 0, st>>>(
+      static_cast<const double*>(ws), nchunk, static_cast<int>(C), 0, out);
+  MGX_LAUNCHED();
+  return MGX_OK;
+}
+
+extern "C" int mgx_pool_forward(const float* x, float* y, const int64_t* geom, int full, int type,
+                                uintptr_t stream) {
+  MGX_REQUIRE(x && y && geom && (type == 0 || type == 1), "mgx_pool_forward: bad arguments");
+  Geom g = mgx::conv::decode(geom, full != 0);
+  MGX_REQUIRE(g.Ho > 0 && g.Wo > 0, "mgx_pool_forward: bad geometry");
+  const int64_t n = int64_t(g.B) * g.Ho * g.Wo * g.C;
+  mgx::conv::pool_fwd_kernel<<<grid_for(n), 256, 0, mgx::as_stream(stream)>>>(x, y, g, type);
+  MGX_LAUNCHED();
+  return MGX_OK;
+}
+
+extern "C" int mgx_pool_backward(const float* x, const float* y, const float* dy, float* dx,
+                                 const int64_t* geom, int full, int type, uintptr_t stream) {
+  MGX_REQUIRE(dy && dx && geom && (type == 1 || (x && y)), "mgx_pool_backward: bad arguments");
+  Geom g = mgx::conv::decode(geom, full != 0);
+  const int64_t n = int64_t(g.B) * g.H * g.W * g.C;
+  mgx::conv::pool_bwd_kernel<<<grid_for(n), 256, 0, mgx::as_stream(stream)>>>(x, y, dy, dx, g, type);
+  MGX_LAUNCHED();
+  return MGX_OK;
+}
+
+extern "C" int mgx_chan_copy(const float* src, int64_t lds, int64_t soff, float* dst, int64_t ldd,
+                             int64_t doff, int64_t rows, int64_t cols, uintptr_t stream) {
+  MGX_REQUIRE(src && dst && rows >= 0 && cols >= 0, "mgx_chan_copy: bad arguments");
+  if (rows == 0 || cols == 0) return MGX_OK;
+  mgx::conv::chan_copy_kernel<<<grid_for(rows * cols / 4 + 1), 256, 0, mgx::as_stream(stream)>>>(
+      src, lds, soff, dst, ldd, doff, rows, cols);
+  MGX_LAUNCHED();
+  return MGX_OK;
+}

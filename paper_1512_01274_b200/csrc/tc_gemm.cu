@@ -70,16 +70,37 @@ __device__ __forceinline__ uint64_t smem_desc_sw128(const void* p) {
   return d;
 }
 
-// instruction descriptor kind::f16: D f32, A/B bf16, both K-major, M128 N128
-constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((BN >> 3) << 17) | ((BM >> 4) << 24);
+// tcgen05 shared-memory matrix descriptor, MN-major, 128-byte swizzle:
+// 64-element (128 B) MN rows, K rows 128 B apart; 8-row K groups 1024 B
+// apart (SBO); 64-wide MN chunks kMnChunkBytes apart (LBO).
+constexpr int kMnChunkBytes = BK * 128;  // one TMA box: 64 K rows x 128 B
+__device__ __forceinline__ uint64_t smem_desc_mn_sw128(const void* p) {
+  const uint64_t addr = smem_u32(p);
+  uint64_t d = 0;
+  d |= (addr >> 4) & 0x3FFFull;
+  d |= (uint64_t(kMnChunkBytes >> 4) & 0x3FFF) << 16;  // LBO: next 64 MN elements
+  d |= (uint64_t(1024 >> 4) & 0x3FFF) << 32;           // SBO: next 8 K rows
+  d |= uint64_t(1) << 46;
+  d |= uint64_t(2) << 61;
+  return d;
+}
 
+// instruction descriptor kind::f16: D f32, A/B bf16, M128 N128; bit 15 / 16
+// select an MN-major A / B operand
+template <bool A_MN, bool B_MN>
+constexpr uint32_t idesc() {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((A_MN ? 1u : 0u) << 15) | ((B_MN ? 1u : 0u) << 16) |
+         ((BN >> 3) << 17) | ((BM >> 4) << 24);
+}
+
+template <bool A_MN, bool B_MN>
 __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
                                           uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(accumulate));
+      "l"(adesc), "l"(bdesc), "r"(idesc<A_MN, B_MN>()), "r"(accumulate));
 }
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -87,10 +108,28 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
                : "memory");
 }
 
+// one 128-row x 64-K operand tile into `dst`: a single K-major box, or two
+// MN-major boxes (MN 0..63, 64..127) stacked kMnChunkBytes apart
+template <bool MN>
+__device__ __forceinline__ void load_operand(uint8_t* dst, const CUtensorMap* map, uint64_t* bar,
+                                             int k0, int r0) {
+  if (!MN) {
+    tma_load_2d(dst, map, bar, k0, r0);
+  } else {
+    tma_load_2d(dst, map, bar, r0, k0);
+    tma_load_2d(dst + kMnChunkBytes, map, bar, r0 + 64, k0);
+  }
+}
+
+// C[M,N] (+bias, act) = sum_k A(m,k) B(n,k).  K-major operand X: X[r*ld + k];
+// MN-major: X[k*ld + r].  Split-K: blockIdx.z takes K blocks
+// [z*kps, (z+1)*kps) and writes its partial tile to C + z*split_stride.
+template <bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(128, 1)
 tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
                     const __grid_constant__ CUtensorMap map_b, const float* __restrict__ bias,
-                    float* __restrict__ C, int ldc, int M, int N, int K, int act) {
+                    float* __restrict__ C, int ldc, int M, int N, int K, int act, int kps,
+                    int64_t split_stride) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte aligned stage ring (SW128 atoms need it)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -101,7 +140,10 @@ tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
-  const int nk = (K + BK - 1) / BK;
+  const int nk_all = (K + BK - 1) / BK;
+  const int kb0 = blockIdx.z * kps;
+  const int nk = min(nk_all, kb0 + kps) - kb0;
+  C += int64_t(blockIdx.z) * split_stride;
 
   if (threadIdx.x == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
@@ -132,8 +174,8 @@ tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
       mbar_wait(&empty[s], ph ^ 1);
       uint8_t* sa = smem + s * kStageBytes;
       mbar_expect_tx(&full[s], kStageBytes);
-      tma_load_2d(sa, &map_a, &full[s], kb * BK, m0);
-      tma_load_2d(sa + kTileBytes, &map_b, &full[s], kb * BK, n0);
+      load_operand<A_MN>(sa, &map_a, &full[s], (kb0 + kb) * BK, m0);
+      load_operand<B_MN>(sa + kTileBytes, &map_b, &full[s], (kb0 + kb) * BK, n0);
     }
   } else if (warp == 1 && lane == 0) {
     // ---------------- MMA issuer
@@ -143,12 +185,15 @@ tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
       mbar_wait(&full[s], ph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint8_t* sa = smem + s * kStageBytes;
-      const uint64_t adesc = smem_desc_sw128(sa);
-      const uint64_t bdesc = smem_desc_sw128(sa + kTileBytes);
+      const uint64_t adesc = A_MN ? smem_desc_mn_sw128(sa) : smem_desc_sw128(sa);
+      const uint64_t bdesc = B_MN ? smem_desc_mn_sw128(sa + kTileBytes) : smem_desc_sw128(sa + kTileBytes);
 #pragma unroll
       for (int k = 0; k < BK / UMMA_K; ++k) {
-        // +32 bytes per K16 step inside the 128-byte swizzle row (>>4 -> +2)
-        umma_bf16(tmem, adesc + 2 * k, bdesc + 2 * k, (kb > 0 || k > 0) ? 1u : 0u);
+        // K-major: +32 bytes per K16 step inside the 128-byte swizzle row
+        // (>>4 -> +2); MN-major: +16 K rows of 128 bytes (>>4 -> +128)
+        const uint64_t da = A_MN ? 128ull * k : 2ull * k;
+        const uint64_t db = B_MN ? 128ull * k : 2ull * k;
+        umma_bf16<A_MN, B_MN>(tmem, adesc + da, bdesc + db, (kb > 0 || k > 0) ? 1u : 0u);
       }
       umma_commit(&empty[s]);
     }
@@ -172,6 +217,10 @@ tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
     if (row < M) {
       float* crow = C + int64_t(row) * ldc;
+      if (nk <= 0) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) r[j] = 0u;  // empty split: contributes zeros
+      }
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         const int n = n0 + c0 + j;
@@ -188,6 +237,23 @@ tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   if (warp == 1) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN));
+  }
+}
+
+// Split-K epilogue: C[m, n] = act(sum_z ws[z][m, n] (+ bias[n])), partial
+// tiles summed in ascending split order (deterministic).
+__global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, int64_t split_stride,
+                                     const float* __restrict__ bias, float* __restrict__ C,
+                                     int64_t ldc, int64_t M, int64_t N, int act) {
+  const int64_t total = M * N;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
+    const int64_t m = i / N, n = i - m * N;
+    const int64_t o = m * N + n;
+    float v = ws[o];
+    for (int z = 1; z < splits; ++z) v = fadd(v, ws[z * split_stride + o]);
+    if (bias) v = fadd(v, __ldg(bias + n));
+    C[m * ldc + n] = act_forward(act, v);
   }
 }
 
@@ -239,10 +305,24 @@ static int get_encode() {
   return MGX_OK;
 }
 
-static int make_map(CUtensorMap* map, const void* base, int64_t rows, int64_t K, int64_t ld) {
-  cuuint64_t dims[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(rows)};
+// K-major operand: dims {K, rows}, box {64, 128}; MN-major: dims {rows, K}
+// (rows contiguous), box {64, 64} (loaded twice per 128-row tile)
+static int make_map(CUtensorMap* map, const void* base, int64_t rows, int64_t K, int64_t ld,
+                    bool mn) {
+  cuuint64_t dims[2];
+  cuuint32_t box[2];
+  if (!mn) {
+    dims[0] = static_cast<cuuint64_t>(K);
+    dims[1] = static_cast<cuuint64_t>(rows);
+    box[0] = BK;
+    box[1] = BM;
+  } else {
+    dims[0] = static_cast<cuuint64_t>(rows);
+    dims[1] = static_cast<cuuint64_t>(K);
+    box[0] = 64;
+    box[1] = BK;
+  }
   cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * 2)};
-  cuuint32_t box[2] = {BK, BM};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
                         strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -255,34 +335,99 @@ static int make_map(CUtensorMap* map, const void* base, int64_t rows, int64_t K,
   return MGX_OK;
 }
 
+template <bool A_MN, bool B_MN>
+static int launch_variant(const CUtensorMap& ma, const CUtensorMap& mb, dim3 grid,
+                          const float* bias, float* C, int ldc, int M, int N, int K, int act,
+                          int kps, int64_t split_stride, cudaStream_t st) {
+  static bool configured = false;
+  if (!configured) {
+    MGX_CUDA(cudaFuncSetAttribute(tc_gemm_bf16_kernel<A_MN, B_MN>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+    configured = true;
+  }
+  tc_gemm_bf16_kernel<A_MN, B_MN><<<grid, 128, kSmemBytes, st>>>(ma, mb, bias, C, ldc, M, N, K,
+                                                                   act, kps, split_stride);
+  MGX_LAUNCHED();
+  return MGX_OK;
+}
+
 }  // namespace tc
 }  // namespace mgx
+
+extern "C" int mgx_gemm_bf16_tc_ex(const void* A, int64_t lda, int a_mn, const void* B,
+                                   int64_t ldb, int b_mn, const float* bias, float* C, int64_t ldc,
+                                   int64_t M, int64_t N, int64_t K, int act, int splits,
+                                   float* workspace, uintptr_t stream) {
+  using namespace mgx::tc;
+  MGX_REQUIRE(A && B && C && M > 0 && N > 0 && K > 0, "mgx_gemm_bf16_tc: bad arguments");
+  MGX_REQUIRE(lda % 8 == 0 && ldb % 8 == 0,
+              "mgx_gemm_bf16_tc: leading dimensions must be multiples of 8");
+  MGX_REQUIRE(lda >= (a_mn ? M : K) && ldb >= (b_mn ? N : K),
+              "mgx_gemm_bf16_tc: leading dimension smaller than the operand row");
+  MGX_REQUIRE(mgx::aligned16(A) && mgx::aligned16(B), "mgx_gemm_bf16_tc: operands not 16-byte aligned");
+  MGX_REQUIRE(M < (1ll << 31) && N < (1ll << 31) && K < (1ll << 31) && ldc < (1ll << 31),
+              "mgx_gemm_bf16_tc: dimensions exceed 2^31");
+  MGX_REQUIRE(splits >= 0, "mgx_gemm_bf16_tc: negative split count");
+  MGX_TRY(get_encode());
+  CUtensorMap ma, mb;
+  MGX_TRY(make_map(&ma, A, M, K, lda, a_mn != 0));
+  MGX_TRY(make_map(&mb, B, N, K, ldb, b_mn != 0));
+  const int64_t tiles = mgx::ceil_div(N, BN) * mgx::ceil_div(M, BM);
+  const int64_t nk = mgx::ceil_div(K, BK);
+  if (splits == 0) {
+    // auto: enough K splits to cover the SMs once, each split >= 4 K blocks
+    splits = 1;
+    if (workspace && tiles < mgx::kNumSMs) {
+      int64_t want = mgx::kNumSMs / tiles;
+      int64_t most = nk / 4;
+      splits = static_cast<int>(want < most ? want : most);
+      if (splits < 1) splits = 1;
+    }
+  }
+  MGX_REQUIRE(splits == 1 || workspace, "mgx_gemm_bf16_tc: split-K needs a workspace");
+  int kps = static_cast<int>(mgx::ceil_div(nk, splits));
+  splits = static_cast<int>(mgx::ceil_div(nk, kps));
+  dim3 grid(static_cast<unsigned>(mgx::ceil_div(N, BN)), static_cast<unsigned>(mgx::ceil_div(M, BM)),
+            static_cast<unsigned>(splits));
+  cudaStream_t st = mgx::as_stream(stream);
+  float* out = splits == 1 ? C : workspace;
+  const int64_t sstride = M * N;
+  const int oldc = splits == 1 ? static_cast<int>(ldc) : static_cast<int>(N);
+  const float* ebias = splits == 1 ? bias : nullptr;
+  const int eact = splits == 1 ? act : 0;
+  const int m = static_cast<int>(M), n = static_cast<int>(N), k = static_cast<int>(K);
+  int rc;
+  if (!a_mn && !b_mn) rc = launch_variant<false, false>(ma, mb, grid, ebias, out, oldc, m, n, k, eact, kps, sstride, st);
+  else if (!a_mn && b_mn) rc = launch_variant<false, true>(ma, mb, grid, ebias, out, oldc, m, n, k, eact, kps, sstride, st);
+  else if (a_mn && !b_mn) rc = launch_variant<true, false>(ma, mb, grid, ebias, out, oldc, m, n, k, eact, kps, sstride, st);
+  else rc = launch_variant<true, true>(ma, mb, grid, ebias, out, oldc, m, n, k, eact, kps, sstride, st);
+  if (rc != MGX_OK || splits == 1) return rc;
+  int64_t blocks = mgx::ceil_div(M * N, 256);
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  splitk_reduce_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(workspace, splits, sstride,
+                                                                      bias, C, ldc, M, N, act);
+  MGX_LAUNCHED();
+  return MGX_OK;
+}
 
 extern "C" int mgx_gemm_bf16_tc(const void* A, int64_t lda, const void* B, int64_t ldb,
                                 const float* bias, float* C, int64_t ldc, int64_t M, int64_t N,
                                 int64_t K, int act, uintptr_t stream) {
+  return mgx_gemm_bf16_tc_ex(A, lda, 0, B, ldb, 0, bias, C, ldc, M, N, K, act, 1, nullptr, stream);
+}
+
+extern "C" int mgx_gemm_splitk_workspace(int64_t M, int64_t N, int64_t K, int64_t* out_floats) {
   using namespace mgx::tc;
-  MGX_REQUIRE(A && B && C && M > 0 && N > 0 && K > 0, "mgx_gemm_bf16_tc: bad arguments");
-  MGX_REQUIRE(K % 8 == 0 && lda % 8 == 0 && ldb % 8 == 0,
-              "mgx_gemm_bf16_tc: K and leading dimensions must be multiples of 8");
-  MGX_REQUIRE(mgx::aligned16(A) && mgx::aligned16(B), "mgx_gemm_bf16_tc: operands not 16-byte aligned");
-  MGX_REQUIRE(M < (1ll << 31) && N < (1ll << 31) && K < (1ll << 31) && ldc < (1ll << 31),
-              "mgx_gemm_bf16_tc: dimensions exceed 2^31");
-  MGX_TRY(get_encode());
-  CUtensorMap ma, mb;
-  MGX_TRY(make_map(&ma, A, M, K, lda));
-  MGX_TRY(make_map(&mb, B, N, K, ldb));
-  static bool configured = false;
-  if (!configured) {
-    MGX_CUDA(cudaFuncSetAttribute(tc_gemm_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  kSmemBytes));
-    configured = true;
+  MGX_REQUIRE(out_floats && M > 0 && N > 0 && K > 0, "mgx_gemm_splitk_workspace: bad arguments");
+  const int64_t tiles = mgx::ceil_div(N, BN) * mgx::ceil_div(M, BM);
+  const int64_t nk = mgx::ceil_div(K, BK);
+  int64_t splits = 1;
+  if (tiles < mgx::kNumSMs) {
+    int64_t want = mgx::kNumSMs / tiles, most = nk / 4;
+    splits = want < most ? want : most;
+    if (splits < 1) splits = 1;
   }
-  dim3 grid(static_cast<unsigned>(mgx::ceil_div(N, BN)), static_cast<unsigned>(mgx::ceil_div(M, BM)));
-  tc_gemm_bf16_kernel<<<grid, 128, kSmemBytes, mgx::as_stream(stream)>>>(
-      ma, mb, bias, C, static_cast<int>(ldc), static_cast<int>(M), static_cast<int>(N),
-      static_cast<int>(K), act);
-  MGX_LAUNCHED();
+  *out_floats = splits > 1 ? splits * M * N : 0;
   return MGX_OK;
 }
 

@@ -40,6 +40,10 @@ def current_stream() -> int:
     return current_engine().stream_handle
 
 
+def current_device() -> int:
+    return current_engine().device
+
+
 class ResourceTag:
     """Identity of one mutable resource (engine.py:27-50)."""
 

@@ -43,6 +43,11 @@ class OperatorDef:
     lower_forward: Optional[Callable] = None
     # (slot, env: {role: View}, out: View, attrs) -> [Instr]
     lower_backward: Optional[Callable] = None
+    # attrs -> input names when they depend on attributes (no_bias)
+    inputs_for: Optional[Callable] = None
+
+    def input_names_for(self, attrs: dict) -> tuple:
+        return self.inputs_for(attrs) if self.inputs_for is not None else self.input_names
 
     @property
     def num_inputs(self) -> int:
@@ -139,6 +144,121 @@ def instr_cost(ins: L.Instr) -> tuple:
     streams = {L.OP_FILL: 1, L.OP_COPY: 2, L.OP_EW: 3, L.OP_SCALAR: 2, L.OP_ACT_FWD: 2,
                L.OP_ACT_BWD: 3, L.OP_AXPY: 3}.get(op, 0)
     return 4 * streams * d[0], d[0]
+
+
+# ------------------------------------------------------- lowering context
+
+class LowerCtx:
+    """Device scratch and cross-node memo for lowering one bound graph.
+
+    ``scratch(n)`` is op-local memory (reused by the next node's lowering:
+    instructions run in program order on one stream); ``persistent(n)``
+    lives as long as the program (bf16 operand copies a node's backward
+    reuses from its forward, BatchNorm statistics).  The executor lowers
+    twice: a measuring pass against a fake base, then the real pass against
+    two allocations of the measured sizes.  ``node`` is the graph node being
+    lowered, ``training`` whether the bind requested gradients."""
+
+    ALIGN = 256
+    FAKE_BASE = 1 << 44
+
+    def __init__(self, training: bool, scratch_base: Optional[int] = None,
+                 persist_base: Optional[int] = None, device: int = 0):
+        self.training = training
+        self.device = device
+        self.measuring = scratch_base is None
+        self._sbase = self.FAKE_BASE if scratch_base is None else scratch_base
+        self._pbase = self.FAKE_BASE * 2 if persist_base is None else persist_base
+        self._op_off = 0
+        self._p_off = 0
+        self.scratch_peak = 0
+        self.memo: Dict[tuple, object] = {}
+        self.node = None
+
+    def begin_op(self, node) -> None:
+        self.node = node
+        self._op_off = 0
+
+    def _al(self, n: int) -> int:
+        return -(-max(int(n), 1) // self.ALIGN) * self.ALIGN
+
+    def scratch(self, nbytes: int) -> int:
+        ptr = self._sbase + self._op_off
+        self._op_off += self._al(nbytes)
+        self.scratch_peak = max(self.scratch_peak, self._op_off)
+        return ptr
+
+    def persistent(self, nbytes: int) -> int:
+        ptr = self._pbase + self._p_off
+        self._p_off += self._al(nbytes)
+        return ptr
+
+    @property
+    def persistent_bytes(self) -> int:
+        return self._p_off
+
+    def input_node(self, role: str):
+        """Source node of ``role`` ('in0', 'og', ...) of the node being
+        lowered (a Backward node's roles name its inputs)."""
+        n = self.node
+        if n is None:
+            return None
+        if n.op == "Backward":
+            roles = n.attrs["roles"]
+            if role not in roles:
+                return None
+            return n.inputs[roles.index(role)][0]
+        if role.startswith("in"):
+            return n.inputs[int(role[2:])][0]
+        return None
+
+
+class _EagerCtx(LowerCtx):
+    """Context for plugin-style eager calls: real allocations per request,
+    kept alive with the context object's owner list."""
+
+    _keep: list = []
+
+    def __init__(self, device: int):
+        super().__init__(training=True, scratch_base=0, persist_base=0, device=device)
+
+    def _alloc(self, nbytes: int) -> int:
+        import torch
+        t = torch.empty(self._al(nbytes), dtype=torch.uint8, device=f"cuda:{self.device}")
+        _EagerCtx._keep.append(t)
+        del _EagerCtx._keep[:-256]
+        return t.data_ptr()
+
+    def scratch(self, nbytes: int) -> int:
+        return self._alloc(nbytes)
+
+    def persistent(self, nbytes: int) -> int:
+        return self._alloc(nbytes)
+
+
+_CTX: List[LowerCtx] = []
+
+
+def current_ctx() -> LowerCtx:
+    """The lowering context of the bind in progress (or an eager one)."""
+    if _CTX:
+        return _CTX[-1]
+    from .engine import current_device
+    return _EagerCtx(current_device())
+
+
+class lowering:
+    """``with lowering(ctx): ...`` makes ``ctx`` current."""
+
+    def __init__(self, ctx: LowerCtx):
+        self.ctx = ctx
+
+    def __enter__(self):
+        _CTX.append(self.ctx)
+        return self.ctx
+
+    def __exit__(self, *exc):
+        _CTX.pop()
 
 
 def run_instrs(instrs: List[L.Instr], stream: int) -> None:
@@ -631,3 +751,7 @@ def node_lowering(op_name: str, attrs: dict) -> Optional[Callable]:
         of = get_op(attrs["of"])
         return _backward_lower if of.lower_backward is not None else None
     return op.lower_forward
+
+
+# convolution-net operators register themselves into OPS
+from . import conv_ops  # noqa: E402,F401

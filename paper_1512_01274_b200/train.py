@@ -69,21 +69,40 @@ def mlp(hidden: Sequence[int], classes: int) -> SymbolGraph:
     return symbol.apply("SoftmaxOutput", {}, [net], name="softmax")
 
 
+AUX_SUFFIXES = ("_moving_mean", "_moving_var")
+
+
 def param_names(g: SymbolGraph) -> List[str]:
-    return [n for n in g.list_arguments() if n not in RESERVED_ARGS]
+    """Trainable arguments in list_arguments order (the KVStore keys)."""
+    return [n for n in g.list_arguments()
+            if n not in RESERVED_ARGS and not n.endswith(AUX_SUFFIXES)]
+
+
+def aux_names(g: SymbolGraph) -> List[str]:
+    """BatchNorm moving statistics: per-worker state, never pushed."""
+    return [n for n in g.list_arguments() if n.endswith(AUX_SUFFIXES)]
 
 
 def init_params(g: SymbolGraph, arg_shapes: Dict[str, tuple], seed: int) -> Dict[str, np.ndarray]:
-    """randn*0.1 weights in parameter order, zero biases (train.py:74-85)."""
+    """randn*0.1 weights in parameter order, zero biases (train.py:74-85);
+    BatchNorm gamma ones and beta zeros (no RNG draw, like the biases)."""
     rs = np.random.RandomState(seed)
     out = {}
     for name in param_names(g):
         shape = arg_shapes[name]
-        if name.endswith("_bias"):
+        if name.endswith(("_bias", "_beta")):
             out[name] = np.zeros(shape, dtype=np.float32)
+        elif name.endswith("_gamma"):
+            out[name] = np.ones(shape, dtype=np.float32)
         else:
             out[name] = (rs.randn(*shape) * 0.1).astype(np.float32)
     return out
+
+
+def init_aux(g: SymbolGraph, arg_shapes: Dict[str, tuple]) -> Dict[str, np.ndarray]:
+    """moving_mean zeros, moving_var ones (MXNet's aux initialisation)."""
+    return {n: (np.zeros if n.endswith("_moving_mean") else np.ones)(arg_shapes[n], np.float32)
+            for n in aux_names(g)}
 
 
 def cross_entropy_mean(probs: np.ndarray, labels: np.ndarray, eps: float = 1e-12) -> float:
@@ -122,6 +141,9 @@ class DataParallelStep:
         self.g, self.kv = g, kv
         self.engine = engine or kv.engine
         self.names = param_names(g)
+        self.aux = aux_names(g)
+        arg_shapes, _ = infer_shape(g, shard_shapes)
+        aux0 = init_aux(g, arg_shapes)
         for i, n in enumerate(self.names):
             kv.init(i, params0[n])
         self.workers = list(kv.local_workers)
@@ -135,6 +157,8 @@ class DataParallelStep:
             for i, n in enumerate(self.names):
                 args[n] = kv.weight_tensor(i, w)
                 grads[n] = kv.grad_tensor(i, w)
+            for n in self.aux:
+                args[n] = tmod.from_host(arg_shapes[n], "float32", aux0[n], engine=self.engine)
             self.args[w], self.grads[w] = args, grads
             self.execs[w] = bind(g, args, {n: "write" for n in self.names}, grads,
                                  strategy=strategy, engine=self.engine, use_graph=use_graph,
@@ -214,7 +238,7 @@ def train_local(g: SymbolGraph, data, cfg: SGDConfig, epochs: int, batch: int,
     it = BatchOrder(feats, labels, batch, seed=shuffle_seed)
     if it.batches_per_epoch < 1:
         raise ArgumentError("batch size exceeds the dataset")
-    given = {"data": (batch, feats.shape[1]), "label": (batch,)}
+    given = {"data": (batch,) + tuple(feats.shape[1:]), "label": (batch,)}
     arg_shapes, _ = infer_shape(g, given)
     params0 = init_params(g, arg_shapes, param_seed)
     names = param_names(g)
@@ -222,6 +246,8 @@ def train_local(g: SymbolGraph, data, cfg: SGDConfig, epochs: int, batch: int,
             "label": tmod.zeros(given["label"], engine=engine)}
     for n in names:
         args[n] = tmod.from_host(arg_shapes[n], "float32", params0[n], engine=engine)
+    for n, v in init_aux(g, arg_shapes).items():
+        args[n] = tmod.from_host(arg_shapes[n], "float32", v, engine=engine)
     grads = {n: tmod.zeros(arg_shapes[n], engine=engine) for n in names}
     vel = {n: tmod.zeros(arg_shapes[n], engine=engine) for n in names}
     ex = bind(g, args, {n: "write" for n in names}, grads, strategy=strategy, engine=engine)
@@ -271,7 +297,7 @@ def train_distributed(g: SymbolGraph, data, cfg: SGDConfig, epochs: int, batch: 
     it = BatchOrder(feats, labels, batch, seed=shuffle_seed)
     if it.batches_per_epoch < 1:
         raise ArgumentError("batch size exceeds the dataset")
-    given = {"data": (shard, feats.shape[1]), "label": (shard,)}
+    given = {"data": (shard,) + tuple(feats.shape[1:]), "label": (shard,)}
     arg_shapes, _ = infer_shape(g, given)
     params0 = init_params(g, arg_shapes, param_seed)
     engine = engine or default_engine()

@@ -1,0 +1,235 @@
+"""Convolution-net kernels through the C-ABI (configs 3-5).
+
+No reference oracle exists for these operators (parity
+unpinned by reference); they are checked against oracle/convnet.py's
+float64 restatement of MXNet's semantics.  Tolerances:
+  * tensor-core GEMM/conv: operands rounded to bf16 exactly like the kernel,
+    fp32 accumulation vs fp64: rtol 1e-4, atol 1e-4 * sqrt(K)/8 * max|term|;
+  * BatchNorm / pooling / concat / col2im (fp32 arithmetic, fixed order):
+    rtol 1e-5 / atol 1e-5 (max pooling and concat: exact).
+"""
+
+import numpy as np
+import pytest
+
+from oracle import convnet as oc
+
+pytestmark = pytest.mark.gpu
+
+
+def _geom(shape, k, s, p):
+    b, h, w, c = shape
+    return np.array([b, h, w, c, (k[0] << 16) | k[1], (s[0] << 16) | s[1], (p[0] << 16) | p[1]],
+                    np.int64)
+
+
+def _ptr(a):
+    import ctypes
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+@pytest.mark.parametrize("a_mn,b_mn", [(0, 0), (0, 1), (1, 0), (1, 1)])
+@pytest.mark.parametrize("m,n,k", [(128, 128, 64), (200, 72, 40), (64, 300, 1000), (20, 576, 6400)])
+def test_gemm_operand_majors(cuda, a_mn, b_mn, m, n, k):
+    torch = cuda
+    from paper_1512_01274_b200 import _lib as L
+    g = torch.Generator(device="cuda").manual_seed(m + 7 * n + 13 * k + a_mn + 2 * b_mn)
+    a = torch.randn(m, k, device="cuda", generator=g).to(torch.bfloat16)
+    b = torch.randn(n, k, device="cuda", generator=g).to(torch.bfloat16)
+    pad = lambda v: -(-v // 8) * 8  # noqa: E731
+    # store A as [m, lda] (K-major) or [k, lda] (MN-major), same for B
+    if a_mn:
+        lda = pad(m)
+        abuf = torch.zeros(k, lda, dtype=torch.bfloat16, device="cuda")
+        abuf[:, :m] = a.T
+    else:
+        lda = pad(k)
+        abuf = torch.zeros(m, lda, dtype=torch.bfloat16, device="cuda")
+        abuf[:, :k] = a
+    if b_mn:
+        ldb = pad(n)
+        bbuf = torch.zeros(k, ldb, dtype=torch.bfloat16, device="cuda")
+        bbuf[:, :n] = b.T
+    else:
+        ldb = pad(k)
+        bbuf = torch.zeros(n, ldb, dtype=torch.bfloat16, device="cuda")
+        bbuf[:, :k] = b
+    c = torch.full((m, n), float("nan"), device="cuda")
+    ws = torch.empty(64 * m * n + 1, device="cuda")
+    L.call("mgx_gemm_bf16_tc_ex", abuf.data_ptr(), lda, a_mn, bbuf.data_ptr(), ldb, b_mn, None,
+           c.data_ptr(), n, m, n, k, 0, 0, ws.data_ptr(), 0)
+    torch.cuda.synchronize()
+    ref = a.double() @ b.double().T
+    torch.testing.assert_close(c.double(), ref, rtol=1e-4, atol=1e-3 * max(1.0, (k / 64) ** 0.5))
+
+
+CONV_CASES = [
+    # (B, H, W, C, F, k, s, p)
+    (2, 8, 8, 16, 24, (1, 1), (1, 1), (0, 0)),
+    (2, 9, 7, 8, 16, (3, 3), (1, 1), (1, 1)),
+    (3, 12, 12, 1, 20, (5, 5), (1, 1), (0, 0)),
+    (2, 15, 15, 3, 8, (7, 7), (2, 2), (3, 3)),
+    (1, 23, 23, 3, 12, (11, 11), (4, 4), (2, 2)),
+    (2, 9, 9, 12, 20, (3, 3), (2, 2), (1, 1)),
+]
+
+
+def _conv_case(torch, case, seed):
+    b, h, w, c, f, k, s, p = case
+    g = torch.Generator().manual_seed(seed)
+    x = torch.randn(b, h, w, c, generator=g, dtype=torch.float64)
+    wt = torch.randn(f, k[0], k[1], c, generator=g, dtype=torch.float64) * 0.2
+    bias = torch.randn(f, generator=g, dtype=torch.float64)
+    return x, wt, bias
+
+
+@pytest.mark.parametrize("case", CONV_CASES)
+def test_conv_executor_forward_backward(cuda, engine, case):
+    """Convolution node bound through the executor: forward, dX, dW, db
+    against the float64 oracle on bf16-rounded operands."""
+    torch = cuda
+    from paper_1512_01274_b200 import symbol
+    from paper_1512_01274_b200 import tensor as tmod
+    from paper_1512_01274_b200.executor import bind
+    b, h, wd, c, f, k, s, p = case
+    x, wt, bias = _conv_case(torch, case, sum(case[:5]))
+    net = symbol.apply("Convolution", {"kernel": k, "num_filter": f, "stride": s, "pad": p},
+                       [symbol.variable("data")], name="conv")
+    shapes, named = symbol.infer_shape(net, {"data": tuple(x.shape)})
+    oshape = named["conv"]
+    og = torch.randn(*oshape, generator=torch.Generator().manual_seed(5), dtype=torch.float64)
+    head = net.head_grad_names() if hasattr(net, "head_grad_names") else []
+    args = {"data": tmod.from_host(x.shape, "float32", x.float().numpy(), engine=engine),
+            "conv_weight": tmod.from_host(wt.shape, "float32", wt.float().numpy(), engine=engine),
+            "conv_bias": tmod.from_host(bias.shape, "float32", bias.float().numpy(), engine=engine)}
+    grads = {n: tmod.zeros(tuple(t.shape), engine=engine) for n, t in
+             (("data", x), ("conv_weight", wt), ("conv_bias", bias))}
+    args["conv_head_grad"] = tmod.from_host(oshape, "float32", og.float().numpy(), engine=engine)
+    del head
+    ex = bind(net, args, {n: "write" for n in grads}, grads, engine=engine)
+    ex.forward()
+    ex.backward()
+    y = tmod.to_numpy(ex.outputs[0])
+    # oracle on the same bf16-rounded operands
+    xr, wr = oc.bf16(x).requires_grad_(True), oc.bf16(wt).requires_grad_(True)
+    br = bias.clone().requires_grad_(True)
+    yr = oc.conv2d_nhwc(xr, wr, br, s, p)
+    ogr = oc.bf16(og.float().double())
+    (yr * ogr).sum().backward()
+    kk = k[0] * k[1] * c
+    tol = 1e-4 * max(1.0, kk ** 0.5 / 8)
+    np.testing.assert_allclose(y, yr.detach().numpy(), rtol=1e-4, atol=tol)
+    np.testing.assert_allclose(tmod.to_numpy(grads["data"]), xr.grad.numpy(), rtol=1e-4,
+                               atol=1e-4 * max(1.0, (f * k[0] * k[1]) ** 0.5 / 8))
+    np.testing.assert_allclose(tmod.to_numpy(grads["conv_weight"]), wr.grad.numpy(), rtol=1e-4,
+                               atol=1e-4 * max(1.0, (b * oshape[1] * oshape[2]) ** 0.5 / 8))
+    np.testing.assert_allclose(tmod.to_numpy(grads["conv_bias"]), og.sum(dim=(0, 1, 2)).numpy(),
+                               rtol=1e-5, atol=1e-4)
+
+
+@pytest.mark.parametrize("m,c", [(1000, 16), (4096, 64), (333, 200), (64 * 49, 1024), (50, 3)])
+@pytest.mark.parametrize("fix_gamma", [True, False])
+def test_batchnorm_kernels(cuda, m, c, fix_gamma):
+    torch = cuda
+    from paper_1512_01274_b200 import _lib as L
+    import ctypes
+    g = torch.Generator().manual_seed(m + c)
+    x = torch.randn(m, c, generator=g, dtype=torch.float64) * 3 + 1
+    gamma = torch.rand(c, generator=g, dtype=torch.float64) + 0.5
+    beta = torch.randn(c, generator=g, dtype=torch.float64)
+    dy = torch.randn(m, c, generator=g, dtype=torch.float64)
+    xd, gd, bd, dyd = (t.float().cuda() for t in (x, gamma, beta, dy))
+    mm = torch.zeros(c, device="cuda")
+    mv = torch.ones(c, device="cuda")
+    wsb = ctypes.c_int64()
+    L.call("mgx_reduce_workspace_bytes", m, c, ctypes.byref(wsb))
+    ws = torch.empty(wsb.value // 4 + 1, device="cuda")
+    st = torch.empty(2 * c, device="cuda")
+    y = torch.empty(m, c, device="cuda")
+    sums = torch.empty(2 * c, device="cuda")
+    dx = torch.empty(m, c, device="cuda")
+    gp = None if fix_gamma else gd.data_ptr()
+    L.call("mgx_bn_stats", xd.data_ptr(), m, c, ws.data_ptr(), st.data_ptr(), mm.data_ptr(),
+           mv.data_ptr(), 1e-3, 0.9, 0, 0)
+    L.call("mgx_bn_apply", xd.data_ptr(), st.data_ptr(), gp, bd.data_ptr(), y.data_ptr(), m, c, 0, 0)
+    L.call("mgx_bn_bwd_reduce", dyd.data_ptr(), xd.data_ptr(), st.data_ptr(), m, c, ws.data_ptr(),
+           sums.data_ptr(), 0)
+    L.call("mgx_bn_bwd_dx", dyd.data_ptr(), xd.data_ptr(), st.data_ptr(), sums.data_ptr(), gp,
+           dx.data_ptr(), m, c, 0)
+    torch.cuda.synchronize()
+    xr = xd.double().cpu().requires_grad_(True)
+    gr = gd.double().cpu().requires_grad_(True)
+    br = bd.double().cpu().requires_grad_(True)
+    yr, mean, var = oc.batchnorm(xr, gr, br, 1e-3, fix_gamma)
+    (yr * dyd.double().cpu()).sum().backward()
+    np.testing.assert_allclose(y.cpu().numpy(), yr.detach().numpy(), rtol=1e-5, atol=2e-5)
+    np.testing.assert_allclose(dx.cpu().numpy(), xr.grad.numpy(), rtol=1e-4, atol=1e-5)
+    np.testing.assert_allclose(sums[:c].cpu().numpy(), br.grad.numpy(), rtol=1e-5, atol=1e-4)
+    if not fix_gamma:
+        np.testing.assert_allclose(sums[c:].cpu().numpy(), gr.grad.numpy(), rtol=1e-5, atol=1e-4)
+    np.testing.assert_allclose(mm.cpu().numpy(), (0.1 * mean).detach().numpy(), rtol=1e-5, atol=1e-6)
+    np.testing.assert_allclose(mv.cpu().numpy(), (0.9 + 0.1 * var).detach().numpy(), rtol=1e-5, atol=1e-6)
+
+
+POOL_CASES = [
+    # (shape, kernel, stride, pad, type)
+    ((2, 12, 12, 8), (2, 2), (2, 2), (0, 0), "max"),
+    ((2, 13, 13, 16), (3, 3), (2, 2), (0, 0), "max"),
+    ((2, 14, 14, 8), (3, 3), (1, 1), (1, 1), "max"),
+    ((2, 14, 14, 8), (3, 3), (1, 1), (1, 1), "avg"),
+    ((2, 27, 27, 4), (3, 3), (2, 2), (1, 1), "max"),
+    ((1, 7, 7, 32), (7, 7), (1, 1), (0, 0), "avg"),
+]
+
+
+@pytest.mark.parametrize("case", POOL_CASES)
+@pytest.mark.parametrize("ties", [False, True])
+def test_pooling_kernels(cuda, case, ties):
+    torch = cuda
+    from paper_1512_01274_b200 import _lib as L
+    shape, k, s, p, kind = case
+    g = torch.Generator().manual_seed(sum(shape))
+    x = torch.randn(*shape, generator=g, dtype=torch.float64)
+    if ties:  # post-ReLU maps: many equal zeros in a window
+        x = torch.relu(x - 0.5).float().double()
+    x = x.float().double()
+    xr = x.clone().requires_grad_(True)
+    yr = oc.pool_nhwc(xr, {"kernel": k, "stride": s, "pad": p, "pool_type": kind})
+    dy = torch.randn(*yr.shape, generator=g, dtype=torch.float64).float().double()
+    (yr * dy).sum().backward()
+    geom = _geom(shape, k, s, p)
+    xd, dyd = x.float().cuda(), dy.float().cuda()
+    y = torch.empty(*yr.shape, device="cuda")
+    dx = torch.empty(*shape, device="cuda")
+    t = 0 if kind == "max" else 1
+    L.call("mgx_pool_forward", xd.data_ptr(), y.data_ptr(), _ptr(geom), 0, t, 0)
+    L.call("mgx_pool_backward", xd.data_ptr(), y.data_ptr(), dyd.data_ptr(), dx.data_ptr(),
+           _ptr(geom), 0, t, 0)
+    torch.cuda.synchronize()
+    if kind == "max":
+        np.testing.assert_array_equal(y.cpu().numpy(), yr.detach().float().numpy())
+    else:
+        np.testing.assert_allclose(y.cpu().numpy(), yr.detach().numpy(), rtol=1e-5, atol=1e-6)
+    np.testing.assert_allclose(dx.cpu().numpy(), xr.grad.numpy(), rtol=1e-5, atol=1e-6)
+
+
+def test_chan_copy_and_colsum(cuda):
+    torch = cuda
+    from paper_1512_01274_b200 import _lib as L
+    import ctypes
+    a = torch.randn(37, 12, device="cuda")
+    b = torch.randn(37, 5, device="cuda")
+    out = torch.zeros(37, 17, device="cuda")
+    L.call("mgx_chan_copy", a.data_ptr(), 12, 0, out.data_ptr(), 17, 0, 37, 12, 0)
+    L.call("mgx_chan_copy", b.data_ptr(), 5, 0, out.data_ptr(), 17, 12, 37, 5, 0)
+    torch.cuda.synchronize()
+    assert torch.equal(out, torch.cat([a, b], dim=1))
+    x = torch.randn(5000, 24, device="cuda")
+    wsb = ctypes.c_int64()
+    L.call("mgx_reduce_workspace_bytes", 5000, 24, ctypes.byref(wsb))
+    ws = torch.empty(wsb.value // 4 + 1, device="cuda")
+    s = torch.empty(24, device="cuda")
+    L.call("mgx_colsum", x.data_ptr(), 5000, 24, ws.data_ptr(), s.data_ptr(), 0)
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(s.cpu().numpy(), x.double().sum(0).cpu().numpy(), rtol=1e-6,
+                               atol=1e-5)

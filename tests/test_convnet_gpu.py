@@ -1,0 +1,159 @@
+"""Whole convolution nets through bind/forward/backward and the
+data-parallel step (configs 3-5), against oracle/convnet.py (float64,
+operands of every tensor-core contraction rounded to bf16 like the device).
+
+Parity here is unpinned by the reference (it has no conv ops).  Stated
+tolerance for gradients: |device - oracle| <= 2e-2 * max|oracle| + rtol 2e-2
+(bf16 operand rounding of the output gradients compounds through the layers;
+the oracle rounds forward operands only), outputs rtol 1e-3 / atol 1e-4."""
+
+import numpy as np
+import pytest
+
+from oracle import convnet as oc
+
+pytestmark = pytest.mark.gpu
+
+
+def mini_inception(classes=10):
+    from paper_1512_01274_b200 import nets, symbol
+    net = symbol.variable("data")
+    net = nets._conv_factory(net, 16, (3, 3), "1", s=(2, 2), p=(1, 1))
+    net = symbol.apply("Pooling", {"kernel": (3, 3), "stride": (2, 2), "pool_type": "max"}, [net],
+                       name="pool_1")
+    net = nets._inception_a(net, 8, 8, 16, 8, 8, "avg", 8, "3a")
+    net = nets._inception_b(net, 8, 16, 8, 8, "3c")
+    net = nets._inception_a(net, 8, 8, 8, 8, 8, "max", 8, "5b")
+    net = symbol.apply("Pooling", {"kernel": (1, 1), "pool_type": "avg", "global_pool": True},
+                       [net], name="global_pool")
+    net = symbol.apply("Flatten", {}, [net], name="flatten")
+    net = symbol.apply("FullyConnected", {"num_hidden": classes}, [net], name="fc1")
+    return symbol.apply("SoftmaxOutput", {}, [net], name="softmax")
+
+
+def _bind_net(engine, g, data_shape, seed=0):
+    from paper_1512_01274_b200 import symbol
+    from paper_1512_01274_b200 import tensor as tmod
+    from paper_1512_01274_b200.executor import bind
+    from paper_1512_01274_b200.train import aux_names, init_aux, init_params, param_names
+    b = data_shape[0]
+    shapes, _ = symbol.infer_shape(g, {"data": data_shape, "label": (b,)})
+    rs = np.random.RandomState(seed)
+    x = rs.randn(*data_shape).astype(np.float32)
+    lab = rs.randint(0, shapes[param_names(g)[-1]][0], b).astype(np.float32)
+    p0 = init_params(g, shapes, seed)
+    a0 = init_aux(g, shapes)
+    names = param_names(g)
+    args = {"data": tmod.from_host(data_shape, "float32", x, engine=engine),
+            "label": tmod.from_host((b,), "float32", lab, engine=engine)}
+    for n in names:
+        args[n] = tmod.from_host(shapes[n], "float32", p0[n], engine=engine)
+    for n in aux_names(g):
+        args[n] = tmod.from_host(shapes[n], "float32", a0[n], engine=engine)
+    grads = {n: tmod.zeros(shapes[n], engine=engine) for n in names}
+    ex = bind(g, args, {n: "write" for n in names}, grads, engine=engine)
+    values = {"data": x, "label": lab, **p0, **a0}
+    return ex, args, grads, values, names
+
+
+def _check_net(engine, g, data_shape):
+    from paper_1512_01274_b200 import tensor as tmod
+    from paper_1512_01274_b200.train import aux_names
+    ex, args, grads, values, names = _bind_net(engine, g, data_shape)
+    ex.forward()
+    ex.backward()
+    outs, g_want, aux_want = oc.run_graph(g, values, wrt=names, bf16_operands=True)
+    p = tmod.to_numpy(ex.outputs[0])
+    np.testing.assert_allclose(p, outs["softmax"], rtol=1e-3, atol=1e-4)
+    for n in names:
+        want = g_want[n]
+        # conv biases in front of a BatchNorm have an exactly-zero gradient:
+        # the device returns fp32 rounding noise there (absolute floor 1e-6)
+        scale = float(np.abs(want).max())
+        np.testing.assert_allclose(tmod.to_numpy(grads[n]), want, rtol=2e-2,
+                                   atol=2e-2 * scale + 1e-6, err_msg=n)
+    for n in aux_names(g):
+        np.testing.assert_allclose(tmod.to_numpy(args[n]), aux_want[n], rtol=1e-4, atol=1e-5,
+                                   err_msg=n)
+    return ex, grads, names
+
+
+def test_lenet_gradients_match_oracle(engine):
+    from paper_1512_01274_b200 import nets
+    _check_net(engine, nets.lenet(10), (16, 28, 28, 1))
+
+
+def test_mini_inception_gradients_match_oracle(engine):
+    _check_net(engine, mini_inception(), (4, 32, 32, 3))
+
+
+def test_convnet_step_is_deterministic(engine):
+    """Fixed-order reductions everywhere: two identical passes give
+    bitwise-identical gradients."""
+    from paper_1512_01274_b200 import tensor as tmod
+    ex, args, grads, values, names = _bind_net(engine, mini_inception(), (4, 32, 32, 3))
+    ex.forward()
+    ex.backward()
+    first = {n: tmod.to_numpy(grads[n]).copy() for n in names}
+    ex.forward()
+    ex.backward()
+    for n in names:
+        np.testing.assert_array_equal(tmod.to_numpy(grads[n]), first[n], err_msg=n)
+
+
+def test_lenet_data_parallel_step_matches_single_worker(engine):
+    """W=2 workers of 16 images through the device KVStore == the SGD update
+    computed from the oracle's per-worker gradients (tolerance as above)."""
+    from paper_1512_01274_b200 import nets, symbol
+    from paper_1512_01274_b200 import tensor as tmod
+    from paper_1512_01274_b200.kvstore import KVStore
+    from paper_1512_01274_b200.optim import SGDConfig, make_sgd_updater
+    from paper_1512_01274_b200.train import DataParallelStep, init_aux, init_params
+    g = nets.lenet(10)
+    shard = (16, 28, 28, 1)
+    shapes, _ = symbol.infer_shape(g, {"data": shard, "label": (16,)})
+    p0 = init_params(g, shapes, 3)
+    kv = KVStore(1, 2, engine=engine)
+    step = DataParallelStep(g, kv, {"data": shard, "label": (16,)}, p0, engine=engine)
+    kv.set_updater(make_sgd_updater(SGDConfig(0.05, 0.9, 1e-4), scale=2))
+    rs = np.random.RandomState(11)
+    xs = rs.randn(32, 28, 28, 1).astype(np.float32)
+    ls = rs.randint(0, 10, 32).astype(np.float32)
+    step.step({w: (xs[16 * w:16 * (w + 1)], ls[16 * w:16 * (w + 1)]) for w in step.workers})
+    kv.round_barrier()
+    engine.wait_all()
+    total = {}
+    for w in range(2):
+        vals = {"data": xs[16 * w:16 * (w + 1)], "label": ls[16 * w:16 * (w + 1)], **p0,
+                **init_aux(g, shapes)}
+        _o, gw, _a = oc.run_graph(g, vals, wrt=step.names, bf16_operands=True)
+        for n in step.names:
+            total[n] = total.get(n, 0) + gw[n]
+    for n in step.names:
+        gmean = total[n] / 2
+        want = p0[n] - 0.05 * (gmean + 1e-4 * p0[n])  # first step: v = -eta*(g + wd*w)
+        got = tmod.to_numpy(step.args[0][n])
+        scale = 0.05 * (float(np.abs(gmean).max()) or 1.0)
+        np.testing.assert_allclose(got, want, rtol=1e-3, atol=3e-2 * scale, err_msg=n)
+    kv.close()
+
+
+def test_inception_bn_full_size_runs(engine):
+    """The config-5 graph binds and trains at its real spatial size (small
+    batch): finite loss that goes down over a few steps on a fixed batch."""
+    from paper_1512_01274_b200 import nets
+    from paper_1512_01274_b200 import tensor as tmod
+    from paper_1512_01274_b200.optim import SGDConfig, sgd_step
+    ex, args, grads, values, names = _bind_net(engine, nets.inception_bn(1000), (4, 224, 224, 3))
+    vel = {n: tmod.zeros(grads[n].shape, engine=engine) for n in names}
+    lab = values["label"].astype(np.int64)
+    losses = []
+    for _ in range(4):
+        ex.forward()
+        ex.backward()
+        p = tmod.to_numpy(ex.outputs[0])
+        losses.append(float(-np.log(np.maximum(p[np.arange(4), lab], 1e-12)).mean()))
+        for n in names:
+            sgd_step(args[n], grads[n], vel[n], vel[n], SGDConfig(0.01, 0.9, 1e-4))
+    assert np.all(np.isfinite(losses))
+    assert losses[-1] < losses[0]
