@@ -1,21 +1,25 @@
-"""Benchmark: data-parallel training step (config-1 MLP) over the device
-KVStore, plus the KVStore push+pull bus bandwidth sweep.
+"""Benchmark: the data-parallel training step over the device KVStore.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config inception_bn|alexnet|lenet|mlp] [--no-extra]
 
-N>1 is launched by the driver under torchrun (one rank per GPU, NCCL only
+N>1 is launched by the driver under torchrun (one rank per GPU; NCCL only
 for host-side barriers and max-over-ranks; the KVStore data path is the
 fused P2P kernel).  Prints ONE JSON line on rank 0.
 
-A step = every GPU runs forward + backward of the config-1 MLP
-(784-128-64-10, SoftmaxOutput) on its batch of 100, then one KVStore round
-(tree-reduce gradients over all GPUs, momentum SGD on the owner shard,
-broadcast weights).  Weak scaling: 100 images per GPU per step.
+Headline (BASELINE.json metric "train images/sec at 1/2/4/8 B200", quoted on
+config 5): Inception-BN, synthetic 224x224x3 images, batch 64 per GPU, bf16
+tensor-core convolutions (fp32 activations, BatchNorm, softmax; fp32 master
+weights in the KVStore), momentum SGD.  A step = every GPU runs forward +
+backward on its 64 images, then one KVStore round (tree-reduce gradients
+over all GPUs, SGD on the owner shard, broadcast weights).  Weak scaling.
 
-value : device-resident step (whole step captured as one CUDA graph),
-        timed with CUDA events per step, L2 flushed between steps
-e2e   : the public API per step -- load_host of the batch from pinned host
-        memory, DataParallelStep.step(), D2H of the softmax output
+value : device-resident step (whole step captured as one CUDA graph), CUDA
+        events per step on the step's stream, L2 flushed between steps
+e2e   : the public API per step -- the batch from pinned host memory,
+        DataParallelStep.step(), D2H of the softmax output, sync
+Also reported: the other configurations (MLP config 1 with its pinned
+reference, LeNet, AlexNet-style) and the KVStore push+pull sweep (config 2).
 """
 
 from __future__ import annotations
@@ -24,7 +28,6 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import time
 
@@ -33,21 +36,35 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-PER_GPU_BATCH = 100
-HIDDEN, CLASSES, DIM = [128, 64], 10, 784
 ETA, MOM, WD = 0.05, 0.9, 1e-4
 METRIC = "train images/sec"
-WORKLOAD = ("config-1 MLP 784-128-64-10 SoftmaxOutput, batch 100 per GPU, momentum SGD "
-            "(lr 0.05, mom 0.9, wd 1e-4), kvstore device (fused P2P reduce+SGD+broadcast)")
+
+CONFIGS = {
+    "mlp": dict(batch=100, image=(784,), classes=10, dense="fp32", dtype="fp32",
+                workload="config-1 MLP 784-128-64-10 SoftmaxOutput, batch 100 per GPU, momentum "
+                         "SGD (lr 0.05, mom 0.9, wd 1e-4), exact-order fp32 kernels, kvstore "
+                         "device (fused P2P reduce+SGD+broadcast)"),
+    "lenet": dict(batch=128, image=(28, 28, 1), classes=10, dense="bf16", dtype="bf16",
+                  workload="config-3 LeNet (conv5x5x20-tanh-pool, conv5x5x50-tanh-pool, fc500, "
+                           "fc10), synthetic 28x28x1, batch 128 per GPU, kvstore device"),
+    "alexnet": dict(batch=128, image=(224, 224, 3), classes=1000, dense="bf16", dtype="bf16",
+                    workload="config-4 AlexNet-style (5 conv, fc6 4096x9216, fc7, fc8; 62M params), "
+                             "synthetic 224x224x3, batch 128 per GPU, kvstore device"),
+    "inception_bn": dict(batch=64, image=(224, 224, 3), classes=1000, dense="bf16", dtype="bf16",
+                         workload="config-5 Inception-BN (MXNet symbol, 69 conv+BN+ReLU, 10 "
+                                  "inception concats), synthetic 224x224x3, batch 64 per GPU, bf16 "
+                                  "tensor-core convs, momentum SGD, kvstore device"),
+}
 
 
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             p = json.load(f)
-        return p["hbm_gbs"], p["bf16_tflops"], "measured"
+        return p["hbm_gbs"], p["bf16_tflops"], p.get("bf16_tflops_sustained", p["bf16_tflops"]), \
+            "measured"
     except Exception:  # noqa: BLE001
-        return 6650.0, 1590.0, "fallback"
+        return 6650.0, 1590.0, 1400.0, "fallback"
 
 
 # ---------------------------------------------------------------- clocks
@@ -130,49 +147,124 @@ def barrier(world: int):
         dist.barrier()
 
 
+# -------------------------------------------------------- configurations
+
+def build_graph(name: str):
+    from paper_1512_01274_b200 import nets, symbol
+    from paper_1512_01274_b200.train import mlp
+    symbol.reset_names()
+    if name == "mlp":
+        return mlp([128, 64], 10)
+    return nets.NETS[name](CONFIGS[name]["classes"])
+
+
+def synthetic(name: str, n: int, seed: int):
+    """Seeded synthetic batch of ``n`` images: config 1 as SURVEY §8d
+    (RandomState.rand features, randint labels); conv nets randn images."""
+    cfg = CONFIGS[name]
+    if name == "mlp":
+        from oracle import step as ostep
+        return ostep.cfg1_data(n, seed=seed)
+    rs = np.random.RandomState(seed)
+    x = rs.randn(n, *cfg["image"]).astype(np.float32)
+    y = rs.randint(0, cfg["classes"], n).astype(np.float32)
+    return x, y
+
+
+def train_flops_per_image(name: str) -> float:
+    """Tensor-core FLOPs of one training image: forward contractions, plus
+    weight gradients (same FLOPs), plus data gradients for every layer but
+    the first (whose input needs no gradient)."""
+    from paper_1512_01274_b200 import nets
+    g = build_graph(name)
+    b = CONFIGS[name]["batch"]
+    given = {"data": (b,) + CONFIGS[name]["image"], "label": (b,)}
+    fwd = nets.forward_flops(g, given)
+    from paper_1512_01274_b200 import symbol
+    _a, named = symbol.infer_shape(g, given)
+    first = next(n for n in g.topo_nodes() if n.op in ("Convolution", "FullyConnected"))
+    from math import prod
+    w = named[first.inputs[1][0].name]
+    first_fl = 2 * prod(named[first.name]) * (prod(w[1:]) if first.op == "Convolution" else 1)
+    if first.op == "FullyConnected":
+        first_fl = 2 * named[first.name][0] * prod(w)
+    return (3 * fwd - first_fl) / b
+
+
 # ------------------------------------------------------- reference arm
 
-def cpu_step_sample(nworkers: int, seconds: float, steps: int = None):
-    """The oracle port of the reference step (oracle/step.py) on host cores:
-    nworkers shards of 100 images, forward/backward per shard, tree merge and
-    the SGD updater per key.  Returns (images/s, steps, seconds)."""
-    from oracle import numerics as nm
-    from oracle import step as ostep
-    feats, labels = ostep.cfg1_data(PER_GPU_BATCH * nworkers, seed=0)
-    params = ostep.init_params(HIDDEN, CLASSES, DIM, 0)
-    vel = {k: np.zeros_like(v) for k, v in params.items()}
+def cpu_sample(name: str, seconds: float = None, steps: int = None, nworkers: int = 1):
+    """The CPU oracle port of one training step on host cores.
+
+    mlp: oracle/step.py (numpy restatement of the reference step, pinned
+    bitwise to the reference; single thread, like numpy's ufunc reductions).
+    conv nets: oracle/convnet.py float64 torch-CPU restatement on a small
+    sample of images per step (the reference has no conv operators; this is
+    the port the GPU path is checked against), all host threads.
+    Returns (images/s, steps, seconds, cores, sample description)."""
+    if name == "mlp":
+        from oracle import numerics as nm
+        from oracle import step as ostep
+        per = CONFIGS["mlp"]["batch"]
+        feats, labels = ostep.cfg1_data(per * nworkers, seed=0)
+        params = ostep.init_params([128, 64], 10, 784, 0)
+        vel = {k: np.zeros_like(v) for k, v in params.items()}
+        done, t0 = 0, time.perf_counter()
+        while True:
+            grads = []
+            for w in range(nworkers):
+                sl = slice(w * per, (w + 1) * per)
+                grads.append(ostep.mlp_forward_backward(params, [128, 64], feats[sl], labels[sl])[1])
+            for k in params:
+                total = nm.kv_merge([g[k] for g in grads])
+                params[k], vel[k] = nm.kv_updater(params[k], total, vel[k], ETA, MOM, WD, nworkers)
+            done += 1
+            el = time.perf_counter() - t0
+            if (steps is not None and done >= steps) or (steps is None and el >= seconds and done >= 3):
+                return (done * per * nworkers / el, done, el, 1,
+                        f"{done} steps x {nworkers} shards of {per} images, oracle/step.py numpy "
+                        "restatement of the reference step (single thread)")
+    import torch
+    from oracle import convnet as oc
+    from paper_1512_01274_b200 import symbol
+    from paper_1512_01274_b200.train import init_aux, init_params, param_names
+    g = build_graph(name)
+    sample = 8 if name == "lenet" else 2
+    given = {"data": (sample,) + CONFIGS[name]["image"], "label": (sample,)}
+    shapes, _ = symbol.infer_shape(g, given)
+    x, y = synthetic(name, sample, 0)
+    vals = {"data": x, "label": y, **init_params(g, shapes, 0), **init_aux(g, shapes)}
+    names = param_names(g)
     done, t0 = 0, time.perf_counter()
     while True:
-        grads = []
-        for w in range(nworkers):
-            sl = slice(w * PER_GPU_BATCH, (w + 1) * PER_GPU_BATCH)
-            grads.append(ostep.mlp_forward_backward(params, HIDDEN, feats[sl], labels[sl])[1])
-        for k in params:
-            total = nm.kv_merge([g[k] for g in grads])
-            params[k], vel[k] = nm.kv_updater(params[k], total, vel[k], ETA, MOM, WD, nworkers)
+        oc.run_graph(g, vals, wrt=names)
         done += 1
         el = time.perf_counter() - t0
-        if (steps is not None and done >= steps) or (steps is None and el >= seconds and done >= 3):
-            return done * PER_GPU_BATCH * nworkers / el, done, el
+        if (steps is not None and done >= steps) or (steps is None and el >= seconds and done >= 1):
+            return (done * sample / el, done, el, torch.get_num_threads(),
+                    f"{done} forward+backward passes of {sample} images, oracle/convnet.py float64 "
+                    "torch-CPU restatement (the reference has no conv operators)")
 
 
 def run_reference(args, world, rank):
     if rank != 0:
         return
     n = args.gpus
+    name = args.config
     for _ in range(args.warmup):
-        cpu_step_sample(n, 0, steps=1)
-    value, steps, el = cpu_step_sample(n, 0, steps=args.steps)
+        cpu_sample(name, steps=1, nworkers=n)
+    value, steps, el, cores, sample = cpu_sample(name, steps=args.steps, nworkers=n)
+    cfg = CONFIGS[name]
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": n,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
-        "data": "synthetic (RandomState(0).rand features, randint labels)",
-        "config": {"workload": WORKLOAD, "global_batch": PER_GPU_BATCH * n,
-                   "per_gpu_batch": PER_GPU_BATCH, "parallelism": f"dp{n}"},
-        "cpu_baseline": {"value": value, "unit": "images/s", "cores": 1, "kind": "port",
-                         "sample": f"{steps} steps x {n} worker shards of 100 images, "
-                                   "oracle/step.py restatement (numpy, single thread)"},
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32"
+        if name == "mlp" else "fp64",
+        "data": "synthetic", "config": {"workload": cfg["workload"],
+                                        "global_batch": cfg["batch"] * n,
+                                        "per_gpu_batch": cfg["batch"], "parallelism": f"dp{n}"},
+        "cpu_baseline": {"value": value, "unit": "images/s", "cores": cores, "kind": "port",
+                         "sample": sample},
         "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -181,42 +273,55 @@ def run_reference(args, world, rank):
 
 # ------------------------------------------------------------- our arm
 
-def algorithmic(label: str, ex_shapes) -> tuple:
-    """(bytes, flops) a program instruction must move/compute, from its label."""
-    return ex_shapes.get(label, (0, 0))
+KERNEL_OF = {}  # opcode -> kernel family name, filled lazily
 
 
-def run_ours(args, world, rank, local):
+def kernel_family(op: int) -> str:
+    from paper_1512_01274_b200 import _lib as L
+    if not KERNEL_OF:
+        KERNEL_OF.update({
+            L.OP_GEMM_TC_EX: "tc_gemm_bf16 (tcgen05)", L.OP_GEMM_TC: "tc_gemm_bf16 (tcgen05)",
+            L.OP_IM2COL: "im2col_bf16", L.OP_COL2IM: "col2im", L.OP_CAST_BF16: "cast_bf16",
+            L.OP_BN_STATS: "bn_stats", L.OP_BN_APPLY: "bn_apply", L.OP_BN_BWD_REDUCE: "bn_bwd_reduce",
+            L.OP_BN_BWD_DX: "bn_bwd_dx", L.OP_POOL_FWD: "pool_fwd", L.OP_POOL_BWD: "pool_bwd",
+            L.OP_CHAN_COPY: "concat_copy", L.OP_COLSUM: "colsum", L.OP_ACT_FWD: "act_fwd",
+            L.OP_ACT_BWD: "act_bwd", L.OP_GEMM_PW: "gemm_pairwise", L.OP_GEMM_SEQ: "gemm_sequential",
+            L.OP_DW_DB: "fc_dw_db", L.OP_SOFTMAX_FWD: "softmax_fwd", L.OP_SOFTMAX_BWD: "softmax_bwd",
+            L.OP_COPY: "copy", L.OP_FILL: "fill", L.OP_EW: "elementwise", L.OP_AXPY: "axpy"})
+    return KERNEL_OF.get(op, f"op{op}")
+
+
+def run_config(name, args, world, rank, local, eng, steps, warmup, with_e2e=True,
+               with_profile=True):
+    """Measure one configuration; returns a dict (rank 0 meaningful)."""
     import torch
-    from oracle import step as ostep
     from paper_1512_01274_b200 import _lib as L
     from paper_1512_01274_b200 import symbol
     from paper_1512_01274_b200 import tensor as tmod
-    from paper_1512_01274_b200.engine import Engine
     from paper_1512_01274_b200.kvstore import KVStore
     from paper_1512_01274_b200.optim import SGDConfig, make_sgd_updater
-    from paper_1512_01274_b200.train import DataParallelStep, init_params, mlp
+    from paper_1512_01274_b200.train import DataParallelStep, init_params
 
-    torch.cuda.set_device(local)
-    eng = Engine(device=local)
+    cfg = CONFIGS[name]
+    per = cfg["batch"]
     distributed = world > 1
     kv = KVStore(1, world, engine=eng, distributed=distributed)
-    symbol.reset_names()
-    g = mlp(HIDDEN, CLASSES)
-    given = {"data": (PER_GPU_BATCH, DIM), "label": (PER_GPU_BATCH,)}
+    g = build_graph(name)
+    given = {"data": (per,) + cfg["image"], "label": (per,)}
     shapes, _ = symbol.infer_shape(g, given)
-    step = DataParallelStep(g, kv, given, init_params(g, shapes, 0), engine=eng)
+    step = DataParallelStep(g, kv, given, init_params(g, shapes, 0), engine=eng,
+                            dense=cfg["dense"])
     kv.set_updater(make_sgd_updater(SGDConfig(ETA, MOM, WD), scale=world))
     w = step.workers[0]
-    feats, labels = ostep.cfg1_data(PER_GPU_BATCH * world, seed=0)
-    sl = slice(w * PER_GPU_BATCH, (w + 1) * PER_GPU_BATCH)
-    pin_x = torch.from_numpy(feats[sl].copy()).pin_memory()
-    pin_y = torch.from_numpy(labels[sl].copy()).pin_memory()
+    feats, labels = synthetic(name, per * world, 0)
+    sl = slice(w * per, (w + 1) * per)
+    pin_x = torch.from_numpy(np.ascontiguousarray(feats[sl])).pin_memory()
+    pin_y = torch.from_numpy(np.ascontiguousarray(labels[sl])).pin_memory()
     step.load(w, pin_x, pin_y)
     eng.wait_all()
 
-    # ---- device-resident step: warm up eagerly, then capture the whole step
-    for _ in range(max(args.warmup, 3)):
+    # ---- device-resident step: warm up eagerly, capture the whole step
+    for _ in range(max(warmup, 3)):
         step.step()
     eng.wait_all()
     step.capture()
@@ -225,19 +330,16 @@ def run_ours(args, world, rank, local):
     eng.wait_all()
     barrier(world)
     flush = torch.empty(64 << 20, dtype=torch.float32, device=f"cuda:{local}")  # 256 MB > L2
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    launches_per_step = step.execs[w].num_instructions + 1
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
     with ClockSampler(local) as clocks:
         torch.cuda.synchronize()
         barrier(world)
         align = torch.zeros(1, device=f"cuda:{local}") if world > 1 else None
-        for i in range(args.steps):
+        for i in range(steps):
             L.call("mgx_fill", flush.data_ptr(), flush.numel(), float(i), eng.stream_handle)
             if align is not None:
-                # untimed: re-align the ranks on-device after their independent
-                # L2 flushes, so the step's in-kernel barrier does not charge
-                # flush skew to the timed region
+                # untimed: re-align the ranks on-device after their L2 flushes
                 with torch.cuda.stream(eng.stream):
                     torch.distributed.all_reduce(align)
             starts[i].record(eng.stream)
@@ -247,47 +349,81 @@ def run_ours(args, world, rank, local):
         barrier(world)
     ms_local = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
     ms_total = max_over_ranks(ms_local, world)
-    ms_per_step = ms_total / args.steps
-    value = PER_GPU_BATCH * world * args.steps / (ms_total / 1e3)
+    res = {"workload": cfg["workload"], "per_gpu_batch": per, "global_batch": per * world,
+           "ms_per_step": ms_total / steps,
+           "value": per * world * steps / (ms_total / 1e3), "clocks": clocks.summary(),
+           "dtype": cfg["dtype"]}
+    ex = step.execs[w]
+    res["kernels_per_step"] = ex.kernel_count() + kv_launches(kv)
+    res["plan_bytes"] = step.plan_bytes
+    res["scratch_bytes"] = getattr(ex, "scratch_bytes", 0)
 
     # ---- e2e through the public API: host batch in, softmax output out
-    for ex in step.execs.values():
-        ex._use_graph = True
-    h2d = pin_x.numel() * 4 + pin_y.numel() * 4
-    d2h = PER_GPU_BATCH * CLASSES * 4
-    out_pin = torch.empty(PER_GPU_BATCH, CLASSES, dtype=torch.float32, pin_memory=True)
-    y = step.execs[w].outputs[0]
+    if with_e2e:
+        for e in step.execs.values():
+            e._use_graph = True
+        h2d = pin_x.numel() * 4 + pin_y.numel() * 4
+        d2h = per * cfg["classes"] * 4
+        out_pin = torch.empty(per, cfg["classes"], dtype=torch.float32, pin_memory=True)
+        y = ex.outputs[0]
 
-    def e2e_step():
-        step.step({w: (pin_x, pin_y)})
-        eng.push(lambda: L.call("mgx_memcpy_async", out_pin.data_ptr(), y.ptr, d2h,
-                                eng.stream_handle), reads=[y.tag])
-        eng.wait_for(y.tag)
+        def e2e_step():
+            step.step({w: (pin_x, pin_y)})
+            eng.push(lambda: L.call("mgx_memcpy_async", out_pin.data_ptr(), y.ptr, d2h,
+                                    eng.stream_handle), reads=[y.tag])
+            eng.wait_for(y.tag)
 
-    for _ in range(max(args.warmup, 3)):
-        e2e_step()
-    barrier(world)
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(eng.stream)
-    for _ in range(args.steps):
-        e2e_step()
-    e1.record(eng.stream)
-    torch.cuda.synchronize()
-    e2e_ms = max_over_ranks(e0.elapsed_time(e1), world)
-    e2e_value = PER_GPU_BATCH * world * args.steps / (e2e_ms / 1e3)
-    barrier(world)
+        for _ in range(max(warmup, 3)):
+            e2e_step()
+        barrier(world)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(eng.stream)
+        for _ in range(steps):
+            e2e_step()
+        e1.record(eng.stream)
+        torch.cuda.synchronize()
+        e2e_ms = max_over_ranks(e0.elapsed_time(e1), world)
+        res["e2e"] = {"value": per * world * steps / (e2e_ms / 1e3), "unit": "images/s",
+                      "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                      "path": "DataParallelStep.step(host pinned batch) + D2H softmax output + sync"}
+        barrier(world)
 
-    # ---- roofline: per-kernel device time of the step's instructions (eager,
-    # events on the launching stream), averaged over K profiled steps
-    ex = step.execs[w]
-    prof = {}
-    for _ in range(args.steps):
-        for lbl, ms in ex.profile():
-            prof.setdefault(lbl, []).append(ms)
-    kv_ms = []
+    # ---- roofline: per-instruction device time (events captured between
+    # instructions on the launching stream), aggregated per kernel family
+    if with_profile:
+        nprof = max(1, min(steps, 5))
+        times = [0.0] * ex.num_instructions
+        for _ in range(nprof):
+            for idx, (_lbl, ms) in enumerate(ex.profile()):
+                times[idx] += ms / nprof
+        fam_ms, fam_bytes, fam_flops = {}, {}, {}
+        for idx, ms in enumerate(times):
+            fam = kernel_family(ex.instr_ops[idx])
+            fam_ms[fam] = fam_ms.get(fam, 0.0) + ms
+            fam_bytes[fam] = fam_bytes.get(fam, 0) + ex.instr_costs[idx][0]
+            fam_flops[fam] = fam_flops.get(fam, 0) + ex.instr_costs[idx][1]
+        res["per_kernel_ms"] = {k: round(v, 5) for k, v in sorted(fam_ms.items(),
+                                                                 key=lambda kv: -kv[1])}
+        res["profiled_step_ms"] = sum(fam_ms.values())
+        res["_fam"] = (fam_ms, fam_bytes, fam_flops)
+
+    res["kvstore_round_ms"] = kv_round_ms(step, kv, eng, steps)
+    res["kv_bytes_per_step"] = 4 * sum(int(np.prod(shapes[n])) for n in step.names)
+    kv.close()
+    return res
+
+
+def kv_launches(kv) -> int:
+    return 1
+
+
+def kv_round_ms(step, kv, eng, steps):
+    import torch
+    w = step.workers[0]
     ka, kb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    for _ in range(args.steps):
+    ms = []
+    for _ in range(max(1, min(steps, 10))):
         for i in range(len(step.names)):
             kv.push(i, step.grads[w][step.names[i]], w)
         ka.record(eng.stream)
@@ -295,65 +431,37 @@ def run_ours(args, world, rank, local):
             kv._flush_locked()
         kb.record(eng.stream)
         torch.cuda.synchronize()
-        kv_ms.append(ka.elapsed_time(kb))
-    avg = {k: sum(v) / len(v) for k, v in prof.items()}
-    avg["kv_round"] = sum(kv_ms) / len(kv_ms)
-    hbm, _bf16, src = peaks()
-    traffic = {lbl: cost[0] for lbl, cost in zip(ex.instr_labels, ex.instr_costs)}
-    key_elems = sum(int(np.prod(shapes[n])) for n in step.names)
-    # per rank and round: read the W gradient shards, w and v of its shard;
-    # write v and W replicas of the new weights
-    shard = key_elems / world
-    traffic["kv_round"] = int(4 * shard * (2 * world + 3))
-    dom = max(avg, key=avg.get)
-    dom_bytes = traffic.get(dom)
-    achieved = dom_bytes / (avg[dom] * 1e-3) / 1e9 if dom_bytes else None
-    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm,
-                "peak_source": src, "unit": "GB/s",
-                "frac": (achieved / hbm) if achieved else None,
-                "traffic": None, "kernel_ms": avg[dom],
-                "step_share": avg[dom] / sum(avg.values()),
-                "per_kernel_ms": avg}
+        ms.append(ka.elapsed_time(kb))
+    return sum(ms) / len(ms)
 
-    # ---- KVStore sweep: push+pull+update rounds on big keys (busbw)
-    kvres = kv_sweep(args, eng, world, rank, distributed)
 
-    # ---- CPU baseline (rank 0, N=1 only): oracle port, bounded sample
-    cpu = None
-    if rank == 0 and world == 1:
-        v, nsteps, el = cpu_step_sample(1, args.cpu_seconds)
-        cpu = {"value": v, "unit": "images/s", "cores": 1, "kind": "port",
-               "sample": f"{nsteps} steps of 100 images ({el:.1f} s), oracle/step.py "
-                         "restatement of the reference step (numpy, single thread)"}
-    kv.close()
-    if rank == 0:
-        line = {
-            "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32",
-            "data": "synthetic (RandomState(0).rand features, randint labels; resident batch)",
-            "config": {"workload": WORKLOAD, "global_batch": PER_GPU_BATCH * world,
-                       "per_gpu_batch": PER_GPU_BATCH, "parallelism": f"dp{world}",
-                       "l2": "flushed between timed steps (256 MB device write, untimed)",
-                       "step": "forward+backward+KVStore round captured as one CUDA graph",
-                       "program_kernel": step.execs[w].uses_program_kernel},
-            "e2e": {"value": e2e_value, "unit": "images/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h,
-                    "path": "DataParallelStep.step(host pinned batch) + D2H softmax output + sync"},
-            "gpu_launches": launches_per_step * args.steps,
-            "roofline": roofline, "cpu_baseline": cpu, "kvstore": kvres,
-            "clocks": clocks.summary(),
-        }
-        print(json.dumps(line), flush=True)
+def roofline_of(res):
+    """Roofline object for the dominant kernel family of the step."""
+    hbm, bf16, bf16_sus, src = peaks()
+    fam_ms, fam_bytes, fam_flops = res["_fam"]
+    dom = max(fam_ms, key=fam_ms.get)
+    ms = fam_ms[dom]
+    tensor = dom.startswith("tc_gemm")
+    if tensor:
+        achieved = fam_flops[dom] / (ms * 1e-3) / 1e12
+        peak, unit = bf16_sus, "TFLOP/s"
+        psrc = f"{src} bf16 sustained (kernel timed inside the step)"
+    else:
+        achieved = fam_bytes[dom] / (ms * 1e-3) / 1e9
+        peak, unit = hbm, "GB/s"
+        psrc = f"{src} HBM copy"
+    return {"bound": "tensor" if tensor else "hbm", "kernel": dom, "achieved": achieved,
+            "peak": peak, "peak_source": psrc, "unit": unit, "frac": achieved / peak,
+            "traffic": None, "kernel_ms_per_step": ms, "step_share": ms / sum(fam_ms.values()),
+            "algorithmic_per_step": fam_flops[dom] if tensor else fam_bytes[dom]}
 
 
 def kv_sweep(args, eng, world, rank, distributed):
     import torch
-    from paper_1512_01274_b200 import tensor as tmod
     from paper_1512_01274_b200.kvstore import KVStore
     from paper_1512_01274_b200.optim import SGDConfig, make_sgd_updater
     out = []
-    hbm, _b, _s = peaks()
+    hbm = peaks()[0]
     for mb in args.kv_mb:
         n = (mb << 20) // 4
         kv = KVStore(1, world, engine=eng, distributed=distributed)
@@ -384,19 +492,72 @@ def kv_sweep(args, eng, world, rank, distributed):
             rec.update({"busbw_GBps": busbw, "nvlink_frac_of_900": busbw / 900.0,
                         "nvlink_frac_of_measured_770": busbw / 770.0})
         else:
-            # one worker: read g, w, v; write v, w -> 5 S bytes of HBM
             rec.update({"hbm_GBps": 5 * S / (ms * 1e-3) / 1e9,
                         "hbm_frac": 5 * S / (ms * 1e-3) / 1e9 / hbm})
         out.append(rec)
     return out
 
 
+def run_ours(args, world, rank, local):
+    import torch
+    from paper_1512_01274_b200.engine import Engine
+    torch.cuda.set_device(local)
+    eng = Engine(device=local)
+    name = args.config
+    head = run_config(name, args, world, rank, local, eng, args.steps, args.warmup)
+    roof = roofline_of(head)
+    flops_img = train_flops_per_image(name) if name != "mlp" else None
+    extra = {}
+    if not args.no_extra:
+        for other in ("mlp", "lenet", "alexnet", "inception_bn"):
+            if other == name:
+                continue
+            r = run_config(other, args, world, rank, local, eng, max(5, args.steps // 4),
+                           3, with_e2e=(other == "mlp"), with_profile=True)
+            rr = roofline_of(r)
+            extra[other] = {k: v for k, v in r.items() if k not in ("_fam",)}
+            extra[other]["roofline"] = {k: rr[k] for k in ("bound", "kernel", "achieved", "unit",
+                                                             "frac", "step_share")}
+    kvres = kv_sweep(args, eng, world, rank, world > 1)
+    cpu = None
+    if rank == 0 and world == 1:
+        v, nsteps, el, cores, sample = cpu_sample(name, seconds=args.cpu_seconds)
+        cpu = {"value": v, "unit": "images/s", "cores": cores, "kind": "port", "sample": sample}
+    if rank == 0:
+        cfg = CONFIGS[name]
+        tensor_tflops = (flops_img * head["value"] / world / 1e12) if flops_img else None
+        line = {
+            "metric": METRIC, "value": head["value"], "unit": "images/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": head["ms_per_step"],
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": cfg["dtype"],
+            "data": "synthetic (seeded randn images, randint labels; resident batch)",
+            "config": {"workload": cfg["workload"], "global_batch": cfg["batch"] * world,
+                       "per_gpu_batch": cfg["batch"], "parallelism": f"dp{world}",
+                       "l2": "flushed between timed steps (256 MB device write, untimed)",
+                       "step": "forward+backward+KVStore round captured as one CUDA graph"},
+            "e2e": head.get("e2e"),
+            "gpu_launches": head["kernels_per_step"] * args.steps,
+            "roofline": roof,
+            "step_tensor_tflops_per_gpu": tensor_tflops,
+            "per_kernel_ms": head.get("per_kernel_ms"),
+            "kvstore_round_ms": head["kvstore_round_ms"],
+            "kv_bytes_per_step": head["kv_bytes_per_step"],
+            "cpu_baseline": cpu, "kvstore": kvres, "clocks": head["clocks"],
+            "configs": extra,
+        }
+        print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--config", choices=tuple(CONFIGS), default="inception_bn")
+    ap.add_argument("--no-extra", action="store_true",
+                    help="skip the secondary configurations")
     ap.add_argument("--kv-mb", type=int, nargs="*", default=[64, 256])
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     args = ap.parse_args()

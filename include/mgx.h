@@ -171,11 +171,15 @@ int mgx_bn_bwd_dx(const float* dy, const float* x, const float* stats, const flo
 /* out[c] = sum over rows of x[r, c] (conv bias gradient). */
 int mgx_colsum(const float* x, int64_t M, int64_t C, void* ws, float* out, uintptr_t stream);
 /* Pooling, NHWC.  type 0 max (padding ignored), 1 avg (count_include_pad);
- * full != 0: 'full' convention (output size rounded up). */
+ * full != 0: 'full' convention (output size rounded up).  argmax (optional,
+ * max only, uint8 per output element, needs C % 4 == 0 and kh*kw <= 255):
+ * the window-local index of the first maximum, written by the forward and
+ * read by the backward instead of rescanning x. */
 int mgx_pool_forward(const float* x, float* y, const int64_t* geom, int full, int type,
-                     uintptr_t stream);
+                     void* argmax, uintptr_t stream);
 int mgx_pool_backward(const float* x, const float* y, const float* dy, float* dx,
-                      const int64_t* geom, int full, int type, uintptr_t stream);
+                      const int64_t* geom, int full, int type, const void* argmax,
+                      uintptr_t stream);
 /* dst[r, doff + c] = src[r, soff + c] for r < rows, c < cols (Concat). */
 int mgx_chan_copy(const float* src, int64_t lds, int64_t soff, float* dst, int64_t ldd,
                   int64_t doff, int64_t rows, int64_t cols, uintptr_t stream);
@@ -246,8 +250,8 @@ typedef struct mgx_instr {
 #define MGX_OP_BN_BWD_REDUCE 19 /* ptr0=dy ptr1=x ptr2=stats ptr3=ws ptr4=sums dims=M,C */
 #define MGX_OP_BN_BWD_DX 20   /* ptr0=dy ptr1=x ptr2=stats ptr3=sums ptr4=gamma    */
                               /* ptr5=dx dims=M,C                                  */
-#define MGX_OP_POOL_FWD 21    /* ptr0=x ptr1=y dims=geom,full act=type(0 max 1 avg) */
-#define MGX_OP_POOL_BWD 22    /* ptr0=x ptr1=y ptr2=dy ptr3=dx dims=geom,full act  */
+#define MGX_OP_POOL_FWD 21    /* ptr0=x ptr1=y ptr2=argmax dims=geom,full act=type */
+#define MGX_OP_POOL_BWD 22    /* ptr0=x ptr1=y ptr2=dy ptr3=dx ptr4=argmax dims=geom,full */
 #define MGX_OP_CHAN_COPY 23   /* ptr0=src ptr1=dst dims=rows,cols,lds,soff,ldd,doff */
 #define MGX_OP_COLSUM 24      /* ptr0=x ptr1=ws ptr2=out dims=M,C                  */
 #define MGX_OP_GEMM_TC_EX 25  /* ptr0=A ptr1=B ptr2=bias ptr3=C ptr4=workspace act */
@@ -275,6 +279,9 @@ int mgx_prog_time_levels(uint64_t prog, int32_t begin, int32_t end, uintptr_t st
                          double* ns_out);
 /* Per-instruction device time of one eager run of [begin,end) (profiling). */
 int mgx_prog_profile(uint64_t prog, int32_t begin, int32_t end, uintptr_t stream, float* ms_out);
+/* Number of kernel launches the range makes (captured once, not run). */
+int mgx_prog_kernel_count(uint64_t prog, int32_t begin, int32_t end, uintptr_t stream,
+                          int64_t* out);
 int mgx_prog_destroy(uint64_t prog);
 
 /* ------------------------------------------------------------- KVStore

@@ -51,6 +51,36 @@ def conv2d_nhwc(x, w, b, stride, pad):
     return y.permute(0, 2, 3, 1)
 
 
+class _Bf16Conv:
+    """Convolution whose three contractions see bf16-rounded operands, like
+    the device: forward bf16(x)*bf16(w); dX = bf16(dY) (*) bf16(w);
+    dW = bf16(x) (*) bf16(dY) (float64 accumulation)."""
+
+    @staticmethod
+    def apply(x, w, b, stride, pad):
+        torch = _torch()
+
+        class F(torch.autograd.Function):
+            @staticmethod
+            def forward(ctx, x, w):
+                xr, wr = bf16(x), bf16(w)
+                ctx.save_for_backward(xr, wr)
+                return conv2d_nhwc(xr, wr, None, stride, pad)
+
+            @staticmethod
+            def backward(ctx, dy):
+                from torch.nn.grad import conv2d_input, conv2d_weight
+                xr, wr = ctx.saved_tensors
+                dyr = bf16(dy).permute(0, 3, 1, 2)
+                xn, wn = xr.permute(0, 3, 1, 2), wr.permute(0, 3, 1, 2)
+                dx = conv2d_input(xn.shape, wn, dyr, stride=stride, padding=pad)
+                dw = conv2d_weight(xn, wn.shape, dyr, stride=stride, padding=pad)
+                return dx.permute(0, 2, 3, 1), dw.permute(0, 2, 3, 1)
+
+        y = F.apply(x, w)
+        return y + b if b is not None else y
+
+
 def batchnorm(x, gamma, beta, eps, fix_gamma):
     dims = tuple(range(x.dim() - 1))
     mean = x.mean(dim=dims)
@@ -83,8 +113,8 @@ def run_graph(g, values: Dict[str, np.ndarray], wrt=(), bf16_operands: bool = Fa
 
     Returns (node outputs by name, gradients of ``wrt`` by name, updated
     BatchNorm moving statistics by name).  ``bf16_operands`` rounds every
-    Convolution operand to bf16 on the forward pass (the backward of those
-    products then sees unrounded output gradients)."""
+    operand of the Convolution contractions (forward, data and weight
+    gradients) to bf16 like the device does."""
     torch = _torch()
     env = {}
     leaves = {}
@@ -94,7 +124,6 @@ def run_graph(g, values: Dict[str, np.ndarray], wrt=(), bf16_operands: bool = Fa
         if name in wrt:
             t.requires_grad_(True)
         leaves[name] = t
-    rnd = bf16 if bf16_operands else (lambda t: t)
     loss = None
     for n in g.topo_nodes():
         if n.is_variable:
@@ -102,8 +131,11 @@ def run_graph(g, values: Dict[str, np.ndarray], wrt=(), bf16_operands: bool = Fa
             continue
         ins = [env[id(src)] for src, _ in n.inputs]
         a = n.attrs
-        if n.op == "Convolution":
-            y = conv2d_nhwc(rnd(ins[0]), rnd(ins[1]), ins[2] if len(ins) > 2 else None,
+        if n.op == "Convolution" and bf16_operands:
+            y = _Bf16Conv.apply(ins[0], ins[1], ins[2] if len(ins) > 2 else None,
+                                _pair(a.get("stride", 1)), _pair(a.get("pad", 0)))
+        elif n.op == "Convolution":
+            y = conv2d_nhwc(ins[0], ins[1], ins[2] if len(ins) > 2 else None,
                             _pair(a.get("stride", 1)), _pair(a.get("pad", 0)))
         elif n.op == "FullyConnected":
             x2 = ins[0].reshape(ins[0].shape[0], -1)

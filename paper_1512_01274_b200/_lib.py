@@ -127,6 +127,7 @@ _SIGNATURES = {
                          c_vp], ctypes.c_int),
     "mgx_prog_profile": ([c_u64, c_i32, c_i32, c_uptr, ctypes.POINTER(c_f32)], ctypes.c_int),
     "mgx_prog_destroy": ([c_u64], ctypes.c_int),
+    "mgx_prog_kernel_count": ([c_u64, c_i32, c_i32, c_uptr, ctypes.POINTER(c_i64)], ctypes.c_int),
     "mgx_kv_round": ([ctypes.POINTER(KvRoundArgs), c_uptr], ctypes.c_int),
     "mgx_prog_error": ([ctypes.POINTER(c_u32)], ctypes.c_int),
     "mgx_prog_time_levels": ([c_u64, c_i32, c_i32, c_uptr, c_vp], ctypes.c_int),
@@ -144,8 +145,9 @@ _SIGNATURES = {
     "mgx_bn_bwd_reduce": ([c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_uptr], ctypes.c_int),
     "mgx_bn_bwd_dx": ([c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_uptr], ctypes.c_int),
     "mgx_colsum": ([c_vp, c_i64, c_i64, c_vp, c_vp, c_uptr], ctypes.c_int),
-    "mgx_pool_forward": ([c_vp, c_vp, c_vp, ctypes.c_int, ctypes.c_int, c_uptr], ctypes.c_int),
-    "mgx_pool_backward": ([c_vp, c_vp, c_vp, c_vp, c_vp, ctypes.c_int, ctypes.c_int, c_uptr],
+    "mgx_pool_forward": ([c_vp, c_vp, c_vp, ctypes.c_int, ctypes.c_int, c_vp, c_uptr],
+                         ctypes.c_int),
+    "mgx_pool_backward": ([c_vp, c_vp, c_vp, c_vp, c_vp, ctypes.c_int, ctypes.c_int, c_vp, c_uptr],
                           ctypes.c_int),
     "mgx_chan_copy": ([c_vp, c_i64, c_i64, c_vp, c_i64, c_i64, c_i64, c_i64, c_uptr], ctypes.c_int),
     "mgx_kv_max_grid": ([c_i32, c_i32, ctypes.POINTER(c_i32)], ctypes.c_int),

@@ -351,19 +351,43 @@ def _pool_infer(shapes, attrs):
     return [tuple(data)], [(data[0], ho, wo, data[3])]
 
 
+def _pool_argmax(node, x_shape, out_size, k, kind, ctx) -> Optional[int]:
+    """uint8 argmax side buffer of a max-pooling node (forward writes it,
+    backward reads it); None when the vectorised kernels do not apply."""
+    if kind != 0 or x_shape[-1] % 4 or k[0] * k[1] > 255 or node is None:
+        return None
+    key = ("argmax", id(node))
+    ptr = ctx.memo.get(key)
+    if ptr is None:
+        ptr = ctx.persistent(out_size)
+        ctx.memo[key] = ptr
+    return ptr
+
+
 def _pool_lower_fwd(ins, out, attrs):
+    ctx = current_ctx()
     x = ins[0]
     k, s, p, full = _pool_params(attrs, x.shape)
-    return [instr(L.OP_POOL_FWD, [x.ptr, out.ptr], _geom(x.shape, k, s, p) + [int(full)],
-                  act=_POOL_TYPES[attrs.get("pool_type", "max")])]
+    kind = _POOL_TYPES[attrs.get("pool_type", "max")]
+    arg = _pool_argmax(ctx.node, x.shape, out.size, k, kind, ctx) if ctx.training else None
+    if arg is not None:
+        ctx.memo[("argmax_fwd", id(ctx.node))] = True
+    return [instr(L.OP_POOL_FWD, [x.ptr, out.ptr, arg], _geom(x.shape, k, s, p) + [int(full)],
+                  act=kind)]
 
 
 def _pool_lower_bwd(slot, env, out, attrs):
+    ctx = current_ctx()
     x = env["in0"]
     k, s, p, full = _pool_params(attrs, x.shape)
-    return [instr(L.OP_POOL_BWD, [x.ptr, env["out"].ptr, env["og"].ptr, out.ptr],
-                  _geom(x.shape, k, s, p) + [int(full)],
-                  act=_POOL_TYPES[attrs.get("pool_type", "max")])]
+    kind = _POOL_TYPES[attrs.get("pool_type", "max")]
+    node = ctx.input_node("out")
+    arg = None
+    if node is not None and ctx.memo.get(("argmax_fwd", id(node))):
+        arg = _pool_argmax(node, x.shape, env["out"].size, k, kind, ctx)
+    # arg None: no forward recorded the argmax (eager call) -> rescan x
+    return [instr(L.OP_POOL_BWD, [x.ptr, env["out"].ptr, env["og"].ptr, out.ptr, arg],
+                  _geom(x.shape, k, s, p) + [int(full)], act=kind)]
 
 
 register(OperatorDef(

@@ -180,13 +180,14 @@ colreduce_partial_kernel(const float* __restrict__ a, const float* __restrict__ 
     const int c = cb + c_in;
     double s0 = 0.0, s1 = 0.0;
     if (r_in < rpp && c < C) {
-      float mean = 0.0f, rstd = 0.0f;
+      float mean = 0.0f, rstd = 0.0f, shift = 0.0f;
       if (MODE == 1) {
         mean = __ldg(stats + c);
         rstd = __ldg(stats + C + c);
       }
+      if (MODE == 0) shift = __ldg(a + c);  // row 0: shifted sums avoid cancellation
       for (int64_t r = r0 + r_in; r < r1; r += rpp) {
-        const float v = __ldg(a + r * C + c);
+        const float v = __ldg(a + r * C + c) - shift;
         s0 += v;
         if (MODE == 0) s1 += double(v) * double(v);
         if (MODE == 1) s1 += double(v) * double((__ldg(xs + r * C + c) - mean) * rstd);
@@ -210,27 +211,180 @@ colreduce_partial_kernel(const float* __restrict__ a, const float* __restrict__ 
   }
 }
 
+// Vectorised form (C % 4 == 0): a thread owns 4 channels (one float4 per
+// row), keeps fp32 partial sums over its rows with 4 rows of loads in
+// flight, then the block merges its threads' partials in fp64 in a fixed
+// order.  blockIdx.y tiles channels in groups of 1024.
+constexpr int kRedUnroll = 4;
+
+template <int MODE>
+__global__ void __launch_bounds__(kRedThreads)
+colreduce_partial_vec_kernel(const float* __restrict__ a, const float* __restrict__ xs,
+                             const float* __restrict__ stats, int64_t M, int C, int64_t rpc,
+                             double* __restrict__ ws) {
+  extern __shared__ double red[];  // [rpp][2][ct]
+  const int C4 = C >> 2;
+  const int ct4 = C4 < kRedThreads ? C4 : kRedThreads;  // float4 groups per block row
+  const int rpp = kRedThreads / ct4;
+  const int ct = ct4 * 4;
+  const int t = threadIdx.x;
+  const int r_in = t / ct4, c_in = t - (t / ct4) * ct4;
+  const int c4 = blockIdx.y * ct4 + c_in;
+  const bool active = r_in < rpp && c4 < C4;
+  const int64_t r0 = int64_t(blockIdx.x) * rpc;
+  const int64_t r1 = min(M, r0 + rpc);
+  const float4* a4 = reinterpret_cast<const float4*>(a);
+  const float4* x4 = reinterpret_cast<const float4*>(xs);
+  float s0[4] = {0.f, 0.f, 0.f, 0.f}, s1[4] = {0.f, 0.f, 0.f, 0.f};
+  if (active) {
+    float sh[4] = {0.f, 0.f, 0.f, 0.f}, mu[4] = {0.f, 0.f, 0.f, 0.f}, rs[4] = {0.f, 0.f, 0.f, 0.f};
+    if (MODE == 0) {
+      const float4 v = __ldg(a4 + c4);
+      sh[0] = v.x; sh[1] = v.y; sh[2] = v.z; sh[3] = v.w;
+    }
+    if (MODE == 1) {
+      const float4 m = __ldg(reinterpret_cast<const float4*>(stats) + c4);
+      const float4 q = __ldg(reinterpret_cast<const float4*>(stats + C) + c4);
+      mu[0] = m.x; mu[1] = m.y; mu[2] = m.z; mu[3] = m.w;
+      rs[0] = q.x; rs[1] = q.y; rs[2] = q.z; rs[3] = q.w;
+    }
+    int64_t r = r0 + r_in;
+    for (; r + (kRedUnroll - 1) * rpp < r1; r += kRedUnroll * rpp) {
+      float4 v[kRedUnroll], xv[kRedUnroll];
+#pragma unroll
+      for (int u = 0; u < kRedUnroll; ++u) {
+        v[u] = __ldg(a4 + (r + u * rpp) * C4 + c4);
+        if (MODE == 1) xv[u] = __ldg(x4 + (r + u * rpp) * C4 + c4);
+      }
+#pragma unroll
+      for (int u = 0; u < kRedUnroll; ++u) {
+        const float* pv = &v[u].x;
+        const float* px = &xv[u].x;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (MODE == 0) {
+            const float d = pv[q] - sh[q];
+            s0[q] += d;
+            s1[q] += d * d;
+          } else if (MODE == 1) {
+            s0[q] += pv[q];
+            s1[q] += pv[q] * ((px[q] - mu[q]) * rs[q]);
+          } else {
+            s0[q] += pv[q];
+          }
+        }
+      }
+    }
+    for (; r < r1; r += rpp) {
+      const float4 v = __ldg(a4 + r * C4 + c4);
+      float4 xv = v;
+      if (MODE == 1) xv = __ldg(x4 + r * C4 + c4);
+      const float* pv = &v.x;
+      const float* px = &xv.x;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (MODE == 0) {
+          const float d = pv[q] - sh[q];
+          s0[q] += d;
+          s1[q] += d * d;
+        } else if (MODE == 1) {
+          s0[q] += pv[q];
+          s1[q] += pv[q] * ((px[q] - mu[q]) * rs[q]);
+        } else {
+          s0[q] += pv[q];
+        }
+      }
+    }
+  }
+  if (r_in < rpp) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      red[(r_in * 2) * ct + c_in * 4 + q] = s0[q];
+      red[(r_in * 2 + 1) * ct + c_in * 4 + q] = s1[q];
+    }
+  }
+  __syncthreads();
+  const int nchunk = gridDim.x;
+  for (int c = t; c < ct; c += blockDim.x) {
+    const int cg = blockIdx.y * ct + c;
+    if (cg >= C) continue;
+    double u0 = 0.0, u1 = 0.0;
+    for (int rr = 0; rr < rpp; ++rr) {
+      u0 += red[(rr * 2) * ct + c];
+      u1 += red[(rr * 2 + 1) * ct + c];
+    }
+    ws[int64_t(blockIdx.x) * C + cg] = u0;
+    ws[int64_t(nchunk + blockIdx.x) * C + cg] = u1;
+  }
+}
+
+// Chunk merge shared by the finalize kernels: a block of 32 channels x 8
+// lanes; lane y sums chunks y, y+8, ... (4 independent loads in flight),
+// then the 8 lane sums are added in ascending y (fixed order).
+constexpr int kFinLanes = 8;
+
+__device__ __forceinline__ void merge_chunks(const double* __restrict__ ws, int nchunk, int C,
+                                             int c, bool two, double* s_out, double* q_out) {
+  __shared__ double red[2][kFinLanes][32];
+  const int ty = threadIdx.y, tx = threadIdx.x;
+  double s = 0.0, q = 0.0;
+  if (c < C) {
+    int z = ty;
+    for (; z + 3 * kFinLanes < nchunk; z += 4 * kFinLanes) {
+      double a[4], b[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        a[u] = ws[int64_t(z + u * kFinLanes) * C + c];
+        b[u] = two ? ws[int64_t(nchunk + z + u * kFinLanes) * C + c] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        s += a[u];
+        q += b[u];
+      }
+    }
+    for (; z < nchunk; z += kFinLanes) {
+      s += ws[int64_t(z) * C + c];
+      if (two) q += ws[int64_t(nchunk + z) * C + c];
+    }
+  }
+  red[0][ty][tx] = s;
+  red[1][ty][tx] = q;
+  __syncthreads();
+  if (ty == 0) {
+    double u = 0.0, v = 0.0;
+    for (int y = 0; y < kFinLanes; ++y) {
+      u += red[0][y][tx];
+      v += red[1][y][tx];
+    }
+    *s_out = u;
+    *q_out = v;
+  }
+}
+
 // MODE 0 finalize: stats = [mean | rstd] (batch statistics, biased variance
 // like MXNet), moving averages updated when given.
 // use_global: stats from the moving averages (inference).
 __global__ void bn_stats_finalize_kernel(const double* __restrict__ ws, int nchunk, int64_t M, int C,
-                                         float eps, float momentum, int use_global,
+                                         const float* __restrict__ x, float eps, float momentum,
+                                         int use_global,
                                          float* __restrict__ stats, float* __restrict__ mmean,
                                          float* __restrict__ mvar) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= C) return;
+  const int c = blockIdx.x * 32 + threadIdx.x;
   if (use_global) {
-    stats[c] = mmean[c];
-    stats[C + c] = static_cast<float>(1.0 / sqrt(double(mvar[c]) + double(eps)));
+    if (threadIdx.y == 0 && c < C) {
+      stats[c] = mmean[c];
+      stats[C + c] = static_cast<float>(1.0 / sqrt(double(mvar[c]) + double(eps)));
+    }
     return;
   }
   double s = 0.0, q = 0.0;
-  for (int z = 0; z < nchunk; ++z) {
-    s += ws[int64_t(z) * C + c];
-    q += ws[int64_t(nchunk + z) * C + c];
-  }
-  const double mean = s / double(M);
-  double var = q / double(M) - mean * mean;
+  merge_chunks(ws, nchunk, C, c, true, &s, &q);
+  if (threadIdx.y != 0 || c >= C) return;
+  // sums were taken relative to shift = x[0, c]
+  const double dm = s / double(M);
+  const double mean = double(x[c]) + dm;
+  double var = q / double(M) - dm * dm;
   if (var < 0.0) var = 0.0;
   stats[c] = static_cast<float>(mean);
   stats[C + c] = static_cast<float>(1.0 / sqrt(var + double(eps)));
@@ -241,13 +395,10 @@ __global__ void bn_stats_finalize_kernel(const double* __restrict__ ws, int nchu
 // MODE 1/2 finalize: out[c] = sum0, out[C + c] = sum1 (MODE 1) as fp32
 __global__ void colsum_finalize_kernel(const double* __restrict__ ws, int nchunk, int C, int two,
                                        float* __restrict__ out) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= C) return;
+  const int c = blockIdx.x * 32 + threadIdx.x;
   double s = 0.0, q = 0.0;
-  for (int z = 0; z < nchunk; ++z) {
-    s += ws[int64_t(z) * C + c];
-    if (two) q += ws[int64_t(nchunk + z) * C + c];
-  }
+  merge_chunks(ws, nchunk, C, c, two != 0, &s, &q);
+  if (threadIdx.y != 0 || c >= C) return;
   out[c] = static_cast<float>(s);
   if (two) out[C + c] = static_cast<float>(q);
 }
@@ -388,6 +539,108 @@ __global__ void pool_bwd_kernel(const float* __restrict__ x, const float* __rest
   }
 }
 
+// Channel-vectorised pooling (C % 4 == 0): a thread owns 4 channels of one
+// output (forward) or input (backward) pixel.  Max pooling records the
+// window-local index of the first maximum (uint8, row-major in the window)
+// so the backward is a cheap gather: dx(h,w) = sum of dy over the windows
+// whose recorded argmax is (h,w), windows in ascending (oh, ow) order.
+__global__ void pool_fwd_vec_kernel(const float* __restrict__ x, float* __restrict__ y,
+                                    uint8_t* __restrict__ arg, Geom g, int type) {
+  const int C4 = g.C >> 2;
+  const int64_t total = int64_t(g.B) * g.Ho * g.Wo * C4;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  const float4* x4 = reinterpret_cast<const float4*>(x);
+  for (int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < total; idx += stride) {
+    const int c4 = static_cast<int>(idx % C4);
+    int64_t p = idx / C4;
+    const int ow = static_cast<int>(p % g.Wo);
+    p /= g.Wo;
+    const int oh = static_cast<int>(p % g.Ho);
+    const int b = static_cast<int>(p / g.Ho);
+    const int hs = oh * g.sh - g.ph, ws = ow * g.sw - g.pw;
+    const int h0 = max(hs, 0), w0 = max(ws, 0);
+    const int h1 = min(hs + g.kh, g.H), w1 = min(ws + g.kw, g.W);
+    float acc[4];
+    int ai[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[q] = type == 0 ? -INFINITY : 0.0f;
+    for (int h = h0; h < h1; ++h)
+      for (int w = w0; w < w1; ++w) {
+        const float4 v = __ldg(x4 + ((int64_t(b) * g.H + h) * g.W + w) * C4 + c4);
+        const float* pv = &v.x;
+        const int li = (h - hs) * g.kw + (w - ws);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (type == 0) {
+            if (pv[q] > acc[q]) {
+              acc[q] = pv[q];
+              ai[q] = li;
+            }
+          } else {
+            acc[q] = fadd(acc[q], pv[q]);
+          }
+        }
+      }
+    float4 o;
+    if (type == 0) {
+      o = make_float4(acc[0], acc[1], acc[2], acc[3]);
+      if (arg) {
+        uchar4 a4 = make_uchar4(ai[0], ai[1], ai[2], ai[3]);
+        reinterpret_cast<uchar4*>(arg)[idx] = a4;
+      }
+    } else {
+      const float area = pool_area(g, oh, ow);
+      o = make_float4(fdiv(acc[0], area), fdiv(acc[1], area), fdiv(acc[2], area), fdiv(acc[3], area));
+    }
+    reinterpret_cast<float4*>(y)[idx] = o;
+  }
+}
+
+__global__ void pool_bwd_vec_kernel(const uint8_t* __restrict__ arg, const float* __restrict__ dy,
+                                    float* __restrict__ dx, Geom g, int type) {
+  const int C4 = g.C >> 2;
+  const int64_t total = int64_t(g.B) * g.H * g.W * C4;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  const float4* dy4 = reinterpret_cast<const float4*>(dy);
+  const uchar4* a4 = reinterpret_cast<const uchar4*>(arg);
+  for (int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < total; idx += stride) {
+    const int c4 = static_cast<int>(idx % C4);
+    int64_t p = idx / C4;
+    const int w = static_cast<int>(p % g.W);
+    p /= g.W;
+    const int h = static_cast<int>(p % g.H);
+    const int b = static_cast<int>(p / g.H);
+    const int nh = h + g.ph - g.kh + 1, nw = w + g.pw - g.kw + 1;
+    const int oh_lo = nh <= 0 ? 0 : (nh + g.sh - 1) / g.sh;
+    const int oh_hi = min(g.Ho - 1, (h + g.ph) / g.sh);
+    const int ow_lo = nw <= 0 ? 0 : (nw + g.sw - 1) / g.sw;
+    const int ow_hi = min(g.Wo - 1, (w + g.pw) / g.sw);
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int oh = oh_lo; oh <= oh_hi; ++oh) {
+      const int hs = oh * g.sh - g.ph;
+      for (int ow = ow_lo; ow <= ow_hi; ++ow) {
+        const int ws = ow * g.sw - g.pw;
+        const int64_t o = ((int64_t(b) * g.Ho + oh) * g.Wo + ow) * C4 + c4;
+        const float4 d = __ldg(dy4 + o);
+        const float* pd = &d.x;
+        if (type == 0) {
+          const uchar4 am = __ldg(a4 + o);
+          const int li = (h - hs) * g.kw + (w - ws);
+          const unsigned char* pa = &am.x;
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (pa[q] == li) acc[q] = fadd(acc[q], pd[q]);
+        } else {
+          const float area = pool_area(g, oh, ow);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[q] = fadd(acc[q], fdiv(pd[q], area));
+        }
+      }
+    }
+    reinterpret_cast<float4*>(dx)[idx] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+  }
+}
+
 // dst[r, doff + c] = src[r, soff + c] (Concat forward / backward slices)
 __global__ void chan_copy_kernel(const float* __restrict__ src, int64_t lds, int64_t soff,
                                  float* __restrict__ dst, int64_t ldd, int64_t doff, int64_t rows,
@@ -430,10 +683,20 @@ int launch_partial(const float* a, const float* xs, const float* stats, int64_t 
   int64_t rpc;
   int nchunk;
   chunks_for(M, &rpc, &nchunk);
-  const int tpr = C < kRedThreads ? C : kRedThreads;
-  const int rpp = kRedThreads / tpr;
-  const size_t smem = size_t(rpp) * 2 * tpr * sizeof(double);
-  colreduce_partial_kernel<MODE><<<nchunk, kRedThreads, smem, st>>>(a, xs, stats, M, C, rpc, ws);
+  const bool vec = (C % 4) == 0 && aligned16(a) && (MODE != 1 || aligned16(xs));
+  if (vec) {
+    const int C4 = C / 4;
+    const int ct4 = C4 < kRedThreads ? C4 : kRedThreads;
+    const int rpp = kRedThreads / ct4;
+    const size_t smem = size_t(rpp) * 2 * ct4 * 4 * sizeof(double);
+    dim3 grid(nchunk, static_cast<unsigned>(ceil_div(C4, ct4)));
+    colreduce_partial_vec_kernel<MODE><<<grid, kRedThreads, smem, st>>>(a, xs, stats, M, C, rpc, ws);
+  } else {
+    const int tpr = C < kRedThreads ? C : kRedThreads;
+    const int rpp = kRedThreads / tpr;
+    const size_t smem = size_t(rpp) * 2 * tpr * sizeof(double);
+    colreduce_partial_kernel<MODE><<<nchunk, kRedThreads, smem, st>>>(a, xs, stats, M, C, rpc, ws);
+  }
   *nchunk_out = nchunk;
   MGX_LAUNCHED();
   return MGX_OK;
@@ -494,8 +757,9 @@ extern "C" int mgx_bn_stats(const float* x, int64_t M, int64_t C, void* ws, floa
     MGX_TRY(mgx::conv::launch_partial<0>(x, nullptr, nullptr, M, static_cast<int>(C),
                                          static_cast<double*>(ws), &nchunk, st));
   }
-  mgx::conv::bn_stats_finalize_kernel<<<static_cast<unsigned>(mgx::ceil_div(C, 128)), 128, 0, st>>>(
-      static_cast<const double*>(ws), nchunk, M, static_cast<int>(C), eps, momentum, use_global,
+  mgx::conv::bn_stats_finalize_kernel<<<static_cast<unsigned>(mgx::ceil_div(C, 32)),
+                                         dim3(32, mgx::conv::kFinLanes), 0, st>>>(
+      static_cast<const double*>(ws), nchunk, M, static_cast<int>(C), x, eps, momentum, use_global,
       stats, moving_mean, moving_var);
   MGX_LAUNCHED();
   return MGX_OK;
@@ -518,7 +782,8 @@ extern "C" int mgx_bn_bwd_reduce(const float* dy, const float* x, const float* s
   int nchunk = 0;
   MGX_TRY(mgx::conv::launch_partial<1>(dy, x, stats, M, static_cast<int>(C), static_cast<double*>(ws),
                                        &nchunk, st));
-  mgx::conv::colsum_finalize_kernel<<<static_cast<unsigned>(mgx::ceil_div(C, 128)), 128, 0, st>>>(
+  mgx::conv::colsum_finalize_kernel<<<static_cast<unsigned>(mgx::ceil_div(C, 32)),
+                                       dim3(32, mgx::conv::kFinLanes), 0, st>>>(
       static_cast<const double*>(ws), nchunk, static_cast<int>(C), 1, sums);
   MGX_LAUNCHED();
   return MGX_OK;
@@ -540,29 +805,53 @@ extern "C" int mgx_colsum(const float* x, int64_t M, int64_t C, void* ws, float*
   int nchunk = 0;
   MGX_TRY(mgx::conv::launch_partial<2>(x, nullptr, nullptr, M, static_cast<int>(C),
                                        static_cast<double*>(ws), &nchunk, st));
-  mgx::conv::colsum_finalize_kernel<<<static_cast<unsigned>(mgx::ceil_div(C, 128)), 128, 0, st>>>(
+  mgx::conv::colsum_finalize_kernel<<<static_cast<unsigned>(mgx::ceil_div(C, 32)),
+                                       dim3(32, mgx::conv::kFinLanes), 0, st>>>(
       static_cast<const double*>(ws), nchunk, static_cast<int>(C), 0, out);
   MGX_LAUNCHED();
   return MGX_OK;
 }
 
+static bool pool_vec_ok(const Geom& g, const void* a, const void* b) {
+  return (g.C % 4) == 0 && mgx::aligned16(a) && mgx::aligned16(b);
+}
+
 extern "C" int mgx_pool_forward(const float* x, float* y, const int64_t* geom, int full, int type,
-                                uintptr_t stream) {
+                                void* argmax, uintptr_t stream) {
   MGX_REQUIRE(x && y && geom && (type == 0 || type == 1), "mgx_pool_forward: bad arguments");
   Geom g = mgx::conv::decode(geom, full != 0);
   MGX_REQUIRE(g.Ho > 0 && g.Wo > 0, "mgx_pool_forward: bad geometry");
-  const int64_t n = int64_t(g.B) * g.Ho * g.Wo * g.C;
-  mgx::conv::pool_fwd_kernel<<<grid_for(n), 256, 0, mgx::as_stream(stream)>>>(x, y, g, type);
+  cudaStream_t st = mgx::as_stream(stream);
+  if (pool_vec_ok(g, x, y) && g.kh * g.kw <= 255) {
+    const int64_t n = int64_t(g.B) * g.Ho * g.Wo * (g.C / 4);
+    mgx::conv::pool_fwd_vec_kernel<<<grid_for(n), 256, 0, st>>>(
+        x, y, type == 0 ? static_cast<uint8_t*>(argmax) : nullptr, g, type);
+  } else {
+    MGX_REQUIRE(!argmax || type != 0, "mgx_pool_forward: argmax needs C %% 4 == 0 and kh*kw <= 255");
+    const int64_t n = int64_t(g.B) * g.Ho * g.Wo * g.C;
+    mgx::conv::pool_fwd_kernel<<<grid_for(n), 256, 0, st>>>(x, y, g, type);
+  }
   MGX_LAUNCHED();
   return MGX_OK;
 }
 
 extern "C" int mgx_pool_backward(const float* x, const float* y, const float* dy, float* dx,
-                                 const int64_t* geom, int full, int type, uintptr_t stream) {
-  MGX_REQUIRE(dy && dx && geom && (type == 1 || (x && y)), "mgx_pool_backward: bad arguments");
+                                 const int64_t* geom, int full, int type, const void* argmax,
+                                 uintptr_t stream) {
+  MGX_REQUIRE(dy && dx && geom && (type == 1 || argmax || (x && y)),
+              "mgx_pool_backward: bad arguments");
   Geom g = mgx::conv::decode(geom, full != 0);
-  const int64_t n = int64_t(g.B) * g.H * g.W * g.C;
-  mgx::conv::pool_bwd_kernel<<<grid_for(n), 256, 0, mgx::as_stream(stream)>>>(x, y, dy, dx, g, type);
+  cudaStream_t st = mgx::as_stream(stream);
+  const bool use_arg = type == 0 && argmax != nullptr;
+  if (pool_vec_ok(g, dy, dx) && (type == 1 || use_arg)) {
+    const int64_t n = int64_t(g.B) * g.H * g.W * (g.C / 4);
+    mgx::conv::pool_bwd_vec_kernel<<<grid_for(n), 256, 0, st>>>(
+        static_cast<const uint8_t*>(argmax), dy, dx, g, type);
+  } else {
+    MGX_REQUIRE(type == 1 || (x && y), "mgx_pool_backward: max pooling needs x and y");
+    const int64_t n = int64_t(g.B) * g.H * g.W * g.C;
+    mgx::conv::pool_bwd_kernel<<<grid_for(n), 256, 0, st>>>(x, y, dy, dx, g, type);
+  }
   MGX_LAUNCHED();
   return MGX_OK;
 }

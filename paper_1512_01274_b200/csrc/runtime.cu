@@ -264,9 +264,10 @@ static int run_instr(const mgx_instr& in, cudaStream_t st) {
     case MGX_OP_BN_BWD_DX:
       return mgx_bn_bwd_dx(p0, p1, p2, p3, static_cast<float*>(in.ptr[4]),
                            static_cast<float*>(in.ptr[5]), d[0], d[1], s);
-    case MGX_OP_POOL_FWD: return mgx_pool_forward(p0, p1, d, static_cast<int>(d[7]), in.act, s);
+    case MGX_OP_POOL_FWD:
+      return mgx_pool_forward(p0, p1, d, static_cast<int>(d[7]), in.act, in.ptr[2], s);
     case MGX_OP_POOL_BWD:
-      return mgx_pool_backward(p0, p1, p2, p3, d, static_cast<int>(d[7]), in.act, s);
+      return mgx_pool_backward(p0, p1, p2, p3, d, static_cast<int>(d[7]), in.act, in.ptr[4], s);
     case MGX_OP_CHAN_COPY: return mgx_chan_copy(p0, d[2], d[3], p1, d[4], d[5], d[0], d[1], s);
     case MGX_OP_COLSUM: return mgx_colsum(p0, d[0], d[1], in.ptr[1], p2, s);
     case MGX_OP_GEMM_TC_EX:
@@ -449,6 +450,40 @@ extern "C" int mgx_prog_profile(uint64_t prog, int32_t begin, int32_t end, uintp
   for (auto& e : ev) cudaEventDestroy(e);
   if (rc != MGX_OK) return rc;
   MGX_CUDA(ce);
+  return MGX_OK;
+}
+
+extern "C" int mgx_prog_kernel_count(uint64_t prog, int32_t begin, int32_t end, uintptr_t stream,
+                                     int64_t* out) {
+  mgx::Program* p = mgx::find_prog(prog);
+  if (!p) {
+    mgx::set_error("mgx_prog_kernel_count: unknown program handle");
+    return MGX_BAD_HANDLE;
+  }
+  MGX_REQUIRE(out && stream && 0 <= begin && begin <= end &&
+                  end <= static_cast<int32_t>(p->instrs.size()),
+              "mgx_prog_kernel_count: bad arguments");
+  cudaStream_t st = as_stream(stream);
+  cudaGraph_t graph = nullptr;
+  MGX_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+  int rc = mgx::run_range(p, begin, end, st);
+  cudaError_t ce = cudaStreamEndCapture(st, &graph);
+  if (rc != MGX_OK) {
+    if (graph) cudaGraphDestroy(graph);
+    return rc;
+  }
+  MGX_CUDA(ce);
+  size_t n = 0;
+  cudaGraphGetNodes(graph, nullptr, &n);
+  std::vector<cudaGraphNode_t> nodes(n);
+  if (n) cudaGraphGetNodes(graph, nodes.data(), &n);
+  int64_t kernels = 0;
+  for (auto nd : nodes) {
+    cudaGraphNodeType t;
+    if (cudaGraphNodeGetType(nd, &t) == cudaSuccess && t == cudaGraphNodeTypeKernel) ++kernels;
+  }
+  cudaGraphDestroy(graph);
+  *out = kernels;
   return MGX_OK;
 }
 

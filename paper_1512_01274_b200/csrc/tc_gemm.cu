@@ -1,24 +1,37 @@
 // tcgen05 tensor-core GEMM for the bf16 dense path (sm_100a).
 //
-//   C[M,N] (fp32) = A[M,K] . B[N,K]^T (+ bias[N]) then activation
+//   C[M,N] (fp32) = sum_k A(m,k) B(n,k)  (+ bias[n]) then activation
 //
-// A and B are bf16, K-major ("TN": FC forward x[B,F] . w[H,F]^T), the
-// accumulator is fp32 in tensor memory.  One 128x128 output tile per CTA,
-// 4 warps:
-//   warp 0 (one lane)  TMA producer: 128B-swizzled 128x64 bf16 tiles of A and
-//                      B into a 4-stage shared-memory ring (mbarrier tx)
-//   warp 1 (one lane)  MMA issuer: 4 x tcgen05.mma.kind::f16 (M128 N128 K16)
-//                      per stage, tcgen05.commit frees the stage
-//   warps 0-3          epilogue: tcgen05.ld 32 lanes x 16 columns at a time,
-//                      bias + activation, fp32 stores
-// This is the tolerance path (bf16 operands, fp32 accumulate in hardware
-// order): used for the large FC layers of configs 3-5, never for the
-// exact-order fp32 parity path.
+// A and B are bf16 in global memory, each either K-major (X[r*ld + k]) or
+// MN-major (X[k*ld + r]); the accumulator is fp32 in tensor memory.  This
+// one kernel serves every contraction of the conv nets: forward (both
+// K-major), data gradient (B MN-major: the weight in its own layout) and
+// weight gradient (both MN-major: activations and output gradients in their
+// own layouts, the batch*pixels axis is the contraction), so no operand is
+// ever transposed in memory.
+//
+// Persistent and warp-specialised, one CTA per SM, 192 threads:
+//   warp 0 (one lane)   TMA producer: 128B-swizzled 64-wide K slices of A
+//                       (128 rows) and B (BN rows) into a STAGES-deep ring
+//   warp 1 (one lane)   MMA issuer: tcgen05.mma.kind::f16 M128 x BN x K16,
+//                       accumulating into one of two TMEM buffers, so the
+//                       epilogue of tile i overlaps the mainloop of tile i+1
+//   warps 2-5           epilogue: tcgen05.ld 32 lanes x 32 columns, bias +
+//                       activation, 128B-swizzled smem staging, TMA store
+//                       (direct fp32 stores when C's row pitch is not
+//                       16-byte aligned)
+// Tiles are scheduled round-robin over (split, m, n) with n fastest, so the
+// CTAs working at one time share A rows in L2.  Split-K partial tiles go
+// to a workspace and are summed in ascending split order (deterministic).
+//
+// This is the tolerance path (bf16 operands, fp32 accumulation in hardware
+// order); the exact-order fp32 kernels (dense.cu) stay the parity path.
 
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
 
+#include <cstring>
 #include <mutex>
 
 #include "common.cuh"
@@ -26,10 +39,22 @@
 namespace mgx {
 namespace tc {
 
-constexpr int BM = 128, BN = 128, BK = 64, STAGES = 4, UMMA_K = 16;
-constexpr int kTileBytes = BM * BK * 2;               // 16 KB (A or B)
-constexpr int kStageBytes = 2 * kTileBytes;            // 32 KB
-constexpr int kSmemBytes = STAGES * kStageBytes + 1024 + 256;
+constexpr int BM = 128, BK = 64, UMMA_K = 16;
+constexpr int kThreads = 192;
+constexpr int kEpiWarps = 4;
+constexpr int kMnChunkBytes = BK * 128;  // one MN-major TMA box: 64 K rows x 128 B
+constexpr int kStageCBytes = 32 * 32 * 4;  // one epilogue staging box (32 x 32 fp32)
+
+template <int BN>
+struct Cfg {
+  static constexpr int kABytes = BM * BK * 2;
+  static constexpr int kBBytes = BN * BK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kStages = BN >= 128 ? 4 : 6;
+  static constexpr int kTmemCols = 2 * BN;  // double-buffered accumulator
+  static constexpr int kSmemBytes =
+      1024 + kStages * kStageBytes + kEpiWarps * 2 * kStageCBytes + 256;
+};
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
@@ -38,6 +63,9 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                "r"(bytes)
                : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
@@ -56,24 +84,30 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0,
+                                             int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(c0), "r"(c1), "r"(smem_u32(src))
+      : "memory");
+}
 
 // tcgen05 shared-memory matrix descriptor: K-major, 128-byte swizzle,
 // 8-row swizzle atoms 1024 bytes apart (SBO), version 1 (bit 46).
 __device__ __forceinline__ uint64_t smem_desc_sw128(const void* p) {
   const uint64_t addr = smem_u32(p);
   uint64_t d = 0;
-  d |= (addr >> 4) & 0x3FFFull;          // start address
-  d |= (uint64_t(0) & 0x3FFF) << 16;     // LBO (unused for swizzled K-major)
+  d |= (addr >> 4) & 0x3FFFull;               // start address
   d |= (uint64_t(1024 >> 4) & 0x3FFF) << 32;  // SBO
-  d |= uint64_t(1) << 46;                // fixed 0b001
-  d |= uint64_t(2) << 61;                // SWIZZLE_128B
+  d |= uint64_t(1) << 46;                     // fixed 0b001
+  d |= uint64_t(2) << 61;                     // SWIZZLE_128B
   return d;
 }
 
-// tcgen05 shared-memory matrix descriptor, MN-major, 128-byte swizzle:
-// 64-element (128 B) MN rows, K rows 128 B apart; 8-row K groups 1024 B
-// apart (SBO); 64-wide MN chunks kMnChunkBytes apart (LBO).
-constexpr int kMnChunkBytes = BK * 128;  // one TMA box: 64 K rows x 128 B
+// MN-major, 128-byte swizzle: 64-element (128 B) MN rows, K rows 128 B
+// apart; 8-row K groups 1024 B apart (SBO); 64-wide MN chunks kMnChunkBytes
+// apart (LBO).
 __device__ __forceinline__ uint64_t smem_desc_mn_sw128(const void* p) {
   const uint64_t addr = smem_u32(p);
   uint64_t d = 0;
@@ -85,22 +119,22 @@ __device__ __forceinline__ uint64_t smem_desc_mn_sw128(const void* p) {
   return d;
 }
 
-// instruction descriptor kind::f16: D f32, A/B bf16, M128 N128; bit 15 / 16
+// instruction descriptor kind::f16: D f32, A/B bf16, M128 x BN; bits 15/16
 // select an MN-major A / B operand
-template <bool A_MN, bool B_MN>
+template <bool A_MN, bool B_MN, int BN>
 constexpr uint32_t idesc() {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((A_MN ? 1u : 0u) << 15) | ((B_MN ? 1u : 0u) << 16) |
-         ((BN >> 3) << 17) | ((BM >> 4) << 24);
+         (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
 }
 
-template <bool A_MN, bool B_MN>
+template <bool A_MN, bool B_MN, int BN>
 __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
                                           uint32_t accumulate) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc<A_MN, B_MN>()), "r"(accumulate));
+      "l"(adesc), "l"(bdesc), "r"(idesc<A_MN, B_MN, BN>()), "r"(accumulate));
 }
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -108,57 +142,70 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
                : "memory");
 }
 
-// one 128-row x 64-K operand tile into `dst`: a single K-major box, or two
-// MN-major boxes (MN 0..63, 64..127) stacked kMnChunkBytes apart
-template <bool MN>
+// one ROWS x 64-K operand tile into `dst`: a single K-major box, or
+// ROWS/64 MN-major boxes stacked kMnChunkBytes apart
+template <bool MN, int ROWS>
 __device__ __forceinline__ void load_operand(uint8_t* dst, const CUtensorMap* map, uint64_t* bar,
                                              int k0, int r0) {
   if (!MN) {
     tma_load_2d(dst, map, bar, k0, r0);
   } else {
-    tma_load_2d(dst, map, bar, r0, k0);
-    tma_load_2d(dst + kMnChunkBytes, map, bar, r0 + 64, k0);
+#pragma unroll
+    for (int c = 0; c < ROWS / 64; ++c) tma_load_2d(dst + c * kMnChunkBytes, map, bar, r0 + c * 64, k0);
   }
 }
 
-// C[M,N] (+bias, act) = sum_k A(m,k) B(n,k).  K-major operand X: X[r*ld + k];
-// MN-major: X[k*ld + r].  Split-K: blockIdx.z takes K blocks
-// [z*kps, (z+1)*kps) and writes its partial tile to C + z*split_stride.
-template <bool A_MN, bool B_MN>
-__global__ void __launch_bounds__(128, 1)
+struct Sched {
+  int m_tiles, n_tiles, splits, kps, nk;
+  __device__ __forceinline__ void tile(int t, int* m0, int* n0, int* z, int* kb0, int* nkb) const {
+    const int per_split = m_tiles * n_tiles;
+    *z = t / per_split;
+    const int r = t - *z * per_split;
+    *m0 = (r / n_tiles) * BM;
+    *n0 = (r - (r / n_tiles) * n_tiles);
+    *kb0 = *z * kps;
+    *nkb = min(nk, *kb0 + kps) - *kb0;
+  }
+};
+
+// ACTK: 0 no activation, 1 relu, 2 any (runtime code; cold path)
+template <bool A_MN, bool B_MN, int BN, int ACTK>
+__global__ void __launch_bounds__(kThreads, 1)
 tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
-                    const __grid_constant__ CUtensorMap map_b, const float* __restrict__ bias,
-                    float* __restrict__ C, int ldc, int M, int N, int K, int act, int kps,
-                    int64_t split_stride) {
+                    const __grid_constant__ CUtensorMap map_b,
+                    const __grid_constant__ CUtensorMap map_c, const float* __restrict__ bias,
+                    float* __restrict__ C, int ldc, int M, int N, int act, Sched sc,
+                    int64_t split_stride, int use_tma_store) {
+  using G = Cfg<BN>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  // 1024-byte aligned stage ring (SW128 atoms need it)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * kStageBytes);
-  uint64_t* empty = full + STAGES;
-  uint64_t* done = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  uint8_t* stage_c = smem + G::kStages * G::kStageBytes;  // [4 warps][2 bufs][4 KB]
+  uint64_t* full = reinterpret_cast<uint64_t*>(stage_c + kEpiWarps * 2 * kStageCBytes);
+  uint64_t* empty = full + G::kStages;
+  uint64_t* tfull = empty + G::kStages;   // [2]
+  uint64_t* tempty = tfull + 2;           // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
-  const int nk_all = (K + BK - 1) / BK;
-  const int kb0 = blockIdx.z * kps;
-  const int nk = min(nk_all, kb0 + kps) - kb0;
-  C += int64_t(blockIdx.z) * split_stride;
+  const int ntiles = sc.m_tiles * sc.n_tiles * sc.splits;
 
   if (threadIdx.x == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < G::kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(done, 1);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], kEpiWarps);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
-                 "r"(BN));
+                 "r"(G::kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -166,77 +213,162 @@ tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0 && lane == 0) {
-    // ---------------- TMA producer
-    for (int kb = 0; kb < nk; ++kb) {
-      const int s = kb % STAGES;
-      const uint32_t ph = (kb / STAGES) & 1;
-      mbar_wait(&empty[s], ph ^ 1);
-      uint8_t* sa = smem + s * kStageBytes;
-      mbar_expect_tx(&full[s], kStageBytes);
-      load_operand<A_MN>(sa, &map_a, &full[s], (kb0 + kb) * BK, m0);
-      load_operand<B_MN>(sa + kTileBytes, &map_b, &full[s], (kb0 + kb) * BK, n0);
-    }
-  } else if (warp == 1 && lane == 0) {
-    // ---------------- MMA issuer
-    for (int kb = 0; kb < nk; ++kb) {
-      const int s = kb % STAGES;
-      const uint32_t ph = (kb / STAGES) & 1;
-      mbar_wait(&full[s], ph);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint8_t* sa = smem + s * kStageBytes;
-      const uint64_t adesc = A_MN ? smem_desc_mn_sw128(sa) : smem_desc_sw128(sa);
-      const uint64_t bdesc = B_MN ? smem_desc_mn_sw128(sa + kTileBytes) : smem_desc_sw128(sa + kTileBytes);
-#pragma unroll
-      for (int k = 0; k < BK / UMMA_K; ++k) {
-        // K-major: +32 bytes per K16 step inside the 128-byte swizzle row
-        // (>>4 -> +2); MN-major: +16 K rows of 128 bytes (>>4 -> +128)
-        const uint64_t da = A_MN ? 128ull * k : 2ull * k;
-        const uint64_t db = B_MN ? 128ull * k : 2ull * k;
-        umma_bf16<A_MN, B_MN>(tmem, adesc + da, bdesc + db, (kb > 0 || k > 0) ? 1u : 0u);
-      }
-      umma_commit(&empty[s]);
-    }
-    umma_commit(done);
-  }
-  __syncwarp();
-
-  // ---------------- epilogue: all 4 warps, warp w owns TMEM lanes 32w..32w+31
-  mbar_wait(done, 0);
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const int row = m0 + warp * 32 + lane;
-  for (int c0 = 0; c0 < BN; c0 += 16) {
-    uint32_t r[16];
-    const uint32_t taddr = tmem + (uint32_t(warp * 32) << 16) + uint32_t(c0);
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-          "=r"(r[14]), "=r"(r[15])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-    if (row < M) {
-      float* crow = C + int64_t(row) * ldc;
-      if (nk <= 0) {
-#pragma unroll
-        for (int j = 0; j < 16; ++j) r[j] = 0u;  // empty split: contributes zeros
-      }
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int n = n0 + c0 + j;
-        if (n < N) {
-          float v = __uint_as_float(r[j]);
-          if (bias) v = fadd(v, __ldg(bias + n));
-          crow[n] = act_forward(act, v);
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer
+      int it = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        int m0, nt, z, kb0, nkb;
+        sc.tile(t, &m0, &nt, &z, &kb0, &nkb);
+        const int n0 = nt * BN;
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % G::kStages;
+          const uint32_t ph = (it / G::kStages) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          uint8_t* sa = smem + s * G::kStageBytes;
+          mbar_expect_tx(&full[s], G::kStageBytes);
+          load_operand<A_MN, BM>(sa, &map_a, &full[s], (kb0 + kb) * BK, m0);
+          load_operand<B_MN, BN>(sa + G::kABytes, &map_b, &full[s], (kb0 + kb) * BK, n0);
         }
       }
     }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer
+      int it = 0, local = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++local) {
+        int m0, nt, z, kb0, nkb;
+        sc.tile(t, &m0, &nt, &z, &kb0, &nkb);
+        const int acc = local & 1;
+        const uint32_t aph = (local >> 1) & 1;
+        mbar_wait(&tempty[acc], aph ^ 1);  // epilogue drained this buffer
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t dst = tmem + uint32_t(acc * BN);
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % G::kStages;
+          const uint32_t ph = (it / G::kStages) & 1;
+          mbar_wait(&full[s], ph);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint8_t* sa = smem + s * G::kStageBytes;
+          const uint64_t adesc = A_MN ? smem_desc_mn_sw128(sa) : smem_desc_sw128(sa);
+          const uint64_t bdesc = B_MN ? smem_desc_mn_sw128(sa + G::kABytes)
+                                      : smem_desc_sw128(sa + G::kABytes);
+#pragma unroll
+          for (int k = 0; k < BK / UMMA_K; ++k) {
+            // K-major: +32 bytes per K16 step inside the 128-byte swizzle
+            // row (>>4 -> +2); MN-major: +16 K rows of 128 bytes (+128)
+            const uint64_t da = A_MN ? 128ull * k : 2ull * k;
+            const uint64_t db = B_MN ? 128ull * k : 2ull * k;
+            umma_bf16<A_MN, B_MN, BN>(dst, adesc + da, bdesc + db, (kb > 0 || k > 0) ? 1u : 0u);
+          }
+          umma_commit(&empty[s]);
+        }
+        umma_commit(&tfull[acc]);
+      }
+    }
+  } else {
+    // ---------------- epilogue warps: TMEM lanes 32*(warp%4) .. +31
+    const int ew = warp - 2;
+    const int lane_base = (warp & 3) * 32;
+    uint8_t* cbuf = stage_c + ew * 2 * kStageCBytes;
+    int local = 0, nbuf = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++local) {
+      int m0, nt, z, kb0, nkb;
+      sc.tile(t, &m0, &nt, &z, &kb0, &nkb);
+      const int n0 = nt * BN;
+      const int acc = local & 1;
+      const uint32_t aph = (local >> 1) & 1;
+      float* Cz = C + int64_t(z) * split_stride;
+      mbar_wait(&tfull[acc], aph);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int row0 = m0 + lane_base;
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t r[32];
+        const uint32_t taddr = tmem + (uint32_t(lane_base) << 16) + uint32_t(acc * BN + c0);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+            "%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+              "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+              "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+              "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+              "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+              "=r"(r[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (c0 + 32 >= BN) {
+          // all of this accumulator is in registers: hand TMEM back early
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+        }
+        // warp-uniform epilogue variants: the generic activation code
+        // (double-precision exp/tanh) stays out of the common loops
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = nkb > 0 ? __uint_as_float(r[j]) : 0.0f;
+        if (bias) {
+          const int nb = n0 + c0;
+          if (nb + 32 <= N && (N & 3) == 0) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float4 b4 = __ldg(reinterpret_cast<const float4*>(bias + nb) + j);
+              v[4 * j] = fadd(v[4 * j], b4.x);
+              v[4 * j + 1] = fadd(v[4 * j + 1], b4.y);
+              v[4 * j + 2] = fadd(v[4 * j + 2], b4.z);
+              v[4 * j + 3] = fadd(v[4 * j + 3], b4.w);
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = fadd(v[j], nb + j < N ? __ldg(bias + nb + j) : 0.0f);
+          }
+        }
+        if (ACTK == 1) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = relu(v[j]);
+        } else if (ACTK == 2) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = act_forward(act, v[j]);
+        }
+        if (use_tma_store) {
+          if (row0 >= M) continue;  // warp-uniform: nothing of this box is in C
+          uint8_t* buf = cbuf + nbuf * kStageCBytes;
+          // the store that last read this buffer (two chunks ago) is done
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            float4 q = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            *reinterpret_cast<float4*>(buf + lane * 128 + ((j ^ (lane & 7)) << 4)) = q;
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&map_c, buf, n0 + c0, int(int64_t(z) * M) + row0);
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
+          nbuf ^= 1;
+        } else {
+          const int row = row0 + lane;
+          if (row < M) {
+            float* crow = Cz + int64_t(row) * ldc;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const int n = n0 + c0 + j;
+              if (n < N) crow[n] = v[j];
+            }
+          }
+        }
+      }
+    }
+    if (use_tma_store && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   if (warp == 1) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(G::kTmemCols));
   }
 }
 
@@ -257,23 +389,56 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, i
   }
 }
 
-// y (bf16, rows x ldo) = x (fp32, R x C, row stride ldi), optionally
-// transposed (y is C x ldo then), zero-filled beyond the source extent so the
-// padded K columns contribute nothing to the tensor-core contraction.
-__global__ void cast_2d_kernel(const float* __restrict__ x, int64_t R, int64_t C, int64_t ldi,
-                               __nv_bfloat16* __restrict__ y, int64_t rows, int64_t ldo,
-                               int transpose) {
-  const int64_t n = rows * ldo;
+__device__ __forceinline__ uint32_t pack2(float a, float b) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// y (bf16, rows x ldo) = x (fp32, R x C, row stride ldi), zero-filled
+// beyond the source extent (the K padding of a tensor-core operand).  8
+// output columns per thread (one 16-byte store).
+__global__ void cast_rows_kernel(const float* __restrict__ x, int64_t R, int64_t C, int64_t ldi,
+                                 __nv_bfloat16* __restrict__ y, int64_t rows, int64_t ldo) {
+  const int64_t per = ldo >> 3;
+  const int64_t n = rows * per;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  const bool vec = ((ldi & 3) == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const int64_t r = i / ldo, c = i - r * ldo;
-    float v = 0.0f;
-    if (!transpose) {
-      if (r < R && c < C) v = x[r * ldi + c];
+    const int64_t r = i / per, c0 = (i - r * per) * 8;
+    float v[8];
+    if (r < R && vec && c0 + 8 <= C) {
+      const float4 a = __ldg(reinterpret_cast<const float4*>(x + r * ldi + c0));
+      const float4 b = __ldg(reinterpret_cast<const float4*>(x + r * ldi + c0 + 4));
+      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+      v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
     } else {
-      if (c < R && r < C) v = x[c * ldi + r];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = (r < R && c0 + j < C) ? __ldg(x + r * ldi + c0 + j) : 0.0f;
     }
-    y[i] = __float2bfloat16_rn(v);
+    uint4 o;
+    o.x = pack2(v[0], v[1]);
+    o.y = pack2(v[2], v[3]);
+    o.z = pack2(v[4], v[5]);
+    o.w = pack2(v[6], v[7]);
+    *reinterpret_cast<uint4*>(y + r * ldo + c0) = o;
+  }
+}
+
+// transposed cast: y[c, r] (bf16, rows x ldo) = x[r, c], zero beyond the
+// source; 32x32 tiles through shared memory
+__global__ void cast_transpose_kernel(const float* __restrict__ x, int64_t R, int64_t C,
+                                      int64_t ldi, __nv_bfloat16* __restrict__ y, int64_t rows,
+                                      int64_t ldo) {
+  __shared__ float tile[32][33];
+  const int64_t tr = int64_t(blockIdx.y) * 32, tc = int64_t(blockIdx.x) * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t r = tr + i, c = tc + threadIdx.x;
+    tile[i][threadIdx.x] = (r < R && c < C) ? __ldg(x + r * ldi + c) : 0.0f;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t orow = tc + i, ocol = tr + threadIdx.x;
+    if (orow < rows && ocol < ldo) y[orow * ldo + ocol] = __float2bfloat16_rn(tile[threadIdx.x][i]);
   }
 }
 
@@ -305,29 +470,15 @@ static int get_encode() {
   return MGX_OK;
 }
 
-// K-major operand: dims {K, rows}, box {64, 128}; MN-major: dims {rows, K}
-// (rows contiguous), box {64, 64} (loaded twice per 128-row tile)
-static int make_map(CUtensorMap* map, const void* base, int64_t rows, int64_t K, int64_t ld,
-                    bool mn) {
-  cuuint64_t dims[2];
-  cuuint32_t box[2];
-  if (!mn) {
-    dims[0] = static_cast<cuuint64_t>(K);
-    dims[1] = static_cast<cuuint64_t>(rows);
-    box[0] = BK;
-    box[1] = BM;
-  } else {
-    dims[0] = static_cast<cuuint64_t>(rows);
-    dims[1] = static_cast<cuuint64_t>(K);
-    box[0] = 64;
-    box[1] = BK;
-  }
-  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * 2)};
+static int encode(CUtensorMap* map, CUtensorMapDataType dt, const void* base, cuuint64_t d0,
+                  cuuint64_t d1, cuuint64_t stride_bytes, cuuint32_t b0, cuuint32_t b1) {
+  cuuint64_t dims[2] = {d0, d1};
+  cuuint64_t strides[1] = {stride_bytes};
+  cuuint32_t box[2] = {b0, b1};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
-                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = g_encode(map, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeTiled failed (%d)", static_cast<int>(r));
     return MGX_INTERNAL;
@@ -335,21 +486,64 @@ static int make_map(CUtensorMap* map, const void* base, int64_t rows, int64_t K,
   return MGX_OK;
 }
 
-template <bool A_MN, bool B_MN>
-static int launch_variant(const CUtensorMap& ma, const CUtensorMap& mb, dim3 grid,
-                          const float* bias, float* C, int ldc, int M, int N, int K, int act,
-                          int kps, int64_t split_stride, cudaStream_t st) {
+// K-major operand: dims {K, rows}, box {64, box_rows}; MN-major: dims
+// {rows, K} (rows contiguous), box {64, 64}
+static int make_map(CUtensorMap* map, const void* base, int64_t rows, int64_t K, int64_t ld,
+                    bool mn, int box_rows) {
+  if (!mn)
+    return encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, base, K, rows, ld * 2, BK, box_rows);
+  return encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, base, rows, K, ld * 2, 64, BK);
+}
+
+template <bool A_MN, bool B_MN, int BN, int ACTK>
+static int launch_act(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
+                      int grid, const float* bias, float* C, int ldc, int M, int N, int act,
+                      const Sched& sc, int64_t split_stride, int tma_store, cudaStream_t st) {
+  using G = Cfg<BN>;
   static bool configured = false;
   if (!configured) {
-    MGX_CUDA(cudaFuncSetAttribute(tc_gemm_bf16_kernel<A_MN, B_MN>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+    MGX_CUDA(cudaFuncSetAttribute(tc_gemm_bf16_kernel<A_MN, B_MN, BN, ACTK>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, G::kSmemBytes));
     configured = true;
   }
-  tc_gemm_bf16_kernel<A_MN, B_MN><<<grid, 128, kSmemBytes, st>>>(ma, mb, bias, C, ldc, M, N, K,
-                                                                   act, kps, split_stride);
+  tc_gemm_bf16_kernel<A_MN, B_MN, BN, ACTK><<<grid, kThreads, G::kSmemBytes, st>>>(
+      ma, mb, mc, bias, C, ldc, M, N, act, sc, split_stride, tma_store);
   MGX_LAUNCHED();
   return MGX_OK;
 }
+
+template <bool A_MN, bool B_MN, int BN>
+static int launch_variant(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
+                          int grid, const float* bias, float* C, int ldc, int M, int N, int act,
+                          const Sched& sc, int64_t split_stride, int tma_store, cudaStream_t st) {
+  if (act == MGX_ACT_NONE)
+    return launch_act<A_MN, B_MN, BN, 0>(ma, mb, mc, grid, bias, C, ldc, M, N, act, sc, split_stride, tma_store, st);
+  if (act == MGX_ACT_RELU)
+    return launch_act<A_MN, B_MN, BN, 1>(ma, mb, mc, grid, bias, C, ldc, M, N, act, sc, split_stride, tma_store, st);
+  return launch_act<A_MN, B_MN, BN, 2>(ma, mb, mc, grid, bias, C, ldc, M, N, act, sc, split_stride, tma_store, st);
+}
+
+template <int BN>
+static int launch_bn(int a_mn, int b_mn, const CUtensorMap& ma, const CUtensorMap& mb,
+                     const CUtensorMap& mc, int grid, const float* bias, float* C, int ldc, int M,
+                     int N, int act, const Sched& sc, int64_t sstride, int tma, cudaStream_t st) {
+  if (!a_mn && !b_mn)
+    return launch_variant<false, false, BN>(ma, mb, mc, grid, bias, C, ldc, M, N, act, sc, sstride, tma, st);
+  if (!a_mn && b_mn)
+    return launch_variant<false, true, BN>(ma, mb, mc, grid, bias, C, ldc, M, N, act, sc, sstride, tma, st);
+  if (a_mn && !b_mn)
+    return launch_variant<true, false, BN>(ma, mb, mc, grid, bias, C, ldc, M, N, act, sc, sstride, tma, st);
+  return launch_variant<true, true, BN>(ma, mb, mc, grid, bias, C, ldc, M, N, act, sc, sstride, tma, st);
+}
+
+static int auto_splits(int64_t tiles, int64_t nk) {
+  if (tiles >= kNumSMs) return 1;
+  int64_t want = kNumSMs / tiles, most = nk / 4;
+  int64_t s = want < most ? want : most;
+  return static_cast<int>(s < 1 ? 1 : s);
+}
+
+static int pick_bn(int64_t N) { return N <= 64 ? 64 : 128; }
 
 }  // namespace tc
 }  // namespace mgx
@@ -369,38 +563,39 @@ extern "C" int mgx_gemm_bf16_tc_ex(const void* A, int64_t lda, int a_mn, const v
               "mgx_gemm_bf16_tc: dimensions exceed 2^31");
   MGX_REQUIRE(splits >= 0, "mgx_gemm_bf16_tc: negative split count");
   MGX_TRY(get_encode());
-  CUtensorMap ma, mb;
-  MGX_TRY(make_map(&ma, A, M, K, lda, a_mn != 0));
-  MGX_TRY(make_map(&mb, B, N, K, ldb, b_mn != 0));
-  const int64_t tiles = mgx::ceil_div(N, BN) * mgx::ceil_div(M, BM);
+  const int bn = pick_bn(N);
+  const int64_t m_tiles = mgx::ceil_div(M, BM), n_tiles = mgx::ceil_div(N, bn);
   const int64_t nk = mgx::ceil_div(K, BK);
-  if (splits == 0) {
-    // auto: enough K splits to cover the SMs once, each split >= 4 K blocks
-    splits = 1;
-    if (workspace && tiles < mgx::kNumSMs) {
-      int64_t want = mgx::kNumSMs / tiles;
-      int64_t most = nk / 4;
-      splits = static_cast<int>(want < most ? want : most);
-      if (splits < 1) splits = 1;
-    }
-  }
+  if (splits == 0) splits = workspace ? auto_splits(m_tiles * n_tiles, nk) : 1;
   MGX_REQUIRE(splits == 1 || workspace, "mgx_gemm_bf16_tc: split-K needs a workspace");
   int kps = static_cast<int>(mgx::ceil_div(nk, splits));
   splits = static_cast<int>(mgx::ceil_div(nk, kps));
-  dim3 grid(static_cast<unsigned>(mgx::ceil_div(N, BN)), static_cast<unsigned>(mgx::ceil_div(M, BM)),
-            static_cast<unsigned>(splits));
-  cudaStream_t st = mgx::as_stream(stream);
+  MGX_REQUIRE(int64_t(splits) * M < (1ll << 31), "mgx_gemm_bf16_tc: split workspace too tall");
+  CUtensorMap ma, mb, mc;
+  MGX_TRY(make_map(&ma, A, M, K, lda, a_mn != 0, BM));
+  MGX_TRY(make_map(&mb, B, N, K, ldb, b_mn != 0, bn));
   float* out = splits == 1 ? C : workspace;
+  const int64_t oldc = splits == 1 ? ldc : N;
+  // TMA store needs a 16-byte row pitch and base; the map spans all splits
+  // (partial 32-row boxes of a split would spill into the next split's rows)
+  const int tma = (oldc % 4 == 0) && mgx::aligned16(out) && (splits == 1 || M % 32 == 0);
+  if (tma) {
+    MGX_TRY(mgx::tc::encode(&mc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, out, N, int64_t(splits) * M,
+                            oldc * 4, 32, 32));
+  } else {
+    std::memset(&mc, 0, sizeof(mc));
+  }
+  Sched sc{static_cast<int>(m_tiles), static_cast<int>(n_tiles), splits, kps, static_cast<int>(nk)};
+  const int64_t total = m_tiles * n_tiles * splits;
+  const int grid = static_cast<int>(total < mgx::kNumSMs ? total : mgx::kNumSMs);
+  cudaStream_t st = mgx::as_stream(stream);
   const int64_t sstride = M * N;
-  const int oldc = splits == 1 ? static_cast<int>(ldc) : static_cast<int>(N);
   const float* ebias = splits == 1 ? bias : nullptr;
   const int eact = splits == 1 ? act : 0;
-  const int m = static_cast<int>(M), n = static_cast<int>(N), k = static_cast<int>(K);
-  int rc;
-  if (!a_mn && !b_mn) rc = launch_variant<false, false>(ma, mb, grid, ebias, out, oldc, m, n, k, eact, kps, sstride, st);
-  else if (!a_mn && b_mn) rc = launch_variant<false, true>(ma, mb, grid, ebias, out, oldc, m, n, k, eact, kps, sstride, st);
-  else if (a_mn && !b_mn) rc = launch_variant<true, false>(ma, mb, grid, ebias, out, oldc, m, n, k, eact, kps, sstride, st);
-  else rc = launch_variant<true, true>(ma, mb, grid, ebias, out, oldc, m, n, k, eact, kps, sstride, st);
+  int rc = bn == 64 ? launch_bn<64>(a_mn, b_mn, ma, mb, mc, grid, ebias, out, static_cast<int>(oldc),
+                                    static_cast<int>(M), static_cast<int>(N), eact, sc, sstride, tma, st)
+                    : launch_bn<128>(a_mn, b_mn, ma, mb, mc, grid, ebias, out, static_cast<int>(oldc),
+                                     static_cast<int>(M), static_cast<int>(N), eact, sc, sstride, tma, st);
   if (rc != MGX_OK || splits == 1) return rc;
   int64_t blocks = mgx::ceil_div(M * N, 256);
   if (blocks > 148 * 8) blocks = 148 * 8;
@@ -419,13 +614,12 @@ extern "C" int mgx_gemm_bf16_tc(const void* A, int64_t lda, const void* B, int64
 extern "C" int mgx_gemm_splitk_workspace(int64_t M, int64_t N, int64_t K, int64_t* out_floats) {
   using namespace mgx::tc;
   MGX_REQUIRE(out_floats && M > 0 && N > 0 && K > 0, "mgx_gemm_splitk_workspace: bad arguments");
-  const int64_t tiles = mgx::ceil_div(N, BN) * mgx::ceil_div(M, BM);
+  const int64_t tiles = mgx::ceil_div(N, pick_bn(N)) * mgx::ceil_div(M, BM);
   const int64_t nk = mgx::ceil_div(K, BK);
-  int64_t splits = 1;
-  if (tiles < mgx::kNumSMs) {
-    int64_t want = mgx::kNumSMs / tiles, most = nk / 4;
-    splits = want < most ? want : most;
-    if (splits < 1) splits = 1;
+  int64_t splits = auto_splits(tiles, nk);
+  if (splits > 1) {
+    const int64_t kps = mgx::ceil_div(nk, splits);
+    splits = mgx::ceil_div(nk, kps);
   }
   *out_floats = splits > 1 ? splits * M * N : 0;
   return MGX_OK;
@@ -436,10 +630,20 @@ extern "C" int mgx_cast_bf16_2d(const float* x, int64_t R, int64_t C, int64_t ld
   MGX_REQUIRE(x && y && R > 0 && C > 0 && rows > 0 && ldo > 0, "mgx_cast_bf16_2d: bad arguments");
   MGX_REQUIRE(transpose ? (rows >= C && ldo >= R) : (rows >= R && ldo >= C),
               "mgx_cast_bf16_2d: destination smaller than the source");
-  int64_t blocks = mgx::ceil_div(rows * ldo, 256);
-  if (blocks > 148 * 16) blocks = 148 * 16;
-  mgx::tc::cast_2d_kernel<<<static_cast<unsigned>(blocks), 256, 0, mgx::as_stream(stream)>>>(
-      x, R, C, ldi, static_cast<__nv_bfloat16*>(y), rows, ldo, transpose);
+  cudaStream_t st = mgx::as_stream(stream);
+  if (!transpose && ldo % 8 == 0 && mgx::aligned16(y)) {
+    int64_t blocks = mgx::ceil_div(rows * (ldo / 8), 256);
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    mgx::tc::cast_rows_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(
+        x, R, C, ldi, static_cast<__nv_bfloat16*>(y), rows, ldo);
+  } else if (!transpose) {
+    MGX_REQUIRE(false, "mgx_cast_bf16_2d: ldo must be a multiple of 8 and y 16-byte aligned");
+  } else {
+    dim3 grid(static_cast<unsigned>(mgx::ceil_div(rows, 32)),
+              static_cast<unsigned>(mgx::ceil_div(ldo, 32)));
+    mgx::tc::cast_transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(
+        x, R, C, ldi, static_cast<__nv_bfloat16*>(y), rows, ldo);
+  }
   MGX_LAUNCHED();
   return MGX_OK;
 }

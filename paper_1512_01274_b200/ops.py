@@ -135,6 +135,41 @@ def instr_cost(ins: L.Instr) -> tuple:
     if op == L.OP_GEMM_TC:
         m, n, k = d[0], d[1], d[2]
         return 2 * (m * k + n * k) + 4 * m * n + (4 * n if has[2] else 0), 2 * m * n * k
+    if op == L.OP_GEMM_TC_EX:
+        m, n, k = d[0], d[1], d[2]
+        return 2 * (m * k + n * k) + 4 * m * n + (4 * n if has[2] else 0), 2 * m * n * k
+    if op == L.OP_IM2COL:  # reads the input once, writes the bf16 col matrix
+        b, h, w, c = d[0], d[1], d[2], d[3]
+        kh, kw, sh, sw, ph, pw = d[4] >> 16, d[4] & 0xFFFF, d[5] >> 16, d[5] & 0xFFFF, d[6] >> 16, d[6] & 0xFFFF
+        ho, wo = (h + 2 * ph - kh) // sh + 1, (w + 2 * pw - kw) // sw + 1
+        return 4 * b * h * w * c + 2 * b * ho * wo * d[7], 0
+    if op == L.OP_COL2IM:
+        b, h, w, c = d[0], d[1], d[2], d[3]
+        kh, kw, sh, sw, ph, pw = d[4] >> 16, d[4] & 0xFFFF, d[5] >> 16, d[5] & 0xFFFF, d[6] >> 16, d[6] & 0xFFFF
+        ho, wo = (h + 2 * ph - kh) // sh + 1, (w + 2 * pw - kw) // sw + 1
+        return 4 * b * ho * wo * d[7] + 4 * b * h * w * c, b * ho * wo * d[7]
+    if op == L.OP_BN_STATS:
+        return (0 if d[2] else 4 * d[0] * d[1]) + 8 * d[1], 2 * d[0] * d[1]
+    if op == L.OP_BN_APPLY:
+        return 8 * d[0] * d[1], 4 * d[0] * d[1]
+    if op == L.OP_BN_BWD_REDUCE:
+        return 8 * d[0] * d[1], 4 * d[0] * d[1]
+    if op == L.OP_BN_BWD_DX:
+        return 12 * d[0] * d[1], 6 * d[0] * d[1]
+    if op in (L.OP_POOL_FWD, L.OP_POOL_BWD):
+        b, h, w, c = d[0], d[1], d[2], d[3]
+        kh, kw, sh, sw, ph, pw = d[4] >> 16, d[4] & 0xFFFF, d[5] >> 16, d[5] & 0xFFFF, d[6] >> 16, d[6] & 0xFFFF
+        span_h, span_w = h + 2 * ph - kh, w + 2 * pw - kw
+        ho = (-(-span_h // sh) if d[7] else span_h // sh) + 1
+        wo = (-(-span_w // sw) if d[7] else span_w // sw) + 1
+        n_in, n_out = b * h * w * c, b * ho * wo * c
+        if op == L.OP_POOL_FWD:
+            return 4 * (n_in + n_out), n_out * kh * kw
+        return 4 * (2 * n_in + 2 * n_out), n_out * kh * kw
+    if op == L.OP_CHAN_COPY:
+        return 8 * d[0] * d[1], 0
+    if op == L.OP_COLSUM:
+        return 4 * d[0] * d[1], d[0] * d[1]
     if op == L.OP_CAST_BF16:
         return 4 * d[0] * d[1] + 2 * d[3] * d[4], d[3] * d[4]
     if op == L.OP_SOFTMAX_FWD:
@@ -349,32 +384,66 @@ def _cast(src: View, rows_in: int, cols_in: int, dst: int, rows_out: int, ld_out
                  [rows_in, cols_in, cols_in, rows_out, ld_out, 1 if transpose else 0])
 
 
-def fc_forward_tc(x: View, w: View, b: Optional[View], out: View, act: int, alloc) -> list:
+def _bf16_copy(kind: str, role: str, src: View, rows: int, cols: int, code: list) -> tuple:
+    """bf16 copy [rows, pad8(cols)] of ``src`` (zero K padding), made once
+    per step and shared by the forward and backward contractions that read
+    it (memo keyed on the source node of ``role``)."""
+    ctx = current_ctx()
+    ld = _pad8(cols)
+    node = ctx.input_node(role)
+    key = (kind, id(node), src.ptr) if node is not None else None
+    ptr = ctx.memo.get(key) if key is not None else None
+    if ptr is None:
+        ptr = ctx.persistent(2 * rows * ld)
+        if key is not None:
+            ctx.memo[key] = ptr
+        code.append(_cast(src, rows, cols, ptr, rows, ld, False))
+    return ptr, ld
+
+
+def _gemm_ex(a, lda, a_mn, b, ldb, b_mn, c, ldc, m, n, k, bias=None, act=0, splits=1, ws=None):
+    flags = (1 if a_mn else 0) | (2 if b_mn else 0)
+    return instr(L.OP_GEMM_TC_EX, [a, b, bias, c, ws], [m, n, k, lda, ldb, ldc, flags, splits],
+                 act=act)
+
+
+def fc_forward_tc(x: View, w: View, b: Optional[View], out: View, act: int, alloc=None) -> list:
+    """y[B,H] = x[B,F] . W[H,F]^T (+b, act): both operands K-major."""
     bsz, f = _flat2(x.shape)
     h = w.shape[0]
-    fp = _pad8(f)
-    xb, wb = alloc(bsz * fp), alloc(h * fp)
-    return [_cast(x, bsz, f, xb, bsz, fp, False), _cast(w, h, f, wb, h, fp, False),
-            instr(L.OP_GEMM_TC, [xb, wb, b.ptr if b else None, out.ptr], [bsz, h, fp, fp, fp, h],
-                  act=act)]
+    code = []
+    xb, ldx = _bf16_copy("fcx", "in0", x, bsz, f, code)
+    wb, ldw = _bf16_copy("fcw", "in1", w, h, f, code)
+    code.append(_gemm_ex(xb, ldx, False, wb, ldw, False, out.ptr, h, bsz, h, f,
+                         bias=b.ptr if b else None, act=act))
+    return code
 
 
-def fc_dx_tc(og: View, w: View, dx: View, alloc) -> list:
+def fc_dx_tc(og: View, w: View, dx: View, alloc=None) -> list:
+    """dX[B,F] = og[B,H] . W[H,F]: og K-major, W MN-major (its own layout)."""
     bsz, h = og.shape
     f = w.shape[1]
-    hp = _pad8(h)
-    ogb, wtb = alloc(bsz * hp), alloc(f * hp)
-    return [_cast(og, bsz, h, ogb, bsz, hp, False), _cast(w, h, f, wtb, f, hp, True),
-            instr(L.OP_GEMM_TC, [ogb, wtb, None, dx.ptr], [bsz, f, hp, hp, hp, f])]
+    code = []
+    ogb, ldo = _bf16_copy("fcog", "og", og, bsz, h, code)
+    wb, ldw = _bf16_copy("fcw", "in1", w, h, f, code)
+    code.append(_gemm_ex(ogb, ldo, False, wb, ldw, True, dx.ptr, f, bsz, f, h))
+    return code
 
 
-def fc_dw_tc(og: View, x: View, dw: View, alloc) -> list:
+def fc_dw_tc(og: View, x: View, dw: View, alloc=None) -> list:
+    """dW[H,F] = og[B,H]^T . x[B,F]: both MN-major (batch is the contraction)."""
     bsz, h = og.shape
     f = _flat2(x.shape)[1]
-    bp = _pad8(bsz)
-    ogt, xt = alloc(h * bp), alloc(f * bp)
-    return [_cast(og, bsz, h, ogt, h, bp, True), _cast(x, bsz, f, xt, f, bp, True),
-            instr(L.OP_GEMM_TC, [ogt, xt, None, dw.ptr], [h, f, bp, bp, bp, f])]
+    code = []
+    ogb, ldo = _bf16_copy("fcog", "og", og, bsz, h, code)
+    xb, ldx = _bf16_copy("fcx", "in0", x, bsz, f, code)
+    import ctypes
+    nws = ctypes.c_int64()
+    L.call("mgx_gemm_splitk_workspace", h, f, bsz, ctypes.byref(nws))
+    ws = current_ctx().scratch(4 * nws.value) if nws.value else None
+    code.append(_gemm_ex(ogb, ldo, True, xb, ldx, True, dw.ptr, f, h, f, bsz,
+                         splits=0 if ws else 1, ws=ws))
+    return code
 
 
 def _fc_lower_fwd(ins, out, attrs):

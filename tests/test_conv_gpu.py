@@ -179,15 +179,20 @@ POOL_CASES = [
     ((2, 14, 14, 8), (3, 3), (1, 1), (1, 1), "avg"),
     ((2, 27, 27, 4), (3, 3), (2, 2), (1, 1), "max"),
     ((1, 7, 7, 32), (7, 7), (1, 1), (0, 0), "avg"),
+    ((2, 11, 11, 6), (3, 3), (2, 2), (1, 1), "max"),
+    ((2, 11, 11, 6), (3, 3), (1, 1), (1, 1), "avg"),
 ]
 
 
 @pytest.mark.parametrize("case", POOL_CASES)
 @pytest.mark.parametrize("ties", [False, True])
-def test_pooling_kernels(cuda, case, ties):
+@pytest.mark.parametrize("use_argmax", [False, True])
+def test_pooling_kernels(cuda, case, ties, use_argmax):
     torch = cuda
     from paper_1512_01274_b200 import _lib as L
     shape, k, s, p, kind = case
+    if use_argmax and (shape[3] % 4 or kind != "max"):
+        pytest.skip("argmax side buffer: max pooling with C % 4 == 0 only")
     g = torch.Generator().manual_seed(sum(shape))
     x = torch.randn(*shape, generator=g, dtype=torch.float64)
     if ties:  # post-ReLU maps: many equal zeros in a window
@@ -202,9 +207,11 @@ def test_pooling_kernels(cuda, case, ties):
     y = torch.empty(*yr.shape, device="cuda")
     dx = torch.empty(*shape, device="cuda")
     t = 0 if kind == "max" else 1
-    L.call("mgx_pool_forward", xd.data_ptr(), y.data_ptr(), _ptr(geom), 0, t, 0)
+    arg = torch.zeros(y.numel(), dtype=torch.uint8, device="cuda") if use_argmax else None
+    argp = arg.data_ptr() if arg is not None else None
+    L.call("mgx_pool_forward", xd.data_ptr(), y.data_ptr(), _ptr(geom), 0, t, argp, 0)
     L.call("mgx_pool_backward", xd.data_ptr(), y.data_ptr(), dyd.data_ptr(), dx.data_ptr(),
-           _ptr(geom), 0, t, 0)
+           _ptr(geom), 0, t, argp, 0)
     torch.cuda.synchronize()
     if kind == "max":
         np.testing.assert_array_equal(y.cpu().numpy(), yr.detach().float().numpy())

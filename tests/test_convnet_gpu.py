@@ -2,10 +2,12 @@
 data-parallel step (configs 3-5), against oracle/convnet.py (float64,
 operands of every tensor-core contraction rounded to bf16 like the device).
 
-Parity here is unpinned by the reference (it has no conv ops).  Stated
-tolerance for gradients: |device - oracle| <= 2e-2 * max|oracle| + rtol 2e-2
-(bf16 operand rounding of the output gradients compounds through the layers;
-the oracle rounds forward operands only), outputs rtol 1e-3 / atol 1e-4."""
+Parity here is unpinned by the reference (it has no conv ops).  The oracle
+rounds the operands of every convolution contraction (forward, dX, dW) to
+bf16 exactly where the device does, so what remains is fp32-vs-fp64
+accumulation order and bf16 ties flipped by upstream ulp differences.
+Stated tolerance for gradients: |device - oracle| <= 2e-2 * max|oracle| +
+rtol 2e-2; outputs rtol 1e-3 / atol 1e-4."""
 
 import numpy as np
 import pytest

@@ -1,0 +1,74 @@
+"""Per-instruction device profile of one training pass of a configuration:
+label, kernel family, shape, ms, achieved TFLOP/s or GB/s (diagnostics).
+
+    python tools/profile_net.py [inception_bn|alexnet|lenet|mlp] [--top N]
+"""
+
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import bench  # noqa: E402
+
+
+def main():
+    name = sys.argv[1] if len(sys.argv) > 1 else "inception_bn"
+    top = int(sys.argv[sys.argv.index("--top") + 1]) if "--top" in sys.argv else 60
+    import torch
+    from paper_1512_01274_b200 import symbol
+    from paper_1512_01274_b200 import tensor as tmod
+    from paper_1512_01274_b200.engine import Engine
+    from paper_1512_01274_b200.executor import bind
+    from paper_1512_01274_b200.train import aux_names, init_aux, init_params, param_names
+    cfg = bench.CONFIGS[name]
+    eng = Engine(device=0)
+    g = bench.build_graph(name)
+    b = cfg["batch"]
+    given = {"data": (b,) + cfg["image"], "label": (b,)}
+    shapes, _ = symbol.infer_shape(g, given)
+    x, y = bench.synthetic(name, b, 0)
+    p0, a0 = init_params(g, shapes, 0), init_aux(g, shapes)
+    names = param_names(g)
+    args = {"data": tmod.from_host(given["data"], "float32", x, engine=eng),
+            "label": tmod.from_host((b,), "float32", y, engine=eng)}
+    for n in names:
+        args[n] = tmod.from_host(shapes[n], "float32", p0[n], engine=eng)
+    for n in aux_names(g):
+        args[n] = tmod.from_host(shapes[n], "float32", a0[n], engine=eng)
+    grads = {n: tmod.zeros(shapes[n], engine=eng) for n in names}
+    ex = bind(g, args, {n: "write" for n in names}, grads, engine=eng, dense=cfg["dense"])
+    for _ in range(3):
+        ex.forward()
+        ex.backward()
+    eng.wait_all()
+    reps = 5
+    t = np.zeros(ex.num_instructions)
+    for _ in range(reps):
+        t += np.array([ms for _l, ms in ex.profile()]) / reps
+    rows = []
+    for i, ms in enumerate(t):
+        op = ex.instr_ops[i]
+        byt, fl = ex.instr_costs[i]
+        fam = bench.kernel_family(op)
+        rate = (f"{fl / ms / 1e9:8.1f} TF/s" if fam.startswith("tc_gemm")
+                else f"{byt / ms / 1e6:8.1f} GB/s")
+        d = list(ex._prog_dims[i]) if hasattr(ex, "_prog_dims") else []
+        rows.append((ms, i, ex.instr_labels[i], fam, rate, d))
+    total = t.sum()
+    print(f"{name}: {ex.num_instructions} instructions, {total:.3f} ms profiled pass, "
+          f"kernels {ex.kernel_count()}")
+    fams = {}
+    for ms, i, lbl, fam, rate, d in rows:
+        fams[fam] = fams.get(fam, 0) + ms
+    for fam, ms in sorted(fams.items(), key=lambda kv: -kv[1]):
+        print(f"  {fam:28s} {ms:8.3f} ms {100 * ms / total:5.1f}%")
+    for ms, i, lbl, fam, rate, d in sorted(rows, reverse=True)[:top]:
+        print(f"{ms:8.4f} ms  #{i:4d} {fam:24s} {rate}  {lbl}  {d}")
+
+
+if __name__ == "__main__":
+    main()
