@@ -150,6 +150,11 @@ int mgx_gemm_splitk_workspace(int64_t M, int64_t N, int64_t K, int64_t* out_floa
 /* col[m, k] (bf16, row stride ldk % 8 == 0) = x(NHWC) at tap k = (i, j, c) of
  * output pixel m; zero in the padding and for k >= kh*kw*C. */
 int mgx_im2col_bf16(const float* x, void* col, const int64_t* geom, int64_t ldk, uintptr_t stream);
+/* wf[c, (i*kw+j)*F + f] (bf16, row stride ld) = w[f, kh-1-i, kw-1-j, c]:
+ * the transposed-convolution weight of a stride-1 data gradient
+ * dX = im2col(dY, pad kh-1-ph) . wf^T. */
+int mgx_weight_flip_bf16(const float* w, int64_t F, int64_t kh, int64_t kw, int64_t C, void* wf,
+                         int64_t ld, uintptr_t stream);
 /* dx(NHWC) = adjoint of im2col applied to dcol (fp32, row stride ldk). */
 int mgx_col2im(const float* dcol, int64_t ldk, float* dx, const int64_t* geom, uintptr_t stream);
 /* fp64 workspace bytes for the per-channel reductions of an M x C matrix. */
@@ -162,12 +167,18 @@ int mgx_bn_stats(const float* x, int64_t M, int64_t C, void* ws, float* stats, f
 /* y = act((x - mean) * rstd * gamma + beta); gamma NULL = fix_gamma (1). */
 int mgx_bn_apply(const float* x, const float* stats, const float* gamma, const float* beta,
                  float* y, int64_t M, int64_t C, int act, uintptr_t stream);
-/* sums = [sum dy | sum dy*xhat] per channel (dbeta, dgamma). */
+/* sums = [sum dy | sum dy*xhat] per channel; also written to dbeta and
+ * dgamma when non-NULL (dgamma zero-filled when dgamma_zero: fix_gamma).
+ * mask (optional): a ReLU output; dy is then og * (mask > 0), the ReLU
+ * backward fused in. */
 int mgx_bn_bwd_reduce(const float* dy, const float* x, const float* stats, int64_t M, int64_t C,
-                      void* ws, float* sums, uintptr_t stream);
-/* dx = gamma * rstd * (dy - (sum dy + xhat * sum dy*xhat) / M). */
+                      void* ws, float* sums, float* dbeta, float* dgamma, int dgamma_zero,
+                      const float* mask, uintptr_t stream);
+/* dx = gamma * rstd * (dy - (sum dy + xhat * sum dy*xhat) / M), with the
+ * same optional ReLU mask; dy and mask may alias dx. */
 int mgx_bn_bwd_dx(const float* dy, const float* x, const float* stats, const float* sums,
-                  const float* gamma, float* dx, int64_t M, int64_t C, uintptr_t stream);
+                  const float* gamma, float* dx, int64_t M, int64_t C, const float* mask,
+                  uintptr_t stream);
 /* out[c] = sum over rows of x[r, c] (conv bias gradient). */
 int mgx_colsum(const float* x, int64_t M, int64_t C, void* ws, float* out, uintptr_t stream);
 /* Pooling, NHWC.  type 0 max (padding ignored), 1 avg (count_include_pad);
@@ -247,15 +258,17 @@ typedef struct mgx_instr {
                               /* dims=M,C,use_global fattr=eps,momentum            */
 #define MGX_OP_BN_APPLY 18    /* ptr0=x ptr1=stats ptr2=gamma ptr3=beta ptr4=y     */
                               /* dims=M,C act                                      */
-#define MGX_OP_BN_BWD_REDUCE 19 /* ptr0=dy ptr1=x ptr2=stats ptr3=ws ptr4=sums dims=M,C */
+#define MGX_OP_BN_BWD_REDUCE 19 /* ptr0=dy ptr1=x ptr2=stats ptr3=ws ptr4=sums     */
+                              /* ptr5=mask dims=M,C,dbeta*,dgamma*,dgamma_zero    */
 #define MGX_OP_BN_BWD_DX 20   /* ptr0=dy ptr1=x ptr2=stats ptr3=sums ptr4=gamma    */
-                              /* ptr5=dx dims=M,C                                  */
+                              /* ptr5=dx dims=M,C,mask*  (* = address in a dim)    */
 #define MGX_OP_POOL_FWD 21    /* ptr0=x ptr1=y ptr2=argmax dims=geom,full act=type */
 #define MGX_OP_POOL_BWD 22    /* ptr0=x ptr1=y ptr2=dy ptr3=dx ptr4=argmax dims=geom,full */
 #define MGX_OP_CHAN_COPY 23   /* ptr0=src ptr1=dst dims=rows,cols,lds,soff,ldd,doff */
 #define MGX_OP_COLSUM 24      /* ptr0=x ptr1=ws ptr2=out dims=M,C                  */
 #define MGX_OP_GEMM_TC_EX 25  /* ptr0=A ptr1=B ptr2=bias ptr3=C ptr4=workspace act */
                               /* dims=M,N,K,lda,ldb,ldc,(a_mn|b_mn<<1),splits      */
+#define MGX_OP_WFLIP 26       /* ptr0=w ptr1=wf(bf16) dims=F,kh,kw,C,ld            */
 
 /* Run instructions eagerly, in order, on stream (no program object). */
 int mgx_instr_run(const mgx_instr* instrs, int32_t count, uintptr_t stream);

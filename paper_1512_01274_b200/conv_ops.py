@@ -184,6 +184,23 @@ def _conv_lower_bwd(slot, env, out, attrs):
     if k == (1, 1) and s == (1, 1) and p == (0, 0):
         code.append(_gemm(dyb, ldf, False, wb, ldk, True, out.ptr, c, m, c, f))
         return code
+    if s == (1, 1) and p[0] < k[0] and p[1] < k[1]:
+        # stride 1: dX = im2col(dY, pad k-1-p) . wflip^T, a forward
+        # convolution of the output gradient (no fp32 dcol, no col2im)
+        kf = k[0] * k[1] * f
+        ldkf = _pad8(kf)
+        key = ("wflip", id(ctx.input_node("in1")), w.ptr)
+        wfl = ctx.memo.get(key)
+        if wfl is None:
+            wfl = ctx.persistent(2 * c * ldkf)
+            ctx.memo[key] = wfl
+            code.append(instr(L.OP_WFLIP, [w.ptr, wfl], [f, k[0], k[1], c, ldkf]))
+        b_, h_, w_ = x.shape[0], x.shape[1], x.shape[2]
+        dcolt = ctx.scratch(2 * b_ * h_ * w_ * ldkf)
+        pf = (k[0] - 1 - p[0], k[1] - 1 - p[1])
+        code.append(instr(L.OP_IM2COL, [og.ptr, dcolt], _geom(og.shape, k, (1, 1), pf) + [ldkf]))
+        code.append(_gemm(dcolt, ldkf, False, wfl, ldkf, False, out.ptr, c, b_ * h_ * w_, c, kf))
+        return code
     dcol = ctx.scratch(4 * m * kk)
     code.append(_gemm(dyb, ldf, False, wb, ldk, True, dcol, kk, m, kk, f))
     code.append(instr(L.OP_COL2IM, [dcol, out.ptr], _geom(x.shape, k, s, p) + [kk]))
@@ -231,10 +248,11 @@ def _bn_infer(shapes, attrs):
             [tuple(data)])
 
 
-def _bn_stats(x: View, attrs, ctx, code: list, update: bool, mm=None, mv=None) -> int:
+def _bn_stats(x: View, attrs, ctx, code: list, update: bool, mm=None, mv=None,
+              xnode=None) -> int:
     m, c = prod(x.shape[:-1]), x.shape[-1]
     eps = float(attrs.get("eps", 1e-3))
-    key = ("bnstats", id(ctx.input_node("in0")), x.ptr, eps)
+    key = ("bnstats", id(xnode if xnode is not None else ctx.input_node("in0")), x.ptr, eps)
     st = ctx.memo.get(key)
     if st is None:
         st = ctx.persistent(8 * c)
@@ -278,16 +296,40 @@ def _bn_lower_bwd(slot, env, out, attrs):
         sums = ctx.persistent(8 * c)
         ctx.memo[key] = sums
         ws = ctx.scratch(_reduce_ws(m, c))
-        code.append(instr(L.OP_BN_BWD_REDUCE, [og.ptr, x.ptr, st, ws, sums], [m, c]))
+        code.append(instr(L.OP_BN_BWD_REDUCE, [og.ptr, x.ptr, st, ws, sums, None], [m, c, 0, 0, 0]))
     fix = attrs.get("fix_gamma", True)
     if slot == 0:
         gamma = None if fix else env["in1"].ptr
-        code.append(instr(L.OP_BN_BWD_DX, [og.ptr, x.ptr, st, sums, gamma, out.ptr], [m, c]))
+        code.append(instr(L.OP_BN_BWD_DX, [og.ptr, x.ptr, st, sums, gamma, out.ptr], [m, c, 0]))
     elif slot == 1:
         code.append(instr(L.OP_FILL, [out.ptr], [c], [0.0]) if fix else
                     instr(L.OP_COPY, [sums + 4 * c, out.ptr], [c]))
     else:
         code.append(instr(L.OP_COPY, [sums, out.ptr], [c]))
+    return code
+
+
+def bn_backward_group(og: View, relu_y: Optional[View], x: View, gamma: View, attrs,
+                      xnode, dx: Optional[View], dgamma: Optional[View],
+                      dbeta: Optional[View]) -> list:
+    """All requested BatchNorm gradients of one node in one pass pair (the
+    executor's fusion of the sibling Backward nodes, optionally with the
+    ReLU backward in front of them): one reduction that also writes dbeta /
+    dgamma, then dx.  relu_y: the ReLU output whose mask applies to og."""
+    ctx = current_ctx()
+    m, c = prod(x.shape[:-1]), x.shape[-1]
+    code = []
+    st = _bn_stats(x, attrs, ctx, code, update=False, xnode=xnode)
+    fix = attrs.get("fix_gamma", True)
+    sums = ctx.persistent(8 * c)
+    ws = ctx.scratch(_reduce_ws(m, c))
+    mask = relu_y.ptr if relu_y is not None else None
+    code.append(instr(L.OP_BN_BWD_REDUCE, [og.ptr, x.ptr, st, ws, sums, mask],
+                      [m, c, dbeta.ptr if dbeta else 0, dgamma.ptr if dgamma else 0,
+                       1 if fix else 0]))
+    if dx is not None:
+        code.append(instr(L.OP_BN_BWD_DX, [og.ptr, x.ptr, st, sums, None if fix else gamma.ptr,
+                                           dx.ptr], [m, c, mask or 0]))
     return code
 
 

@@ -151,6 +151,27 @@ __global__ void col2im_kernel(const float* __restrict__ dcol, int64_t ldk, float
   }
 }
 
+// wf[c, (i*kw + j)*F + f] (bf16, row stride ld, zero beyond kh*kw*F) =
+// w[f, kh-1-i, kw-1-j, c]: the weight of the transposed convolution that
+// computes a stride-1 data gradient as im2col(dY) . wf^T.
+__global__ void weight_flip_kernel(const float* __restrict__ w, int F, int kh, int kw, int C,
+                                   __nv_bfloat16* __restrict__ wf, int64_t ld) {
+  const int64_t total = int64_t(C) * ld;
+  const int K = kh * kw * F;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < total; idx += stride) {
+    const int c = static_cast<int>(idx / ld);
+    const int k = static_cast<int>(idx - int64_t(c) * ld);
+    float v = 0.0f;
+    if (k < K) {
+      const int tap = k / F, f = k - tap * F;
+      const int i = tap / kw, j = tap - (tap / kw) * kw;
+      v = __ldg(w + ((int64_t(f) * kh + (kh - 1 - i)) * kw + (kw - 1 - j)) * C + c);
+    }
+    wf[idx] = __float2bfloat16_rn(v);
+  }
+}
+
 // ------------------------------------------------------- column reductions
 // Per-channel sums over the M rows of an [M, C] matrix, in two fixed-order
 // stages: block z reduces rows [z*rpc, (z+1)*rpc) into ws[z][*] (fp64), then
@@ -167,7 +188,7 @@ template <int MODE>
 __global__ void __launch_bounds__(kRedThreads)
 colreduce_partial_kernel(const float* __restrict__ a, const float* __restrict__ xs,
                          const float* __restrict__ stats, int64_t M, int C, int64_t rpc,
-                         double* __restrict__ ws) {
+                         double* __restrict__ ws, const float* __restrict__ mask) {
   extern __shared__ double red[];  // [rpp][2*C]
   const int tpr = C < kRedThreads ? C : kRedThreads;  // threads per row
   const int rpp = kRedThreads / tpr;                  // rows per pass
@@ -187,7 +208,8 @@ colreduce_partial_kernel(const float* __restrict__ a, const float* __restrict__ 
       }
       if (MODE == 0) shift = __ldg(a + c);  // row 0: shifted sums avoid cancellation
       for (int64_t r = r0 + r_in; r < r1; r += rpp) {
-        const float v = __ldg(a + r * C + c) - shift;
+        float v = __ldg(a + r * C + c) - shift;
+        if (MODE == 1 && mask && !(__ldg(mask + r * C + c) > 0.0f)) v = 0.0f;
         s0 += v;
         if (MODE == 0) s1 += double(v) * double(v);
         if (MODE == 1) s1 += double(v) * double((__ldg(xs + r * C + c) - mean) * rstd);
@@ -221,7 +243,7 @@ template <int MODE>
 __global__ void __launch_bounds__(kRedThreads)
 colreduce_partial_vec_kernel(const float* __restrict__ a, const float* __restrict__ xs,
                              const float* __restrict__ stats, int64_t M, int C, int64_t rpc,
-                             double* __restrict__ ws) {
+                             double* __restrict__ ws, const float* __restrict__ mask) {
   extern __shared__ double red[];  // [rpp][2][ct]
   const int C4 = C >> 2;
   const int ct4 = C4 < kRedThreads ? C4 : kRedThreads;  // float4 groups per block row
@@ -256,6 +278,17 @@ colreduce_partial_vec_kernel(const float* __restrict__ a, const float* __restric
         v[u] = __ldg(a4 + (r + u * rpp) * C4 + c4);
         if (MODE == 1) xv[u] = __ldg(x4 + (r + u * rpp) * C4 + c4);
       }
+      if (MODE == 1 && mask) {
+        // dy = og * (relu output > 0): the fused ReLU backward
+#pragma unroll
+        for (int u = 0; u < kRedUnroll; ++u) {
+          const float4 y = __ldg(reinterpret_cast<const float4*>(mask) + (r + u * rpp) * C4 + c4);
+          v[u].x = y.x > 0.0f ? v[u].x : 0.0f;
+          v[u].y = y.y > 0.0f ? v[u].y : 0.0f;
+          v[u].z = y.z > 0.0f ? v[u].z : 0.0f;
+          v[u].w = y.w > 0.0f ? v[u].w : 0.0f;
+        }
+      }
 #pragma unroll
       for (int u = 0; u < kRedUnroll; ++u) {
         const float* pv = &v[u].x;
@@ -276,9 +309,16 @@ colreduce_partial_vec_kernel(const float* __restrict__ a, const float* __restric
       }
     }
     for (; r < r1; r += rpp) {
-      const float4 v = __ldg(a4 + r * C4 + c4);
+      float4 v = __ldg(a4 + r * C4 + c4);
       float4 xv = v;
       if (MODE == 1) xv = __ldg(x4 + r * C4 + c4);
+      if (MODE == 1 && mask) {
+        const float4 y = __ldg(reinterpret_cast<const float4*>(mask) + r * C4 + c4);
+        v.x = y.x > 0.0f ? v.x : 0.0f;
+        v.y = y.y > 0.0f ? v.y : 0.0f;
+        v.z = y.z > 0.0f ? v.z : 0.0f;
+        v.w = y.w > 0.0f ? v.w : 0.0f;
+      }
       const float* pv = &v.x;
       const float* px = &xv.x;
 #pragma unroll
@@ -392,15 +432,20 @@ __global__ void bn_stats_finalize_kernel(const double* __restrict__ ws, int nchu
   if (mvar) mvar[c] = static_cast<float>(double(mvar[c]) * momentum + var * (1.0 - momentum));
 }
 
-// MODE 1/2 finalize: out[c] = sum0, out[C + c] = sum1 (MODE 1) as fp32
+// MODE 1/2 finalize: out[c] = sum0, out[C + c] = sum1 (MODE 1) as fp32;
+// optionally also straight into gradient buffers: out0[c] = sum0 and
+// out1[c] = sum1 (or 0 when zero1: BatchNorm's fix_gamma)
 __global__ void colsum_finalize_kernel(const double* __restrict__ ws, int nchunk, int C, int two,
-                                       float* __restrict__ out) {
+                                       float* __restrict__ out, float* __restrict__ out0,
+                                       float* __restrict__ out1, int zero1) {
   const int c = blockIdx.x * 32 + threadIdx.x;
   double s = 0.0, q = 0.0;
   merge_chunks(ws, nchunk, C, c, two != 0, &s, &q);
   if (threadIdx.y != 0 || c >= C) return;
   out[c] = static_cast<float>(s);
   if (two) out[C + c] = static_cast<float>(q);
+  if (out0) out0[c] = static_cast<float>(s);
+  if (out1) out1[c] = zero1 ? 0.0f : static_cast<float>(q);
 }
 
 // y = (x - mean) * rstd * gamma + beta, then act; gamma == nullptr: fixed 1
@@ -434,19 +479,51 @@ __global__ void bn_apply_kernel(const float* __restrict__ x, const float* __rest
 }
 
 // dx = gamma * rstd * (dy - (sum_dy + xhat * sum_dyxhat) / M)
-__global__ void bn_bwd_dx_kernel(const float* __restrict__ dy, const float* __restrict__ x,
+// (mask: relu output; dy is taken as og * (mask > 0), the fused ReLU
+// backward.  dy/mask may alias dx: each element is read before written.)
+__global__ void bn_bwd_dx_kernel(const float* dy, const float* __restrict__ x,
                                  const float* __restrict__ stats, const float* __restrict__ sums,
-                                 const float* __restrict__ gamma, float* __restrict__ dx, int64_t M,
-                                 int C) {
+                                 const float* __restrict__ gamma, float* dx, int64_t M, int C,
+                                 const float* mask) {
   const int64_t total = M * C;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   const float invm = static_cast<float>(1.0 / double(M));
+  if ((C & 3) == 0) {
+    const int64_t t4 = total >> 2;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < t4; i += stride) {
+      const int c0 = static_cast<int>((i << 2) % C);
+      float4 d = reinterpret_cast<const float4*>(dy)[i];
+      const float4 xv = __ldg(reinterpret_cast<const float4*>(x) + i);
+      float* pd = &d.x;
+      const float* px = &xv.x;
+      if (mask) {
+        const float4 y = reinterpret_cast<const float4*>(mask)[i];
+        const float* py = &y.x;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) pd[q] = py[q] > 0.0f ? pd[q] : 0.0f;
+      }
+      float4 o;
+      float* po = &o.x;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int c = c0 + q;
+        const float rstd = __ldg(stats + C + c);
+        const float xhat = (px[q] - __ldg(stats + c)) * rstd;
+        const float g = gamma ? __ldg(gamma + c) : 1.0f;
+        po[q] = g * rstd * (pd[q] - (__ldg(sums + c) + xhat * __ldg(sums + C + c)) * invm);
+      }
+      reinterpret_cast<float4*>(dx)[i] = o;
+    }
+    return;
+  }
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
     const int c = static_cast<int>(i % C);
     const float rstd = __ldg(stats + C + c);
     const float xhat = (x[i] - __ldg(stats + c)) * rstd;
     const float g = gamma ? __ldg(gamma + c) : 1.0f;
-    dx[i] = g * rstd * (dy[i] - (__ldg(sums + c) + xhat * __ldg(sums + C + c)) * invm);
+    float d = dy[i];
+    if (mask && !(mask[i] > 0.0f)) d = 0.0f;
+    dx[i] = g * rstd * (d - (__ldg(sums + c) + xhat * __ldg(sums + C + c)) * invm);
   }
 }
 
@@ -679,23 +756,26 @@ inline void chunks_for(int64_t M, int64_t* rpc, int* nchunk) {
 
 template <int MODE>
 int launch_partial(const float* a, const float* xs, const float* stats, int64_t M, int C,
-                   double* ws, int* nchunk_out, cudaStream_t st) {
+                   double* ws, int* nchunk_out, cudaStream_t st, const float* mask = nullptr) {
   int64_t rpc;
   int nchunk;
   chunks_for(M, &rpc, &nchunk);
-  const bool vec = (C % 4) == 0 && aligned16(a) && (MODE != 1 || aligned16(xs));
+  const bool vec = (C % 4) == 0 && aligned16(a) && (MODE != 1 || aligned16(xs)) &&
+                   (!mask || aligned16(mask));
   if (vec) {
     const int C4 = C / 4;
     const int ct4 = C4 < kRedThreads ? C4 : kRedThreads;
     const int rpp = kRedThreads / ct4;
     const size_t smem = size_t(rpp) * 2 * ct4 * 4 * sizeof(double);
     dim3 grid(nchunk, static_cast<unsigned>(ceil_div(C4, ct4)));
-    colreduce_partial_vec_kernel<MODE><<<grid, kRedThreads, smem, st>>>(a, xs, stats, M, C, rpc, ws);
+    colreduce_partial_vec_kernel<MODE><<<grid, kRedThreads, smem, st>>>(a, xs, stats, M, C, rpc, ws,
+                                                                      mask);
   } else {
     const int tpr = C < kRedThreads ? C : kRedThreads;
     const int rpp = kRedThreads / tpr;
     const size_t smem = size_t(rpp) * 2 * tpr * sizeof(double);
-    colreduce_partial_kernel<MODE><<<nchunk, kRedThreads, smem, st>>>(a, xs, stats, M, C, rpc, ws);
+    colreduce_partial_kernel<MODE><<<nchunk, kRedThreads, smem, st>>>(a, xs, stats, M, C, rpc, ws,
+                                                                    mask);
   }
   *nchunk_out = nchunk;
   MGX_LAUNCHED();
@@ -776,24 +856,30 @@ extern "C" int mgx_bn_apply(const float* x, const float* stats, const float* gam
 }
 
 extern "C" int mgx_bn_bwd_reduce(const float* dy, const float* x, const float* stats, int64_t M,
-                                 int64_t C, void* ws, float* sums, uintptr_t stream) {
+                                 int64_t C, void* ws, float* sums, float* dbeta, float* dgamma,
+                                 int dgamma_zero, const float* mask, uintptr_t stream) {
   MGX_REQUIRE(dy && x && stats && ws && sums && M > 0 && C > 0, "mgx_bn_bwd_reduce: bad arguments");
   cudaStream_t st = mgx::as_stream(stream);
   int nchunk = 0;
   MGX_TRY(mgx::conv::launch_partial<1>(dy, x, stats, M, static_cast<int>(C), static_cast<double*>(ws),
-                                       &nchunk, st));
+                                       &nchunk, st, mask));
   mgx::conv::colsum_finalize_kernel<<<static_cast<unsigned>(mgx::ceil_div(C, 32)),
                                        dim3(32, mgx::conv::kFinLanes), 0, st>>>(
-      static_cast<const double*>(ws), nchunk, static_cast<int>(C), 1, sums);
+      static_cast<const double*>(ws), nchunk, static_cast<int>(C), 1, sums, dbeta, dgamma,
+      dgamma_zero);
   MGX_LAUNCHED();
   return MGX_OK;
 }
 
 extern "C" int mgx_bn_bwd_dx(const float* dy, const float* x, const float* stats, const float* sums,
-                             const float* gamma, float* dx, int64_t M, int64_t C, uintptr_t stream) {
+                             const float* gamma, float* dx, int64_t M, int64_t C, const float* mask,
+                             uintptr_t stream) {
   MGX_REQUIRE(dy && x && stats && sums && dx && M > 0 && C > 0, "mgx_bn_bwd_dx: bad arguments");
-  mgx::conv::bn_bwd_dx_kernel<<<grid_for(M * C), 256, 0, mgx::as_stream(stream)>>>(
-      dy, x, stats, sums, gamma, dx, M, static_cast<int>(C));
+  const bool vec = (C % 4) == 0 && mgx::aligned16(dy) && mgx::aligned16(x) && mgx::aligned16(dx) &&
+                   (!mask || mgx::aligned16(mask));
+  MGX_REQUIRE(vec || (C % 4) != 0, "mgx_bn_bwd_dx: C %% 4 == 0 needs 16-byte aligned tensors");
+  mgx::conv::bn_bwd_dx_kernel<<<grid_for(M * C / ((C & 3) ? 1 : 4)), 256, 0, mgx::as_stream(stream)>>>(
+      dy, x, stats, sums, gamma, dx, M, static_cast<int>(C), mask);
   MGX_LAUNCHED();
   return MGX_OK;
 }
@@ -807,7 +893,7 @@ extern "C" int mgx_colsum(const float* x, int64_t M, int64_t C, void* ws, float*
                                        static_cast<double*>(ws), &nchunk, st));
   mgx::conv::colsum_finalize_kernel<<<static_cast<unsigned>(mgx::ceil_div(C, 32)),
                                        dim3(32, mgx::conv::kFinLanes), 0, st>>>(
-      static_cast<const double*>(ws), nchunk, static_cast<int>(C), 0, out);
+      static_cast<const double*>(ws), nchunk, static_cast<int>(C), 0, out, nullptr, nullptr, 0);
   MGX_LAUNCHED();
   return MGX_OK;
 }
@@ -862,6 +948,17 @@ extern "C" int mgx_chan_copy(const float* src, int64_t lds, int64_t soff, float*
   if (rows == 0 || cols == 0) return MGX_OK;
   mgx::conv::chan_copy_kernel<<<grid_for(rows * cols / 4 + 1), 256, 0, mgx::as_stream(stream)>>>(
       src, lds, soff, dst, ldd, doff, rows, cols);
+  MGX_LAUNCHED();
+  return MGX_OK;
+}
+
+extern "C" int mgx_weight_flip_bf16(const float* w, int64_t F, int64_t kh, int64_t kw, int64_t C,
+                                    void* wf, int64_t ld, uintptr_t stream) {
+  MGX_REQUIRE(w && wf && F > 0 && kh > 0 && kw > 0 && C > 0 && ld >= kh * kw * F,
+              "mgx_weight_flip_bf16: bad arguments");
+  mgx::conv::weight_flip_kernel<<<grid_for(C * ld), 256, 0, mgx::as_stream(stream)>>>(
+      w, static_cast<int>(F), static_cast<int>(kh), static_cast<int>(kw), static_cast<int>(C),
+      static_cast<__nv_bfloat16*>(wf), ld);
   MGX_LAUNCHED();
   return MGX_OK;
 }

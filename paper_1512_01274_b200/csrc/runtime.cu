@@ -260,15 +260,19 @@ static int run_instr(const mgx_instr& in, cudaStream_t st) {
     case MGX_OP_BN_APPLY:
       return mgx_bn_apply(p0, p1, p2, p3, static_cast<float*>(in.ptr[4]), d[0], d[1], in.act, s);
     case MGX_OP_BN_BWD_REDUCE:
-      return mgx_bn_bwd_reduce(p0, p1, p2, d[0], d[1], in.ptr[3], static_cast<float*>(in.ptr[4]), s);
+      return mgx_bn_bwd_reduce(p0, p1, p2, d[0], d[1], in.ptr[3], static_cast<float*>(in.ptr[4]),
+                               reinterpret_cast<float*>(d[2]), reinterpret_cast<float*>(d[3]),
+                               static_cast<int>(d[4]), static_cast<const float*>(in.ptr[5]), s);
     case MGX_OP_BN_BWD_DX:
       return mgx_bn_bwd_dx(p0, p1, p2, p3, static_cast<float*>(in.ptr[4]),
-                           static_cast<float*>(in.ptr[5]), d[0], d[1], s);
+                           static_cast<float*>(in.ptr[5]), d[0], d[1],
+                           reinterpret_cast<const float*>(d[2]), s);
     case MGX_OP_POOL_FWD:
       return mgx_pool_forward(p0, p1, d, static_cast<int>(d[7]), in.act, in.ptr[2], s);
     case MGX_OP_POOL_BWD:
       return mgx_pool_backward(p0, p1, p2, p3, d, static_cast<int>(d[7]), in.act, in.ptr[4], s);
     case MGX_OP_CHAN_COPY: return mgx_chan_copy(p0, d[2], d[3], p1, d[4], d[5], d[0], d[1], s);
+    case MGX_OP_WFLIP: return mgx_weight_flip_bf16(p0, d[0], d[1], d[2], d[3], in.ptr[1], d[4], s);
     case MGX_OP_COLSUM: return mgx_colsum(p0, d[0], d[1], in.ptr[1], p2, s);
     case MGX_OP_GEMM_TC_EX:
       return mgx_gemm_bf16_tc_ex(in.ptr[0], d[3], static_cast<int>(d[6] & 1), in.ptr[1], d[4],

@@ -153,9 +153,9 @@ def test_batchnorm_kernels(cuda, m, c, fix_gamma):
            mv.data_ptr(), 1e-3, 0.9, 0, 0)
     L.call("mgx_bn_apply", xd.data_ptr(), st.data_ptr(), gp, bd.data_ptr(), y.data_ptr(), m, c, 0, 0)
     L.call("mgx_bn_bwd_reduce", dyd.data_ptr(), xd.data_ptr(), st.data_ptr(), m, c, ws.data_ptr(),
-           sums.data_ptr(), 0)
+           sums.data_ptr(), None, None, 0, None, 0)
     L.call("mgx_bn_bwd_dx", dyd.data_ptr(), xd.data_ptr(), st.data_ptr(), sums.data_ptr(), gp,
-           dx.data_ptr(), m, c, 0)
+           dx.data_ptr(), m, c, None, 0)
     torch.cuda.synchronize()
     xr = xd.double().cpu().requires_grad_(True)
     gr = gd.double().cpu().requires_grad_(True)
