@@ -424,9 +424,11 @@ def kv_round_ms(step, kv, eng, steps):
     ka, kb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ms = []
     for _ in range(max(1, min(steps, 10))):
+        # pushes launch the fused round as soon as a bucket is complete:
+        # bracket the pushes and the final flush
+        ka.record(eng.stream)
         for i in range(len(step.names)):
             kv.push(i, step.grads[w][step.names[i]], w)
-        ka.record(eng.stream)
         with kv._lock:
             kv._flush_locked()
         kb.record(eng.stream)

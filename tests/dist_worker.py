@@ -95,6 +95,40 @@ def check_capture(eng, world, rank, failures):
             failures.append(f"capture {n} differs from eager")
 
 
+def check_convnet(eng, world, rank, failures):
+    """LeNet (bf16 tensor-core convs, config 3) trained 3 steps with one
+    rank per GPU == the same step with all `world` workers in one process
+    (bitwise: identical kernels, identical tree order in the store)."""
+    from paper_1512_01274_b200 import nets, symbol
+    from paper_1512_01274_b200 import tensor as tmod
+    from paper_1512_01274_b200.kvstore import KVStore
+    from paper_1512_01274_b200.optim import SGDConfig, make_sgd_updater
+    from paper_1512_01274_b200.train import DataParallelStep, init_params
+    rs = np.random.RandomState(7)
+    xs = rs.randn(3, 16 * world, 28, 28, 1).astype(F32)
+    ls = rs.randint(0, 10, (3, 16 * world)).astype(F32)
+    given = {"data": (16, 28, 28, 1), "label": (16,)}
+    results = []
+    for distributed in (True, False):
+        symbol.reset_names()
+        g = nets.lenet(10)
+        shapes, _ = symbol.infer_shape(g, given)
+        kv = KVStore(1, world, engine=eng, distributed=distributed)
+        st = DataParallelStep(g, kv, given, init_params(g, shapes, 0), engine=eng, dense="bf16")
+        kv.set_updater(make_sgd_updater(SGDConfig(0.05, 0.9, 1e-4), scale=world))
+        for s in range(3):
+            st.step({w: (xs[s, 16 * w:16 * (w + 1)], ls[s, 16 * w:16 * (w + 1)])
+                     for w in st.workers})
+        kv.round_barrier()
+        w0 = st.workers[0]
+        results.append({n: tmod.to_numpy(st.args[w0][n]) for n in st.names})
+        kv.close()
+    for n in results[0]:
+        if not np.array_equal(results[0][n], results[1][n]):
+            failures.append(f"convnet {n}: distributed != single-process "
+                            f"(max diff {np.abs(results[0][n] - results[1][n]).max()})")
+
+
 def main():
     import torch
     import torch.distributed as dist
@@ -105,7 +139,7 @@ def main():
     from paper_1512_01274_b200.engine import Engine
     eng = Engine(device=local)
     failures = []
-    for check in (check_kv_golden, check_training, check_capture):
+    for check in (check_kv_golden, check_training, check_capture, check_convnet):
         try:
             check(eng, world, rank, failures)
         except Exception:  # noqa: BLE001
