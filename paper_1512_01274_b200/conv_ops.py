@@ -300,7 +300,7 @@ def _bn_lower_bwd(slot, env, out, attrs):
     fix = attrs.get("fix_gamma", True)
     if slot == 0:
         gamma = None if fix else env["in1"].ptr
-        code.append(instr(L.OP_BN_BWD_DX, [og.ptr, x.ptr, st, sums, gamma, out.ptr], [m, c, 0]))
+        code.append(instr(L.OP_BN_BWD_DX, [og.ptr, x.ptr, st, sums, gamma, out.ptr], [m, c, 0, 0, 0]))
     elif slot == 1:
         code.append(instr(L.OP_FILL, [out.ptr], [c], [0.0]) if fix else
                     instr(L.OP_COPY, [sums + 4 * c, out.ptr], [c]))
@@ -311,7 +311,7 @@ def _bn_lower_bwd(slot, env, out, attrs):
 
 def bn_backward_group(og: View, relu_y: Optional[View], x: View, gamma: View, attrs,
                       xnode, dx: Optional[View], dgamma: Optional[View],
-                      dbeta: Optional[View]) -> list:
+                      dbeta: Optional[View], dbias_conv: Optional[View] = None) -> list:
     """All requested BatchNorm gradients of one node in one pass pair (the
     executor's fusion of the sibling Backward nodes, optionally with the
     ReLU backward in front of them): one reduction that also writes dbeta /
@@ -328,8 +328,10 @@ def bn_backward_group(og: View, relu_y: Optional[View], x: View, gamma: View, at
                       [m, c, dbeta.ptr if dbeta else 0, dgamma.ptr if dgamma else 0,
                        1 if fix else 0]))
     if dx is not None:
+        dws = ctx.scratch(_reduce_ws(m, c)) if dbias_conv is not None else 0
         code.append(instr(L.OP_BN_BWD_DX, [og.ptr, x.ptr, st, sums, None if fix else gamma.ptr,
-                                           dx.ptr], [m, c, mask or 0]))
+                                           dx.ptr],
+                          [m, c, mask or 0, dbias_conv.ptr if dbias_conv is not None else 0, dws]))
     return code
 
 

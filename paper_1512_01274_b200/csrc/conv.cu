@@ -402,6 +402,75 @@ __device__ __forceinline__ void merge_chunks(const double* __restrict__ ws, int 
   }
 }
 
+// BatchNorm dx pass that also reduces its own output per channel (the
+// gradient of the bias of the convolution feeding the BatchNorm): the row
+// tiling of colreduce_partial_vec_kernel, dx written elementwise, fp32
+// partial sums of dx merged per block in fp64 into ws[chunk][C].
+__global__ void __launch_bounds__(kRedThreads)
+bn_dx_colsum_kernel(const float* dy, const float* __restrict__ x, const float* __restrict__ stats,
+                    const float* __restrict__ sums, const float* __restrict__ gamma, float* dx,
+                    const float* mask, int64_t M, int C, int64_t rpc, double* __restrict__ ws) {
+  extern __shared__ double red[];  // [rpp][ct]
+  const int C4 = C >> 2;
+  const int ct4 = C4 < kRedThreads ? C4 : kRedThreads;
+  const int rpp = kRedThreads / ct4;
+  const int ct = ct4 * 4;
+  const int t = threadIdx.x;
+  const int r_in = t / ct4, c_in = t - (t / ct4) * ct4;
+  const int c4 = blockIdx.y * ct4 + c_in;
+  const bool active = r_in < rpp && c4 < C4;
+  const int64_t r0 = int64_t(blockIdx.x) * rpc;
+  const int64_t r1 = min(M, r0 + rpc);
+  const float invm = static_cast<float>(1.0 / double(M));
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  if (active) {
+    float mu[4], rs[4], g[4], s1[4], s2[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int c = c4 * 4 + q;
+      mu[q] = __ldg(stats + c);
+      rs[q] = __ldg(stats + C + c);
+      g[q] = gamma ? __ldg(gamma + c) : 1.0f;
+      s1[q] = __ldg(sums + c);
+      s2[q] = __ldg(sums + C + c);
+    }
+    for (int64_t r = r0 + r_in; r < r1; r += rpp) {
+      const int64_t i = r * C4 + c4;
+      float4 d = reinterpret_cast<const float4*>(dy)[i];
+      const float4 xv = __ldg(reinterpret_cast<const float4*>(x) + i);
+      float* pd = &d.x;
+      const float* px = &xv.x;
+      if (mask) {
+        const float4 y = reinterpret_cast<const float4*>(mask)[i];
+        const float* py = &y.x;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) pd[q] = py[q] > 0.0f ? pd[q] : 0.0f;
+      }
+      float4 o;
+      float* po = &o.x;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float xhat = (px[q] - mu[q]) * rs[q];
+        po[q] = g[q] * rs[q] * (pd[q] - (s1[q] + xhat * s2[q]) * invm);
+        acc[q] += po[q];
+      }
+      reinterpret_cast<float4*>(dx)[i] = o;
+    }
+  }
+  if (r_in < rpp) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) red[r_in * ct + c_in * 4 + q] = acc[q];
+  }
+  __syncthreads();
+  for (int c = t; c < ct; c += blockDim.x) {
+    const int cg = blockIdx.y * ct + c;
+    if (cg >= C) continue;
+    double u = 0.0;
+    for (int rr = 0; rr < rpp; ++rr) u += red[rr * ct + c];
+    ws[int64_t(blockIdx.x) * C + cg] = u;
+  }
+}
+
 // MODE 0 finalize: stats = [mean | rstd] (batch statistics, biased variance
 // like MXNet), moving averages updated when given.
 // use_global: stats from the moving averages (inference).
@@ -666,8 +735,8 @@ __global__ void pool_fwd_vec_kernel(const float* __restrict__ x, float* __restri
         reinterpret_cast<uchar4*>(arg)[idx] = a4;
       }
     } else {
-      const float area = pool_area(g, oh, ow);
-      o = make_float4(fdiv(acc[0], area), fdiv(acc[1], area), fdiv(acc[2], area), fdiv(acc[3], area));
+      const float inv = 1.0f / pool_area(g, oh, ow);
+      o = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
     }
     reinterpret_cast<float4*>(y)[idx] = o;
   }
@@ -708,9 +777,9 @@ __global__ void pool_bwd_vec_kernel(const uint8_t* __restrict__ arg, const float
           for (int q = 0; q < 4; ++q)
             if (pa[q] == li) acc[q] = fadd(acc[q], pd[q]);
         } else {
-          const float area = pool_area(g, oh, ow);
+          const float inv = 1.0f / pool_area(g, oh, ow);
 #pragma unroll
-          for (int q = 0; q < 4; ++q) acc[q] = fadd(acc[q], fdiv(pd[q], area));
+          for (int q = 0; q < 4; ++q) acc[q] = fadd(acc[q], pd[q] * inv);
         }
       }
     }
@@ -873,12 +942,32 @@ extern "C" int mgx_bn_bwd_reduce(const float* dy, const float* x, const float* s
 
 extern "C" int mgx_bn_bwd_dx(const float* dy, const float* x, const float* stats, const float* sums,
                              const float* gamma, float* dx, int64_t M, int64_t C, const float* mask,
-                             uintptr_t stream) {
+                             float* dsum, void* ws, uintptr_t stream) {
   MGX_REQUIRE(dy && x && stats && sums && dx && M > 0 && C > 0, "mgx_bn_bwd_dx: bad arguments");
   const bool vec = (C % 4) == 0 && mgx::aligned16(dy) && mgx::aligned16(x) && mgx::aligned16(dx) &&
                    (!mask || mgx::aligned16(mask));
   MGX_REQUIRE(vec || (C % 4) != 0, "mgx_bn_bwd_dx: C %% 4 == 0 needs 16-byte aligned tensors");
-  mgx::conv::bn_bwd_dx_kernel<<<grid_for(M * C / ((C & 3) ? 1 : 4)), 256, 0, mgx::as_stream(stream)>>>(
+  cudaStream_t st = mgx::as_stream(stream);
+  if (dsum) {
+    // fused: dx plus its per-channel sum (conv bias gradient) in one pass
+    MGX_REQUIRE(ws && vec, "mgx_bn_bwd_dx: dsum needs a workspace and C %% 4 == 0");
+    int64_t rpc;
+    int nchunk;
+    mgx::conv::chunks_for(M, &rpc, &nchunk);
+    const int C4 = static_cast<int>(C / 4);
+    const int ct4 = C4 < mgx::conv::kRedThreads ? C4 : mgx::conv::kRedThreads;
+    const int rpp = mgx::conv::kRedThreads / ct4;
+    const size_t smem = size_t(rpp) * ct4 * 4 * sizeof(double);
+    dim3 grid(nchunk, static_cast<unsigned>(mgx::ceil_div(C4, ct4)));
+    mgx::conv::bn_dx_colsum_kernel<<<grid, mgx::conv::kRedThreads, smem, st>>>(
+        dy, x, stats, sums, gamma, dx, mask, M, static_cast<int>(C), rpc, static_cast<double*>(ws));
+    mgx::conv::colsum_finalize_kernel<<<static_cast<unsigned>(mgx::ceil_div(C, 32)),
+                                         dim3(32, mgx::conv::kFinLanes), 0, st>>>(
+        static_cast<const double*>(ws), nchunk, static_cast<int>(C), 0, dsum, nullptr, nullptr, 0);
+    MGX_LAUNCHED();
+    return MGX_OK;
+  }
+  mgx::conv::bn_bwd_dx_kernel<<<grid_for(M * C / ((C & 3) ? 1 : 4)), 256, 0, st>>>(
       dy, x, stats, sums, gamma, dx, M, static_cast<int>(C), mask);
   MGX_LAUNCHED();
   return MGX_OK;

@@ -155,8 +155,17 @@ def test_batchnorm_kernels(cuda, m, c, fix_gamma):
     L.call("mgx_bn_bwd_reduce", dyd.data_ptr(), xd.data_ptr(), st.data_ptr(), m, c, ws.data_ptr(),
            sums.data_ptr(), None, None, 0, None, 0)
     L.call("mgx_bn_bwd_dx", dyd.data_ptr(), xd.data_ptr(), st.data_ptr(), sums.data_ptr(), gp,
-           dx.data_ptr(), m, c, None, 0)
+           dx.data_ptr(), m, c, None, None, None, 0)
     torch.cuda.synchronize()
+    if c % 4 == 0:  # fused dx + per-channel sum of dx
+        dx2 = torch.empty(m, c, device="cuda")
+        dsum = torch.empty(c, device="cuda")
+        L.call("mgx_bn_bwd_dx", dyd.data_ptr(), xd.data_ptr(), st.data_ptr(), sums.data_ptr(), gp,
+               dx2.data_ptr(), m, c, None, dsum.data_ptr(), ws.data_ptr(), 0)
+        torch.cuda.synchronize()
+        assert torch.equal(dx2, dx)
+        np.testing.assert_allclose(dsum.cpu().numpy(), dx.double().sum(0).cpu().numpy(),
+                                   rtol=1e-4, atol=1e-5)
     xr = xd.double().cpu().requires_grad_(True)
     gr = gd.double().cpu().requires_grad_(True)
     br = bd.double().cpu().requires_grad_(True)

@@ -57,6 +57,7 @@ def main():
         rate = (f"{fl / ms / 1e9:8.1f} TF/s" if fam.startswith("tc_gemm")
                 else f"{byt / ms / 1e6:8.1f} GB/s")
         d = list(ex._prog_dims[i]) if hasattr(ex, "_prog_dims") else []
+        d = d + ["ptrs:" + "".join("1" if p else "0" for p in ex._prog_ptrs[i])]
         rows.append((ms, i, ex.instr_labels[i], fam, rate, d))
     total = t.sum()
     print(f"{name}: {ex.num_instructions} instructions, {total:.3f} ms profiled pass, "
