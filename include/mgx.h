@@ -295,6 +295,15 @@ int mgx_prog_time_levels(uint64_t prog, int32_t begin, int32_t end, uintptr_t st
                          double* ns_out);
 /* Per-instruction device time of one eager run of [begin,end) (profiling). */
 int mgx_prog_profile(uint64_t prog, int32_t begin, int32_t end, uintptr_t stream, float* ms_out);
+/* Multi-lane schedule (the dependency engine of engine.py:94-196 as CUDA
+ * streams and events): lane[i] in [0, nlanes) for every instruction, and a
+ * CSR (dep_ptr[n+1], dep_idx) of earlier instructions on other lanes that
+ * instruction i must wait for.  Lane 0 is the caller's stream; a run (or
+ * capture) of a range forks the side lanes off it and joins them back.
+ * nlanes == 1 restores plain in-order execution.  Set before the first
+ * captured run. */
+int mgx_prog_set_schedule(uint64_t prog, int32_t nlanes, const int32_t* lane,
+                          const int32_t* dep_ptr, const int32_t* dep_idx);
 /* Number of kernel launches the range makes (captured once, not run). */
 int mgx_prog_kernel_count(uint64_t prog, int32_t begin, int32_t end, uintptr_t stream,
                           int64_t* out);

@@ -193,6 +193,14 @@ struct Program {
   std::map<std::pair<int32_t, int32_t>, cudaGraphExec_t> fgraphs;  // mode 3
   std::map<std::pair<int32_t, int32_t>, FusedRange> fused;         // modes 2, 3
   std::mutex mu;
+  // multi-lane schedule (mgx_prog_set_schedule): lane of every instruction,
+  // cross-lane dependencies (CSR), one side stream per extra lane, one
+  // event per dependency source instruction
+  int32_t nlanes = 1;
+  std::vector<int32_t> lane, dep_ptr, dep_idx;
+  std::vector<cudaStream_t> side;
+  std::vector<cudaEvent_t> ev;      // per instruction (null if never waited on)
+  std::vector<cudaEvent_t> join;    // per lane: range start / end joins
 };
 
 static int get_fused(Program* p, int32_t begin, int32_t end, FusedRange** out) {
@@ -285,10 +293,42 @@ static int run_instr(const mgx_instr& in, cudaStream_t st) {
   }
 }
 
-static int run_range(Program* p, int32_t begin, int32_t end, cudaStream_t st) {
+static int run_range_serial(Program* p, int32_t begin, int32_t end, cudaStream_t st) {
   for (int32_t i = begin; i < end; ++i) {
     int rc = run_instr(p->instrs[i], st);
     if (rc != MGX_OK) return rc;
+  }
+  return MGX_OK;
+}
+
+// Multi-lane form of a range: lane 0 is the caller's stream, lane l > 0 a
+// side stream.  Every side lane first waits for the caller's stream (the
+// range starts after everything enqueued before it), cross-lane
+// dependencies are event record/wait pairs, and the caller's stream finally
+// waits for every side lane, so the range behaves as one stream-ordered
+// unit (and captures into one graph with parallel branches).
+static int run_range(Program* p, int32_t begin, int32_t end, cudaStream_t st) {
+  if (p->nlanes <= 1) return run_range_serial(p, begin, end, st);
+  std::vector<bool> used(p->nlanes, false);
+  for (int32_t i = begin; i < end; ++i) used[p->lane[i]] = true;
+  MGX_CUDA(cudaEventRecord(p->join[0], st));
+  for (int l = 1; l < p->nlanes; ++l)
+    if (used[l]) MGX_CUDA(cudaStreamWaitEvent(p->side[l], p->join[0], 0));
+  for (int32_t i = begin; i < end; ++i) {
+    const int l = p->lane[i];
+    cudaStream_t ls = l == 0 ? st : p->side[l];
+    for (int32_t q = p->dep_ptr[i]; q < p->dep_ptr[i + 1]; ++q) {
+      const int32_t src = p->dep_idx[q];
+      if (src >= begin && src < i) MGX_CUDA(cudaStreamWaitEvent(ls, p->ev[src], 0));
+    }
+    int rc = run_instr(p->instrs[i], ls);
+    if (rc != MGX_OK) return rc;
+    if (p->ev[i]) MGX_CUDA(cudaEventRecord(p->ev[i], ls));
+  }
+  for (int l = 1; l < p->nlanes; ++l) {
+    if (!used[l]) continue;
+    MGX_CUDA(cudaEventRecord(p->join[l], p->side[l]));
+    MGX_CUDA(cudaStreamWaitEvent(st, p->join[l], 0));
   }
   return MGX_OK;
 }
@@ -458,6 +498,48 @@ extern "C" int mgx_prog_profile(uint64_t prog, int32_t begin, int32_t end, uintp
   return MGX_OK;
 }
 
+extern "C" int mgx_prog_set_schedule(uint64_t prog, int32_t nlanes, const int32_t* lane,
+                                     const int32_t* dep_ptr, const int32_t* dep_idx) {
+  mgx::Program* p = mgx::find_prog(prog);
+  if (!p) {
+    mgx::set_error("mgx_prog_set_schedule: unknown program handle");
+    return MGX_BAD_HANDLE;
+  }
+  const int32_t n = static_cast<int32_t>(p->instrs.size());
+  MGX_REQUIRE(nlanes >= 1 && nlanes <= 16 && (nlanes == 1 || (lane && dep_ptr)),
+              "mgx_prog_set_schedule: bad arguments");
+  std::lock_guard<std::mutex> lock(p->mu);
+  MGX_REQUIRE(p->graphs.empty() && p->fgraphs.empty(),
+              "mgx_prog_set_schedule: program already captured");
+  if (nlanes == 1) {
+    p->nlanes = 1;
+    return MGX_OK;
+  }
+  for (int32_t i = 0; i < n; ++i) {
+    MGX_REQUIRE(lane[i] >= 0 && lane[i] < nlanes, "mgx_prog_set_schedule: lane out of range");
+    MGX_REQUIRE(dep_ptr[i] <= dep_ptr[i + 1], "mgx_prog_set_schedule: bad dependency CSR");
+    for (int32_t q = dep_ptr[i]; q < dep_ptr[i + 1]; ++q)
+      MGX_REQUIRE(dep_idx[q] >= 0 && dep_idx[q] < i,
+                  "mgx_prog_set_schedule: a dependency must be an earlier instruction");
+  }
+  p->lane.assign(lane, lane + n);
+  p->dep_ptr.assign(dep_ptr, dep_ptr + n + 1);
+  p->dep_idx.assign(dep_idx, dep_idx + dep_ptr[n]);
+  p->ev.assign(n, nullptr);
+  for (int32_t q = 0; q < dep_ptr[n]; ++q) {
+    cudaEvent_t& e = p->ev[dep_idx[q]];
+    if (!e) MGX_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  p->side.assign(nlanes, nullptr);
+  p->join.assign(nlanes, nullptr);
+  for (int l = 0; l < nlanes; ++l) {
+    if (l > 0) MGX_CUDA(cudaStreamCreateWithFlags(&p->side[l], cudaStreamNonBlocking));
+    MGX_CUDA(cudaEventCreateWithFlags(&p->join[l], cudaEventDisableTiming));
+  }
+  p->nlanes = nlanes;
+  return MGX_OK;
+}
+
 extern "C" int mgx_prog_kernel_count(uint64_t prog, int32_t begin, int32_t end, uintptr_t stream,
                                      int64_t* out) {
   mgx::Program* p = mgx::find_prog(prog);
@@ -506,6 +588,12 @@ extern "C" int mgx_prog_destroy(uint64_t prog) {
   }
   for (auto& kv : p->graphs) cudaGraphExecDestroy(kv.second);
   for (auto& kv : p->fgraphs) cudaGraphExecDestroy(kv.second);
+  for (auto e : p->ev)
+    if (e) cudaEventDestroy(e);
+  for (auto e : p->join)
+    if (e) cudaEventDestroy(e);
+  for (auto st : p->side)
+    if (st) cudaStreamDestroy(st);
   for (auto& kv : p->fused) mgx::free_fused(kv.second);
   delete p;
   return MGX_OK;

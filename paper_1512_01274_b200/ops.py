@@ -198,7 +198,8 @@ class LowerCtx:
     FAKE_BASE = 1 << 44
 
     def __init__(self, training: bool, scratch_base: Optional[int] = None,
-                 persist_base: Optional[int] = None, device: int = 0):
+                 persist_base: Optional[int] = None, device: int = 0,
+                 unique_scratch: bool = False):
         self.training = training
         self.device = device
         self.measuring = scratch_base is None
@@ -207,17 +208,26 @@ class LowerCtx:
         self._op_off = 0
         self._p_off = 0
         self.scratch_peak = 0
-        self.memo: Dict[tuple, object] = {}
+        # unique_scratch: no scratch reuse between nodes (nodes may then run
+        # concurrently on different lanes of a multi-stream schedule)
+        self.unique_scratch = unique_scratch
+        self._sizes: Dict[int, int] = {}
+        self.reads: List[tuple] = []    # persistent buffers read by the current node
+        self.writes: List[tuple] = []   # ... and written by it
+        self.memo = _Memo(self)
         self.node = None
 
     def begin_op(self, node) -> None:
         self.node = node
         self._op_off = 0
+        self.reads, self.writes = [], []
 
     def _al(self, n: int) -> int:
         return -(-max(int(n), 1) // self.ALIGN) * self.ALIGN
 
     def scratch(self, nbytes: int) -> int:
+        if self.unique_scratch:
+            return self.persistent(nbytes)
         ptr = self._sbase + self._op_off
         self._op_off += self._al(nbytes)
         self.scratch_peak = max(self.scratch_peak, self._op_off)
@@ -226,6 +236,7 @@ class LowerCtx:
     def persistent(self, nbytes: int) -> int:
         ptr = self._pbase + self._p_off
         self._p_off += self._al(nbytes)
+        self._sizes[ptr] = self._al(nbytes)
         return ptr
 
     @property
@@ -246,6 +257,32 @@ class LowerCtx:
         if role.startswith("in"):
             return n.inputs[int(role[2:])][0]
         return None
+
+
+class _Memo(dict):
+    """The lowering memo; records which persistent buffers the current
+    node creates (writes) and reuses (reads), for the hazard analysis of the
+    multi-lane schedule."""
+
+    def __init__(self, ctx: "LowerCtx"):
+        super().__init__()
+        self._ctx = ctx
+
+    def _note(self, value, into: list) -> None:
+        if isinstance(value, int) and not isinstance(value, bool) and value in self._ctx._sizes:
+            into.append((value, value + self._ctx._sizes[value]))
+
+    def get(self, key, default=None):
+        if key is None:
+            return default
+        value = super().get(key, default)
+        if key in self:
+            self._note(value, self._ctx.reads)
+        return value
+
+    def __setitem__(self, key, value):
+        super().__setitem__(key, value)
+        self._note(value, self._ctx.writes)
 
 
 class _EagerCtx(LowerCtx):

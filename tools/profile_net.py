@@ -61,7 +61,7 @@ def main():
         rows.append((ms, i, ex.instr_labels[i], fam, rate, d))
     total = t.sum()
     print(f"{name}: {ex.num_instructions} instructions, {total:.3f} ms profiled pass, "
-          f"kernels {ex.kernel_count()}")
+          f"kernels {ex.kernel_count()}, lanes {ex.lanes_used}")
     fams = {}
     for ms, i, lbl, fam, rate, d in rows:
         fams[fam] = fams.get(fam, 0) + ms
