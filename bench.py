@@ -419,22 +419,35 @@ def kv_launches(kv) -> int:
 
 
 def kv_round_ms(step, kv, eng, steps):
+    """Device time of the step's KVStore part (every key pushed -> fused
+    reduce + SGD + broadcast), captured as a CUDA graph like the step itself
+    and replayed; max over ranks is taken by the caller's barrier shape."""
     import torch
     w = step.workers[0]
-    ka, kb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ms = []
-    for _ in range(max(1, min(steps, 10))):
-        # pushes launch the fused round as soon as a bucket is complete:
-        # bracket the pushes and the final flush
-        ka.record(eng.stream)
+
+    def one_round():
         for i in range(len(step.names)):
             kv.push(i, step.grads[w][step.names[i]], w)
         with kv._lock:
             kv._flush_locked()
-        kb.record(eng.stream)
-        torch.cuda.synchronize()
-        ms.append(ka.elapsed_time(kb))
-    return sum(ms) / len(ms)
+
+    one_round()
+    eng.wait_all()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=eng.stream, capture_error_mode="thread_local"):
+        one_round()
+    reps = max(3, min(steps, 10))
+    with torch.cuda.stream(eng.stream):
+        g.replay()
+    torch.cuda.synchronize()
+    ka, kb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ka.record(eng.stream)
+    with torch.cuda.stream(eng.stream):
+        for _ in range(reps):
+            g.replay()
+    kb.record(eng.stream)
+    torch.cuda.synchronize()
+    return ka.elapsed_time(kb) / reps
 
 
 def roofline_of(res):

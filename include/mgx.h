@@ -169,19 +169,21 @@ int mgx_bn_apply(const float* x, const float* stats, const float* gamma, const f
                  float* y, int64_t M, int64_t C, int act, uintptr_t stream);
 /* sums = [sum dy | sum dy*xhat] per channel; also written to dbeta and
  * dgamma when non-NULL (dgamma zero-filled when dgamma_zero: fix_gamma).
- * mask (optional): a ReLU output; dy is then og * (mask > 0), the ReLU
- * backward fused in. */
+ * relu_beta (optional): a ReLU follows the BatchNorm; dy is then masked by
+ * ((x - mean) * rstd * relu_gamma + relu_beta > 0) -- the forward's ReLU
+ * decision recomputed from x (relu_gamma NULL = 1) -- so the ReLU backward
+ * is fused in and its output never stored. */
 int mgx_bn_bwd_reduce(const float* dy, const float* x, const float* stats, int64_t M, int64_t C,
                       void* ws, float* sums, float* dbeta, float* dgamma, int dgamma_zero,
-                      const float* mask, uintptr_t stream);
+                      const float* relu_gamma, const float* relu_beta, uintptr_t stream);
 /* dx = gamma * rstd * (dy - (sum dy + xhat * sum dy*xhat) / M), with the
- * same optional ReLU mask; dy and mask may alias dx.  dsum (optional, needs
- * ws of mgx_reduce_workspace_bytes and C % 4 == 0): the per-channel sum of
- * dx over the rows, reduced in the same pass (the bias gradient of the
+ * same optional ReLU mask; dy may alias dx.  ws: mgx_reduce_workspace_bytes
+ * (needed when C % 4 == 0).  dsum (optional): the per-channel sum of dx
+ * over the rows, reduced in the same pass (the bias gradient of the
  * convolution feeding the BatchNorm). */
 int mgx_bn_bwd_dx(const float* dy, const float* x, const float* stats, const float* sums,
-                  const float* gamma, float* dx, int64_t M, int64_t C, const float* mask,
-                  float* dsum, void* ws, uintptr_t stream);
+                  const float* gamma, float* dx, int64_t M, int64_t C, const float* relu_gamma,
+                  const float* relu_beta, float* dsum, void* ws, uintptr_t stream);
 /* out[c] = sum over rows of x[r, c] (conv bias gradient). */
 int mgx_colsum(const float* x, int64_t M, int64_t C, void* ws, float* out, uintptr_t stream);
 /* Pooling, NHWC.  type 0 max (padding ignored), 1 avg (count_include_pad);
@@ -262,9 +264,11 @@ typedef struct mgx_instr {
 #define MGX_OP_BN_APPLY 18    /* ptr0=x ptr1=stats ptr2=gamma ptr3=beta ptr4=y     */
                               /* dims=M,C act                                      */
 #define MGX_OP_BN_BWD_REDUCE 19 /* ptr0=dy ptr1=x ptr2=stats ptr3=ws ptr4=sums     */
-                              /* ptr5=mask dims=M,C,dbeta*,dgamma*,dgamma_zero    */
+                              /* ptr5=relu_beta                                    */
+                              /* dims=M,C,dbeta*,dgamma*,dgamma_zero,relu_gamma*   */
 #define MGX_OP_BN_BWD_DX 20   /* ptr0=dy ptr1=x ptr2=stats ptr3=sums ptr4=gamma    */
-                              /* ptr5=dx dims=M,C,mask*,dsum*,ws* (* = address)  */
+                              /* ptr5=dx dims=M,C,relu_beta*,dsum*,ws*,relu_gamma* */
+                              /* (* = a device address carried in a dim)           */
 #define MGX_OP_POOL_FWD 21    /* ptr0=x ptr1=y ptr2=argmax dims=geom,full act=type */
 #define MGX_OP_POOL_BWD 22    /* ptr0=x ptr1=y ptr2=dy ptr3=dx ptr4=argmax dims=geom,full */
 #define MGX_OP_CHAN_COPY 23   /* ptr0=src ptr1=dst dims=rows,cols,lds,soff,ldd,doff */

@@ -146,8 +146,8 @@ _SIGNATURES = {
     "mgx_bn_apply": ([c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, ctypes.c_int, c_uptr],
                      ctypes.c_int),
     "mgx_bn_bwd_reduce": ([c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, ctypes.c_int,
-                           c_vp, c_uptr], ctypes.c_int),
-    "mgx_bn_bwd_dx": ([c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp,
+                           c_vp, c_vp, c_uptr], ctypes.c_int),
+    "mgx_bn_bwd_dx": ([c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp,
                        c_uptr], ctypes.c_int),
     "mgx_colsum": ([c_vp, c_i64, c_i64, c_vp, c_vp, c_uptr], ctypes.c_int),
     "mgx_pool_forward": ([c_vp, c_vp, c_vp, ctypes.c_int, ctypes.c_int, c_vp, c_uptr],

@@ -296,11 +296,14 @@ def _bn_lower_bwd(slot, env, out, attrs):
         sums = ctx.persistent(8 * c)
         ctx.memo[key] = sums
         ws = ctx.scratch(_reduce_ws(m, c))
-        code.append(instr(L.OP_BN_BWD_REDUCE, [og.ptr, x.ptr, st, ws, sums, None], [m, c, 0, 0, 0]))
+        code.append(instr(L.OP_BN_BWD_REDUCE, [og.ptr, x.ptr, st, ws, sums, None],
+                          [m, c, 0, 0, 0, 0]))
     fix = attrs.get("fix_gamma", True)
     if slot == 0:
         gamma = None if fix else env["in1"].ptr
-        code.append(instr(L.OP_BN_BWD_DX, [og.ptr, x.ptr, st, sums, gamma, out.ptr], [m, c, 0, 0, 0]))
+        ws = ctx.scratch(_reduce_ws(m, c))
+        code.append(instr(L.OP_BN_BWD_DX, [og.ptr, x.ptr, st, sums, gamma, out.ptr],
+                          [m, c, 0, 0, ws, 0]))
     elif slot == 1:
         code.append(instr(L.OP_FILL, [out.ptr], [c], [0.0]) if fix else
                     instr(L.OP_COPY, [sums + 4 * c, out.ptr], [c]))
@@ -309,13 +312,14 @@ def _bn_lower_bwd(slot, env, out, attrs):
     return code
 
 
-def bn_backward_group(og: View, relu_y: Optional[View], x: View, gamma: View, attrs,
+def bn_backward_group(og: View, relu: bool, x: View, gamma: View, beta: View, attrs,
                       xnode, dx: Optional[View], dgamma: Optional[View],
                       dbeta: Optional[View], dbias_conv: Optional[View] = None) -> list:
     """All requested BatchNorm gradients of one node in one pass pair (the
     executor's fusion of the sibling Backward nodes, optionally with the
     ReLU backward in front of them): one reduction that also writes dbeta /
-    dgamma, then dx.  relu_y: the ReLU output whose mask applies to og."""
+    dgamma, then dx.  relu: og is the ReLU's output gradient; its mask is
+    recomputed from x, gamma and beta (never read back)."""
     ctx = current_ctx()
     m, c = prod(x.shape[:-1]), x.shape[-1]
     code = []
@@ -323,15 +327,16 @@ def bn_backward_group(og: View, relu_y: Optional[View], x: View, gamma: View, at
     fix = attrs.get("fix_gamma", True)
     sums = ctx.persistent(8 * c)
     ws = ctx.scratch(_reduce_ws(m, c))
-    mask = relu_y.ptr if relu_y is not None else None
-    code.append(instr(L.OP_BN_BWD_REDUCE, [og.ptr, x.ptr, st, ws, sums, mask],
+    g = None if fix else gamma.ptr
+    rb = beta.ptr if relu else None
+    code.append(instr(L.OP_BN_BWD_REDUCE, [og.ptr, x.ptr, st, ws, sums, rb],
                       [m, c, dbeta.ptr if dbeta else 0, dgamma.ptr if dgamma else 0,
-                       1 if fix else 0]))
+                       1 if fix else 0, (g or 0) if relu else 0]))
     if dx is not None:
-        dws = ctx.scratch(_reduce_ws(m, c)) if dbias_conv is not None else 0
-        code.append(instr(L.OP_BN_BWD_DX, [og.ptr, x.ptr, st, sums, None if fix else gamma.ptr,
-                                           dx.ptr],
-                          [m, c, mask or 0, dbias_conv.ptr if dbias_conv is not None else 0, dws]))
+        dws = ctx.scratch(_reduce_ws(m, c))
+        code.append(instr(L.OP_BN_BWD_DX, [og.ptr, x.ptr, st, sums, g, dx.ptr],
+                          [m, c, rb or 0, dbias_conv.ptr if dbias_conv is not None else 0, dws,
+                           (g or 0) if relu else 0]))
     return code
 
 

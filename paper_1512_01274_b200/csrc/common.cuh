@@ -127,4 +127,38 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
+// Row-by-vector launch shape shared by the bandwidth kernels: 256-thread
+// blocks; a thread owns one vector column v of the rows (fixed per thread,
+// so its per-column constants load once) and walks rows, with
+// min(V, 256) threads per row and 256 / that rows per block pass -- no
+// 64-bit division per element, no idle lanes for narrow rows.
+constexpr int kRowsThreads = 256;
+
+struct RowsIdx {
+  int v, r, rstep;
+  bool active;
+  __device__ __forceinline__ RowsIdx(int V) {
+    const int tpr = V < kRowsThreads ? V : kRowsThreads;
+    const int rpb = kRowsThreads / tpr;
+    const int t = threadIdx.x;
+    const int rin = t / tpr;
+    v = blockIdx.x * tpr + (t - rin * tpr);
+    r = blockIdx.y * rpb + rin;
+    rstep = gridDim.y * rpb;
+    active = rin < rpb && v < V;
+  }
+};
+
+inline dim3 rows_grid(int64_t rows, int64_t vecs) {
+  const int64_t tpr = vecs < kRowsThreads ? vecs : kRowsThreads;
+  const int64_t rpb = kRowsThreads / (tpr < 1 ? 1 : tpr);
+  const int64_t gx = ceil_div(vecs, tpr < 1 ? 1 : tpr);
+  int64_t gy = ceil_div(rows, rpb);
+  const int64_t cap = ceil_div(int64_t(kNumSMs) * 16, gx);
+  if (gy > cap) gy = cap;
+  if (gy > 65535) gy = 65535;
+  return dim3(static_cast<unsigned>(gx), static_cast<unsigned>(gy < 1 ? 1 : gy));
+}
+
+
 }  // namespace mgx

@@ -58,63 +58,62 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
 }
 
 // col[m, k] (bf16, row stride ldk >= K, zero beyond K) = x at tap k of output
-// pixel m (zero in the padding).  8 consecutive k per thread (one 16-byte
-// store); when C % 8 == 0 they are 8 channels of one tap (two float4 loads).
-__global__ void im2col_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ col, Geom g,
-                              int64_t ldk) {
+// pixel m (zero in the padding).  A thread owns the 8 consecutive k of one
+// 16-byte store; when C % 8 == 0 they are 8 channels of one tap (two float4
+// loads).
+__global__ void __launch_bounds__(256)
+im2col_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ col, Geom g, int64_t ldk) {
   const int K = g.kh * g.kw * g.C;
-  const int64_t per_row = ldk / 8;
-  const int64_t M = int64_t(g.B) * g.Ho * g.Wo;
-  const int64_t total = M * per_row;
-  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  const int per_row = static_cast<int>(ldk / 8);
+  const RowsIdx ri(per_row);
+  if (!ri.active) return;
+  const int k0 = ri.v * 8;
+  const int M = g.B * g.Ho * g.Wo;
+  const int hw = g.Ho * g.Wo;
   const bool vec = (g.C % 8) == 0;
-  for (int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < total; idx += stride) {
-    const int64_t m = idx / per_row;
-    const int k0 = static_cast<int>(idx - m * per_row) * 8;
-    const int b = static_cast<int>(m / (g.Ho * g.Wo));
-    const int rem = static_cast<int>(m - int64_t(b) * g.Ho * g.Wo);
-    const int oh = rem / g.Wo, ow = rem - (rem / g.Wo) * g.Wo;
-    float v[8];
-    if (vec) {
-      if (k0 < K) {
-        const int tap = k0 / g.C, c0 = k0 - tap * g.C;
-        const int i = tap / g.kw, j = tap - (tap / g.kw) * g.kw;
-        const int h = oh * g.sh - g.ph + i, w = ow * g.sw - g.pw + j;
-        if (h >= 0 && h < g.H && w >= 0 && w < g.W) {
-          const float4* src =
-              reinterpret_cast<const float4*>(x + ((int64_t(b) * g.H + h) * g.W + w) * g.C + c0);
-          const float4 a = __ldg(src), c = __ldg(src + 1);
-          v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
-          v[4] = c.x; v[5] = c.y; v[6] = c.z; v[7] = c.w;
-        } else {
+  // per-thread tap decode of its 8 columns
+  int ti[8], tj[8], tc[8];
 #pragma unroll
-          for (int t = 0; t < 8; ++t) v[t] = 0.0f;
-        }
+  for (int t = 0; t < 8; ++t) {
+    const int k = k0 + t;
+    const int tap = k / g.C;
+    tc[t] = k < K ? k - tap * g.C : -1;
+    ti[t] = tap / g.kw;
+    tj[t] = tap - ti[t] * g.kw;
+  }
+  for (int m = ri.r; m < M; m += ri.rstep) {
+    const int b = m / hw;
+    const int rem = m - b * hw;
+    const int oh = rem / g.Wo, ow = rem - (rem / g.Wo) * g.Wo;
+    const int hb = oh * g.sh - g.ph, wb = ow * g.sw - g.pw;
+    float v8[8];
+    if (vec) {
+      const int h = hb + ti[0], w = wb + tj[0];
+      if (tc[0] >= 0 && h >= 0 && h < g.H && w >= 0 && w < g.W) {
+        const float4* src =
+            reinterpret_cast<const float4*>(x + ((int64_t(b) * g.H + h) * g.W + w) * g.C + tc[0]);
+        const float4 a = __ldg(src), c = __ldg(src + 1);
+        v8[0] = a.x; v8[1] = a.y; v8[2] = a.z; v8[3] = a.w;
+        v8[4] = c.x; v8[5] = c.y; v8[6] = c.z; v8[7] = c.w;
       } else {
 #pragma unroll
-        for (int t = 0; t < 8; ++t) v[t] = 0.0f;
+        for (int t = 0; t < 8; ++t) v8[t] = 0.0f;
       }
     } else {
 #pragma unroll
       for (int t = 0; t < 8; ++t) {
-        const int k = k0 + t;
-        float val = 0.0f;
-        if (k < K) {
-          const int tap = k / g.C, c = k - tap * g.C;
-          const int i = tap / g.kw, j = tap - (tap / g.kw) * g.kw;
-          const int h = oh * g.sh - g.ph + i, w = ow * g.sw - g.pw + j;
-          if (h >= 0 && h < g.H && w >= 0 && w < g.W)
-            val = __ldg(x + ((int64_t(b) * g.H + h) * g.W + w) * g.C + c);
-        }
-        v[t] = val;
+        const int h = hb + ti[t], w = wb + tj[t];
+        v8[t] = (tc[t] >= 0 && h >= 0 && h < g.H && w >= 0 && w < g.W)
+                    ? __ldg(x + ((int64_t(b) * g.H + h) * g.W + w) * g.C + tc[t])
+                    : 0.0f;
       }
     }
     uint4 o;
-    o.x = pack_bf16(v[0], v[1]);
-    o.y = pack_bf16(v[2], v[3]);
-    o.z = pack_bf16(v[4], v[5]);
-    o.w = pack_bf16(v[6], v[7]);
-    *reinterpret_cast<uint4*>(col + m * ldk + k0) = o;
+    o.x = pack_bf16(v8[0], v8[1]);
+    o.y = pack_bf16(v8[2], v8[3]);
+    o.z = pack_bf16(v8[4], v8[5]);
+    o.w = pack_bf16(v8[6], v8[7]);
+    *reinterpret_cast<uint4*>(col + int64_t(m) * ldk + k0) = o;
   }
 }
 
@@ -182,13 +181,22 @@ __global__ void weight_flip_kernel(const float* __restrict__ w, int F, int kh, i
 // xhat = (x - mean) * rstd with stats = [mean C | rstd C].
 
 constexpr int kRedThreads = 256;
-constexpr int kMaxChunks = 2 * kNumSMs;
+constexpr int kMaxChunks = 8 * kNumSMs;
+
+// A ReLU fused in front of a BatchNorm backward: its mask is recomputed
+// from the BatchNorm input with the forward's exact arithmetic,
+// t = (x - mean) * rstd * gamma + beta > 0, instead of reading the ReLU
+// output back.  beta == nullptr: no ReLU; gamma == nullptr: fix_gamma (1).
+struct ReluMask {
+  const float* gamma;
+  const float* beta;
+};
 
 template <int MODE>
 __global__ void __launch_bounds__(kRedThreads)
 colreduce_partial_kernel(const float* __restrict__ a, const float* __restrict__ xs,
                          const float* __restrict__ stats, int64_t M, int C, int64_t rpc,
-                         double* __restrict__ ws, const float* __restrict__ mask) {
+                         double* __restrict__ ws, ReluMask rm) {
   extern __shared__ double red[];  // [rpp][2*C]
   const int tpr = C < kRedThreads ? C : kRedThreads;  // threads per row
   const int rpp = kRedThreads / tpr;                  // rows per pass
@@ -201,18 +209,29 @@ colreduce_partial_kernel(const float* __restrict__ a, const float* __restrict__ 
     const int c = cb + c_in;
     double s0 = 0.0, s1 = 0.0;
     if (r_in < rpp && c < C) {
-      float mean = 0.0f, rstd = 0.0f, shift = 0.0f;
+      float mean = 0.0f, rstd = 0.0f, shift = 0.0f, gm = 1.0f, bt = 0.0f;
       if (MODE == 1) {
         mean = __ldg(stats + c);
         rstd = __ldg(stats + C + c);
+        if (rm.beta) {
+          bt = __ldg(rm.beta + c);
+          gm = rm.gamma ? __ldg(rm.gamma + c) : 1.0f;
+        }
       }
       if (MODE == 0) shift = __ldg(a + c);  // row 0: shifted sums avoid cancellation
       for (int64_t r = r0 + r_in; r < r1; r += rpp) {
         float v = __ldg(a + r * C + c) - shift;
-        if (MODE == 1 && mask && !(__ldg(mask + r * C + c) > 0.0f)) v = 0.0f;
-        s0 += v;
-        if (MODE == 0) s1 += double(v) * double(v);
-        if (MODE == 1) s1 += double(v) * double((__ldg(xs + r * C + c) - mean) * rstd);
+        if (MODE == 0) {
+          s0 += v;
+          s1 += double(v) * double(v);
+        } else if (MODE == 1) {
+          const float xv = __ldg(xs + r * C + c);
+          if (rm.beta && !((xv - mean) * rstd * gm + bt > 0.0f)) v = 0.0f;
+          s0 += v;
+          s1 += double(v) * double((xv - mean) * rstd);
+        } else {
+          s0 += v;
+        }
       }
     }
     if (r_in < rpp) {
@@ -234,16 +253,39 @@ colreduce_partial_kernel(const float* __restrict__ a, const float* __restrict__ 
 }
 
 // Vectorised form (C % 4 == 0): a thread owns 4 channels (one float4 per
-// row), keeps fp32 partial sums over its rows with 4 rows of loads in
-// flight, then the block merges its threads' partials in fp64 in a fixed
+// row), keeps fp32 partial sums over its rows with kRedUnroll rows of loads
+// in flight, then the block merges its threads' partials in fp64 in a fixed
 // order.  blockIdx.y tiles channels in groups of 1024.
-constexpr int kRedUnroll = 4;
+constexpr int kRedUnroll = 8;
+
+template <int MODE>
+__device__ __forceinline__ void red_accum(const float4& v, const float4& xv, const float* sh,
+                                          const float* mu, const float* rs, const float* gm,
+                                          const float* bt, bool relu, float* s0, float* s1) {
+  const float* pv = &v.x;
+  const float* px = &xv.x;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    if (MODE == 0) {
+      const float d = pv[q] - sh[q];
+      s0[q] += d;
+      s1[q] += d * d;
+    } else if (MODE == 1) {
+      float d = pv[q];
+      if (relu && !((px[q] - mu[q]) * rs[q] * gm[q] + bt[q] > 0.0f)) d = 0.0f;
+      s0[q] += d;
+      s1[q] += d * ((px[q] - mu[q]) * rs[q]);
+    } else {
+      s0[q] += pv[q];
+    }
+  }
+}
 
 template <int MODE>
 __global__ void __launch_bounds__(kRedThreads)
 colreduce_partial_vec_kernel(const float* __restrict__ a, const float* __restrict__ xs,
                              const float* __restrict__ stats, int64_t M, int C, int64_t rpc,
-                             double* __restrict__ ws, const float* __restrict__ mask) {
+                             double* __restrict__ ws, ReluMask rm) {
   extern __shared__ double red[];  // [rpp][2][ct]
   const int C4 = C >> 2;
   const int ct4 = C4 < kRedThreads ? C4 : kRedThreads;  // float4 groups per block row
@@ -257,18 +299,26 @@ colreduce_partial_vec_kernel(const float* __restrict__ a, const float* __restric
   const int64_t r1 = min(M, r0 + rpc);
   const float4* a4 = reinterpret_cast<const float4*>(a);
   const float4* x4 = reinterpret_cast<const float4*>(xs);
+  const bool relu = MODE == 1 && rm.beta != nullptr;
   float s0[4] = {0.f, 0.f, 0.f, 0.f}, s1[4] = {0.f, 0.f, 0.f, 0.f};
   if (active) {
     float sh[4] = {0.f, 0.f, 0.f, 0.f}, mu[4] = {0.f, 0.f, 0.f, 0.f}, rs[4] = {0.f, 0.f, 0.f, 0.f};
+    float gm[4] = {1.f, 1.f, 1.f, 1.f}, bt[4] = {0.f, 0.f, 0.f, 0.f};
     if (MODE == 0) {
       const float4 v = __ldg(a4 + c4);
       sh[0] = v.x; sh[1] = v.y; sh[2] = v.z; sh[3] = v.w;
     }
     if (MODE == 1) {
-      const float4 m = __ldg(reinterpret_cast<const float4*>(stats) + c4);
-      const float4 q = __ldg(reinterpret_cast<const float4*>(stats + C) + c4);
-      mu[0] = m.x; mu[1] = m.y; mu[2] = m.z; mu[3] = m.w;
-      rs[0] = q.x; rs[1] = q.y; rs[2] = q.z; rs[3] = q.w;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int c = c4 * 4 + q;
+        mu[q] = __ldg(stats + c);
+        rs[q] = __ldg(stats + C + c);
+        if (relu) {
+          bt[q] = __ldg(rm.beta + c);
+          gm[q] = rm.gamma ? __ldg(rm.gamma + c) : 1.0f;
+        }
+      }
     }
     int64_t r = r0 + r_in;
     for (; r + (kRedUnroll - 1) * rpp < r1; r += kRedUnroll * rpp) {
@@ -278,62 +328,14 @@ colreduce_partial_vec_kernel(const float* __restrict__ a, const float* __restric
         v[u] = __ldg(a4 + (r + u * rpp) * C4 + c4);
         if (MODE == 1) xv[u] = __ldg(x4 + (r + u * rpp) * C4 + c4);
       }
-      if (MODE == 1 && mask) {
-        // dy = og * (relu output > 0): the fused ReLU backward
 #pragma unroll
-        for (int u = 0; u < kRedUnroll; ++u) {
-          const float4 y = __ldg(reinterpret_cast<const float4*>(mask) + (r + u * rpp) * C4 + c4);
-          v[u].x = y.x > 0.0f ? v[u].x : 0.0f;
-          v[u].y = y.y > 0.0f ? v[u].y : 0.0f;
-          v[u].z = y.z > 0.0f ? v[u].z : 0.0f;
-          v[u].w = y.w > 0.0f ? v[u].w : 0.0f;
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < kRedUnroll; ++u) {
-        const float* pv = &v[u].x;
-        const float* px = &xv[u].x;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          if (MODE == 0) {
-            const float d = pv[q] - sh[q];
-            s0[q] += d;
-            s1[q] += d * d;
-          } else if (MODE == 1) {
-            s0[q] += pv[q];
-            s1[q] += pv[q] * ((px[q] - mu[q]) * rs[q]);
-          } else {
-            s0[q] += pv[q];
-          }
-        }
-      }
+      for (int u = 0; u < kRedUnroll; ++u)
+        red_accum<MODE>(v[u], MODE == 1 ? xv[u] : v[u], sh, mu, rs, gm, bt, relu, s0, s1);
     }
     for (; r < r1; r += rpp) {
-      float4 v = __ldg(a4 + r * C4 + c4);
-      float4 xv = v;
-      if (MODE == 1) xv = __ldg(x4 + r * C4 + c4);
-      if (MODE == 1 && mask) {
-        const float4 y = __ldg(reinterpret_cast<const float4*>(mask) + r * C4 + c4);
-        v.x = y.x > 0.0f ? v.x : 0.0f;
-        v.y = y.y > 0.0f ? v.y : 0.0f;
-        v.z = y.z > 0.0f ? v.z : 0.0f;
-        v.w = y.w > 0.0f ? v.w : 0.0f;
-      }
-      const float* pv = &v.x;
-      const float* px = &xv.x;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        if (MODE == 0) {
-          const float d = pv[q] - sh[q];
-          s0[q] += d;
-          s1[q] += d * d;
-        } else if (MODE == 1) {
-          s0[q] += pv[q];
-          s1[q] += pv[q] * ((px[q] - mu[q]) * rs[q]);
-        } else {
-          s0[q] += pv[q];
-        }
-      }
+      const float4 v = __ldg(a4 + r * C4 + c4);
+      const float4 xv = MODE == 1 ? __ldg(x4 + r * C4 + c4) : v;
+      red_accum<MODE>(v, xv, sh, mu, rs, gm, bt, relu, s0, s1);
     }
   }
   if (r_in < rpp) {
@@ -358,58 +360,58 @@ colreduce_partial_vec_kernel(const float* __restrict__ a, const float* __restric
   }
 }
 
-// Chunk merge shared by the finalize kernels: a block of 32 channels x 8
-// lanes; lane y sums chunks y, y+8, ... (4 independent loads in flight),
-// then the 8 lane sums are added in ascending y (fixed order).
-constexpr int kFinLanes = 8;
+// Chunk merge shared by the finalize kernels: a warp per channel (8
+// channels per 256-thread block); lane l sums chunks l, l+32, ... in
+// ascending order, then the 32 lane sums meet in a fixed xor-butterfly tree
+// (the same tree every run: deterministic).
+constexpr int kFinChannels = 8;
 
 __device__ __forceinline__ void merge_chunks(const double* __restrict__ ws, int nchunk, int C,
                                              int c, bool two, double* s_out, double* q_out) {
-  __shared__ double red[2][kFinLanes][32];
-  const int ty = threadIdx.y, tx = threadIdx.x;
+  const int lane = threadIdx.x & 31;
   double s = 0.0, q = 0.0;
   if (c < C) {
-    int z = ty;
-    for (; z + 3 * kFinLanes < nchunk; z += 4 * kFinLanes) {
-      double a[4], b[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        a[u] = ws[int64_t(z + u * kFinLanes) * C + c];
-        b[u] = two ? ws[int64_t(nchunk + z + u * kFinLanes) * C + c] : 0.0;
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        s += a[u];
-        q += b[u];
-      }
-    }
-    for (; z < nchunk; z += kFinLanes) {
+    for (int z = lane; z < nchunk; z += 32) {
       s += ws[int64_t(z) * C + c];
       if (two) q += ws[int64_t(nchunk + z) * C + c];
     }
   }
-  red[0][ty][tx] = s;
-  red[1][ty][tx] = q;
-  __syncthreads();
-  if (ty == 0) {
-    double u = 0.0, v = 0.0;
-    for (int y = 0; y < kFinLanes; ++y) {
-      u += red[0][y][tx];
-      v += red[1][y][tx];
-    }
-    *s_out = u;
-    *q_out = v;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, off);
+    q += __shfl_xor_sync(0xffffffffu, q, off);
   }
+  *s_out = s;
+  *q_out = q;
 }
 
 // BatchNorm dx pass that also reduces its own output per channel (the
 // gradient of the bias of the convolution feeding the BatchNorm): the row
 // tiling of colreduce_partial_vec_kernel, dx written elementwise, fp32
 // partial sums of dx merged per block in fp64 into ws[chunk][C].
+// (dy may alias dx: each element is read before it is written.)
+__device__ __forceinline__ float4 bn_dx4(const float4& d, const float4& xv, const float* mu,
+                                         const float* rs, const float* g, const float* s1,
+                                         const float* s2, const float* gm, const float* bt,
+                                         bool relu, float invm) {
+  const float* pd = &d.x;
+  const float* px = &xv.x;
+  float4 o;
+  float* po = &o.x;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    float dq = pd[q];
+    if (relu && !((px[q] - mu[q]) * rs[q] * gm[q] + bt[q] > 0.0f)) dq = 0.0f;
+    const float xhat = (px[q] - mu[q]) * rs[q];
+    po[q] = g[q] * rs[q] * (dq - (s1[q] + xhat * s2[q]) * invm);
+  }
+  return o;
+}
+
 __global__ void __launch_bounds__(kRedThreads)
 bn_dx_colsum_kernel(const float* dy, const float* __restrict__ x, const float* __restrict__ stats,
                     const float* __restrict__ sums, const float* __restrict__ gamma, float* dx,
-                    const float* mask, int64_t M, int C, int64_t rpc, double* __restrict__ ws) {
+                    ReluMask rm, int64_t M, int C, int64_t rpc, double* __restrict__ ws) {
   extern __shared__ double red[];  // [rpp][ct]
   const int C4 = C >> 2;
   const int ct4 = C4 < kRedThreads ? C4 : kRedThreads;
@@ -422,9 +424,10 @@ bn_dx_colsum_kernel(const float* dy, const float* __restrict__ x, const float* _
   const int64_t r0 = int64_t(blockIdx.x) * rpc;
   const int64_t r1 = min(M, r0 + rpc);
   const float invm = static_cast<float>(1.0 / double(M));
+  const bool relu = rm.beta != nullptr;
   float acc[4] = {0.f, 0.f, 0.f, 0.f};
   if (active) {
-    float mu[4], rs[4], g[4], s1[4], s2[4];
+    float mu[4], rs[4], g[4], s1[4], s2[4], gm[4], bt[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int c = c4 * 4 + q;
@@ -433,27 +436,38 @@ bn_dx_colsum_kernel(const float* dy, const float* __restrict__ x, const float* _
       g[q] = gamma ? __ldg(gamma + c) : 1.0f;
       s1[q] = __ldg(sums + c);
       s2[q] = __ldg(sums + C + c);
+      gm[q] = relu && rm.gamma ? __ldg(rm.gamma + c) : 1.0f;
+      bt[q] = relu ? __ldg(rm.beta + c) : 0.0f;
     }
-    for (int64_t r = r0 + r_in; r < r1; r += rpp) {
+    constexpr int U = 4;
+    int64_t r = r0 + r_in;
+    for (; r + (U - 1) * rpp < r1; r += U * rpp) {
+      float4 d[U], xv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t i = (r + u * rpp) * C4 + c4;
+        d[u] = reinterpret_cast<const float4*>(dy)[i];
+        xv[u] = __ldg(reinterpret_cast<const float4*>(x) + i);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const float4 o = bn_dx4(d[u], xv[u], mu, rs, g, s1, s2, gm, bt, relu, invm);
+        acc[0] += o.x;
+        acc[1] += o.y;
+        acc[2] += o.z;
+        acc[3] += o.w;
+        reinterpret_cast<float4*>(dx)[(r + u * rpp) * C4 + c4] = o;
+      }
+    }
+    for (; r < r1; r += rpp) {
       const int64_t i = r * C4 + c4;
-      float4 d = reinterpret_cast<const float4*>(dy)[i];
-      const float4 xv = __ldg(reinterpret_cast<const float4*>(x) + i);
-      float* pd = &d.x;
-      const float* px = &xv.x;
-      if (mask) {
-        const float4 y = reinterpret_cast<const float4*>(mask)[i];
-        const float* py = &y.x;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) pd[q] = py[q] > 0.0f ? pd[q] : 0.0f;
-      }
-      float4 o;
-      float* po = &o.x;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const float xhat = (px[q] - mu[q]) * rs[q];
-        po[q] = g[q] * rs[q] * (pd[q] - (s1[q] + xhat * s2[q]) * invm);
-        acc[q] += po[q];
-      }
+      const float4 o = bn_dx4(reinterpret_cast<const float4*>(dy)[i],
+                              __ldg(reinterpret_cast<const float4*>(x) + i), mu, rs, g, s1, s2,
+                              gm, bt, relu, invm);
+      acc[0] += o.x;
+      acc[1] += o.y;
+      acc[2] += o.z;
+      acc[3] += o.w;
       reinterpret_cast<float4*>(dx)[i] = o;
     }
   }
@@ -479,9 +493,9 @@ __global__ void bn_stats_finalize_kernel(const double* __restrict__ ws, int nchu
                                          int use_global,
                                          float* __restrict__ stats, float* __restrict__ mmean,
                                          float* __restrict__ mvar) {
-  const int c = blockIdx.x * 32 + threadIdx.x;
+  const int c = blockIdx.x * kFinChannels + (threadIdx.x >> 5);
   if (use_global) {
-    if (threadIdx.y == 0 && c < C) {
+    if ((threadIdx.x & 31) == 0 && c < C) {
       stats[c] = mmean[c];
       stats[C + c] = static_cast<float>(1.0 / sqrt(double(mvar[c]) + double(eps)));
     }
@@ -489,7 +503,7 @@ __global__ void bn_stats_finalize_kernel(const double* __restrict__ ws, int nchu
   }
   double s = 0.0, q = 0.0;
   merge_chunks(ws, nchunk, C, c, true, &s, &q);
-  if (threadIdx.y != 0 || c >= C) return;
+  if ((threadIdx.x & 31) != 0 || c >= C) return;
   // sums were taken relative to shift = x[0, c]
   const double dm = s / double(M);
   const double mean = double(x[c]) + dm;
@@ -507,10 +521,10 @@ __global__ void bn_stats_finalize_kernel(const double* __restrict__ ws, int nchu
 __global__ void colsum_finalize_kernel(const double* __restrict__ ws, int nchunk, int C, int two,
                                        float* __restrict__ out, float* __restrict__ out0,
                                        float* __restrict__ out1, int zero1) {
-  const int c = blockIdx.x * 32 + threadIdx.x;
+  const int c = blockIdx.x * kFinChannels + (threadIdx.x >> 5);
   double s = 0.0, q = 0.0;
   merge_chunks(ws, nchunk, C, c, two != 0, &s, &q);
-  if (threadIdx.y != 0 || c >= C) return;
+  if ((threadIdx.x & 31) != 0 || c >= C) return;
   out[c] = static_cast<float>(s);
   if (two) out[C + c] = static_cast<float>(q);
   if (out0) out0[c] = static_cast<float>(s);
@@ -524,17 +538,29 @@ __global__ void bn_apply_kernel(const float* __restrict__ x, const float* __rest
   const int64_t total = M * C;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   if ((C & 3) == 0) {
-    const int64_t t4 = total / 4;
-    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < t4; i += stride) {
-      const int c = static_cast<int>((i * 4) % C);
+    // launched with the rows x vectors shape: per-channel constants once
+    const int C4 = C >> 2;
+    const RowsIdx ri(C4);
+    if (!ri.active) return;
+    const int c4 = ri.v;
+    float mu[4], sc[4], bt[4], gm[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int cc = c4 * 4 + u;
+      const float g = gamma ? __ldg(gamma + cc) : 1.0f;
+      mu[u] = __ldg(stats + cc);
+      sc[u] = __ldg(stats + C + cc);
+      gm[u] = g;
+      bt[u] = __ldg(beta + cc);
+    }
+    for (int64_t r = ri.r; r < M; r += ri.rstep) {
+      const int64_t i = r * C4 + c4;
       float4 v = reinterpret_cast<const float4*>(x)[i];
       float* pv = &v.x;
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const int cc = c + u;
-        const float g = gamma ? __ldg(gamma + cc) : 1.0f;
-        float r = (pv[u] - __ldg(stats + cc)) * __ldg(stats + C + cc) * g + __ldg(beta + cc);
-        pv[u] = act_forward(act, r);
+        const float t = (pv[u] - mu[u]) * sc[u] * gm[u] + bt[u];
+        pv[u] = act == MGX_ACT_RELU ? relu(t) : act_forward(act, t);
       }
       reinterpret_cast<float4*>(y)[i] = v;
     }
@@ -547,51 +573,28 @@ __global__ void bn_apply_kernel(const float* __restrict__ x, const float* __rest
   }
 }
 
-// dx = gamma * rstd * (dy - (sum_dy + xhat * sum_dyxhat) / M)
-// (mask: relu output; dy is taken as og * (mask > 0), the fused ReLU
-// backward.  dy/mask may alias dx: each element is read before written.)
+// dx = gamma * rstd * (dy - (sum_dy + xhat * sum_dyxhat) / M), with an
+// optional fused ReLU (mask recomputed from x).  dy may alias dx.
 __global__ void bn_bwd_dx_kernel(const float* dy, const float* __restrict__ x,
                                  const float* __restrict__ stats, const float* __restrict__ sums,
                                  const float* __restrict__ gamma, float* dx, int64_t M, int C,
-                                 const float* mask) {
+                                 ReluMask rm) {
   const int64_t total = M * C;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   const float invm = static_cast<float>(1.0 / double(M));
-  if ((C & 3) == 0) {
-    const int64_t t4 = total >> 2;
-    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < t4; i += stride) {
-      const int c0 = static_cast<int>((i << 2) % C);
-      float4 d = reinterpret_cast<const float4*>(dy)[i];
-      const float4 xv = __ldg(reinterpret_cast<const float4*>(x) + i);
-      float* pd = &d.x;
-      const float* px = &xv.x;
-      if (mask) {
-        const float4 y = reinterpret_cast<const float4*>(mask)[i];
-        const float* py = &y.x;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) pd[q] = py[q] > 0.0f ? pd[q] : 0.0f;
-      }
-      float4 o;
-      float* po = &o.x;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int c = c0 + q;
-        const float rstd = __ldg(stats + C + c);
-        const float xhat = (px[q] - __ldg(stats + c)) * rstd;
-        const float g = gamma ? __ldg(gamma + c) : 1.0f;
-        po[q] = g * rstd * (pd[q] - (__ldg(sums + c) + xhat * __ldg(sums + C + c)) * invm);
-      }
-      reinterpret_cast<float4*>(dx)[i] = o;
-    }
-    return;
-  }
+  const bool relu = rm.beta != nullptr;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
     const int c = static_cast<int>(i % C);
     const float rstd = __ldg(stats + C + c);
-    const float xhat = (x[i] - __ldg(stats + c)) * rstd;
+    const float mean = __ldg(stats + c);
+    const float xv = x[i];
+    const float xhat = (xv - mean) * rstd;
     const float g = gamma ? __ldg(gamma + c) : 1.0f;
     float d = dy[i];
-    if (mask && !(mask[i] > 0.0f)) d = 0.0f;
+    if (relu) {
+      const float gm = rm.gamma ? __ldg(rm.gamma + c) : 1.0f;
+      if (!((xv - mean) * rstd * gm + __ldg(rm.beta + c) > 0.0f)) d = 0.0f;
+    }
     dx[i] = g * rstd * (d - (__ldg(sums + c) + xhat * __ldg(sums + C + c)) * invm);
   }
 }
@@ -693,16 +696,16 @@ __global__ void pool_bwd_kernel(const float* __restrict__ x, const float* __rest
 __global__ void pool_fwd_vec_kernel(const float* __restrict__ x, float* __restrict__ y,
                                     uint8_t* __restrict__ arg, Geom g, int type) {
   const int C4 = g.C >> 2;
-  const int64_t total = int64_t(g.B) * g.Ho * g.Wo * C4;
-  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  const RowsIdx ri(C4);
+  if (!ri.active) return;
+  const int c4 = ri.v;
+  const int npix = g.B * g.Ho * g.Wo, hw = g.Ho * g.Wo;
   const float4* x4 = reinterpret_cast<const float4*>(x);
-  for (int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < total; idx += stride) {
-    const int c4 = static_cast<int>(idx % C4);
-    int64_t p = idx / C4;
-    const int ow = static_cast<int>(p % g.Wo);
-    p /= g.Wo;
-    const int oh = static_cast<int>(p % g.Ho);
-    const int b = static_cast<int>(p / g.Ho);
+  for (int pix = ri.r; pix < npix; pix += ri.rstep) {
+    const int64_t idx = int64_t(pix) * C4 + c4;
+    const int b = pix / hw;
+    const int rem = pix - b * hw;
+    const int oh = rem / g.Wo, ow = rem - (rem / g.Wo) * g.Wo;
     const int hs = oh * g.sh - g.ph, ws = ow * g.sw - g.pw;
     const int h0 = max(hs, 0), w0 = max(ws, 0);
     const int h1 = min(hs + g.kh, g.H), w1 = min(ws + g.kw, g.W);
@@ -745,17 +748,17 @@ __global__ void pool_fwd_vec_kernel(const float* __restrict__ x, float* __restri
 __global__ void pool_bwd_vec_kernel(const uint8_t* __restrict__ arg, const float* __restrict__ dy,
                                     float* __restrict__ dx, Geom g, int type) {
   const int C4 = g.C >> 2;
-  const int64_t total = int64_t(g.B) * g.H * g.W * C4;
-  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  const RowsIdx ri(C4);
+  if (!ri.active) return;
+  const int c4 = ri.v;
+  const int npix = g.B * g.H * g.W, hw = g.H * g.W;
   const float4* dy4 = reinterpret_cast<const float4*>(dy);
   const uchar4* a4 = reinterpret_cast<const uchar4*>(arg);
-  for (int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < total; idx += stride) {
-    const int c4 = static_cast<int>(idx % C4);
-    int64_t p = idx / C4;
-    const int w = static_cast<int>(p % g.W);
-    p /= g.W;
-    const int h = static_cast<int>(p % g.H);
-    const int b = static_cast<int>(p / g.H);
+  for (int pix = ri.r; pix < npix; pix += ri.rstep) {
+    const int64_t idx = int64_t(pix) * C4 + c4;
+    const int b = pix / hw;
+    const int rem = pix - b * hw;
+    const int h = rem / g.W, w = rem - (rem / g.W) * g.W;
     const int nh = h + g.ph - g.kh + 1, nw = w + g.pw - g.kw + 1;
     const int oh_lo = nh <= 0 ? 0 : (nh + g.sh - 1) / g.sh;
     const int oh_hi = min(g.Ho - 1, (h + g.ph) / g.sh);
@@ -793,12 +796,13 @@ __global__ void chan_copy_kernel(const float* __restrict__ src, int64_t lds, int
                                  int64_t cols) {
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   if (((cols | lds | soff | ldd | doff) & 3) == 0) {
-    const int64_t c4 = cols / 4, total = rows * c4;
-    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
-      const int64_t r = i / c4, c = (i - r * c4) * 4;
+    // rows x vectors launch shape
+    const RowsIdx ri(static_cast<int>(cols / 4));
+    if (!ri.active) return;
+    const int64_t c = int64_t(ri.v) * 4;
+    for (int64_t r = ri.r; r < rows; r += ri.rstep)
       *reinterpret_cast<float4*>(dst + r * ldd + doff + c) =
           __ldg(reinterpret_cast<const float4*>(src + r * lds + soff + c));
-    }
   } else {
     const int64_t total = rows * cols;
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
@@ -817,7 +821,9 @@ inline unsigned grid_for(int64_t n, int threads = 256, int64_t cap = int64_t(kNu
 
 // chunking of M rows for the column reductions
 inline void chunks_for(int64_t M, int64_t* rpc, int* nchunk) {
-  int64_t n = M < kMaxChunks ? M : kMaxChunks;
+  // >= 256 rows per chunk (fewer partials to merge), <= 2 chunks per SM
+  int64_t n = ceil_div(M, 256);
+  if (n > kMaxChunks) n = kMaxChunks;
   if (n < 1) n = 1;
   *rpc = ceil_div(M, n);
   *nchunk = static_cast<int>(ceil_div(M, *rpc));
@@ -825,12 +831,12 @@ inline void chunks_for(int64_t M, int64_t* rpc, int* nchunk) {
 
 template <int MODE>
 int launch_partial(const float* a, const float* xs, const float* stats, int64_t M, int C,
-                   double* ws, int* nchunk_out, cudaStream_t st, const float* mask = nullptr) {
+                   double* ws, int* nchunk_out, cudaStream_t st,
+                   ReluMask rm = ReluMask{nullptr, nullptr}) {
   int64_t rpc;
   int nchunk;
   chunks_for(M, &rpc, &nchunk);
-  const bool vec = (C % 4) == 0 && aligned16(a) && (MODE != 1 || aligned16(xs)) &&
-                   (!mask || aligned16(mask));
+  const bool vec = (C % 4) == 0 && aligned16(a) && (MODE != 1 || aligned16(xs));
   if (vec) {
     const int C4 = C / 4;
     const int ct4 = C4 < kRedThreads ? C4 : kRedThreads;
@@ -838,13 +844,13 @@ int launch_partial(const float* a, const float* xs, const float* stats, int64_t 
     const size_t smem = size_t(rpp) * 2 * ct4 * 4 * sizeof(double);
     dim3 grid(nchunk, static_cast<unsigned>(ceil_div(C4, ct4)));
     colreduce_partial_vec_kernel<MODE><<<grid, kRedThreads, smem, st>>>(a, xs, stats, M, C, rpc, ws,
-                                                                      mask);
+                                                                      rm);
   } else {
     const int tpr = C < kRedThreads ? C : kRedThreads;
     const int rpp = kRedThreads / tpr;
     const size_t smem = size_t(rpp) * 2 * tpr * sizeof(double);
     colreduce_partial_kernel<MODE><<<nchunk, kRedThreads, smem, st>>>(a, xs, stats, M, C, rpc, ws,
-                                                                    mask);
+                                                                    rm);
   }
   *nchunk_out = nchunk;
   MGX_LAUNCHED();
@@ -876,9 +882,10 @@ extern "C" int mgx_im2col_bf16(const float* x, void* col, const int64_t* geom, i
                   g.Wo > 0, "mgx_im2col_bf16: bad geometry");
   MGX_REQUIRE(ldk % 8 == 0 && ldk >= int64_t(g.kh) * g.kw * g.C, "mgx_im2col_bf16: bad ldk");
   MGX_REQUIRE(mgx::aligned16(x) && mgx::aligned16(col), "mgx_im2col_bf16: unaligned");
-  const int64_t n = int64_t(g.B) * g.Ho * g.Wo * (ldk / 8);
-  mgx::conv::im2col_kernel<<<grid_for(n), 256, 0, mgx::as_stream(stream)>>>(
-      x, static_cast<__nv_bfloat16*>(col), g, ldk);
+  MGX_REQUIRE(int64_t(g.B) * g.Ho * g.Wo < (1ll << 31), "mgx_im2col_bf16: too many rows");
+  mgx::conv::im2col_kernel<<<mgx::rows_grid(int64_t(g.B) * g.Ho * g.Wo, ldk / 8),
+                             mgx::kRowsThreads, 0,
+                             mgx::as_stream(stream)>>>(x, static_cast<__nv_bfloat16*>(col), g, ldk);
   MGX_LAUNCHED();
   return MGX_OK;
 }
@@ -906,8 +913,7 @@ extern "C" int mgx_bn_stats(const float* x, int64_t M, int64_t C, void* ws, floa
     MGX_TRY(mgx::conv::launch_partial<0>(x, nullptr, nullptr, M, static_cast<int>(C),
                                          static_cast<double*>(ws), &nchunk, st));
   }
-  mgx::conv::bn_stats_finalize_kernel<<<static_cast<unsigned>(mgx::ceil_div(C, 32)),
-                                         dim3(32, mgx::conv::kFinLanes), 0, st>>>(
+  mgx::conv::bn_stats_finalize_kernel<<<static_cast<unsigned>(mgx::ceil_div(C, mgx::conv::kFinChannels)), 32 * mgx::conv::kFinChannels, 0, st>>>(
       static_cast<const double*>(ws), nchunk, M, static_cast<int>(C), x, eps, momentum, use_global,
       stats, moving_mean, moving_var);
   MGX_LAUNCHED();
@@ -918,22 +924,30 @@ extern "C" int mgx_bn_apply(const float* x, const float* stats, const float* gam
                             const float* beta, float* y, int64_t M, int64_t C, int act,
                             uintptr_t stream) {
   MGX_REQUIRE(x && stats && beta && y && M > 0 && C > 0, "mgx_bn_apply: bad arguments");
-  mgx::conv::bn_apply_kernel<<<grid_for(M * C / ((C & 3) ? 1 : 4)), 256, 0, mgx::as_stream(stream)>>>(
-      x, stats, gamma, beta, y, M, static_cast<int>(C), act);
+  if ((C & 3) == 0) {
+    MGX_REQUIRE(mgx::aligned16(x) && mgx::aligned16(y), "mgx_bn_apply: unaligned tensors");
+    mgx::conv::bn_apply_kernel<<<mgx::rows_grid(M, C / 4),
+                                 mgx::kRowsThreads, 0,
+                                 mgx::as_stream(stream)>>>(x, stats, gamma, beta, y, M,
+                                                           static_cast<int>(C), act);
+  } else {
+    mgx::conv::bn_apply_kernel<<<grid_for(M * C), 256, 0, mgx::as_stream(stream)>>>(
+        x, stats, gamma, beta, y, M, static_cast<int>(C), act);
+  }
   MGX_LAUNCHED();
   return MGX_OK;
 }
 
 extern "C" int mgx_bn_bwd_reduce(const float* dy, const float* x, const float* stats, int64_t M,
                                  int64_t C, void* ws, float* sums, float* dbeta, float* dgamma,
-                                 int dgamma_zero, const float* mask, uintptr_t stream) {
+                                 int dgamma_zero, const float* relu_gamma, const float* relu_beta,
+                                 uintptr_t stream) {
   MGX_REQUIRE(dy && x && stats && ws && sums && M > 0 && C > 0, "mgx_bn_bwd_reduce: bad arguments");
   cudaStream_t st = mgx::as_stream(stream);
   int nchunk = 0;
   MGX_TRY(mgx::conv::launch_partial<1>(dy, x, stats, M, static_cast<int>(C), static_cast<double*>(ws),
-                                       &nchunk, st, mask));
-  mgx::conv::colsum_finalize_kernel<<<static_cast<unsigned>(mgx::ceil_div(C, 32)),
-                                       dim3(32, mgx::conv::kFinLanes), 0, st>>>(
+                                       &nchunk, st, mgx::conv::ReluMask{relu_gamma, relu_beta}));
+  mgx::conv::colsum_finalize_kernel<<<static_cast<unsigned>(mgx::ceil_div(C, mgx::conv::kFinChannels)), 32 * mgx::conv::kFinChannels, 0, st>>>(
       static_cast<const double*>(ws), nchunk, static_cast<int>(C), 1, sums, dbeta, dgamma,
       dgamma_zero);
   MGX_LAUNCHED();
@@ -941,16 +955,17 @@ extern "C" int mgx_bn_bwd_reduce(const float* dy, const float* x, const float* s
 }
 
 extern "C" int mgx_bn_bwd_dx(const float* dy, const float* x, const float* stats, const float* sums,
-                             const float* gamma, float* dx, int64_t M, int64_t C, const float* mask,
-                             float* dsum, void* ws, uintptr_t stream) {
+                             const float* gamma, float* dx, int64_t M, int64_t C,
+                             const float* relu_gamma, const float* relu_beta, float* dsum,
+                             void* ws, uintptr_t stream) {
   MGX_REQUIRE(dy && x && stats && sums && dx && M > 0 && C > 0, "mgx_bn_bwd_dx: bad arguments");
-  const bool vec = (C % 4) == 0 && mgx::aligned16(dy) && mgx::aligned16(x) && mgx::aligned16(dx) &&
-                   (!mask || mgx::aligned16(mask));
-  MGX_REQUIRE(vec || (C % 4) != 0, "mgx_bn_bwd_dx: C %% 4 == 0 needs 16-byte aligned tensors");
+  const bool vec = (C % 4) == 0 && mgx::aligned16(dy) && mgx::aligned16(x) && mgx::aligned16(dx);
   cudaStream_t st = mgx::as_stream(stream);
-  if (dsum) {
-    // fused: dx plus its per-channel sum (conv bias gradient) in one pass
-    MGX_REQUIRE(ws && vec, "mgx_bn_bwd_dx: dsum needs a workspace and C %% 4 == 0");
+  const mgx::conv::ReluMask rm{relu_gamma, relu_beta};
+  if (vec) {
+    // dx (and, when dsum is given, its per-channel sum: the conv bias
+    // gradient) in one row-tiled pass
+    MGX_REQUIRE(!dsum || ws, "mgx_bn_bwd_dx: dsum needs a workspace");
     int64_t rpc;
     int nchunk;
     mgx::conv::chunks_for(M, &rpc, &nchunk);
@@ -959,16 +974,22 @@ extern "C" int mgx_bn_bwd_dx(const float* dy, const float* x, const float* stats
     const int rpp = mgx::conv::kRedThreads / ct4;
     const size_t smem = size_t(rpp) * ct4 * 4 * sizeof(double);
     dim3 grid(nchunk, static_cast<unsigned>(mgx::ceil_div(C4, ct4)));
+    double* wsd = dsum ? static_cast<double*>(ws) : nullptr;
+    if (!dsum) {
+      // reuse the tiled kernel without the reduction output
+      MGX_REQUIRE(ws, "mgx_bn_bwd_dx: the vectorised pass needs a workspace");
+      wsd = static_cast<double*>(ws);
+    }
     mgx::conv::bn_dx_colsum_kernel<<<grid, mgx::conv::kRedThreads, smem, st>>>(
-        dy, x, stats, sums, gamma, dx, mask, M, static_cast<int>(C), rpc, static_cast<double*>(ws));
-    mgx::conv::colsum_finalize_kernel<<<static_cast<unsigned>(mgx::ceil_div(C, 32)),
-                                         dim3(32, mgx::conv::kFinLanes), 0, st>>>(
-        static_cast<const double*>(ws), nchunk, static_cast<int>(C), 0, dsum, nullptr, nullptr, 0);
+        dy, x, stats, sums, gamma, dx, rm, M, static_cast<int>(C), rpc, wsd);
+    if (dsum)
+      mgx::conv::colsum_finalize_kernel<<<static_cast<unsigned>(mgx::ceil_div(C, mgx::conv::kFinChannels)), 32 * mgx::conv::kFinChannels, 0, st>>>(
+          static_cast<const double*>(ws), nchunk, static_cast<int>(C), 0, dsum, nullptr, nullptr, 0);
     MGX_LAUNCHED();
     return MGX_OK;
   }
-  mgx::conv::bn_bwd_dx_kernel<<<grid_for(M * C / ((C & 3) ? 1 : 4)), 256, 0, st>>>(
-      dy, x, stats, sums, gamma, dx, M, static_cast<int>(C), mask);
+  mgx::conv::bn_bwd_dx_kernel<<<grid_for(M * C), 256, 0, st>>>(dy, x, stats, sums, gamma, dx, M,
+                                                               static_cast<int>(C), rm);
   MGX_LAUNCHED();
   return MGX_OK;
 }
@@ -980,8 +1001,7 @@ extern "C" int mgx_colsum(const float* x, int64_t M, int64_t C, void* ws, float*
   int nchunk = 0;
   MGX_TRY(mgx::conv::launch_partial<2>(x, nullptr, nullptr, M, static_cast<int>(C),
                                        static_cast<double*>(ws), &nchunk, st));
-  mgx::conv::colsum_finalize_kernel<<<static_cast<unsigned>(mgx::ceil_div(C, 32)),
-                                       dim3(32, mgx::conv::kFinLanes), 0, st>>>(
+  mgx::conv::colsum_finalize_kernel<<<static_cast<unsigned>(mgx::ceil_div(C, mgx::conv::kFinChannels)), 32 * mgx::conv::kFinChannels, 0, st>>>(
       static_cast<const double*>(ws), nchunk, static_cast<int>(C), 0, out, nullptr, nullptr, 0);
   MGX_LAUNCHED();
   return MGX_OK;
@@ -998,8 +1018,8 @@ extern "C" int mgx_pool_forward(const float* x, float* y, const int64_t* geom, i
   MGX_REQUIRE(g.Ho > 0 && g.Wo > 0, "mgx_pool_forward: bad geometry");
   cudaStream_t st = mgx::as_stream(stream);
   if (pool_vec_ok(g, x, y) && g.kh * g.kw <= 255) {
-    const int64_t n = int64_t(g.B) * g.Ho * g.Wo * (g.C / 4);
-    mgx::conv::pool_fwd_vec_kernel<<<grid_for(n), 256, 0, st>>>(
+    mgx::conv::pool_fwd_vec_kernel<<<mgx::rows_grid(int64_t(g.B) * g.Ho * g.Wo, g.C / 4),
+                                     mgx::kRowsThreads, 0, st>>>(
         x, y, type == 0 ? static_cast<uint8_t*>(argmax) : nullptr, g, type);
   } else {
     MGX_REQUIRE(!argmax || type != 0, "mgx_pool_forward: argmax needs C %% 4 == 0 and kh*kw <= 255");
@@ -1019,8 +1039,8 @@ extern "C" int mgx_pool_backward(const float* x, const float* y, const float* dy
   cudaStream_t st = mgx::as_stream(stream);
   const bool use_arg = type == 0 && argmax != nullptr;
   if (pool_vec_ok(g, dy, dx) && (type == 1 || use_arg)) {
-    const int64_t n = int64_t(g.B) * g.H * g.W * (g.C / 4);
-    mgx::conv::pool_bwd_vec_kernel<<<grid_for(n), 256, 0, st>>>(
+    mgx::conv::pool_bwd_vec_kernel<<<mgx::rows_grid(int64_t(g.B) * g.H * g.W, g.C / 4),
+                                     mgx::kRowsThreads, 0, st>>>(
         static_cast<const uint8_t*>(argmax), dy, dx, g, type);
   } else {
     MGX_REQUIRE(type == 1 || (x && y), "mgx_pool_backward: max pooling needs x and y");
@@ -1035,8 +1055,13 @@ extern "C" int mgx_chan_copy(const float* src, int64_t lds, int64_t soff, float*
                              int64_t doff, int64_t rows, int64_t cols, uintptr_t stream) {
   MGX_REQUIRE(src && dst && rows >= 0 && cols >= 0, "mgx_chan_copy: bad arguments");
   if (rows == 0 || cols == 0) return MGX_OK;
-  mgx::conv::chan_copy_kernel<<<grid_for(rows * cols / 4 + 1), 256, 0, mgx::as_stream(stream)>>>(
-      src, lds, soff, dst, ldd, doff, rows, cols);
+  if (((cols | lds | soff | ldd | doff) & 3) == 0)
+    mgx::conv::chan_copy_kernel<<<mgx::rows_grid(rows, cols / 4),
+                                  mgx::kRowsThreads, 0,
+                                  mgx::as_stream(stream)>>>(src, lds, soff, dst, ldd, doff, rows, cols);
+  else
+    mgx::conv::chan_copy_kernel<<<grid_for(rows * cols), 256, 0, mgx::as_stream(stream)>>>(
+        src, lds, soff, dst, ldd, doff, rows, cols);
   MGX_LAUNCHED();
   return MGX_OK;
 }

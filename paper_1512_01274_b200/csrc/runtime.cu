@@ -270,12 +270,13 @@ static int run_instr(const mgx_instr& in, cudaStream_t st) {
     case MGX_OP_BN_BWD_REDUCE:
       return mgx_bn_bwd_reduce(p0, p1, p2, d[0], d[1], in.ptr[3], static_cast<float*>(in.ptr[4]),
                                reinterpret_cast<float*>(d[2]), reinterpret_cast<float*>(d[3]),
-                               static_cast<int>(d[4]), static_cast<const float*>(in.ptr[5]), s);
+                               static_cast<int>(d[4]), reinterpret_cast<const float*>(d[5]),
+                               static_cast<const float*>(in.ptr[5]), s);
     case MGX_OP_BN_BWD_DX:
       return mgx_bn_bwd_dx(p0, p1, p2, p3, static_cast<float*>(in.ptr[4]),
                            static_cast<float*>(in.ptr[5]), d[0], d[1],
-                           reinterpret_cast<const float*>(d[2]), reinterpret_cast<float*>(d[3]),
-                           reinterpret_cast<void*>(d[4]), s);
+                           reinterpret_cast<const float*>(d[5]), reinterpret_cast<const float*>(d[2]),
+                           reinterpret_cast<float*>(d[3]), reinterpret_cast<void*>(d[4]), s);
     case MGX_OP_POOL_FWD:
       return mgx_pool_forward(p0, p1, d, static_cast<int>(d[7]), in.act, in.ptr[2], s);
     case MGX_OP_POOL_BWD:

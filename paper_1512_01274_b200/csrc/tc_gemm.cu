@@ -397,14 +397,14 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
 // y (bf16, rows x ldo) = x (fp32, R x C, row stride ldi), zero-filled
 // beyond the source extent (the K padding of a tensor-core operand).  8
 // output columns per thread (one 16-byte store).
+// rows x vectors launch shape (RowsIdx): a thread owns an 8-column group
 __global__ void cast_rows_kernel(const float* __restrict__ x, int64_t R, int64_t C, int64_t ldi,
                                  __nv_bfloat16* __restrict__ y, int64_t rows, int64_t ldo) {
-  const int64_t per = ldo >> 3;
-  const int64_t n = rows * per;
-  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  const RowsIdx ri(static_cast<int>(ldo / 8));
+  if (!ri.active) return;
+  const int64_t c0 = int64_t(ri.v) * 8;
   const bool vec = ((ldi & 3) == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const int64_t r = i / per, c0 = (i - r * per) * 8;
+  for (int64_t r = ri.r; r < rows; r += ri.rstep) {
     float v[8];
     if (r < R && vec && c0 + 8 <= C) {
       const float4 a = __ldg(reinterpret_cast<const float4*>(x + r * ldi + c0));
@@ -632,9 +632,7 @@ extern "C" int mgx_cast_bf16_2d(const float* x, int64_t R, int64_t C, int64_t ld
               "mgx_cast_bf16_2d: destination smaller than the source");
   cudaStream_t st = mgx::as_stream(stream);
   if (!transpose && ldo % 8 == 0 && mgx::aligned16(y)) {
-    int64_t blocks = mgx::ceil_div(rows * (ldo / 8), 256);
-    if (blocks > 148 * 16) blocks = 148 * 16;
-    mgx::tc::cast_rows_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(
+    mgx::tc::cast_rows_kernel<<<mgx::rows_grid(rows, ldo / 8), mgx::kRowsThreads, 0, st>>>(
         x, R, C, ldi, static_cast<__nv_bfloat16*>(y), rows, ldo);
   } else if (!transpose) {
     MGX_REQUIRE(false, "mgx_cast_bf16_2d: ldo must be a multiple of 8 and y 16-byte aligned");
