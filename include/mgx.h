@@ -142,6 +142,19 @@ int mgx_gemm_bf16_tc_ex(const void* A, int64_t lda, int a_mn, const void* B, int
                         int b_mn, const float* bias, float* C, int64_t ldc, int64_t M,
                         int64_t N, int64_t K, int act, int splits, float* workspace,
                         uintptr_t stream);
+/* Implicit-GEMM convolution contractions: one operand is gathered on the
+ * fly from a compact bf16 NHWC tensor `src` (C % 8 == 0) by cp.async
+ * producer warps inside the tcgen05 GEMM, never materialised:
+ *   gather(src)[m, k] = src[b, oh*sh-ph+i, ow*sw-pw+j, c],
+ *   m = (b, oh, ow) output pixel, k = (i*kw + j)*C + c  (geom as below).
+ * mode 1: C[M=pixels, N] = gather . op[N, K]^T      (op K-major, row stride
+ *         ldop: convolution forward / stride-1 data gradient)
+ * mode 2: C[M, N=kh*kw*C] = op[K=pixels, M]^T . gather  (op MN-major: the
+ *         output gradient; weight gradient).  Split-K as mgx_gemm_bf16_tc_ex. */
+int mgx_gemm_bf16_conv(int mode, const void* src, const int64_t* geom, const void* op,
+                       int64_t ldop, const float* bias, float* C, int64_t ldc, int64_t M,
+                       int64_t N, int64_t K, int act, int splits, float* workspace,
+                       uintptr_t stream);
 /* Workspace (floats) the auto split-K choice needs for an M x N x K GEMM. */
 int mgx_gemm_splitk_workspace(int64_t M, int64_t N, int64_t K, int64_t* out_floats);
 
@@ -166,7 +179,7 @@ int mgx_bn_stats(const float* x, int64_t M, int64_t C, void* ws, float* stats, f
                  float* moving_var, float eps, float momentum, int use_global, uintptr_t stream);
 /* y = act((x - mean) * rstd * gamma + beta); gamma NULL = fix_gamma (1). */
 int mgx_bn_apply(const float* x, const float* stats, const float* gamma, const float* beta,
-                 float* y, int64_t M, int64_t C, int act, uintptr_t stream);
+                 float* y, int64_t M, int64_t C, int act, void* y16, uintptr_t stream);
 /* sums = [sum dy | sum dy*xhat] per channel; also written to dbeta and
  * dgamma when non-NULL (dgamma zero-filled when dgamma_zero: fix_gamma).
  * relu_beta (optional): a ReLU follows the BatchNorm; dy is then masked by
@@ -183,7 +196,7 @@ int mgx_bn_bwd_reduce(const float* dy, const float* x, const float* stats, int64
  * convolution feeding the BatchNorm). */
 int mgx_bn_bwd_dx(const float* dy, const float* x, const float* stats, const float* sums,
                   const float* gamma, float* dx, int64_t M, int64_t C, const float* relu_gamma,
-                  const float* relu_beta, float* dsum, void* ws, uintptr_t stream);
+                  const float* relu_beta, float* dsum, void* ws, void* dx16, uintptr_t stream);
 /* out[c] = sum over rows of x[r, c] (conv bias gradient). */
 int mgx_colsum(const float* x, int64_t M, int64_t C, void* ws, float* out, uintptr_t stream);
 /* Pooling, NHWC.  type 0 max (padding ignored), 1 avg (count_include_pad);
@@ -192,13 +205,13 @@ int mgx_colsum(const float* x, int64_t M, int64_t C, void* ws, float* out, uintp
  * the window-local index of the first maximum, written by the forward and
  * read by the backward instead of rescanning x. */
 int mgx_pool_forward(const float* x, float* y, const int64_t* geom, int full, int type,
-                     void* argmax, uintptr_t stream);
+                     void* argmax, void* y16, uintptr_t stream);
 int mgx_pool_backward(const float* x, const float* y, const float* dy, float* dx,
                       const int64_t* geom, int full, int type, const void* argmax,
                       uintptr_t stream);
 /* dst[r, doff + c] = src[r, soff + c] for r < rows, c < cols (Concat). */
 int mgx_chan_copy(const float* src, int64_t lds, int64_t soff, float* dst, int64_t ldd,
-                  int64_t doff, int64_t rows, int64_t cols, uintptr_t stream);
+                  int64_t doff, int64_t rows, int64_t cols, void* dst16, uintptr_t stream);
 
 /* Momentum SGD, tensor path (optim.py:39-50): 5 separately rounded steps. */
 int mgx_sgd_step(float* w, const float* g, float* v, int64_t n,
@@ -262,20 +275,26 @@ typedef struct mgx_instr {
 #define MGX_OP_BN_STATS 17    /* ptr0=x ptr1=ws ptr2=stats ptr3=mmean ptr4=mvar    */
                               /* dims=M,C,use_global fattr=eps,momentum            */
 #define MGX_OP_BN_APPLY 18    /* ptr0=x ptr1=stats ptr2=gamma ptr3=beta ptr4=y     */
-                              /* dims=M,C act                                      */
+                              /* ptr5=y16 (optional bf16 copy) dims=M,C act        */
 #define MGX_OP_BN_BWD_REDUCE 19 /* ptr0=dy ptr1=x ptr2=stats ptr3=ws ptr4=sums     */
                               /* ptr5=relu_beta                                    */
                               /* dims=M,C,dbeta*,dgamma*,dgamma_zero,relu_gamma*   */
 #define MGX_OP_BN_BWD_DX 20   /* ptr0=dy ptr1=x ptr2=stats ptr3=sums ptr4=gamma    */
-                              /* ptr5=dx dims=M,C,relu_beta*,dsum*,ws*,relu_gamma* */
+                              /* ptr5=dx dims=M,C,relu_beta*,dsum*,ws*,relu_gamma*, */
+                              /* dx16* (optional bf16 copy)                        */
                               /* (* = a device address carried in a dim)           */
-#define MGX_OP_POOL_FWD 21    /* ptr0=x ptr1=y ptr2=argmax dims=geom,full act=type */
+#define MGX_OP_POOL_FWD 21    /* ptr0=x ptr1=y ptr2=argmax ptr3=y16 dims=geom,full */
 #define MGX_OP_POOL_BWD 22    /* ptr0=x ptr1=y ptr2=dy ptr3=dx ptr4=argmax dims=geom,full */
-#define MGX_OP_CHAN_COPY 23   /* ptr0=src ptr1=dst dims=rows,cols,lds,soff,ldd,doff */
+#define MGX_OP_CHAN_COPY 23   /* ptr0=src ptr1=dst ptr2=dst16 dims=rows,cols,lds,    */
+                              /* soff,ldd,doff                                     */
 #define MGX_OP_COLSUM 24      /* ptr0=x ptr1=ws ptr2=out dims=M,C                  */
 #define MGX_OP_GEMM_TC_EX 25  /* ptr0=A ptr1=B ptr2=bias ptr3=C ptr4=workspace act */
                               /* dims=M,N,K,lda,ldb,ldc,(a_mn|b_mn<<1),splits      */
 #define MGX_OP_WFLIP 26       /* ptr0=w ptr1=wf(bf16) dims=F,kh,kw,C,ld            */
+#define MGX_OP_GEMM_CONV 27   /* ptr0=src(bf16 NHWC) ptr1=op ptr2=bias ptr3=C      */
+                              /* ptr4=workspace dims=M,N,K,ldop,ldc,               */
+                              /* mode|splits<<8, B<<48|H<<32|W<<16|C,              */
+                              /* kh<<40|kw<<32|sh<<24|sw<<16|ph<<8|pw              */
 
 /* Run instructions eagerly, in order, on stream (no program object). */
 int mgx_instr_run(const mgx_instr* instrs, int32_t count, uintptr_t stream);

@@ -30,7 +30,7 @@ OP_ACT_FWD, OP_ACT_BWD, OP_SOFTMAX_FWD, OP_SOFTMAX_BWD, OP_AXPY = 8, 9, 10, 11, 
 OP_CAST_BF16, OP_GEMM_TC = 13, 14
 OP_IM2COL, OP_COL2IM, OP_BN_STATS, OP_BN_APPLY, OP_BN_BWD_REDUCE, OP_BN_BWD_DX = 15, 16, 17, 18, 19, 20
 OP_POOL_FWD, OP_POOL_BWD, OP_CHAN_COPY, OP_COLSUM, OP_GEMM_TC_EX = 21, 22, 23, 24, 25
-OP_WFLIP = 26
+OP_WFLIP, OP_GEMM_CONV = 26, 27
 
 KV_ADD, KV_SGD, KV_AGG = 0, 1, 2
 KV_MAX_SEGS = 256
@@ -136,6 +136,8 @@ _SIGNATURES = {
     "mgx_gemm_bf16_tc_ex": ([c_vp, c_i64, ctypes.c_int, c_vp, c_i64, ctypes.c_int, c_vp, c_vp,
                              c_i64, c_i64, c_i64, c_i64, ctypes.c_int, ctypes.c_int, c_vp, c_uptr],
                             ctypes.c_int),
+    "mgx_gemm_bf16_conv": ([ctypes.c_int, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_i64, c_i64,
+                            c_i64, ctypes.c_int, ctypes.c_int, c_vp, c_uptr], ctypes.c_int),
     "mgx_gemm_splitk_workspace": ([c_i64, c_i64, c_i64, ctypes.POINTER(c_i64)], ctypes.c_int),
     "mgx_im2col_bf16": ([c_vp, c_vp, c_vp, c_i64, c_uptr], ctypes.c_int),
     "mgx_col2im": ([c_vp, c_i64, c_vp, c_vp, c_uptr], ctypes.c_int),
@@ -143,18 +145,19 @@ _SIGNATURES = {
     "mgx_reduce_workspace_bytes": ([c_i64, c_i64, ctypes.POINTER(c_i64)], ctypes.c_int),
     "mgx_bn_stats": ([c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_f32, c_f32, ctypes.c_int,
                       c_uptr], ctypes.c_int),
-    "mgx_bn_apply": ([c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, ctypes.c_int, c_uptr],
+    "mgx_bn_apply": ([c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, ctypes.c_int, c_vp, c_uptr],
                      ctypes.c_int),
     "mgx_bn_bwd_reduce": ([c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, ctypes.c_int,
                            c_vp, c_vp, c_uptr], ctypes.c_int),
     "mgx_bn_bwd_dx": ([c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp,
-                       c_uptr], ctypes.c_int),
+                       c_vp, c_uptr], ctypes.c_int),
     "mgx_colsum": ([c_vp, c_i64, c_i64, c_vp, c_vp, c_uptr], ctypes.c_int),
-    "mgx_pool_forward": ([c_vp, c_vp, c_vp, ctypes.c_int, ctypes.c_int, c_vp, c_uptr],
+    "mgx_pool_forward": ([c_vp, c_vp, c_vp, ctypes.c_int, ctypes.c_int, c_vp, c_vp, c_uptr],
                          ctypes.c_int),
     "mgx_pool_backward": ([c_vp, c_vp, c_vp, c_vp, c_vp, ctypes.c_int, ctypes.c_int, c_vp, c_uptr],
                           ctypes.c_int),
-    "mgx_chan_copy": ([c_vp, c_i64, c_i64, c_vp, c_i64, c_i64, c_i64, c_i64, c_uptr], ctypes.c_int),
+    "mgx_chan_copy": ([c_vp, c_i64, c_i64, c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_uptr],
+                      ctypes.c_int),
     "mgx_kv_max_grid": ([c_i32, c_i32, ctypes.POINTER(c_i32)], ctypes.c_int),
     "mgx_kv_config": ([c_i32, c_i32, ctypes.POINTER(c_i32), ctypes.POINTER(c_i32),
                        ctypes.POINTER(c_i32)], ctypes.c_int),

@@ -114,45 +114,104 @@ def _splitk_ws(m: int, n: int, k: int) -> int:
     return out.value
 
 
+def _weights_bf16(w: View, ctx, code: list):
+    """wb[F, ldk] bf16 (zero K padding) of a convolution weight; once per
+    step (memo on the weight node)."""
+    f = w.shape[0]
+    kk = prod(w.shape[1:])
+    ldk = _pad8(kk)
+    key = ("wb", id(ctx.input_node("in1")), w.ptr)
+    wb = ctx.memo.get(key)
+    if wb is None:
+        wb = ctx.persistent(2 * f * ldk)
+        ctx.memo[key] = wb
+        code.append(_cast_rows(w, f, kk, wb, ldk))
+    return wb, ldk
+
+
 def _conv_operands(x: View, w: View, attrs, ctx, code: list):
-    """bf16 operand copies shared by the forward and the backward of one
-    convolution: col = im2col(x) [M, ldk], wb = w [F, ldk].  Emitted once
-    per step (memo on the source nodes)."""
+    """Explicit-GEMM operands (C % 8 != 0): col = im2col(x) [M, ldk] and the
+    bf16 weight, shared by the forward and the backward."""
     k, s, p = _conv_params(attrs)
     b, h, wd, c = x.shape
     ho, wo = _conv_out(h, wd, k, s, p)
     m, kk = b * ho * wo, k[0] * k[1] * c
     ldk = _pad8(kk)
     f = w.shape[0]
-    xn, wn = ctx.input_node("in0"), ctx.input_node("in1")
+    xn = ctx.input_node("in0")
     key_c = ("col", id(xn), x.ptr, tuple(k), tuple(s), tuple(p))
     col = ctx.memo.get(key_c)
     if col is None:
         col = ctx.persistent(2 * m * ldk)
         ctx.memo[key_c] = col
         code.append(instr(L.OP_IM2COL, [x.ptr, col], _geom(x.shape, k, s, p) + [ldk]))
-    key_w = ("wb", id(wn), w.ptr)
-    wb = ctx.memo.get(key_w)
-    if wb is None:
-        wb = ctx.persistent(2 * f * ldk)
-        ctx.memo[key_w] = wb
-        code.append(_cast_rows(w, f, kk, wb, ldk))
+    wb, _ = _weights_bf16(w, ctx, code)
     return col, wb, (m, kk, ldk, f, k, s, p, ho, wo)
+
+
+def _implicit_ok(c: int) -> bool:
+    return c % 8 == 0
+
+
+def _shadow(v: View, node, ctx, code: list) -> int:
+    """Compact bf16 NHWC copy of ``v`` for the implicit GEMM: the producer's
+    (written in its own pass) or a cast made here once per step."""
+    sh = ctx.shadow_of(node)
+    if sh is None:
+        n = v.size
+        key = ("shadow", id(node) if node is not None else v.ptr)
+        sh = ctx.persistent(2 * n)
+        ctx.memo[key] = sh
+        c = v.shape[-1]
+        code.append(_cast_rows(v, n // c, c, sh, c))
+    return sh
+
+
+def _pack_geom(shape, k, s, p) -> tuple:
+    b, h, w, c = shape
+    assert max(b, h, w, c) < (1 << 16) and max(*k, *s, *p) < (1 << 8)
+    return ((b << 48) | (h << 32) | (w << 16) | c,
+            (k[0] << 40) | (k[1] << 32) | (s[0] << 24) | (s[1] << 16) | (p[0] << 8) | p[1])
+
+
+def _gemm_conv(mode: int, src: int, shape, k, s, p, op: int, ldop: int, out: int, ldc: int,
+               m: int, n: int, kdim: int, bias=None, act: int = 0, splits: int = 1, ws=None):
+    g1, g2 = _pack_geom(shape, k, s, p)
+    return instr(L.OP_GEMM_CONV, [src, op, bias, out, ws],
+                 [m, n, kdim, ldop, ldc, mode | (splits << 8), g1, g2], act=act)
 
 
 def _conv_lower_fwd(ins, out, attrs):
     ctx = current_ctx()
     code = []
-    col, wb, (m, kk, ldk, f, *_r) = _conv_operands(ins[0], ins[1], attrs, ctx, code)
+    x, w = ins[0], ins[1]
     bias = ins[2].ptr if len(ins) > 2 else None
+    k, s, p = _conv_params(attrs)
+    f = w.shape[0]
+    if _implicit_ok(x.shape[3]):
+        # implicit GEMM: the A operand gathered from x's bf16 copy in-kernel
+        sh = _shadow(x, ctx.input_node("in0"), ctx, code)
+        wb, ldk = _weights_bf16(w, ctx, code)
+        b, h, wd, c = x.shape
+        ho, wo = _conv_out(h, wd, k, s, p)
+        kk = k[0] * k[1] * c
+        code.append(_gemm_conv(1, sh, x.shape, k, s, p, wb, ldk, out.ptr, f, b * ho * wo, f, kk,
+                               bias=bias))
+        return code
+    col, wb, (m, kk, ldk, f, *_r) = _conv_operands(x, w, attrs, ctx, code)
     code.append(_gemm(col, ldk, False, wb, ldk, False, out.ptr, f, m, f, kk, bias=bias))
     return code
 
 
 def _conv_dy(og: View, f: int, ctx, code: list):
+    """bf16 output gradient [M, ld]: the producer's compact copy (ld = F)
+    when there is one, else a padded cast made once per step."""
+    node = ctx.input_node("og")
+    if f % 8 == 0:
+        return _shadow(og, node, ctx, code), f
     m = prod(og.shape[:-1])
     ldf = _pad8(f)
-    key = ("dyb", id(ctx.input_node("og")), og.ptr)
+    key = ("dyb", id(node), og.ptr)
     dyb = ctx.memo.get(key)
     if dyb is None:
         dyb = ctx.persistent(2 * m * ldf)
@@ -170,23 +229,34 @@ def _conv_lower_bwd(slot, env, out, attrs):
         ws = ctx.scratch(_reduce_ws(m, f))
         return [instr(L.OP_COLSUM, [og.ptr, ws, out.ptr], [m, f])]
     x, w = env["in0"], env["in1"]
-    col, wb, (m, kk, ldk, f, k, s, p, ho, wo) = _conv_operands(x, w, attrs, ctx, code)
-    dyb, ldf = _conv_dy(og, f, ctx, code)
+    k, s, p = _conv_params(attrs)
+    b, h, wd, c = x.shape
+    ho, wo = _conv_out(h, wd, k, s, p)
+    m, kk, f = b * ho * wo, k[0] * k[1] * c, w.shape[0]
+    implicit = _implicit_ok(c)
     if slot == 1:
         # dW[f, kk] = sum_m dY[m, f] col[m, kk]: both operands MN-major, split-K
+        dyb, ldf = _conv_dy(og, f, ctx, code)
         nws = _splitk_ws(f, kk, m)
         ws = ctx.scratch(4 * nws) if nws else None
+        if implicit:
+            sh = _shadow(x, ctx.input_node("in0"), ctx, code)
+            code.append(_gemm_conv(2, sh, x.shape, k, s, p, dyb, ldf, out.ptr, kk, f, kk, m,
+                                   splits=0 if ws else 1, ws=ws))
+            return code
+        col, _wb, (m, kk, ldk, *_r) = _conv_operands(x, w, attrs, ctx, code)
         code.append(_gemm(dyb, ldf, True, col, ldk, True, out.ptr, kk, f, kk, m,
                           splits=0 if ws else 1, ws=ws))
         return code
-    # dX: dcol[m, kk] = dY[m, f] . W[f, kk] (W MN-major), then col2im
-    c = x.shape[3]
+    # dX
+    dyb, ldf = _conv_dy(og, f, ctx, code)
+    wb, ldk = _weights_bf16(w, ctx, code)
     if k == (1, 1) and s == (1, 1) and p == (0, 0):
         code.append(_gemm(dyb, ldf, False, wb, ldk, True, out.ptr, c, m, c, f))
         return code
     if s == (1, 1) and p[0] < k[0] and p[1] < k[1]:
-        # stride 1: dX = im2col(dY, pad k-1-p) . wflip^T, a forward
-        # convolution of the output gradient (no fp32 dcol, no col2im)
+        # stride 1: dX = conv(dY, flipped W, pad k-1-p): implicit GEMM over
+        # dY's bf16 copy when F % 8 == 0, else explicit im2col(dY)
         kf = k[0] * k[1] * f
         ldkf = _pad8(kf)
         key = ("wflip", id(ctx.input_node("in1")), w.ptr)
@@ -195,11 +265,14 @@ def _conv_lower_bwd(slot, env, out, attrs):
             wfl = ctx.persistent(2 * c * ldkf)
             ctx.memo[key] = wfl
             code.append(instr(L.OP_WFLIP, [w.ptr, wfl], [f, k[0], k[1], c, ldkf]))
-        b_, h_, w_ = x.shape[0], x.shape[1], x.shape[2]
-        dcolt = ctx.scratch(2 * b_ * h_ * w_ * ldkf)
         pf = (k[0] - 1 - p[0], k[1] - 1 - p[1])
+        if f % 8 == 0:
+            code.append(_gemm_conv(1, dyb, og.shape, k, (1, 1), pf, wfl, ldkf, out.ptr, c,
+                                   b * h * wd, c, kf))
+            return code
+        dcolt = ctx.scratch(2 * b * h * wd * ldkf)
         code.append(instr(L.OP_IM2COL, [og.ptr, dcolt], _geom(og.shape, k, (1, 1), pf) + [ldkf]))
-        code.append(_gemm(dcolt, ldkf, False, wfl, ldkf, False, out.ptr, c, b_ * h_ * w_, c, kf))
+        code.append(_gemm(dcolt, ldkf, False, wfl, ldkf, False, out.ptr, c, b * h * wd, c, kf))
         return code
     dcol = ctx.scratch(4 * m * kk)
     code.append(_gemm(dyb, ldf, False, wb, ldk, True, dcol, kk, m, kk, f))
@@ -274,7 +347,8 @@ def bn_forward_instrs(ins, out: View, attrs, act: int = 0) -> list:
     code = []
     st = _bn_stats(x, attrs, ctx, code, update=True, mm=ins[3], mv=ins[4])
     gamma = None if attrs.get("fix_gamma", True) else ins[1].ptr
-    code.append(instr(L.OP_BN_APPLY, [x.ptr, st, gamma, ins[2].ptr, out.ptr], [m, c], act=act))
+    y16 = ctx.shadow_out(out.size) if c % 8 == 0 else None
+    code.append(instr(L.OP_BN_APPLY, [x.ptr, st, gamma, ins[2].ptr, out.ptr, y16], [m, c], act=act))
     return code
 
 
@@ -314,7 +388,8 @@ def _bn_lower_bwd(slot, env, out, attrs):
 
 def bn_backward_group(og: View, relu: bool, x: View, gamma: View, beta: View, attrs,
                       xnode, dx: Optional[View], dgamma: Optional[View],
-                      dbeta: Optional[View], dbias_conv: Optional[View] = None) -> list:
+                      dbeta: Optional[View], dbias_conv: Optional[View] = None,
+                      dx_node=None) -> list:
     """All requested BatchNorm gradients of one node in one pass pair (the
     executor's fusion of the sibling Backward nodes, optionally with the
     ReLU backward in front of them): one reduction that also writes dbeta /
@@ -334,9 +409,10 @@ def bn_backward_group(og: View, relu: bool, x: View, gamma: View, beta: View, at
                        1 if fix else 0, (g or 0) if relu else 0]))
     if dx is not None:
         dws = ctx.scratch(_reduce_ws(m, c))
+        dx16 = ctx.shadow_out(dx.size, dx_node) if (c % 8 == 0 and dx_node is not None) else None
         code.append(instr(L.OP_BN_BWD_DX, [og.ptr, x.ptr, st, sums, g, dx.ptr],
                           [m, c, rb or 0, dbias_conv.ptr if dbias_conv is not None else 0, dws,
-                           (g or 0) if relu else 0]))
+                           (g or 0) if relu else 0, dx16 or 0]))
     return code
 
 
@@ -421,7 +497,8 @@ def _pool_lower_fwd(ins, out, attrs):
     arg = _pool_argmax(ctx.node, x.shape, out.size, k, kind, ctx) if ctx.training else None
     if arg is not None:
         ctx.memo[("argmax_fwd", id(ctx.node))] = True
-    return [instr(L.OP_POOL_FWD, [x.ptr, out.ptr, arg], _geom(x.shape, k, s, p) + [int(full)],
+    y16 = ctx.shadow_out(out.size) if (x.shape[-1] % 8 == 0 and k[0] * k[1] <= 255) else None
+    return [instr(L.OP_POOL_FWD, [x.ptr, out.ptr, arg, y16], _geom(x.shape, k, s, p) + [int(full)],
                   act=kind)]
 
 
@@ -476,10 +553,12 @@ def _concat_infer(shapes, attrs):
 
 def _concat_lower_fwd(ins, out, attrs):
     rows, tot = prod(out.shape[:-1]), out.shape[-1]
+    ok16 = tot % 8 == 0 and all(x.shape[-1] % 4 == 0 for x in ins)
+    o16 = current_ctx().shadow_out(out.size) if ok16 else None
     code, off = [], 0
     for x in ins:
         c = x.shape[-1]
-        code.append(instr(L.OP_CHAN_COPY, [x.ptr, out.ptr], [rows, c, c, 0, tot, off]))
+        code.append(instr(L.OP_CHAN_COPY, [x.ptr, out.ptr, o16], [rows, c, c, 0, tot, off]))
         off += c
     return code
 

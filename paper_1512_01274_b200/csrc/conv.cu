@@ -411,7 +411,8 @@ __device__ __forceinline__ float4 bn_dx4(const float4& d, const float4& xv, cons
 __global__ void __launch_bounds__(kRedThreads)
 bn_dx_colsum_kernel(const float* dy, const float* __restrict__ x, const float* __restrict__ stats,
                     const float* __restrict__ sums, const float* __restrict__ gamma, float* dx,
-                    ReluMask rm, int64_t M, int C, int64_t rpc, double* __restrict__ ws) {
+                    ReluMask rm, int64_t M, int C, int64_t rpc, double* __restrict__ ws,
+                    __nv_bfloat16* __restrict__ dx16) {
   extern __shared__ double red[];  // [rpp][ct]
   const int C4 = C >> 2;
   const int ct4 = C4 < kRedThreads ? C4 : kRedThreads;
@@ -457,6 +458,12 @@ bn_dx_colsum_kernel(const float* dy, const float* __restrict__ x, const float* _
         acc[2] += o.z;
         acc[3] += o.w;
         reinterpret_cast<float4*>(dx)[(r + u * rpp) * C4 + c4] = o;
+        if (dx16) {
+          uint2 h;
+          h.x = pack_bf16(o.x, o.y);
+          h.y = pack_bf16(o.z, o.w);
+          reinterpret_cast<uint2*>(dx16)[(r + u * rpp) * C4 + c4] = h;
+        }
       }
     }
     for (; r < r1; r += rpp) {
@@ -469,6 +476,12 @@ bn_dx_colsum_kernel(const float* dy, const float* __restrict__ x, const float* _
       acc[2] += o.z;
       acc[3] += o.w;
       reinterpret_cast<float4*>(dx)[i] = o;
+      if (dx16) {
+        uint2 h;
+        h.x = pack_bf16(o.x, o.y);
+        h.y = pack_bf16(o.z, o.w);
+        reinterpret_cast<uint2*>(dx16)[i] = h;
+      }
     }
   }
   if (r_in < rpp) {
@@ -534,7 +547,8 @@ __global__ void colsum_finalize_kernel(const double* __restrict__ ws, int nchunk
 // y = (x - mean) * rstd * gamma + beta, then act; gamma == nullptr: fixed 1
 __global__ void bn_apply_kernel(const float* __restrict__ x, const float* __restrict__ stats,
                                 const float* __restrict__ gamma, const float* __restrict__ beta,
-                                float* __restrict__ y, int64_t M, int C, int act) {
+                                float* __restrict__ y, int64_t M, int C, int act,
+                                __nv_bfloat16* __restrict__ y16) {
   const int64_t total = M * C;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   if ((C & 3) == 0) {
@@ -563,6 +577,12 @@ __global__ void bn_apply_kernel(const float* __restrict__ x, const float* __rest
         pv[u] = act == MGX_ACT_RELU ? relu(t) : act_forward(act, t);
       }
       reinterpret_cast<float4*>(y)[i] = v;
+      if (y16) {
+        uint2 h;
+        h.x = pack_bf16(v.x, v.y);
+        h.y = pack_bf16(v.z, v.w);
+        reinterpret_cast<uint2*>(y16)[i] = h;
+      }
     }
   } else {
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
@@ -694,7 +714,8 @@ __global__ void pool_bwd_kernel(const float* __restrict__ x, const float* __rest
 // so the backward is a cheap gather: dx(h,w) = sum of dy over the windows
 // whose recorded argmax is (h,w), windows in ascending (oh, ow) order.
 __global__ void pool_fwd_vec_kernel(const float* __restrict__ x, float* __restrict__ y,
-                                    uint8_t* __restrict__ arg, Geom g, int type) {
+                                    uint8_t* __restrict__ arg, Geom g, int type,
+                                    __nv_bfloat16* __restrict__ y16) {
   const int C4 = g.C >> 2;
   const RowsIdx ri(C4);
   if (!ri.active) return;
@@ -742,6 +763,12 @@ __global__ void pool_fwd_vec_kernel(const float* __restrict__ x, float* __restri
       o = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
     }
     reinterpret_cast<float4*>(y)[idx] = o;
+    if (y16) {
+      uint2 h;
+      h.x = pack_bf16(o.x, o.y);
+      h.y = pack_bf16(o.z, o.w);
+      reinterpret_cast<uint2*>(y16)[idx] = h;
+    }
   }
 }
 
@@ -793,16 +820,23 @@ __global__ void pool_bwd_vec_kernel(const uint8_t* __restrict__ arg, const float
 // dst[r, doff + c] = src[r, soff + c] (Concat forward / backward slices)
 __global__ void chan_copy_kernel(const float* __restrict__ src, int64_t lds, int64_t soff,
                                  float* __restrict__ dst, int64_t ldd, int64_t doff, int64_t rows,
-                                 int64_t cols) {
+                                 int64_t cols, __nv_bfloat16* __restrict__ dst16) {
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   if (((cols | lds | soff | ldd | doff) & 3) == 0) {
     // rows x vectors launch shape
     const RowsIdx ri(static_cast<int>(cols / 4));
     if (!ri.active) return;
     const int64_t c = int64_t(ri.v) * 4;
-    for (int64_t r = ri.r; r < rows; r += ri.rstep)
-      *reinterpret_cast<float4*>(dst + r * ldd + doff + c) =
-          __ldg(reinterpret_cast<const float4*>(src + r * lds + soff + c));
+    for (int64_t r = ri.r; r < rows; r += ri.rstep) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(src + r * lds + soff + c));
+      *reinterpret_cast<float4*>(dst + r * ldd + doff + c) = v;
+      if (dst16) {
+        uint2 h;
+        h.x = pack_bf16(v.x, v.y);
+        h.y = pack_bf16(v.z, v.w);
+        *reinterpret_cast<uint2*>(dst16 + r * ldd + doff + c) = h;
+      }
+    }
   } else {
     const int64_t total = rows * cols;
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
@@ -921,18 +955,20 @@ extern "C" int mgx_bn_stats(const float* x, int64_t M, int64_t C, void* ws, floa
 }
 
 extern "C" int mgx_bn_apply(const float* x, const float* stats, const float* gamma,
-                            const float* beta, float* y, int64_t M, int64_t C, int act,
+                            const float* beta, float* y, int64_t M, int64_t C, int act, void* y16,
                             uintptr_t stream) {
   MGX_REQUIRE(x && stats && beta && y && M > 0 && C > 0, "mgx_bn_apply: bad arguments");
+  MGX_REQUIRE(!y16 || (C % 4 == 0 && mgx::aligned16(y16)), "mgx_bn_apply: bf16 copy needs C %% 4 == 0");
   if ((C & 3) == 0) {
     MGX_REQUIRE(mgx::aligned16(x) && mgx::aligned16(y), "mgx_bn_apply: unaligned tensors");
     mgx::conv::bn_apply_kernel<<<mgx::rows_grid(M, C / 4),
                                  mgx::kRowsThreads, 0,
                                  mgx::as_stream(stream)>>>(x, stats, gamma, beta, y, M,
-                                                           static_cast<int>(C), act);
+                                                           static_cast<int>(C), act,
+                                                           static_cast<__nv_bfloat16*>(y16));
   } else {
     mgx::conv::bn_apply_kernel<<<grid_for(M * C), 256, 0, mgx::as_stream(stream)>>>(
-        x, stats, gamma, beta, y, M, static_cast<int>(C), act);
+        x, stats, gamma, beta, y, M, static_cast<int>(C), act, nullptr);
   }
   MGX_LAUNCHED();
   return MGX_OK;
@@ -957,8 +993,9 @@ extern "C" int mgx_bn_bwd_reduce(const float* dy, const float* x, const float* s
 extern "C" int mgx_bn_bwd_dx(const float* dy, const float* x, const float* stats, const float* sums,
                              const float* gamma, float* dx, int64_t M, int64_t C,
                              const float* relu_gamma, const float* relu_beta, float* dsum,
-                             void* ws, uintptr_t stream) {
+                             void* ws, void* dx16, uintptr_t stream) {
   MGX_REQUIRE(dy && x && stats && sums && dx && M > 0 && C > 0, "mgx_bn_bwd_dx: bad arguments");
+  MGX_REQUIRE(!dx16 || (C % 4 == 0 && mgx::aligned16(dx16)), "mgx_bn_bwd_dx: bf16 copy needs C %% 4 == 0");
   const bool vec = (C % 4) == 0 && mgx::aligned16(dy) && mgx::aligned16(x) && mgx::aligned16(dx);
   cudaStream_t st = mgx::as_stream(stream);
   const mgx::conv::ReluMask rm{relu_gamma, relu_beta};
@@ -981,7 +1018,8 @@ extern "C" int mgx_bn_bwd_dx(const float* dy, const float* x, const float* stats
       wsd = static_cast<double*>(ws);
     }
     mgx::conv::bn_dx_colsum_kernel<<<grid, mgx::conv::kRedThreads, smem, st>>>(
-        dy, x, stats, sums, gamma, dx, rm, M, static_cast<int>(C), rpc, wsd);
+        dy, x, stats, sums, gamma, dx, rm, M, static_cast<int>(C), rpc, wsd,
+        static_cast<__nv_bfloat16*>(dx16));
     if (dsum)
       mgx::conv::colsum_finalize_kernel<<<static_cast<unsigned>(mgx::ceil_div(C, mgx::conv::kFinChannels)), 32 * mgx::conv::kFinChannels, 0, st>>>(
           static_cast<const double*>(ws), nchunk, static_cast<int>(C), 0, dsum, nullptr, nullptr, 0);
@@ -1012,7 +1050,7 @@ static bool pool_vec_ok(const Geom& g, const void* a, const void* b) {
 }
 
 extern "C" int mgx_pool_forward(const float* x, float* y, const int64_t* geom, int full, int type,
-                                void* argmax, uintptr_t stream) {
+                                void* argmax, void* y16, uintptr_t stream) {
   MGX_REQUIRE(x && y && geom && (type == 0 || type == 1), "mgx_pool_forward: bad arguments");
   Geom g = mgx::conv::decode(geom, full != 0);
   MGX_REQUIRE(g.Ho > 0 && g.Wo > 0, "mgx_pool_forward: bad geometry");
@@ -1020,9 +1058,11 @@ extern "C" int mgx_pool_forward(const float* x, float* y, const int64_t* geom, i
   if (pool_vec_ok(g, x, y) && g.kh * g.kw <= 255) {
     mgx::conv::pool_fwd_vec_kernel<<<mgx::rows_grid(int64_t(g.B) * g.Ho * g.Wo, g.C / 4),
                                      mgx::kRowsThreads, 0, st>>>(
-        x, y, type == 0 ? static_cast<uint8_t*>(argmax) : nullptr, g, type);
+        x, y, type == 0 ? static_cast<uint8_t*>(argmax) : nullptr, g, type,
+        static_cast<__nv_bfloat16*>(y16));
   } else {
     MGX_REQUIRE(!argmax || type != 0, "mgx_pool_forward: argmax needs C %% 4 == 0 and kh*kw <= 255");
+    MGX_REQUIRE(!y16, "mgx_pool_forward: a bf16 copy needs C %% 4 == 0");
     const int64_t n = int64_t(g.B) * g.Ho * g.Wo * g.C;
     mgx::conv::pool_fwd_kernel<<<grid_for(n), 256, 0, st>>>(x, y, g, type);
   }
@@ -1052,16 +1092,20 @@ extern "C" int mgx_pool_backward(const float* x, const float* y, const float* dy
 }
 
 extern "C" int mgx_chan_copy(const float* src, int64_t lds, int64_t soff, float* dst, int64_t ldd,
-                             int64_t doff, int64_t rows, int64_t cols, uintptr_t stream) {
+                             int64_t doff, int64_t rows, int64_t cols, void* dst16,
+                             uintptr_t stream) {
   MGX_REQUIRE(src && dst && rows >= 0 && cols >= 0, "mgx_chan_copy: bad arguments");
+  MGX_REQUIRE(!dst16 || (((cols | lds | soff | ldd | doff) & 3) == 0 && mgx::aligned16(dst16)),
+              "mgx_chan_copy: a bf16 copy needs 4-aligned columns");
   if (rows == 0 || cols == 0) return MGX_OK;
   if (((cols | lds | soff | ldd | doff) & 3) == 0)
     mgx::conv::chan_copy_kernel<<<mgx::rows_grid(rows, cols / 4),
                                   mgx::kRowsThreads, 0,
-                                  mgx::as_stream(stream)>>>(src, lds, soff, dst, ldd, doff, rows, cols);
+                                  mgx::as_stream(stream)>>>(src, lds, soff, dst, ldd, doff, rows, cols,
+                                                            static_cast<__nv_bfloat16*>(dst16));
   else
     mgx::conv::chan_copy_kernel<<<grid_for(rows * cols), 256, 0, mgx::as_stream(stream)>>>(
-        src, lds, soff, dst, ldd, doff, rows, cols);
+        src, lds, soff, dst, ldd, doff, rows, cols, nullptr);
   MGX_LAUNCHED();
   return MGX_OK;
 }

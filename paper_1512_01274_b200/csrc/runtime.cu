@@ -266,7 +266,8 @@ static int run_instr(const mgx_instr& in, cudaStream_t st) {
       return mgx_bn_stats(p0, d[0], d[1], in.ptr[1], p2, p3, static_cast<float*>(in.ptr[4]),
                           in.fattr[0], in.fattr[1], static_cast<int>(d[2]), s);
     case MGX_OP_BN_APPLY:
-      return mgx_bn_apply(p0, p1, p2, p3, static_cast<float*>(in.ptr[4]), d[0], d[1], in.act, s);
+      return mgx_bn_apply(p0, p1, p2, p3, static_cast<float*>(in.ptr[4]), d[0], d[1], in.act,
+                          in.ptr[5], s);
     case MGX_OP_BN_BWD_REDUCE:
       return mgx_bn_bwd_reduce(p0, p1, p2, d[0], d[1], in.ptr[3], static_cast<float*>(in.ptr[4]),
                                reinterpret_cast<float*>(d[2]), reinterpret_cast<float*>(d[3]),
@@ -276,12 +277,26 @@ static int run_instr(const mgx_instr& in, cudaStream_t st) {
       return mgx_bn_bwd_dx(p0, p1, p2, p3, static_cast<float*>(in.ptr[4]),
                            static_cast<float*>(in.ptr[5]), d[0], d[1],
                            reinterpret_cast<const float*>(d[5]), reinterpret_cast<const float*>(d[2]),
-                           reinterpret_cast<float*>(d[3]), reinterpret_cast<void*>(d[4]), s);
+                           reinterpret_cast<float*>(d[3]), reinterpret_cast<void*>(d[4]),
+                           reinterpret_cast<void*>(d[6]), s);
     case MGX_OP_POOL_FWD:
-      return mgx_pool_forward(p0, p1, d, static_cast<int>(d[7]), in.act, in.ptr[2], s);
+      return mgx_pool_forward(p0, p1, d, static_cast<int>(d[7]), in.act, in.ptr[2], in.ptr[3], s);
     case MGX_OP_POOL_BWD:
       return mgx_pool_backward(p0, p1, p2, p3, d, static_cast<int>(d[7]), in.act, in.ptr[4], s);
-    case MGX_OP_CHAN_COPY: return mgx_chan_copy(p0, d[2], d[3], p1, d[4], d[5], d[0], d[1], s);
+    case MGX_OP_CHAN_COPY:
+      return mgx_chan_copy(p0, d[2], d[3], p1, d[4], d[5], d[0], d[1], in.ptr[2], s);
+    case MGX_OP_GEMM_CONV: {
+      // dims: M, N, K, ldop, ldc, mode | splits << 8, B<<48|H<<32|W<<16|C,
+      // kh<<40|kw<<32|sh<<24|sw<<16|ph<<8|pw ; ptr0 src, ptr1 op
+      const int64_t a = d[6], w = d[7];
+      const int64_t geom[7] = {(a >> 48) & 0xFFFF, (a >> 32) & 0xFFFF, (a >> 16) & 0xFFFF,
+                               a & 0xFFFF, (((w >> 40) & 0xFF) << 16) | ((w >> 32) & 0xFF),
+                               (((w >> 24) & 0xFF) << 16) | ((w >> 16) & 0xFF),
+                               (((w >> 8) & 0xFF) << 16) | (w & 0xFF)};
+      return mgx_gemm_bf16_conv(static_cast<int>(d[5] & 0xFF), in.ptr[0], geom, in.ptr[1], d[3],
+                                p2, p3, d[4], d[0], d[1], d[2], in.act, static_cast<int>(d[5] >> 8),
+                                static_cast<float*>(in.ptr[4]), s);
+    }
     case MGX_OP_WFLIP: return mgx_weight_flip_bf16(p0, d[0], d[1], d[2], d[3], in.ptr[1], d[4], s);
     case MGX_OP_COLSUM: return mgx_colsum(p0, d[0], d[1], in.ptr[1], p2, s);
     case MGX_OP_GEMM_TC_EX:

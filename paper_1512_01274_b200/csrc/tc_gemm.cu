@@ -156,7 +156,7 @@ __device__ __forceinline__ void load_operand(uint8_t* dst, const CUtensorMap* ma
 }
 
 struct Sched {
-  int m_tiles, n_tiles, splits, kps, nk;
+  int m_tiles, n_tiles, splits, kps, nk, kext;
   __device__ __forceinline__ void tile(int t, int* m0, int* n0, int* z, int* kb0, int* nkb) const {
     const int per_split = m_tiles * n_tiles;
     *z = t / per_split;
@@ -168,14 +168,38 @@ struct Sched {
   }
 };
 
+// Implicit-GEMM operand: G[m, k] = src[b, oh*sh - ph + i, ow*sw - pw + j, c]
+// for output pixel m = (b, oh, ow) and k = (i*kw + j)*C + c, zero outside
+// the input or beyond K = kh*kw*C; src is a compact bf16 NHWC tensor with
+// C % 8 == 0, so 8 consecutive k are one 16-byte load.
+struct Gather {
+  const __nv_bfloat16* src;
+  int B, H, W, C, kh, kw, sh, sw, ph, pw, Ho, Wo;
+};
+
+constexpr int kGatherThreads = 128;  // warps 6..9
+
+__device__ __forceinline__ void cp_async16_zfill(uint32_t dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
+               "r"(valid ? 16 : 0)
+               : "memory");
+}
+
+// GM: 0 plain (both operands by TMA); 1 A gathered (K-major: forward /
+// data gradient of a convolution); 2 B gathered (MN-major: weight gradient)
+template <int GM>
+constexpr int threads_for() {
+  return GM ? kThreads + kGatherThreads : kThreads;
+}
+
 // ACTK: 0 no activation, 1 relu, 2 any (runtime code; cold path)
-template <bool A_MN, bool B_MN, int BN, int ACTK>
-__global__ void __launch_bounds__(kThreads, 1)
+template <bool A_MN, bool B_MN, int BN, int ACTK, int GM>
+__global__ void __launch_bounds__(threads_for<GM>(), 1)
 tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
                     const __grid_constant__ CUtensorMap map_b,
                     const __grid_constant__ CUtensorMap map_c, const float* __restrict__ bias,
                     float* __restrict__ C, int ldc, int M, int N, int act, Sched sc,
-                    int64_t split_stride, int use_tma_store) {
+                    int64_t split_stride, int use_tma_store, const __grid_constant__ Gather ga) {
   using G = Cfg<BN>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -193,7 +217,8 @@ tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
     for (int s = 0; s < G::kStages; ++s) {
-      mbar_init(&full[s], 1);
+      // gathered operand: the 128 gather threads arrive (cp.async noinc)
+      mbar_init(&full[s], GM ? 1 + kGatherThreads : 1);
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -226,9 +251,10 @@ tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
           const uint32_t ph = (it / G::kStages) & 1;
           mbar_wait(&empty[s], ph ^ 1);
           uint8_t* sa = smem + s * G::kStageBytes;
-          mbar_expect_tx(&full[s], G::kStageBytes);
-          load_operand<A_MN, BM>(sa, &map_a, &full[s], (kb0 + kb) * BK, m0);
-          load_operand<B_MN, BN>(sa + G::kABytes, &map_b, &full[s], (kb0 + kb) * BK, n0);
+          mbar_expect_tx(&full[s], GM == 1 ? G::kBBytes : GM == 2 ? G::kABytes : G::kStageBytes);
+          if (GM != 1) load_operand<A_MN, BM>(sa, &map_a, &full[s], (kb0 + kb) * BK, m0);
+          if (GM != 2)
+            load_operand<B_MN, BN>(sa + G::kABytes, &map_b, &full[s], (kb0 + kb) * BK, n0);
         }
       }
     }
@@ -249,6 +275,8 @@ tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
           const uint32_t ph = (it / G::kStages) & 1;
           mbar_wait(&full[s], ph);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          // cp.async (generic proxy) writes -> tcgen05.mma (async proxy) reads
+          if (GM) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           const uint8_t* sa = smem + s * G::kStageBytes;
           const uint64_t adesc = A_MN ? smem_desc_mn_sw128(sa) : smem_desc_sw128(sa);
           const uint64_t bdesc = B_MN ? smem_desc_mn_sw128(sa + G::kABytes)
@@ -266,7 +294,107 @@ tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
         umma_commit(&tfull[acc]);
       }
     }
-  } else {
+  } else if (GM && warp >= 6) {
+    // ---------------- gather producers (implicit GEMM): cp.async 16-byte
+    // chunks straight into the 128B-swizzled operand tile, zero-filled
+    // outside the input; the mbarrier arrival fires when they land
+    const int g = threadIdx.x - kThreads;
+    int it = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      int m0, nt, z, kb0, nkb;
+      sc.tile(t, &m0, &nt, &z, &kb0, &nkb);
+      const int n0 = nt * BN;
+      if (GM == 1) {
+        // A tile (K-major): lanes cover the 8 16-byte chunks of a 128-byte
+        // row, so a warp instruction fills 4 whole rows (coalesced); thread
+        // (q = g & 7, r0 = g >> 3) owns rows r0 + 16*i, i < 8
+        const int q = g & 7, r0 = g >> 3;
+        const int hw = ga.Ho * ga.Wo;
+        int hb[8], wb[8];
+        const __nv_bfloat16* img[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int m = m0 + r0 + 16 * i;
+          const int b = m < M ? m / hw : -1;
+          const int rem = m - (b < 0 ? 0 : b) * hw;
+          const int oh = rem / ga.Wo, ow = rem - (rem / ga.Wo) * ga.Wo;
+          hb[i] = b < 0 ? -(1 << 20) : oh * ga.sh - ga.ph;  // invalid row: always out of range
+          wb[i] = ow * ga.sw - ga.pw;
+          img[i] = ga.src + int64_t(b < 0 ? 0 : b) * ga.H * ga.W * ga.C;
+        }
+        const int K = ga.kh * ga.kw * ga.C;
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % G::kStages;
+          const uint32_t ph = (it / G::kStages) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          const uint32_t tile = smem_u32(smem + s * G::kStageBytes);
+          const int k = (kb0 + kb) * BK + q * 8;
+          const int tap = k / ga.C, c = k - tap * ga.C;
+          const int ti = tap / ga.kw, tj = tap - ti * ga.kw;
+          const bool kv = k < K;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int r = r0 + 16 * i;
+            const int h = hb[i] + ti, w = wb[i] + tj;
+            const bool v = kv && h >= 0 && h < ga.H && w >= 0 && w < ga.W;
+            const void* src = v ? static_cast<const void*>(img[i] + (int64_t(h) * ga.W + w) * ga.C + c)
+                                : static_cast<const void*>(ga.src);
+            cp_async16_zfill(tile + uint32_t(r * 128 + ((q ^ (r & 7)) << 4)), src, v);
+          }
+          asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(
+                           smem_u32(&full[s]))
+                       : "memory");
+        }
+      } else {
+        // B tile (MN-major): 64 K rows (pixels) x BN columns in 64-column
+        // groups of 128-byte rows; lanes cover the 8 chunks of a row; thread
+        // (q = g & 7, r0 = g >> 3) owns rows r0 + 16*i (i < 4) of every group
+        const int q = g & 7, r0 = g >> 3;
+        constexpr int NG = BN / 64;
+        int gi[NG], gj[NG], gc[NG];
+#pragma unroll
+        for (int cg = 0; cg < NG; ++cg) {
+          const int n = n0 + cg * 64 + q * 8;
+          const int tap = n / ga.C;
+          gc[cg] = n < N ? n - tap * ga.C : -1;
+          gi[cg] = tap / ga.kw;
+          gj[cg] = tap - gi[cg] * ga.kw;
+        }
+        const int hw = ga.Ho * ga.Wo;
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % G::kStages;
+          const uint32_t ph = (it / G::kStages) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          const uint32_t tile = smem_u32(smem + s * G::kStageBytes + G::kABytes);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int kr = r0 + 16 * i;
+            const int m = (kb0 + kb) * BK + kr;
+            const bool mv = m < sc.kext;
+            const int b = mv ? m / hw : 0;
+            const int rem = m - b * hw;
+            const int oh = rem / ga.Wo, ow = rem - (rem / ga.Wo) * ga.Wo;
+            const int hb = oh * ga.sh - ga.ph, wb = ow * ga.sw - ga.pw;
+            const __nv_bfloat16* img = ga.src + int64_t(b) * ga.H * ga.W * ga.C;
+#pragma unroll
+            for (int cg = 0; cg < NG; ++cg) {
+              const int h = hb + gi[cg], w = wb + gj[cg];
+              const bool v = mv && gc[cg] >= 0 && h >= 0 && h < ga.H && w >= 0 && w < ga.W;
+              const void* src =
+                  v ? static_cast<const void*>(img + (int64_t(h) * ga.W + w) * ga.C + gc[cg])
+                    : static_cast<const void*>(ga.src);
+              cp_async16_zfill(tile + uint32_t(cg * kMnChunkBytes + kr * 128 + ((q ^ (kr & 7)) << 4)),
+                               src, v);
+            }
+          }
+          asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(
+                           smem_u32(&full[s]))
+                       : "memory");
+        }
+      }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+  } else if (warp >= 2) {
     // ---------------- epilogue warps: TMEM lanes 32*(warp%4) .. +31
     const int ew = warp - 2;
     const int lane_base = (warp & 3) * 32;
@@ -495,45 +623,56 @@ static int make_map(CUtensorMap* map, const void* base, int64_t rows, int64_t K,
   return encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, base, rows, K, ld * 2, 64, BK);
 }
 
-template <bool A_MN, bool B_MN, int BN, int ACTK>
+template <bool A_MN, bool B_MN, int BN, int ACTK, int GM>
 static int launch_act(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
                       int grid, const float* bias, float* C, int ldc, int M, int N, int act,
-                      const Sched& sc, int64_t split_stride, int tma_store, cudaStream_t st) {
+                      const Sched& sc, int64_t split_stride, int tma_store, const Gather& ga,
+                      cudaStream_t st) {
   using G = Cfg<BN>;
   static bool configured = false;
   if (!configured) {
-    MGX_CUDA(cudaFuncSetAttribute(tc_gemm_bf16_kernel<A_MN, B_MN, BN, ACTK>,
+    MGX_CUDA(cudaFuncSetAttribute(tc_gemm_bf16_kernel<A_MN, B_MN, BN, ACTK, GM>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, G::kSmemBytes));
     configured = true;
   }
-  tc_gemm_bf16_kernel<A_MN, B_MN, BN, ACTK><<<grid, kThreads, G::kSmemBytes, st>>>(
-      ma, mb, mc, bias, C, ldc, M, N, act, sc, split_stride, tma_store);
+  tc_gemm_bf16_kernel<A_MN, B_MN, BN, ACTK, GM><<<grid, threads_for<GM>(), G::kSmemBytes, st>>>(
+      ma, mb, mc, bias, C, ldc, M, N, act, sc, split_stride, tma_store, ga);
   MGX_LAUNCHED();
   return MGX_OK;
 }
 
-template <bool A_MN, bool B_MN, int BN>
-static int launch_variant(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
-                          int grid, const float* bias, float* C, int ldc, int M, int N, int act,
-                          const Sched& sc, int64_t split_stride, int tma_store, cudaStream_t st) {
-  if (act == MGX_ACT_NONE)
-    return launch_act<A_MN, B_MN, BN, 0>(ma, mb, mc, grid, bias, C, ldc, M, N, act, sc, split_stride, tma_store, st);
-  if (act == MGX_ACT_RELU)
-    return launch_act<A_MN, B_MN, BN, 1>(ma, mb, mc, grid, bias, C, ldc, M, N, act, sc, split_stride, tma_store, st);
-  return launch_act<A_MN, B_MN, BN, 2>(ma, mb, mc, grid, bias, C, ldc, M, N, act, sc, split_stride, tma_store, st);
+struct Launch {
+  CUtensorMap ma, mb, mc;
+  int grid;
+  const float* bias;
+  float* C;
+  int ldc, M, N, act;
+  Sched sc;
+  int64_t sstride;
+  int tma;
+  Gather ga;
+};
+
+template <bool A_MN, bool B_MN, int BN, int GM>
+static int launch_acts(const Launch& l, cudaStream_t st) {
+  if (l.act == MGX_ACT_NONE)
+    return launch_act<A_MN, B_MN, BN, 0, GM>(l.ma, l.mb, l.mc, l.grid, l.bias, l.C, l.ldc, l.M, l.N,
+                                             l.act, l.sc, l.sstride, l.tma, l.ga, st);
+  if (l.act == MGX_ACT_RELU)
+    return launch_act<A_MN, B_MN, BN, 1, GM>(l.ma, l.mb, l.mc, l.grid, l.bias, l.C, l.ldc, l.M, l.N,
+                                             l.act, l.sc, l.sstride, l.tma, l.ga, st);
+  return launch_act<A_MN, B_MN, BN, 2, GM>(l.ma, l.mb, l.mc, l.grid, l.bias, l.C, l.ldc, l.M, l.N,
+                                           l.act, l.sc, l.sstride, l.tma, l.ga, st);
 }
 
 template <int BN>
-static int launch_bn(int a_mn, int b_mn, const CUtensorMap& ma, const CUtensorMap& mb,
-                     const CUtensorMap& mc, int grid, const float* bias, float* C, int ldc, int M,
-                     int N, int act, const Sched& sc, int64_t sstride, int tma, cudaStream_t st) {
-  if (!a_mn && !b_mn)
-    return launch_variant<false, false, BN>(ma, mb, mc, grid, bias, C, ldc, M, N, act, sc, sstride, tma, st);
-  if (!a_mn && b_mn)
-    return launch_variant<false, true, BN>(ma, mb, mc, grid, bias, C, ldc, M, N, act, sc, sstride, tma, st);
-  if (a_mn && !b_mn)
-    return launch_variant<true, false, BN>(ma, mb, mc, grid, bias, C, ldc, M, N, act, sc, sstride, tma, st);
-  return launch_variant<true, true, BN>(ma, mb, mc, grid, bias, C, ldc, M, N, act, sc, sstride, tma, st);
+static int launch_bn(int a_mn, int b_mn, int gm, const Launch& l, cudaStream_t st) {
+  if (gm == 1) return launch_acts<false, false, BN, 1>(l, st);  // implicit A, B K-major
+  if (gm == 2) return launch_acts<true, true, BN, 2>(l, st);    // A MN-major, implicit B
+  if (!a_mn && !b_mn) return launch_acts<false, false, BN, 0>(l, st);
+  if (!a_mn && b_mn) return launch_acts<false, true, BN, 0>(l, st);
+  if (a_mn && !b_mn) return launch_acts<true, false, BN, 0>(l, st);
+  return launch_acts<true, true, BN, 0>(l, st);
 }
 
 static int auto_splits(int64_t tiles, int64_t nk) {
@@ -548,17 +687,23 @@ static int pick_bn(int64_t N) { return N <= 64 ? 64 : 128; }
 }  // namespace tc
 }  // namespace mgx
 
-extern "C" int mgx_gemm_bf16_tc_ex(const void* A, int64_t lda, int a_mn, const void* B,
-                                   int64_t ldb, int b_mn, const float* bias, float* C, int64_t ldc,
-                                   int64_t M, int64_t N, int64_t K, int act, int splits,
-                                   float* workspace, uintptr_t stream) {
-  using namespace mgx::tc;
-  MGX_REQUIRE(A && B && C && M > 0 && N > 0 && K > 0, "mgx_gemm_bf16_tc: bad arguments");
-  MGX_REQUIRE(lda % 8 == 0 && ldb % 8 == 0,
+namespace mgx {
+namespace tc {
+
+// shared implementation: gm 0 plain, 1 implicit A (ga describes it), 2
+// implicit B
+static int gemm_impl(const void* A, int64_t lda, int a_mn, const void* B, int64_t ldb, int b_mn,
+                     const float* bias, float* C, int64_t ldc, int64_t M, int64_t N, int64_t K,
+                     int act, int splits, float* workspace, int gm, const Gather& ga,
+                     cudaStream_t st) {
+  MGX_REQUIRE(C && M > 0 && N > 0 && K > 0, "mgx_gemm_bf16_tc: bad arguments");
+  MGX_REQUIRE((gm == 1 || A) && (gm == 2 || B), "mgx_gemm_bf16_tc: missing operand");
+  MGX_REQUIRE((gm == 1 || lda % 8 == 0) && (gm == 2 || ldb % 8 == 0),
               "mgx_gemm_bf16_tc: leading dimensions must be multiples of 8");
-  MGX_REQUIRE(lda >= (a_mn ? M : K) && ldb >= (b_mn ? N : K),
+  MGX_REQUIRE((gm == 1 || lda >= (a_mn ? M : K)) && (gm == 2 || ldb >= (b_mn ? N : K)),
               "mgx_gemm_bf16_tc: leading dimension smaller than the operand row");
-  MGX_REQUIRE(mgx::aligned16(A) && mgx::aligned16(B), "mgx_gemm_bf16_tc: operands not 16-byte aligned");
+  MGX_REQUIRE((gm == 1 || mgx::aligned16(A)) && (gm == 2 || mgx::aligned16(B)),
+              "mgx_gemm_bf16_tc: operands not 16-byte aligned");
   MGX_REQUIRE(M < (1ll << 31) && N < (1ll << 31) && K < (1ll << 31) && ldc < (1ll << 31),
               "mgx_gemm_bf16_tc: dimensions exceed 2^31");
   MGX_REQUIRE(splits >= 0, "mgx_gemm_bf16_tc: negative split count");
@@ -571,38 +716,88 @@ extern "C" int mgx_gemm_bf16_tc_ex(const void* A, int64_t lda, int a_mn, const v
   int kps = static_cast<int>(mgx::ceil_div(nk, splits));
   splits = static_cast<int>(mgx::ceil_div(nk, kps));
   MGX_REQUIRE(int64_t(splits) * M < (1ll << 31), "mgx_gemm_bf16_tc: split workspace too tall");
-  CUtensorMap ma, mb, mc;
-  MGX_TRY(make_map(&ma, A, M, K, lda, a_mn != 0, BM));
-  MGX_TRY(make_map(&mb, B, N, K, ldb, b_mn != 0, bn));
+  Launch l;
+  std::memset(&l, 0, sizeof(l));
+  if (gm != 1) MGX_TRY(make_map(&l.ma, A, M, K, lda, a_mn != 0, BM));
+  if (gm != 2) MGX_TRY(make_map(&l.mb, B, N, K, ldb, b_mn != 0, bn));
   float* out = splits == 1 ? C : workspace;
   const int64_t oldc = splits == 1 ? ldc : N;
   // TMA store needs a 16-byte row pitch and base; the map spans all splits
   // (partial 32-row boxes of a split would spill into the next split's rows)
-  const int tma = (oldc % 4 == 0) && mgx::aligned16(out) && (splits == 1 || M % 32 == 0);
-  if (tma) {
-    MGX_TRY(mgx::tc::encode(&mc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, out, N, int64_t(splits) * M,
+  l.tma = (oldc % 4 == 0) && mgx::aligned16(out) && (splits == 1 || M % 32 == 0);
+  if (l.tma)
+    MGX_TRY(mgx::tc::encode(&l.mc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, out, N, int64_t(splits) * M,
                             oldc * 4, 32, 32));
-  } else {
-    std::memset(&mc, 0, sizeof(mc));
-  }
-  Sched sc{static_cast<int>(m_tiles), static_cast<int>(n_tiles), splits, kps, static_cast<int>(nk)};
+  l.sc = Sched{static_cast<int>(m_tiles), static_cast<int>(n_tiles), splits, kps,
+               static_cast<int>(nk), static_cast<int>(K)};
   const int64_t total = m_tiles * n_tiles * splits;
-  const int grid = static_cast<int>(total < mgx::kNumSMs ? total : mgx::kNumSMs);
-  cudaStream_t st = mgx::as_stream(stream);
-  const int64_t sstride = M * N;
-  const float* ebias = splits == 1 ? bias : nullptr;
-  const int eact = splits == 1 ? act : 0;
-  int rc = bn == 64 ? launch_bn<64>(a_mn, b_mn, ma, mb, mc, grid, ebias, out, static_cast<int>(oldc),
-                                    static_cast<int>(M), static_cast<int>(N), eact, sc, sstride, tma, st)
-                    : launch_bn<128>(a_mn, b_mn, ma, mb, mc, grid, ebias, out, static_cast<int>(oldc),
-                                     static_cast<int>(M), static_cast<int>(N), eact, sc, sstride, tma, st);
+  l.grid = static_cast<int>(total < mgx::kNumSMs ? total : mgx::kNumSMs);
+  l.sstride = M * N;
+  l.bias = splits == 1 ? bias : nullptr;
+  l.act = splits == 1 ? act : 0;
+  l.C = out;
+  l.ldc = static_cast<int>(oldc);
+  l.M = static_cast<int>(M);
+  l.N = static_cast<int>(N);
+  l.ga = ga;
+  int rc = bn == 64 ? launch_bn<64>(a_mn, b_mn, gm, l, st) : launch_bn<128>(a_mn, b_mn, gm, l, st);
   if (rc != MGX_OK || splits == 1) return rc;
   int64_t blocks = mgx::ceil_div(M * N, 256);
   if (blocks > 148 * 8) blocks = 148 * 8;
-  splitk_reduce_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(workspace, splits, sstride,
+  splitk_reduce_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(workspace, splits, l.sstride,
                                                                       bias, C, ldc, M, N, act);
   MGX_LAUNCHED();
   return MGX_OK;
+}
+
+}  // namespace tc
+}  // namespace mgx
+
+extern "C" int mgx_gemm_bf16_tc_ex(const void* A, int64_t lda, int a_mn, const void* B,
+                                   int64_t ldb, int b_mn, const float* bias, float* C, int64_t ldc,
+                                   int64_t M, int64_t N, int64_t K, int act, int splits,
+                                   float* workspace, uintptr_t stream) {
+  mgx::tc::Gather none;
+  std::memset(&none, 0, sizeof(none));
+  return mgx::tc::gemm_impl(A, lda, a_mn, B, ldb, b_mn, bias, C, ldc, M, N, K, act, splits,
+                            workspace, 0, none, mgx::as_stream(stream));
+}
+
+extern "C" int mgx_gemm_bf16_conv(int mode, const void* src, const int64_t* geom, const void* op,
+                                  int64_t ldop, const float* bias, float* C, int64_t ldc,
+                                  int64_t M, int64_t N, int64_t K, int act, int splits,
+                                  float* workspace, uintptr_t stream) {
+  using namespace mgx::tc;
+  MGX_REQUIRE(src && geom && op && (mode == 1 || mode == 2), "mgx_gemm_bf16_conv: bad arguments");
+  MGX_REQUIRE(mgx::aligned16(src), "mgx_gemm_bf16_conv: source not 16-byte aligned");
+  Gather ga;
+  ga.src = static_cast<const __nv_bfloat16*>(src);
+  ga.B = static_cast<int>(geom[0]);
+  ga.H = static_cast<int>(geom[1]);
+  ga.W = static_cast<int>(geom[2]);
+  ga.C = static_cast<int>(geom[3]);
+  ga.kh = static_cast<int>(geom[4] >> 16);
+  ga.kw = static_cast<int>(geom[4] & 0xFFFF);
+  ga.sh = static_cast<int>(geom[5] >> 16);
+  ga.sw = static_cast<int>(geom[5] & 0xFFFF);
+  ga.ph = static_cast<int>(geom[6] >> 16);
+  ga.pw = static_cast<int>(geom[6] & 0xFFFF);
+  ga.Ho = (ga.H + 2 * ga.ph - ga.kh) / ga.sh + 1;
+  ga.Wo = (ga.W + 2 * ga.pw - ga.kw) / ga.sw + 1;
+  MGX_REQUIRE(ga.C % 8 == 0 && ga.C > 0 && ga.Ho > 0 && ga.Wo > 0 && ga.B > 0,
+              "mgx_gemm_bf16_conv: the gathered tensor needs C %% 8 == 0");
+  const int64_t pixels = int64_t(ga.B) * ga.Ho * ga.Wo;
+  const int64_t kconv = int64_t(ga.kh) * ga.kw * ga.C;
+  if (mode == 1) {
+    // C[pixels, N] = gather(src)[pixels, kconv] . op[N, kconv]^T
+    MGX_REQUIRE(M == pixels && K == kconv, "mgx_gemm_bf16_conv: M/K do not match the geometry");
+    return gemm_impl(nullptr, 0, 0, op, ldop, 0, bias, C, ldc, M, N, K, act, splits, workspace, 1,
+                     ga, mgx::as_stream(stream));
+  }
+  // C[M, kconv] = op[pixels, M]^T (MN-major) . gather(src)[pixels, kconv]
+  MGX_REQUIRE(K == pixels && N == kconv, "mgx_gemm_bf16_conv: N/K do not match the geometry");
+  return gemm_impl(op, ldop, 1, nullptr, 0, 1, bias, C, ldc, M, N, K, act, splits, workspace, 2,
+                   ga, mgx::as_stream(stream));
 }
 
 extern "C" int mgx_gemm_bf16_tc(const void* A, int64_t lda, const void* B, int64_t ldb,

@@ -138,6 +138,12 @@ def instr_cost(ins: L.Instr) -> tuple:
     if op == L.OP_GEMM_TC_EX:
         m, n, k = d[0], d[1], d[2]
         return 2 * (m * k + n * k) + 4 * m * n + (4 * n if has[2] else 0), 2 * m * n * k
+    if op == L.OP_GEMM_CONV:  # implicit GEMM: the gathered source counted once
+        m, n, k = d[0], d[1], d[2]
+        a, w = d[6], d[7]
+        src = 2 * ((a >> 48) & 0xFFFF) * ((a >> 32) & 0xFFFF) * ((a >> 16) & 0xFFFF) * (a & 0xFFFF)
+        opb = 2 * (n * k if (d[5] & 0xFF) == 1 else m * k)
+        return src + opb + 4 * m * n + (4 * n if has[2] else 0), 2 * m * n * k
     if op == L.OP_IM2COL:  # reads the input once, writes the bf16 col matrix
         b, h, w, c = d[0], d[1], d[2], d[3]
         kh, kw, sh, sw, ph, pw = d[4] >> 16, d[4] & 0xFFFF, d[5] >> 16, d[5] & 0xFFFF, d[6] >> 16, d[6] & 0xFFFF
@@ -216,11 +222,36 @@ class LowerCtx:
         self.writes: List[tuple] = []   # ... and written by it
         self.memo = _Memo(self)
         self.node = None
+        # implicit-GEMM operands: ids of nodes whose outputs feed a
+        # convolution (set by the executor); out_node = the node whose
+        # output the current lowering writes
+        self.want_shadow: set = set()
+        self.out_node = None
 
     def begin_op(self, node) -> None:
         self.node = node
+        self.out_node = node
         self._op_off = 0
         self.reads, self.writes = [], []
+
+    def shadow_out(self, elems: int, node=None) -> Optional[int]:
+        """A compact bf16 copy of the output of ``node`` (default: the node
+        being lowered) when a convolution consumes it: the producer writes
+        it in the same pass, the convolution gathers from it."""
+        node = node if node is not None else self.out_node
+        if node is None or id(node) not in self.want_shadow:
+            return None
+        key = ("shadow", id(node))
+        ptr = self.memo.get(key)
+        if ptr is None:
+            ptr = self.persistent(2 * elems)
+            self.memo[key] = ptr
+        return ptr
+
+    def shadow_of(self, node) -> Optional[int]:
+        if node is None:
+            return None
+        return self.memo.get(("shadow", id(node)))
 
     def _al(self, n: int) -> int:
         return -(-max(int(n), 1) // self.ALIGN) * self.ALIGN

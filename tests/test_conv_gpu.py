@@ -151,19 +151,23 @@ def test_batchnorm_kernels(cuda, m, c, fix_gamma):
     gp = None if fix_gamma else gd.data_ptr()
     L.call("mgx_bn_stats", xd.data_ptr(), m, c, ws.data_ptr(), st.data_ptr(), mm.data_ptr(),
            mv.data_ptr(), 1e-3, 0.9, 0, 0)
-    L.call("mgx_bn_apply", xd.data_ptr(), st.data_ptr(), gp, bd.data_ptr(), y.data_ptr(), m, c, 0, 0)
+    y16 = torch.empty(m, c, dtype=torch.bfloat16, device="cuda") if c % 4 == 0 else None
+    L.call("mgx_bn_apply", xd.data_ptr(), st.data_ptr(), gp, bd.data_ptr(), y.data_ptr(), m, c, 0,
+           y16.data_ptr() if y16 is not None else None, 0)
     L.call("mgx_bn_bwd_reduce", dyd.data_ptr(), xd.data_ptr(), st.data_ptr(), m, c, ws.data_ptr(),
            sums.data_ptr(), None, None, 0, None, None, 0)
     L.call("mgx_bn_bwd_dx", dyd.data_ptr(), xd.data_ptr(), st.data_ptr(), sums.data_ptr(), gp,
-           dx.data_ptr(), m, c, None, None, None, ws.data_ptr(), 0)
+           dx.data_ptr(), m, c, None, None, None, ws.data_ptr(), None, 0)
     torch.cuda.synchronize()
     if c % 4 == 0:  # fused dx + per-channel sum of dx
         dx2 = torch.empty(m, c, device="cuda")
         dsum = torch.empty(c, device="cuda")
+        dx16 = torch.empty(m, c, dtype=torch.bfloat16, device="cuda")
         L.call("mgx_bn_bwd_dx", dyd.data_ptr(), xd.data_ptr(), st.data_ptr(), sums.data_ptr(), gp,
-               dx2.data_ptr(), m, c, None, None, dsum.data_ptr(), ws.data_ptr(), 0)
+               dx2.data_ptr(), m, c, None, None, dsum.data_ptr(), ws.data_ptr(), dx16.data_ptr(), 0)
         torch.cuda.synchronize()
         assert torch.equal(dx2, dx)
+        assert torch.equal(dx16, dx.to(torch.bfloat16))
         # sum_rows(dx) cancels to ~0: compare against the summed magnitude
         mag = float(dx.double().abs().sum(0).max())
         np.testing.assert_allclose(dsum.cpu().numpy(), dx.double().sum(0).cpu().numpy(),
@@ -174,6 +178,8 @@ def test_batchnorm_kernels(cuda, m, c, fix_gamma):
     yr, mean, var = oc.batchnorm(xr, gr, br, 1e-3, fix_gamma)
     (yr * dyd.double().cpu()).sum().backward()
     np.testing.assert_allclose(y.cpu().numpy(), yr.detach().numpy(), rtol=1e-5, atol=2e-5)
+    if y16 is not None:  # the bf16 copy written in the same pass
+        assert torch.equal(y16, y.to(torch.bfloat16))
     np.testing.assert_allclose(dx.cpu().numpy(), xr.grad.numpy(), rtol=1e-4, atol=1e-5)
     np.testing.assert_allclose(sums[:c].cpu().numpy(), br.grad.numpy(), rtol=1e-5, atol=1e-4)
     if not fix_gamma:
@@ -220,10 +226,14 @@ def test_pooling_kernels(cuda, case, ties, use_argmax):
     t = 0 if kind == "max" else 1
     arg = torch.zeros(y.numel(), dtype=torch.uint8, device="cuda") if use_argmax else None
     argp = arg.data_ptr() if arg is not None else None
-    L.call("mgx_pool_forward", xd.data_ptr(), y.data_ptr(), _ptr(geom), 0, t, argp, 0)
+    y16 = torch.empty(*yr.shape, dtype=torch.bfloat16, device="cuda") if shape[3] % 4 == 0 else None
+    L.call("mgx_pool_forward", xd.data_ptr(), y.data_ptr(), _ptr(geom), 0, t, argp,
+           y16.data_ptr() if y16 is not None else None, 0)
     L.call("mgx_pool_backward", xd.data_ptr(), y.data_ptr(), dyd.data_ptr(), dx.data_ptr(),
            _ptr(geom), 0, t, argp, 0)
     torch.cuda.synchronize()
+    if y16 is not None:
+        assert torch.equal(y16, y.to(torch.bfloat16))
     if kind == "max":
         np.testing.assert_array_equal(y.cpu().numpy(), yr.detach().float().numpy())
     else:
@@ -238,10 +248,19 @@ def test_chan_copy_and_colsum(cuda):
     a = torch.randn(37, 12, device="cuda")
     b = torch.randn(37, 5, device="cuda")
     out = torch.zeros(37, 17, device="cuda")
-    L.call("mgx_chan_copy", a.data_ptr(), 12, 0, out.data_ptr(), 17, 0, 37, 12, 0)
-    L.call("mgx_chan_copy", b.data_ptr(), 5, 0, out.data_ptr(), 17, 12, 37, 5, 0)
+    L.call("mgx_chan_copy", a.data_ptr(), 12, 0, out.data_ptr(), 17, 0, 37, 12, None, 0)
+    L.call("mgx_chan_copy", b.data_ptr(), 5, 0, out.data_ptr(), 17, 12, 37, 5, None, 0)
     torch.cuda.synchronize()
     assert torch.equal(out, torch.cat([a, b], dim=1))
+    # channel-aligned concat with its bf16 copy
+    a2, b2 = torch.randn(37, 16, device="cuda"), torch.randn(37, 24, device="cuda")
+    o2 = torch.zeros(37, 40, device="cuda")
+    o16 = torch.zeros(37, 40, dtype=torch.bfloat16, device="cuda")
+    L.call("mgx_chan_copy", a2.data_ptr(), 16, 0, o2.data_ptr(), 40, 0, 37, 16, o16.data_ptr(), 0)
+    L.call("mgx_chan_copy", b2.data_ptr(), 24, 0, o2.data_ptr(), 40, 16, 37, 24, o16.data_ptr(), 0)
+    torch.cuda.synchronize()
+    assert torch.equal(o2, torch.cat([a2, b2], dim=1))
+    assert torch.equal(o16, o2.to(torch.bfloat16))
     x = torch.randn(5000, 24, device="cuda")
     wsb = ctypes.c_int64()
     L.call("mgx_reduce_workspace_bytes", 5000, 24, ctypes.byref(wsb))
@@ -284,7 +303,7 @@ def test_batchnorm_backward_with_fused_relu(cuda, m, c, fix_gamma):
            beta.data_ptr(), 0)
     L.call("mgx_bn_bwd_dx", og.data_ptr(), x.data_ptr(), st.data_ptr(), sums.data_ptr(), gp,
            dx.data_ptr(), m, c, gp, beta.data_ptr(), dsum.data_ptr() if c % 4 == 0 else None,
-           ws.data_ptr(), 0)
+           ws.data_ptr(), None, 0)
     torch.cuda.synchronize()
     xr = x.double().cpu().requires_grad_(True)
     gr = gamma.double().cpu().requires_grad_(True)
@@ -301,3 +320,54 @@ def test_batchnorm_backward_with_fused_relu(cuda, m, c, fix_gamma):
         mag = float(dx.double().abs().sum(0).max())
         np.testing.assert_allclose(dsum.cpu().numpy(), dx.double().sum(0).cpu().numpy(),
                                    rtol=1e-4, atol=2e-7 * mag)
+
+
+IMPLICIT_CASES = [
+    # (B, H, W, C, F, k, s, p)
+    (2, 9, 7, 16, 24, (3, 3), (1, 1), (1, 1)),
+    (2, 8, 8, 64, 72, (1, 1), (1, 1), (0, 0)),
+    (3, 13, 11, 8, 40, (5, 5), (1, 1), (2, 2)),
+    (2, 15, 15, 24, 136, (3, 3), (2, 2), (1, 1)),
+    (1, 23, 23, 8, 16, (7, 7), (2, 2), (3, 3)),
+    (4, 27, 27, 96, 192, (3, 3), (1, 1), (1, 1)),
+]
+
+
+@pytest.mark.parametrize("case", IMPLICIT_CASES)
+def test_implicit_gemm_convolution(cuda, case):
+    """mgx_gemm_bf16_conv: the operand gathered by cp.async producer warps
+    inside the tcgen05 GEMM equals the explicit im2col contraction (mode 1:
+    forward; mode 2: weight gradient) against float64 on bf16 operands."""
+    torch = cuda
+    from paper_1512_01274_b200 import _lib as L
+    b, h, w, c, f, k, s, p = case
+    g = torch.Generator().manual_seed(sum(case[:5]))
+    x = torch.randn(b, h, w, c, generator=g, dtype=torch.float64).to(torch.bfloat16)
+    wt = (torch.randn(f, k[0], k[1], c, generator=g, dtype=torch.float64) * 0.2).to(torch.bfloat16)
+    geom = _geom((b, h, w, c), k, s, p)
+    ho, wo = (h + 2 * p[0] - k[0]) // s[0] + 1, (w + 2 * p[1] - k[1]) // s[1] + 1
+    m, kk = b * ho * wo, k[0] * k[1] * c
+    xd, wd = x.cuda(), wt.reshape(f, kk).contiguous().cuda()
+    ldw = -(-kk // 8) * 8
+    wpad = torch.zeros(f, ldw, dtype=torch.bfloat16, device="cuda")
+    wpad[:, :kk] = wd
+    out = torch.full((m, f), float("nan"), device="cuda")
+    L.call("mgx_gemm_bf16_conv", 1, xd.data_ptr(), _ptr(geom), wpad.data_ptr(), ldw, None,
+           out.data_ptr(), f, m, f, kk, 0, 1, None, 0)
+    # weight gradient: dW[f, kk] = sum_m dY[m, f] gather(x)[m, kk]
+    dy = torch.randn(m, f, generator=g, dtype=torch.float64).to(torch.bfloat16)
+    ldf = -(-f // 8) * 8
+    dyd = torch.zeros(m, ldf, dtype=torch.bfloat16, device="cuda")
+    dyd[:, :f] = dy.cuda()
+    dw = torch.full((f, kk), float("nan"), device="cuda")
+    ws = torch.empty(64 * f * kk + 1, device="cuda")
+    L.call("mgx_gemm_bf16_conv", 2, xd.data_ptr(), _ptr(geom), dyd.data_ptr(), ldf, None,
+           dw.data_ptr(), kk, f, kk, m, 0, 0, ws.data_ptr(), 0)
+    torch.cuda.synchronize()
+    ref = oc.conv2d_nhwc(x.double(), wt.double(), None, s, p).reshape(m, f)
+    torch.testing.assert_close(out.double().cpu(), ref, rtol=1e-4, atol=1e-3 * max(1, kk / 64) ** 0.5)
+    xr = x.double().permute(0, 3, 1, 2)
+    from torch.nn.grad import conv2d_weight
+    dwr = conv2d_weight(xr, (f, c, k[0], k[1]), dy.double().reshape(b, ho, wo, f).permute(0, 3, 1, 2),
+                        stride=s, padding=p).permute(0, 2, 3, 1).reshape(f, kk)
+    torch.testing.assert_close(dw.double().cpu(), dwr, rtol=1e-4, atol=1e-3 * max(1, m / 64) ** 0.5)
