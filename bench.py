@@ -350,7 +350,8 @@ def run_config(name, args, world, rank, local, eng, steps, warmup, with_e2e=True
         barrier(world)
     ms_local = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
     ms_total = max_over_ranks(ms_local, world)
-    res = {"workload": cfg["workload"], "per_gpu_batch": per, "global_batch": per * world,
+    res = {"config_name": name, "workload": cfg["workload"], "per_gpu_batch": per,
+           "global_batch": per * world,
            "ms_per_step": ms_total / steps,
            "value": per * world * steps / (ms_total / 1e3), "clocks": clocks.summary(),
            "dtype": cfg["dtype"]}
@@ -466,10 +467,21 @@ def roofline_of(res):
         achieved = fam_bytes[dom] / (ms * 1e-3) / 1e9
         peak, unit = hbm, "GB/s"
         psrc = f"{src} HBM copy"
+    traffic, tsrc = None, None
+    try:
+        with open(os.path.join(ROOT, "profiles", f"traffic_{res['config_name']}.json")) as f:
+            t = json.load(f)
+        if t.get("kernel") == dom:
+            traffic, tsrc = t["dram_bytes_per_pass"], t["source"]
+    except Exception:  # noqa: BLE001 - no committed ncu capture for this config
+        pass
     return {"bound": "tensor" if tensor else "hbm", "kernel": dom, "achieved": achieved,
             "peak": peak, "peak_source": psrc, "unit": unit, "frac": achieved / peak,
-            "traffic": None, "kernel_ms_per_step": ms, "step_share": ms / sum(fam_ms.values()),
-            "algorithmic_per_step": fam_flops[dom] if tensor else fam_bytes[dom]}
+            "traffic": traffic, "traffic_unit": "DRAM bytes per step (all launches of the family)",
+            "traffic_source": tsrc, "kernel_ms_per_step": ms,
+            "step_share": ms / sum(fam_ms.values()),
+            "algorithmic_per_step": fam_flops[dom] if tensor else fam_bytes[dom],
+            "algorithmic_bytes_per_step": fam_bytes[dom]}
 
 
 def kv_sweep(args, eng, world, rank, distributed):
