@@ -141,7 +141,7 @@ int mgx_cast_bf16_2d(const float* x, int64_t R, int64_t C, int64_t ldi, void* y,
 int mgx_gemm_bf16_tc_ex(const void* A, int64_t lda, int a_mn, const void* B, int64_t ldb,
                         int b_mn, const float* bias, float* C, int64_t ldc, int64_t M,
                         int64_t N, int64_t K, int act, int splits, float* workspace,
-                        uintptr_t stream);
+                        float* colstats, uintptr_t stream);
 /* Implicit-GEMM convolution contractions: one operand is gathered on the
  * fly from a compact bf16 NHWC tensor `src` (C % 8 == 0) by cp.async
  * producer warps inside the tcgen05 GEMM, never materialised:
@@ -154,7 +154,17 @@ int mgx_gemm_bf16_tc_ex(const void* A, int64_t lda, int a_mn, const void* B, int
 int mgx_gemm_bf16_conv(int mode, const void* src, const int64_t* geom, const void* op,
                        int64_t ldop, const float* bias, float* C, int64_t ldc, int64_t M,
                        int64_t N, int64_t K, int act, int splits, float* workspace,
-                       uintptr_t stream);
+                       float* colstats, uintptr_t stream);
+/* colstats (optional, both GEMM entry points, one split, C pitch % 4 == 0):
+ * the epilogue also writes, for every 32-row block b and column n of C, the
+ * pair (mean, M2) of the block's valid rows as float2 colstats[b*N + n] --
+ * the BatchNorm statistics of a convolution output without re-reading it.
+ * mgx_bn_stats_from_tiles merges them (Chan's update, fp64, fixed order)
+ * into stats = [mean | rstd] and updates the moving averages like
+ * mgx_bn_stats. */
+int mgx_bn_stats_from_tiles(const void* part, int64_t M, int64_t C, float* stats,
+                            float* moving_mean, float* moving_var, float eps, float momentum,
+                            uintptr_t stream);
 /* Workspace (floats) the auto split-K choice needs for an M x N x K GEMM. */
 int mgx_gemm_splitk_workspace(int64_t M, int64_t N, int64_t K, int64_t* out_floats);
 
@@ -273,7 +283,7 @@ typedef struct mgx_instr {
 #define MGX_OP_IM2COL 15      /* ptr0=x ptr1=col(bf16) dims=geom,ldk               */
 #define MGX_OP_COL2IM 16      /* ptr0=dcol ptr1=dx dims=geom,ldk                   */
 #define MGX_OP_BN_STATS 17    /* ptr0=x ptr1=ws ptr2=stats ptr3=mmean ptr4=mvar    */
-                              /* dims=M,C,use_global fattr=eps,momentum            */
+                              /* dims=M,C,use_global,from_tiles fattr=eps,momentum */
 #define MGX_OP_BN_APPLY 18    /* ptr0=x ptr1=stats ptr2=gamma ptr3=beta ptr4=y     */
                               /* ptr5=y16 (optional bf16 copy) dims=M,C act        */
 #define MGX_OP_BN_BWD_REDUCE 19 /* ptr0=dy ptr1=x ptr2=stats ptr3=ws ptr4=sums     */
@@ -288,11 +298,12 @@ typedef struct mgx_instr {
 #define MGX_OP_CHAN_COPY 23   /* ptr0=src ptr1=dst ptr2=dst16 dims=rows,cols,lds,    */
                               /* soff,ldd,doff                                     */
 #define MGX_OP_COLSUM 24      /* ptr0=x ptr1=ws ptr2=out dims=M,C                  */
-#define MGX_OP_GEMM_TC_EX 25  /* ptr0=A ptr1=B ptr2=bias ptr3=C ptr4=workspace act */
+#define MGX_OP_GEMM_TC_EX 25  /* ptr0=A ptr1=B ptr2=bias ptr3=C ptr4=workspace     */
+                              /* ptr5=colstats act                                 */
                               /* dims=M,N,K,lda,ldb,ldc,(a_mn|b_mn<<1),splits      */
 #define MGX_OP_WFLIP 26       /* ptr0=w ptr1=wf(bf16) dims=F,kh,kw,C,ld            */
 #define MGX_OP_GEMM_CONV 27   /* ptr0=src(bf16 NHWC) ptr1=op ptr2=bias ptr3=C      */
-                              /* ptr4=workspace dims=M,N,K,ldop,ldc,               */
+                              /* ptr4=workspace ptr5=colstats dims=M,N,K,ldop,ldc, */
                               /* mode|splits<<8, B<<48|H<<32|W<<16|C,              */
                               /* kh<<40|kw<<32|sh<<24|sw<<16|ph<<8|pw              */
 

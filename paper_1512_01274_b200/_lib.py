@@ -134,10 +134,12 @@ _SIGNATURES = {
     "mgx_prog_error": ([ctypes.POINTER(c_u32)], ctypes.c_int),
     "mgx_prog_time_levels": ([c_u64, c_i32, c_i32, c_uptr, c_vp], ctypes.c_int),
     "mgx_gemm_bf16_tc_ex": ([c_vp, c_i64, ctypes.c_int, c_vp, c_i64, ctypes.c_int, c_vp, c_vp,
-                             c_i64, c_i64, c_i64, c_i64, ctypes.c_int, ctypes.c_int, c_vp, c_uptr],
-                            ctypes.c_int),
+                             c_i64, c_i64, c_i64, c_i64, ctypes.c_int, ctypes.c_int, c_vp, c_vp,
+                             c_uptr], ctypes.c_int),
     "mgx_gemm_bf16_conv": ([ctypes.c_int, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_i64, c_i64,
-                            c_i64, ctypes.c_int, ctypes.c_int, c_vp, c_uptr], ctypes.c_int),
+                            c_i64, ctypes.c_int, ctypes.c_int, c_vp, c_vp, c_uptr], ctypes.c_int),
+    "mgx_bn_stats_from_tiles": ([c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_f32, c_f32, c_uptr],
+                                ctypes.c_int),
     "mgx_gemm_splitk_workspace": ([c_i64, c_i64, c_i64, ctypes.POINTER(c_i64)], ctypes.c_int),
     "mgx_im2col_bf16": ([c_vp, c_vp, c_vp, c_i64, c_uptr], ctypes.c_int),
     "mgx_col2im": ([c_vp, c_i64, c_vp, c_vp, c_uptr], ctypes.c_int),

@@ -175,13 +175,20 @@ def _pack_geom(shape, k, s, p) -> tuple:
 
 
 def _gemm_conv(mode: int, src: int, shape, k, s, p, op: int, ldop: int, out: int, ldc: int,
-               m: int, n: int, kdim: int, bias=None, act: int = 0, splits: int = 1, ws=None):
+               m: int, n: int, kdim: int, bias=None, act: int = 0, splits: int = 1, ws=None,
+               colstats=None):
     g1, g2 = _pack_geom(shape, k, s, p)
-    return instr(L.OP_GEMM_CONV, [src, op, bias, out, ws],
+    return instr(L.OP_GEMM_CONV, [src, op, bias, out, ws, colstats],
                  [m, n, kdim, ldop, ldc, mode | (splits << 8), g1, g2], act=act)
 
 
 def _conv_lower_fwd(ins, out, attrs):
+    return conv_forward_instrs(ins, out, attrs)
+
+
+def conv_forward_instrs(ins, out, attrs, colstats: Optional[int] = None) -> list:
+    """Convolution forward; colstats: buffer for the epilogue's per-32-row
+    (mean, M2) column statistics (a BatchNorm follows, executor fusion)."""
     ctx = current_ctx()
     code = []
     x, w = ins[0], ins[1]
@@ -196,10 +203,12 @@ def _conv_lower_fwd(ins, out, attrs):
         ho, wo = _conv_out(h, wd, k, s, p)
         kk = k[0] * k[1] * c
         code.append(_gemm_conv(1, sh, x.shape, k, s, p, wb, ldk, out.ptr, f, b * ho * wo, f, kk,
-                               bias=bias))
+                               bias=bias, colstats=colstats))
         return code
     col, wb, (m, kk, ldk, f, *_r) = _conv_operands(x, w, attrs, ctx, code)
-    code.append(_gemm(col, ldk, False, wb, ldk, False, out.ptr, f, m, f, kk, bias=bias))
+    g = _gemm(col, ldk, False, wb, ldk, False, out.ptr, f, m, f, kk, bias=bias)
+    g.ptr[5] = colstats or None
+    code.append(g)
     return code
 
 
@@ -322,7 +331,7 @@ def _bn_infer(shapes, attrs):
 
 
 def _bn_stats(x: View, attrs, ctx, code: list, update: bool, mm=None, mv=None,
-              xnode=None) -> int:
+              xnode=None, tiles: Optional[int] = None) -> int:
     m, c = prod(x.shape[:-1]), x.shape[-1]
     eps = float(attrs.get("eps", 1e-3))
     key = ("bnstats", id(xnode if xnode is not None else ctx.input_node("in0")), x.ptr, eps)
@@ -331,21 +340,28 @@ def _bn_stats(x: View, attrs, ctx, code: list, update: bool, mm=None, mv=None,
         st = ctx.persistent(8 * c)
         ctx.memo[key] = st
         use_global = (not ctx.training) or bool(attrs.get("use_global_stats", False))
-        ws = ctx.scratch(_reduce_ws(m, c))
-        code.append(instr(L.OP_BN_STATS,
-                          [x.ptr, ws, st, mm.ptr if (update or use_global) and mm else None,
-                           mv.ptr if (update or use_global) and mv else None],
-                          [m, c, 1 if use_global else 0],
-                          [eps, float(attrs.get("momentum", 0.9))]))
+        mmp = mm.ptr if (update or use_global) and mm else None
+        mvp = mv.ptr if (update or use_global) and mv else None
+        if tiles is not None and not use_global:
+            # from the convolution epilogue's per-tile statistics (no re-read)
+            code.append(instr(L.OP_BN_STATS, [x.ptr, tiles, st, mmp, mvp], [m, c, 0, 1],
+                              [eps, float(attrs.get("momentum", 0.9))]))
+        else:
+            ws = ctx.scratch(_reduce_ws(m, c))
+            code.append(instr(L.OP_BN_STATS, [x.ptr, ws, st, mmp, mvp],
+                              [m, c, 1 if use_global else 0, 0],
+                              [eps, float(attrs.get("momentum", 0.9))]))
     return st
 
 
-def bn_forward_instrs(ins, out: View, attrs, act: int = 0) -> list:
+def bn_forward_instrs(ins, out: View, attrs, act: int = 0, tiles: Optional[int] = None,
+                      xnode=None) -> list:
     ctx = current_ctx()
     x = ins[0]
     m, c = prod(x.shape[:-1]), x.shape[-1]
     code = []
-    st = _bn_stats(x, attrs, ctx, code, update=True, mm=ins[3], mv=ins[4])
+    st = _bn_stats(x, attrs, ctx, code, update=True, mm=ins[3], mv=ins[4], xnode=xnode,
+                   tiles=tiles)
     gamma = None if attrs.get("fix_gamma", True) else ins[1].ptr
     y16 = ctx.shadow_out(out.size) if c % 8 == 0 else None
     code.append(instr(L.OP_BN_APPLY, [x.ptr, st, gamma, ins[2].ptr, out.ptr, y16], [m, c], act=act))
@@ -434,6 +450,19 @@ register(OperatorDef(
 ))
 
 AUX_SUFFIXES = ("_moving_mean", "_moving_var")
+
+
+def conv_bn_instrs(cins, cout: View, cattrs, bins, bout: View, battrs, act: int, conv_node):
+    """Convolution -> BatchNorm (-> activation) forward: the GEMM epilogue
+    produces the BatchNorm statistics of its output (per 32-row (mean, M2)
+    pairs), so the BatchNorm never re-reads the convolution output for its
+    statistics (executor fusion)."""
+    ctx = current_ctx()
+    m, f = prod(cout.shape[:-1]), cout.shape[-1]
+    tiles = ctx.scratch(8 * (-(-m // 32)) * f)
+    code = conv_forward_instrs(cins, cout, cattrs, colstats=tiles)
+    code += bn_forward_instrs(bins, bout, battrs, act=act, tiles=tiles, xnode=conv_node)
+    return code
 
 
 # ------------------------------------------------------------------ Pooling

@@ -528,6 +528,56 @@ __global__ void bn_stats_finalize_kernel(const double* __restrict__ ws, int nchu
   if (mvar) mvar[c] = static_cast<float>(double(mvar[c]) * momentum + var * (1.0 - momentum));
 }
 
+// BatchNorm statistics from the GEMM epilogue's per-32-row (mean, M2)
+// pairs of the convolution output: a block per channel; thread t merges
+// row blocks t, t+256, ... (Chan's pairwise update, fp64), then a fixed
+// halving tree over the 256 partial results (deterministic).
+__global__ void bn_stats_from_tiles_kernel(const float2* __restrict__ part, int64_t M, int C,
+                                           float eps, float momentum, float* __restrict__ stats,
+                                           float* __restrict__ mmean, float* __restrict__ mvar) {
+  __shared__ double sn[256], smu[256], sm2[256];
+  const int c = blockIdx.x;
+  const int t = threadIdx.x;
+  const int nb = static_cast<int>((M + 31) / 32);
+  double n = 0.0, mu = 0.0, m2 = 0.0;
+  for (int b = t; b < nb; b += blockDim.x) {
+    const float2 p = part[int64_t(b) * C + c];
+    const int64_t left = M - int64_t(b) * 32;
+    const double nb_ = double(left < 32 ? left : 32);
+    const double tot = n + nb_;
+    const double d = double(p.x) - mu;
+    mu += d * nb_ / tot;
+    m2 += double(p.y) + d * d * n * nb_ / tot;
+    n = tot;
+  }
+  sn[t] = n;
+  smu[t] = mu;
+  sm2[t] = m2;
+  __syncthreads();
+  for (int h = blockDim.x / 2; h > 0; h >>= 1) {
+    if (t < h) {
+      const double na = sn[t], nb_ = sn[t + h];
+      const double tot = na + nb_;
+      if (nb_ > 0.0) {
+        const double d = smu[t + h] - smu[t];
+        smu[t] = tot > 0.0 ? smu[t] + d * nb_ / tot : 0.0;
+        sm2[t] = sm2[t] + sm2[t + h] + (tot > 0.0 ? d * d * na * nb_ / tot : 0.0);
+        sn[t] = tot;
+      }
+    }
+    __syncthreads();
+  }
+  if (t == 0) {
+    const double mean = smu[0];
+    double var = sm2[0] / double(M);
+    if (var < 0.0) var = 0.0;
+    stats[c] = static_cast<float>(mean);
+    stats[C + c] = static_cast<float>(1.0 / sqrt(var + double(eps)));
+    if (mmean) mmean[c] = static_cast<float>(double(mmean[c]) * momentum + mean * (1.0 - momentum));
+    if (mvar) mvar[c] = static_cast<float>(double(mvar[c]) * momentum + var * (1.0 - momentum));
+  }
+}
+
 // MODE 1/2 finalize: out[c] = sum0, out[C + c] = sum1 (MODE 1) as fp32;
 // optionally also straight into gradient buffers: out0[c] = sum0 and
 // out1[c] = sum1 (or 0 when zero1: BatchNorm's fix_gamma)
@@ -1117,6 +1167,17 @@ extern "C" int mgx_weight_flip_bf16(const float* w, int64_t F, int64_t kh, int64
   mgx::conv::weight_flip_kernel<<<grid_for(C * ld), 256, 0, mgx::as_stream(stream)>>>(
       w, static_cast<int>(F), static_cast<int>(kh), static_cast<int>(kw), static_cast<int>(C),
       static_cast<__nv_bfloat16*>(wf), ld);
+  MGX_LAUNCHED();
+  return MGX_OK;
+}
+
+extern "C" int mgx_bn_stats_from_tiles(const void* part, int64_t M, int64_t C, float* stats,
+                                       float* moving_mean, float* moving_var, float eps,
+                                       float momentum, uintptr_t stream) {
+  MGX_REQUIRE(part && stats && M > 0 && C > 0, "mgx_bn_stats_from_tiles: bad arguments");
+  mgx::conv::bn_stats_from_tiles_kernel<<<static_cast<unsigned>(C), 256, 0, mgx::as_stream(stream)>>>(
+      static_cast<const float2*>(part), M, static_cast<int>(C), eps, momentum, stats, moving_mean,
+      moving_var);
   MGX_LAUNCHED();
   return MGX_OK;
 }

@@ -263,6 +263,9 @@ static int run_instr(const mgx_instr& in, cudaStream_t st) {
     case MGX_OP_IM2COL: return mgx_im2col_bf16(p0, in.ptr[1], d, d[7], s);
     case MGX_OP_COL2IM: return mgx_col2im(p0, d[7], p1, d, s);
     case MGX_OP_BN_STATS:
+      if (d[3] == 1)  // from the convolution GEMM's per-tile (mean, M2) pairs in ptr1
+        return mgx_bn_stats_from_tiles(in.ptr[1], d[0], d[1], p2, p3,
+                                       static_cast<float*>(in.ptr[4]), in.fattr[0], in.fattr[1], s);
       return mgx_bn_stats(p0, d[0], d[1], in.ptr[1], p2, p3, static_cast<float*>(in.ptr[4]),
                           in.fattr[0], in.fattr[1], static_cast<int>(d[2]), s);
     case MGX_OP_BN_APPLY:
@@ -295,14 +298,15 @@ static int run_instr(const mgx_instr& in, cudaStream_t st) {
                                (((w >> 8) & 0xFF) << 16) | (w & 0xFF)};
       return mgx_gemm_bf16_conv(static_cast<int>(d[5] & 0xFF), in.ptr[0], geom, in.ptr[1], d[3],
                                 p2, p3, d[4], d[0], d[1], d[2], in.act, static_cast<int>(d[5] >> 8),
-                                static_cast<float*>(in.ptr[4]), s);
+                                static_cast<float*>(in.ptr[4]), static_cast<float*>(in.ptr[5]), s);
     }
     case MGX_OP_WFLIP: return mgx_weight_flip_bf16(p0, d[0], d[1], d[2], d[3], in.ptr[1], d[4], s);
     case MGX_OP_COLSUM: return mgx_colsum(p0, d[0], d[1], in.ptr[1], p2, s);
     case MGX_OP_GEMM_TC_EX:
       return mgx_gemm_bf16_tc_ex(in.ptr[0], d[3], static_cast<int>(d[6] & 1), in.ptr[1], d[4],
                                  static_cast<int>((d[6] >> 1) & 1), p2, p3, d[5], d[0], d[1], d[2],
-                                 in.act, static_cast<int>(d[7]), static_cast<float*>(in.ptr[4]), s);
+                                 in.act, static_cast<int>(d[7]), static_cast<float*>(in.ptr[4]),
+                                 static_cast<float*>(in.ptr[5]), s);
     default:
       set_error("program: unknown opcode %d", in.op);
       return MGX_BAD_ARGUMENT;

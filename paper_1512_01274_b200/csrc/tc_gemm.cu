@@ -199,7 +199,8 @@ tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
                     const __grid_constant__ CUtensorMap map_b,
                     const __grid_constant__ CUtensorMap map_c, const float* __restrict__ bias,
                     float* __restrict__ C, int ldc, int M, int N, int act, Sched sc,
-                    int64_t split_stride, int use_tma_store, const __grid_constant__ Gather ga) {
+                    int64_t split_stride, int use_tma_store, const __grid_constant__ Gather ga,
+                    float2* __restrict__ colstats) {
   using G = Cfg<BN>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -475,6 +476,26 @@ tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
             tma_store_2d(&map_c, buf, n0 + c0, int(int64_t(z) * M) + row0);
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           }
+          if (colstats) {
+            // per-column (mean, M2) of this warp's valid rows, read back
+            // column-wise from the staged box (one row per step: conflict
+            // free): the BatchNorm statistics of the convolution output,
+            // merged later in a fixed order (bn_stats_from_tiles)
+            const int nrows = min(32, M - row0);
+            const int col = n0 + c0 + lane;
+            const uint8_t* cp = buf + ((lane & 3) << 2);
+            float sum = 0.0f;
+            for (int r = 0; r < nrows; ++r)
+              sum += *reinterpret_cast<const float*>(cp + r * 128 + (((lane >> 2) ^ (r & 7)) << 4));
+            const float mean = sum / float(nrows);
+            float m2 = 0.0f;
+            for (int r = 0; r < nrows; ++r) {
+              const float d =
+                  *reinterpret_cast<const float*>(cp + r * 128 + (((lane >> 2) ^ (r & 7)) << 4)) - mean;
+              m2 += d * d;
+            }
+            if (col < N) colstats[int64_t(row0 >> 5) * N + col] = make_float2(mean, m2);
+          }
           nbuf ^= 1;
         } else {
           const int row = row0 + lane;
@@ -627,7 +648,7 @@ template <bool A_MN, bool B_MN, int BN, int ACTK, int GM>
 static int launch_act(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
                       int grid, const float* bias, float* C, int ldc, int M, int N, int act,
                       const Sched& sc, int64_t split_stride, int tma_store, const Gather& ga,
-                      cudaStream_t st) {
+                      float2* colstats, cudaStream_t st) {
   using G = Cfg<BN>;
   static bool configured = false;
   if (!configured) {
@@ -636,7 +657,7 @@ static int launch_act(const CUtensorMap& ma, const CUtensorMap& mb, const CUtens
     configured = true;
   }
   tc_gemm_bf16_kernel<A_MN, B_MN, BN, ACTK, GM><<<grid, threads_for<GM>(), G::kSmemBytes, st>>>(
-      ma, mb, mc, bias, C, ldc, M, N, act, sc, split_stride, tma_store, ga);
+      ma, mb, mc, bias, C, ldc, M, N, act, sc, split_stride, tma_store, ga, colstats);
   MGX_LAUNCHED();
   return MGX_OK;
 }
@@ -651,18 +672,19 @@ struct Launch {
   int64_t sstride;
   int tma;
   Gather ga;
+  float2* colstats;
 };
 
 template <bool A_MN, bool B_MN, int BN, int GM>
 static int launch_acts(const Launch& l, cudaStream_t st) {
   if (l.act == MGX_ACT_NONE)
     return launch_act<A_MN, B_MN, BN, 0, GM>(l.ma, l.mb, l.mc, l.grid, l.bias, l.C, l.ldc, l.M, l.N,
-                                             l.act, l.sc, l.sstride, l.tma, l.ga, st);
+                                             l.act, l.sc, l.sstride, l.tma, l.ga, l.colstats, st);
   if (l.act == MGX_ACT_RELU)
     return launch_act<A_MN, B_MN, BN, 1, GM>(l.ma, l.mb, l.mc, l.grid, l.bias, l.C, l.ldc, l.M, l.N,
-                                             l.act, l.sc, l.sstride, l.tma, l.ga, st);
+                                             l.act, l.sc, l.sstride, l.tma, l.ga, l.colstats, st);
   return launch_act<A_MN, B_MN, BN, 2, GM>(l.ma, l.mb, l.mc, l.grid, l.bias, l.C, l.ldc, l.M, l.N,
-                                           l.act, l.sc, l.sstride, l.tma, l.ga, st);
+                                           l.act, l.sc, l.sstride, l.tma, l.ga, l.colstats, st);
 }
 
 template <int BN>
@@ -695,7 +717,7 @@ namespace tc {
 static int gemm_impl(const void* A, int64_t lda, int a_mn, const void* B, int64_t ldb, int b_mn,
                      const float* bias, float* C, int64_t ldc, int64_t M, int64_t N, int64_t K,
                      int act, int splits, float* workspace, int gm, const Gather& ga,
-                     cudaStream_t st) {
+                     float* colstats, cudaStream_t st) {
   MGX_REQUIRE(C && M > 0 && N > 0 && K > 0, "mgx_gemm_bf16_tc: bad arguments");
   MGX_REQUIRE((gm == 1 || A) && (gm == 2 || B), "mgx_gemm_bf16_tc: missing operand");
   MGX_REQUIRE((gm == 1 || lda % 8 == 0) && (gm == 2 || ldb % 8 == 0),
@@ -740,6 +762,9 @@ static int gemm_impl(const void* A, int64_t lda, int a_mn, const void* B, int64_
   l.M = static_cast<int>(M);
   l.N = static_cast<int>(N);
   l.ga = ga;
+  l.colstats = reinterpret_cast<float2*>(colstats);
+  MGX_REQUIRE(!colstats || (splits == 1 && l.tma && mgx::aligned16(colstats)),
+              "mgx_gemm_bf16_tc: column statistics need one split and a 16-byte aligned C pitch");
   int rc = bn == 64 ? launch_bn<64>(a_mn, b_mn, gm, l, st) : launch_bn<128>(a_mn, b_mn, gm, l, st);
   if (rc != MGX_OK || splits == 1) return rc;
   int64_t blocks = mgx::ceil_div(M * N, 256);
@@ -756,17 +781,17 @@ static int gemm_impl(const void* A, int64_t lda, int a_mn, const void* B, int64_
 extern "C" int mgx_gemm_bf16_tc_ex(const void* A, int64_t lda, int a_mn, const void* B,
                                    int64_t ldb, int b_mn, const float* bias, float* C, int64_t ldc,
                                    int64_t M, int64_t N, int64_t K, int act, int splits,
-                                   float* workspace, uintptr_t stream) {
+                                   float* workspace, float* colstats, uintptr_t stream) {
   mgx::tc::Gather none;
   std::memset(&none, 0, sizeof(none));
   return mgx::tc::gemm_impl(A, lda, a_mn, B, ldb, b_mn, bias, C, ldc, M, N, K, act, splits,
-                            workspace, 0, none, mgx::as_stream(stream));
+                            workspace, 0, none, colstats, mgx::as_stream(stream));
 }
 
 extern "C" int mgx_gemm_bf16_conv(int mode, const void* src, const int64_t* geom, const void* op,
                                   int64_t ldop, const float* bias, float* C, int64_t ldc,
                                   int64_t M, int64_t N, int64_t K, int act, int splits,
-                                  float* workspace, uintptr_t stream) {
+                                  float* workspace, float* colstats, uintptr_t stream) {
   using namespace mgx::tc;
   MGX_REQUIRE(src && geom && op && (mode == 1 || mode == 2), "mgx_gemm_bf16_conv: bad arguments");
   MGX_REQUIRE(mgx::aligned16(src), "mgx_gemm_bf16_conv: source not 16-byte aligned");
@@ -792,18 +817,19 @@ extern "C" int mgx_gemm_bf16_conv(int mode, const void* src, const int64_t* geom
     // C[pixels, N] = gather(src)[pixels, kconv] . op[N, kconv]^T
     MGX_REQUIRE(M == pixels && K == kconv, "mgx_gemm_bf16_conv: M/K do not match the geometry");
     return gemm_impl(nullptr, 0, 0, op, ldop, 0, bias, C, ldc, M, N, K, act, splits, workspace, 1,
-                     ga, mgx::as_stream(stream));
+                     ga, colstats, mgx::as_stream(stream));
   }
   // C[M, kconv] = op[pixels, M]^T (MN-major) . gather(src)[pixels, kconv]
   MGX_REQUIRE(K == pixels && N == kconv, "mgx_gemm_bf16_conv: N/K do not match the geometry");
   return gemm_impl(op, ldop, 1, nullptr, 0, 1, bias, C, ldc, M, N, K, act, splits, workspace, 2,
-                   ga, mgx::as_stream(stream));
+                   ga, colstats, mgx::as_stream(stream));
 }
 
 extern "C" int mgx_gemm_bf16_tc(const void* A, int64_t lda, const void* B, int64_t ldb,
                                 const float* bias, float* C, int64_t ldc, int64_t M, int64_t N,
                                 int64_t K, int act, uintptr_t stream) {
-  return mgx_gemm_bf16_tc_ex(A, lda, 0, B, ldb, 0, bias, C, ldc, M, N, K, act, 1, nullptr, stream);
+  return mgx_gemm_bf16_tc_ex(A, lda, 0, B, ldb, 0, bias, C, ldc, M, N, K, act, 1, nullptr, nullptr,
+                             stream);
 }
 
 extern "C" int mgx_gemm_splitk_workspace(int64_t M, int64_t N, int64_t K, int64_t* out_floats) {

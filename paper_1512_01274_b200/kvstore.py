@@ -179,7 +179,13 @@ class KVStore:
     def __init__(self, machines: int = 1, workers: int = 1, mode: str = "sequential",
                  etype: str = "float32", engine: Optional[Engine] = None,
                  tcp: Optional[str] = None, distributed: bool = False,
-                 bucket_bytes: int = DEFAULT_BUCKET_BYTES, timeout: float = 120.0):
+                 bucket_bytes: int = DEFAULT_BUCKET_BYTES, timeout: float = 120.0,
+                 bucket_flush: bool = True):
+        # bucket_flush: launch a bucket's round as soon as all its keys are
+        # pushed (default); False defers every round to the next pull /
+        # barrier / explicit flush, so a whole step's keys reduce in one
+        # launch (one pair of cross-GPU barriers instead of one per bucket)
+        self.bucket_flush = bucket_flush
         if machines < 1 or workers < 1:
             raise ArgumentError("topology needs machines >= 1 and workers >= 1")
         if mode not in MODES:
@@ -298,7 +304,7 @@ class KVStore:
                 self._pushed[key] = set()
                 self._pending.append(key)
                 self._cv.notify_all()
-                if self._bucket_complete_locked(k):
+                if self.bucket_flush and self._bucket_complete_locked(k):
                     self._flush_locked()
 
     def pull(self, key: int, out: Tensor, worker: int) -> None:

@@ -139,6 +139,9 @@ class DataParallelStep:
                  engine: Optional[Engine] = None, use_graph: bool = True, dense: str = "fp32"):
         _check_graph(g)
         self.g, self.kv = g, kv
+        # the step pushes every key back to back after the backward: reduce
+        # them in one flush (the next pull, capture() or round_barrier)
+        kv.bucket_flush = False
         self.engine = engine or kv.engine
         self.names = param_names(g)
         self.aux = aux_names(g)

@@ -57,7 +57,7 @@ def test_gemm_operand_majors(cuda, a_mn, b_mn, m, n, k):
     c = torch.full((m, n), float("nan"), device="cuda")
     ws = torch.empty(64 * m * n + 1, device="cuda")
     L.call("mgx_gemm_bf16_tc_ex", abuf.data_ptr(), lda, a_mn, bbuf.data_ptr(), ldb, b_mn, None,
-           c.data_ptr(), n, m, n, k, 0, 0, ws.data_ptr(), 0)
+           c.data_ptr(), n, m, n, k, 0, 0, ws.data_ptr(), None, 0)
     torch.cuda.synchronize()
     ref = a.double() @ b.double().T
     torch.testing.assert_close(c.double(), ref, rtol=1e-4, atol=1e-3 * max(1.0, (k / 64) ** 0.5))
@@ -352,8 +352,10 @@ def test_implicit_gemm_convolution(cuda, case):
     wpad = torch.zeros(f, ldw, dtype=torch.bfloat16, device="cuda")
     wpad[:, :kk] = wd
     out = torch.full((m, f), float("nan"), device="cuda")
+    # forward with the epilogue's per-32-row column statistics (BatchNorm input)
+    cs = torch.full((-(-m // 32), f, 2), float("nan"), device="cuda") if f % 4 == 0 else None
     L.call("mgx_gemm_bf16_conv", 1, xd.data_ptr(), _ptr(geom), wpad.data_ptr(), ldw, None,
-           out.data_ptr(), f, m, f, kk, 0, 1, None, 0)
+           out.data_ptr(), f, m, f, kk, 0, 1, None, cs.data_ptr() if cs is not None else None, 0)
     # weight gradient: dW[f, kk] = sum_m dY[m, f] gather(x)[m, kk]
     dy = torch.randn(m, f, generator=g, dtype=torch.float64).to(torch.bfloat16)
     ldf = -(-f // 8) * 8
@@ -362,8 +364,24 @@ def test_implicit_gemm_convolution(cuda, case):
     dw = torch.full((f, kk), float("nan"), device="cuda")
     ws = torch.empty(64 * f * kk + 1, device="cuda")
     L.call("mgx_gemm_bf16_conv", 2, xd.data_ptr(), _ptr(geom), dyd.data_ptr(), ldf, None,
-           dw.data_ptr(), kk, f, kk, m, 0, 0, ws.data_ptr(), 0)
+           dw.data_ptr(), kk, f, kk, m, 0, 0, ws.data_ptr(), None, 0)
     torch.cuda.synchronize()
+    if cs is not None:
+        # BatchNorm statistics merged from the tiles == mgx_bn_stats over the output
+        import ctypes
+        st1, st2 = torch.empty(2 * f, device="cuda"), torch.empty(2 * f, device="cuda")
+        mm1, mv1 = torch.zeros(f, device="cuda"), torch.ones(f, device="cuda")
+        mm2, mv2 = torch.zeros(f, device="cuda"), torch.ones(f, device="cuda")
+        L.call("mgx_bn_stats_from_tiles", cs.data_ptr(), m, f, st1.data_ptr(), mm1.data_ptr(),
+               mv1.data_ptr(), 1e-3, 0.9, 0)
+        wsb = ctypes.c_int64()
+        L.call("mgx_reduce_workspace_bytes", m, f, ctypes.byref(wsb))
+        rws = torch.empty(wsb.value // 4 + 1, device="cuda")
+        L.call("mgx_bn_stats", out.data_ptr(), m, f, rws.data_ptr(), st2.data_ptr(), mm2.data_ptr(),
+               mv2.data_ptr(), 1e-3, 0.9, 0, 0)
+        torch.cuda.synchronize()
+        torch.testing.assert_close(st1, st2, rtol=1e-5, atol=1e-6)
+        torch.testing.assert_close(mv1, mv2, rtol=1e-5, atol=1e-6)
     ref = oc.conv2d_nhwc(x.double(), wt.double(), None, s, p).reshape(m, f)
     torch.testing.assert_close(out.double().cpu(), ref, rtol=1e-4, atol=1e-3 * max(1, kk / 64) ** 0.5)
     xr = x.double().permute(0, 3, 1, 2)

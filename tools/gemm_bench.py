@@ -34,7 +34,7 @@ def main():
         c = torch.empty(m * n, device="cuda")
         ws = torch.empty(200 * m * n if sp == 0 else 1, device="cuda")
         args = (a.data_ptr(), lda, amn, b.data_ptr(), ldb, bmn, None, c.data_ptr(), n, m, n, k, 0,
-                sp, ws.data_ptr(), 0)
+                sp, ws.data_ptr(), None, 0)
         for _ in range(3):
             L.call("mgx_gemm_bf16_tc_ex", *args)
         torch.cuda.synchronize()
