@@ -370,17 +370,22 @@ def run_config(name, args, world, rank, local, eng, steps, warmup, with_e2e=True
         y = ex.outputs[0]
 
         def e2e_step():
-            step.step({w: (pin_x, pin_y)})
+            # this step's batch was staged (H2D on the copy stream) while the
+            # previous step ran; stage the next one before waiting on this
+            step.step(staged=True)
+            step.stage(w, pin_x, pin_y)
             eng.push(lambda: L.call("mgx_memcpy_async", out_pin.data_ptr(), y.ptr, d2h,
                                     eng.stream_handle), reads=[y.tag])
             eng.wait_for(y.tag)
 
+        step.stage(w, pin_x, pin_y)
         for _ in range(max(warmup, 3)):
             e2e_step()
         barrier(world)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(eng.stream)
+        step.stage(w, pin_x, pin_y)  # the first timed step's copy, inside the region
         for _ in range(steps):
             e2e_step()
         e1.record(eng.stream)
@@ -388,7 +393,8 @@ def run_config(name, args, world, rank, local, eng, steps, warmup, with_e2e=True
         e2e_ms = max_over_ranks(e0.elapsed_time(e1), world)
         res["e2e"] = {"value": per * world * steps / (e2e_ms / 1e3), "unit": "images/s",
                       "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                      "path": "DataParallelStep.step(host pinned batch) + D2H softmax output + sync"}
+                      "path": "DataParallelStep.stage (pinned H2D on a copy stream, overlapping the "
+                              "previous step) + step + D2H softmax output + sync, every step"}
         barrier(world)
 
     # ---- roofline: per-instruction device time (events captured between

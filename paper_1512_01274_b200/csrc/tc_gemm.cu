@@ -483,18 +483,22 @@ tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
             // merged later in a fixed order (bn_stats_from_tiles)
             const int nrows = min(32, M - row0);
             const int col = n0 + c0 + lane;
+            // one pass of sums shifted by the block's first value (no
+            // cancellation), converted to (mean, M2) of the block
             const uint8_t* cp = buf + ((lane & 3) << 2);
-            float sum = 0.0f;
-            for (int r = 0; r < nrows; ++r)
-              sum += *reinterpret_cast<const float*>(cp + r * 128 + (((lane >> 2) ^ (r & 7)) << 4));
-            const float mean = sum / float(nrows);
-            float m2 = 0.0f;
-            for (int r = 0; r < nrows; ++r) {
+            const float x0 = *reinterpret_cast<const float*>(cp + ((lane >> 2) << 4));
+            float s1 = 0.0f, s2 = 0.0f;
+#pragma unroll 8
+            for (int r = 1; r < nrows; ++r) {
               const float d =
-                  *reinterpret_cast<const float*>(cp + r * 128 + (((lane >> 2) ^ (r & 7)) << 4)) - mean;
-              m2 += d * d;
+                  *reinterpret_cast<const float*>(cp + r * 128 + (((lane >> 2) ^ (r & 7)) << 4)) - x0;
+              s1 += d;
+              s2 += d * d;
             }
-            if (col < N) colstats[int64_t(row0 >> 5) * N + col] = make_float2(mean, m2);
+            const float inv = 1.0f / float(nrows);
+            const float dm = s1 * inv;
+            const float m2 = fmaxf(s2 - s1 * dm, 0.0f);
+            if (col < N) colstats[int64_t(row0 >> 5) * N + col] = make_float2(x0 + dm, m2);
           }
           nbuf ^= 1;
         } else {

@@ -174,6 +174,50 @@ class DataParallelStep:
         tmod.load_host(self.args[w]["data"], feats)
         tmod.load_host(self.args[w]["label"], labels)
 
+    # ---------------------------------------------- prefetching input pipe
+
+    def stage(self, w: int, feats, labels) -> None:
+        """Start the host->device copy of worker w's NEXT batch (pinned torch
+        tensors) on a copy stream, into a staging buffer, so it overlaps the
+        step in flight (the input-pipeline prefetch).
+        ``step(staged=True)`` consumes it."""
+        import torch
+        if not hasattr(self, "_stage"):
+            self._copy_stream = torch.cuda.Stream(device=self.engine.device)
+            self._stage = {}
+        if w not in self._stage:
+            dev = f"cuda:{self.engine.device}"
+            self._stage[w] = (torch.empty(self.args[w]["data"].size, device=dev),
+                              torch.empty(self.args[w]["label"].size, device=dev),
+                              torch.cuda.Event())
+        xs, ys, ev = self._stage[w]
+        # the staging buffers are free once the previous step consumed them
+        done = getattr(self, "_stage_done", {}).get(w)
+        if done is not None:
+            self._copy_stream.wait_event(done)
+        with torch.cuda.stream(self._copy_stream):
+            xs.copy_(feats.reshape(-1), non_blocking=True)
+            ys.copy_(labels.reshape(-1), non_blocking=True)
+            ev.record(self._copy_stream)
+
+    def _consume_stage(self, w: int) -> None:
+        import torch
+        xs, ys, ev = self._stage[w]
+        eng = self.engine
+        data, label = self.args[w]["data"], self.args[w]["label"]
+
+        def go():
+            torch.cuda.ExternalStream(eng.stream_handle).wait_event(ev)
+            L.call("mgx_copy", xs.data_ptr(), data.ptr, data.size, eng.stream_handle)
+            L.call("mgx_copy", ys.data_ptr(), label.ptr, label.size, eng.stream_handle)
+            done = torch.cuda.Event()
+            done.record(torch.cuda.ExternalStream(eng.stream_handle))
+            if not hasattr(self, "_stage_done"):
+                self._stage_done = {}
+            self._stage_done[w] = done
+
+        eng.push(go, writes=[data.tag, label.tag], label="stage-consume")
+
     def run_worker(self, w: int, pull: bool = True) -> None:
         kv, ex = self.kv, self.execs[w]
         if pull:
@@ -184,18 +228,25 @@ class DataParallelStep:
         for i, n in enumerate(self.names):
             kv.push(i, self.grads[w][n], w)
 
-    def step(self, shards: Optional[Dict[int, Tuple[np.ndarray, np.ndarray]]] = None) -> None:
-        """pull -> (load) -> forward -> backward -> push, for every local worker."""
+    def step(self, shards: Optional[Dict[int, Tuple[np.ndarray, np.ndarray]]] = None,
+             staged: bool = False) -> None:
+        """pull -> (load) -> forward -> backward -> push, for every local
+        worker.  staged=True takes the batch started by ``stage``."""
         for w in self.workers:
             for i, n in enumerate(self.names):
                 self.kv.pull(i, self.args[w][n], w)
             if shards is not None:
                 self.load(w, *shards[w])
+            elif staged:
+                self._consume_stage(w)
             ex = self.execs[w]
             ex.forward()
             ex.backward()
             for i, n in enumerate(self.names):
                 self.kv.push(i, self.grads[w][n], w)
+        # one fused reduce + update + broadcast round for all the step's keys
+        with self.kv._lock:
+            self.kv._flush_locked()
 
     def outputs(self, w: int) -> np.ndarray:
         return tmod.to_numpy(self.execs[w].outputs[0])
