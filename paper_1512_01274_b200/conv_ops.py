@@ -123,9 +123,8 @@ def _weights_bf16(w: View, ctx, code: list):
     key = ("wb", id(ctx.input_node("in1")), w.ptr)
     wb = ctx.memo.get(key)
     if wb is None:
-        wb = ctx.persistent(2 * f * ldk)
-        ctx.memo[key] = wb
-        code.append(_cast_rows(w, f, kk, wb, ldk))
+        wb = ctx.prep(key, 2 * f * ldk, lambda dst: [_cast_rows(w, f, kk, dst, ldk)],
+                      (w.ptr, w.ptr + 4 * w.size))
     return wb, ldk
 
 
@@ -271,9 +270,9 @@ def _conv_lower_bwd(slot, env, out, attrs):
         key = ("wflip", id(ctx.input_node("in1")), w.ptr)
         wfl = ctx.memo.get(key)
         if wfl is None:
-            wfl = ctx.persistent(2 * c * ldkf)
-            ctx.memo[key] = wfl
-            code.append(instr(L.OP_WFLIP, [w.ptr, wfl], [f, k[0], k[1], c, ldkf]))
+            wfl = ctx.prep(key, 2 * c * ldkf,
+                           lambda dst: [instr(L.OP_WFLIP, [w.ptr, dst], [f, k[0], k[1], c, ldkf])],
+                           (w.ptr, w.ptr + 4 * w.size))
         pf = (k[0] - 1 - p[0], k[1] - 1 - p[1])
         if f % 8 == 0:
             code.append(_gemm_conv(1, dyb, og.shape, k, (1, 1), pf, wfl, ldkf, out.ptr, c,

@@ -50,8 +50,11 @@ struct Cfg {
   static constexpr int kABytes = BM * BK * 2;
   static constexpr int kBBytes = BN * BK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kStages = BN >= 128 ? 4 : 6;
-  static constexpr int kTmemCols = 2 * BN;  // double-buffered accumulator
+  // deep rings for the gather-fed implicit GEMM (L2 round trips per stage):
+  // 6 x 32 KB (BN 128) / 8 x 24 KB (BN 64) + 32 KB epilogue staging <= 227 KB
+  static constexpr int kStages = BN >= 192 ? 4 : (BN >= 128 ? 6 : 8);
+  // double-buffered accumulator, rounded up to a power of two columns
+  static constexpr int kTmemCols = 2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512);
   static constexpr int kSmemBytes =
       1024 + kStages * kStageBytes + kEpiWarps * 2 * kStageCBytes + 256;
 };
@@ -708,7 +711,21 @@ static int auto_splits(int64_t tiles, int64_t nk) {
   return static_cast<int>(s < 1 ? 1 : s);
 }
 
-static int pick_bn(int64_t N) { return N <= 64 ? 64 : 128; }
+// N tile: the width in {64, 128, 192, 256} that wastes the fewest columns
+// (ties to the wider tile: one tile row gathers/loads A once per BN columns)
+static int pick_bn(int64_t M, int64_t N) {
+  (void)M;
+  int best = 64;
+  int64_t waste = ceil_div(N, 64) * 64 - N;
+  for (int bn : {128, 192, 256}) {
+    const int64_t w = ceil_div(N, bn) * bn - N;
+    if (w <= waste) {
+      waste = w;
+      best = bn;
+    }
+  }
+  return best;
+}
 
 }  // namespace tc
 }  // namespace mgx
@@ -734,7 +751,7 @@ static int gemm_impl(const void* A, int64_t lda, int a_mn, const void* B, int64_
               "mgx_gemm_bf16_tc: dimensions exceed 2^31");
   MGX_REQUIRE(splits >= 0, "mgx_gemm_bf16_tc: negative split count");
   MGX_TRY(get_encode());
-  const int bn = pick_bn(N);
+  const int bn = pick_bn(M, N);
   const int64_t m_tiles = mgx::ceil_div(M, BM), n_tiles = mgx::ceil_div(N, bn);
   const int64_t nk = mgx::ceil_div(K, BK);
   if (splits == 0) splits = workspace ? auto_splits(m_tiles * n_tiles, nk) : 1;
@@ -769,7 +786,10 @@ static int gemm_impl(const void* A, int64_t lda, int a_mn, const void* B, int64_
   l.colstats = reinterpret_cast<float2*>(colstats);
   MGX_REQUIRE(!colstats || (splits == 1 && l.tma && mgx::aligned16(colstats)),
               "mgx_gemm_bf16_tc: column statistics need one split and a 16-byte aligned C pitch");
-  int rc = bn == 64 ? launch_bn<64>(a_mn, b_mn, gm, l, st) : launch_bn<128>(a_mn, b_mn, gm, l, st);
+  int rc = bn == 64    ? launch_bn<64>(a_mn, b_mn, gm, l, st)
+           : bn == 128 ? launch_bn<128>(a_mn, b_mn, gm, l, st)
+           : bn == 192 ? launch_bn<192>(a_mn, b_mn, gm, l, st)
+                       : launch_bn<256>(a_mn, b_mn, gm, l, st);
   if (rc != MGX_OK || splits == 1) return rc;
   int64_t blocks = mgx::ceil_div(M * N, 256);
   if (blocks > 148 * 8) blocks = 148 * 8;
@@ -839,7 +859,7 @@ extern "C" int mgx_gemm_bf16_tc(const void* A, int64_t lda, const void* B, int64
 extern "C" int mgx_gemm_splitk_workspace(int64_t M, int64_t N, int64_t K, int64_t* out_floats) {
   using namespace mgx::tc;
   MGX_REQUIRE(out_floats && M > 0 && N > 0 && K > 0, "mgx_gemm_splitk_workspace: bad arguments");
-  const int64_t tiles = mgx::ceil_div(N, pick_bn(N)) * mgx::ceil_div(M, BM);
+  const int64_t tiles = mgx::ceil_div(N, pick_bn(M, N)) * mgx::ceil_div(M, BM);
   const int64_t nk = mgx::ceil_div(K, BK);
   int64_t splits = auto_splits(tiles, nk);
   if (splits > 1) {

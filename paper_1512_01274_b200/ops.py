@@ -227,12 +227,27 @@ class LowerCtx:
         # output the current lowering writes
         self.want_shadow: set = set()
         self.out_node = None
+        self.pre: list = []
 
     def begin_op(self, node) -> None:
         self.node = node
         self.out_node = node
         self._op_off = 0
         self.reads, self.writes = [], []
+        self.pre = []
+
+    def prep(self, key, nbytes: int, instrs, src_range) -> int:
+        """Independent preparation work of the current node (a weight cast):
+        allocates the persistent result under memo ``key`` and queues the
+        instructions as their own group (their only input is ``src_range``),
+        so a multi-lane schedule can run them off the node's critical path.
+        The node itself records a read of the result."""
+        ptr = self.persistent(nbytes)
+        dict.__setitem__(self.memo, key, ptr)
+        rng = (ptr, ptr + self._sizes[ptr])
+        self.pre.append((instrs(ptr), [src_range], [rng]))
+        self.reads.append(rng)
+        return ptr
 
     def shadow_out(self, elems: int, node=None) -> Optional[int]:
         """A compact bf16 copy of the output of ``node`` (default: the node

@@ -60,6 +60,25 @@ def main():
         d = d + ["ptrs:" + "".join("1" if p else "0" for p in ex._prog_ptrs[i])]
         rows.append((ms, i, ex.instr_labels[i], fam, rate, d))
     total = t.sum()
+    # critical path of the multi-lane schedule with these durations (each
+    # lane in order, cross-lane event waits; forward and backward joined)
+    if getattr(ex, "schedule", None) is not None:
+        lane, ptr, idx = ex.schedule
+        for over in (0.0, 0.002):
+            fin = [0.0] * len(t)
+            lane_end, start, cp_total, lane_busy = {}, 0.0, 0.0, {}
+            for i in range(len(t)):
+                if i == ex._n_fwd:  # join before the backward range
+                    start = max(fin[:i]) if i else 0.0
+                    lane_end = {}
+                d = max(t[i] - over, 0.0005)
+                s0 = max([lane_end.get(lane[i], start)] + [fin[j] for j in idx[ptr[i]:ptr[i + 1]]])
+                fin[i] = s0 + d
+                lane_end[lane[i]] = fin[i]
+                lane_busy[lane[i]] = lane_busy.get(lane[i], 0.0) + d
+            print(f"modeled multi-lane pass (per-instruction overhead {over * 1e3:.0f} us "
+                  f"removed): {max(fin):.3f} ms; lane busy ms: "
+                  + ", ".join(f"{k}:{v:.2f}" for k, v in sorted(lane_busy.items())))
     print(f"{name}: {ex.num_instructions} instructions, {total:.3f} ms profiled pass, "
           f"kernels {ex.kernel_count()}, lanes {ex.lanes_used}")
     fams = {}
