@@ -155,65 +155,85 @@ __global__ void __launch_bounds__(THREADS) kv_round_kernel(const __grid_constant
 
   const int64_t stride = int64_t(gridDim.x) * THREADS;
   const float* wsrc = p.weights[p.self_replica];
-  for (int s = 0; live && s < p.nseg; ++s) {
-    const int64_t off = p.segs[s].off;
-    const int64_t n4 = (p.segs[s].len + 3) >> 2;
-    const int64_t voff = p.segs[s].voff;
-    for (int64_t base = int64_t(blockIdx.x) * THREADS + threadIdx.x; base < n4;
-         base += stride * UNROLL) {
-      float4 g[UNROLL][NW];
-      float4 w[UNROLL];
-      float4 v[UNROLL];
+  // One flat index space over all segments (float4 units): every thread has
+  // UNROLL independent vectors in flight regardless of how many small keys
+  // the round holds (a per-segment loop serialised one latency per key).
+  __shared__ int64_t pre[kKvMaxSegs + 1];
+  if (threadIdx.x == 0) {
+    int64_t acc = 0;
+    for (int s = 0; s < p.nseg; ++s) {
+      pre[s] = acc;
+      acc += (p.segs[s].len + 3) >> 2;
+    }
+    pre[p.nseg] = acc;
+  }
+  __syncthreads();
+  const int64_t total4 = pre[p.nseg];
+  for (int64_t base = int64_t(blockIdx.x) * THREADS + threadIdx.x; live && base < total4;
+       base += stride * UNROLL) {
+    float4 g[UNROLL][NW];
+    float4 w[UNROLL];
+    float4 v[UNROLL];
+    int64_t eoff[UNROLL], evoff[UNROLL];
 #pragma unroll
-      for (int u = 0; u < UNROLL; ++u) {
-        const int64_t i = base + u * stride;
-        if (i < n4) {
-#pragma unroll
-          for (int j = 0; j < NW; ++j) g[u][j] = ld_nc_v4(p.grads[j] + off + 4 * i);
-          if (p.updater != MGX_KV_AGG) w[u] = ld_nc_v4(wsrc + off + 4 * i);
-          if (p.updater == MGX_KV_SGD)
-            v[u] = *reinterpret_cast<const float4*>(p.velocity + voff + 4 * i);
+    for (int u = 0; u < UNROLL; ++u) {
+      const int64_t gi = base + u * stride;
+      eoff[u] = -1;
+      if (gi < total4) {
+        // segment of gi: last s with pre[s] <= gi (binary search)
+        int lo = 0, hi = p.nseg - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (pre[mid] <= gi) lo = mid;
+          else hi = mid - 1;
         }
-      }
+        const int64_t i = gi - pre[lo];
+        eoff[u] = p.segs[lo].off + 4 * i;
+        evoff[u] = p.segs[lo].voff + 4 * i;
 #pragma unroll
-      for (int u = 0; u < UNROLL; ++u) {
-        const int64_t i = base + u * stride;
-        if (i >= n4) continue;
-        float tot[4];
+        for (int j = 0; j < NW; ++j) g[u][j] = ld_nc_v4(p.grads[j] + eoff[u]);
+        if (p.updater != MGX_KV_AGG) w[u] = ld_nc_v4(wsrc + eoff[u]);
+        if (p.updater == MGX_KV_SGD) v[u] = *reinterpret_cast<const float4*>(p.velocity + evoff[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < UNROLL; ++u) {
+      if (eoff[u] < 0) continue;
+      const int64_t off = eoff[u], voff = evoff[u];
+      float tot[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        float vals[NW];
+#pragma unroll
+        for (int j = 0; j < NW; ++j) vals[j] = reinterpret_cast<const float*>(&g[u][j])[c];
+        tot[c] = two_level<M, W>(vals);
+      }
+      if (p.updater == MGX_KV_AGG) {
+        *reinterpret_cast<float4*>(p.agg_out + off) = make_float4(tot[0], tot[1], tot[2], tot[3]);
+        continue;
+      }
+      float* wc = reinterpret_cast<float*>(&w[u]);
+      if (p.updater == MGX_KV_SGD) {
+        // make_sgd_updater (optim.py:72-76) -> sgd_arrays (optim.py:53-61):
+        //   g = incoming * f32(1/scale); tmp = g + w*wd; v = v*mom;
+        //   v = v + tmp*(-eta); w = w + v*1
+        float* vc = reinterpret_cast<float*>(&v[u]);
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-          float vals[NW];
-#pragma unroll
-          for (int j = 0; j < NW; ++j) vals[j] = reinterpret_cast<const float*>(&g[u][j])[c];
-          tot[c] = two_level<M, W>(vals);
+          const float gg = fmul(tot[c], p.rescale);
+          const float tmp = fadd(gg, fmul(wc[c], p.weight_decay));
+          vc[c] = fmul(vc[c], p.momentum);
+          vc[c] = fadd(vc[c], fmul(tmp, p.neg_eta));
+          wc[c] = fadd(wc[c], fmul(vc[c], 1.0f));
         }
-        if (p.updater == MGX_KV_AGG) {
-          *reinterpret_cast<float4*>(p.agg_out + off + 4 * i) = make_float4(tot[0], tot[1], tot[2], tot[3]);
-          continue;
-        }
-        float* wc = reinterpret_cast<float*>(&w[u]);
-        if (p.updater == MGX_KV_SGD) {
-          // make_sgd_updater (optim.py:72-76) -> sgd_arrays (optim.py:53-61):
-          //   g = incoming * f32(1/scale); tmp = g + w*wd; v = v*mom;
-          //   v = v + tmp*(-eta); w = w + v*1
-          float* vc = reinterpret_cast<float*>(&v[u]);
+        *reinterpret_cast<float4*>(p.velocity + voff) = v[u];
+      } else {
+        // add_updater (kvstore.py:47-49): stored += incoming
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            const float gg = fmul(tot[c], p.rescale);
-            const float tmp = fadd(gg, fmul(wc[c], p.weight_decay));
-            vc[c] = fmul(vc[c], p.momentum);
-            vc[c] = fadd(vc[c], fmul(tmp, p.neg_eta));
-            wc[c] = fadd(wc[c], fmul(vc[c], 1.0f));
-          }
-          *reinterpret_cast<float4*>(p.velocity + voff + 4 * i) = v[u];
-        } else {
-          // add_updater (kvstore.py:47-49): stored += incoming
-#pragma unroll
-          for (int c = 0; c < 4; ++c) wc[c] = fadd(wc[c], tot[c]);
-        }
-#pragma unroll
-        for (int j = 0; j < NW; ++j) st_v4(p.weights[j] + off + 4 * i, w[u]);
+        for (int c = 0; c < 4; ++c) wc[c] = fadd(wc[c], tot[c]);
       }
+#pragma unroll
+      for (int j = 0; j < NW; ++j) st_v4(p.weights[j] + off, w[u]);
     }
   }
   if (barrier) {
