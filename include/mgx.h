@@ -385,6 +385,20 @@ typedef struct mgx_kv_round_args {
                                  it, so captured launches replay correctly */
   uint32_t* error_word;       /* device word set non-zero on barrier timeout */
   int32_t grid;               /* 0 = auto; required (same on all ranks) with flags */
+  /* push mode (flags != NULL, updater SGD or ADD; nscatter > 0): every
+   * NVLink transfer is a remote STORE.  Phase 1 writes this process's
+   * gradient values for every owner's segments into that owner's staging
+   * buffer; after the barrier each owner reduces its shard from its own
+   * staging buffer (local HBM, same tree order) and stores the new weights
+   * into every replica.  scatter[i] = {arena offset, length, element offset
+   * in stage[scatter_owner[i]]}; this process's staging buffer holds one
+   * slot of stage_slot elements per worker, laid out like its momentum
+   * shard (segs[].voff). */
+  const mgx_kv_seg* scatter;  /* HOST array, nscatter <= 256 */
+  const int32_t* scatter_owner;
+  int32_t nscatter;
+  float* const* stage;        /* HOST array of M*W staging-buffer pointers */
+  int64_t stage_slot;
 } mgx_kv_round_args;
 
 int mgx_kv_round(const mgx_kv_round_args* args, uintptr_t stream);

@@ -70,6 +70,8 @@ class KvRoundArgs(ctypes.Structure):
         ("momentum", c_f32), ("weight_decay", c_f32),
         ("flags", ctypes.POINTER(c_vp)), ("rank", c_i32), ("epoch_ctr", c_vp),
         ("error_word", c_vp), ("grid", c_i32),
+        ("scatter", ctypes.POINTER(KvSeg)), ("scatter_owner", ctypes.POINTER(c_i32)),
+        ("nscatter", c_i32), ("stage", ctypes.POINTER(c_vp)), ("stage_slot", c_i64),
     ]
 
 

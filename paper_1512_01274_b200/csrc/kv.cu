@@ -52,7 +52,24 @@ struct KvParams {
   uint32_t* epoch_ctr;  // device: [completed launches, blocks finished]
   float rescale, neg_eta, momentum, weight_decay;
   mgx_kv_seg segs[kKvMaxSegs];
+  // push mode (nscatter > 0)
+  int32_t nscatter;
+  int64_t stage_slot;
+  float* stage[kKvMaxNW];
+  mgx_kv_seg scatter[kKvMaxSegs];
+  int8_t scatter_owner[kKvMaxSegs];
 };
+
+// flat index -> segment: last s with pre[s] <= gi
+__device__ __forceinline__ int seg_of(const int64_t* pre, int n, int64_t gi) {
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (pre[mid] <= gi) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
 
 // largest power of two strictly below n (n >= 2): kernels.py:39
 __host__ __device__ constexpr int hpow2(int n) {
@@ -89,6 +106,17 @@ __device__ __forceinline__ float4 ld_nc_v4(const float* p) {
   asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
                : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
                : "l"(p));
+  return r;
+}
+
+// coherent 128-bit load (L2, not the read-only path): for data other GPUs
+// stored during this kernel (the push-mode staging buffer)
+__device__ __forceinline__ float4 ld_cg_v4(const float* p) {
+  float4 r;
+  asm volatile("ld.global.cg.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p)
+               : "memory");
   return r;
 }
 
@@ -151,10 +179,66 @@ __global__ void __launch_bounds__(THREADS) kv_round_kernel(const __grid_constant
     if (threadIdx.x == 0) s_epoch = *reinterpret_cast<volatile uint32_t*>(p.epoch_ctr) + 1;
     __syncthreads();
   }
-  const bool live = !barrier || block_barrier<NW>(p, 0, s_epoch);
-
+  const bool push = p.nscatter > 0;
   const int64_t stride = int64_t(gridDim.x) * THREADS;
+  bool live = true;
+  if (push) {
+    // phase 1: this rank's gradient values for every owner's shard, stored
+    // into that owner's staging slot (remote writes; the previous round's
+    // closing barrier guarantees every owner finished reading its stage).
+    // The scatter list is owner-major and each owner's part lists its
+    // segments exactly as that owner's own list does, and the loop below
+    // has phase 2's thread -> element mapping: the element owner r reads in
+    // block b after the same-index barrier was written by block b here.
+    __shared__ int64_t spre[kKvMaxSegs];
+    __shared__ int64_t gtot[kKvMaxNW];
+    __shared__ int gq[kKvMaxNW + 1];
+    if (threadIdx.x == 0) {
+      int q = 0;
+      for (int o = 0; o < NW; ++o) {
+        gq[o] = q;
+        int64_t acc = 0;
+        while (q < p.nscatter && p.scatter_owner[q] == o) {
+          spre[q] = acc;  // prefix within the owner's group
+          acc += (p.scatter[q].len + 3) >> 2;
+          ++q;
+        }
+        gtot[o] = acc;
+      }
+      gq[NW] = q;
+    }
+    __syncthreads();
+    const float* gsrc = p.grads[p.rank];
+    for (int o = 0; o < NW; ++o) {
+      const int q0 = gq[o], q1 = gq[o + 1];
+      if (q0 == q1) continue;
+      const int64_t tot = gtot[o];
+      float* const dst_base = p.stage[o];
+      for (int64_t base = int64_t(blockIdx.x) * THREADS + threadIdx.x; base < tot;
+           base += stride * UNROLL) {
+        float4 v[UNROLL];
+        float* dst[UNROLL];
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u) {
+          const int64_t gi = base + u * stride;
+          dst[u] = nullptr;
+          if (gi < tot) {
+            const int q = q0 + seg_of(spre + q0, q1 - q0, gi);
+            const int64_t i = gi - spre[q];
+            v[u] = ld_nc_v4(gsrc + p.scatter[q].off + 4 * i);
+            dst[u] = dst_base + p.scatter[q].voff + 4 * i;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u)
+          if (dst[u]) st_v4(dst[u], v[u]);
+      }
+    }
+  }
+  if (barrier) live = block_barrier<NW>(p, 0, s_epoch);
+
   const float* wsrc = p.weights[p.self_replica];
+  const float* my_stage = push ? p.stage[p.rank] : nullptr;
   // One flat index space over all segments (float4 units): every thread has
   // UNROLL independent vectors in flight regardless of how many small keys
   // the round holds (a per-segment loop serialised one latency per key).
@@ -190,8 +274,14 @@ __global__ void __launch_bounds__(THREADS) kv_round_kernel(const __grid_constant
         const int64_t i = gi - pre[lo];
         eoff[u] = p.segs[lo].off + 4 * i;
         evoff[u] = p.segs[lo].voff + 4 * i;
+        if (push) {
+          // every worker's values for this shard are in the local stage
 #pragma unroll
-        for (int j = 0; j < NW; ++j) g[u][j] = ld_nc_v4(p.grads[j] + eoff[u]);
+          for (int j = 0; j < NW; ++j) g[u][j] = ld_cg_v4(my_stage + j * p.stage_slot + evoff[u]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < NW; ++j) g[u][j] = ld_nc_v4(p.grads[j] + eoff[u]);
+        }
         if (p.updater != MGX_KV_AGG) w[u] = ld_nc_v4(wsrc + eoff[u]);
         if (p.updater == MGX_KV_SGD) v[u] = *reinterpret_cast<const float4*>(p.velocity + evoff[u]);
       }
@@ -396,6 +486,26 @@ extern "C" int mgx_kv_round(const mgx_kv_round_args* a, uintptr_t stream) {
   p.neg_eta = a->neg_eta;
   p.momentum = a->momentum;
   p.weight_decay = a->weight_decay;
+  p.nscatter = a->nscatter;
+  if (a->nscatter > 0) {
+    MGX_REQUIRE(a->flags && a->scatter && a->scatter_owner && a->stage && a->stage_slot > 0 &&
+                    a->updater != MGX_KV_AGG && a->nscatter <= mgx::kKvMaxSegs,
+                "mgx_kv_round: bad push-mode arguments");
+    p.stage_slot = a->stage_slot;
+    for (int j = 0; j < NW; ++j) {
+      p.stage[j] = a->stage[j];
+      MGX_REQUIRE(p.stage[j], "mgx_kv_round: null staging pointer %d", j);
+    }
+    for (int q = 0; q < a->nscatter; ++q) {
+      const mgx_kv_seg& sg = a->scatter[q];
+      MGX_REQUIRE(sg.off % 4 == 0 && sg.voff % 4 == 0 && sg.len >= 0 && a->scatter_owner[q] >= 0 &&
+                      a->scatter_owner[q] < NW,
+                  "mgx_kv_round: bad scatter segment %d", q);
+      p.scatter[q] = sg;
+      p.scatter_owner[q] = static_cast<int8_t>(a->scatter_owner[q]);
+    }
+    MGX_REQUIRE(a->stage_slot % 4 == 0, "mgx_kv_round: stage slot not 16-byte aligned");
+  }
 
   int cap = 0;
   MGX_TRY(mgx::kv_capacity(var, &cap));

@@ -162,6 +162,8 @@ class _Arena:
     voff: Dict[Tuple[int, int], int] = field(default_factory=dict)  # (bucket, owner)
     agg: int = 0
     epoch_ctr: int = 0
+    stage: List[int] = field(default_factory=list)    # push-mode staging buffers, per worker
+    stage_slot: int = 0                                 # elements per slot of this rank's stage
     owned_local: List[int] = field(default_factory=list)  # pointers this process allocated
     opened: List[int] = field(default_factory=list)       # IPC-mapped pointers
     torch_views: Dict[Tuple[str, int], object] = field(default_factory=dict)
@@ -186,6 +188,14 @@ class KVStore:
         # barrier / explicit flush, so a whole step's keys reduce in one
         # launch (one pair of cross-GPU barriers instead of one per bucket)
         self.bucket_flush = bucket_flush
+        # push_mode: distributed rounds move every NVLink byte as a remote
+        # store (gradients scattered to their owners' staging buffers, a
+        # barrier, then weights broadcast).  Off by default: the one-phase
+        # pull round (owners load peer gradients while storing weights, both
+        # link directions busy at once) measured faster (N=2, 256 MB: 621 vs
+        # 583 GB/s busbw).  MGX_KV_PUSH=1 turns it on.
+        import os as _os
+        self.push_mode = _os.environ.get("MGX_KV_PUSH", "0") == "1"
         if machines < 1 or workers < 1:
             raise ArgumentError("topology needs machines >= 1 and workers >= 1")
         if mode not in MODES:
@@ -493,6 +503,10 @@ class KVStore:
             ar.voff[(b, self.rank)] = off
         ar.vlen = vpos
         ar.velocity = alloc(max(4 * vpos, 256))
+        # push-mode staging: one slot per worker, laid out like the momentum
+        # shard (every worker stores its gradient values for this shard there)
+        ar.stage_slot = -(-max(vpos, 1) // KEY_ALIGN) * KEY_ALIGN
+        own_s = alloc(4 * ar.stage_slot * self.nw)
         for kk in ar.keys:
             key = self._keys[kk]
             L.call("mgx_memcpy_async", own_w + 4 * key.off, key.init.ctypes.data,
@@ -504,12 +518,12 @@ class KVStore:
             L.call("mgx_ipc_get_handle", p, buf)
             return buf.raw
 
-        mine = (handle(own_w), handle(own_g), handle(own_f))
+        mine = (handle(own_w), handle(own_g), handle(own_f), handle(own_s))
         everyone: List = [None] * self.nw
         dist.all_gather_object(everyone, mine)
 
         def open_(h, own):
-            if h == mine[0] or h == mine[1] or h == mine[2]:
+            if h in mine:
                 return own
             p = ctypes.c_void_p()
             L.call("mgx_ipc_open_handle", ctypes.create_string_buffer(h, L.IPC_HANDLE_BYTES),
@@ -518,10 +532,11 @@ class KVStore:
             return p.value
 
         for r in range(self.nw):
-            hw, hg, hf = everyone[r]
+            hw, hg, hf, hs = everyone[r]
             ar.weights.append(own_w if r == self.rank else open_(hw, own_w))
             ar.grads.append(own_g if r == self.rank else open_(hg, own_g))
             ar.flags.append(own_f if r == self.rank else open_(hf, own_f))
+            ar.stage.append(own_s if r == self.rank else open_(hs, own_s))
         dist.barrier()
         # every replica starts from worker 0's init value (kvstore init
         # broadcasts one value, kvstore.py:177-181)
@@ -601,15 +616,34 @@ class KVStore:
                      for kk in keys]
             counts = [len(owner_segments(spans, ar.buckets, self.nw, r)) for r in range(self.nw)]
             nchunks = launches_for(counts, L.KV_MAX_SEGS)
+        scatter = None
+        if barrier and not custom and self.push_mode and nchunks == 1:
+            scatter = self._scatter_segments(ar, keys)
+            if len(scatter) > L.KV_MAX_SEGS:
+                scatter = None
         for c in range(nchunks):
             chunk = segs[c * L.KV_MAX_SEGS: (c + 1) * L.KV_MAX_SEGS]
             self._launch_one(ar, chunk, machines, workers, grads, weights, updater, total,
-                             barrier=barrier)
+                             barrier=barrier, scatter=scatter)
         if custom:
             self._run_custom_updater(ar, keys)
 
+    def _scatter_segments(self, ar: _Arena, keys: List[int]) -> List[Tuple[int, int, int, int]]:
+        """Push mode, phase 1: for every owner (ascending), that owner's
+        segments in its own order, with the element offset of this rank's
+        slot in the owner's staging buffer: (arena off, len, stage off, owner)."""
+        spans = [(self._keys[kk].off, padded(self._keys[kk].numel), self._keys[kk].bucket)
+                 for kk in keys]
+        out = []
+        for o in range(self.nw):
+            vb, vlen = compact_velocity_layout(ar.buckets, self.nw, o)
+            slot = -(-max(vlen, 1) // KEY_ALIGN) * KEY_ALIGN
+            for off, ln, voff in owner_segments(spans, ar.buckets, self.nw, o, vb):
+                out.append((off, ln, self.rank * slot + voff, o))
+        return out
+
     def _launch_one(self, ar, segs, machines, workers, grads, weights, updater, total,
-                    barrier: bool) -> None:
+                    barrier: bool, scatter=None) -> None:
         nw = machines * workers
         a = L.KvRoundArgs()
         seg_arr = (L.KvSeg * max(len(segs), 1))()
@@ -641,6 +675,19 @@ class KVStore:
         else:
             a.flags = None
             a.grid = 0
+        a.nscatter = 0
+        if scatter:
+            sc_arr = (L.KvSeg * len(scatter))()
+            own_arr = (ctypes.c_int32 * len(scatter))()
+            for q, (off, ln, soff, o) in enumerate(scatter):
+                sc_arr[q].off, sc_arr[q].len, sc_arr[q].voff = off, ln, soff
+                own_arr[q] = o
+            st_arr = (ctypes.c_void_p * nw)(*ar.stage)
+            a.scatter = sc_arr
+            a.scatter_owner = own_arr
+            a.nscatter = len(scatter)
+            a.stage = ctypes.cast(st_arr, ctypes.POINTER(ctypes.c_void_p))
+            a.stage_slot = ar.stage_slot
         # an eventual-mode push reduces one source; the kernel stores into
         # that many replicas, the rest are refreshed by a copy below
         broadcast_rest = nw == 1 and len(weights) > 1

@@ -18,9 +18,10 @@ def check_kv_golden(eng, world, rank, failures):
     from paper_1512_01274_b200.optim import SGDConfig, make_sgd_updater
     golden = np.load(os.path.join(ROOT, "tests", "golden", "kv_golden.npz"))
     numels = [1000, 10, 5003]
-    for bucket in (4 << 20, 4096):
+    for bucket, push in ((4 << 20, False), (4096, False), (4 << 20, True), (4096, True)):
         for upd in ("sgd", "add"):
             kv = KVStore(1, world, engine=eng, distributed=True, bucket_bytes=bucket)
+            kv.push_mode = push  # all-remote-store rounds: same tree order, bitwise
             for key, n in enumerate(numels):
                 kv.init(key, (np.random.RandomState(key).randn(n) * 0.1).astype(F32))
             if upd == "sgd":
@@ -35,7 +36,7 @@ def check_kv_golden(eng, world, rank, failures):
                 got = tmod.to_numpy(o)
                 want = golden[f"m1w{world}_{upd}_k{key}"]
                 if not np.array_equal(got, want):
-                    failures.append(f"kv {upd} bucket={bucket} key={key}: "
+                    failures.append(f"kv {upd} bucket={bucket} push={push} key={key}: "
                                     f"max diff {np.abs(got - want).max()}")
             kv.round_barrier()
             kv.close()
