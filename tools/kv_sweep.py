@@ -23,6 +23,9 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--mb", type=int, nargs="+", default=[64, 256])
     ap.add_argument("--rounds", type=int, default=20)
+    ap.add_argument("--nccl", action="store_true",
+                    help="also time NCCL all_reduce (fp32, sum) on the same sizes: the "
+                         "library baseline for the collective part alone")
     args = ap.parse_args()
     rank, world, local = (int(os.environ[k]) for k in ("RANK", "WORLD_SIZE", "LOCAL_RANK"))
     torch.cuda.set_device(local)
@@ -59,6 +62,26 @@ def main():
             print(json.dumps({"n": world, "variant": os.environ.get("MGX_KV_VARIANT", "default"),
                               "key_mb": mb, "ms": ms, "algbw": algbw,
                               "busbw": algbw * 2 * (world - 1) / world}), flush=True)
+        if args.nccl:
+            x = torch.ones(n, dtype=torch.float32, device=f"cuda:{local}")
+            for _ in range(3):
+                dist.all_reduce(x)
+            torch.cuda.synchronize()
+            dist.barrier()
+            a.record()
+            for _ in range(args.rounds):
+                dist.all_reduce(x)
+            b.record()
+            torch.cuda.synchronize()
+            t = torch.tensor([a.elapsed_time(b) / args.rounds], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            nms = float(t.item())
+            nalg = S / (nms * 1e-3) / 1e9
+            if rank == 0:
+                print(json.dumps({"n": world, "variant": "nccl_all_reduce", "key_mb": mb, "ms": nms,
+                                  "algbw": nalg, "busbw": nalg * 2 * (world - 1) / world}),
+                      flush=True)
+            del x
     dist.barrier()
     dist.destroy_process_group()
 
