@@ -282,6 +282,7 @@ def kernel_family(op: int) -> str:
         KERNEL_OF.update({
             L.OP_GEMM_TC_EX: "tc_gemm_bf16 (tcgen05)", L.OP_GEMM_TC: "tc_gemm_bf16 (tcgen05)",
             L.OP_GEMM_CONV: "tc_gemm_bf16 (tcgen05)", L.OP_WFLIP: "weight_flip",
+            L.OP_SUM_N: "sum_n", L.OP_CONCAT: "concat",
             L.OP_IM2COL: "im2col_bf16", L.OP_COL2IM: "col2im", L.OP_CAST_BF16: "cast_bf16",
             L.OP_BN_STATS: "bn_stats", L.OP_BN_APPLY: "bn_apply", L.OP_BN_BWD_REDUCE: "bn_bwd_reduce",
             L.OP_BN_BWD_DX: "bn_bwd_dx", L.OP_POOL_FWD: "pool_fwd", L.OP_POOL_BWD: "pool_bwd",

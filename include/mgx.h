@@ -219,6 +219,13 @@ int mgx_pool_forward(const float* x, float* y, const int64_t* geom, int full, in
 int mgx_pool_backward(const float* x, const float* y, const float* dy, float* dx,
                       const int64_t* geom, int full, int type, const void* argmax,
                       uintptr_t stream);
+/* out = ((srcs[0] + srcs[1]) + srcs[2]) + ... (count <= 6, n % 4 == 0): a
+ * chain of ElementwiseAdds (ops.py:222-250) in one pass, same order. */
+int mgx_sum_n(const float* const* srcs, int32_t count, float* out, int64_t n, uintptr_t stream);
+/* Concat along channels in one pass (count <= 4 inputs of rows x channels[k],
+ * channels % 4 == 0), with an optional bf16 copy of the output. */
+int mgx_concat(const float* const* srcs, const int64_t* channels, int32_t count, float* out,
+               void* out16, int64_t rows, uintptr_t stream);
 /* dst[r, doff + c] = src[r, soff + c] for r < rows, c < cols (Concat). */
 int mgx_chan_copy(const float* src, int64_t lds, int64_t soff, float* dst, int64_t ldd,
                   int64_t doff, int64_t rows, int64_t cols, void* dst16, uintptr_t stream);
@@ -302,6 +309,9 @@ typedef struct mgx_instr {
                               /* ptr5=colstats act                                 */
                               /* dims=M,N,K,lda,ldb,ldc,(a_mn|b_mn<<1),splits      */
 #define MGX_OP_WFLIP 26       /* ptr0=w ptr1=wf(bf16) dims=F,kh,kw,C,ld            */
+#define MGX_OP_SUM_N 28       /* ptr0..4=sources ptr5=out dims=n,count             */
+#define MGX_OP_CONCAT 29      /* ptr0..3=inputs ptr4=out ptr5=out16                 */
+                              /* dims=rows,count,c0,c1,c2,c3                       */
 #define MGX_OP_GEMM_CONV 27   /* ptr0=src(bf16 NHWC) ptr1=op ptr2=bias ptr3=C      */
                               /* ptr4=workspace ptr5=colstats dims=M,N,K,ldop,ldc, */
                               /* mode|splits<<8, B<<48|H<<32|W<<16|C,              */

@@ -30,7 +30,7 @@ OP_ACT_FWD, OP_ACT_BWD, OP_SOFTMAX_FWD, OP_SOFTMAX_BWD, OP_AXPY = 8, 9, 10, 11, 
 OP_CAST_BF16, OP_GEMM_TC = 13, 14
 OP_IM2COL, OP_COL2IM, OP_BN_STATS, OP_BN_APPLY, OP_BN_BWD_REDUCE, OP_BN_BWD_DX = 15, 16, 17, 18, 19, 20
 OP_POOL_FWD, OP_POOL_BWD, OP_CHAN_COPY, OP_COLSUM, OP_GEMM_TC_EX = 21, 22, 23, 24, 25
-OP_WFLIP, OP_GEMM_CONV = 26, 27
+OP_WFLIP, OP_GEMM_CONV, OP_SUM_N, OP_CONCAT = 26, 27, 28, 29
 
 KV_ADD, KV_SGD, KV_AGG = 0, 1, 2
 KV_MAX_SEGS = 256
@@ -160,6 +160,8 @@ _SIGNATURES = {
                          ctypes.c_int),
     "mgx_pool_backward": ([c_vp, c_vp, c_vp, c_vp, c_vp, ctypes.c_int, ctypes.c_int, c_vp, c_uptr],
                           ctypes.c_int),
+    "mgx_sum_n": ([c_vp, c_i32, c_vp, c_i64, c_uptr], ctypes.c_int),
+    "mgx_concat": ([c_vp, c_vp, c_i32, c_vp, c_vp, c_i64, c_uptr], ctypes.c_int),
     "mgx_chan_copy": ([c_vp, c_i64, c_i64, c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_uptr],
                       ctypes.c_int),
     "mgx_kv_max_grid": ([c_i32, c_i32, ctypes.POINTER(c_i32)], ctypes.c_int),

@@ -583,6 +583,11 @@ def _concat_lower_fwd(ins, out, attrs):
     rows, tot = prod(out.shape[:-1]), out.shape[-1]
     ok16 = tot % 8 == 0 and all(x.shape[-1] % 4 == 0 for x in ins)
     o16 = current_ctx().shadow_out(out.size) if ok16 else None
+    if ok16 and len(ins) <= 4:
+        # one pass over the output (and its bf16 copy)
+        chans = [x.shape[-1] for x in ins] + [0] * (4 - len(ins))
+        return [instr(L.OP_CONCAT, [x.ptr for x in ins] + [None] * (4 - len(ins)) + [out.ptr, o16],
+                      [rows, len(ins)] + chans)]
     code, off = [], 0
     for x in ins:
         c = x.shape[-1]

@@ -867,6 +867,61 @@ __global__ void pool_bwd_vec_kernel(const uint8_t* __restrict__ arg, const float
   }
 }
 
+// out = ((s0 + s1) + s2) + ... : a chain of ElementwiseAdds (the gradient
+// fan-in build_gradient emits, symbol.py:254-258) in one pass, same
+// left-to-right rounding order.
+struct SumSrcs {
+  const float* p[6];
+  int n;
+};
+
+__global__ void sum_n_kernel(SumSrcs src, float* __restrict__ out, int64_t n4) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += stride) {
+    float4 a = __ldg(reinterpret_cast<const float4*>(src.p[0]) + i);
+    for (int k = 1; k < src.n; ++k) {
+      const float4 b = __ldg(reinterpret_cast<const float4*>(src.p[k]) + i);
+      a.x = fadd(a.x, b.x);
+      a.y = fadd(a.y, b.y);
+      a.z = fadd(a.z, b.z);
+      a.w = fadd(a.w, b.w);
+    }
+    reinterpret_cast<float4*>(out)[i] = a;
+  }
+}
+
+// Concat along channels in one pass: out[r, :] = [in0[r, :] | in1[r, :] | ...]
+// (all channel counts % 4 == 0), with the optional bf16 copy of out.
+struct CatSrcs {
+  const float* p[4];
+  int c[4];
+  int n;
+};
+
+__global__ void concat_kernel(CatSrcs in, float* __restrict__ out, int64_t rows, int ctot,
+                              __nv_bfloat16* __restrict__ out16) {
+  const RowsIdx ri(ctot >> 2);
+  if (!ri.active) return;
+  const int col = ri.v * 4;
+  int k = 0, base = 0;
+  while (k < in.n - 1 && col >= base + in.c[k]) {
+    base += in.c[k];
+    ++k;
+  }
+  const int cc = col - base, ck = in.c[k];
+  const float* src = in.p[k];
+  for (int64_t r = ri.r; r < rows; r += ri.rstep) {
+    const float4 v = __ldg(reinterpret_cast<const float4*>(src + r * ck + cc));
+    *reinterpret_cast<float4*>(out + r * ctot + col) = v;
+    if (out16) {
+      uint2 h;
+      h.x = pack_bf16(v.x, v.y);
+      h.y = pack_bf16(v.z, v.w);
+      *reinterpret_cast<uint2*>(out16 + r * ctot + col) = h;
+    }
+  }
+}
+
 // dst[r, doff + c] = src[r, soff + c] (Concat forward / backward slices)
 __global__ void chan_copy_kernel(const float* __restrict__ src, int64_t lds, int64_t soff,
                                  float* __restrict__ dst, int64_t ldd, int64_t doff, int64_t rows,
@@ -1178,6 +1233,46 @@ extern "C" int mgx_bn_stats_from_tiles(const void* part, int64_t M, int64_t C, f
   mgx::conv::bn_stats_from_tiles_kernel<<<static_cast<unsigned>(C), 256, 0, mgx::as_stream(stream)>>>(
       static_cast<const float2*>(part), M, static_cast<int>(C), eps, momentum, stats, moving_mean,
       moving_var);
+  MGX_LAUNCHED();
+  return MGX_OK;
+}
+
+extern "C" int mgx_sum_n(const float* const* srcs, int32_t count, float* out, int64_t n,
+                         uintptr_t stream) {
+  MGX_REQUIRE(srcs && out && count >= 1 && count <= 6 && n >= 0, "mgx_sum_n: bad arguments");
+  MGX_REQUIRE(n % 4 == 0 && mgx::aligned16(out), "mgx_sum_n: needs n %% 4 == 0 and aligned data");
+  mgx::conv::SumSrcs s;
+  s.n = count;
+  for (int k = 0; k < 6; ++k) s.p[k] = k < count ? srcs[k] : nullptr;
+  for (int k = 0; k < count; ++k)
+    MGX_REQUIRE(s.p[k] && mgx::aligned16(s.p[k]), "mgx_sum_n: source %d null or unaligned", k);
+  if (n == 0) return MGX_OK;
+  mgx::conv::sum_n_kernel<<<grid_for(n / 4), 256, 0, mgx::as_stream(stream)>>>(s, out, n / 4);
+  MGX_LAUNCHED();
+  return MGX_OK;
+}
+
+extern "C" int mgx_concat(const float* const* srcs, const int64_t* channels, int32_t count,
+                          float* out, void* out16, int64_t rows, uintptr_t stream) {
+  MGX_REQUIRE(srcs && channels && out && count >= 1 && count <= 4 && rows >= 0,
+              "mgx_concat: bad arguments");
+  mgx::conv::CatSrcs in;
+  in.n = count;
+  int ctot = 0;
+  for (int k = 0; k < 4; ++k) {
+    in.p[k] = k < count ? srcs[k] : nullptr;
+    in.c[k] = k < count ? static_cast<int>(channels[k]) : 0;
+  }
+  for (int k = 0; k < count; ++k) {
+    MGX_REQUIRE(in.p[k] && in.c[k] > 0 && in.c[k] % 4 == 0 && mgx::aligned16(in.p[k]),
+                "mgx_concat: input %d needs channels %% 4 == 0 and aligned data", k);
+    ctot += in.c[k];
+  }
+  MGX_REQUIRE(mgx::aligned16(out) && (!out16 || mgx::aligned16(out16)), "mgx_concat: unaligned output");
+  if (rows == 0) return MGX_OK;
+  mgx::conv::concat_kernel<<<mgx::rows_grid(rows, ctot / 4), mgx::kRowsThreads, 0,
+                             mgx::as_stream(stream)>>>(in, out, rows, ctot,
+                                                       static_cast<__nv_bfloat16*>(out16));
   MGX_LAUNCHED();
   return MGX_OK;
 }

@@ -300,6 +300,19 @@ static int run_instr(const mgx_instr& in, cudaStream_t st) {
                                 p2, p3, d[4], d[0], d[1], d[2], in.act, static_cast<int>(d[5] >> 8),
                                 static_cast<float*>(in.ptr[4]), static_cast<float*>(in.ptr[5]), s);
     }
+    case MGX_OP_SUM_N: {
+      const float* srcs[5];
+      const int cnt = static_cast<int>(d[1]);
+      for (int k = 0; k < 5; ++k) srcs[k] = static_cast<const float*>(in.ptr[k]);
+      MGX_REQUIRE(cnt >= 1 && cnt <= 5, "program: SUM_N count %d", cnt);
+      return mgx_sum_n(srcs, cnt, static_cast<float*>(in.ptr[5]), d[0], s);
+    }
+    case MGX_OP_CONCAT: {
+      const float* srcs[4];
+      for (int k = 0; k < 4; ++k) srcs[k] = static_cast<const float*>(in.ptr[k]);
+      return mgx_concat(srcs, d + 2, static_cast<int32_t>(d[1]), static_cast<float*>(in.ptr[4]),
+                        in.ptr[5], d[0], s);
+    }
     case MGX_OP_WFLIP: return mgx_weight_flip_bf16(p0, d[0], d[1], d[2], d[3], in.ptr[1], d[4], s);
     case MGX_OP_COLSUM: return mgx_colsum(p0, d[0], d[1], in.ptr[1], p2, s);
     case MGX_OP_GEMM_TC_EX:

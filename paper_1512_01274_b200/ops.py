@@ -172,6 +172,10 @@ def instr_cost(ins: L.Instr) -> tuple:
         if op == L.OP_POOL_FWD:
             return 4 * (n_in + n_out), n_out * kh * kw
         return 4 * (2 * n_in + 2 * n_out), n_out * kh * kw
+    if op == L.OP_SUM_N:
+        return 4 * d[0] * (d[1] + 1), d[0] * (d[1] - 1)
+    if op == L.OP_CONCAT:
+        return 8 * d[0] * sum(d[2:2 + d[1]]), 0
     if op == L.OP_CHAN_COPY:
         return 8 * d[0] * d[1], 0
     if op == L.OP_COLSUM:

@@ -389,3 +389,26 @@ def test_implicit_gemm_convolution(cuda, case):
     dwr = conv2d_weight(xr, (f, c, k[0], k[1]), dy.double().reshape(b, ho, wo, f).permute(0, 3, 1, 2),
                         stride=s, padding=p).permute(0, 2, 3, 1).reshape(f, kk)
     torch.testing.assert_close(dw.double().cpu(), dwr, rtol=1e-4, atol=1e-3 * max(1, m / 64) ** 0.5)
+
+
+def test_sum_n_and_concat_kernels(cuda):
+    """One-pass ElementwiseAdd chains (same left-to-right rounding: bitwise)
+    and one-pass channel concat with its bf16 copy (exact)."""
+    torch = cuda
+    from paper_1512_01274_b200 import _lib as L
+    import ctypes
+    xs = [torch.randn(4096 * 3, device="cuda") for _ in range(4)]
+    out = torch.empty_like(xs[0])
+    arr = (ctypes.c_void_p * 4)(*[x.data_ptr() for x in xs])
+    L.call("mgx_sum_n", arr, 4, out.data_ptr(), out.numel(), 0)
+    torch.cuda.synchronize()
+    assert torch.equal(out, ((xs[0] + xs[1]) + xs[2]) + xs[3])
+    ins = [torch.randn(123, c, device="cuda") for c in (32, 64, 96, 8)]
+    cat = torch.empty(123, 200, device="cuda")
+    c16 = torch.empty(123, 200, dtype=torch.bfloat16, device="cuda")
+    arr = (ctypes.c_void_p * 4)(*[x.data_ptr() for x in ins])
+    ch = (ctypes.c_int64 * 4)(32, 64, 96, 8)
+    L.call("mgx_concat", arr, ch, 4, cat.data_ptr(), c16.data_ptr(), 123, 0)
+    torch.cuda.synchronize()
+    assert torch.equal(cat, torch.cat(ins, dim=1))
+    assert torch.equal(c16, cat.to(torch.bfloat16))

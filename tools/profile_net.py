@@ -79,6 +79,31 @@ def main():
             print(f"modeled multi-lane pass (per-instruction overhead {over * 1e3:.0f} us "
                   f"removed): {max(fin):.3f} ms; lane busy ms: "
                   + ", ".join(f"{k}:{v:.2f}" for k, v in sorted(lane_busy.items())))
+        # critical path backtrace (overhead-removed durations)
+        fin = [0.0] * len(t)
+        pred = [-1] * len(t)
+        lane_last, start_i = {}, -1
+        for i in range(len(t)):
+            if i == ex._n_fwd:
+                start_i = max(range(i), key=lambda q: fin[q]) if i else -1
+                lane_last = {}
+            d = max(t[i] - 0.002, 0.0005)
+            cands = [lane_last.get(lane[i], start_i)] + list(idx[ptr[i]:ptr[i + 1]])
+            best = max(cands, key=lambda q: fin[q] if q >= 0 else 0.0)
+            fin[i] = (fin[best] if best >= 0 else 0.0) + d
+            pred[i] = best
+            lane_last[lane[i]] = i
+        cur = max(range(len(t)), key=lambda q: fin[q])
+        path = []
+        while cur >= 0:
+            path.append(cur)
+            cur = pred[cur]
+        fams_cp = {}
+        for i in path:
+            f = bench.kernel_family(ex.instr_ops[i])
+            fams_cp[f] = fams_cp.get(f, 0.0) + max(t[i] - 0.002, 0.0005)
+        print(f"critical path: {len(path)} instructions, "
+              + ", ".join(f"{k} {v:.3f}" for k, v in sorted(fams_cp.items(), key=lambda kv: -kv[1])))
     print(f"{name}: {ex.num_instructions} instructions, {total:.3f} ms profiled pass, "
           f"kernels {ex.kernel_count()}, lanes {ex.lanes_used}")
     fams = {}
