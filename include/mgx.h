@@ -200,7 +200,8 @@ int mgx_bn_bwd_reduce(const float* dy, const float* x, const float* stats, int64
                       void* ws, float* sums, float* dbeta, float* dgamma, int dgamma_zero,
                       const float* relu_gamma, const float* relu_beta, uintptr_t stream);
 /* dx = gamma * rstd * (dy - (sum dy + xhat * sum dy*xhat) / M), with the
- * same optional ReLU mask; dy may alias dx.  ws: mgx_reduce_workspace_bytes
+ * same optional ReLU mask; dy may alias dx.  dx may be NULL when dx16 is
+ * given (every consumer reads the bf16 copy).  ws: mgx_reduce_workspace_bytes
  * (needed when C % 4 == 0).  dsum (optional): the per-channel sum of dx
  * over the rows, reduced in the same pass (the bias gradient of the
  * convolution feeding the BatchNorm). */

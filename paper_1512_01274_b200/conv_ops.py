@@ -404,7 +404,7 @@ def _bn_lower_bwd(slot, env, out, attrs):
 def bn_backward_group(og: View, relu: bool, x: View, gamma: View, beta: View, attrs,
                       xnode, dx: Optional[View], dgamma: Optional[View],
                       dbeta: Optional[View], dbias_conv: Optional[View] = None,
-                      dx_node=None) -> list:
+                      dx_node=None, dx_fp32: bool = True) -> list:
     """All requested BatchNorm gradients of one node in one pass pair (the
     executor's fusion of the sibling Backward nodes, optionally with the
     ReLU backward in front of them): one reduction that also writes dbeta /
@@ -425,7 +425,10 @@ def bn_backward_group(og: View, relu: bool, x: View, gamma: View, beta: View, at
     if dx is not None:
         dws = ctx.scratch(_reduce_ws(m, c))
         dx16 = ctx.shadow_out(dx.size, dx_node) if (c % 8 == 0 and dx_node is not None) else None
-        code.append(instr(L.OP_BN_BWD_DX, [og.ptr, x.ptr, st, sums, g, dx.ptr],
+        # dx_fp32=False: every consumer of dx reads its bf16 copy (the
+        # convolution's implicit GEMMs) -- the fp32 tensor is never stored
+        dxp = dx.ptr if (dx_fp32 or dx16 is None) else None
+        code.append(instr(L.OP_BN_BWD_DX, [og.ptr, x.ptr, st, sums, g, dxp],
                           [m, c, rb or 0, dbias_conv.ptr if dbias_conv is not None else 0, dws,
                            (g or 0) if relu else 0, dx16 or 0]))
     return code

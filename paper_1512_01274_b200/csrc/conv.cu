@@ -457,7 +457,7 @@ bn_dx_colsum_kernel(const float* dy, const float* __restrict__ x, const float* _
         acc[1] += o.y;
         acc[2] += o.z;
         acc[3] += o.w;
-        reinterpret_cast<float4*>(dx)[(r + u * rpp) * C4 + c4] = o;
+        if (dx) reinterpret_cast<float4*>(dx)[(r + u * rpp) * C4 + c4] = o;
         if (dx16) {
           uint2 h;
           h.x = pack_bf16(o.x, o.y);
@@ -475,7 +475,7 @@ bn_dx_colsum_kernel(const float* dy, const float* __restrict__ x, const float* _
       acc[1] += o.y;
       acc[2] += o.z;
       acc[3] += o.w;
-      reinterpret_cast<float4*>(dx)[i] = o;
+      if (dx) reinterpret_cast<float4*>(dx)[i] = o;
       if (dx16) {
         uint2 h;
         h.x = pack_bf16(o.x, o.y);
@@ -1099,9 +1099,12 @@ extern "C" int mgx_bn_bwd_dx(const float* dy, const float* x, const float* stats
                              const float* gamma, float* dx, int64_t M, int64_t C,
                              const float* relu_gamma, const float* relu_beta, float* dsum,
                              void* ws, void* dx16, uintptr_t stream) {
-  MGX_REQUIRE(dy && x && stats && sums && dx && M > 0 && C > 0, "mgx_bn_bwd_dx: bad arguments");
+  MGX_REQUIRE(dy && x && stats && sums && (dx || dx16) && M > 0 && C > 0,
+              "mgx_bn_bwd_dx: bad arguments");
   MGX_REQUIRE(!dx16 || (C % 4 == 0 && mgx::aligned16(dx16)), "mgx_bn_bwd_dx: bf16 copy needs C %% 4 == 0");
-  const bool vec = (C % 4) == 0 && mgx::aligned16(dy) && mgx::aligned16(x) && mgx::aligned16(dx);
+  const bool vec = (C % 4) == 0 && mgx::aligned16(dy) && mgx::aligned16(x) &&
+                   (!dx || mgx::aligned16(dx));
+  MGX_REQUIRE(dx || vec, "mgx_bn_bwd_dx: dx may only be omitted on the vectorised path");
   cudaStream_t st = mgx::as_stream(stream);
   const mgx::conv::ReluMask rm{relu_gamma, relu_beta};
   if (vec) {
