@@ -187,7 +187,8 @@ int mgx_reduce_workspace_bytes(int64_t M, int64_t C, int64_t* out);
  * moving averages when use_global. */
 int mgx_bn_stats(const float* x, int64_t M, int64_t C, void* ws, float* stats, float* moving_mean,
                  float* moving_var, float eps, float momentum, int use_global, uintptr_t stream);
-/* y = act((x - mean) * rstd * gamma + beta); gamma NULL = fix_gamma (1). */
+/* y = act((x - mean) * rstd * gamma + beta); gamma NULL = fix_gamma (1).
+ * y16 (C % 4 == 0): also a bf16 copy; y may then be NULL (copy only). */
 int mgx_bn_apply(const float* x, const float* stats, const float* gamma, const float* beta,
                  float* y, int64_t M, int64_t C, int act, void* y16, uintptr_t stream);
 /* sums = [sum dy | sum dy*xhat] per channel; also written to dbeta and

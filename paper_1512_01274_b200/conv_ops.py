@@ -354,7 +354,11 @@ def _bn_stats(x: View, attrs, ctx, code: list, update: bool, mm=None, mv=None,
 
 
 def bn_forward_instrs(ins, out: View, attrs, act: int = 0, tiles: Optional[int] = None,
-                      xnode=None) -> list:
+                      xnode=None, y_fp32: bool = True) -> list:
+    """BatchNorm (+ activation) forward: statistics, then one apply pass
+    writing the fp32 output and, when a convolution consumes it, its bf16
+    copy; ``y_fp32=False`` (the executor proved every consumer reads the
+    copy) drops the fp32 write."""
     ctx = current_ctx()
     x = ins[0]
     m, c = prod(x.shape[:-1]), x.shape[-1]
@@ -363,7 +367,8 @@ def bn_forward_instrs(ins, out: View, attrs, act: int = 0, tiles: Optional[int] 
                    tiles=tiles)
     gamma = None if attrs.get("fix_gamma", True) else ins[1].ptr
     y16 = ctx.shadow_out(out.size) if c % 8 == 0 else None
-    code.append(instr(L.OP_BN_APPLY, [x.ptr, st, gamma, ins[2].ptr, out.ptr, y16], [m, c], act=act))
+    yp = out.ptr if (y_fp32 or y16 is None) else None
+    code.append(instr(L.OP_BN_APPLY, [x.ptr, st, gamma, ins[2].ptr, yp, y16], [m, c], act=act))
     return code
 
 
@@ -454,7 +459,8 @@ register(OperatorDef(
 AUX_SUFFIXES = ("_moving_mean", "_moving_var")
 
 
-def conv_bn_instrs(cins, cout: View, cattrs, bins, bout: View, battrs, act: int, conv_node):
+def conv_bn_instrs(cins, cout: View, cattrs, bins, bout: View, battrs, act: int, conv_node,
+                   y_fp32: bool = True):
     """Convolution -> BatchNorm (-> activation) forward: the GEMM epilogue
     produces the BatchNorm statistics of its output (per 32-row (mean, M2)
     pairs), so the BatchNorm never re-reads the convolution output for its
@@ -463,7 +469,8 @@ def conv_bn_instrs(cins, cout: View, cattrs, bins, bout: View, battrs, act: int,
     m, f = prod(cout.shape[:-1]), cout.shape[-1]
     tiles = ctx.scratch(8 * (-(-m // 32)) * f)
     code = conv_forward_instrs(cins, cout, cattrs, colstats=tiles)
-    code += bn_forward_instrs(bins, bout, battrs, act=act, tiles=tiles, xnode=conv_node)
+    code += bn_forward_instrs(bins, bout, battrs, act=act, tiles=tiles, xnode=conv_node,
+                              y_fp32=y_fp32)
     return code
 
 

@@ -626,7 +626,7 @@ __global__ void bn_apply_kernel(const float* __restrict__ x, const float* __rest
         const float t = (pv[u] - mu[u]) * sc[u] * gm[u] + bt[u];
         pv[u] = act == MGX_ACT_RELU ? relu(t) : act_forward(act, t);
       }
-      reinterpret_cast<float4*>(y)[i] = v;
+      if (y) reinterpret_cast<float4*>(y)[i] = v;
       if (y16) {
         uint2 h;
         h.x = pack_bf16(v.x, v.y);
@@ -1062,10 +1062,10 @@ extern "C" int mgx_bn_stats(const float* x, int64_t M, int64_t C, void* ws, floa
 extern "C" int mgx_bn_apply(const float* x, const float* stats, const float* gamma,
                             const float* beta, float* y, int64_t M, int64_t C, int act, void* y16,
                             uintptr_t stream) {
-  MGX_REQUIRE(x && stats && beta && y && M > 0 && C > 0, "mgx_bn_apply: bad arguments");
+  MGX_REQUIRE(x && stats && beta && (y || y16) && M > 0 && C > 0, "mgx_bn_apply: bad arguments");
   MGX_REQUIRE(!y16 || (C % 4 == 0 && mgx::aligned16(y16)), "mgx_bn_apply: bf16 copy needs C %% 4 == 0");
   if ((C & 3) == 0) {
-    MGX_REQUIRE(mgx::aligned16(x) && mgx::aligned16(y), "mgx_bn_apply: unaligned tensors");
+    MGX_REQUIRE(mgx::aligned16(x) && (!y || mgx::aligned16(y)), "mgx_bn_apply: unaligned tensors");
     mgx::conv::bn_apply_kernel<<<mgx::rows_grid(M, C / 4),
                                  mgx::kRowsThreads, 0,
                                  mgx::as_stream(stream)>>>(x, stats, gamma, beta, y, M,
