@@ -215,7 +215,8 @@ int mgx_colsum(const float* x, int64_t M, int64_t C, void* ws, float* out, uintp
  * full != 0: 'full' convention (output size rounded up).  argmax (optional,
  * max only, uint8 per output element, needs C % 4 == 0 and kh*kw <= 255):
  * the window-local index of the first maximum, written by the forward and
- * read by the backward instead of rescanning x. */
+ * read by the backward instead of rescanning x.  y16 (C % 4 == 0): a bf16
+ * copy of y; y may then be NULL (copy only). */
 int mgx_pool_forward(const float* x, float* y, const int64_t* geom, int full, int type,
                      void* argmax, void* y16, uintptr_t stream);
 int mgx_pool_backward(const float* x, const float* y, const float* dy, float* dx,

@@ -536,7 +536,8 @@ def _pool_lower_fwd(ins, out, attrs):
     if arg is not None:
         ctx.memo[("argmax_fwd", id(ctx.node))] = True
     y16 = ctx.shadow_out(out.size) if (x.shape[-1] % 8 == 0 and k[0] * k[1] <= 255) else None
-    return [instr(L.OP_POOL_FWD, [x.ptr, out.ptr, arg, y16], _geom(x.shape, k, s, p) + [int(full)],
+    yp = None if (ctx.fp32_dead and y16 is not None) else out.ptr
+    return [instr(L.OP_POOL_FWD, [x.ptr, yp, arg, y16], _geom(x.shape, k, s, p) + [int(full)],
                   act=kind)]
 
 

@@ -759,60 +759,83 @@ __global__ void pool_bwd_kernel(const float* __restrict__ x, const float* __rest
 }
 
 // Channel-vectorised pooling (C % 4 == 0): a thread owns 4 channels of one
-// output (forward) or input (backward) pixel.  Max pooling records the
-// window-local index of the first maximum (uint8, row-major in the window)
-// so the backward is a cheap gather: dx(h,w) = sum of dy over the windows
-// whose recorded argmax is (h,w), windows in ascending (oh, ow) order.
-__global__ void pool_fwd_vec_kernel(const float* __restrict__ x, float* __restrict__ y,
-                                    uint8_t* __restrict__ arg, Geom g, int type,
-                                    __nv_bfloat16* __restrict__ y16) {
+// output (forward) or input (backward) pixel, items enumerated linearly over
+// (pixel, channel vector) so no lane idles whatever C is.  Max pooling
+// records the window-local index of the first maximum (uint8, row-major in
+// the window) so the backward is a cheap gather: dx(h,w) = sum of dy over the
+// windows whose recorded argmax is (h,w), windows in ascending (oh, ow)
+// order.  K, S > 0: a square K x K window with stride S known at compile
+// time (the 3x3 / stride 1-2 poolings of the nets): every tap / covering
+// window is unrolled with bounds predicates so all loads of a pixel are in
+// flight at once; K == 0: runtime geometry.  TYPE 0 max, 1 avg.
+template <int K, int S, int TYPE>
+__global__ void __launch_bounds__(256)
+pool_fwd_vec_kernel(const float* __restrict__ x, float* __restrict__ y,
+                    uint8_t* __restrict__ arg, Geom g, __nv_bfloat16* __restrict__ y16) {
   const int C4 = g.C >> 2;
-  const RowsIdx ri(C4);
-  if (!ri.active) return;
-  const int c4 = ri.v;
-  const int npix = g.B * g.Ho * g.Wo, hw = g.Ho * g.Wo;
+  const int kh = K ? K : g.kh, kw = K ? K : g.kw;
+  const int sh = K ? S : g.sh, sw = K ? S : g.sw;
+  const int hw = g.Ho * g.Wo;
+  const int64_t total = int64_t(g.B) * hw * C4;
+  const int64_t step = int64_t(gridDim.x) * blockDim.x;
   const float4* x4 = reinterpret_cast<const float4*>(x);
-  for (int pix = ri.r; pix < npix; pix += ri.rstep) {
-    const int64_t idx = int64_t(pix) * C4 + c4;
+  for (int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < total; idx += step) {
+    const int pix = static_cast<int>(idx / C4);
+    const int c4 = static_cast<int>(idx - int64_t(pix) * C4);
     const int b = pix / hw;
     const int rem = pix - b * hw;
     const int oh = rem / g.Wo, ow = rem - (rem / g.Wo) * g.Wo;
-    const int hs = oh * g.sh - g.ph, ws = ow * g.sw - g.pw;
-    const int h0 = max(hs, 0), w0 = max(ws, 0);
-    const int h1 = min(hs + g.kh, g.H), w1 = min(ws + g.kw, g.W);
+    const int hs = oh * sh - g.ph, ws = ow * sw - g.pw;
     float acc[4];
     int ai[4] = {0, 0, 0, 0};
 #pragma unroll
-    for (int q = 0; q < 4; ++q) acc[q] = type == 0 ? -INFINITY : 0.0f;
-    for (int h = h0; h < h1; ++h)
-      for (int w = w0; w < w1; ++w) {
-        const float4 v = __ldg(x4 + ((int64_t(b) * g.H + h) * g.W + w) * C4 + c4);
-        const float* pv = &v.x;
-        const int li = (h - hs) * g.kw + (w - ws);
+    for (int q = 0; q < 4; ++q) acc[q] = TYPE == 0 ? -INFINITY : 0.0f;
+    auto tap = [&](const float4 v, int li) {
+      const float* pv = &v.x;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          if (type == 0) {
-            if (pv[q] > acc[q]) {
-              acc[q] = pv[q];
-              ai[q] = li;
-            }
-          } else {
-            acc[q] = fadd(acc[q], pv[q]);
+      for (int q = 0; q < 4; ++q) {
+        if (TYPE == 0) {
+          if (pv[q] > acc[q]) {
+            acc[q] = pv[q];
+            ai[q] = li;
           }
+        } else {
+          acc[q] = fadd(acc[q], pv[q]);
         }
       }
-    float4 o;
-    if (type == 0) {
-      o = make_float4(acc[0], acc[1], acc[2], acc[3]);
-      if (arg) {
-        uchar4 a4 = make_uchar4(ai[0], ai[1], ai[2], ai[3]);
-        reinterpret_cast<uchar4*>(arg)[idx] = a4;
-      }
+    };
+    const float4* xb = x4 + int64_t(b) * g.H * g.W * C4 + c4;
+    if constexpr (K > 0) {
+      float4 v[K * K];
+      bool ok[K * K];
+#pragma unroll
+      for (int i = 0; i < K; ++i)
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+          const int h = hs + i, w = ws + j;
+          ok[i * K + j] = h >= 0 && h < g.H && w >= 0 && w < g.W;
+          v[i * K + j] = ok[i * K + j] ? __ldg(xb + (int64_t(h) * g.W + w) * C4)
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+      for (int t = 0; t < K * K; ++t)
+        if (ok[t]) tap(v[t], t);
     } else {
-      const float inv = 1.0f / pool_area(g, oh, ow);
+      const int h0 = max(hs, 0), w0 = max(ws, 0);
+      const int h1 = min(hs + kh, g.H), w1 = min(ws + kw, g.W);
+      for (int h = h0; h < h1; ++h)
+        for (int w = w0; w < w1; ++w)
+          tap(__ldg(xb + (int64_t(h) * g.W + w) * C4), (h - hs) * kw + (w - ws));
+    }
+    float4 o;
+    if (TYPE == 0) {
+      o = make_float4(acc[0], acc[1], acc[2], acc[3]);
+      if (arg) reinterpret_cast<uchar4*>(arg)[idx] = make_uchar4(ai[0], ai[1], ai[2], ai[3]);
+    } else {
+      const float inv = __frcp_rn(pool_area(g, oh, ow));
       o = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
     }
-    reinterpret_cast<float4*>(y)[idx] = o;
+    if (y) reinterpret_cast<float4*>(y)[idx] = o;
     if (y16) {
       uint2 h;
       h.x = pack_bf16(o.x, o.y);
@@ -822,46 +845,72 @@ __global__ void pool_fwd_vec_kernel(const float* __restrict__ x, float* __restri
   }
 }
 
-__global__ void pool_bwd_vec_kernel(const uint8_t* __restrict__ arg, const float* __restrict__ dy,
-                                    float* __restrict__ dx, Geom g, int type) {
+template <int K, int S, int TYPE>
+__global__ void __launch_bounds__(256)
+pool_bwd_vec_kernel(const uint8_t* __restrict__ arg, const float* __restrict__ dy,
+                    float* __restrict__ dx, Geom g) {
   const int C4 = g.C >> 2;
-  const RowsIdx ri(C4);
-  if (!ri.active) return;
-  const int c4 = ri.v;
-  const int npix = g.B * g.H * g.W, hw = g.H * g.W;
+  const int kh = K ? K : g.kh, kw = K ? K : g.kw;
+  const int sh = K ? S : g.sh, sw = K ? S : g.sw;
+  const int hw = g.H * g.W;
+  const int64_t total = int64_t(g.B) * hw * C4;
+  const int64_t step = int64_t(gridDim.x) * blockDim.x;
   const float4* dy4 = reinterpret_cast<const float4*>(dy);
   const uchar4* a4 = reinterpret_cast<const uchar4*>(arg);
-  for (int pix = ri.r; pix < npix; pix += ri.rstep) {
-    const int64_t idx = int64_t(pix) * C4 + c4;
+  for (int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < total; idx += step) {
+    const int pix = static_cast<int>(idx / C4);
+    const int c4 = static_cast<int>(idx - int64_t(pix) * C4);
     const int b = pix / hw;
     const int rem = pix - b * hw;
     const int h = rem / g.W, w = rem - (rem / g.W) * g.W;
-    const int nh = h + g.ph - g.kh + 1, nw = w + g.pw - g.kw + 1;
-    const int oh_lo = nh <= 0 ? 0 : (nh + g.sh - 1) / g.sh;
-    const int oh_hi = min(g.Ho - 1, (h + g.ph) / g.sh);
-    const int ow_lo = nw <= 0 ? 0 : (nw + g.sw - 1) / g.sw;
-    const int ow_hi = min(g.Wo - 1, (w + g.pw) / g.sw);
+    // output windows covering (h, w): oh*sh - ph <= h < oh*sh - ph + kh
+    const int nh = h + g.ph - kh + 1, nw = w + g.pw - kw + 1;
+    const int oh_lo = nh <= 0 ? 0 : (nh + sh - 1) / sh;
+    const int oh_hi = min(g.Ho - 1, (h + g.ph) / sh);
+    const int ow_lo = nw <= 0 ? 0 : (nw + sw - 1) / sw;
+    const int ow_hi = min(g.Wo - 1, (w + g.pw) / sw);
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
-    for (int oh = oh_lo; oh <= oh_hi; ++oh) {
-      const int hs = oh * g.sh - g.ph;
-      for (int ow = ow_lo; ow <= ow_hi; ++ow) {
-        const int ws = ow * g.sw - g.pw;
-        const int64_t o = ((int64_t(b) * g.Ho + oh) * g.Wo + ow) * C4 + c4;
-        const float4 d = __ldg(dy4 + o);
-        const float* pd = &d.x;
-        if (type == 0) {
-          const uchar4 am = __ldg(a4 + o);
-          const int li = (h - hs) * g.kw + (w - ws);
-          const unsigned char* pa = &am.x;
+    const int64_t ob = int64_t(b) * g.Ho * g.Wo * C4 + c4;
+    auto win = [&](int oh, int ow, const float4 d, const uchar4 am) {
+      const float* pd = &d.x;
+      if (TYPE == 0) {
+        const int li = (h - (oh * sh - g.ph)) * kw + (w - (ow * sw - g.pw));
+        const unsigned char* pa = &am.x;
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
-            if (pa[q] == li) acc[q] = fadd(acc[q], pd[q]);
-        } else {
-          const float inv = 1.0f / pool_area(g, oh, ow);
+        for (int q = 0; q < 4; ++q)
+          if (pa[q] == li) acc[q] = fadd(acc[q], pd[q]);
+      } else {
+        const float inv = __frcp_rn(pool_area(g, oh, ow));
 #pragma unroll
-          for (int q = 0; q < 4; ++q) acc[q] = fadd(acc[q], pd[q] * inv);
-        }
+        for (int q = 0; q < 4; ++q) acc[q] = fadd(acc[q], pd[q] * inv);
       }
+    };
+    if constexpr (K > 0) {
+      constexpr int NW = (K + S - 1) / S;  // covering windows per dimension
+      float4 d[NW * NW];
+      uchar4 am[NW * NW];
+#pragma unroll
+      for (int i = 0; i < NW; ++i)
+#pragma unroll
+        for (int j = 0; j < NW; ++j) {
+          const int oh = oh_lo + i, ow = ow_lo + j;
+          const bool ok = oh <= oh_hi && ow <= ow_hi;
+          const int64_t o = ob + (int64_t(oh) * g.Wo + ow) * C4;
+          d[i * NW + j] = ok ? __ldg(dy4 + o) : make_float4(0.f, 0.f, 0.f, 0.f);
+          if (TYPE == 0) am[i * NW + j] = ok ? __ldg(a4 + o) : make_uchar4(255, 255, 255, 255);
+        }
+#pragma unroll
+      for (int i = 0; i < NW; ++i)
+#pragma unroll
+        for (int j = 0; j < NW; ++j)
+          if (oh_lo + i <= oh_hi && ow_lo + j <= ow_hi)
+            win(oh_lo + i, ow_lo + j, d[i * NW + j], am[i * NW + j]);
+    } else {
+      for (int oh = oh_lo; oh <= oh_hi; ++oh)
+        for (int ow = ow_lo; ow <= ow_hi; ++ow) {
+          const int64_t o = ob + (int64_t(oh) * g.Wo + ow) * C4;
+          win(oh, ow, __ldg(dy4 + o), TYPE == 0 ? __ldg(a4 + o) : make_uchar4(0, 0, 0, 0));
+        }
     }
     reinterpret_cast<float4*>(dx)[idx] = make_float4(acc[0], acc[1], acc[2], acc[3]);
   }
@@ -1157,18 +1206,37 @@ static bool pool_vec_ok(const Geom& g, const void* a, const void* b) {
   return (g.C % 4) == 0 && mgx::aligned16(a) && mgx::aligned16(b);
 }
 
+// 10 * K + S for the square K x K / stride S windows with unrolled kernels
+static int pool_square(const Geom& g) {
+  if (g.kh == 3 && g.kw == 3 && g.sh == g.sw && (g.sh == 1 || g.sh == 2)) return 30 + g.sh;
+  return 0;
+}
+
 extern "C" int mgx_pool_forward(const float* x, float* y, const int64_t* geom, int full, int type,
                                 void* argmax, void* y16, uintptr_t stream) {
-  MGX_REQUIRE(x && y && geom && (type == 0 || type == 1), "mgx_pool_forward: bad arguments");
+  MGX_REQUIRE(x && (y || y16) && geom && (type == 0 || type == 1),
+              "mgx_pool_forward: bad arguments");
   Geom g = mgx::conv::decode(geom, full != 0);
   MGX_REQUIRE(g.Ho > 0 && g.Wo > 0, "mgx_pool_forward: bad geometry");
   cudaStream_t st = mgx::as_stream(stream);
-  if (pool_vec_ok(g, x, y) && g.kh * g.kw <= 255) {
-    mgx::conv::pool_fwd_vec_kernel<<<mgx::rows_grid(int64_t(g.B) * g.Ho * g.Wo, g.C / 4),
-                                     mgx::kRowsThreads, 0, st>>>(
-        x, y, type == 0 ? static_cast<uint8_t*>(argmax) : nullptr, g, type,
-        static_cast<__nv_bfloat16*>(y16));
+  if (pool_vec_ok(g, x, y ? y : y16) && g.kh * g.kw <= 255) {
+    const unsigned grid = grid_for(int64_t(g.B) * g.Ho * g.Wo * (g.C / 4));
+    uint8_t* arg = type == 0 ? static_cast<uint8_t*>(argmax) : nullptr;
+    __nv_bfloat16* h16 = static_cast<__nv_bfloat16*>(y16);
+    const int sq = pool_square(g) * 2 + type;
+#define MGX_POOL_FWD(K_, S_, T_) \
+  mgx::conv::pool_fwd_vec_kernel<K_, S_, T_><<<grid, 256, 0, st>>>(x, y, arg, g, h16)
+    switch (sq) {
+      case 62: MGX_POOL_FWD(3, 1, 0); break;
+      case 63: MGX_POOL_FWD(3, 1, 1); break;
+      case 64: MGX_POOL_FWD(3, 2, 0); break;
+      case 65: MGX_POOL_FWD(3, 2, 1); break;
+      case 0: MGX_POOL_FWD(0, 0, 0); break;
+      default: MGX_POOL_FWD(0, 0, 1); break;
+    }
+#undef MGX_POOL_FWD
   } else {
+    MGX_REQUIRE(y, "mgx_pool_forward: y may be NULL only on the vectorised path");
     MGX_REQUIRE(!argmax || type != 0, "mgx_pool_forward: argmax needs C %% 4 == 0 and kh*kw <= 255");
     MGX_REQUIRE(!y16, "mgx_pool_forward: a bf16 copy needs C %% 4 == 0");
     const int64_t n = int64_t(g.B) * g.Ho * g.Wo * g.C;
@@ -1187,9 +1255,20 @@ extern "C" int mgx_pool_backward(const float* x, const float* y, const float* dy
   cudaStream_t st = mgx::as_stream(stream);
   const bool use_arg = type == 0 && argmax != nullptr;
   if (pool_vec_ok(g, dy, dx) && (type == 1 || use_arg)) {
-    mgx::conv::pool_bwd_vec_kernel<<<mgx::rows_grid(int64_t(g.B) * g.H * g.W, g.C / 4),
-                                     mgx::kRowsThreads, 0, st>>>(
-        static_cast<const uint8_t*>(argmax), dy, dx, g, type);
+    const unsigned grid = grid_for(int64_t(g.B) * g.H * g.W * (g.C / 4));
+    const uint8_t* arg = static_cast<const uint8_t*>(argmax);
+    const int sq = pool_square(g) * 2 + type;
+#define MGX_POOL_BWD(K_, S_, T_) \
+  mgx::conv::pool_bwd_vec_kernel<K_, S_, T_><<<grid, 256, 0, st>>>(arg, dy, dx, g)
+    switch (sq) {
+      case 62: MGX_POOL_BWD(3, 1, 0); break;
+      case 63: MGX_POOL_BWD(3, 1, 1); break;
+      case 64: MGX_POOL_BWD(3, 2, 0); break;
+      case 65: MGX_POOL_BWD(3, 2, 1); break;
+      case 0: MGX_POOL_BWD(0, 0, 0); break;
+      default: MGX_POOL_BWD(0, 0, 1); break;
+    }
+#undef MGX_POOL_BWD
   } else {
     MGX_REQUIRE(type == 1 || (x && y), "mgx_pool_backward: max pooling needs x and y");
     const int64_t n = int64_t(g.B) * g.H * g.W * g.C;

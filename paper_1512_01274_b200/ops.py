@@ -226,6 +226,9 @@ class LowerCtx:
         self.writes: List[tuple] = []   # ... and written by it
         self.memo = _Memo(self)
         self.node = None
+        # set by the executor: the fp32 output of the node being lowered has
+        # no reader (every consumer gathers from its bf16 copy)
+        self.fp32_dead = False
         # implicit-GEMM operands: ids of nodes whose outputs feed a
         # convolution (set by the executor); out_node = the node whose
         # output the current lowering writes
