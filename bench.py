@@ -285,7 +285,8 @@ def kernel_family(op: int) -> str:
             L.OP_SUM_N: "sum_n", L.OP_CONCAT: "concat",
             L.OP_IM2COL: "im2col_bf16", L.OP_COL2IM: "col2im", L.OP_CAST_BF16: "cast_bf16",
             L.OP_BN_STATS: "bn_stats", L.OP_BN_APPLY: "bn_apply", L.OP_BN_BWD_REDUCE: "bn_bwd_reduce",
-            L.OP_BN_BWD_DX: "bn_bwd_dx", L.OP_POOL_FWD: "pool_fwd", L.OP_POOL_BWD: "pool_bwd",
+            L.OP_BN_BWD_DX: "bn_bwd_dx", L.OP_BN_FWD_FUSED: "bn_fwd_fused",
+            L.OP_BN_BWD_FUSED: "bn_bwd_fused", L.OP_POOL_FWD: "pool_fwd", L.OP_POOL_BWD: "pool_bwd",
             L.OP_CHAN_COPY: "concat_copy", L.OP_COLSUM: "colsum", L.OP_ACT_FWD: "act_fwd",
             L.OP_ACT_BWD: "act_bwd", L.OP_GEMM_PW: "gemm_pairwise", L.OP_GEMM_SEQ: "gemm_sequential",
             L.OP_DW_DB: "fc_dw_db", L.OP_SOFTMAX_FWD: "softmax_fwd", L.OP_SOFTMAX_BWD: "softmax_bwd",

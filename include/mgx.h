@@ -209,6 +209,26 @@ int mgx_bn_bwd_reduce(const float* dy, const float* x, const float* stats, int64
 int mgx_bn_bwd_dx(const float* dy, const float* x, const float* stats, const float* sums,
                   const float* gamma, float* dx, int64_t M, int64_t C, const float* relu_gamma,
                   const float* relu_beta, float* dsum, void* ws, void* dx16, uintptr_t stream);
+/* Cluster-fused BatchNorm (training) for layers whose rows fit on-chip
+ * (bn_fused.cu): a thread-block cluster owns a channel slice and all rows,
+ * stages them in shared memory once, reduces over DSMEM in a fixed order.
+ * mgx_bn_fused_ok: *ok = 1 when (M, C) has such a launch shape (C % 8 == 0,
+ * tile fits); the fused entry points reject other shapes.
+ * fwd: stats [mean | rstd] + moving averages + y = act(bn(x)) -> y (fp32,
+ * optional) / y16 (bf16, optional) in one kernel.
+ * bwd: dy' = dy masked by the fused ReLU (relu_beta non-NULL: mask
+ * (x - mean) rstd relu_gamma + relu_beta > 0); dbeta = sum dy', dgamma =
+ * sum dy' xhat (0 when dgamma_zero), sums = [dbeta | dgamma] (optional),
+ * dx = gamma rstd (dy' - (dbeta + xhat dgamma) / M) -> dx / dx16 (each
+ * optional, one required), dsum = sum dx (optional) in one kernel. */
+int mgx_bn_fused_ok(int64_t M, int64_t C, int backward, int* ok);
+int mgx_bn_fwd_fused(const float* x, int64_t M, int64_t C, float* stats, float* moving_mean,
+                     float* moving_var, float eps, float momentum, const float* gamma,
+                     const float* beta, float* y, void* y16, int act, uintptr_t stream);
+int mgx_bn_bwd_fused(const float* dy, const float* x, const float* stats, const float* gamma,
+                     int64_t M, int64_t C, const float* relu_gamma, const float* relu_beta,
+                     float* dbeta, float* dgamma, int dgamma_zero, float* sums, float* dx,
+                     void* dx16, float* dsum, uintptr_t stream);
 /* out[c] = sum over rows of x[r, c] (conv bias gradient). */
 int mgx_colsum(const float* x, int64_t M, int64_t C, void* ws, float* out, uintptr_t stream);
 /* Pooling, NHWC.  type 0 max (padding ignored), 1 avg (count_include_pad);
@@ -315,6 +335,12 @@ typedef struct mgx_instr {
 #define MGX_OP_SUM_N 28       /* ptr0..4=sources ptr5=out dims=n,count             */
 #define MGX_OP_CONCAT 29      /* ptr0..3=inputs ptr4=out ptr5=out16                 */
                               /* dims=rows,count,c0,c1,c2,c3                       */
+#define MGX_OP_BN_FWD_FUSED 30 /* ptr0=x ptr1=stats ptr2=gamma ptr3=beta ptr4=y    */
+                              /* ptr5=y16 dims=M,C,mmean*,mvar* fattr=eps,momentum */
+                              /* act                                               */
+#define MGX_OP_BN_BWD_FUSED 31 /* ptr0=dy ptr1=x ptr2=stats ptr3=gamma ptr4=dx     */
+                              /* ptr5=dx16 dims=M,C,relu_gamma*,relu_beta*,dbeta*, */
+                              /* dgamma*,dgamma_zero,dsum*                          */
 #define MGX_OP_GEMM_CONV 27   /* ptr0=src(bf16 NHWC) ptr1=op ptr2=bias ptr3=C      */
                               /* ptr4=workspace ptr5=colstats dims=M,N,K,ldop,ldc, */
                               /* mode|splits<<8, B<<48|H<<32|W<<16|C,              */

@@ -329,6 +329,26 @@ def _bn_infer(shapes, attrs):
             [tuple(data)])
 
 
+_FUSED_OK = {}
+
+
+def bn_fused_ok(m: int, c: int, backward: bool) -> bool:
+    """Whether the cluster-fused BatchNorm kernels (bn_fused.cu) take this
+    (rows, channels) shape: one launch per pass instead of 2-4."""
+    key = (m, c, bool(backward))
+    if key not in _FUSED_OK:
+        import ctypes
+        ok = ctypes.c_int(0)
+        L.call("mgx_bn_fused_ok", m, c, 1 if backward else 0, ctypes.byref(ok))
+        _FUSED_OK[key] = bool(ok.value)
+    return _FUSED_OK[key]
+
+
+def _bn_train_fused(attrs, ctx, m, c) -> bool:
+    return (ctx.training and not attrs.get("use_global_stats", False)
+            and bn_fused_ok(m, c, False))
+
+
 def _bn_stats(x: View, attrs, ctx, code: list, update: bool, mm=None, mv=None,
               xnode=None, tiles: Optional[int] = None) -> int:
     m, c = prod(x.shape[:-1]), x.shape[-1]
@@ -363,11 +383,21 @@ def bn_forward_instrs(ins, out: View, attrs, act: int = 0, tiles: Optional[int] 
     x = ins[0]
     m, c = prod(x.shape[:-1]), x.shape[-1]
     code = []
-    st = _bn_stats(x, attrs, ctx, code, update=True, mm=ins[3], mv=ins[4], xnode=xnode,
-                   tiles=tiles)
     gamma = None if attrs.get("fix_gamma", True) else ins[1].ptr
     y16 = ctx.shadow_out(out.size) if c % 8 == 0 else None
     yp = out.ptr if (y_fp32 or y16 is None) else None
+    eps = float(attrs.get("eps", 1e-3))
+    key = ("bnstats", id(xnode if xnode is not None else ctx.input_node("in0")), x.ptr, eps)
+    if tiles is None and key not in ctx.memo and _bn_train_fused(attrs, ctx, m, c):
+        # statistics + moving averages + apply in one cluster kernel
+        st = ctx.persistent(8 * c)
+        ctx.memo[key] = st
+        code.append(instr(L.OP_BN_FWD_FUSED, [x.ptr, st, gamma, ins[2].ptr, yp, y16],
+                          [m, c, ins[3].ptr if ins[3] else 0, ins[4].ptr if ins[4] else 0],
+                          [eps, float(attrs.get("momentum", 0.9))], act=act))
+        return code
+    st = _bn_stats(x, attrs, ctx, code, update=True, mm=ins[3], mv=ins[4], xnode=xnode,
+                   tiles=tiles)
     code.append(instr(L.OP_BN_APPLY, [x.ptr, st, gamma, ins[2].ptr, yp, y16], [m, c], act=act))
     return code
 
@@ -420,6 +450,17 @@ def bn_backward_group(og: View, relu: bool, x: View, gamma: View, beta: View, at
     code = []
     st = _bn_stats(x, attrs, ctx, code, update=False, xnode=xnode)
     fix = attrs.get("fix_gamma", True)
+    if dx is not None and bn_fused_ok(m, c, True):
+        # reductions + dx (+ conv bias gradient) in one cluster kernel
+        g = None if fix else gamma.ptr
+        dx16 = ctx.shadow_out(dx.size, dx_node) if (c % 8 == 0 and dx_node is not None) else None
+        dxp = dx.ptr if (dx_fp32 or dx16 is None) else None
+        code.append(instr(L.OP_BN_BWD_FUSED, [og.ptr, x.ptr, st, g, dxp, dx16],
+                          [m, c, (g or 0) if relu else 0, beta.ptr if relu else 0,
+                           dbeta.ptr if dbeta else 0, dgamma.ptr if dgamma else 0,
+                           1 if fix else 0,
+                           dbias_conv.ptr if dbias_conv is not None else 0]))
+        return code
     sums = ctx.persistent(8 * c)
     ws = ctx.scratch(_reduce_ws(m, c))
     g = None if fix else gamma.ptr
@@ -467,6 +508,12 @@ def conv_bn_instrs(cins, cout: View, cattrs, bins, bout: View, battrs, act: int,
     statistics (executor fusion)."""
     ctx = current_ctx()
     m, f = prod(cout.shape[:-1]), cout.shape[-1]
+    if _bn_train_fused(battrs, ctx, m, f):
+        # the cluster-fused BatchNorm computes its own statistics from one
+        # on-chip pass: no epilogue statistics needed
+        code = conv_forward_instrs(cins, cout, cattrs)
+        return code + bn_forward_instrs(bins, bout, battrs, act=act, xnode=conv_node,
+                                        y_fp32=y_fp32)
     tiles = ctx.scratch(8 * (-(-m // 32)) * f)
     code = conv_forward_instrs(cins, cout, cattrs, colstats=tiles)
     code += bn_forward_instrs(bins, bout, battrs, act=act, tiles=tiles, xnode=conv_node,

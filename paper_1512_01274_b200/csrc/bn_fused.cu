@@ -1,0 +1,459 @@
+// Cluster-fused BatchNorm passes for the layers whose rows fit on-chip
+// (the 27x27 / 14x14 / 7x7 stages of the convnets: a few thousand to ~50k
+// rows).  The unfused chain is statistics-partials -> finalize -> apply in
+// the forward and reduce-partials -> finalize -> dx (-> dsum finalize) in
+// the backward: 2 and 3-4 launches per layer, each re-reading the tensors
+// and most of them latency-bound at these sizes.  Here one kernel does the
+// whole pass:
+//
+//   * a thread-block cluster of CS CTAs (8 portable or 16) owns a slice of
+//     W float4 channel vectors (4W channels) and ALL M rows of it, the rows
+//     split evenly over its CTAs;
+//   * every CTA stages its rows x slice of the input(s) into shared memory
+//     with cp.async (the whole tile in flight at once), so HBM is read once;
+//   * per-thread fp32 partial sums -> fixed warp xor-tree and warp-order
+//     merges in fp64 -> each CTA publishes its partials in shared memory ->
+//     barrier.cluster -> every CTA sums the CS partials of the cluster over
+//     DSMEM in rank order (the same order everywhere: deterministic, and
+//     identical in every CTA, so no broadcast is needed);
+//   * the elementwise pass (apply / dx) then runs from shared memory.
+//
+// Same arithmetic as the unfused kernels (conv.cu: shifted sums against row
+// 0 for the statistics, xhat = (x - mean) * rstd, the ReLU mask recomputed
+// from x, dx = gamma * rstd * (dy - (s1 + xhat * s2) / M)); only the order of
+// the partial sums differs.  Reference semantics: MXNet BatchNorm
+// (reference-side operator list in SURVEY.md sec. 8f; oracle/convnet.py).
+
+#include <cooperative_groups.h>
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace mgx {
+namespace bnf {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+
+__device__ __forceinline__ uint32_t pack2(float a, float b) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// Reduce per-thread fp32 pairs (4 channels each) over the CTA's rows to
+// fp64 per-channel pairs in `out[2][4W]`: xor-tree over the lanes that share
+// a channel vector (lane % W), then the warps in order.  scratch: [kWarps][2][4W].
+template <int W>
+__device__ __forceinline__ void cta_reduce(const float* a, const float* b, double* scratch,
+                                           double* out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double da[4], db[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    da[q] = a[q];
+    db[q] = b[q];
+  }
+#pragma unroll
+  for (int off = 16; off >= W; off >>= 1) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      da[q] += __shfl_xor_sync(0xffffffffu, da[q], off);
+      db[q] += __shfl_xor_sync(0xffffffffu, db[q], off);
+    }
+  }
+  constexpr int NC = 4 * W;
+  if (lane < W) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      scratch[(warp * 2) * NC + lane * 4 + q] = da[q];
+      scratch[(warp * 2 + 1) * NC + lane * 4 + q] = db[q];
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 2 * NC) {
+    const int k = threadIdx.x / NC, c = threadIdx.x - (threadIdx.x / NC) * NC;
+    double s = 0.0;
+    for (int w = 0; w < kWarps; ++w) s += scratch[(w * 2 + k) * NC + c];
+    out[k * NC + c] = s;
+  }
+}
+
+// Sum the CS CTAs' published pairs (rank order) into `tot[2][4W]` (every CTA).
+template <int W>
+__device__ __forceinline__ void cluster_sum(cg::cluster_group& cl, double* pub, double* tot) {
+  constexpr int NC = 4 * W;
+  cl.sync();  // every CTA's pub is complete and visible
+  if (threadIdx.x < 2 * NC) {
+    const unsigned n = cl.num_blocks();
+    double s = 0.0;
+    for (unsigned r = 0; r < n; ++r) s += cl.map_shared_rank(pub, r)[threadIdx.x];
+    tot[threadIdx.x] = s;
+  }
+  __syncthreads();
+}
+
+struct Slice {
+  int64_t r0, r1;  // this CTA's rows
+  int c4;          // this thread's channel vector (global)
+  int rin, v;      // row phase / vector within the slice
+};
+
+template <int W>
+__device__ __forceinline__ Slice slice_of(const cg::cluster_group& cl, int64_t M, int64_t rows_cta) {
+  Slice s;
+  const int64_t rank = cl.block_rank();
+  s.r0 = rank * rows_cta;
+  s.r1 = s.r0 + rows_cta < M ? s.r0 + rows_cta : M;
+  s.v = threadIdx.x % W;
+  s.rin = threadIdx.x / W;
+  s.c4 = blockIdx.y * W + s.v;
+  return s;
+}
+
+// Forward: statistics (training, shifted sums against row 0), moving
+// averages, apply (+act) -> y (fp32, optional) and y16 (bf16, optional).
+template <int W>
+__global__ void __launch_bounds__(kThreads)
+bn_fwd_fused_kernel(const float* __restrict__ x, int64_t M, int C, int64_t rows_cta, float eps,
+                    float momentum, float* __restrict__ stats, float* __restrict__ mmean,
+                    float* __restrict__ mvar, const float* __restrict__ gamma,
+                    const float* __restrict__ beta, float* __restrict__ y,
+                    __nv_bfloat16* __restrict__ y16, int act) {
+  constexpr int RP = kThreads / W;  // rows per pass
+  constexpr int NC = 4 * W;
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* pub = reinterpret_cast<double*>(smem);          // [2][NC]
+  double* tot = pub + 2 * NC;                             // [2][NC]
+  double* scratch = tot + 2 * NC;                         // [kWarps][2][NC]
+  float4* tile = reinterpret_cast<float4*>(scratch + kWarps * 2 * NC);  // [rows_cta][W]
+  cg::cluster_group cl = cg::this_cluster();
+  const Slice s = slice_of<W>(cl, M, rows_cta);
+  const int C4 = C >> 2;
+  const float4* x4 = reinterpret_cast<const float4*>(x);
+  for (int64_t r = s.r0 + s.rin; r < s.r1; r += RP)
+    cp_async16(tile + (r - s.r0) * W + s.v, x4 + r * C4 + s.c4, true);
+  cp_async_commit();
+  const float4 shv = __ldg(x4 + s.c4);  // row 0: the shift of the sums
+  const float sh[4] = {shv.x, shv.y, shv.z, shv.w};
+  cp_async_wait<0>();
+  float s0[4] = {0.f, 0.f, 0.f, 0.f}, s1[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int64_t r = s.r0 + s.rin; r < s.r1; r += RP) {
+    const float4 v = tile[(r - s.r0) * W + s.v];
+    const float* pv = &v.x;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float d = pv[q] - sh[q];
+      s0[q] += d;
+      s1[q] += d * d;
+    }
+  }
+  cta_reduce<W>(s0, s1, scratch, pub);
+  cluster_sum<W>(cl, pub, tot);
+  // per-channel statistics (same formulas as bn_stats_finalize_kernel)
+  float mu[4], rs[4], gm[4], bt[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int cl_ = s.v * 4 + q, c = s.c4 * 4 + q;
+    const double dm = tot[cl_] / double(M);
+    const double mean = double(sh[q]) + dm;
+    double var = tot[NC + cl_] / double(M) - dm * dm;
+    if (var < 0.0) var = 0.0;
+    mu[q] = static_cast<float>(mean);
+    rs[q] = static_cast<float>(1.0 / sqrt(var + double(eps)));
+    gm[q] = gamma ? __ldg(gamma + c) : 1.0f;
+    bt[q] = __ldg(beta + c);
+    if (cl.block_rank() == 0 && s.rin == 0) {
+      stats[c] = mu[q];
+      stats[C + c] = rs[q];
+      if (mmean) mmean[c] = static_cast<float>(double(mmean[c]) * momentum + mean * (1.0 - momentum));
+      if (mvar) mvar[c] = static_cast<float>(double(mvar[c]) * momentum + var * (1.0 - momentum));
+    }
+  }
+  for (int64_t r = s.r0 + s.rin; r < s.r1; r += RP) {
+    float4 v = tile[(r - s.r0) * W + s.v];
+    float* pv = &v.x;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float t = (pv[q] - mu[q]) * rs[q] * gm[q] + bt[q];
+      pv[q] = act == MGX_ACT_RELU ? relu(t) : act_forward(act, t);
+    }
+    const int64_t i = r * C4 + s.c4;
+    if (y) reinterpret_cast<float4*>(y)[i] = v;
+    if (y16) {
+      uint2 h;
+      h.x = pack2(v.x, v.y);
+      h.y = pack2(v.z, v.w);
+      reinterpret_cast<uint2*>(y16)[i] = h;
+    }
+  }
+  cl.sync();  // peers may still read this CTA's pub
+}
+
+// Backward: s1 = sum dy', s2 = sum dy' * xhat (dy' = dy with the fused ReLU
+// mask), dbeta/dgamma/sums, then dx = gamma * rstd * (dy' - (s1 + xhat s2)/M)
+// -> dx (fp32, optional) / dx16 (bf16, optional), and dsum = sum dx
+// (the bias gradient of the convolution feeding the BatchNorm, optional).
+template <int W>
+__global__ void __launch_bounds__(kThreads)
+bn_bwd_fused_kernel(const float* __restrict__ dy, const float* __restrict__ x,
+                    const float* __restrict__ stats, const float* __restrict__ gamma, int64_t M,
+                    int C, int64_t rows_cta, const float* __restrict__ relu_gamma,
+                    const float* __restrict__ relu_beta, float* __restrict__ dbeta,
+                    float* __restrict__ dgamma, int dgamma_zero, float* __restrict__ sums,
+                    float* dx, __nv_bfloat16* __restrict__ dx16, float* __restrict__ dsum) {
+  constexpr int RP = kThreads / W;
+  constexpr int NC = 4 * W;
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* pub = reinterpret_cast<double*>(smem);          // [2][NC]
+  double* tot = pub + 2 * NC;                             // [2][NC]
+  double* pub2 = tot + 2 * NC;                            // [2][NC] (dsum)
+  double* scratch = pub2 + 2 * NC;                        // [kWarps][2][NC]
+  float4* tdy = reinterpret_cast<float4*>(scratch + kWarps * 2 * NC);  // [rows_cta][W]
+  float4* tx = tdy + rows_cta * W;
+  cg::cluster_group cl = cg::this_cluster();
+  const Slice s = slice_of<W>(cl, M, rows_cta);
+  const int C4 = C >> 2;
+  const float4* dy4 = reinterpret_cast<const float4*>(dy);
+  const float4* x4 = reinterpret_cast<const float4*>(x);
+  for (int64_t r = s.r0 + s.rin; r < s.r1; r += RP) {
+    cp_async16(tdy + (r - s.r0) * W + s.v, dy4 + r * C4 + s.c4, true);
+    cp_async16(tx + (r - s.r0) * W + s.v, x4 + r * C4 + s.c4, true);
+  }
+  cp_async_commit();
+  const bool relu = relu_beta != nullptr;
+  float mu[4], rs[4], gm[4], bt[4], g[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int c = s.c4 * 4 + q;
+    mu[q] = __ldg(stats + c);
+    rs[q] = __ldg(stats + C + c);
+    g[q] = gamma ? __ldg(gamma + c) : 1.0f;
+    gm[q] = relu && relu_gamma ? __ldg(relu_gamma + c) : 1.0f;
+    bt[q] = relu ? __ldg(relu_beta + c) : 0.0f;
+  }
+  cp_async_wait<0>();
+  float a0[4] = {0.f, 0.f, 0.f, 0.f}, a1[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int64_t r = s.r0 + s.rin; r < s.r1; r += RP) {
+    const int64_t l = (r - s.r0) * W + s.v;
+    const float4 d = tdy[l], xv = tx[l];
+    const float* pd = &d.x;
+    const float* px = &xv.x;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float dq = pd[q];
+      if (relu && !((px[q] - mu[q]) * rs[q] * gm[q] + bt[q] > 0.0f)) dq = 0.0f;
+      a0[q] += dq;
+      a1[q] += dq * ((px[q] - mu[q]) * rs[q]);
+    }
+  }
+  cta_reduce<W>(a0, a1, scratch, pub);
+  cluster_sum<W>(cl, pub, tot);
+  float s1[4], s2[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int cl_ = s.v * 4 + q, c = s.c4 * 4 + q;
+    s1[q] = static_cast<float>(tot[cl_]);
+    s2[q] = static_cast<float>(tot[NC + cl_]);
+    if (cl.block_rank() == 0 && s.rin == 0) {
+      if (sums) {
+        sums[c] = s1[q];
+        sums[C + c] = s2[q];
+      }
+      if (dbeta) dbeta[c] = s1[q];
+      if (dgamma) dgamma[c] = dgamma_zero ? 0.0f : s2[q];
+    }
+  }
+  const float invm = static_cast<float>(1.0 / double(M));
+  float ds[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int64_t r = s.r0 + s.rin; r < s.r1; r += RP) {
+    const int64_t l = (r - s.r0) * W + s.v;
+    const float4 d = tdy[l], xv = tx[l];
+    const float* pd = &d.x;
+    const float* px = &xv.x;
+    float4 o;
+    float* po = &o.x;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float dq = pd[q];
+      if (relu && !((px[q] - mu[q]) * rs[q] * gm[q] + bt[q] > 0.0f)) dq = 0.0f;
+      const float xhat = (px[q] - mu[q]) * rs[q];
+      po[q] = g[q] * rs[q] * (dq - (s1[q] + xhat * s2[q]) * invm);
+      ds[q] += po[q];
+    }
+    const int64_t i = r * C4 + s.c4;
+    if (dx) reinterpret_cast<float4*>(dx)[i] = o;
+    if (dx16) {
+      uint2 h;
+      h.x = pack2(o.x, o.y);
+      h.y = pack2(o.z, o.w);
+      reinterpret_cast<uint2*>(dx16)[i] = h;
+    }
+  }
+  if (dsum) {
+    const float zero[4] = {0.f, 0.f, 0.f, 0.f};
+    __syncthreads();  // scratch reuse
+    cta_reduce<W>(ds, zero, scratch, pub2);
+    cluster_sum<W>(cl, pub2, tot);
+    if (cl.block_rank() == 0 && threadIdx.x < NC)
+      dsum[blockIdx.y * NC + threadIdx.x] = static_cast<float>(tot[threadIdx.x]);
+  }
+  cl.sync();  // peers may still read this CTA's pub / pub2
+}
+
+// ------------------------------------------------------------- launch shape
+
+struct Cfg {
+  int W = 0, CS = 0;
+  int64_t rows_cta = 0;
+  size_t smem = 0;
+};
+
+inline size_t smem_bytes(int W, int64_t rows_cta, int tensors) {
+  const size_t NC = 4 * size_t(W);
+  return (3 * 2 * NC + kWarps * 2 * NC) * sizeof(double) + size_t(rows_cta) * W * 16 * tensors;
+}
+
+// Clusters of 8 (portable) then 16, slices of 8/4/2 vectors: the first shape
+// whose tile fits two CTAs per SM with >= one CTA per SM in total, else the
+// fitting shape with the most CTAs; none fits -> W == 0 (use the unfused
+// kernels).  A deterministic function of (M, C, tensors).
+inline Cfg pick(int64_t M, int64_t C, int tensors) {
+  Cfg best;
+  if (C % 8 != 0 || M < 1) return best;
+  const int64_t C4 = C / 4;
+  int64_t best_ctas = 0;
+  for (int CS : {8, 16}) {
+    for (int W : {8, 4, 2}) {
+      if (C4 % W) continue;
+      const int64_t rows = ceil_div(M, CS);
+      const size_t sm = smem_bytes(W, rows, tensors);
+      const int64_t ctas = int64_t(CS) * (C4 / W);
+      if (sm <= size_t(112) * 1024 && ctas >= kNumSMs) return Cfg{W, CS, rows, sm};
+      if (sm <= size_t(200) * 1024 && ctas > best_ctas) {
+        best = Cfg{W, CS, rows, sm};
+        best_ctas = ctas;
+      }
+    }
+  }
+  return best;
+}
+
+template <typename... Params>
+struct Launcher {
+  // one instance (and one attrs_set flag) per kernel
+  template <void (*kernel)(Params...), typename... Args>
+  static int run(const Cfg& cfg, int64_t C, cudaStream_t st, Args... args);
+};
+
+template <typename... Params>
+template <void (*kernel)(Params...), typename... Args>
+int Launcher<Params...>::run(const Cfg& cfg, int64_t C, cudaStream_t st, Args... args) {
+  static bool attrs_set = false;  // per kernel (a static of this instantiation)
+  if (!attrs_set) {
+    MGX_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  227 * 1024));
+    MGX_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    attrs_set = true;
+  }
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(cfg.CS, static_cast<unsigned>(C / 4 / cfg.W), 1);
+  lc.blockDim = dim3(kThreads, 1, 1);
+  lc.dynamicSmemBytes = cfg.smem;
+  lc.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cfg.CS;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  MGX_CUDA(cudaLaunchKernelEx(&lc, kernel, static_cast<Params>(args)...));
+  return MGX_OK;
+}
+
+template <int W, typename... Args>
+int launch_fwd(const Cfg& cfg, int64_t C, cudaStream_t st, Args... args) {
+  return Launcher<const float*, int64_t, int, int64_t, float, float, float*, float*, float*,
+                  const float*, const float*, float*, __nv_bfloat16*,
+                  int>::template run<bn_fwd_fused_kernel<W>>(cfg, C, st, args...);
+}
+
+template <int W, typename... Args>
+int launch_bwd(const Cfg& cfg, int64_t C, cudaStream_t st, Args... args) {
+  return Launcher<const float*, const float*, const float*, const float*, int64_t, int, int64_t,
+                  const float*, const float*, float*, float*, int, float*, float*,
+                  __nv_bfloat16*, float*>::template run<bn_bwd_fused_kernel<W>>(cfg, C, st,
+                                                                                  args...);
+}
+
+}  // namespace bnf
+}  // namespace mgx
+
+using mgx::bnf::Cfg;
+
+extern "C" int mgx_bn_fused_ok(int64_t M, int64_t C, int backward, int* ok) {
+  MGX_REQUIRE(ok && M > 0 && C > 0, "mgx_bn_fused_ok: bad arguments");
+  *ok = mgx::bnf::pick(M, C, backward ? 2 : 1).W != 0;
+  return MGX_OK;
+}
+
+extern "C" int mgx_bn_fwd_fused(const float* x, int64_t M, int64_t C, float* stats,
+                                float* moving_mean, float* moving_var, float eps, float momentum,
+                                const float* gamma, const float* beta, float* y, void* y16,
+                                int act, uintptr_t stream) {
+  MGX_REQUIRE(x && stats && beta && (y || y16) && M > 0 && C > 0 && C <= 65536,
+              "mgx_bn_fwd_fused: bad arguments");
+  MGX_REQUIRE(mgx::aligned16(x) && (!y || mgx::aligned16(y)) && (!y16 || mgx::aligned16(y16)),
+              "mgx_bn_fwd_fused: unaligned tensors");
+  const Cfg cfg = mgx::bnf::pick(M, C, 1);
+  MGX_REQUIRE(cfg.W != 0, "mgx_bn_fwd_fused: shape (%lld, %lld) does not fit a cluster",
+              static_cast<long long>(M), static_cast<long long>(C));
+  cudaStream_t st = mgx::as_stream(stream);
+  const int Ci = static_cast<int>(C);
+  __nv_bfloat16* h = static_cast<__nv_bfloat16*>(y16);
+  switch (cfg.W) {
+    case 8:
+      return mgx::bnf::launch_fwd<8>(cfg, C, st, x, M, Ci, cfg.rows_cta,
+                              eps, momentum, stats, moving_mean, moving_var, gamma, beta, y, h, act);
+    case 4:
+      return mgx::bnf::launch_fwd<4>(cfg, C, st, x, M, Ci, cfg.rows_cta,
+                              eps, momentum, stats, moving_mean, moving_var, gamma, beta, y, h, act);
+    default:
+      return mgx::bnf::launch_fwd<2>(cfg, C, st, x, M, Ci, cfg.rows_cta,
+                              eps, momentum, stats, moving_mean, moving_var, gamma, beta, y, h, act);
+  }
+}
+
+extern "C" int mgx_bn_bwd_fused(const float* dy, const float* x, const float* stats,
+                                const float* gamma, int64_t M, int64_t C, const float* relu_gamma,
+                                const float* relu_beta, float* dbeta, float* dgamma,
+                                int dgamma_zero, float* sums, float* dx, void* dx16, float* dsum,
+                                uintptr_t stream) {
+  MGX_REQUIRE(dy && x && stats && (dx || dx16) && M > 0 && C > 0 && C <= 65536,
+              "mgx_bn_bwd_fused: bad arguments");
+  MGX_REQUIRE(mgx::aligned16(dy) && mgx::aligned16(x) && (!dx || mgx::aligned16(dx)) &&
+                  (!dx16 || mgx::aligned16(dx16)),
+              "mgx_bn_bwd_fused: unaligned tensors");
+  const Cfg cfg = mgx::bnf::pick(M, C, 2);
+  MGX_REQUIRE(cfg.W != 0, "mgx_bn_bwd_fused: shape (%lld, %lld) does not fit a cluster",
+              static_cast<long long>(M), static_cast<long long>(C));
+  cudaStream_t st = mgx::as_stream(stream);
+  const int Ci = static_cast<int>(C);
+  __nv_bfloat16* h = static_cast<__nv_bfloat16*>(dx16);
+  switch (cfg.W) {
+    case 8:
+      return mgx::bnf::launch_bwd<8>(cfg, C, st, dy, x, stats, gamma, M,
+                              Ci, cfg.rows_cta, relu_gamma, relu_beta, dbeta, dgamma, dgamma_zero,
+                              sums, dx, h, dsum);
+    case 4:
+      return mgx::bnf::launch_bwd<4>(cfg, C, st, dy, x, stats, gamma, M,
+                              Ci, cfg.rows_cta, relu_gamma, relu_beta, dbeta, dgamma, dgamma_zero,
+                              sums, dx, h, dsum);
+    default:
+      return mgx::bnf::launch_bwd<2>(cfg, C, st, dy, x, stats, gamma, M,
+                              Ci, cfg.rows_cta, relu_gamma, relu_beta, dbeta, dgamma, dgamma_zero,
+                              sums, dx, h, dsum);
+  }
+}

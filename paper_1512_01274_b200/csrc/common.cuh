@@ -127,11 +127,12 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
-// Row-by-vector launch shape shared by the bandwidth kernels: 256-thread
-// blocks; a thread owns one vector column v of the rows (fixed per thread,
-// so its per-column constants load once) and walks rows, with
-// min(V, 256) threads per row and 256 / that rows per block pass -- no
-// 64-bit division per element, no idle lanes for narrow rows.
+// Row-by-vector launch shape shared by the bandwidth kernels: a thread
+// owns one vector column v of the rows (fixed per thread, so its per-column
+// constants load once) and walks rows, with tpr = min(V, 256) threads per
+// row and rpb = 256 / tpr rows per block pass; the block is tpr * rpb
+// threads (rows_block), so no lane idles for any V -- no 64-bit division per
+// element either.
 constexpr int kRowsThreads = 256;
 
 struct RowsIdx {
@@ -139,7 +140,7 @@ struct RowsIdx {
   bool active;
   __device__ __forceinline__ RowsIdx(int V) {
     const int tpr = V < kRowsThreads ? V : kRowsThreads;
-    const int rpb = kRowsThreads / tpr;
+    const int rpb = blockDim.x / tpr;
     const int t = threadIdx.x;
     const int rin = t / tpr;
     v = blockIdx.x * tpr + (t - rin * tpr);
@@ -149,11 +150,17 @@ struct RowsIdx {
   }
 };
 
-inline dim3 rows_grid(int64_t rows, int64_t vecs) {
-  const int64_t tpr = vecs < kRowsThreads ? vecs : kRowsThreads;
-  const int64_t rpb = kRowsThreads / (tpr < 1 ? 1 : tpr);
-  const int64_t gx = ceil_div(vecs, tpr < 1 ? 1 : tpr);
-  int64_t gy = ceil_div(rows, rpb);
+inline int rows_block(int64_t vecs) {
+  const int64_t tpr = vecs < kRowsThreads ? (vecs < 1 ? 1 : vecs) : kRowsThreads;
+  return static_cast<int>(tpr * (kRowsThreads / tpr));
+}
+
+// min_rows: rows each thread walks at least (kernels with per-thread setup)
+inline dim3 rows_grid(int64_t rows, int64_t vecs, int64_t min_rows = 1) {
+  const int64_t tpr = vecs < kRowsThreads ? (vecs < 1 ? 1 : vecs) : kRowsThreads;
+  const int64_t rpb = kRowsThreads / tpr;
+  const int64_t gx = ceil_div(vecs < 1 ? 1 : vecs, tpr);
+  int64_t gy = ceil_div(rows, rpb * (min_rows < 1 ? 1 : min_rows));
   const int64_t cap = ceil_div(int64_t(kNumSMs) * 16, gx);
   if (gy > cap) gy = cap;
   if (gy > 65535) gy = 65535;

@@ -320,22 +320,20 @@ colreduce_partial_vec_kernel(const float* __restrict__ a, const float* __restric
         }
       }
     }
-    int64_t r = r0 + r_in;
-    for (; r + (kRedUnroll - 1) * rpp < r1; r += kRedUnroll * rpp) {
+    // rounds of kRedUnroll guarded rows: a short chunk (the small layers'
+    // few rows per thread) still has all its loads in flight at once
+    for (int64_t r = r0 + r_in; r < r1; r += kRedUnroll * rpp) {
       float4 v[kRedUnroll], xv[kRedUnroll];
 #pragma unroll
       for (int u = 0; u < kRedUnroll; ++u) {
-        v[u] = __ldg(a4 + (r + u * rpp) * C4 + c4);
-        if (MODE == 1) xv[u] = __ldg(x4 + (r + u * rpp) * C4 + c4);
+        const int64_t rr = r + u * rpp;
+        v[u] = rr < r1 ? __ldg(a4 + rr * C4 + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
+        if (MODE == 1) xv[u] = rr < r1 ? __ldg(x4 + rr * C4 + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
       }
 #pragma unroll
       for (int u = 0; u < kRedUnroll; ++u)
-        red_accum<MODE>(v[u], MODE == 1 ? xv[u] : v[u], sh, mu, rs, gm, bt, relu, s0, s1);
-    }
-    for (; r < r1; r += rpp) {
-      const float4 v = __ldg(a4 + r * C4 + c4);
-      const float4 xv = MODE == 1 ? __ldg(x4 + r * C4 + c4) : v;
-      red_accum<MODE>(v, xv, sh, mu, rs, gm, bt, relu, s0, s1);
+        if (r + u * rpp < r1)
+          red_accum<MODE>(v[u], MODE == 1 ? xv[u] : v[u], sh, mu, rs, gm, bt, relu, s0, s1);
     }
   }
   if (r_in < rpp) {
@@ -371,9 +369,22 @@ __device__ __forceinline__ void merge_chunks(const double* __restrict__ ws, int 
   const int lane = threadIdx.x & 31;
   double s = 0.0, q = 0.0;
   if (c < C) {
-    for (int z = lane; z < nchunk; z += 32) {
-      s += ws[int64_t(z) * C + c];
-      if (two) q += ws[int64_t(nchunk + z) * C + c];
+    // loads batched 8 deep per lane (latency-bound otherwise), summed in
+    // the same ascending chunk order
+    constexpr int B = 8;
+    for (int z0 = lane; z0 < nchunk; z0 += 32 * B) {
+      double a[B], b[B];
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const int z = z0 + 32 * u;
+        a[u] = z < nchunk ? ws[int64_t(z) * C + c] : 0.0;
+        b[u] = (two && z < nchunk) ? ws[int64_t(nchunk + z) * C + c] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        s += a[u];
+        q += b[u];
+      }
     }
   }
 #pragma unroll
@@ -440,47 +451,33 @@ bn_dx_colsum_kernel(const float* dy, const float* __restrict__ x, const float* _
       gm[q] = relu && rm.gamma ? __ldg(rm.gamma + c) : 1.0f;
       bt[q] = relu ? __ldg(rm.beta + c) : 0.0f;
     }
-    constexpr int U = 4;
-    int64_t r = r0 + r_in;
-    for (; r + (U - 1) * rpp < r1; r += U * rpp) {
+    constexpr int U = 4;  // guarded rounds, all loads of a round in flight
+    for (int64_t r = r0 + r_in; r < r1; r += U * rpp) {
       float4 d[U], xv[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int64_t i = (r + u * rpp) * C4 + c4;
-        d[u] = reinterpret_cast<const float4*>(dy)[i];
-        xv[u] = __ldg(reinterpret_cast<const float4*>(x) + i);
+        const int64_t rr = r + u * rpp;
+        const int64_t i = rr * C4 + c4;
+        d[u] = rr < r1 ? reinterpret_cast<const float4*>(dy)[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+        xv[u] = rr < r1 ? __ldg(reinterpret_cast<const float4*>(x) + i)
+                        : make_float4(0.f, 0.f, 0.f, 0.f);
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
+        const int64_t rr = r + u * rpp;
+        if (rr >= r1) continue;
         const float4 o = bn_dx4(d[u], xv[u], mu, rs, g, s1, s2, gm, bt, relu, invm);
         acc[0] += o.x;
         acc[1] += o.y;
         acc[2] += o.z;
         acc[3] += o.w;
-        if (dx) reinterpret_cast<float4*>(dx)[(r + u * rpp) * C4 + c4] = o;
+        if (dx) reinterpret_cast<float4*>(dx)[rr * C4 + c4] = o;
         if (dx16) {
           uint2 h;
           h.x = pack_bf16(o.x, o.y);
           h.y = pack_bf16(o.z, o.w);
-          reinterpret_cast<uint2*>(dx16)[(r + u * rpp) * C4 + c4] = h;
+          reinterpret_cast<uint2*>(dx16)[rr * C4 + c4] = h;
         }
-      }
-    }
-    for (; r < r1; r += rpp) {
-      const int64_t i = r * C4 + c4;
-      const float4 o = bn_dx4(reinterpret_cast<const float4*>(dy)[i],
-                              __ldg(reinterpret_cast<const float4*>(x) + i), mu, rs, g, s1, s2,
-                              gm, bt, relu, invm);
-      acc[0] += o.x;
-      acc[1] += o.y;
-      acc[2] += o.z;
-      acc[3] += o.w;
-      if (dx) reinterpret_cast<float4*>(dx)[i] = o;
-      if (dx16) {
-        uint2 h;
-        h.x = pack_bf16(o.x, o.y);
-        h.y = pack_bf16(o.z, o.w);
-        reinterpret_cast<uint2*>(dx16)[i] = h;
       }
     }
   }
@@ -617,9 +614,7 @@ __global__ void bn_apply_kernel(const float* __restrict__ x, const float* __rest
       gm[u] = g;
       bt[u] = __ldg(beta + cc);
     }
-    for (int64_t r = ri.r; r < M; r += ri.rstep) {
-      const int64_t i = r * C4 + c4;
-      float4 v = reinterpret_cast<const float4*>(x)[i];
+    auto one = [&](float4 v, int64_t i) {
       float* pv = &v.x;
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
@@ -633,7 +628,17 @@ __global__ void bn_apply_kernel(const float* __restrict__ x, const float* __rest
         h.y = pack_bf16(v.z, v.w);
         reinterpret_cast<uint2*>(y16)[i] = h;
       }
+    };
+    constexpr int U = 4;  // rows in flight per thread
+    int64_t r = ri.r;
+    for (; r + (U - 1) * int64_t(ri.rstep) < M; r += U * int64_t(ri.rstep)) {
+      float4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = __ldg(reinterpret_cast<const float4*>(x) + (r + u * int64_t(ri.rstep)) * C4 + c4);
+#pragma unroll
+      for (int u = 0; u < U; ++u) one(v[u], (r + u * int64_t(ri.rstep)) * C4 + c4);
     }
+    for (; r < M; r += ri.rstep) one(__ldg(reinterpret_cast<const float4*>(x) + r * C4 + c4), r * C4 + c4);
   } else {
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
       const int c = static_cast<int>(i % C);
@@ -1008,9 +1013,17 @@ inline unsigned grid_for(int64_t n, int threads = 256, int64_t cap = int64_t(kNu
 }
 
 // chunking of M rows for the column reductions
-inline void chunks_for(int64_t M, int64_t* rpc, int* nchunk) {
-  // >= 256 rows per chunk (fewer partials to merge), <= 2 chunks per SM
-  int64_t n = ceil_div(M, 256);
+inline void chunks_for(int64_t M, int64_t C, int64_t* rpc, int* nchunk) {
+  // row chunks x column groups ~ 4 blocks per SM (every SM busy even at the
+  // 7x7 / 14x14 layers' few thousand rows), each thread walking >= 2 rows;
+  // a deterministic function of (M, C): the fixed merge order follows
+  const int64_t C4 = C % 4 == 0 ? C / 4 : 0;
+  const int64_t ct4 = C4 == 0 ? 0 : (C4 < kRedThreads ? C4 : kRedThreads);
+  const int64_t groups = C4 == 0 ? 1 : ceil_div(C4, ct4);
+  const int64_t rpp = C4 == 0 ? 1 : kRedThreads / ct4;
+  int64_t n = ceil_div(int64_t(4) * kNumSMs, groups);
+  const int64_t by_rows = ceil_div(M, 2 * rpp);
+  if (n > by_rows) n = by_rows;
   if (n > kMaxChunks) n = kMaxChunks;
   if (n < 1) n = 1;
   *rpc = ceil_div(M, n);
@@ -1023,7 +1036,7 @@ int launch_partial(const float* a, const float* xs, const float* stats, int64_t 
                    ReluMask rm = ReluMask{nullptr, nullptr}) {
   int64_t rpc;
   int nchunk;
-  chunks_for(M, &rpc, &nchunk);
+  chunks_for(M, C, &rpc, &nchunk);
   const bool vec = (C % 4) == 0 && aligned16(a) && (MODE != 1 || aligned16(xs));
   if (vec) {
     const int C4 = C / 4;
@@ -1031,7 +1044,7 @@ int launch_partial(const float* a, const float* xs, const float* stats, int64_t 
     const int rpp = kRedThreads / ct4;
     const size_t smem = size_t(rpp) * 2 * ct4 * 4 * sizeof(double);
     dim3 grid(nchunk, static_cast<unsigned>(ceil_div(C4, ct4)));
-    colreduce_partial_vec_kernel<MODE><<<grid, kRedThreads, smem, st>>>(a, xs, stats, M, C, rpc, ws,
+    colreduce_partial_vec_kernel<MODE><<<grid, ct4 * rpp, smem, st>>>(a, xs, stats, M, C, rpc, ws,
                                                                       rm);
   } else {
     const int tpr = C < kRedThreads ? C : kRedThreads;
@@ -1057,7 +1070,7 @@ extern "C" int mgx_reduce_workspace_bytes(int64_t M, int64_t C, int64_t* out) {
   MGX_REQUIRE(out && M > 0 && C > 0, "mgx_reduce_workspace_bytes: bad arguments");
   int64_t rpc;
   int nchunk;
-  mgx::conv::chunks_for(M, &rpc, &nchunk);
+  mgx::conv::chunks_for(M, C, &rpc, &nchunk);
   *out = int64_t(2) * nchunk * C * 8;
   return MGX_OK;
 }
@@ -1072,7 +1085,7 @@ extern "C" int mgx_im2col_bf16(const float* x, void* col, const int64_t* geom, i
   MGX_REQUIRE(mgx::aligned16(x) && mgx::aligned16(col), "mgx_im2col_bf16: unaligned");
   MGX_REQUIRE(int64_t(g.B) * g.Ho * g.Wo < (1ll << 31), "mgx_im2col_bf16: too many rows");
   mgx::conv::im2col_kernel<<<mgx::rows_grid(int64_t(g.B) * g.Ho * g.Wo, ldk / 8),
-                             mgx::kRowsThreads, 0,
+                             mgx::rows_block(ldk / 8), 0,
                              mgx::as_stream(stream)>>>(x, static_cast<__nv_bfloat16*>(col), g, ldk);
   MGX_LAUNCHED();
   return MGX_OK;
@@ -1115,8 +1128,8 @@ extern "C" int mgx_bn_apply(const float* x, const float* stats, const float* gam
   MGX_REQUIRE(!y16 || (C % 4 == 0 && mgx::aligned16(y16)), "mgx_bn_apply: bf16 copy needs C %% 4 == 0");
   if ((C & 3) == 0) {
     MGX_REQUIRE(mgx::aligned16(x) && (!y || mgx::aligned16(y)), "mgx_bn_apply: unaligned tensors");
-    mgx::conv::bn_apply_kernel<<<mgx::rows_grid(M, C / 4),
-                                 mgx::kRowsThreads, 0,
+    mgx::conv::bn_apply_kernel<<<mgx::rows_grid(M, C / 4, 4),
+                                 mgx::rows_block(C / 4), 0,
                                  mgx::as_stream(stream)>>>(x, stats, gamma, beta, y, M,
                                                            static_cast<int>(C), act,
                                                            static_cast<__nv_bfloat16*>(y16));
@@ -1162,7 +1175,7 @@ extern "C" int mgx_bn_bwd_dx(const float* dy, const float* x, const float* stats
     MGX_REQUIRE(!dsum || ws, "mgx_bn_bwd_dx: dsum needs a workspace");
     int64_t rpc;
     int nchunk;
-    mgx::conv::chunks_for(M, &rpc, &nchunk);
+    mgx::conv::chunks_for(M, C, &rpc, &nchunk);
     const int C4 = static_cast<int>(C / 4);
     const int ct4 = C4 < mgx::conv::kRedThreads ? C4 : mgx::conv::kRedThreads;
     const int rpp = mgx::conv::kRedThreads / ct4;
@@ -1174,7 +1187,7 @@ extern "C" int mgx_bn_bwd_dx(const float* dy, const float* x, const float* stats
       MGX_REQUIRE(ws, "mgx_bn_bwd_dx: the vectorised pass needs a workspace");
       wsd = static_cast<double*>(ws);
     }
-    mgx::conv::bn_dx_colsum_kernel<<<grid, mgx::conv::kRedThreads, smem, st>>>(
+    mgx::conv::bn_dx_colsum_kernel<<<grid, ct4 * rpp, smem, st>>>(
         dy, x, stats, sums, gamma, dx, rm, M, static_cast<int>(C), rpc, wsd,
         static_cast<__nv_bfloat16*>(dx16));
     if (dsum)
@@ -1287,7 +1300,7 @@ extern "C" int mgx_chan_copy(const float* src, int64_t lds, int64_t soff, float*
   if (rows == 0 || cols == 0) return MGX_OK;
   if (((cols | lds | soff | ldd | doff) & 3) == 0)
     mgx::conv::chan_copy_kernel<<<mgx::rows_grid(rows, cols / 4),
-                                  mgx::kRowsThreads, 0,
+                                  mgx::rows_block(cols / 4), 0,
                                   mgx::as_stream(stream)>>>(src, lds, soff, dst, ldd, doff, rows, cols,
                                                             static_cast<__nv_bfloat16*>(dst16));
   else
@@ -1352,7 +1365,7 @@ extern "C" int mgx_concat(const float* const* srcs, const int64_t* channels, int
   }
   MGX_REQUIRE(mgx::aligned16(out) && (!out16 || mgx::aligned16(out16)), "mgx_concat: unaligned output");
   if (rows == 0) return MGX_OK;
-  mgx::conv::concat_kernel<<<mgx::rows_grid(rows, ctot / 4), mgx::kRowsThreads, 0,
+  mgx::conv::concat_kernel<<<mgx::rows_grid(rows, ctot / 4), mgx::rows_block(ctot / 4), 0,
                              mgx::as_stream(stream)>>>(in, out, rows, ctot,
                                                        static_cast<__nv_bfloat16*>(out16));
   MGX_LAUNCHED();

@@ -877,7 +877,7 @@ extern "C" int mgx_cast_bf16_2d(const float* x, int64_t R, int64_t C, int64_t ld
               "mgx_cast_bf16_2d: destination smaller than the source");
   cudaStream_t st = mgx::as_stream(stream);
   if (!transpose && ldo % 8 == 0 && mgx::aligned16(y)) {
-    mgx::tc::cast_rows_kernel<<<mgx::rows_grid(rows, ldo / 8), mgx::kRowsThreads, 0, st>>>(
+    mgx::tc::cast_rows_kernel<<<mgx::rows_grid(rows, ldo / 8), mgx::rows_block(ldo / 8), 0, st>>>(
         x, R, C, ldi, static_cast<__nv_bfloat16*>(y), rows, ldo);
   } else if (!transpose) {
     MGX_REQUIRE(false, "mgx_cast_bf16_2d: ldo must be a multiple of 8 and y 16-byte aligned");

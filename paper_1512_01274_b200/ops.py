@@ -162,6 +162,10 @@ def instr_cost(ins: L.Instr) -> tuple:
         return 8 * d[0] * d[1], 4 * d[0] * d[1]
     if op == L.OP_BN_BWD_DX:
         return 12 * d[0] * d[1], 6 * d[0] * d[1]
+    if op == L.OP_BN_FWD_FUSED:  # read x once, write y and/or y16
+        return (4 + (4 if has[4] else 0) + (2 if has[5] else 0)) * d[0] * d[1], 6 * d[0] * d[1]
+    if op == L.OP_BN_BWD_FUSED:  # read dy and x once, write dx and/or dx16
+        return (8 + (4 if has[4] else 0) + (2 if has[5] else 0)) * d[0] * d[1], 10 * d[0] * d[1]
     if op in (L.OP_POOL_FWD, L.OP_POOL_BWD):
         b, h, w, c = d[0], d[1], d[2], d[3]
         kh, kw, sh, sw, ph, pw = d[4] >> 16, d[4] & 0xFFFF, d[5] >> 16, d[5] & 0xFFFF, d[6] >> 16, d[6] & 0xFFFF

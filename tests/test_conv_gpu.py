@@ -322,6 +322,86 @@ def test_batchnorm_backward_with_fused_relu(cuda, m, c, fix_gamma):
                                    rtol=1e-4, atol=2e-7 * mag)
 
 
+@pytest.mark.parametrize("m,c", [(12544, 96), (3136, 1024), (46656, 64), (1001, 40), (97, 8),
+                                 (12544, 576)])
+@pytest.mark.parametrize("fix_gamma,relu", [(True, True), (False, False), (False, True)])
+def test_batchnorm_cluster_fused(cuda, m, c, fix_gamma, relu):
+    """The cluster-fused BatchNorm passes (one kernel per pass, rows staged
+    on-chip, DSMEM reduction) against the float64 oracle, and against the
+    unfused statistics kernel for the values the backward consumes."""
+    torch = cuda
+    from paper_1512_01274_b200 import _lib as L
+    import ctypes
+    ok = ctypes.c_int()
+    L.call("mgx_bn_fused_ok", m, c, 1, ctypes.byref(ok))
+    assert ok.value == 1
+    L.call("mgx_bn_fused_ok", m, 12, 1, ctypes.byref(ok))
+    assert ok.value == 0  # C % 8 != 0: the unfused kernels
+    g = torch.Generator().manual_seed(m + 3 * c)
+    x = (torch.randn(m, c, generator=g, dtype=torch.float64) * 2 + 0.7).float().cuda()
+    gamma = (torch.rand(c, generator=g, dtype=torch.float64) + 0.5).float().cuda()
+    beta = torch.randn(c, generator=g, dtype=torch.float64).float().cuda()
+    og = torch.randn(m, c, generator=g, dtype=torch.float64).float().cuda()
+    gp = None if fix_gamma else gamma.data_ptr()
+    act = 1 if relu else 0  # MGX_ACT_RELU
+    st = torch.empty(2 * c, device="cuda")
+    mm, mv = torch.zeros(c, device="cuda"), torch.ones(c, device="cuda")
+    y = torch.empty(m, c, device="cuda")
+    y16 = torch.empty(m, c, dtype=torch.bfloat16, device="cuda")
+    L.call("mgx_bn_fwd_fused", x.data_ptr(), m, c, st.data_ptr(), mm.data_ptr(), mv.data_ptr(),
+           1e-3, 0.9, gp, beta.data_ptr(), y.data_ptr(), y16.data_ptr(), act, 0)
+    dx = torch.empty(m, c, device="cuda")
+    dx16 = torch.empty(m, c, dtype=torch.bfloat16, device="cuda")
+    dbeta = torch.full((c,), float("nan"), device="cuda")
+    dgamma = torch.full((c,), float("nan"), device="cuda")
+    sums = torch.empty(2 * c, device="cuda")
+    dsum = torch.empty(c, device="cuda")
+    L.call("mgx_bn_bwd_fused", og.data_ptr(), x.data_ptr(), st.data_ptr(), gp, m, c,
+           gp if relu else None, beta.data_ptr() if relu else None, dbeta.data_ptr(),
+           dgamma.data_ptr(), 1 if fix_gamma else 0, sums.data_ptr(), dx.data_ptr(),
+           dx16.data_ptr(), dsum.data_ptr(), 0)
+    # the unfused statistics for comparison
+    wsb = ctypes.c_int64()
+    L.call("mgx_reduce_workspace_bytes", m, c, ctypes.byref(wsb))
+    ws = torch.empty(wsb.value // 4 + 1, device="cuda")
+    st2 = torch.empty(2 * c, device="cuda")
+    L.call("mgx_bn_stats", x.data_ptr(), m, c, ws.data_ptr(), st2.data_ptr(), None, None, 1e-3,
+           0.9, 0, 0)
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(st.cpu().numpy(), st2.cpu().numpy(), rtol=2e-6, atol=1e-6)
+    assert torch.equal(y16, y.to(torch.bfloat16))
+    assert torch.equal(dx16, dx.to(torch.bfloat16))
+    assert torch.equal(sums[:c], dbeta)
+    xr = x.double().cpu().requires_grad_(True)
+    gr = gamma.double().cpu().requires_grad_(True)
+    br = beta.double().cpu().requires_grad_(True)
+    yr, mean, var = oc.batchnorm(xr, gr, br, 1e-3, fix_gamma)
+    if relu:
+        yr = torch.relu(yr)
+    (yr * og.double().cpu()).sum().backward()
+    np.testing.assert_allclose(y.cpu().numpy(), yr.detach().numpy(), rtol=1e-5, atol=2e-5)
+    np.testing.assert_allclose(mm.cpu().numpy(), (0.1 * mean).detach().numpy(), rtol=1e-5,
+                               atol=1e-6)
+    np.testing.assert_allclose(mv.cpu().numpy(), (0.9 + 0.1 * var).detach().numpy(), rtol=1e-5,
+                               atol=1e-6)
+    np.testing.assert_allclose(dx.cpu().numpy(), xr.grad.numpy(), rtol=1e-4, atol=1e-5)
+    np.testing.assert_allclose(dbeta.cpu().numpy(), br.grad.numpy(), rtol=1e-5, atol=1e-4)
+    if fix_gamma:
+        assert torch.count_nonzero(dgamma).item() == 0
+    else:
+        np.testing.assert_allclose(dgamma.cpu().numpy(), gr.grad.numpy(), rtol=1e-5, atol=1e-4)
+    mag = float(dx.double().abs().sum(0).max())
+    np.testing.assert_allclose(dsum.cpu().numpy(), dx.double().sum(0).cpu().numpy(),
+                               rtol=1e-4, atol=2e-7 * mag)
+    # deterministic: a second run is bitwise identical
+    dx_b = torch.empty_like(dx)
+    L.call("mgx_bn_bwd_fused", og.data_ptr(), x.data_ptr(), st.data_ptr(), gp, m, c,
+           gp if relu else None, beta.data_ptr() if relu else None, None, None, 0, None,
+           dx_b.data_ptr(), None, None, 0)
+    torch.cuda.synchronize()
+    assert torch.equal(dx_b, dx)
+
+
 IMPLICIT_CASES = [
     # (B, H, W, C, F, k, s, p)
     (2, 9, 7, 16, 24, (3, 3), (1, 1), (1, 1)),
