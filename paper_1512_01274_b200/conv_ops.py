@@ -114,6 +114,16 @@ def _splitk_ws(m: int, n: int, k: int) -> int:
     return out.value
 
 
+def _auto_split(m: int, n: int, k: int, ctx):
+    """(splits, workspace) for a GEMM with fewer output tiles than SMs:
+    split-K over the K loop (deterministic in-order reduce) so every SM
+    works; (1, None) when the tiles already fill the GPU."""
+    nws = _splitk_ws(m, n, k)
+    if not nws:
+        return 1, None
+    return 0, ctx.scratch(4 * nws)
+
+
 def _weights_bf16(w: View, ctx, code: list):
     """wb[F, ldk] bf16 (zero K padding) of a convolution weight; once per
     step (memo on the weight node)."""
@@ -201,11 +211,13 @@ def conv_forward_instrs(ins, out, attrs, colstats: Optional[int] = None) -> list
         b, h, wd, c = x.shape
         ho, wo = _conv_out(h, wd, k, s, p)
         kk = k[0] * k[1] * c
+        sp, ws = (1, None) if colstats else _auto_split(b * ho * wo, f, kk, ctx)
         code.append(_gemm_conv(1, sh, x.shape, k, s, p, wb, ldk, out.ptr, f, b * ho * wo, f, kk,
-                               bias=bias, colstats=colstats))
+                               bias=bias, colstats=colstats, splits=sp, ws=ws))
         return code
     col, wb, (m, kk, ldk, f, *_r) = _conv_operands(x, w, attrs, ctx, code)
-    g = _gemm(col, ldk, False, wb, ldk, False, out.ptr, f, m, f, kk, bias=bias)
+    sp, ws = (1, None) if colstats else _auto_split(m, f, kk, ctx)
+    g = _gemm(col, ldk, False, wb, ldk, False, out.ptr, f, m, f, kk, bias=bias, splits=sp, ws=ws)
     g.ptr[5] = colstats or None
     code.append(g)
     return code
@@ -260,7 +272,8 @@ def _conv_lower_bwd(slot, env, out, attrs):
     dyb, ldf = _conv_dy(og, f, ctx, code)
     wb, ldk = _weights_bf16(w, ctx, code)
     if k == (1, 1) and s == (1, 1) and p == (0, 0):
-        code.append(_gemm(dyb, ldf, False, wb, ldk, True, out.ptr, c, m, c, f))
+        sp, ws = _auto_split(m, c, f, ctx)
+        code.append(_gemm(dyb, ldf, False, wb, ldk, True, out.ptr, c, m, c, f, splits=sp, ws=ws))
         return code
     if s == (1, 1) and p[0] < k[0] and p[1] < k[1]:
         # stride 1: dX = conv(dY, flipped W, pad k-1-p): implicit GEMM over
@@ -274,16 +287,19 @@ def _conv_lower_bwd(slot, env, out, attrs):
                            lambda dst: [instr(L.OP_WFLIP, [w.ptr, dst], [f, k[0], k[1], c, ldkf])],
                            (w.ptr, w.ptr + 4 * w.size))
         pf = (k[0] - 1 - p[0], k[1] - 1 - p[1])
+        sp, ws = _auto_split(b * h * wd, c, kf, ctx)
         if f % 8 == 0:
             code.append(_gemm_conv(1, dyb, og.shape, k, (1, 1), pf, wfl, ldkf, out.ptr, c,
-                                   b * h * wd, c, kf))
+                                   b * h * wd, c, kf, splits=sp, ws=ws))
             return code
         dcolt = ctx.scratch(2 * b * h * wd * ldkf)
         code.append(instr(L.OP_IM2COL, [og.ptr, dcolt], _geom(og.shape, k, (1, 1), pf) + [ldkf]))
-        code.append(_gemm(dcolt, ldkf, False, wfl, ldkf, False, out.ptr, c, b * h * wd, c, kf))
+        code.append(_gemm(dcolt, ldkf, False, wfl, ldkf, False, out.ptr, c, b * h * wd, c, kf,
+                          splits=sp, ws=ws))
         return code
     dcol = ctx.scratch(4 * m * kk)
-    code.append(_gemm(dyb, ldf, False, wb, ldk, True, dcol, kk, m, kk, f))
+    sp, ws = _auto_split(m, kk, f, ctx)
+    code.append(_gemm(dyb, ldf, False, wb, ldk, True, dcol, kk, m, kk, f, splits=sp, ws=ws))
     code.append(instr(L.OP_COL2IM, [dcol, out.ptr], _geom(x.shape, k, s, p) + [kk]))
     return code
 

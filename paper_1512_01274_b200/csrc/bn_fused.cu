@@ -26,6 +26,7 @@
 
 #include <cooperative_groups.h>
 #include <cuda_bf16.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 
@@ -34,7 +35,8 @@ namespace cg = cooperative_groups;
 namespace mgx {
 namespace bnf {
 
-constexpr int kThreads = 256;
+constexpr int kThreads = 512;
+constexpr int kStages = 4;  // cp.async commit groups per tile (load/compute overlap)
 constexpr int kWarps = kThreads / 32;
 
 __device__ __forceinline__ uint32_t pack2(float a, float b) {
@@ -42,81 +44,170 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
-// Reduce per-thread fp32 pairs (4 channels each) over the CTA's rows to
-// fp64 per-channel pairs in `out[2][4W]`: xor-tree over the lanes that share
-// a channel vector (lane % W), then the warps in order.  scratch: [kWarps][2][4W].
+// ---- cluster exchange without cluster-wide barriers in the hot path: each
+// CTA pushes its partials into every peer's receive slot with st.async,
+// which completes transaction bytes on the destination's mbarrier; a CTA
+// waits only on its own mbarrier (all CS partials arrived), then sums them
+// in rank order from local shared memory.  The mbarriers are initialised
+// at kernel start and published with one relaxed cluster arrive whose wait
+// sits just before the first push (long since satisfied by then).
+
+__device__ __forceinline__ uint32_t mapa(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_async_f64(uint32_t raddr, double v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(raddr),
+               "l"(__double_as_longlong(v)), "r"(rbar)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+}
+
+// Per-thread fp32 pairs (4 channels each) -> the CTA's per-channel pairs,
+// returned by thread j < 2*4W as element j ([2][4W] order): fp32 xor-tree
+// over the lanes sharing a channel vector (lane % W), then the warp sums in
+// order in fp64.  scratch: [kWarps][2][4W] doubles.
 template <int W>
-__device__ __forceinline__ void cta_reduce(const float* a, const float* b, double* scratch,
-                                           double* out) {
+__device__ __forceinline__ double cta_reduce(const float* a, const float* b, double* scratch) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double da[4], db[4];
+  float fa[4], fb[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    da[q] = a[q];
-    db[q] = b[q];
+    fa[q] = a[q];
+    fb[q] = b[q];
   }
 #pragma unroll
   for (int off = 16; off >= W; off >>= 1) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      da[q] += __shfl_xor_sync(0xffffffffu, da[q], off);
-      db[q] += __shfl_xor_sync(0xffffffffu, db[q], off);
+      fa[q] += __shfl_xor_sync(0xffffffffu, fa[q], off);
+      fb[q] += __shfl_xor_sync(0xffffffffu, fb[q], off);
     }
   }
   constexpr int NC = 4 * W;
   if (lane < W) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      scratch[(warp * 2) * NC + lane * 4 + q] = da[q];
-      scratch[(warp * 2 + 1) * NC + lane * 4 + q] = db[q];
+      scratch[(warp * 2) * NC + lane * 4 + q] = fa[q];
+      scratch[(warp * 2 + 1) * NC + lane * 4 + q] = fb[q];
     }
   }
   __syncthreads();
+  double s = 0.0;
   if (threadIdx.x < 2 * NC) {
     const int k = threadIdx.x / NC, c = threadIdx.x - (threadIdx.x / NC) * NC;
-    double s = 0.0;
-    for (int w = 0; w < kWarps; ++w) s += scratch[(w * 2 + k) * NC + c];
-    out[k * NC + c] = s;
+    double v[kWarps];  // all loads first, then the in-order sum
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) v[w] = scratch[(w * 2 + k) * NC + c];
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) s += v[w];
   }
+  return s;
 }
 
-// Sum the CS CTAs' published pairs (rank order) into `tot[2][4W]` (every CTA).
+// Cluster sum of the CTA pairs: thread j < 2*4W pushes its value into slot
+// [my rank][j] of every CTA's `recv` ([16][2][4W] doubles) on mbarrier `bar`;
+// then every CTA waits for its CS * 2 * 4W * 8 bytes and sums the slots in
+// rank order into tot[2][4W].
 template <int W>
-__device__ __forceinline__ void cluster_sum(cg::cluster_group& cl, double* pub, double* tot) {
-  constexpr int NC = 4 * W;
-  cl.sync();  // every CTA's pub is complete and visible
-  if (threadIdx.x < 2 * NC) {
-    const unsigned n = cl.num_blocks();
+__device__ __forceinline__ void cluster_sum(double v, double* recv, uint64_t* bar, int parity,
+                                            unsigned rank, unsigned n, double* tot) {
+  constexpr int NC2 = 8 * W;  // 2 * 4W
+  const uint32_t rbase = smem_u32(recv), bbase = smem_u32(bar);
+  if (threadIdx.x == 0) mbar_expect(bbase, n * NC2 * 8u);
+  if (threadIdx.x < NC2) {
+    const uint32_t off = (rank * NC2 + threadIdx.x) * 8u;
+    for (unsigned r = 0; r < n; ++r) st_async_f64(mapa(rbase + off, r), v, mapa(bbase, r));
+  }
+  mbar_wait(bbase, parity);
+  if (threadIdx.x < NC2) {
+    double x[16];
+#pragma unroll
+    for (unsigned r = 0; r < 16; ++r) x[r] = r < n ? recv[r * NC2 + threadIdx.x] : 0.0;
     double s = 0.0;
-    for (unsigned r = 0; r < n; ++r) s += cl.map_shared_rank(pub, r)[threadIdx.x];
+#pragma unroll
+    for (unsigned r = 0; r < 16; ++r) s += x[r];
     tot[threadIdx.x] = s;
   }
   __syncthreads();
 }
 
 struct Slice {
-  int64_t r0, r1;  // this CTA's rows
-  int c4;          // this thread's channel vector (global)
-  int rin, v;      // row phase / vector within the slice
+  int r0, r1;  // this CTA's rows
+  int c4;      // this thread's channel vector (global)
+  int rin, v;  // row phase / vector within the slice
+  int per;     // loop iterations per stage (uniform over the CTA)
 };
 
 template <int W>
-__device__ __forceinline__ Slice slice_of(const cg::cluster_group& cl, int64_t M, int64_t rows_cta) {
+__device__ __forceinline__ Slice slice_of(const cg::cluster_group& cl, int M, int rows_cta) {
+  constexpr int RP = kThreads / W;
   Slice s;
-  const int64_t rank = cl.block_rank();
+  const int rank = static_cast<int>(cl.block_rank());
   s.r0 = rank * rows_cta;
   s.r1 = s.r0 + rows_cta < M ? s.r0 + rows_cta : M;
   s.v = threadIdx.x % W;
   s.rin = threadIdx.x / W;
   s.c4 = blockIdx.y * W + s.v;
+  const int iters = (rows_cta + RP - 1) / RP;
+  s.per = (iters + kStages - 1) / kStages;
   return s;
+}
+
+__device__ __forceinline__ void wait_stage(int left) {
+  switch (left) {
+    case 0: cp_async_wait<0>(); break;
+    case 1: cp_async_wait<1>(); break;
+    case 2: cp_async_wait<2>(); break;
+    default: cp_async_wait<3>(); break;
+  }
+}
+
+// Stage the thread's rows of `n` tensors into shared memory: kStages commit
+// groups of s.per row-iterations each (local row l = rin + k * RP).
+template <int W, int N>
+__device__ __forceinline__ void stage_in(const Slice& s, const float4* const (&src)[N],
+                                         float4* const (&dst)[N], int C4) {
+  constexpr int RP = kThreads / W;
+  for (int st = 0; st < kStages; ++st) {
+    for (int k = st * s.per; k < (st + 1) * s.per; ++k) {
+      const int r = s.r0 + s.rin + k * RP;
+      if (r >= s.r1) break;
+      const int l = (s.rin + k * RP) * W + s.v;
+#pragma unroll
+      for (int t = 0; t < N; ++t) cp_async16(dst[t] + l, src[t] + r * C4 + s.c4, true);
+    }
+    cp_async_commit();
+  }
 }
 
 // Forward: statistics (training, shifted sums against row 0), moving
 // averages, apply (+act) -> y (fp32, optional) and y16 (bf16, optional).
 template <int W>
 __global__ void __launch_bounds__(kThreads)
-bn_fwd_fused_kernel(const float* __restrict__ x, int64_t M, int C, int64_t rows_cta, float eps,
+bn_fwd_fused_kernel(const float* __restrict__ x, int M, int C, int rows_cta, float eps,
                     float momentum, float* __restrict__ stats, float* __restrict__ mmean,
                     float* __restrict__ mvar, const float* __restrict__ gamma,
                     const float* __restrict__ beta, float* __restrict__ y,
@@ -124,33 +215,48 @@ bn_fwd_fused_kernel(const float* __restrict__ x, int64_t M, int C, int64_t rows_
   constexpr int RP = kThreads / W;  // rows per pass
   constexpr int NC = 4 * W;
   extern __shared__ __align__(16) unsigned char smem[];
-  double* pub = reinterpret_cast<double*>(smem);          // [2][NC]
-  double* tot = pub + 2 * NC;                             // [2][NC]
-  double* scratch = tot + 2 * NC;                         // [kWarps][2][NC]
-  float4* tile = reinterpret_cast<float4*>(scratch + kWarps * 2 * NC);  // [rows_cta][W]
   cg::cluster_group cl = cg::this_cluster();
+  const unsigned rank = cl.block_rank(), ncta = cl.num_blocks();
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem);                  // [2]
+  double* recv = reinterpret_cast<double*>(smem + 16);                 // [ncta][2][NC]
+  double* tot = recv + 2 * ncta * 2 * NC;                              // [2][NC]
+  double* scratch = tot + 2 * NC;                                      // [kWarps][2][NC]
+  float4* tile = reinterpret_cast<float4*>(scratch + kWarps * 2 * NC);  // [rows_cta][W]
+  if (threadIdx.x == 0) {
+    mbar_init(smem_u32(bars));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  cluster_arrive_relaxed();
   const Slice s = slice_of<W>(cl, M, rows_cta);
   const int C4 = C >> 2;
   const float4* x4 = reinterpret_cast<const float4*>(x);
-  for (int64_t r = s.r0 + s.rin; r < s.r1; r += RP)
-    cp_async16(tile + (r - s.r0) * W + s.v, x4 + r * C4 + s.c4, true);
-  cp_async_commit();
+  {
+    const float4* src[1] = {x4};
+    float4* dst[1] = {tile};
+    stage_in<W, 1>(s, src, dst, C4);
+  }
   const float4 shv = __ldg(x4 + s.c4);  // row 0: the shift of the sums
   const float sh[4] = {shv.x, shv.y, shv.z, shv.w};
-  cp_async_wait<0>();
   float s0[4] = {0.f, 0.f, 0.f, 0.f}, s1[4] = {0.f, 0.f, 0.f, 0.f};
-  for (int64_t r = s.r0 + s.rin; r < s.r1; r += RP) {
-    const float4 v = tile[(r - s.r0) * W + s.v];
-    const float* pv = &v.x;
+  for (int st = 0; st < kStages; ++st) {
+    wait_stage(kStages - 1 - st);
+    for (int k = st * s.per; k < (st + 1) * s.per; ++k) {
+      const int lr = s.rin + k * RP;
+      if (s.r0 + lr >= s.r1) break;
+      const float4 v = tile[lr * W + s.v];
+      const float* pv = &v.x;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const float d = pv[q] - sh[q];
-      s0[q] += d;
-      s1[q] += d * d;
+      for (int q = 0; q < 4; ++q) {
+        const float d = pv[q] - sh[q];
+        s0[q] += d;
+        s1[q] += d * d;
+      }
     }
   }
-  cta_reduce<W>(s0, s1, scratch, pub);
-  cluster_sum<W>(cl, pub, tot);
+  const double part = cta_reduce<W>(s0, s1, scratch);
+  cluster_wait();  // every peer's mbarrier is initialised
+  cluster_sum<W>(part, recv, bars, 0, rank, ncta, tot);
+  cluster_arrive_relaxed();  // all my incoming partials have landed
   // per-channel statistics (same formulas as bn_stats_finalize_kernel)
   float mu[4], rs[4], gm[4], bt[4];
 #pragma unroll
@@ -164,14 +270,14 @@ bn_fwd_fused_kernel(const float* __restrict__ x, int64_t M, int C, int64_t rows_
     rs[q] = static_cast<float>(1.0 / sqrt(var + double(eps)));
     gm[q] = gamma ? __ldg(gamma + c) : 1.0f;
     bt[q] = __ldg(beta + c);
-    if (cl.block_rank() == 0 && s.rin == 0) {
+    if (rank == 0 && s.rin == 0) {
       stats[c] = mu[q];
       stats[C + c] = rs[q];
       if (mmean) mmean[c] = static_cast<float>(double(mmean[c]) * momentum + mean * (1.0 - momentum));
       if (mvar) mvar[c] = static_cast<float>(double(mvar[c]) * momentum + var * (1.0 - momentum));
     }
   }
-  for (int64_t r = s.r0 + s.rin; r < s.r1; r += RP) {
+  for (int r = s.r0 + s.rin; r < s.r1; r += RP) {
     float4 v = tile[(r - s.r0) * W + s.v];
     float* pv = &v.x;
 #pragma unroll
@@ -179,7 +285,7 @@ bn_fwd_fused_kernel(const float* __restrict__ x, int64_t M, int C, int64_t rows_
       const float t = (pv[q] - mu[q]) * rs[q] * gm[q] + bt[q];
       pv[q] = act == MGX_ACT_RELU ? relu(t) : act_forward(act, t);
     }
-    const int64_t i = r * C4 + s.c4;
+    const int i = r * C4 + s.c4;
     if (y) reinterpret_cast<float4*>(y)[i] = v;
     if (y16) {
       uint2 h;
@@ -188,7 +294,7 @@ bn_fwd_fused_kernel(const float* __restrict__ x, int64_t M, int C, int64_t rows_
       reinterpret_cast<uint2*>(y16)[i] = h;
     }
   }
-  cl.sync();  // peers may still read this CTA's pub
+  cluster_wait();  // no CTA leaves while a peer's pushes may be in flight
 }
 
 // Backward: s1 = sum dy', s2 = sum dy' * xhat (dy' = dy with the fused ReLU
@@ -198,30 +304,35 @@ bn_fwd_fused_kernel(const float* __restrict__ x, int64_t M, int C, int64_t rows_
 template <int W>
 __global__ void __launch_bounds__(kThreads)
 bn_bwd_fused_kernel(const float* __restrict__ dy, const float* __restrict__ x,
-                    const float* __restrict__ stats, const float* __restrict__ gamma, int64_t M,
-                    int C, int64_t rows_cta, const float* __restrict__ relu_gamma,
+                    const float* __restrict__ stats, const float* __restrict__ gamma, int M,
+                    int C, int rows_cta, const float* __restrict__ relu_gamma,
                     const float* __restrict__ relu_beta, float* __restrict__ dbeta,
                     float* __restrict__ dgamma, int dgamma_zero, float* __restrict__ sums,
                     float* dx, __nv_bfloat16* __restrict__ dx16, float* __restrict__ dsum) {
   constexpr int RP = kThreads / W;
   constexpr int NC = 4 * W;
   extern __shared__ __align__(16) unsigned char smem[];
-  double* pub = reinterpret_cast<double*>(smem);          // [2][NC]
-  double* tot = pub + 2 * NC;                             // [2][NC]
-  double* pub2 = tot + 2 * NC;                            // [2][NC] (dsum)
-  double* scratch = pub2 + 2 * NC;                        // [kWarps][2][NC]
+  cg::cluster_group cl = cg::this_cluster();
+  const unsigned rank = cl.block_rank(), ncta = cl.num_blocks();
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem);                  // [2]
+  double* recv = reinterpret_cast<double*>(smem + 16);                 // [2][ncta][2][NC]
+  double* tot = recv + 2 * ncta * 2 * NC;                              // [2][NC]
+  double* scratch = tot + 2 * NC;                                      // [kWarps][2][NC]
   float4* tdy = reinterpret_cast<float4*>(scratch + kWarps * 2 * NC);  // [rows_cta][W]
   float4* tx = tdy + rows_cta * W;
-  cg::cluster_group cl = cg::this_cluster();
+  if (threadIdx.x == 0) {
+    mbar_init(smem_u32(bars));
+    mbar_init(smem_u32(bars + 1));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  cluster_arrive_relaxed();
   const Slice s = slice_of<W>(cl, M, rows_cta);
   const int C4 = C >> 2;
-  const float4* dy4 = reinterpret_cast<const float4*>(dy);
-  const float4* x4 = reinterpret_cast<const float4*>(x);
-  for (int64_t r = s.r0 + s.rin; r < s.r1; r += RP) {
-    cp_async16(tdy + (r - s.r0) * W + s.v, dy4 + r * C4 + s.c4, true);
-    cp_async16(tx + (r - s.r0) * W + s.v, x4 + r * C4 + s.c4, true);
+  {
+    const float4* src[2] = {reinterpret_cast<const float4*>(dy), reinterpret_cast<const float4*>(x)};
+    float4* dst[2] = {tdy, tx};
+    stage_in<W, 2>(s, src, dst, C4);
   }
-  cp_async_commit();
   const bool relu = relu_beta != nullptr;
   float mu[4], rs[4], gm[4], bt[4], g[4];
 #pragma unroll
@@ -233,30 +344,36 @@ bn_bwd_fused_kernel(const float* __restrict__ dy, const float* __restrict__ x,
     gm[q] = relu && relu_gamma ? __ldg(relu_gamma + c) : 1.0f;
     bt[q] = relu ? __ldg(relu_beta + c) : 0.0f;
   }
-  cp_async_wait<0>();
   float a0[4] = {0.f, 0.f, 0.f, 0.f}, a1[4] = {0.f, 0.f, 0.f, 0.f};
-  for (int64_t r = s.r0 + s.rin; r < s.r1; r += RP) {
-    const int64_t l = (r - s.r0) * W + s.v;
-    const float4 d = tdy[l], xv = tx[l];
-    const float* pd = &d.x;
-    const float* px = &xv.x;
+  for (int st = 0; st < kStages; ++st) {
+    wait_stage(kStages - 1 - st);
+    for (int k = st * s.per; k < (st + 1) * s.per; ++k) {
+      const int lr = s.rin + k * RP;
+      if (s.r0 + lr >= s.r1) break;
+      const int l = lr * W + s.v;
+      const float4 d = tdy[l], xv = tx[l];
+      const float* pd = &d.x;
+      const float* px = &xv.x;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      float dq = pd[q];
-      if (relu && !((px[q] - mu[q]) * rs[q] * gm[q] + bt[q] > 0.0f)) dq = 0.0f;
-      a0[q] += dq;
-      a1[q] += dq * ((px[q] - mu[q]) * rs[q]);
+      for (int q = 0; q < 4; ++q) {
+        float dq = pd[q];
+        if (relu && !((px[q] - mu[q]) * rs[q] * gm[q] + bt[q] > 0.0f)) dq = 0.0f;
+        a0[q] += dq;
+        a1[q] += dq * ((px[q] - mu[q]) * rs[q]);
+      }
     }
   }
-  cta_reduce<W>(a0, a1, scratch, pub);
-  cluster_sum<W>(cl, pub, tot);
+  const double part = cta_reduce<W>(a0, a1, scratch);
+  cluster_wait();  // every peer's mbarrier is initialised
+  cluster_sum<W>(part, recv, bars, 0, rank, ncta, tot);
+  if (!dsum) cluster_arrive_relaxed();
   float s1[4], s2[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const int cl_ = s.v * 4 + q, c = s.c4 * 4 + q;
     s1[q] = static_cast<float>(tot[cl_]);
     s2[q] = static_cast<float>(tot[NC + cl_]);
-    if (cl.block_rank() == 0 && s.rin == 0) {
+    if (rank == 0 && s.rin == 0) {
       if (sums) {
         sums[c] = s1[q];
         sums[C + c] = s2[q];
@@ -267,8 +384,8 @@ bn_bwd_fused_kernel(const float* __restrict__ dy, const float* __restrict__ x,
   }
   const float invm = static_cast<float>(1.0 / double(M));
   float ds[4] = {0.f, 0.f, 0.f, 0.f};
-  for (int64_t r = s.r0 + s.rin; r < s.r1; r += RP) {
-    const int64_t l = (r - s.r0) * W + s.v;
+  for (int r = s.r0 + s.rin; r < s.r1; r += RP) {
+    const int l = (r - s.r0) * W + s.v;
     const float4 d = tdy[l], xv = tx[l];
     const float* pd = &d.x;
     const float* px = &xv.x;
@@ -282,7 +399,7 @@ bn_bwd_fused_kernel(const float* __restrict__ dy, const float* __restrict__ x,
       po[q] = g[q] * rs[q] * (dq - (s1[q] + xhat * s2[q]) * invm);
       ds[q] += po[q];
     }
-    const int64_t i = r * C4 + s.c4;
+    const int i = r * C4 + s.c4;
     if (dx) reinterpret_cast<float4*>(dx)[i] = o;
     if (dx16) {
       uint2 h;
@@ -293,44 +410,55 @@ bn_bwd_fused_kernel(const float* __restrict__ dy, const float* __restrict__ x,
   }
   if (dsum) {
     const float zero[4] = {0.f, 0.f, 0.f, 0.f};
-    __syncthreads();  // scratch reuse
-    cta_reduce<W>(ds, zero, scratch, pub2);
-    cluster_sum<W>(cl, pub2, tot);
-    if (cl.block_rank() == 0 && threadIdx.x < NC)
+    __syncthreads();  // scratch / tot reuse
+    const double p2 = cta_reduce<W>(ds, zero, scratch);
+    cluster_sum<W>(p2, recv + ncta * 2 * NC, bars + 1, 0, rank, ncta, tot);
+    cluster_arrive_relaxed();
+    if (rank == 0 && threadIdx.x < NC)
       dsum[blockIdx.y * NC + threadIdx.x] = static_cast<float>(tot[threadIdx.x]);
   }
-  cl.sync();  // peers may still read this CTA's pub / pub2
+  cluster_wait();  // no CTA leaves while a peer's pushes may be in flight
 }
 
 // ------------------------------------------------------------- launch shape
 
 struct Cfg {
   int W = 0, CS = 0;
-  int64_t rows_cta = 0;
+  int rows_cta = 0;
   size_t smem = 0;
 };
 
-inline size_t smem_bytes(int W, int64_t rows_cta, int tensors) {
+inline size_t smem_bytes(int W, int CS, int rows_cta, int tensors) {
   const size_t NC = 4 * size_t(W);
-  return (3 * 2 * NC + kWarps * 2 * NC) * sizeof(double) + size_t(rows_cta) * W * 16 * tensors;
+  return 16 + (2 * size_t(CS) * 2 * NC + 2 * NC + kWarps * 2 * NC) * sizeof(double) +
+         size_t(rows_cta) * W * 16 * tensors;
 }
 
 // Clusters of 8 (portable) then 16, slices of 8/4/2 vectors: the first shape
 // whose tile fits two CTAs per SM with >= one CTA per SM in total, else the
 // fitting shape with the most CTAs; none fits -> W == 0 (use the unfused
 // kernels).  A deterministic function of (M, C, tensors).
+inline int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v && *v ? atoi(v) : dflt;
+}
+
 inline Cfg pick(int64_t M, int64_t C, int tensors) {
+  // tuning knobs (read once): narrowest slice, CTA target, smem per CTA
+  static const int min_w = env_int("MGX_BNF_MINW", 2);
+  static const int min_ctas = env_int("MGX_BNF_MINCTAS", kNumSMs);
+  static const int smem_kb = env_int("MGX_BNF_SMEM_KB", 112);
   Cfg best;
-  if (C % 8 != 0 || M < 1) return best;
+  if (C % 8 != 0 || M < 1 || M * (C / 4) >= (int64_t(1) << 31)) return best;
   const int64_t C4 = C / 4;
   int64_t best_ctas = 0;
   for (int CS : {8, 16}) {
     for (int W : {8, 4, 2}) {
-      if (C4 % W) continue;
-      const int64_t rows = ceil_div(M, CS);
-      const size_t sm = smem_bytes(W, rows, tensors);
+      if (C4 % W || W < min_w) continue;
+      const int rows = static_cast<int>(ceil_div(M, CS));
+      const size_t sm = smem_bytes(W, CS, rows, tensors);
       const int64_t ctas = int64_t(CS) * (C4 / W);
-      if (sm <= size_t(112) * 1024 && ctas >= kNumSMs) return Cfg{W, CS, rows, sm};
+      if (sm <= size_t(smem_kb) * 1024 && ctas >= min_ctas) return Cfg{W, CS, rows, sm};
       if (sm <= size_t(200) * 1024 && ctas > best_ctas) {
         best = Cfg{W, CS, rows, sm};
         best_ctas = ctas;
@@ -375,14 +503,14 @@ int Launcher<Params...>::run(const Cfg& cfg, int64_t C, cudaStream_t st, Args...
 
 template <int W, typename... Args>
 int launch_fwd(const Cfg& cfg, int64_t C, cudaStream_t st, Args... args) {
-  return Launcher<const float*, int64_t, int, int64_t, float, float, float*, float*, float*,
+  return Launcher<const float*, int, int, int, float, float, float*, float*, float*,
                   const float*, const float*, float*, __nv_bfloat16*,
                   int>::template run<bn_fwd_fused_kernel<W>>(cfg, C, st, args...);
 }
 
 template <int W, typename... Args>
 int launch_bwd(const Cfg& cfg, int64_t C, cudaStream_t st, Args... args) {
-  return Launcher<const float*, const float*, const float*, const float*, int64_t, int, int64_t,
+  return Launcher<const float*, const float*, const float*, const float*, int, int, int,
                   const float*, const float*, float*, float*, int, float*, float*,
                   __nv_bfloat16*, float*>::template run<bn_bwd_fused_kernel<W>>(cfg, C, st,
                                                                                   args...);

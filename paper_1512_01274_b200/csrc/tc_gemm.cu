@@ -79,6 +79,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// the same wait with a suspend-time hint: the warp sleeps in the barrier
+// until the phase flips instead of re-polling (waiters that are not on the
+// critical issue path -- producers waiting for a free slot, the epilogue
+// waiting for an accumulator -- stop stealing issue slots from the gather)
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(1000000)
+      : "memory");
+}
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
                                             int c0, int c1) {
   asm volatile(
@@ -178,7 +191,16 @@ struct Sched {
 struct Gather {
   const __nv_bfloat16* src;
   int B, H, W, C, kh, kw, sh, sw, ph, pw, Ho, Wo;
+  // n / d as __umul64hi(n, mul) for the runtime divisors (exact for any
+  // 32-bit n; mul = 2^64 / d rounded up, 0 for d == 1)
+  uint64_t mul_hw, mul_wo, mul_c, mul_kw;
 };
+
+__host__ inline uint64_t fastdiv_mul(int d) { return d <= 1 ? 0 : ~uint64_t(0) / uint64_t(d) + 1; }
+__device__ __forceinline__ int fdiv_u(int n, uint64_t mul) {
+  return mul ? static_cast<int>(__umul64hi(static_cast<uint64_t>(static_cast<uint32_t>(n)), mul))
+             : n;
+}
 
 constexpr int kGatherThreads = 128;  // warps 6..9
 
@@ -253,7 +275,7 @@ tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
         for (int kb = 0; kb < nkb; ++kb, ++it) {
           const int s = it % G::kStages;
           const uint32_t ph = (it / G::kStages) & 1;
-          mbar_wait(&empty[s], ph ^ 1);
+          mbar_wait_sleep(&empty[s], ph ^ 1);
           uint8_t* sa = smem + s * G::kStageBytes;
           mbar_expect_tx(&full[s], GM == 1 ? G::kBBytes : GM == 2 ? G::kABytes : G::kStageBytes);
           if (GM != 1) load_operand<A_MN, BM>(sa, &map_a, &full[s], (kb0 + kb) * BK, m0);
@@ -315,39 +337,58 @@ tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
         const int q = g & 7, r0 = g >> 3;
         const int hw = ga.Ho * ga.Wo;
         int hb[8], wb[8];
-        const __nv_bfloat16* img[8];
+        const __nv_bfloat16* rowp[8];  // element (hb, wb, 0) of the row's window (may be virtual)
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           const int m = m0 + r0 + 16 * i;
-          const int b = m < M ? m / hw : -1;
+          const int b = m < M ? fdiv_u(m, ga.mul_hw) : -1;
           const int rem = m - (b < 0 ? 0 : b) * hw;
-          const int oh = rem / ga.Wo, ow = rem - (rem / ga.Wo) * ga.Wo;
+          const int oh = fdiv_u(rem, ga.mul_wo), ow = rem - oh * ga.Wo;
           hb[i] = b < 0 ? -(1 << 20) : oh * ga.sh - ga.ph;  // invalid row: always out of range
           wb[i] = ow * ga.sw - ga.pw;
-          img[i] = ga.src + int64_t(b < 0 ? 0 : b) * ga.H * ga.W * ga.C;
+          rowp[i] = ga.src + (int64_t(b < 0 ? 0 : b) * ga.H * ga.W +
+                              int64_t(hb[i] < 0 && b < 0 ? 0 : hb[i]) * ga.W + wb[i]) * ga.C;
         }
         const int K = ga.kh * ga.kw * ga.C;
+        // (tap row ti, tap column tj, channel c) of this thread's 8 K
+        // columns, advanced by BK per k-block without dividing; koff is
+        // their offset from a row's window origin in the NHWC source
+        int k = kb0 * BK + q * 8;
+        const int tap0 = fdiv_u(k, ga.mul_c);
+        int c = k - tap0 * ga.C;
+        int ti = fdiv_u(tap0, ga.mul_kw), tj = tap0 - ti * ga.kw;
+        int64_t koff = (int64_t(ti) * ga.W + tj) * ga.C + c;
+        const int64_t wskip = int64_t(ga.W - ga.kw) * ga.C;
+        const uint32_t dbase = uint32_t(r0 * 128 + ((q ^ (r0 & 7)) << 4));
         for (int kb = 0; kb < nkb; ++kb, ++it) {
           const int s = it % G::kStages;
           const uint32_t ph = (it / G::kStages) & 1;
-          mbar_wait(&empty[s], ph ^ 1);
-          const uint32_t tile = smem_u32(smem + s * G::kStageBytes);
-          const int k = (kb0 + kb) * BK + q * 8;
-          const int tap = k / ga.C, c = k - tap * ga.C;
-          const int ti = tap / ga.kw, tj = tap - ti * ga.kw;
+          mbar_wait_sleep(&empty[s], ph ^ 1);
+          const uint32_t tile = smem_u32(smem + s * G::kStageBytes) + dbase;
           const bool kv = k < K;
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            const int r = r0 + 16 * i;
             const int h = hb[i] + ti, w = wb[i] + tj;
-            const bool v = kv && h >= 0 && h < ga.H && w >= 0 && w < ga.W;
-            const void* src = v ? static_cast<const void*>(img[i] + (int64_t(h) * ga.W + w) * ga.C + c)
+            const bool v = kv && static_cast<unsigned>(h) < static_cast<unsigned>(ga.H) &&
+                           static_cast<unsigned>(w) < static_cast<unsigned>(ga.W);
+            const void* src = v ? static_cast<const void*>(rowp[i] + koff)
                                 : static_cast<const void*>(ga.src);
-            cp_async16_zfill(tile + uint32_t(r * 128 + ((q ^ (r & 7)) << 4)), src, v);
+            cp_async16_zfill(tile + uint32_t(i * 16 * 128), src, v);
           }
           asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(
                            smem_u32(&full[s]))
                        : "memory");
+          k += BK;
+          c += BK;
+          koff += BK;
+          while (c >= ga.C) {
+            c -= ga.C;
+            if (++tj == ga.kw) {
+              tj = 0;
+              ++ti;
+              koff += wskip;
+            }
+          }
         }
       } else {
         // B tile (MN-major): 64 K rows (pixels) x BN columns in 64-column
@@ -368,16 +409,16 @@ tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
         for (int kb = 0; kb < nkb; ++kb, ++it) {
           const int s = it % G::kStages;
           const uint32_t ph = (it / G::kStages) & 1;
-          mbar_wait(&empty[s], ph ^ 1);
+          mbar_wait_sleep(&empty[s], ph ^ 1);
           const uint32_t tile = smem_u32(smem + s * G::kStageBytes + G::kABytes);
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             const int kr = r0 + 16 * i;
             const int m = (kb0 + kb) * BK + kr;
             const bool mv = m < sc.kext;
-            const int b = mv ? m / hw : 0;
+            const int b = mv ? fdiv_u(m, ga.mul_hw) : 0;
             const int rem = m - b * hw;
-            const int oh = rem / ga.Wo, ow = rem - (rem / ga.Wo) * ga.Wo;
+            const int oh = fdiv_u(rem, ga.mul_wo), ow = rem - oh * ga.Wo;
             const int hb = oh * ga.sh - ga.ph, wb = ow * ga.sw - ga.pw;
             const __nv_bfloat16* img = ga.src + int64_t(b) * ga.H * ga.W * ga.C;
 #pragma unroll
@@ -411,7 +452,7 @@ tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
       const int acc = local & 1;
       const uint32_t aph = (local >> 1) & 1;
       float* Cz = C + int64_t(z) * split_stride;
-      mbar_wait(&tfull[acc], aph);
+      mbar_wait_sleep(&tfull[acc], aph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int row0 = m0 + lane_base;
       for (int c0 = 0; c0 < BN; c0 += 32) {
@@ -542,6 +583,47 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, i
     for (int z = 1; z < splits; ++z) v = fadd(v, ws[z * split_stride + o]);
     if (bias) v = fadd(v, __ldg(bias + n));
     C[m * ldc + n] = act_forward(act, v);
+  }
+}
+
+// float4 form (N % 4 == 0, ldc % 4 == 0, aligned): all split loads of a
+// vector in flight before the in-order sum
+__global__ void splitk_reduce4_kernel(const float4* __restrict__ ws, int splits,
+                                      int64_t split_stride4, const float* __restrict__ bias,
+                                      float4* __restrict__ C, int64_t ldc4, int64_t M, int64_t N4,
+                                      int act) {
+  const int64_t total = M * N4;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
+    const int64_t m = i / N4, n4 = i - m * N4;
+    float4 v = ws[i];
+    constexpr int B = 8;
+    for (int z0 = 1; z0 < splits; z0 += B) {
+      float4 p[B];
+#pragma unroll
+      for (int u = 0; u < B; ++u)
+        if (z0 + u < splits) p[u] = ws[(z0 + u) * split_stride4 + i];
+#pragma unroll
+      for (int u = 0; u < B; ++u)
+        if (z0 + u < splits) {
+          v.x = fadd(v.x, p[u].x);
+          v.y = fadd(v.y, p[u].y);
+          v.z = fadd(v.z, p[u].z);
+          v.w = fadd(v.w, p[u].w);
+        }
+    }
+    if (bias) {
+      const float4 b = __ldg(reinterpret_cast<const float4*>(bias) + n4);
+      v.x = fadd(v.x, b.x);
+      v.y = fadd(v.y, b.y);
+      v.z = fadd(v.z, b.z);
+      v.w = fadd(v.w, b.w);
+    }
+    v.x = act_forward(act, v.x);
+    v.y = act_forward(act, v.y);
+    v.z = act_forward(act, v.z);
+    v.w = act_forward(act, v.w);
+    C[m * ldc4 + n4] = v;
   }
 }
 
@@ -791,6 +873,16 @@ static int gemm_impl(const void* A, int64_t lda, int a_mn, const void* B, int64_
            : bn == 192 ? launch_bn<192>(a_mn, b_mn, gm, l, st)
                        : launch_bn<256>(a_mn, b_mn, gm, l, st);
   if (rc != MGX_OK || splits == 1) return rc;
+  if (N % 4 == 0 && ldc % 4 == 0 && l.sstride % 4 == 0 && mgx::aligned16(C) &&
+      mgx::aligned16(workspace) && (!bias || mgx::aligned16(bias))) {
+    int64_t blocks = mgx::ceil_div(M * N / 4, 256);
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    splitk_reduce4_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(
+        reinterpret_cast<const float4*>(workspace), splits, l.sstride / 4, bias,
+        reinterpret_cast<float4*>(C), ldc / 4, M, N / 4, act);
+    MGX_LAUNCHED();
+    return MGX_OK;
+  }
   int64_t blocks = mgx::ceil_div(M * N, 256);
   if (blocks > 148 * 8) blocks = 148 * 8;
   splitk_reduce_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(workspace, splits, l.sstride,
@@ -835,6 +927,10 @@ extern "C" int mgx_gemm_bf16_conv(int mode, const void* src, const int64_t* geom
   ga.Wo = (ga.W + 2 * ga.pw - ga.kw) / ga.sw + 1;
   MGX_REQUIRE(ga.C % 8 == 0 && ga.C > 0 && ga.Ho > 0 && ga.Wo > 0 && ga.B > 0,
               "mgx_gemm_bf16_conv: the gathered tensor needs C %% 8 == 0");
+  ga.mul_hw = fastdiv_mul(ga.Ho * ga.Wo);
+  ga.mul_wo = fastdiv_mul(ga.Wo);
+  ga.mul_c = fastdiv_mul(ga.C);
+  ga.mul_kw = fastdiv_mul(ga.kw);
   const int64_t pixels = int64_t(ga.B) * ga.Ho * ga.Wo;
   const int64_t kconv = int64_t(ga.kh) * ga.kw * ga.C;
   if (mode == 1) {

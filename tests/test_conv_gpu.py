@@ -442,7 +442,7 @@ def test_implicit_gemm_convolution(cuda, case):
     dyd = torch.zeros(m, ldf, dtype=torch.bfloat16, device="cuda")
     dyd[:, :f] = dy.cuda()
     dw = torch.full((f, kk), float("nan"), device="cuda")
-    ws = torch.empty(64 * f * kk + 1, device="cuda")
+    ws = torch.empty(max(64 * f * kk, 148 * m * f) + 1, device="cuda")
     L.call("mgx_gemm_bf16_conv", 2, xd.data_ptr(), _ptr(geom), dyd.data_ptr(), ldf, None,
            dw.data_ptr(), kk, f, kk, m, 0, 0, ws.data_ptr(), None, 0)
     torch.cuda.synchronize()
@@ -464,6 +464,15 @@ def test_implicit_gemm_convolution(cuda, case):
         torch.testing.assert_close(mv1, mv2, rtol=1e-5, atol=1e-6)
     ref = oc.conv2d_nhwc(x.double(), wt.double(), None, s, p).reshape(m, f)
     torch.testing.assert_close(out.double().cpu(), ref, rtol=1e-4, atol=1e-3 * max(1, kk / 64) ** 0.5)
+    # split-K forward (auto split count, in-order reduce) with a bias: the
+    # same contraction, bias added once after the split sum
+    bias = torch.randn(f, generator=g, dtype=torch.float64).float().cuda()
+    out2 = torch.full((m, f), float("nan"), device="cuda")
+    L.call("mgx_gemm_bf16_conv", 1, xd.data_ptr(), _ptr(geom), wpad.data_ptr(), ldw,
+           bias.data_ptr(), out2.data_ptr(), f, m, f, kk, 0, 0, ws.data_ptr(), None, 0)
+    torch.cuda.synchronize()
+    torch.testing.assert_close(out2.double().cpu(), ref + bias.double().cpu(), rtol=1e-4,
+                               atol=1e-3 * max(1, kk / 64) ** 0.5)
     xr = x.double().permute(0, 3, 1, 2)
     from torch.nn.grad import conv2d_weight
     dwr = conv2d_weight(xr, (f, c, k[0], k[1]), dy.double().reshape(b, ho, wo, f).permute(0, 3, 1, 2),

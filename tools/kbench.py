@@ -120,6 +120,41 @@ def bench_bn(torch, L):
             print(f"{name:14s} ({m}, {c}): {us:8.1f} us  {nb / us / 1e3:7.0f} GB/s")
 
 
+BNF = [(12544, 160), (12544, 576), (46656, 64), (46656, 256), (3136, 352), (3136, 1024)]
+
+
+def bench_bn_fused(torch, L):
+    for m, c in BNF:
+        ok = ctypes.c_int()
+        L.call("mgx_bn_fused_ok", m, c, 1, ctypes.byref(ok))
+        if not ok.value:
+            print(f"bn_fused       ({m}, {c}): no cluster shape")
+            continue
+        x = torch.randn(m, c, device="cuda")
+        dy = torch.randn(m, c, device="cuda")
+        y16 = torch.empty(m, c, device="cuda", dtype=torch.bfloat16)
+        st = torch.empty(2 * c, device="cuda")
+        gam = torch.ones(c, device="cuda")
+        bet = torch.zeros(c, device="cuda")
+        mm, mv = torch.zeros(c, device="cuda"), torch.ones(c, device="cuda")
+        db, dg, ds = (torch.empty(c, device="cuda") for _ in range(3))
+
+        def fwd():
+            L.call("mgx_bn_fwd_fused", x.data_ptr(), m, c, st.data_ptr(), mm.data_ptr(),
+                   mv.data_ptr(), 1e-3, 0.9, gam.data_ptr(), bet.data_ptr(), None,
+                   y16.data_ptr(), 1, 0)
+
+        def bwd():
+            L.call("mgx_bn_bwd_fused", dy.data_ptr(), x.data_ptr(), st.data_ptr(), gam.data_ptr(),
+                   m, c, gam.data_ptr(), bet.data_ptr(), db.data_ptr(), dg.data_ptr(), 0, None,
+                   None, y16.data_ptr(), ds.data_ptr(), 0)
+        fwd()
+        n = m * c
+        for name, fn, nb in (("bn_fwd_fused", fwd, 6 * n), ("bn_bwd_fused", bwd, 10 * n)):
+            us = _time(torch, fn)
+            print(f"{name:14s} ({m}, {c}): {us:8.1f} us  {nb / us / 1e3:7.0f} GB/s")
+
+
 def main():
     what = sys.argv[1] if len(sys.argv) > 1 else "all"
     import torch
@@ -130,6 +165,8 @@ def main():
         bench_pool(torch, L)
     if what in ("bn", "all"):
         bench_bn(torch, L)
+    if what in ("bnf", "all"):
+        bench_bn_fused(torch, L)
 
 
 if __name__ == "__main__":
