@@ -117,6 +117,56 @@ im2col_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ col, Geom
   }
 }
 
+// im2col for few input channels (the RGB stem), one block per output row
+// (b, oh): the kh input rows it touches are staged in shared memory once
+// (coalesced, zero-filled in the padding), then every 16-byte store of the
+// row's col entries reads its 8 elements from shared memory through a
+// per-column offset table -- no per-element tap decode, no redundant global
+// reads.  tile: [kh][WT][C] with WT = (Wo - 1) * sw + kw input columns
+// starting at w = -pw; lut[k] = (k / (kw C)) * WT * C + k % (kw C), -1 for
+// the K padding.
+__global__ void __launch_bounds__(256)
+im2col_rows_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ col, Geom g,
+                   int64_t ldk, int WT) {
+  extern __shared__ float tile[];
+  const int rowlen = WT * g.C;
+  int* lut = reinterpret_cast<int*>(tile + g.kh * rowlen);
+  const int b = blockIdx.x / g.Ho, oh = blockIdx.x - (blockIdx.x / g.Ho) * g.Ho;
+  const int hb = oh * g.sh - g.ph;
+  const int K = g.kh * g.kw * g.C, seg = g.kw * g.C;
+  for (int k = threadIdx.x; k < ldk; k += blockDim.x)
+    lut[k] = k < K ? (k / seg) * rowlen + (k - (k / seg) * seg) : -1;
+  const int e_lo = g.pw * g.C, e_hi = (g.W + g.pw) * g.C;  // in-image part of a staged row
+  for (int i = 0; i < g.kh; ++i) {
+    const int h = hb + i;
+    const bool hv = h >= 0 && h < g.H;
+    const float* src = x + (int64_t(b) * g.H + (hv ? h : 0)) * g.W * g.C - e_lo;
+    for (int e = threadIdx.x; e < rowlen; e += blockDim.x)
+      tile[i * rowlen + e] = (hv && e >= e_lo && e < e_hi) ? __ldg(src + e) : 0.0f;
+  }
+  __syncthreads();
+  const int nj = static_cast<int>(ldk / 8);
+  const int rpb = blockDim.x / nj;
+  const int r = threadIdx.x / nj, j = threadIdx.x - (threadIdx.x / nj) * nj;
+  if (r >= rpb) return;
+  int off[8];
+#pragma unroll
+  for (int t = 0; t < 8; ++t) off[t] = lut[j * 8 + t];
+  const int step = g.sw * g.C;
+  __nv_bfloat16* out = col + (int64_t(b) * g.Ho + oh) * g.Wo * ldk + j * 8;
+  for (int ow = r; ow < g.Wo; ow += rpb) {
+    float v8[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) v8[t] = off[t] >= 0 ? tile[off[t] + ow * step] : 0.0f;
+    uint4 o;
+    o.x = pack_bf16(v8[0], v8[1]);
+    o.y = pack_bf16(v8[2], v8[3]);
+    o.z = pack_bf16(v8[4], v8[5]);
+    o.w = pack_bf16(v8[6], v8[7]);
+    *reinterpret_cast<uint4*>(out + int64_t(ow) * ldk) = o;
+  }
+}
+
 // dx[b,h,w,c] = sum over taps (i, j) ascending of dcol[pixel(oh,ow), (i,j,c)]
 // for every output pixel whose window covers (h, w): the adjoint of im2col
 // as a gather (deterministic, no atomics).
@@ -1084,6 +1134,16 @@ extern "C" int mgx_im2col_bf16(const float* x, void* col, const int64_t* geom, i
   MGX_REQUIRE(ldk % 8 == 0 && ldk >= int64_t(g.kh) * g.kw * g.C, "mgx_im2col_bf16: bad ldk");
   MGX_REQUIRE(mgx::aligned16(x) && mgx::aligned16(col), "mgx_im2col_bf16: unaligned");
   MGX_REQUIRE(int64_t(g.B) * g.Ho * g.Wo < (1ll << 31), "mgx_im2col_bf16: too many rows");
+  const int WT = (g.Wo - 1) * g.sw + g.kw;
+  const size_t smem = size_t(g.kh) * WT * g.C * sizeof(float) + size_t(ldk) * sizeof(int);
+  if (g.C % 8 != 0 && smem <= 48 * 1024 && ldk / 8 <= 256) {
+    const int nj = static_cast<int>(ldk / 8);
+    mgx::conv::im2col_rows_kernel<<<static_cast<unsigned>(int64_t(g.B) * g.Ho), nj * (256 / nj),
+                                    smem, mgx::as_stream(stream)>>>(
+        x, static_cast<__nv_bfloat16*>(col), g, ldk, WT);
+    MGX_LAUNCHED();
+    return MGX_OK;
+  }
   mgx::conv::im2col_kernel<<<mgx::rows_grid(int64_t(g.B) * g.Ho * g.Wo, ldk / 8),
                              mgx::rows_block(ldk / 8), 0,
                              mgx::as_stream(stream)>>>(x, static_cast<__nv_bfloat16*>(col), g, ldk);
