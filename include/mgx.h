@@ -229,6 +229,23 @@ int mgx_bn_bwd_fused(const float* dy, const float* x, const float* stats, const 
                      int64_t M, int64_t C, const float* relu_gamma, const float* relu_beta,
                      float* dbeta, float* dgamma, int dgamma_zero, float* sums, float* dx,
                      void* dx16, float* dsum, uintptr_t stream);
+/* Stem fusion, BatchNorm (+act) feeding a max pooling (argmax recorded):
+ * forward: y = maxpool(act(bn(x))) with the argmax, the normalised tensor
+ * never written; backward: the BatchNorm gradient passes with their output
+ * gradient gathered through the pooling (dy_pool + argmax, the sum
+ * mgx_pool_backward computes) instead of read from a materialised tensor.
+ * geom/full describe the pooling (its input is the BatchNorm's [M, C]). */
+int mgx_bn_act_pool_fwd(const float* x, const float* stats, const float* gamma, const float* beta,
+                        int act, const int64_t* geom, int full, float* y, void* y16, void* argmax,
+                        uintptr_t stream);
+int mgx_bn_bwd_reduce_pooled(const float* dy_pool, const void* argmax, const int64_t* geom,
+                             int full, const float* x, const float* stats, int64_t M, int64_t C,
+                             void* ws, float* sums, float* dbeta, float* dgamma, int dgamma_zero,
+                             const float* relu_gamma, const float* relu_beta, uintptr_t stream);
+int mgx_bn_bwd_dx_pooled(const float* dy_pool, const void* argmax, const int64_t* geom, int full,
+                         const float* x, const float* stats, const float* sums,
+                         const float* gamma, int64_t M, int64_t C, const float* relu_beta,
+                         float* dsum, void* ws, float* dx, void* dx16, uintptr_t stream);
 /* out[c] = sum over rows of x[r, c] (conv bias gradient). */
 int mgx_colsum(const float* x, int64_t M, int64_t C, void* ws, float* out, uintptr_t stream);
 /* Pooling, NHWC.  type 0 max (padding ignored), 1 avg (count_include_pad);
@@ -341,6 +358,16 @@ typedef struct mgx_instr {
 #define MGX_OP_BN_BWD_FUSED 31 /* ptr0=dy ptr1=x ptr2=stats ptr3=gamma ptr4=dx     */
                               /* ptr5=dx16 dims=M,C,relu_gamma*,relu_beta*,dbeta*, */
                               /* dgamma*,dgamma_zero,dsum*                          */
+#define MGX_OP_BN_ACT_POOL 32 /* ptr0=x ptr1=stats ptr2=gamma ptr3=beta ptr4=y     */
+                              /* ptr5=y16 act dims=pool geom (7; full at bit 40 of */
+                              /* dims6),argmax*                                    */
+#define MGX_OP_BN_BWD_REDUCE_POOL 33 /* ptr0=dy_pool ptr1=x ptr2=stats ptr3=ws     */
+                              /* ptr4=sums ptr5=argmax act=dgamma_zero dims=M,C,    */
+                              /* dbeta*,dgamma*,relu_gamma*,relu_beta*,geom packed  */
+                              /* as MGX_OP_GEMM_CONV's (full at bit 48 of dims7)   */
+#define MGX_OP_BN_BWD_DX_POOL 34 /* ptr0=dy_pool ptr1=x ptr2=stats ptr3=sums        */
+                              /* ptr4=gamma ptr5=argmax dims=M,C,relu_beta*,dsum*, */
+                              /* ws*,dx16*,geom packed (bf16 dx only)              */
 #define MGX_OP_GEMM_CONV 27   /* ptr0=src(bf16 NHWC) ptr1=op ptr2=bias ptr3=C      */
                               /* ptr4=workspace ptr5=colstats dims=M,N,K,ldop,ldc, */
                               /* mode|splits<<8, B<<48|H<<32|W<<16|C,              */

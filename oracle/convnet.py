@@ -107,14 +107,41 @@ def pool_nhwc(x, attrs):
     return y.permute(0, 2, 3, 1)
 
 
-def run_graph(g, values: Dict[str, np.ndarray], wrt=(), bf16_operands: bool = False
+class _Bf16FC:
+    """FullyConnected whose three contractions see bf16-rounded operands like
+    the device's bf16 dense mode (executor dense="bf16"): y = bf16(x)
+    bf16(W)^T + b; dX = bf16(dY) bf16(W); dW = bf16(dY)^T bf16(x)."""
+
+    @staticmethod
+    def apply(x2, w, b):
+        torch = _torch()
+
+        class F(torch.autograd.Function):
+            @staticmethod
+            def forward(ctx, x2, w):
+                xr, wr = bf16(x2), bf16(w)
+                ctx.save_for_backward(xr, wr)
+                return xr @ wr.T
+
+            @staticmethod
+            def backward(ctx, dy):
+                xr, wr = ctx.saved_tensors
+                dyr = bf16(dy)
+                return dyr @ wr, dyr.T @ xr
+
+        return F.apply(x2, w) + b
+
+
+def run_graph(g, values: Dict[str, np.ndarray], wrt=(), bf16_operands: bool = False,
+              bf16_fc: bool = False
               ) -> Tuple[Dict[str, np.ndarray], Dict[str, np.ndarray], Dict[str, np.ndarray]]:
     """Forward (and, for a SoftmaxOutput head, backward) of ``g`` in float64.
 
     Returns (node outputs by name, gradients of ``wrt`` by name, updated
     BatchNorm moving statistics by name).  ``bf16_operands`` rounds every
     operand of the Convolution contractions (forward, data and weight
-    gradients) to bf16 like the device does."""
+    gradients) to bf16 like the device does; ``bf16_fc`` does the same for
+    FullyConnected (the device's dense="bf16" mode)."""
     torch = _torch()
     env = {}
     leaves = {}
@@ -137,6 +164,8 @@ def run_graph(g, values: Dict[str, np.ndarray], wrt=(), bf16_operands: bool = Fa
         elif n.op == "Convolution":
             y = conv2d_nhwc(ins[0], ins[1], ins[2] if len(ins) > 2 else None,
                             _pair(a.get("stride", 1)), _pair(a.get("pad", 0)))
+        elif n.op == "FullyConnected" and bf16_fc:
+            y = _Bf16FC.apply(ins[0].reshape(ins[0].shape[0], -1), ins[1], ins[2])
         elif n.op == "FullyConnected":
             x2 = ins[0].reshape(ins[0].shape[0], -1)
             y = x2 @ ins[1].T + ins[2]

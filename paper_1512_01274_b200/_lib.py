@@ -32,6 +32,7 @@ OP_IM2COL, OP_COL2IM, OP_BN_STATS, OP_BN_APPLY, OP_BN_BWD_REDUCE, OP_BN_BWD_DX =
 OP_POOL_FWD, OP_POOL_BWD, OP_CHAN_COPY, OP_COLSUM, OP_GEMM_TC_EX = 21, 22, 23, 24, 25
 OP_WFLIP, OP_GEMM_CONV, OP_SUM_N, OP_CONCAT = 26, 27, 28, 29
 OP_BN_FWD_FUSED, OP_BN_BWD_FUSED = 30, 31
+OP_BN_ACT_POOL, OP_BN_BWD_REDUCE_POOL, OP_BN_BWD_DX_POOL = 32, 33, 34
 
 KV_ADD, KV_SGD, KV_AGG = 0, 1, 2
 KV_MAX_SEGS = 256
@@ -161,6 +162,13 @@ _SIGNATURES = {
                           c_vp, ctypes.c_int, c_uptr], ctypes.c_int),
     "mgx_bn_bwd_fused": ([c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp,
                           ctypes.c_int, c_vp, c_vp, c_vp, c_vp, c_uptr], ctypes.c_int),
+    "mgx_bn_act_pool_fwd": ([c_vp, c_vp, c_vp, c_vp, ctypes.c_int, c_vp, ctypes.c_int, c_vp, c_vp,
+                             c_vp, c_uptr], ctypes.c_int),
+    "mgx_bn_bwd_reduce_pooled": ([c_vp, c_vp, c_vp, ctypes.c_int, c_vp, c_vp, c_i64, c_i64, c_vp,
+                                  c_vp, c_vp, c_vp, ctypes.c_int, c_vp, c_vp, c_uptr],
+                                 ctypes.c_int),
+    "mgx_bn_bwd_dx_pooled": ([c_vp, c_vp, c_vp, ctypes.c_int, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64,
+                              c_vp, c_vp, c_vp, c_vp, c_vp, c_uptr], ctypes.c_int),
     "mgx_colsum": ([c_vp, c_i64, c_i64, c_vp, c_vp, c_uptr], ctypes.c_int),
     "mgx_pool_forward": ([c_vp, c_vp, c_vp, ctypes.c_int, ctypes.c_int, c_vp, c_vp, c_uptr],
                          ctypes.c_int),

@@ -455,7 +455,7 @@ def _bn_lower_bwd(slot, env, out, attrs):
 def bn_backward_group(og: View, relu: bool, x: View, gamma: View, beta: View, attrs,
                       xnode, dx: Optional[View], dgamma: Optional[View],
                       dbeta: Optional[View], dbias_conv: Optional[View] = None,
-                      dx_node=None, dx_fp32: bool = True) -> list:
+                      dx_node=None, dx_fp32: bool = True, pool=None) -> list:
     """All requested BatchNorm gradients of one node in one pass pair (the
     executor's fusion of the sibling Backward nodes, optionally with the
     ReLU backward in front of them): one reduction that also writes dbeta /
@@ -466,6 +466,28 @@ def bn_backward_group(og: View, relu: bool, x: View, gamma: View, beta: View, at
     code = []
     st = _bn_stats(x, attrs, ctx, code, update=False, xnode=xnode)
     fix = attrs.get("fix_gamma", True)
+    if pool is not None:
+        # og = the max pooling's input gradient, gathered from its output
+        # gradient and argmax inside both passes (stem fusion; executor)
+        dyp, pnode, pattrs, pshape = pool
+        k, s, p, full = _pool_params(pattrs, pshape)
+        arg = _pool_argmax(pnode, pshape, dyp.size, k, 0, ctx)
+        g1, g2 = _pack_geom(pshape, k, s, p)
+        g2 |= int(full) << 48
+        g = None if fix else gamma.ptr
+        sums = ctx.persistent(8 * c)
+        ws = ctx.scratch(_reduce_ws(m, c))
+        code.append(instr(L.OP_BN_BWD_REDUCE_POOL, [dyp.ptr, x.ptr, st, ws, sums, arg],
+                          [m, c, dbeta.ptr if dbeta else 0, dgamma.ptr if dgamma else 0,
+                           (g or 0) if relu else 0, beta.ptr if relu else 0, g1, g2],
+                          act=1 if fix else 0))
+        dx16 = ctx.shadow_out(dx.size, dx_node)
+        assert dx16 is not None and not dx_fp32, "pooled BatchNorm dx writes the bf16 copy only"
+        dws = ctx.scratch(_reduce_ws(m, c))
+        code.append(instr(L.OP_BN_BWD_DX_POOL, [dyp.ptr, x.ptr, st, sums, g, arg],
+                          [m, c, beta.ptr if relu else 0,
+                           dbias_conv.ptr if dbias_conv is not None else 0, dws, dx16, g1, g2]))
+        return code
     if dx is not None and bn_fused_ok(m, c, True):
         # reductions + dx (+ conv bias gradient) in one cluster kernel
         g = None if fix else gamma.ptr
@@ -534,6 +556,33 @@ def conv_bn_instrs(cins, cout: View, cattrs, bins, bout: View, battrs, act: int,
     code = conv_forward_instrs(cins, cout, cattrs, colstats=tiles)
     code += bn_forward_instrs(bins, bout, battrs, act=act, tiles=tiles, xnode=conv_node,
                               y_fp32=y_fp32)
+    return code
+
+
+def conv_bn_pool_instrs(cins, cout: View, cattrs, bins, battrs, act: int, conv_node,
+                        pool_node, pattrs, pout: View, y_fp32: bool = True):
+    """Convolution -> BatchNorm -> activation -> max pooling (the stem):
+    statistics from the GEMM epilogue, then ONE pass normalising, activating
+    and pooling with the argmax -- the activation tensor is never written
+    (its backward recomputes the mask from x; the pooling backward reads the
+    argmax).  Executor fusion."""
+    ctx = current_ctx()
+    m, f = prod(cout.shape[:-1]), cout.shape[-1]
+    tiles = ctx.scratch(8 * (-(-m // 32)) * f)
+    code = conv_forward_instrs(cins, cout, cattrs, colstats=tiles)
+    x = bins[0]
+    st = _bn_stats(x, battrs, ctx, code, update=True, mm=bins[3], mv=bins[4], xnode=conv_node,
+                   tiles=tiles)
+    gamma = None if battrs.get("fix_gamma", True) else bins[1].ptr
+    k, s, p, full = _pool_params(pattrs, x.shape)
+    arg = _pool_argmax(pool_node, x.shape, pout.size, k, 0, ctx)
+    ctx.memo[("argmax_fwd", id(pool_node))] = True
+    y16 = ctx.shadow_out(pout.size, pool_node) if f % 8 == 0 else None
+    yp = None if (not y_fp32 and y16 is not None) else pout.ptr
+    geom = _geom(x.shape, k, s, p)
+    geom[6] |= int(full) << 40
+    code.append(instr(L.OP_BN_ACT_POOL, [x.ptr, st, gamma, bins[2].ptr, yp, y16], geom + [arg],
+                      act=act))
     return code
 
 

@@ -57,6 +57,79 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
+// ---- max-pooling gradient gathered on the fly (stem fusion): the input
+// gradient of a max pooling at pixel r = sum of the pooled output gradient
+// over the covering windows whose recorded argmax is r, windows in ascending
+// (oh, ow) order -- exactly pool_bwd_vec_kernel's sum, so a BatchNorm
+// backward can read its output gradient through the pooling without that
+// gradient ever being written (the BatchNorm input is the pooling input).
+struct PoolGrad {
+  const float4* dy;        // pooled output gradient [B, Ho, Wo, C] as channel vectors
+  const uchar4* arg;       // window-local argmax, same shape
+  Geom g;                  // pooling geometry (H, W input; Ho, Wo output)
+  uint64_t mul_hw, mul_w;  // n / (H W), n / W as __umul64hi(n, mul); 0: divisor 1
+};
+
+__host__ inline uint64_t pg_mul(int d) { return d <= 1 ? 0 : ~uint64_t(0) / uint64_t(d) + 1; }
+__device__ __forceinline__ int pg_div(int n, uint64_t mul) {
+  return mul ? static_cast<int>(__umul64hi(static_cast<uint64_t>(static_cast<uint32_t>(n)), mul))
+             : n;
+}
+
+// PK: 32 = a 3x3 / stride 2 window (unrolled), 1 = runtime geometry
+template <int PK>
+__device__ __forceinline__ float4 pool_grad4(const PoolGrad& pg, int r, int c4, int C4) {
+  const Geom& g = pg.g;
+  const int b = pg_div(r, pg.mul_hw);
+  const int rem = r - b * g.H * g.W;
+  const int h = pg_div(rem, pg.mul_w), w = rem - h * g.W;
+  constexpr int K = PK == 32 ? 3 : 0, S = PK == 32 ? 2 : 0;
+  const int kh = K ? K : g.kh, kw = K ? K : g.kw;
+  const int sh = K ? S : g.sh, sw = K ? S : g.sw;
+  const int nh = h + g.ph - kh + 1, nw = w + g.pw - kw + 1;
+  const int oh_lo = nh <= 0 ? 0 : (nh + sh - 1) / sh;
+  const int oh_hi = min(g.Ho - 1, (h + g.ph) / sh);
+  const int ow_lo = nw <= 0 ? 0 : (nw + sw - 1) / sw;
+  const int ow_hi = min(g.Wo - 1, (w + g.pw) / sw);
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  const int64_t ob = int64_t(b) * g.Ho * g.Wo * C4 + c4;
+  auto win = [&](int oh, int ow, const float4 d, const uchar4 am) {
+    const int li = (h - (oh * sh - g.ph)) * kw + (w - (ow * sw - g.pw));
+    const float* pd = &d.x;
+    const unsigned char* pa = &am.x;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (pa[q] == li) acc[q] = fadd(acc[q], pd[q]);
+  };
+  if constexpr (K > 0) {
+    constexpr int NW = (K + S - 1) / S;
+    float4 d[NW * NW];
+    uchar4 am[NW * NW];
+#pragma unroll
+    for (int i = 0; i < NW; ++i)
+#pragma unroll
+      for (int j = 0; j < NW; ++j) {
+        const bool ok = oh_lo + i <= oh_hi && ow_lo + j <= ow_hi;
+        const int64_t o = ob + (int64_t(oh_lo + i) * g.Wo + ow_lo + j) * C4;
+        d[i * NW + j] = ok ? __ldg(pg.dy + o) : make_float4(0.f, 0.f, 0.f, 0.f);
+        am[i * NW + j] = ok ? __ldg(pg.arg + o) : make_uchar4(255, 255, 255, 255);
+      }
+#pragma unroll
+    for (int i = 0; i < NW; ++i)
+#pragma unroll
+      for (int j = 0; j < NW; ++j)
+        if (oh_lo + i <= oh_hi && ow_lo + j <= ow_hi)
+          win(oh_lo + i, ow_lo + j, d[i * NW + j], am[i * NW + j]);
+  } else {
+    for (int oh = oh_lo; oh <= oh_hi; ++oh)
+      for (int ow = ow_lo; ow <= ow_hi; ++ow) {
+        const int64_t o = ob + (int64_t(oh) * g.Wo + ow) * C4;
+        win(oh, ow, __ldg(pg.dy + o), __ldg(pg.arg + o));
+      }
+  }
+  return make_float4(acc[0], acc[1], acc[2], acc[3]);
+}
+
 // col[m, k] (bf16, row stride ldk >= K, zero beyond K) = x at tap k of output
 // pixel m (zero in the padding).  A thread owns the 8 consecutive k of one
 // 16-byte store; when C % 8 == 0 they are 8 channels of one tap (two float4
@@ -469,11 +542,12 @@ __device__ __forceinline__ float4 bn_dx4(const float4& d, const float4& xv, cons
   return o;
 }
 
+template <int PK = 0>
 __global__ void __launch_bounds__(kRedThreads)
 bn_dx_colsum_kernel(const float* dy, const float* __restrict__ x, const float* __restrict__ stats,
                     const float* __restrict__ sums, const float* __restrict__ gamma, float* dx,
                     ReluMask rm, int64_t M, int C, int64_t rpc, double* __restrict__ ws,
-                    __nv_bfloat16* __restrict__ dx16) {
+                    __nv_bfloat16* __restrict__ dx16, PoolGrad pg) {
   extern __shared__ double red[];  // [rpp][ct]
   const int C4 = C >> 2;
   const int ct4 = C4 < kRedThreads ? C4 : kRedThreads;
@@ -508,7 +582,11 @@ bn_dx_colsum_kernel(const float* dy, const float* __restrict__ x, const float* _
       for (int u = 0; u < U; ++u) {
         const int64_t rr = r + u * rpp;
         const int64_t i = rr * C4 + c4;
-        d[u] = rr < r1 ? reinterpret_cast<const float4*>(dy)[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+        if constexpr (PK != 0)
+          d[u] = rr < r1 ? pool_grad4<PK>(pg, static_cast<int>(rr), c4, C4)
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+        else
+          d[u] = rr < r1 ? reinterpret_cast<const float4*>(dy)[i] : make_float4(0.f, 0.f, 0.f, 0.f);
         xv[u] = rr < r1 ? __ldg(reinterpret_cast<const float4*>(x) + i)
                         : make_float4(0.f, 0.f, 0.f, 0.f);
       }
@@ -622,6 +700,215 @@ __global__ void bn_stats_from_tiles_kernel(const float2* __restrict__ part, int6
     stats[C + c] = static_cast<float>(1.0 / sqrt(var + double(eps)));
     if (mmean) mmean[c] = static_cast<float>(double(mmean[c]) * momentum + mean * (1.0 - momentum));
     if (mvar) mvar[c] = static_cast<float>(double(mvar[c]) * momentum + var * (1.0 - momentum));
+  }
+}
+
+// ---- stem fusion, backward reductions over the pooling WINDOWS: only the
+// argmax position of each window receives gradient, so
+//   s1 = sum_p mask(p) og(p)        = sum_windows mask(p*) dy(w)
+//   s2 = sum_p mask(p) og(p) xhat(p) = sum_windows mask(p*) dy(w) xhat(p*)
+// with p* the window's argmax: the pooled gradient, the argmax and one x
+// element per window and channel are read -- the full-resolution gradient
+// is never formed.  Rows = windows (B Ho Wo), tiled like
+// colreduce_partial_vec_kernel; partials per chunk into ws (same layout, so
+// colsum_finalize_kernel merges them).
+__global__ void __launch_bounds__(kRedThreads)
+bn_pool_reduce_kernel(PoolGrad pg, const float* __restrict__ x, const float* __restrict__ stats,
+                      ReluMask rm, int64_t Mp, int C, int64_t rpc, double* __restrict__ ws,
+                      uint32_t mkw, uint64_t mul_howo, uint64_t mul_wo) {
+  extern __shared__ double red[];  // [rpp][2][ct]
+  const Geom& g = pg.g;
+  const int C4 = C >> 2;
+  const int ct4 = C4 < kRedThreads ? C4 : kRedThreads;
+  const int rpp = kRedThreads / ct4;
+  const int ct = ct4 * 4;
+  const int t = threadIdx.x;
+  const int r_in = t / ct4, c_in = t - (t / ct4) * ct4;
+  const int c4 = blockIdx.y * ct4 + c_in;
+  const bool active = r_in < rpp && c4 < C4;
+  const int64_t r0 = int64_t(blockIdx.x) * rpc;
+  const int64_t r1 = min(Mp, r0 + rpc);
+  const bool relu = rm.beta != nullptr;
+  float s0[4] = {0.f, 0.f, 0.f, 0.f}, s1[4] = {0.f, 0.f, 0.f, 0.f};
+  if (active) {
+    float mu[4], rs[4], gm[4], bt[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int c = c4 * 4 + q;
+      mu[q] = __ldg(stats + c);
+      rs[q] = __ldg(stats + C + c);
+      gm[q] = relu && rm.gamma ? __ldg(rm.gamma + c) : 1.0f;
+      bt[q] = relu ? __ldg(rm.beta + c) : 0.0f;
+    }
+    const int howo = g.Ho * g.Wo;
+    constexpr int U = 4;
+    for (int64_t r = r0 + r_in; r < r1; r += U * rpp) {
+      float4 d[U];
+      uchar4 am[U];
+      float xv[U][4];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t rr = r + u * rpp;
+        const bool ok = rr < r1;
+        d[u] = ok ? __ldg(pg.dy + rr * C4 + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
+        am[u] = ok ? __ldg(pg.arg + rr * C4 + c4) : make_uchar4(0, 0, 0, 0);
+        const int ri = static_cast<int>(ok ? rr : r0);
+        const int b = pg_div(ri, mul_howo);
+        const int rem = ri - b * howo;
+        const int oh = pg_div(rem, mul_wo), ow = rem - oh * g.Wo;
+        const float* xb = x + (int64_t(b) * g.H * g.W) * C + c4 * 4;
+        const unsigned char* pa = &am[u].x;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int li = pa[q];
+          const int ti = static_cast<int>((uint32_t(li) * mkw) >> 16), tj = li - ti * g.kw;
+          const int h = oh * g.sh - g.ph + ti, w = ow * g.sw - g.pw + tj;
+          xv[u][q] = ok ? __ldg(xb + (int64_t(h) * g.W + w) * C + q) : 0.0f;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (r + u * rpp >= r1) continue;
+        const float* pd = &d[u].x;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          float dq = pd[q];
+          if (relu && !((xv[u][q] - mu[q]) * rs[q] * gm[q] + bt[q] > 0.0f)) dq = 0.0f;
+          s0[q] += dq;
+          s1[q] += dq * ((xv[u][q] - mu[q]) * rs[q]);
+        }
+      }
+    }
+  }
+  if (r_in < rpp) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      red[(r_in * 2) * ct + c_in * 4 + q] = s0[q];
+      red[(r_in * 2 + 1) * ct + c_in * 4 + q] = s1[q];
+    }
+  }
+  __syncthreads();
+  const int nchunk = gridDim.x;
+  for (int c = t; c < ct; c += blockDim.x) {
+    const int cg = blockIdx.y * ct + c;
+    if (cg >= C) continue;
+    double u0 = 0.0, u1 = 0.0;
+    for (int rr = 0; rr < rpp; ++rr) {
+      u0 += red[(rr * 2) * ct + c];
+      u1 += red[(rr * 2 + 1) * ct + c];
+    }
+    ws[int64_t(blockIdx.x) * C + cg] = u0;
+    ws[int64_t(nchunk + blockIdx.x) * C + cg] = u1;
+  }
+}
+
+// ---- stem fusion, BatchNorm dx through a 3x3 / stride 2 / pad 0 max
+// pooling: a thread owns a 2x2 pixel block (rows = blocks) and 4 channels;
+// exactly 4 windows cover such a block ((a-1 | a) x (b-1 | b) for block
+// (a, b)), so 4 pooled-gradient and argmax loads give the output gradient of
+// all 4 pixels (summed in ascending (oh, ow) order like pool_bwd_vec_kernel);
+// then dx = gamma rstd (mask og - (s1 + xhat s2) / M) -> dx16, and the
+// per-chunk partial sums of dx (conv bias gradient) into ws.
+__global__ void __launch_bounds__(kRedThreads)
+bn_pool_dx_k3s2_kernel(PoolGrad pg, const float* __restrict__ x, const float* __restrict__ stats,
+                       const float* __restrict__ sums, const float* __restrict__ gamma,
+                       ReluMask rm, int64_t M, int64_t Mb, int C, int64_t rpc,
+                       double* __restrict__ ws, __nv_bfloat16* __restrict__ dx16,
+                       uint64_t mul_blk, uint64_t mul_wb) {
+  extern __shared__ double red[];  // [rpp][ct]
+  const Geom& g = pg.g;
+  const int C4 = C >> 2;
+  const int ct4 = C4 < kRedThreads ? C4 : kRedThreads;
+  const int rpp = kRedThreads / ct4;
+  const int ct = ct4 * 4;
+  const int t = threadIdx.x;
+  const int r_in = t / ct4, c_in = t - (t / ct4) * ct4;
+  const int c4 = blockIdx.y * ct4 + c_in;
+  const bool active = r_in < rpp && c4 < C4;
+  const int64_t r0 = int64_t(blockIdx.x) * rpc;
+  const int64_t r1 = min(Mb, r0 + rpc);
+  const float invm = static_cast<float>(1.0 / double(M));
+  const bool relu = rm.beta != nullptr;
+  const int Hb = (g.H + 1) >> 1, Wb = (g.W + 1) >> 1;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  if (active) {
+    float mu[4], rs[4], gg[4], s1[4], s2[4], gm[4], bt[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int c = c4 * 4 + q;
+      mu[q] = __ldg(stats + c);
+      rs[q] = __ldg(stats + C + c);
+      gg[q] = gamma ? __ldg(gamma + c) : 1.0f;
+      s1[q] = __ldg(sums + c);
+      s2[q] = __ldg(sums + C + c);
+      gm[q] = relu && rm.gamma ? __ldg(rm.gamma + c) : 1.0f;
+      bt[q] = relu ? __ldg(rm.beta + c) : 0.0f;
+    }
+    for (int64_t r = r0 + r_in; r < r1; r += rpp) {
+      const int ri = static_cast<int>(r);
+      const int b = pg_div(ri, mul_blk);
+      const int rem = ri - b * Hb * Wb;
+      const int ba = pg_div(rem, mul_wb), bb = rem - ba * Wb;
+      // the 4 covering windows (a-1, b-1), (a-1, b), (a, b-1), (a, b)
+      float4 d[4];
+      uchar4 am[4];
+#pragma unroll
+      for (int wi = 0; wi < 4; ++wi) {
+        const int oh = ba - 1 + (wi >> 1), ow = bb - 1 + (wi & 1);
+        const bool ok = oh >= 0 && oh < g.Ho && ow >= 0 && ow < g.Wo;
+        const int64_t o = ((int64_t(b) * g.Ho + oh) * g.Wo + ow) * C4 + c4;
+        d[wi] = ok ? __ldg(pg.dy + o) : make_float4(0.f, 0.f, 0.f, 0.f);
+        am[wi] = ok ? __ldg(pg.arg + o) : make_uchar4(255, 255, 255, 255);
+      }
+#pragma unroll
+      for (int pi = 0; pi < 4; ++pi) {
+        const int dh = pi >> 1, dw = pi & 1;
+        const int h = 2 * ba + dh, w = 2 * bb + dw;
+        if (h >= g.H || w >= g.W) continue;
+        const int64_t i = ((int64_t(b) * g.H + h) * g.W + w) * C4 + c4;
+        const float4 xv = __ldg(reinterpret_cast<const float4*>(x) + i);
+        const float* px = &xv.x;
+        float og[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int wi = 0; wi < 4; ++wi) {
+          const int wh = wi >> 1, ww = wi & 1;
+          // window (a-1+wh, b-1+ww) covers this pixel at local (h - 2oh, w - 2ow)
+          const int lh = 2 - 2 * wh + dh, lw = 2 - 2 * ww + dw;  // 2*(a - oh) + dh
+          if (lh > 2 || lw > 2) continue;
+          const int li = lh * 3 + lw;
+          const float* pd = &d[wi].x;
+          const unsigned char* pa = &am[wi].x;
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (pa[q] == li) og[q] = fadd(og[q], pd[q]);
+        }
+        float o[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          float dq = og[q];
+          if (relu && !((px[q] - mu[q]) * rs[q] * gm[q] + bt[q] > 0.0f)) dq = 0.0f;
+          const float xhat = (px[q] - mu[q]) * rs[q];
+          o[q] = gg[q] * rs[q] * (dq - (s1[q] + xhat * s2[q]) * invm);
+          acc[q] += o[q];
+        }
+        uint2 hv;
+        hv.x = pack_bf16(o[0], o[1]);
+        hv.y = pack_bf16(o[2], o[3]);
+        reinterpret_cast<uint2*>(dx16)[i] = hv;
+      }
+    }
+  }
+  if (r_in < rpp) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) red[r_in * ct + c_in * 4 + q] = acc[q];
+  }
+  __syncthreads();
+  for (int c = t; c < ct; c += blockDim.x) {
+    const int cg = blockIdx.y * ct + c;
+    if (cg >= C) continue;
+    double u = 0.0;
+    for (int rr = 0; rr < rpp; ++rr) u += red[rr * ct + c];
+    ws[int64_t(blockIdx.x) * C + cg] = u;
   }
 }
 
@@ -823,10 +1110,21 @@ __global__ void pool_bwd_kernel(const float* __restrict__ x, const float* __rest
 // time (the 3x3 / stride 1-2 poolings of the nets): every tap / covering
 // window is unrolled with bounds predicates so all loads of a pixel are in
 // flight at once; K == 0: runtime geometry.  TYPE 0 max, 1 avg.
-template <int K, int S, int TYPE>
+// BN: the pooled values are act(BatchNorm(x)) computed on the fly from the
+// BatchNorm input x (stem fusion: BatchNorm + ReLU + pooling in one pass;
+// the normalised tensor is never written)
+struct BnAct {
+  const float* stats;  // [mean C | rstd C]
+  const float* gamma;  // NULL: 1
+  const float* beta;
+  int act;
+};
+
+template <int K, int S, int TYPE, bool BN = false>
 __global__ void __launch_bounds__(256)
 pool_fwd_vec_kernel(const float* __restrict__ x, float* __restrict__ y,
-                    uint8_t* __restrict__ arg, Geom g, __nv_bfloat16* __restrict__ y16) {
+                    uint8_t* __restrict__ arg, Geom g, __nv_bfloat16* __restrict__ y16,
+                    BnAct bn = BnAct{}) {
   const int C4 = g.C >> 2;
   const int kh = K ? K : g.kh, kw = K ? K : g.kw;
   const int sh = K ? S : g.sh, sw = K ? S : g.sw;
@@ -845,7 +1143,27 @@ pool_fwd_vec_kernel(const float* __restrict__ x, float* __restrict__ y,
     int ai[4] = {0, 0, 0, 0};
 #pragma unroll
     for (int q = 0; q < 4; ++q) acc[q] = TYPE == 0 ? -INFINITY : 0.0f;
-    auto tap = [&](const float4 v, int li) {
+    float4 mu4, rs4, gm4, bt4;
+    if constexpr (BN) {
+      mu4 = __ldg(reinterpret_cast<const float4*>(bn.stats) + c4);
+      rs4 = __ldg(reinterpret_cast<const float4*>(bn.stats + g.C) + c4);
+      gm4 = bn.gamma ? __ldg(reinterpret_cast<const float4*>(bn.gamma) + c4)
+                     : make_float4(1.f, 1.f, 1.f, 1.f);
+      bt4 = __ldg(reinterpret_cast<const float4*>(bn.beta) + c4);
+    }
+    auto tap = [&](float4 v, int li) {
+      if constexpr (BN) {  // the same arithmetic as bn_apply_kernel
+        const float* pm = &mu4.x;
+        const float* pr = &rs4.x;
+        const float* pgm = &gm4.x;
+        const float* pb = &bt4.x;
+        float* pw_ = &v.x;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float t = (pw_[q] - pm[q]) * pr[q] * pgm[q] + pb[q];
+          pw_[q] = bn.act == MGX_ACT_RELU ? relu(t) : act_forward(bn.act, t);
+        }
+      }
       const float* pv = &v.x;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -1249,7 +1567,7 @@ extern "C" int mgx_bn_bwd_dx(const float* dy, const float* x, const float* stats
     }
     mgx::conv::bn_dx_colsum_kernel<<<grid, ct4 * rpp, smem, st>>>(
         dy, x, stats, sums, gamma, dx, rm, M, static_cast<int>(C), rpc, wsd,
-        static_cast<__nv_bfloat16*>(dx16));
+        static_cast<__nv_bfloat16*>(dx16), mgx::conv::PoolGrad{});
     if (dsum)
       mgx::conv::colsum_finalize_kernel<<<static_cast<unsigned>(mgx::ceil_div(C, mgx::conv::kFinChannels)), 32 * mgx::conv::kFinChannels, 0, st>>>(
           static_cast<const double*>(ws), nchunk, static_cast<int>(C), 0, dsum, nullptr, nullptr, 0);
@@ -1347,6 +1665,134 @@ extern "C" int mgx_pool_backward(const float* x, const float* y, const float* dy
     const int64_t n = int64_t(g.B) * g.H * g.W * g.C;
     mgx::conv::pool_bwd_kernel<<<grid_for(n), 256, 0, st>>>(x, y, dy, dx, g, type);
   }
+  MGX_LAUNCHED();
+  return MGX_OK;
+}
+
+// ---- stem fusion: BatchNorm (+act) -> max pooling, forward and backward
+extern "C" int mgx_bn_act_pool_fwd(const float* x, const float* stats, const float* gamma,
+                                   const float* beta, int act, const int64_t* geom, int full,
+                                   float* y, void* y16, void* argmax, uintptr_t stream) {
+  MGX_REQUIRE(x && stats && beta && (y || y16) && argmax && geom,
+              "mgx_bn_act_pool_fwd: bad arguments");
+  Geom g = mgx::conv::decode(geom, full != 0);
+  MGX_REQUIRE(g.Ho > 0 && g.Wo > 0 && g.kh * g.kw <= 255, "mgx_bn_act_pool_fwd: bad geometry");
+  MGX_REQUIRE(g.C % 4 == 0 && mgx::aligned16(x) && mgx::aligned16(stats) && mgx::aligned16(beta) &&
+                  (!gamma || mgx::aligned16(gamma)) && (!y || mgx::aligned16(y)) &&
+                  (!y16 || mgx::aligned16(y16)),
+              "mgx_bn_act_pool_fwd: needs C %% 4 == 0 and 16-byte aligned tensors");
+  cudaStream_t st = mgx::as_stream(stream);
+  const unsigned grid = grid_for(int64_t(g.B) * g.Ho * g.Wo * (g.C / 4));
+  const mgx::conv::BnAct bn{stats, gamma, beta, act};
+  uint8_t* arg = static_cast<uint8_t*>(argmax);
+  __nv_bfloat16* h16 = static_cast<__nv_bfloat16*>(y16);
+  if (pool_square(g) == 32)
+    mgx::conv::pool_fwd_vec_kernel<3, 2, 0, true><<<grid, 256, 0, st>>>(x, y, arg, g, h16, bn);
+  else
+    mgx::conv::pool_fwd_vec_kernel<0, 0, 0, true><<<grid, 256, 0, st>>>(x, y, arg, g, h16, bn);
+  MGX_LAUNCHED();
+  return MGX_OK;
+}
+
+static int pool_grad_of(const float* dy_pool, const void* argmax, const int64_t* geom, int full,
+                        int64_t M, int64_t C, mgx::conv::PoolGrad* pg, int* pk) {
+  MGX_REQUIRE(dy_pool && argmax && geom, "pooled BatchNorm backward: bad arguments");
+  Geom g = mgx::conv::decode(geom, full != 0);
+  MGX_REQUIRE(int64_t(g.B) * g.H * g.W == M && g.C == C && C % 4 == 0 && g.Ho > 0 && g.Wo > 0 &&
+                  M < (int64_t(1) << 31) && mgx::aligned16(dy_pool) && mgx::aligned16(argmax),
+              "pooled BatchNorm backward: geometry does not match the rows");
+  pg->dy = static_cast<const float4*>(static_cast<const void*>(dy_pool));
+  pg->arg = static_cast<const uchar4*>(argmax);
+  pg->g = g;
+  pg->mul_hw = mgx::conv::pg_mul(g.H * g.W);
+  pg->mul_w = mgx::conv::pg_mul(g.W);
+  *pk = pool_square(g) == 32 ? 32 : 1;
+  return MGX_OK;
+}
+
+extern "C" int mgx_bn_bwd_reduce_pooled(const float* dy_pool, const void* argmax,
+                                        const int64_t* geom, int full, const float* x,
+                                        const float* stats, int64_t M, int64_t C, void* ws,
+                                        float* sums, float* dbeta, float* dgamma, int dgamma_zero,
+                                        const float* relu_gamma, const float* relu_beta,
+                                        uintptr_t stream) {
+  MGX_REQUIRE(x && stats && ws && sums && M > 0 && C > 0 && mgx::aligned16(x),
+              "mgx_bn_bwd_reduce_pooled: bad arguments");
+  mgx::conv::PoolGrad pg;
+  int pk = 0;
+  MGX_TRY(pool_grad_of(dy_pool, argmax, geom, full, M, C, &pg, &pk));
+  cudaStream_t st = mgx::as_stream(stream);
+  const int64_t Mp = int64_t(pg.g.B) * pg.g.Ho * pg.g.Wo;
+  int64_t rpc;
+  int nchunk;
+  mgx::conv::chunks_for(Mp, C, &rpc, &nchunk);
+  const int C4 = static_cast<int>(C / 4);
+  const int ct4 = C4 < mgx::conv::kRedThreads ? C4 : mgx::conv::kRedThreads;
+  const int rpp = mgx::conv::kRedThreads / ct4;
+  const size_t smem = size_t(rpp) * 2 * ct4 * 4 * sizeof(double);
+  dim3 grid(nchunk, static_cast<unsigned>(mgx::ceil_div(C4, ct4)));
+  double* wsd = static_cast<double*>(ws);
+  const uint32_t mkw = static_cast<uint32_t>((65536 + pg.g.kw - 1) / pg.g.kw);
+  mgx::conv::bn_pool_reduce_kernel<<<grid, ct4 * rpp, smem, st>>>(
+      pg, x, stats, mgx::conv::ReluMask{relu_gamma, relu_beta}, Mp, static_cast<int>(C), rpc, wsd,
+      mkw, mgx::conv::pg_mul(pg.g.Ho * pg.g.Wo), mgx::conv::pg_mul(pg.g.Wo));
+  mgx::conv::colsum_finalize_kernel<<<static_cast<unsigned>(mgx::ceil_div(C, mgx::conv::kFinChannels)), 32 * mgx::conv::kFinChannels, 0, st>>>(
+      wsd, nchunk, static_cast<int>(C), 1, sums, dbeta, dgamma, dgamma_zero);
+  MGX_LAUNCHED();
+  return MGX_OK;
+}
+
+extern "C" int mgx_bn_bwd_dx_pooled(const float* dy_pool, const void* argmax, const int64_t* geom,
+                                    int full, const float* x, const float* stats,
+                                    const float* sums, const float* gamma, int64_t M, int64_t C,
+                                    const float* relu_beta, float* dsum, void* ws, float* dx,
+                                    void* dx16, uintptr_t stream) {
+  MGX_REQUIRE(x && stats && sums && ws && (dx || dx16) && M > 0 && C > 0 &&
+                  mgx::aligned16(x) && (!dx || mgx::aligned16(dx)) &&
+                  (!dx16 || mgx::aligned16(dx16)),
+              "mgx_bn_bwd_dx_pooled: bad arguments");
+  mgx::conv::PoolGrad pg;
+  int pk = 0;
+  MGX_TRY(pool_grad_of(dy_pool, argmax, geom, full, M, C, &pg, &pk));
+  cudaStream_t st = mgx::as_stream(stream);
+  int64_t rpc;
+  int nchunk;
+  mgx::conv::chunks_for(M, C, &rpc, &nchunk);
+  const int C4 = static_cast<int>(C / 4);
+  const int ct4 = C4 < mgx::conv::kRedThreads ? C4 : mgx::conv::kRedThreads;
+  const int rpp = mgx::conv::kRedThreads / ct4;
+  const size_t smem = size_t(rpp) * ct4 * 4 * sizeof(double);
+  dim3 grid(nchunk, static_cast<unsigned>(mgx::ceil_div(C4, ct4)));
+  // the ReLU mask uses the BatchNorm gamma (relu_beta non-NULL: fused ReLU)
+  const mgx::conv::ReluMask rm{relu_beta ? gamma : nullptr, relu_beta};
+  __nv_bfloat16* h16 = static_cast<__nv_bfloat16*>(dx16);
+  double* wsd = static_cast<double*>(ws);
+  if (pk == 32 && pg.g.ph == 0 && pg.g.pw == 0 && dx == nullptr && dx16 != nullptr) {
+    // 2x2 pixel blocks: 4 windows cover a block
+    const int Hb = (pg.g.H + 1) / 2, Wb = (pg.g.W + 1) / 2;
+    const int64_t Mb = int64_t(pg.g.B) * Hb * Wb;
+    int64_t rpcb;
+    int nchunkb;
+    mgx::conv::chunks_for(Mb, C, &rpcb, &nchunkb);
+    dim3 gridb(nchunkb, static_cast<unsigned>(mgx::ceil_div(C4, ct4)));
+    mgx::conv::bn_pool_dx_k3s2_kernel<<<gridb, ct4 * rpp, smem, st>>>(
+        pg, x, stats, sums, gamma, rm, M, Mb, static_cast<int>(C), rpcb, wsd, h16,
+        mgx::conv::pg_mul(Hb * Wb), mgx::conv::pg_mul(Wb));
+    if (dsum)
+      mgx::conv::colsum_finalize_kernel<<<static_cast<unsigned>(mgx::ceil_div(C, mgx::conv::kFinChannels)), 32 * mgx::conv::kFinChannels, 0, st>>>(
+          wsd, nchunkb, static_cast<int>(C), 0, dsum, nullptr, nullptr, 0);
+    MGX_LAUNCHED();
+    return MGX_OK;
+  }
+  if (pk == 32)
+    mgx::conv::bn_dx_colsum_kernel<32><<<grid, ct4 * rpp, smem, st>>>(
+        nullptr, x, stats, sums, gamma, dx, rm, M, static_cast<int>(C), rpc, wsd, h16, pg);
+  else
+    mgx::conv::bn_dx_colsum_kernel<1><<<grid, ct4 * rpp, smem, st>>>(
+        nullptr, x, stats, sums, gamma, dx, rm, M, static_cast<int>(C), rpc, wsd, h16, pg);
+  if (dsum)
+    mgx::conv::colsum_finalize_kernel<<<static_cast<unsigned>(mgx::ceil_div(C, mgx::conv::kFinChannels)), 32 * mgx::conv::kFinChannels, 0, st>>>(
+        wsd, nchunk, static_cast<int>(C), 0, dsum, nullptr, nullptr, 0);
   MGX_LAUNCHED();
   return MGX_OK;
 }

@@ -300,6 +300,37 @@ static int run_instr(const mgx_instr& in, cudaStream_t st) {
                                 p2, p3, d[4], d[0], d[1], d[2], in.act, static_cast<int>(d[5] >> 8),
                                 static_cast<float*>(in.ptr[4]), static_cast<float*>(in.ptr[5]), s);
     }
+    case MGX_OP_BN_ACT_POOL: {
+      // dims 0..6: pool geometry (input B, H, W, C; k, s, p), bit 40 of
+      // dims[6]: full convention; dims[7]: argmax*
+      const int64_t geom[7] = {d[0], d[1], d[2], d[3], d[4], d[5], d[6] & 0xFFFFFFFFll};
+      return mgx_bn_act_pool_fwd(p0, p1, p2, p3, in.act, geom, static_cast<int>((d[6] >> 40) & 1),
+                                 static_cast<float*>(in.ptr[4]), in.ptr[5],
+                                 reinterpret_cast<void*>(d[7]), s);
+    }
+    case MGX_OP_BN_BWD_REDUCE_POOL:
+    case MGX_OP_BN_BWD_DX_POOL: {
+      // dims 6, 7: the pooling geometry packed like MGX_OP_GEMM_CONV's, bit
+      // 48 of dims[7]: full convention
+      const int64_t a = d[6], w = d[7];
+      const int64_t geom[7] = {(a >> 48) & 0xFFFF, (a >> 32) & 0xFFFF, (a >> 16) & 0xFFFF,
+                               a & 0xFFFF, (((w >> 40) & 0xFF) << 16) | ((w >> 32) & 0xFF),
+                               (((w >> 24) & 0xFF) << 16) | ((w >> 16) & 0xFF),
+                               (((w >> 8) & 0xFF) << 16) | (w & 0xFF)};
+      const int full = static_cast<int>((w >> 48) & 1);
+      if (in.op == MGX_OP_BN_BWD_REDUCE_POOL)
+        return mgx_bn_bwd_reduce_pooled(p0, in.ptr[5], geom, full, p1, p2, d[0], d[1], in.ptr[3],
+                                        static_cast<float*>(in.ptr[4]),
+                                        reinterpret_cast<float*>(d[2]),
+                                        reinterpret_cast<float*>(d[3]), in.act,
+                                        reinterpret_cast<const float*>(d[4]),
+                                        reinterpret_cast<const float*>(d[5]), s);
+      return mgx_bn_bwd_dx_pooled(p0, in.ptr[5], geom, full, p1, p2, p3,
+                                  static_cast<const float*>(in.ptr[4]), d[0], d[1],
+                                  reinterpret_cast<const float*>(d[2]),
+                                  reinterpret_cast<float*>(d[3]), reinterpret_cast<void*>(d[4]),
+                                  nullptr, reinterpret_cast<void*>(d[5]), s);
+    }
     case MGX_OP_SUM_N: {
       const float* srcs[5];
       const int cnt = static_cast<int>(d[1]);

@@ -402,6 +402,83 @@ def test_batchnorm_cluster_fused(cuda, m, c, fix_gamma, relu):
     assert torch.equal(dx_b, dx)
 
 
+@pytest.mark.parametrize("shape,k,s,p", [((2, 18, 18, 16), 3, 2, 0), ((2, 13, 11, 8), 3, 2, 1),
+                                         ((3, 10, 10, 24), 2, 2, 0)])
+@pytest.mark.parametrize("fix_gamma", [True, False])
+def test_bn_act_pool_stem_fusion(cuda, shape, k, s, p, fix_gamma):
+    """BatchNorm + ReLU + max pooling in one pass (bitwise equal to apply ->
+    pool), and the BatchNorm backward reading its gradient through the
+    pooling (reductions over the windows' argmax pixels, dx from the
+    covering windows) against the unfused chain (pool backward -> reduce ->
+    dx): the sums differ only in summation order."""
+    torch = cuda
+    from paper_1512_01274_b200 import _lib as L
+    import ctypes
+    b, h, w, c = shape
+    m = b * h * w
+    g = torch.Generator().manual_seed(m + c + k)
+    x = (torch.randn(m, c, generator=g, dtype=torch.float64) * 2 + 0.3).float().cuda()
+    gamma = (torch.rand(c, generator=g, dtype=torch.float64) + 0.5).float().cuda()
+    beta = torch.randn(c, generator=g, dtype=torch.float64).float().cuda()
+    gp = None if fix_gamma else gamma.data_ptr()
+    geom = _geom(shape, (k, k), (s, s), (p, p))
+    ho, wo = (h + 2 * p - k) // s + 1, (w + 2 * p - k) // s + 1
+    n_out = b * ho * wo * c
+    wsb = ctypes.c_int64()
+    L.call("mgx_reduce_workspace_bytes", m, c, ctypes.byref(wsb))
+    ws = torch.empty(wsb.value // 4 + 1, device="cuda")
+    st = torch.empty(2 * c, device="cuda")
+    L.call("mgx_bn_stats", x.data_ptr(), m, c, ws.data_ptr(), st.data_ptr(), None, None, 1e-3,
+           0.9, 0, 0)
+    # unfused chain
+    z = torch.empty(m, c, device="cuda")
+    L.call("mgx_bn_apply", x.data_ptr(), st.data_ptr(), gp, beta.data_ptr(), z.data_ptr(), m, c, 1,
+           None, 0)
+    y1 = torch.empty(n_out, device="cuda")
+    a1 = torch.empty(n_out, dtype=torch.uint8, device="cuda")
+    L.call("mgx_pool_forward", z.data_ptr(), y1.data_ptr(), _ptr(geom), 0, 0, a1.data_ptr(), None, 0)
+    dyp = torch.randn(n_out, generator=g, dtype=torch.float64).float().cuda()
+    og = torch.empty(m, c, device="cuda")
+    L.call("mgx_pool_backward", None, None, dyp.data_ptr(), og.data_ptr(), _ptr(geom), 0, 0,
+           a1.data_ptr(), 0)
+    sums1 = torch.empty(2 * c, device="cuda")
+    L.call("mgx_bn_bwd_reduce", og.data_ptr(), x.data_ptr(), st.data_ptr(), m, c, ws.data_ptr(),
+           sums1.data_ptr(), None, None, 1 if fix_gamma else 0, gp, beta.data_ptr(), 0)
+    dx1 = torch.empty(m, c, dtype=torch.bfloat16, device="cuda")
+    ds1 = torch.empty(c, device="cuda")
+    L.call("mgx_bn_bwd_dx", og.data_ptr(), x.data_ptr(), st.data_ptr(), sums1.data_ptr(), gp, None,
+           m, c, gp, beta.data_ptr(), ds1.data_ptr(), ws.data_ptr(), dx1.data_ptr(), 0)
+    # fused
+    y2 = torch.empty(n_out, device="cuda")
+    y16 = torch.empty(n_out, dtype=torch.bfloat16, device="cuda")
+    a2 = torch.empty(n_out, dtype=torch.uint8, device="cuda")
+    L.call("mgx_bn_act_pool_fwd", x.data_ptr(), st.data_ptr(), gp, beta.data_ptr(), 1, _ptr(geom),
+           0, y2.data_ptr(), y16.data_ptr(), a2.data_ptr(), 0)
+    sums2 = torch.empty(2 * c, device="cuda")
+    db2, dg2 = torch.empty(c, device="cuda"), torch.empty(c, device="cuda")
+    L.call("mgx_bn_bwd_reduce_pooled", dyp.data_ptr(), a2.data_ptr(), _ptr(geom), 0, x.data_ptr(),
+           st.data_ptr(), m, c, ws.data_ptr(), sums2.data_ptr(), db2.data_ptr(), dg2.data_ptr(),
+           1 if fix_gamma else 0, gp, beta.data_ptr(), 0)
+    dx2 = torch.empty(m, c, dtype=torch.bfloat16, device="cuda")
+    ds2 = torch.empty(c, device="cuda")
+    L.call("mgx_bn_bwd_dx_pooled", dyp.data_ptr(), a2.data_ptr(), _ptr(geom), 0, x.data_ptr(),
+           st.data_ptr(), sums2.data_ptr(), gp, m, c, beta.data_ptr(), ds2.data_ptr(),
+           ws.data_ptr(), None, dx2.data_ptr(), 0)
+    torch.cuda.synchronize()
+    assert torch.equal(y1, y2)
+    assert torch.equal(y16, y2.to(torch.bfloat16))
+    assert torch.equal(a1, a2)
+    mag = float(og.abs().sum()) / c
+    np.testing.assert_allclose(sums2.cpu().numpy(), sums1.cpu().numpy(), rtol=1e-5,
+                               atol=1e-6 * mag)
+    assert torch.equal(db2, sums2[:c])
+    # dx: 1-ulp bf16 flips where the sums' last bits differ
+    np.testing.assert_allclose(dx2.float().cpu().numpy(), dx1.float().cpu().numpy(), rtol=8e-3,
+                               atol=1e-6 * mag)
+    dmag = float(dx1.float().abs().sum(0).max())
+    np.testing.assert_allclose(ds2.cpu().numpy(), ds1.cpu().numpy(), rtol=1e-3, atol=1e-5 * dmag)
+
+
 IMPLICIT_CASES = [
     # (B, H, W, C, F, k, s, p)
     (2, 9, 7, 16, 24, (3, 3), (1, 1), (1, 1)),
