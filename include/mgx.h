@@ -246,6 +246,20 @@ int mgx_bn_bwd_dx_pooled(const float* dy_pool, const void* argmax, const int64_t
                          const float* x, const float* stats, const float* sums,
                          const float* gamma, int64_t M, int64_t C, const float* relu_beta,
                          float* dsum, void* ws, float* dx, void* dx16, uintptr_t stream);
+/* One launch for all per-step weight preparations of a program: jobs is a
+ * DEVICE array of njobs (<= 1024) descriptors (kind 0: bf16 row cast, a..e =
+ * R, C, ldi, rows, ldo -- as mgx_cast_bf16_2d; kind 1: flipped bf16 weight,
+ * a..e = F, kh, kw, C, ld -- as mgx_weight_flip_bf16).  Each job's output
+ * (rows * ldo or C * ld bf16, a multiple of 8, 16-byte aligned) is a run of
+ * 8-element units starting at unit `start`; units = the total. */
+typedef struct mgx_prep_job {
+  const float* src;
+  void* dst;
+  int64_t a, b, c, d, e;
+  int64_t kind;
+  int64_t start;
+} mgx_prep_job;
+int mgx_prep_batch(const void* jobs, int64_t njobs, int64_t units, uintptr_t stream);
 /* out[c] = sum over rows of x[r, c] (conv bias gradient). */
 int mgx_colsum(const float* x, int64_t M, int64_t C, void* ws, float* out, uintptr_t stream);
 /* Pooling, NHWC.  type 0 max (padding ignored), 1 avg (count_include_pad);
@@ -365,6 +379,7 @@ typedef struct mgx_instr {
                               /* ptr4=sums ptr5=argmax act=dgamma_zero dims=M,C,    */
                               /* dbeta*,dgamma*,relu_gamma*,relu_beta*,geom packed  */
                               /* as MGX_OP_GEMM_CONV's (full at bit 48 of dims7)   */
+#define MGX_OP_PREP_BATCH 35  /* ptr0=jobs (device mgx_prep_job[]) dims=njobs,units  */
 #define MGX_OP_BN_BWD_DX_POOL 34 /* ptr0=dy_pool ptr1=x ptr2=stats ptr3=sums        */
                               /* ptr4=gamma ptr5=argmax dims=M,C,relu_beta*,dsum*, */
                               /* ws*,dx16*,geom packed (bf16 dx only)              */

@@ -33,6 +33,7 @@ OP_POOL_FWD, OP_POOL_BWD, OP_CHAN_COPY, OP_COLSUM, OP_GEMM_TC_EX = 21, 22, 23, 2
 OP_WFLIP, OP_GEMM_CONV, OP_SUM_N, OP_CONCAT = 26, 27, 28, 29
 OP_BN_FWD_FUSED, OP_BN_BWD_FUSED = 30, 31
 OP_BN_ACT_POOL, OP_BN_BWD_REDUCE_POOL, OP_BN_BWD_DX_POOL = 32, 33, 34
+OP_PREP_BATCH = 35
 
 KV_ADD, KV_SGD, KV_AGG = 0, 1, 2
 KV_MAX_SEGS = 256
@@ -169,6 +170,7 @@ _SIGNATURES = {
                                  ctypes.c_int),
     "mgx_bn_bwd_dx_pooled": ([c_vp, c_vp, c_vp, ctypes.c_int, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64,
                               c_vp, c_vp, c_vp, c_vp, c_vp, c_uptr], ctypes.c_int),
+    "mgx_prep_batch": ([c_vp, c_i64, c_i64, c_uptr], ctypes.c_int),
     "mgx_colsum": ([c_vp, c_i64, c_i64, c_vp, c_vp, c_uptr], ctypes.c_int),
     "mgx_pool_forward": ([c_vp, c_vp, c_vp, ctypes.c_int, ctypes.c_int, c_vp, c_vp, c_uptr],
                          ctypes.c_int),

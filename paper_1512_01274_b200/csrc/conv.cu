@@ -294,6 +294,66 @@ __global__ void weight_flip_kernel(const float* __restrict__ w, int F, int kh, i
   }
 }
 
+// Every per-step weight preparation of a program in ONE launch (the bf16
+// copies of the convolution weights, row-padded, and the flipped weights of
+// the stride-1 data gradients).  The jobs' outputs form one flat space of
+// 8-element units (every output row length is a multiple of 8); a thread
+// finds its job by binary search over the jobs' first units and writes one
+// 16-byte vector.  Same arithmetic as cast_rows_kernel / weight_flip_kernel
+// (one rounding to bf16 per element).
+constexpr int kPrepMaxJobs = 1024;
+
+__global__ void __launch_bounds__(256)
+prep_batch_kernel(const mgx_prep_job* __restrict__ jobs, int njobs, int64_t units) {
+  __shared__ int64_t start[kPrepMaxJobs];
+  for (int j = threadIdx.x; j < njobs; j += blockDim.x) start[j] = jobs[j].start;
+  __syncthreads();
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t u = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; u < units; u += stride) {
+    int lo = 0, hi = njobs - 1;  // last job with start <= u
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (start[mid] <= u) lo = mid;
+      else hi = mid - 1;
+    }
+    const mgx_prep_job& jb = jobs[lo];
+    const int64_t e0 = (u - start[lo]) * 8;  // first output element of the unit
+    float v[8];
+    if (jb.kind == 0) {
+      // cast rows: dst[r, k] (rows x ldo) = src[r * ldi + k] for r < R, k < C, else 0
+      const int64_t R = jb.a, C = jb.b, ldi = jb.c, ldo = jb.e;
+      const int64_t r = e0 / ldo, k0 = e0 - r * ldo;
+#pragma unroll
+      for (int t = 0; t < 8; ++t)
+        v[t] = r < R && k0 + t < C ? __ldg(jb.src + r * ldi + k0 + t) : 0.0f;
+    } else {
+      // weight flip: dst[c, (i*kw + j)*F + f] (row stride ld) = w[f, kh-1-i, kw-1-j, c]
+      const int F = static_cast<int>(jb.a), kh = static_cast<int>(jb.b);
+      const int kw = static_cast<int>(jb.c), C = static_cast<int>(jb.d);
+      const int64_t ld = jb.e;
+      const int K = kh * kw * F;
+      const int c = static_cast<int>(e0 / ld);
+      const int kb = static_cast<int>(e0 - int64_t(c) * ld);
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        const int k = kb + t;
+        v[t] = 0.0f;
+        if (k < K) {
+          const int tap = k / F, f = k - tap * F;
+          const int i = tap / kw, j = tap - (tap / kw) * kw;
+          v[t] = __ldg(jb.src + ((int64_t(f) * kh + (kh - 1 - i)) * kw + (kw - 1 - j)) * C + c);
+        }
+      }
+    }
+    uint4 o;
+    o.x = pack_bf16(v[0], v[1]);
+    o.y = pack_bf16(v[2], v[3]);
+    o.z = pack_bf16(v[4], v[5]);
+    o.w = pack_bf16(v[6], v[7]);
+    *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(jb.dst) + e0) = o;
+  }
+}
+
 // ------------------------------------------------------- column reductions
 // Per-channel sums over the M rows of an [M, C] matrix, in two fixed-order
 // stages: block z reduces rows [z*rpc, (z+1)*rpc) into ws[z][*] (fp64), then
@@ -1823,6 +1883,15 @@ extern "C" int mgx_weight_flip_bf16(const float* w, int64_t F, int64_t kh, int64
   mgx::conv::weight_flip_kernel<<<grid_for(C * ld), 256, 0, mgx::as_stream(stream)>>>(
       w, static_cast<int>(F), static_cast<int>(kh), static_cast<int>(kw), static_cast<int>(C),
       static_cast<__nv_bfloat16*>(wf), ld);
+  MGX_LAUNCHED();
+  return MGX_OK;
+}
+
+extern "C" int mgx_prep_batch(const void* jobs, int64_t njobs, int64_t units, uintptr_t stream) {
+  MGX_REQUIRE(jobs && njobs > 0 && njobs <= mgx::conv::kPrepMaxJobs && units > 0,
+              "mgx_prep_batch: bad arguments");
+  mgx::conv::prep_batch_kernel<<<grid_for(units), 256, 0, mgx::as_stream(stream)>>>(
+      static_cast<const mgx_prep_job*>(jobs), static_cast<int>(njobs), units);
   MGX_LAUNCHED();
   return MGX_OK;
 }

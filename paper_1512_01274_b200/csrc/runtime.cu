@@ -331,6 +331,8 @@ static int run_instr(const mgx_instr& in, cudaStream_t st) {
                                   reinterpret_cast<float*>(d[3]), reinterpret_cast<void*>(d[4]),
                                   nullptr, reinterpret_cast<void*>(d[5]), s);
     }
+    case MGX_OP_PREP_BATCH:
+      return mgx_prep_batch(in.ptr[0], d[0], d[1], s);
     case MGX_OP_SUM_N: {
       const float* srcs[5];
       const int cnt = static_cast<int>(d[1]);

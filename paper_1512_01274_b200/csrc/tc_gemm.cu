@@ -34,6 +34,8 @@
 #include <cstring>
 #include <mutex>
 
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace mgx {
@@ -586,44 +588,72 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, i
   }
 }
 
-// float4 form (N % 4 == 0, ldc % 4 == 0, aligned): all split loads of a
-// vector in flight before the in-order sum
-__global__ void splitk_reduce4_kernel(const float4* __restrict__ ws, int splits,
-                                      int64_t split_stride4, const float* __restrict__ bias,
-                                      float4* __restrict__ C, int64_t ldc4, int64_t M, int64_t N4,
-                                      int act) {
+// float4 form (N % 4 == 0, ldc % 4 == 0, aligned), parallel over the
+// splits too: a block owns VB output vectors x SL split lanes (SL * VB =
+// 256); lane l sums splits l, l + SL, ... in ascending order, then the SL
+// lane sums meet in ascending lane order through shared memory -- a fixed
+// association (deterministic) with every split load in flight across the
+// block, so a tall split count over a small output is not a serial chain.
+__global__ void __launch_bounds__(256)
+splitk_reduce4_kernel(const float4* __restrict__ ws, int splits, int64_t split_stride4,
+                      const float* __restrict__ bias, float4* __restrict__ C, int64_t ldc4,
+                      int64_t M, int64_t N4, int act, int SL) {
+  __shared__ float4 part[256];
+  const int VB = blockDim.x / SL;
+  const int lane = threadIdx.x / VB, v = threadIdx.x - (threadIdx.x / VB) * VB;
   const int64_t total = M * N4;
-  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
-    const int64_t m = i / N4, n4 = i - m * N4;
-    float4 v = ws[i];
-    constexpr int B = 8;
-    for (int z0 = 1; z0 < splits; z0 += B) {
-      float4 p[B];
+  for (int64_t base = int64_t(blockIdx.x) * VB; base < total; base += int64_t(gridDim.x) * VB) {
+    const int64_t i = base + v;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    bool first = true;
+    if (i < total) {
+      constexpr int B = 4;
+      for (int z0 = lane; z0 < splits; z0 += B * SL) {
+        float4 p[B];
 #pragma unroll
-      for (int u = 0; u < B; ++u)
-        if (z0 + u < splits) p[u] = ws[(z0 + u) * split_stride4 + i];
+        for (int u = 0; u < B; ++u)
+          if (z0 + u * SL < splits) p[u] = ws[(z0 + u * SL) * split_stride4 + i];
 #pragma unroll
-      for (int u = 0; u < B; ++u)
-        if (z0 + u < splits) {
-          v.x = fadd(v.x, p[u].x);
-          v.y = fadd(v.y, p[u].y);
-          v.z = fadd(v.z, p[u].z);
-          v.w = fadd(v.w, p[u].w);
-        }
+        for (int u = 0; u < B; ++u)
+          if (z0 + u * SL < splits) {
+            if (first) {
+              acc = p[u];
+              first = false;
+            } else {
+              acc.x = fadd(acc.x, p[u].x);
+              acc.y = fadd(acc.y, p[u].y);
+              acc.z = fadd(acc.z, p[u].z);
+              acc.w = fadd(acc.w, p[u].w);
+            }
+          }
+      }
     }
-    if (bias) {
-      const float4 b = __ldg(reinterpret_cast<const float4*>(bias) + n4);
-      v.x = fadd(v.x, b.x);
-      v.y = fadd(v.y, b.y);
-      v.z = fadd(v.z, b.z);
-      v.w = fadd(v.w, b.w);
+    part[threadIdx.x] = acc;
+    __syncthreads();
+    if (lane == 0 && i < total) {
+      float4 t = part[v];
+      for (int l = 1; l < SL && l < splits; ++l) {
+        const float4 q = part[l * VB + v];
+        t.x = fadd(t.x, q.x);
+        t.y = fadd(t.y, q.y);
+        t.z = fadd(t.z, q.z);
+        t.w = fadd(t.w, q.w);
+      }
+      const int64_t m = i / N4, n4 = i - m * N4;
+      if (bias) {
+        const float4 b = __ldg(reinterpret_cast<const float4*>(bias) + n4);
+        t.x = fadd(t.x, b.x);
+        t.y = fadd(t.y, b.y);
+        t.z = fadd(t.z, b.z);
+        t.w = fadd(t.w, b.w);
+      }
+      t.x = act_forward(act, t.x);
+      t.y = act_forward(act, t.y);
+      t.z = act_forward(act, t.z);
+      t.w = act_forward(act, t.w);
+      C[m * ldc4 + n4] = t;
     }
-    v.x = act_forward(act, v.x);
-    v.y = act_forward(act, v.y);
-    v.z = act_forward(act, v.z);
-    v.w = act_forward(act, v.w);
-    C[m * ldc4 + n4] = v;
+    __syncthreads();
   }
 }
 
@@ -786,9 +816,17 @@ static int launch_bn(int a_mn, int b_mn, int gm, const Launch& l, cudaStream_t s
   return launch_acts<true, true, BN, 0>(l, st);
 }
 
+// split-K count: fill about `target` CTAs (env MGX_SPLIT_TARGET; default 96
+// of the 148 SMs, measured best on Inception-BN: the graph runs independent
+// branches concurrently, so a GEMM need not own the whole GPU, and fewer
+// splits mean less workspace traffic), at least 4 k-blocks per split
 static int auto_splits(int64_t tiles, int64_t nk) {
-  if (tiles >= kNumSMs) return 1;
-  int64_t want = kNumSMs / tiles, most = nk / 4;
+  static const int64_t target = [] {
+    const char* v = getenv("MGX_SPLIT_TARGET");
+    return int64_t(v && *v ? atoi(v) : 96);
+  }();
+  if (tiles >= target) return 1;
+  int64_t want = target / tiles, most = nk / 4;
   int64_t s = want < most ? want : most;
   return static_cast<int>(s < 1 ? 1 : s);
 }
@@ -875,11 +913,15 @@ static int gemm_impl(const void* A, int64_t lda, int a_mn, const void* B, int64_
   if (rc != MGX_OK || splits == 1) return rc;
   if (N % 4 == 0 && ldc % 4 == 0 && l.sstride % 4 == 0 && mgx::aligned16(C) &&
       mgx::aligned16(workspace) && (!bias || mgx::aligned16(bias))) {
-    int64_t blocks = mgx::ceil_div(M * N / 4, 256);
+    // split lanes: enough to put ~4 split loads per thread in flight
+    int SL = 1;
+    while (SL < 32 && SL * 4 < splits) SL *= 2;
+    const int VB = 256 / SL;
+    int64_t blocks = mgx::ceil_div(M * N / 4, VB);
     if (blocks > 148 * 8) blocks = 148 * 8;
     splitk_reduce4_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(
         reinterpret_cast<const float4*>(workspace), splits, l.sstride / 4, bias,
-        reinterpret_cast<float4*>(C), ldc / 4, M, N / 4, act);
+        reinterpret_cast<float4*>(C), ldc / 4, M, N / 4, act, SL);
     MGX_LAUNCHED();
     return MGX_OK;
   }

@@ -162,6 +162,13 @@ def instr_cost(ins: L.Instr) -> tuple:
         return 8 * d[0] * d[1], 4 * d[0] * d[1]
     if op == L.OP_BN_BWD_DX:
         return 12 * d[0] * d[1], 6 * d[0] * d[1]
+    if op == L.OP_BN_ACT_POOL:  # x read once (taps from L1/L2), pooled y16/y + argmax
+        n_in = d[0] * d[1] * d[2] * d[3]
+        return 4 * n_in + (n_in // 4) * (3 + (4 if has[4] else 0)), 6 * n_in
+    if op == L.OP_BN_BWD_REDUCE_POOL:  # windows: pooled gradient + argmax + x at the argmax
+        return 9 * d[0] * d[1] // 4, 4 * d[0] * d[1]
+    if op == L.OP_BN_BWD_DX_POOL:  # x + pooled gradient + argmax read, dx16 written
+        return 4 * d[0] * d[1] + 5 * d[0] * d[1] // 4 + 2 * d[0] * d[1], 10 * d[0] * d[1]
     if op == L.OP_BN_FWD_FUSED:  # read x once, write y and/or y16
         return (4 + (4 if has[4] else 0) + (2 if has[5] else 0)) * d[0] * d[1], 6 * d[0] * d[1]
     if op == L.OP_BN_BWD_FUSED:  # read dy and x once, write dx and/or dx16

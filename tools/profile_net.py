@@ -104,6 +104,10 @@ def main():
             fams_cp[f] = fams_cp.get(f, 0.0) + max(t[i] - 0.002, 0.0005)
         print(f"critical path: {len(path)} instructions, "
               + ", ".join(f"{k} {v:.3f}" for k, v in sorted(fams_cp.items(), key=lambda kv: -kv[1])))
+        if "--path" in sys.argv:
+            for i in reversed(path):
+                print(f"  cp #{i:4d} lane {lane[i]} {t[i] * 1e3:7.1f} us  "
+                      f"{bench.kernel_family(ex.instr_ops[i]):22s} {ex.instr_labels[i]}")
     print(f"{name}: {ex.num_instructions} instructions, {total:.3f} ms profiled pass, "
           f"kernels {ex.kernel_count()}, lanes {ex.lanes_used}")
     fams = {}
