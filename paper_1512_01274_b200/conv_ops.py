@@ -158,6 +158,10 @@ def _conv_operands(x: View, w: View, attrs, ctx, code: list):
     return col, wb, (m, kk, ldk, f, k, s, p, ho, wo)
 
 
+def _pointwise(k, s, p) -> bool:
+    return tuple(k) == (1, 1) and tuple(s) == (1, 1) and tuple(p) == (0, 0)
+
+
 def _implicit_ok(c: int) -> bool:
     return c % 8 == 0
 
@@ -212,6 +216,14 @@ def conv_forward_instrs(ins, out, attrs, colstats: Optional[int] = None) -> list
         ho, wo = _conv_out(h, wd, k, s, p)
         kk = k[0] * k[1] * c
         sp, ws = (1, None) if colstats else _auto_split(b * ho * wo, f, kk, ctx)
+        if _pointwise(k, s, p):
+            # 1x1 / stride 1: the bf16 copy IS the A operand -- both operands
+            # by TMA, no gather warps
+            g = _gemm(sh, c, False, wb, ldk, False, out.ptr, f, b * h * wd, f, c, bias=bias,
+                      splits=sp, ws=ws)
+            g.ptr[5] = colstats or None
+            code.append(g)
+            return code
         code.append(_gemm_conv(1, sh, x.shape, k, s, p, wb, ldk, out.ptr, f, b * ho * wo, f, kk,
                                bias=bias, colstats=colstats, splits=sp, ws=ws))
         return code
@@ -261,6 +273,10 @@ def _conv_lower_bwd(slot, env, out, attrs):
         ws = ctx.scratch(4 * nws) if nws else None
         if implicit:
             sh = _shadow(x, ctx.input_node("in0"), ctx, code)
+            if _pointwise(k, s, p):  # dW = dY^T x over the bf16 copies, both by TMA
+                code.append(_gemm(dyb, ldf, True, sh, c, True, out.ptr, kk, f, kk, m,
+                                  splits=0 if ws else 1, ws=ws))
+                return code
             code.append(_gemm_conv(2, sh, x.shape, k, s, p, dyb, ldf, out.ptr, kk, f, kk, m,
                                    splits=0 if ws else 1, ws=ws))
             return code
