@@ -435,9 +435,9 @@ inline size_t smem_bytes(int W, int CS, int rows_cta, int tensors) {
 }
 
 // Clusters of 8 (portable) then 16, slices of 8/4/2 vectors: the first shape
-// whose tile fits two CTAs per SM with >= one CTA per SM in total, else the
-// fitting shape with the most CTAs; none fits -> W == 0 (use the unfused
-// kernels).  A deterministic function of (M, C, tensors).
+// whose tile fits `smem_kb` with >= `min_ctas` CTAs, else the fitting shape
+// with the most CTAs; none fits -> W == 0 (use the unfused kernels).  A
+// deterministic function of (M, C, tensors).
 inline int env_int(const char* name, int dflt) {
   const char* v = getenv(name);
   return v && *v ? atoi(v) : dflt;
@@ -445,9 +445,11 @@ inline int env_int(const char* name, int dflt) {
 
 inline Cfg pick(int64_t M, int64_t C, int tensors) {
   // tuning knobs (read once): narrowest slice, CTA target, smem per CTA
-  static const int min_w = env_int("MGX_BNF_MINW", 2);
-  static const int min_ctas = env_int("MGX_BNF_MINCTAS", kNumSMs);
-  static const int smem_kb = env_int("MGX_BNF_SMEM_KB", 112);
+  // defaults measured on Inception-BN (bench sweep): slices of >= 4 vectors
+  // (full 32-byte sectors for the bf16 writes), >= 64 CTAs, up to 200 KB
+  static const int min_w = env_int("MGX_BNF_MINW", 4);
+  static const int min_ctas = env_int("MGX_BNF_MINCTAS", 64);
+  static const int smem_kb = env_int("MGX_BNF_SMEM_KB", 200);
   Cfg best;
   if (C % 8 != 0 || M < 1 || M * (C / 4) >= (int64_t(1) << 31)) return best;
   const int64_t C4 = C / 4;

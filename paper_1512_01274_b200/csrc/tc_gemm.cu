@@ -831,16 +831,23 @@ static int auto_splits(int64_t tiles, int64_t nk) {
   return static_cast<int>(s < 1 ? 1 : s);
 }
 
-// N tile: the width in {64, 128, 192, 256} that wastes the fewest columns
-// (ties to the wider tile: one tile row gathers/loads A once per BN columns)
+// N tile: the width in {64, 128, 192, 256} minimising n_tiles * (BN + 64):
+// the columns computed (padding included) plus a fixed per-tile cost worth
+// ~64 columns (operand A re-load / re-gather, pipeline fill, epilogue) --
+// narrow tiles multiply that cost and issue 4x more, smaller MMAs; ties go
+// to the wider tile.  (env MGX_BN_TILE_COST overrides the 64.)
 static int pick_bn(int64_t M, int64_t N) {
   (void)M;
+  static const int64_t over = [] {
+    const char* v = getenv("MGX_BN_TILE_COST");
+    return int64_t(v && *v ? atoi(v) : 64);
+  }();
   int best = 64;
-  int64_t waste = ceil_div(N, 64) * 64 - N;
+  int64_t cost = ceil_div(N, 64) * (64 + over);
   for (int bn : {128, 192, 256}) {
-    const int64_t w = ceil_div(N, bn) * bn - N;
-    if (w <= waste) {
-      waste = w;
+    const int64_t c = ceil_div(N, bn) * (bn + over);
+    if (c <= cost) {
+      cost = c;
       best = bn;
     }
   }

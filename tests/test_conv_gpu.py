@@ -322,7 +322,7 @@ def test_batchnorm_backward_with_fused_relu(cuda, m, c, fix_gamma):
                                    rtol=1e-4, atol=2e-7 * mag)
 
 
-@pytest.mark.parametrize("m,c", [(12544, 96), (3136, 1024), (46656, 64), (1001, 40), (97, 8),
+@pytest.mark.parametrize("m,c", [(12544, 96), (3136, 1024), (23328, 64), (1001, 48), (97, 16),
                                  (12544, 576)])
 @pytest.mark.parametrize("fix_gamma,relu", [(True, True), (False, False), (False, True)])
 def test_batchnorm_cluster_fused(cuda, m, c, fix_gamma, relu):
