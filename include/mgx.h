@@ -220,12 +220,15 @@ int mgx_bn_bwd_dx(const float* dy, const float* x, const float* stats, const flo
  * (x - mean) rstd relu_gamma + relu_beta > 0); dbeta = sum dy', dgamma =
  * sum dy' xhat (0 when dgamma_zero), sums = [dbeta | dgamma] (optional),
  * dx = gamma rstd (dy' - (dbeta + xhat dgamma) / M) -> dx / dx16 (each
- * optional, one required), dsum = sum dx (optional) in one kernel. */
+ * optional, one required), dsum = sum dx (optional) in one kernel.  ldd: row
+ * stride of dy in floats (C; larger when dy is a channel slice of a wider
+ * gradient, e.g. the gradient of a Concat read in place). */
 int mgx_bn_fused_ok(int64_t M, int64_t C, int backward, int* ok);
 int mgx_bn_fwd_fused(const float* x, int64_t M, int64_t C, float* stats, float* moving_mean,
                      float* moving_var, float eps, float momentum, const float* gamma,
                      const float* beta, float* y, void* y16, int act, uintptr_t stream);
-int mgx_bn_bwd_fused(const float* dy, const float* x, const float* stats, const float* gamma,
+int mgx_bn_bwd_fused(const float* dy, int64_t ldd, const float* x, const float* stats,
+                     const float* gamma,
                      int64_t M, int64_t C, const float* relu_gamma, const float* relu_beta,
                      float* dbeta, float* dgamma, int dgamma_zero, float* sums, float* dx,
                      void* dx16, float* dsum, uintptr_t stream);
@@ -371,7 +374,7 @@ typedef struct mgx_instr {
                               /* act                                               */
 #define MGX_OP_BN_BWD_FUSED 31 /* ptr0=dy ptr1=x ptr2=stats ptr3=gamma ptr4=dx     */
                               /* ptr5=dx16 dims=M,C,relu_gamma*,relu_beta*,dbeta*, */
-                              /* dgamma*,dgamma_zero,dsum*                          */
+                              /* dgamma*,dgamma_zero|ldd<<8,dsum* (ldd 0: C)        */
 #define MGX_OP_BN_ACT_POOL 32 /* ptr0=x ptr1=stats ptr2=gamma ptr3=beta ptr4=y     */
                               /* ptr5=y16 act dims=pool geom (7; full at bit 40 of */
                               /* dims6),argmax*                                    */

@@ -161,7 +161,7 @@ _SIGNATURES = {
     "mgx_bn_fused_ok": ([c_i64, c_i64, ctypes.c_int, ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
     "mgx_bn_fwd_fused": ([c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_f32, c_f32, c_vp, c_vp, c_vp,
                           c_vp, ctypes.c_int, c_uptr], ctypes.c_int),
-    "mgx_bn_bwd_fused": ([c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp,
+    "mgx_bn_bwd_fused": ([c_vp, c_i64, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp,
                           ctypes.c_int, c_vp, c_vp, c_vp, c_vp, c_uptr], ctypes.c_int),
     "mgx_bn_act_pool_fwd": ([c_vp, c_vp, c_vp, c_vp, ctypes.c_int, c_vp, ctypes.c_int, c_vp, c_vp,
                              c_vp, c_uptr], ctypes.c_int),

@@ -471,7 +471,8 @@ def _bn_lower_bwd(slot, env, out, attrs):
 def bn_backward_group(og: View, relu: bool, x: View, gamma: View, beta: View, attrs,
                       xnode, dx: Optional[View], dgamma: Optional[View],
                       dbeta: Optional[View], dbias_conv: Optional[View] = None,
-                      dx_node=None, dx_fp32: bool = True, pool=None) -> list:
+                      dx_node=None, dx_fp32: bool = True, pool=None,
+                      og_slice: Optional[tuple] = None) -> list:
     """All requested BatchNorm gradients of one node in one pass pair (the
     executor's fusion of the sibling Backward nodes, optionally with the
     ReLU backward in front of them): one reduction that also writes dbeta /
@@ -505,16 +506,20 @@ def bn_backward_group(og: View, relu: bool, x: View, gamma: View, beta: View, at
                            dbias_conv.ptr if dbias_conv is not None else 0, dws, dx16, g1, g2]))
         return code
     if dx is not None and bn_fused_ok(m, c, True):
-        # reductions + dx (+ conv bias gradient) in one cluster kernel
+        # reductions + dx (+ conv bias gradient) in one cluster kernel;
+        # og_slice = (pointer, row stride): the output gradient read in
+        # place from a channel slice of a Concat's gradient (executor)
         g = None if fix else gamma.ptr
         dx16 = ctx.shadow_out(dx.size, dx_node) if (c % 8 == 0 and dx_node is not None) else None
         dxp = dx.ptr if (dx_fp32 or dx16 is None) else None
-        code.append(instr(L.OP_BN_BWD_FUSED, [og.ptr, x.ptr, st, g, dxp, dx16],
+        ogp, ldd = og_slice if og_slice is not None else (og.ptr, 0)
+        code.append(instr(L.OP_BN_BWD_FUSED, [ogp, x.ptr, st, g, dxp, dx16],
                           [m, c, (g or 0) if relu else 0, beta.ptr if relu else 0,
                            dbeta.ptr if dbeta else 0, dgamma.ptr if dgamma else 0,
-                           1 if fix else 0,
+                           (1 if fix else 0) | (ldd << 8),
                            dbias_conv.ptr if dbias_conv is not None else 0]))
         return code
+    assert og_slice is None, "an in-place gradient slice needs the cluster BatchNorm kernel"
     sums = ctx.persistent(8 * c)
     ws = ctx.scratch(_reduce_ws(m, c))
     g = None if fix else gamma.ptr

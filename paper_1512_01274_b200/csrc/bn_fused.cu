@@ -189,7 +189,7 @@ __device__ __forceinline__ void wait_stage(int left) {
 // groups of s.per row-iterations each (local row l = rin + k * RP).
 template <int W, int N>
 __device__ __forceinline__ void stage_in(const Slice& s, const float4* const (&src)[N],
-                                         float4* const (&dst)[N], int C4) {
+                                         float4* const (&dst)[N], const int (&ld4)[N]) {
   constexpr int RP = kThreads / W;
   for (int st = 0; st < kStages; ++st) {
     for (int k = st * s.per; k < (st + 1) * s.per; ++k) {
@@ -197,7 +197,7 @@ __device__ __forceinline__ void stage_in(const Slice& s, const float4* const (&s
       if (r >= s.r1) break;
       const int l = (s.rin + k * RP) * W + s.v;
 #pragma unroll
-      for (int t = 0; t < N; ++t) cp_async16(dst[t] + l, src[t] + r * C4 + s.c4, true);
+      for (int t = 0; t < N; ++t) cp_async16(dst[t] + l, src[t] + r * ld4[t] + s.c4, true);
     }
     cp_async_commit();
   }
@@ -233,7 +233,8 @@ bn_fwd_fused_kernel(const float* __restrict__ x, int M, int C, int rows_cta, flo
   {
     const float4* src[1] = {x4};
     float4* dst[1] = {tile};
-    stage_in<W, 1>(s, src, dst, C4);
+    const int ld4[1] = {C4};
+    stage_in<W, 1>(s, src, dst, ld4);
   }
   const float4 shv = __ldg(x4 + s.c4);  // row 0: the shift of the sums
   const float sh[4] = {shv.x, shv.y, shv.z, shv.w};
@@ -303,7 +304,7 @@ bn_fwd_fused_kernel(const float* __restrict__ x, int M, int C, int rows_cta, flo
 // (the bias gradient of the convolution feeding the BatchNorm, optional).
 template <int W>
 __global__ void __launch_bounds__(kThreads)
-bn_bwd_fused_kernel(const float* __restrict__ dy, const float* __restrict__ x,
+bn_bwd_fused_kernel(const float* __restrict__ dy, int ldd, const float* __restrict__ x,
                     const float* __restrict__ stats, const float* __restrict__ gamma, int M,
                     int C, int rows_cta, const float* __restrict__ relu_gamma,
                     const float* __restrict__ relu_beta, float* __restrict__ dbeta,
@@ -331,7 +332,8 @@ bn_bwd_fused_kernel(const float* __restrict__ dy, const float* __restrict__ x,
   {
     const float4* src[2] = {reinterpret_cast<const float4*>(dy), reinterpret_cast<const float4*>(x)};
     float4* dst[2] = {tdy, tx};
-    stage_in<W, 2>(s, src, dst, C4);
+    const int ld4[2] = {ldd >> 2, C4};
+    stage_in<W, 2>(s, src, dst, ld4);
   }
   const bool relu = relu_beta != nullptr;
   float mu[4], rs[4], gm[4], bt[4], g[4];
@@ -512,7 +514,7 @@ int launch_fwd(const Cfg& cfg, int64_t C, cudaStream_t st, Args... args) {
 
 template <int W, typename... Args>
 int launch_bwd(const Cfg& cfg, int64_t C, cudaStream_t st, Args... args) {
-  return Launcher<const float*, const float*, const float*, const float*, int, int, int,
+  return Launcher<const float*, int, const float*, const float*, const float*, int, int, int,
                   const float*, const float*, float*, float*, int, float*, float*,
                   __nv_bfloat16*, float*>::template run<bn_bwd_fused_kernel<W>>(cfg, C, st,
                                                                                   args...);
@@ -556,13 +558,14 @@ extern "C" int mgx_bn_fwd_fused(const float* x, int64_t M, int64_t C, float* sta
   }
 }
 
-extern "C" int mgx_bn_bwd_fused(const float* dy, const float* x, const float* stats,
+extern "C" int mgx_bn_bwd_fused(const float* dy, int64_t ldd, const float* x, const float* stats,
                                 const float* gamma, int64_t M, int64_t C, const float* relu_gamma,
                                 const float* relu_beta, float* dbeta, float* dgamma,
                                 int dgamma_zero, float* sums, float* dx, void* dx16, float* dsum,
                                 uintptr_t stream) {
-  MGX_REQUIRE(dy && x && stats && (dx || dx16) && M > 0 && C > 0 && C <= 65536,
-              "mgx_bn_bwd_fused: bad arguments");
+  MGX_REQUIRE(dy && x && stats && (dx || dx16) && M > 0 && C > 0 && C <= 65536 &&
+                  ldd >= C && ldd % 4 == 0 && ldd < (int64_t(1) << 24),
+              "mgx_bn_bwd_fused: bad arguments (dy row stride ldd >= C, multiple of 4)");
   MGX_REQUIRE(mgx::aligned16(dy) && mgx::aligned16(x) && (!dx || mgx::aligned16(dx)) &&
                   (!dx16 || mgx::aligned16(dx16)),
               "mgx_bn_bwd_fused: unaligned tensors");
@@ -574,15 +577,15 @@ extern "C" int mgx_bn_bwd_fused(const float* dy, const float* x, const float* st
   __nv_bfloat16* h = static_cast<__nv_bfloat16*>(dx16);
   switch (cfg.W) {
     case 8:
-      return mgx::bnf::launch_bwd<8>(cfg, C, st, dy, x, stats, gamma, M,
+      return mgx::bnf::launch_bwd<8>(cfg, C, st, dy, static_cast<int>(ldd), x, stats, gamma, M,
                               Ci, cfg.rows_cta, relu_gamma, relu_beta, dbeta, dgamma, dgamma_zero,
                               sums, dx, h, dsum);
     case 4:
-      return mgx::bnf::launch_bwd<4>(cfg, C, st, dy, x, stats, gamma, M,
+      return mgx::bnf::launch_bwd<4>(cfg, C, st, dy, static_cast<int>(ldd), x, stats, gamma, M,
                               Ci, cfg.rows_cta, relu_gamma, relu_beta, dbeta, dgamma, dgamma_zero,
                               sums, dx, h, dsum);
     default:
-      return mgx::bnf::launch_bwd<2>(cfg, C, st, dy, x, stats, gamma, M,
+      return mgx::bnf::launch_bwd<2>(cfg, C, st, dy, static_cast<int>(ldd), x, stats, gamma, M,
                               Ci, cfg.rows_cta, relu_gamma, relu_beta, dbeta, dgamma, dgamma_zero,
                               sums, dx, h, dsum);
   }

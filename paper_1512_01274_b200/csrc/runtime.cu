@@ -351,9 +351,10 @@ static int run_instr(const mgx_instr& in, cudaStream_t st) {
                               reinterpret_cast<float*>(d[3]), in.fattr[0], in.fattr[1], p2, p3,
                               static_cast<float*>(in.ptr[4]), in.ptr[5], in.act, s);
     case MGX_OP_BN_BWD_FUSED:
-      return mgx_bn_bwd_fused(p0, p1, p2, p3, d[0], d[1], reinterpret_cast<const float*>(d[2]),
+      return mgx_bn_bwd_fused(p0, (d[6] >> 8) ? (d[6] >> 8) : d[1], p1, p2, p3, d[0], d[1],
+                              reinterpret_cast<const float*>(d[2]),
                               reinterpret_cast<const float*>(d[3]), reinterpret_cast<float*>(d[4]),
-                              reinterpret_cast<float*>(d[5]), static_cast<int>(d[6]), nullptr,
+                              reinterpret_cast<float*>(d[5]), static_cast<int>(d[6] & 0xFF), nullptr,
                               static_cast<float*>(in.ptr[4]), in.ptr[5],
                               reinterpret_cast<float*>(d[7]), s);
     case MGX_OP_WFLIP: return mgx_weight_flip_bf16(p0, d[0], d[1], d[2], d[3], in.ptr[1], d[4], s);

@@ -356,7 +356,7 @@ def test_batchnorm_cluster_fused(cuda, m, c, fix_gamma, relu):
     dgamma = torch.full((c,), float("nan"), device="cuda")
     sums = torch.empty(2 * c, device="cuda")
     dsum = torch.empty(c, device="cuda")
-    L.call("mgx_bn_bwd_fused", og.data_ptr(), x.data_ptr(), st.data_ptr(), gp, m, c,
+    L.call("mgx_bn_bwd_fused", og.data_ptr(), c, x.data_ptr(), st.data_ptr(), gp, m, c,
            gp if relu else None, beta.data_ptr() if relu else None, dbeta.data_ptr(),
            dgamma.data_ptr(), 1 if fix_gamma else 0, sums.data_ptr(), dx.data_ptr(),
            dx16.data_ptr(), dsum.data_ptr(), 0)
@@ -395,11 +395,21 @@ def test_batchnorm_cluster_fused(cuda, m, c, fix_gamma, relu):
                                rtol=1e-4, atol=2e-7 * mag)
     # deterministic: a second run is bitwise identical
     dx_b = torch.empty_like(dx)
-    L.call("mgx_bn_bwd_fused", og.data_ptr(), x.data_ptr(), st.data_ptr(), gp, m, c,
+    L.call("mgx_bn_bwd_fused", og.data_ptr(), c, x.data_ptr(), st.data_ptr(), gp, m, c,
            gp if relu else None, beta.data_ptr() if relu else None, None, None, 0, None,
            dx_b.data_ptr(), None, None, 0)
     torch.cuda.synchronize()
     assert torch.equal(dx_b, dx)
+    # the output gradient read in place from a channel slice of a wider
+    # tensor (a Concat's gradient): row stride ldd = c + 16, offset 8
+    wide = torch.zeros(m, c + 16, device="cuda")
+    wide[:, 8:8 + c] = og
+    dx_w = torch.empty_like(dx)
+    L.call("mgx_bn_bwd_fused", wide.data_ptr() + 8 * 4, c + 16, x.data_ptr(), st.data_ptr(), gp,
+           m, c, gp if relu else None, beta.data_ptr() if relu else None, None, None, 0, None,
+           dx_w.data_ptr(), None, None, 0)
+    torch.cuda.synchronize()
+    assert torch.equal(dx_w, dx)
 
 
 @pytest.mark.parametrize("shape,k,s,p", [((2, 18, 18, 16), 3, 2, 0), ((2, 13, 11, 8), 3, 2, 1),

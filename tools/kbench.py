@@ -145,7 +145,7 @@ def bench_bn_fused(torch, L):
                    y16.data_ptr(), 1, 0)
 
         def bwd():
-            L.call("mgx_bn_bwd_fused", dy.data_ptr(), x.data_ptr(), st.data_ptr(), gam.data_ptr(),
+            L.call("mgx_bn_bwd_fused", dy.data_ptr(), c, x.data_ptr(), st.data_ptr(), gam.data_ptr(),
                    m, c, gam.data_ptr(), bet.data_ptr(), db.data_ptr(), dg.data_ptr(), 0, None,
                    None, y16.data_ptr(), ds.data_ptr(), 0)
         fwd()
