@@ -545,21 +545,23 @@ colreduce_partial_vec_kernel(const float* __restrict__ a, const float* __restric
 // channels per 256-thread block); lane l sums chunks l, l+32, ... in
 // ascending order, then the 32 lane sums meet in a fixed xor-butterfly tree
 // (the same tree every run: deterministic).
-constexpr int kFinChannels = 8;
+constexpr int kFinChannels = 1;  // channels per 256-thread finalize block
 
 __device__ __forceinline__ void merge_chunks(const double* __restrict__ ws, int nchunk, int C,
                                              int c, bool two, double* s_out, double* q_out) {
-  const int lane = threadIdx.x & 31;
+  // the whole block on one channel: thread t sums chunks t, t + 256, ...
+  // (loads batched 8 deep, ascending), then a fixed xor tree per warp and
+  // the 8 warp sums in warp order -- deterministic; valid in thread 0
+  __shared__ double wsum[2][8];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   double s = 0.0, q = 0.0;
   if (c < C) {
-    // loads batched 8 deep per lane (latency-bound otherwise), summed in
-    // the same ascending chunk order
     constexpr int B = 8;
-    for (int z0 = lane; z0 < nchunk; z0 += 32 * B) {
+    for (int z0 = t; z0 < nchunk; z0 += 256 * B) {
       double a[B], b[B];
 #pragma unroll
       for (int u = 0; u < B; ++u) {
-        const int z = z0 + 32 * u;
+        const int z = z0 + 256 * u;
         a[u] = z < nchunk ? ws[int64_t(z) * C + c] : 0.0;
         b[u] = (two && z < nchunk) ? ws[int64_t(nchunk + z) * C + c] : 0.0;
       }
@@ -574,6 +576,19 @@ __device__ __forceinline__ void merge_chunks(const double* __restrict__ ws, int 
   for (int off = 16; off > 0; off >>= 1) {
     s += __shfl_xor_sync(0xffffffffu, s, off);
     q += __shfl_xor_sync(0xffffffffu, q, off);
+  }
+  if (lane == 0) {
+    wsum[0][warp] = s;
+    wsum[1][warp] = q;
+  }
+  __syncthreads();
+  if (t == 0) {
+    s = 0.0;
+    q = 0.0;
+    for (int w = 0; w < 8; ++w) {
+      s += wsum[0][w];
+      q += wsum[1][w];
+    }
   }
   *s_out = s;
   *q_out = q;
@@ -691,9 +706,9 @@ __global__ void bn_stats_finalize_kernel(const double* __restrict__ ws, int nchu
                                          int use_global,
                                          float* __restrict__ stats, float* __restrict__ mmean,
                                          float* __restrict__ mvar) {
-  const int c = blockIdx.x * kFinChannels + (threadIdx.x >> 5);
+  const int c = blockIdx.x;
   if (use_global) {
-    if ((threadIdx.x & 31) == 0 && c < C) {
+    if (threadIdx.x == 0 && c < C) {
       stats[c] = mmean[c];
       stats[C + c] = static_cast<float>(1.0 / sqrt(double(mvar[c]) + double(eps)));
     }
@@ -701,7 +716,7 @@ __global__ void bn_stats_finalize_kernel(const double* __restrict__ ws, int nchu
   }
   double s = 0.0, q = 0.0;
   merge_chunks(ws, nchunk, C, c, true, &s, &q);
-  if ((threadIdx.x & 31) != 0 || c >= C) return;
+  if (threadIdx.x != 0 || c >= C) return;
   // sums were taken relative to shift = x[0, c]
   const double dm = s / double(M);
   const double mean = double(x[c]) + dm;
@@ -978,10 +993,10 @@ bn_pool_dx_k3s2_kernel(PoolGrad pg, const float* __restrict__ x, const float* __
 __global__ void colsum_finalize_kernel(const double* __restrict__ ws, int nchunk, int C, int two,
                                        float* __restrict__ out, float* __restrict__ out0,
                                        float* __restrict__ out1, int zero1) {
-  const int c = blockIdx.x * kFinChannels + (threadIdx.x >> 5);
+  const int c = blockIdx.x;
   double s = 0.0, q = 0.0;
   merge_chunks(ws, nchunk, C, c, two != 0, &s, &q);
-  if ((threadIdx.x & 31) != 0 || c >= C) return;
+  if (threadIdx.x != 0 || c >= C) return;
   out[c] = static_cast<float>(s);
   if (two) out[C + c] = static_cast<float>(q);
   if (out0) out0[c] = static_cast<float>(s);
@@ -1552,7 +1567,7 @@ extern "C" int mgx_bn_stats(const float* x, int64_t M, int64_t C, void* ws, floa
     MGX_TRY(mgx::conv::launch_partial<0>(x, nullptr, nullptr, M, static_cast<int>(C),
                                          static_cast<double*>(ws), &nchunk, st));
   }
-  mgx::conv::bn_stats_finalize_kernel<<<static_cast<unsigned>(mgx::ceil_div(C, mgx::conv::kFinChannels)), 32 * mgx::conv::kFinChannels, 0, st>>>(
+  mgx::conv::bn_stats_finalize_kernel<<<static_cast<unsigned>(mgx::ceil_div(C, mgx::conv::kFinChannels)), 256, 0, st>>>(
       static_cast<const double*>(ws), nchunk, M, static_cast<int>(C), x, eps, momentum, use_global,
       stats, moving_mean, moving_var);
   MGX_LAUNCHED();
@@ -1588,7 +1603,7 @@ extern "C" int mgx_bn_bwd_reduce(const float* dy, const float* x, const float* s
   int nchunk = 0;
   MGX_TRY(mgx::conv::launch_partial<1>(dy, x, stats, M, static_cast<int>(C), static_cast<double*>(ws),
                                        &nchunk, st, mgx::conv::ReluMask{relu_gamma, relu_beta}));
-  mgx::conv::colsum_finalize_kernel<<<static_cast<unsigned>(mgx::ceil_div(C, mgx::conv::kFinChannels)), 32 * mgx::conv::kFinChannels, 0, st>>>(
+  mgx::conv::colsum_finalize_kernel<<<static_cast<unsigned>(mgx::ceil_div(C, mgx::conv::kFinChannels)), 256, 0, st>>>(
       static_cast<const double*>(ws), nchunk, static_cast<int>(C), 1, sums, dbeta, dgamma,
       dgamma_zero);
   MGX_LAUNCHED();
@@ -1629,7 +1644,7 @@ extern "C" int mgx_bn_bwd_dx(const float* dy, const float* x, const float* stats
         dy, x, stats, sums, gamma, dx, rm, M, static_cast<int>(C), rpc, wsd,
         static_cast<__nv_bfloat16*>(dx16), mgx::conv::PoolGrad{});
     if (dsum)
-      mgx::conv::colsum_finalize_kernel<<<static_cast<unsigned>(mgx::ceil_div(C, mgx::conv::kFinChannels)), 32 * mgx::conv::kFinChannels, 0, st>>>(
+      mgx::conv::colsum_finalize_kernel<<<static_cast<unsigned>(mgx::ceil_div(C, mgx::conv::kFinChannels)), 256, 0, st>>>(
           static_cast<const double*>(ws), nchunk, static_cast<int>(C), 0, dsum, nullptr, nullptr, 0);
     MGX_LAUNCHED();
     return MGX_OK;
@@ -1647,7 +1662,7 @@ extern "C" int mgx_colsum(const float* x, int64_t M, int64_t C, void* ws, float*
   int nchunk = 0;
   MGX_TRY(mgx::conv::launch_partial<2>(x, nullptr, nullptr, M, static_cast<int>(C),
                                        static_cast<double*>(ws), &nchunk, st));
-  mgx::conv::colsum_finalize_kernel<<<static_cast<unsigned>(mgx::ceil_div(C, mgx::conv::kFinChannels)), 32 * mgx::conv::kFinChannels, 0, st>>>(
+  mgx::conv::colsum_finalize_kernel<<<static_cast<unsigned>(mgx::ceil_div(C, mgx::conv::kFinChannels)), 256, 0, st>>>(
       static_cast<const double*>(ws), nchunk, static_cast<int>(C), 0, out, nullptr, nullptr, 0);
   MGX_LAUNCHED();
   return MGX_OK;
@@ -1796,7 +1811,7 @@ extern "C" int mgx_bn_bwd_reduce_pooled(const float* dy_pool, const void* argmax
   mgx::conv::bn_pool_reduce_kernel<<<grid, ct4 * rpp, smem, st>>>(
       pg, x, stats, mgx::conv::ReluMask{relu_gamma, relu_beta}, Mp, static_cast<int>(C), rpc, wsd,
       mkw, mgx::conv::pg_mul(pg.g.Ho * pg.g.Wo), mgx::conv::pg_mul(pg.g.Wo));
-  mgx::conv::colsum_finalize_kernel<<<static_cast<unsigned>(mgx::ceil_div(C, mgx::conv::kFinChannels)), 32 * mgx::conv::kFinChannels, 0, st>>>(
+  mgx::conv::colsum_finalize_kernel<<<static_cast<unsigned>(mgx::ceil_div(C, mgx::conv::kFinChannels)), 256, 0, st>>>(
       wsd, nchunk, static_cast<int>(C), 1, sums, dbeta, dgamma, dgamma_zero);
   MGX_LAUNCHED();
   return MGX_OK;
@@ -1839,7 +1854,7 @@ extern "C" int mgx_bn_bwd_dx_pooled(const float* dy_pool, const void* argmax, co
         pg, x, stats, sums, gamma, rm, M, Mb, static_cast<int>(C), rpcb, wsd, h16,
         mgx::conv::pg_mul(Hb * Wb), mgx::conv::pg_mul(Wb));
     if (dsum)
-      mgx::conv::colsum_finalize_kernel<<<static_cast<unsigned>(mgx::ceil_div(C, mgx::conv::kFinChannels)), 32 * mgx::conv::kFinChannels, 0, st>>>(
+      mgx::conv::colsum_finalize_kernel<<<static_cast<unsigned>(mgx::ceil_div(C, mgx::conv::kFinChannels)), 256, 0, st>>>(
           wsd, nchunkb, static_cast<int>(C), 0, dsum, nullptr, nullptr, 0);
     MGX_LAUNCHED();
     return MGX_OK;
@@ -1851,7 +1866,7 @@ extern "C" int mgx_bn_bwd_dx_pooled(const float* dy_pool, const void* argmax, co
     mgx::conv::bn_dx_colsum_kernel<1><<<grid, ct4 * rpp, smem, st>>>(
         nullptr, x, stats, sums, gamma, dx, rm, M, static_cast<int>(C), rpc, wsd, h16, pg);
   if (dsum)
-    mgx::conv::colsum_finalize_kernel<<<static_cast<unsigned>(mgx::ceil_div(C, mgx::conv::kFinChannels)), 32 * mgx::conv::kFinChannels, 0, st>>>(
+    mgx::conv::colsum_finalize_kernel<<<static_cast<unsigned>(mgx::ceil_div(C, mgx::conv::kFinChannels)), 256, 0, st>>>(
         wsd, nchunk, static_cast<int>(C), 0, dsum, nullptr, nullptr, 0);
   MGX_LAUNCHED();
   return MGX_OK;
