@@ -1364,6 +1364,76 @@ pool_bwd_vec_kernel(const uint8_t* __restrict__ arg, const float* __restrict__ d
   }
 }
 
+// 3x3 / stride 1 / pad 1 average pooling (count_include_pad: every window
+// divides by 9) as a shared-memory box filter: a block stages a strip of
+// TR (+2 halo) rows x (W + 2) columns x 8 channel vectors, zero-padded, with
+// one coalesced read of each input element, then every output sums its 9
+// taps from shared memory.  Forward: taps in row-major order, then * 1/9;
+// backward: dx = sum over the covering windows in ascending (oh, ow) order
+// of dy * 1/9 -- pool_fwd_vec_kernel / pool_bwd_vec_kernel's arithmetic
+// (padding taps add exact zeros).
+constexpr int kAvgTR = 8, kAvgVS = 8;
+
+template <bool BWD>
+__global__ void __launch_bounds__(256)
+pool_avg3_tile_kernel(const float4* __restrict__ src, float4* __restrict__ dst,
+                      uint2* __restrict__ dst16, Geom g) {
+  extern __shared__ float4 avg_tile[];  // [kAvgTR + 2][W + 2][kAvgVS]
+  const int C4 = g.C >> 2;
+  const int nvs = (C4 + kAvgVS - 1) / kAvgVS;
+  const int ns = (g.H + kAvgTR - 1) / kAvgTR;
+  const int b = blockIdx.x / (nvs * ns);
+  const int rem = blockIdx.x - b * nvs * ns;
+  const int vs = rem / ns, strip = rem - (rem / ns) * ns;
+  const int h0 = strip * kAvgTR, v0 = vs * kAvgVS;
+  const int WP = g.W + 2;
+  const int rows = min(kAvgTR, g.H - h0);
+  const int nload = (rows + 2) * WP * kAvgVS;
+  for (int e = threadIdx.x; e < nload; e += blockDim.x) {
+    const int v = e % kAvgVS, cw = (e / kAvgVS) % WP, rr = e / (kAvgVS * WP);
+    const int h = h0 - 1 + rr, w = cw - 1, c4 = v0 + v;
+    avg_tile[e] = (h >= 0 && h < g.H && w >= 0 && w < g.W && c4 < C4)
+                  ? __ldg(src + ((int64_t(b) * g.H + h) * g.W + w) * C4 + c4)
+                  : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  __syncthreads();
+  const float inv = __frcp_rn(9.0f);
+  const int nout = rows * g.W * kAvgVS;
+  for (int e = threadIdx.x; e < nout; e += blockDim.x) {
+    const int v = e % kAvgVS, w = (e / kAvgVS) % g.W, r = e / (kAvgVS * g.W);
+    const int c4 = v0 + v;
+    if (c4 >= C4) continue;
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        const float4 t = avg_tile[((r + i) * WP + (w + j)) * kAvgVS + v];
+        if (BWD) {
+          acc[0] = fadd(acc[0], t.x * inv);
+          acc[1] = fadd(acc[1], t.y * inv);
+          acc[2] = fadd(acc[2], t.z * inv);
+          acc[3] = fadd(acc[3], t.w * inv);
+        } else {
+          acc[0] = fadd(acc[0], t.x);
+          acc[1] = fadd(acc[1], t.y);
+          acc[2] = fadd(acc[2], t.z);
+          acc[3] = fadd(acc[3], t.w);
+        }
+      }
+    float4 o = BWD ? make_float4(acc[0], acc[1], acc[2], acc[3])
+                   : make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
+    const int64_t i = ((int64_t(b) * g.H + h0 + r) * g.W + w) * C4 + c4;
+    if (dst) dst[i] = o;
+    if (dst16) {
+      uint2 hv;
+      hv.x = pack_bf16(o.x, o.y);
+      hv.y = pack_bf16(o.z, o.w);
+      dst16[i] = hv;
+    }
+  }
+}
+
 // out = ((s0 + s1) + s2) + ... : a chain of ElementwiseAdds (the gradient
 // fan-in build_gradient emits, symbol.py:254-258) in one pass, same
 // left-to-right rounding order.
@@ -1685,6 +1755,18 @@ extern "C" int mgx_pool_forward(const float* x, float* y, const int64_t* geom, i
   Geom g = mgx::conv::decode(geom, full != 0);
   MGX_REQUIRE(g.Ho > 0 && g.Wo > 0, "mgx_pool_forward: bad geometry");
   cudaStream_t st = mgx::as_stream(stream);
+  if (type == 1 && !full && pool_square(g) == 31 && g.ph == 1 && g.pw == 1 && g.Ho == g.H &&
+      g.Wo == g.W && g.C % 4 == 0 && mgx::aligned16(x) && (!y || mgx::aligned16(y)) &&
+      (!y16 || mgx::aligned16(y16)) && size_t(mgx::conv::kAvgTR + 2) * (g.W + 2) * 8 * 16 <= 48 * 1024) {
+    const int C4 = g.C / 4;
+    const int64_t blocks = int64_t(g.B) * ((C4 + 7) / 8) * ((g.H + mgx::conv::kAvgTR - 1) / mgx::conv::kAvgTR);
+    const size_t smem = size_t(mgx::conv::kAvgTR + 2) * (g.W + 2) * mgx::conv::kAvgVS * 16;
+    mgx::conv::pool_avg3_tile_kernel<false><<<static_cast<unsigned>(blocks), 256, smem, st>>>(
+        reinterpret_cast<const float4*>(x), reinterpret_cast<float4*>(y),
+        reinterpret_cast<uint2*>(y16), g);
+    MGX_LAUNCHED();
+    return MGX_OK;
+  }
   if (pool_vec_ok(g, x, y ? y : y16) && g.kh * g.kw <= 255) {
     const unsigned grid = grid_for(int64_t(g.B) * g.Ho * g.Wo * (g.C / 4));
     uint8_t* arg = type == 0 ? static_cast<uint8_t*>(argmax) : nullptr;
@@ -1720,6 +1802,17 @@ extern "C" int mgx_pool_backward(const float* x, const float* y, const float* dy
   Geom g = mgx::conv::decode(geom, full != 0);
   cudaStream_t st = mgx::as_stream(stream);
   const bool use_arg = type == 0 && argmax != nullptr;
+  if (type == 1 && !full && pool_square(g) == 31 && g.ph == 1 && g.pw == 1 && g.Ho == g.H &&
+      g.Wo == g.W && g.C % 4 == 0 && mgx::aligned16(dy) && mgx::aligned16(dx) &&
+      size_t(mgx::conv::kAvgTR + 2) * (g.W + 2) * 8 * 16 <= 48 * 1024) {
+    const int C4 = g.C / 4;
+    const int64_t blocks = int64_t(g.B) * ((C4 + 7) / 8) * ((g.H + mgx::conv::kAvgTR - 1) / mgx::conv::kAvgTR);
+    const size_t smem = size_t(mgx::conv::kAvgTR + 2) * (g.W + 2) * mgx::conv::kAvgVS * 16;
+    mgx::conv::pool_avg3_tile_kernel<true><<<static_cast<unsigned>(blocks), 256, smem, st>>>(
+        reinterpret_cast<const float4*>(dy), reinterpret_cast<float4*>(dx), nullptr, g);
+    MGX_LAUNCHED();
+    return MGX_OK;
+  }
   if (pool_vec_ok(g, dy, dx) && (type == 1 || use_arg)) {
     const unsigned grid = grid_for(int64_t(g.B) * g.H * g.W * (g.C / 4));
     const uint8_t* arg = static_cast<const uint8_t*>(argmax);
