@@ -313,6 +313,22 @@ def _conv_lower_bwd(slot, env, out, attrs):
         code.append(_gemm(dcolt, ldkf, False, wfl, ldkf, False, out.ptr, c, b * h * wd, c, kf,
                           splits=sp, ws=ws))
         return code
+    if s == (2, 2) and p[0] < k[0] and p[1] < k[1] and f % 8 == 0:
+        # stride 2: dX = the stride-1 transposed convolution of dY read
+        # dilated by 2 (gather mode 3) with the flipped weights -- no column
+        # matrix, no col2im
+        kf = k[0] * k[1] * f
+        ldkf = _pad8(kf)
+        key = ("wflip", id(ctx.input_node("in1")), w.ptr)
+        wfl = ctx.memo.get(key)
+        if wfl is None:
+            wfl = ctx.prep(key, 2 * c * ldkf,
+                           lambda dst: [instr(L.OP_WFLIP, [w.ptr, dst], [f, k[0], k[1], c, ldkf])],
+                           (w.ptr, w.ptr + 4 * w.size))
+        sp, ws = _auto_split(b * h * wd, c, kf, ctx)
+        code.append(_gemm_conv(3, dyb, x.shape, k, s, p, wfl, ldkf, out.ptr, c, b * h * wd, c, kf,
+                               splits=sp, ws=ws))
+        return code
     dcol = ctx.scratch(4 * m * kk)
     sp, ws = _auto_split(m, kk, f, ctx)
     code.append(_gemm(dyb, ldf, False, wb, ldk, True, dcol, kk, m, kk, f, splits=sp, ws=ws))

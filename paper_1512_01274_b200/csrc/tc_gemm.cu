@@ -193,6 +193,10 @@ struct Sched {
 struct Gather {
   const __nv_bfloat16* src;
   int B, H, W, C, kh, kw, sh, sw, ph, pw, Ho, Wo;
+  // dil 2: the source is read as if dilated by 2 (zeros between its pixels;
+  // the data gradient of a stride-2 convolution as a stride-1 transposed
+  // one): virtual position v is source position v / 2 when v is even
+  int dil;
   // n / d as __umul64hi(n, mul) for the runtime divisors (exact for any
   // 32-bit n; mul = 2^64 / d rounded up, 0 for d == 1)
   uint64_t mul_hw, mul_wo, mul_c, mul_kw;
@@ -348,8 +352,12 @@ tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
           const int oh = fdiv_u(rem, ga.mul_wo), ow = rem - oh * ga.Wo;
           hb[i] = b < 0 ? -(1 << 20) : oh * ga.sh - ga.ph;  // invalid row: always out of range
           wb[i] = ow * ga.sw - ga.pw;
-          rowp[i] = ga.src + (int64_t(b < 0 ? 0 : b) * ga.H * ga.W +
-                              int64_t(hb[i] < 0 && b < 0 ? 0 : hb[i]) * ga.W + wb[i]) * ga.C;
+          // dil 1: element (hb, wb, 0) of the row's window (may be virtual);
+          // dil 2: the row's image base
+          rowp[i] = ga.dil == 1
+                        ? ga.src + (int64_t(b < 0 ? 0 : b) * ga.H * ga.W +
+                                    int64_t(hb[i] < 0 && b < 0 ? 0 : hb[i]) * ga.W + wb[i]) * ga.C
+                        : ga.src + int64_t(b < 0 ? 0 : b) * ga.H * ga.W * ga.C;
         }
         const int K = ga.kh * ga.kw * ga.C;
         // (tap row ti, tap column tj, channel c) of this thread's 8 K
@@ -368,14 +376,28 @@ tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
           mbar_wait_sleep(&empty[s], ph ^ 1);
           const uint32_t tile = smem_u32(smem + s * G::kStageBytes) + dbase;
           const bool kv = k < K;
+          if (ga.dil == 1) {
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int h = hb[i] + ti, w = wb[i] + tj;
-            const bool v = kv && static_cast<unsigned>(h) < static_cast<unsigned>(ga.H) &&
-                           static_cast<unsigned>(w) < static_cast<unsigned>(ga.W);
-            const void* src = v ? static_cast<const void*>(rowp[i] + koff)
-                                : static_cast<const void*>(ga.src);
-            cp_async16_zfill(tile + uint32_t(i * 16 * 128), src, v);
+            for (int i = 0; i < 8; ++i) {
+              const int h = hb[i] + ti, w = wb[i] + tj;
+              const bool v = kv && static_cast<unsigned>(h) < static_cast<unsigned>(ga.H) &&
+                             static_cast<unsigned>(w) < static_cast<unsigned>(ga.W);
+              const void* src = v ? static_cast<const void*>(rowp[i] + koff)
+                                  : static_cast<const void*>(ga.src);
+              cp_async16_zfill(tile + uint32_t(i * 16 * 128), src, v);
+            }
+          } else {
+            // dilated by 2: even virtual positions only, halved
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int h = hb[i] + ti, w = wb[i] + tj;
+              const bool v = kv && h >= 0 && w >= 0 && ((h | w) & 1) == 0 && (h >> 1) < ga.H &&
+                             (w >> 1) < ga.W;
+              const void* src =
+                  v ? static_cast<const void*>(rowp[i] + (int64_t(h >> 1) * ga.W + (w >> 1)) * ga.C + c)
+                    : static_cast<const void*>(ga.src);
+              cp_async16_zfill(tile + uint32_t(i * 16 * 128), src, v);
+            }
           }
           asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(
                            smem_u32(&full[s]))
@@ -958,7 +980,7 @@ extern "C" int mgx_gemm_bf16_conv(int mode, const void* src, const int64_t* geom
                                   int64_t M, int64_t N, int64_t K, int act, int splits,
                                   float* workspace, float* colstats, uintptr_t stream) {
   using namespace mgx::tc;
-  MGX_REQUIRE(src && geom && op && (mode == 1 || mode == 2), "mgx_gemm_bf16_conv: bad arguments");
+  MGX_REQUIRE(src && geom && op && (mode >= 1 && mode <= 3), "mgx_gemm_bf16_conv: bad arguments");
   MGX_REQUIRE(mgx::aligned16(src), "mgx_gemm_bf16_conv: source not 16-byte aligned");
   Gather ga;
   ga.src = static_cast<const __nv_bfloat16*>(src);
@@ -974,6 +996,34 @@ extern "C" int mgx_gemm_bf16_conv(int mode, const void* src, const int64_t* geom
   ga.pw = static_cast<int>(geom[6] & 0xFFFF);
   ga.Ho = (ga.H + 2 * ga.ph - ga.kh) / ga.sh + 1;
   ga.Wo = (ga.W + 2 * ga.pw - ga.kw) / ga.sw + 1;
+  ga.dil = 1;
+  if (mode == 3) {
+    // data gradient of a stride-2 convolution whose FORWARD geometry is
+    // `geom` (input B x H x W x C): src = dY [B, Ho, Wo, F] read dilated by
+    // 2 with pad k-1-p, op = the flipped weights [C, kh*kw*F], output
+    // dX [B*H*W, C] -- no column matrix, no col2im
+    MGX_REQUIRE(ga.sh == 2 && ga.sw == 2 && ga.ph < ga.kh && ga.pw < ga.kw && K % (ga.kh * ga.kw) == 0,
+                "mgx_gemm_bf16_conv: mode 3 needs stride 2 and pad < kernel");
+    const int F = static_cast<int>(K / (ga.kh * ga.kw));
+    const int H = ga.H, W = ga.W, Ho = ga.Ho, Wo = ga.Wo;
+    MGX_REQUIRE(F % 8 == 0 && M == int64_t(ga.B) * H * W && N == ga.C,
+                "mgx_gemm_bf16_conv: mode 3 shapes (F %% 8 == 0, M = B*H*W, N = C)");
+    ga.H = Ho;
+    ga.W = Wo;
+    ga.C = F;
+    ga.sh = ga.sw = 1;
+    ga.ph = ga.kh - 1 - ga.ph;
+    ga.pw = ga.kw - 1 - ga.pw;
+    ga.Ho = H;
+    ga.Wo = W;
+    ga.dil = 2;
+    ga.mul_hw = fastdiv_mul(H * W);
+    ga.mul_wo = fastdiv_mul(W);
+    ga.mul_c = fastdiv_mul(F);
+    ga.mul_kw = fastdiv_mul(ga.kw);
+    return gemm_impl(nullptr, 0, 0, op, ldop, 0, bias, C, ldc, M, N, K, act, splits, workspace, 1,
+                     ga, colstats, mgx::as_stream(stream));
+  }
   MGX_REQUIRE(ga.C % 8 == 0 && ga.C > 0 && ga.Ho > 0 && ga.Wo > 0 && ga.B > 0,
               "mgx_gemm_bf16_conv: the gathered tensor needs C %% 8 == 0");
   ga.mul_hw = fastdiv_mul(ga.Ho * ga.Wo);

@@ -142,8 +142,12 @@ def instr_cost(ins: L.Instr) -> tuple:
         m, n, k = d[0], d[1], d[2]
         a, w = d[6], d[7]
         src = 2 * ((a >> 48) & 0xFFFF) * ((a >> 32) & 0xFFFF) * ((a >> 16) & 0xFFFF) * (a & 0xFFFF)
-        opb = 2 * (n * k if (d[5] & 0xFF) == 1 else m * k)
-        return src + opb + 4 * m * n + (4 * n if has[2] else 0), 2 * m * n * k
+        mode = d[5] & 0xFF
+        opb = 2 * (n * k if mode in (1, 3) else m * k)
+        # mode 3 (stride-2 data gradient over the dilated dY): 3 of 4 taps
+        # multiply inserted zeros -- the algorithmic work is a quarter
+        flops = 2 * m * n * k // (4 if mode == 3 else 1)
+        return src + opb + 4 * m * n + (4 * n if has[2] else 0), flops
     if op == L.OP_IM2COL:  # reads the input once, writes the bf16 col matrix
         b, h, w, c = d[0], d[1], d[2], d[3]
         kh, kw, sh, sw, ph, pw = d[4] >> 16, d[4] & 0xFFFF, d[5] >> 16, d[5] & 0xFFFF, d[6] >> 16, d[6] & 0xFFFF

@@ -71,6 +71,11 @@ CONV_CASES = [
     (2, 15, 15, 3, 8, (7, 7), (2, 2), (3, 3)),
     (1, 23, 23, 3, 12, (11, 11), (4, 4), (2, 2)),
     (2, 9, 9, 12, 20, (3, 3), (2, 2), (1, 1)),
+    # stride-2 data gradient as a transposed convolution over dY read dilated
+    # (gather mode 3): exact and ragged (14 -> 7) output extents
+    (2, 14, 14, 16, 24, (3, 3), (2, 2), (1, 1)),
+    (2, 27, 27, 32, 16, (3, 3), (2, 2), (0, 0)),
+    (2, 10, 11, 8, 16, (3, 3), (2, 2), (1, 1)),
 ]
 
 
