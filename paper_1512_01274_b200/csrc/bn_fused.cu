@@ -452,8 +452,9 @@ inline Cfg pick(int64_t M, int64_t C, int tensors) {
   static const int min_w = env_int("MGX_BNF_MINW", 4);
   static const int min_ctas = env_int("MGX_BNF_MINCTAS", 64);
   static const int smem_kb = env_int("MGX_BNF_SMEM_KB", 200);
+  static const int max_m = env_int("MGX_BNF_MAXM", 1 << 30);
   Cfg best;
-  if (C % 8 != 0 || M < 1 || M * (C / 4) >= (int64_t(1) << 31)) return best;
+  if (C % 8 != 0 || M < 1 || M > max_m || M * (C / 4) >= (int64_t(1) << 31)) return best;
   const int64_t C4 = C / 4;
   int64_t best_ctas = 0;
   for (int CS : {8, 16}) {
