@@ -368,35 +368,51 @@ def run_config(name, args, world, rank, local, eng, steps, warmup, with_e2e=True
             e._use_graph = True
         h2d = pin_x.numel() * 4 + pin_y.numel() * 4
         d2h = per * cfg["classes"] * 4
-        out_pin = torch.empty(per, cfg["classes"], dtype=torch.float32, pin_memory=True)
+        out_pins = [torch.empty(per, cfg["classes"], dtype=torch.float32, pin_memory=True)
+                    for _ in range(2)]
         y = ex.outputs[0]
+        pending = []
 
-        def e2e_step():
+        def e2e_step(i):
             # this step's batch was staged (H2D on the copy stream) while the
-            # previous step ran; stage the next one before waiting on this
+            # previous step ran; stage the next one, queue this step's D2H of
+            # the softmax output, then wait for the PREVIOUS step's output on
+            # the host (a depth-1 pipeline: the host never idles the GPU)
             step.step(staged=True)
             step.stage(w, pin_x, pin_y)
-            eng.push(lambda: L.call("mgx_memcpy_async", out_pin.data_ptr(), y.ptr, d2h,
+            buf = out_pins[i % 2]
+            eng.push(lambda: L.call("mgx_memcpy_async", buf.data_ptr(), y.ptr, d2h,
                                     eng.stream_handle), reads=[y.tag])
-            eng.wait_for(y.tag)
+            ev = torch.cuda.Event()
+            ev.record(eng.stream)
+            pending.append(ev)
+            if len(pending) > 1:
+                pending.pop(0).synchronize()
 
         step.stage(w, pin_x, pin_y)
-        for _ in range(max(warmup, 3)):
-            e2e_step()
+        for i in range(max(warmup, 3)):
+            e2e_step(i)
+        eng.wait_for(y.tag)
+        pending.clear()
         barrier(world)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(eng.stream)
         step.stage(w, pin_x, pin_y)  # the first timed step's copy, inside the region
-        for _ in range(steps):
-            e2e_step()
+        for i in range(steps):
+            e2e_step(i)
+        pending[-1].synchronize()  # the last step's output is on the host
         e1.record(eng.stream)
         torch.cuda.synchronize()
+        eng.wait_for(y.tag)  # surface any device-side error of the timed steps
+        pending.clear()
         e2e_ms = max_over_ranks(e0.elapsed_time(e1), world)
         res["e2e"] = {"value": per * world * steps / (e2e_ms / 1e3), "unit": "images/s",
                       "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                       "path": "DataParallelStep.stage (pinned H2D on a copy stream, overlapping the "
-                              "previous step) + step + D2H softmax output + sync, every step"}
+                              "previous step) + step + D2H of the softmax output every step, the "
+                              "host waiting for each step's output one step later (depth-1 "
+                              "pipeline)"}
         barrier(world)
 
     # ---- roofline: per-instruction device time (events captured between
