@@ -218,9 +218,14 @@ __device__ __forceinline__ void cp_async16_zfill(uint32_t dst, const void* src, 
 
 // GM: 0 plain (both operands by TMA); 1 A gathered (K-major: forward /
 // data gradient of a convolution); 2 B gathered (MN-major: weight gradient)
+// GM 3: A (K-major) loaded by TMA in im2col mode -- no gather warps
+template <int GM>
+constexpr bool gathered() {
+  return GM == 1 || GM == 2;
+}
 template <int GM>
 constexpr int threads_for() {
-  return GM ? kThreads + kGatherThreads : kThreads;
+  return gathered<GM>() ? kThreads + kGatherThreads : kThreads;
 }
 
 // ACTK: 0 no activation, 1 relu, 2 any (runtime code; cold path)
@@ -250,7 +255,7 @@ tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
     for (int s = 0; s < G::kStages; ++s) {
       // gathered operand: the 128 gather threads arrive (cp.async noinc)
-      mbar_init(&full[s], GM ? 1 + kGatherThreads : 1);
+      mbar_init(&full[s], gathered<GM>() ? 1 + kGatherThreads : 1);
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -278,13 +283,43 @@ tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
         int m0, nt, z, kb0, nkb;
         sc.tile(t, &m0, &nt, &z, &kb0, &nkb);
         const int n0 = nt * BN;
+        // GM 3: the tile's first output pixel -> its window origin (im2col
+        // coordinates); (tap, channel block) advanced per k-block
+        int iw = 0, ih = 0, in_ = 0, tap = 0, cb = 0;
+        if (GM == 3) {
+          const int hw = ga.Ho * ga.Wo;
+          in_ = m0 / hw;
+          const int rem = m0 - in_ * hw;
+          const int oh = rem / ga.Wo, ow = rem - (rem / ga.Wo) * ga.Wo;
+          ih = oh * ga.sh - ga.ph;
+          iw = ow * ga.sw - ga.pw;
+          const int k0 = kb0 * BK;
+          tap = k0 / ga.C;
+          cb = k0 - tap * ga.C;
+        }
         for (int kb = 0; kb < nkb; ++kb, ++it) {
           const int s = it % G::kStages;
           const uint32_t ph = (it / G::kStages) & 1;
           mbar_wait_sleep(&empty[s], ph ^ 1);
           uint8_t* sa = smem + s * G::kStageBytes;
           mbar_expect_tx(&full[s], GM == 1 ? G::kBBytes : GM == 2 ? G::kABytes : G::kStageBytes);
-          if (GM != 1) load_operand<A_MN, BM>(sa, &map_a, &full[s], (kb0 + kb) * BK, m0);
+          if (GM == 3) {
+            const int ti = tap / ga.kw, tj = tap - (tap / ga.kw) * ga.kw;
+            asm volatile(
+                "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%2, %3, %4, %5}], [%6], {%7, %8};" ::"r"(smem_u32(sa)),
+                "l"(reinterpret_cast<uint64_t>(&map_a)), "r"(cb), "r"(iw), "r"(ih), "r"(in_),
+                "r"(smem_u32(&full[s])), "h"(static_cast<uint16_t>(tj)),
+                "h"(static_cast<uint16_t>(ti))
+                : "memory");
+            cb += BK;
+            if (cb == ga.C) {
+              cb = 0;
+              ++tap;
+            }
+          } else if (GM != 1) {
+            load_operand<A_MN, BM>(sa, &map_a, &full[s], (kb0 + kb) * BK, m0);
+          }
           if (GM != 2)
             load_operand<B_MN, BN>(sa + G::kABytes, &map_b, &full[s], (kb0 + kb) * BK, n0);
         }
@@ -308,7 +343,7 @@ tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
           mbar_wait(&full[s], ph);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           // cp.async (generic proxy) writes -> tcgen05.mma (async proxy) reads
-          if (GM) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          if (gathered<GM>()) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           const uint8_t* sa = smem + s * G::kStageBytes;
           const uint64_t adesc = A_MN ? smem_desc_mn_sw128(sa) : smem_desc_sw128(sa);
           const uint64_t bdesc = B_MN ? smem_desc_mn_sw128(sa + G::kABytes)
@@ -326,7 +361,7 @@ tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
         umma_commit(&tfull[acc]);
       }
     }
-  } else if (GM && warp >= 6) {
+  } else if (gathered<GM>() && warp >= 6) {
     // ---------------- gather producers (implicit GEMM): cp.async 16-byte
     // chunks straight into the 128B-swizzled operand tile, zero-filled
     // outside the input; the mbarrier arrival fires when they land
@@ -744,6 +779,48 @@ __global__ void cast_f32_bf16_kernel(const float* __restrict__ x, __nv_bfloat16*
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 static std::once_flag g_encode_once;
 
+typedef CUresult (*PFN_encode_im2col)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                       const cuuint64_t*, const cuuint64_t*, const int*,
+                                       const int*, cuuint32_t, cuuint32_t, const cuuint32_t*,
+                                       CUtensorMapInterleave, CUtensorMapSwizzle,
+                                       CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static PFN_encode_im2col g_encode_im2col = nullptr;
+static std::once_flag g_im2col_once;
+
+// TMA im2col map of a bf16 NHWC tensor for a k x k / stride s / pad p
+// convolution: each load gives 128 consecutive output pixels x 64 channels
+// of one filter tap (offsets in the instruction), zero in the padding
+static int encode_im2col(CUtensorMap* map, const void* src, int B, int H, int W, int C, int kh,
+                         int kw, int sh, int sw, int ph, int pw) {
+  std::call_once(g_im2col_once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &fn, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode_im2col = reinterpret_cast<PFN_encode_im2col>(fn);
+  });
+  if (!g_encode_im2col) {
+    set_error("cuTensorMapEncodeIm2col unavailable from the driver");
+    return MGX_INTERNAL;
+  }
+  cuuint64_t dims[4] = {cuuint64_t(C), cuuint64_t(W), cuuint64_t(H), cuuint64_t(B)};
+  cuuint64_t strides[3] = {cuuint64_t(C) * 2, cuuint64_t(W) * C * 2, cuuint64_t(H) * W * C * 2};
+  int lower[2] = {-pw, -ph};
+  int upper[2] = {pw - (kw - 1), ph - (kh - 1)};
+  cuuint32_t estr[4] = {1, cuuint32_t(sw), cuuint32_t(sh), 1};
+  CUresult r = g_encode_im2col(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(src),
+                               dims, strides, lower, upper, BK, BM, estr,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeIm2col failed (%d)", static_cast<int>(r));
+    return MGX_INTERNAL;
+  }
+  return MGX_OK;
+}
+
 static int get_encode() {
   std::call_once(g_encode_once, [] {
     cudaDriverEntryPointQueryResult q;
@@ -831,6 +908,7 @@ static int launch_acts(const Launch& l, cudaStream_t st) {
 template <int BN>
 static int launch_bn(int a_mn, int b_mn, int gm, const Launch& l, cudaStream_t st) {
   if (gm == 1) return launch_acts<false, false, BN, 1>(l, st);  // implicit A, B K-major
+  if (gm == 3) return launch_acts<false, false, BN, 3>(l, st);  // A by TMA im2col, B K-major
   if (gm == 2) return launch_acts<true, true, BN, 2>(l, st);    // A MN-major, implicit B
   if (!a_mn && !b_mn) return launch_acts<false, false, BN, 0>(l, st);
   if (!a_mn && b_mn) return launch_acts<false, true, BN, 0>(l, st);
@@ -889,12 +967,13 @@ static int gemm_impl(const void* A, int64_t lda, int a_mn, const void* B, int64_
                      int act, int splits, float* workspace, int gm, const Gather& ga,
                      float* colstats, cudaStream_t st) {
   MGX_REQUIRE(C && M > 0 && N > 0 && K > 0, "mgx_gemm_bf16_tc: bad arguments");
-  MGX_REQUIRE((gm == 1 || A) && (gm == 2 || B), "mgx_gemm_bf16_tc: missing operand");
-  MGX_REQUIRE((gm == 1 || lda % 8 == 0) && (gm == 2 || ldb % 8 == 0),
+  const bool a_impl = gm == 1 || gm == 3;  // A gathered / by TMA im2col
+  MGX_REQUIRE((a_impl || A) && (gm == 2 || B), "mgx_gemm_bf16_tc: missing operand");
+  MGX_REQUIRE((a_impl || lda % 8 == 0) && (gm == 2 || ldb % 8 == 0),
               "mgx_gemm_bf16_tc: leading dimensions must be multiples of 8");
-  MGX_REQUIRE((gm == 1 || lda >= (a_mn ? M : K)) && (gm == 2 || ldb >= (b_mn ? N : K)),
+  MGX_REQUIRE((a_impl || lda >= (a_mn ? M : K)) && (gm == 2 || ldb >= (b_mn ? N : K)),
               "mgx_gemm_bf16_tc: leading dimension smaller than the operand row");
-  MGX_REQUIRE((gm == 1 || mgx::aligned16(A)) && (gm == 2 || mgx::aligned16(B)),
+  MGX_REQUIRE((a_impl || mgx::aligned16(A)) && (gm == 2 || mgx::aligned16(B)),
               "mgx_gemm_bf16_tc: operands not 16-byte aligned");
   MGX_REQUIRE(M < (1ll << 31) && N < (1ll << 31) && K < (1ll << 31) && ldc < (1ll << 31),
               "mgx_gemm_bf16_tc: dimensions exceed 2^31");
@@ -910,7 +989,11 @@ static int gemm_impl(const void* A, int64_t lda, int a_mn, const void* B, int64_
   MGX_REQUIRE(int64_t(splits) * M < (1ll << 31), "mgx_gemm_bf16_tc: split workspace too tall");
   Launch l;
   std::memset(&l, 0, sizeof(l));
-  if (gm != 1) MGX_TRY(make_map(&l.ma, A, M, K, lda, a_mn != 0, BM));
+  if (gm == 3)
+    MGX_TRY(encode_im2col(&l.ma, ga.src, ga.B, ga.H, ga.W, ga.C, ga.kh, ga.kw, ga.sh, ga.sw,
+                          ga.ph, ga.pw));
+  else if (gm != 1)
+    MGX_TRY(make_map(&l.ma, A, M, K, lda, a_mn != 0, BM));
   if (gm != 2) MGX_TRY(make_map(&l.mb, B, N, K, ldb, b_mn != 0, bn));
   float* out = splits == 1 ? C : workspace;
   const int64_t oldc = splits == 1 ? ldc : N;
@@ -1035,8 +1118,17 @@ extern "C" int mgx_gemm_bf16_conv(int mode, const void* src, const int64_t* geom
   if (mode == 1) {
     // C[pixels, N] = gather(src)[pixels, kconv] . op[N, kconv]^T
     MGX_REQUIRE(M == pixels && K == kconv, "mgx_gemm_bf16_conv: M/K do not match the geometry");
-    return gemm_impl(nullptr, 0, 0, op, ldop, 0, bias, C, ldc, M, N, K, act, splits, workspace, 1,
-                     ga, colstats, mgx::as_stream(stream));
+    // whole 64-channel blocks per tap: the A tile by one TMA im2col load per
+    // k-block instead of the gather warps (env MGX_TMA_IM2COL=0 disables)
+    static const bool tma_im2col = [] {
+      const char* v = getenv("MGX_TMA_IM2COL");
+      return !(v && *v == '0');
+    }();
+    const bool use_tma = tma_im2col && ga.C % BK == 0 && ga.ph <= 127 && ga.pw <= 127 &&
+                         ga.kh - 1 - ga.ph <= 128 && ga.kw - 1 - ga.pw <= 128 && ga.sh <= 8 &&
+                         ga.sw <= 8;
+    return gemm_impl(nullptr, 0, 0, op, ldop, 0, bias, C, ldc, M, N, K, act, splits, workspace,
+                     use_tma ? 3 : 1, ga, colstats, mgx::as_stream(stream));
   }
   // C[M, kconv] = op[pixels, M]^T (MN-major) . gather(src)[pixels, kconv]
   MGX_REQUIRE(K == pixels && N == kconv, "mgx_gemm_bf16_conv: N/K do not match the geometry");

@@ -502,6 +502,11 @@ IMPLICIT_CASES = [
     (2, 15, 15, 24, 136, (3, 3), (2, 2), (1, 1)),
     (1, 23, 23, 8, 16, (7, 7), (2, 2), (3, 3)),
     (4, 27, 27, 96, 192, (3, 3), (1, 1), (1, 1)),
+    # C % 64 == 0: the A tile by TMA im2col loads (gather mode 3 of the kernel)
+    (2, 14, 14, 64, 96, (3, 3), (1, 1), (1, 1)),
+    (2, 15, 15, 128, 64, (3, 3), (2, 2), (1, 1)),
+    (1, 9, 11, 64, 40, (5, 5), (1, 1), (2, 2)),
+    (3, 7, 7, 192, 128, (3, 3), (1, 1), (1, 1)),
 ]
 
 
