@@ -919,6 +919,7 @@ bn_pool_dx_k3s2_kernel(PoolGrad pg, const float* __restrict__ x, const float* __
       gm[q] = relu && rm.gamma ? __ldg(rm.gamma + c) : 1.0f;
       bt[q] = relu ? __ldg(rm.beta + c) : 0.0f;
     }
+#pragma unroll 2
     for (int64_t r = r0 + r_in; r < r1; r += rpp) {
       const int ri = static_cast<int>(r);
       const int b = pg_div(ri, mul_blk);
