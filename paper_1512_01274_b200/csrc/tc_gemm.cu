@@ -916,17 +916,22 @@ static int launch_bn(int a_mn, int b_mn, int gm, const Launch& l, cudaStream_t s
   return launch_acts<true, true, BN, 0>(l, st);
 }
 
-// split-K count: fill about `target` CTAs (env MGX_SPLIT_TARGET; default 96
-// of the 148 SMs, measured best on Inception-BN: the graph runs independent
-// branches concurrently, so a GEMM need not own the whole GPU, and fewer
-// splits mean less workspace traffic), at least 4 k-blocks per split
+// split-K count: fill about `target` CTAs (env MGX_SPLIT_TARGET, default
+// 128 of the 148 SMs: the graph runs independent branches concurrently, so a
+// GEMM need not own the whole GPU), each split at least `min_kb` k-blocks
+// (env MGX_SPLIT_MINK, default 16: short splits are all prologue, epilogue
+// and workspace traffic) -- both measured best on Inception-BN
 static int auto_splits(int64_t tiles, int64_t nk) {
   static const int64_t target = [] {
     const char* v = getenv("MGX_SPLIT_TARGET");
-    return int64_t(v && *v ? atoi(v) : 96);
+    return int64_t(v && *v ? atoi(v) : 128);
+  }();
+  static const int64_t min_kb = [] {
+    const char* v = getenv("MGX_SPLIT_MINK");
+    return int64_t(v && *v ? atoi(v) : 16);
   }();
   if (tiles >= target) return 1;
-  int64_t want = target / tiles, most = nk / 4;
+  int64_t want = target / tiles, most = nk / min_kb;
   int64_t s = want < most ? want : most;
   return static_cast<int>(s < 1 ? 1 : s);
 }
