@@ -457,7 +457,9 @@ inline Cfg pick(int64_t M, int64_t C, int tensors) {
   if (C % 8 != 0 || M < 1 || M > max_m || M * (C / 4) >= (int64_t(1) << 31)) return best;
   const int64_t C4 = C / 4;
   int64_t best_ctas = 0;
-  for (int CS : {8, 16}) {
+  static const int cs_first = env_int("MGX_BNF_CS_FIRST", 8);
+  const int cs_order[2] = {cs_first, cs_first == 8 ? 16 : 8};
+  for (int CS : cs_order) {
     for (int W : {8, 4, 2}) {
       if (C4 % W || W < min_w) continue;
       const int rows = static_cast<int>(ceil_div(M, CS));
