@@ -1373,12 +1373,12 @@ pool_bwd_vec_kernel(const uint8_t* __restrict__ arg, const float* __restrict__ d
 // backward: dx = sum over the covering windows in ascending (oh, ow) order
 // of dy * 1/9 -- pool_fwd_vec_kernel / pool_bwd_vec_kernel's arithmetic
 // (padding taps add exact zeros).
-constexpr int kAvgTR = 8, kAvgVS = 8;
+constexpr int kAvgVS = 8;  // the strip height is chosen per shape (host)
 
 template <bool BWD>
 __global__ void __launch_bounds__(256)
 pool_avg3_tile_kernel(const float4* __restrict__ src, float4* __restrict__ dst,
-                      uint2* __restrict__ dst16, Geom g) {
+                      uint2* __restrict__ dst16, Geom g, int kAvgTR) {
   extern __shared__ float4 avg_tile[];  // [kAvgTR + 2][W + 2][kAvgVS]
   const int C4 = g.C >> 2;
   const int nvs = (C4 + kAvgVS - 1) / kAvgVS;
@@ -1743,6 +1743,19 @@ static bool pool_vec_ok(const Geom& g, const void* a, const void* b) {
   return (g.C % 4) == 0 && mgx::aligned16(a) && mgx::aligned16(b);
 }
 
+// rows per strip of pool_avg3_tile_kernel: as tall as 48 KB of shared
+// memory allows (whole 14x14 maps; 27x27 in two strips), 0 if not even one
+static int avg3_strip_rows(const Geom& g) {
+  const int64_t row_bytes = int64_t(g.W + 2) * mgx::conv::kAvgVS * 16;
+  int64_t tr = 48 * 1024 / row_bytes - 2;
+  if (tr > g.H) tr = g.H;
+  if (tr >= 2) {  // balance the strips: ceil(H / ceil(H / tr))
+    const int64_t ns = (g.H + tr - 1) / tr;
+    tr = (g.H + ns - 1) / ns;
+  }
+  return tr < 1 ? 0 : static_cast<int>(tr);
+}
+
 // 10 * K + S for the square K x K / stride S windows with unrolled kernels
 static int pool_square(const Geom& g) {
   if (g.kh == 3 && g.kw == 3 && g.sh == g.sw && (g.sh == 1 || g.sh == 2)) return 30 + g.sh;
@@ -1756,15 +1769,16 @@ extern "C" int mgx_pool_forward(const float* x, float* y, const int64_t* geom, i
   Geom g = mgx::conv::decode(geom, full != 0);
   MGX_REQUIRE(g.Ho > 0 && g.Wo > 0, "mgx_pool_forward: bad geometry");
   cudaStream_t st = mgx::as_stream(stream);
+  const int avg_tr = avg3_strip_rows(g);
   if (type == 1 && !full && pool_square(g) == 31 && g.ph == 1 && g.pw == 1 && g.Ho == g.H &&
       g.Wo == g.W && g.C % 4 == 0 && mgx::aligned16(x) && (!y || mgx::aligned16(y)) &&
-      (!y16 || mgx::aligned16(y16)) && size_t(mgx::conv::kAvgTR + 2) * (g.W + 2) * 8 * 16 <= 48 * 1024) {
+      (!y16 || mgx::aligned16(y16)) && avg_tr > 0) {
     const int C4 = g.C / 4;
-    const int64_t blocks = int64_t(g.B) * ((C4 + 7) / 8) * ((g.H + mgx::conv::kAvgTR - 1) / mgx::conv::kAvgTR);
-    const size_t smem = size_t(mgx::conv::kAvgTR + 2) * (g.W + 2) * mgx::conv::kAvgVS * 16;
+    const int64_t blocks = int64_t(g.B) * ((C4 + 7) / 8) * ((g.H + avg_tr - 1) / avg_tr);
+    const size_t smem = size_t(avg_tr + 2) * (g.W + 2) * mgx::conv::kAvgVS * 16;
     mgx::conv::pool_avg3_tile_kernel<false><<<static_cast<unsigned>(blocks), 256, smem, st>>>(
         reinterpret_cast<const float4*>(x), reinterpret_cast<float4*>(y),
-        reinterpret_cast<uint2*>(y16), g);
+        reinterpret_cast<uint2*>(y16), g, avg_tr);
     MGX_LAUNCHED();
     return MGX_OK;
   }
@@ -1803,14 +1817,14 @@ extern "C" int mgx_pool_backward(const float* x, const float* y, const float* dy
   Geom g = mgx::conv::decode(geom, full != 0);
   cudaStream_t st = mgx::as_stream(stream);
   const bool use_arg = type == 0 && argmax != nullptr;
+  const int avg_tr = avg3_strip_rows(g);
   if (type == 1 && !full && pool_square(g) == 31 && g.ph == 1 && g.pw == 1 && g.Ho == g.H &&
-      g.Wo == g.W && g.C % 4 == 0 && mgx::aligned16(dy) && mgx::aligned16(dx) &&
-      size_t(mgx::conv::kAvgTR + 2) * (g.W + 2) * 8 * 16 <= 48 * 1024) {
+      g.Wo == g.W && g.C % 4 == 0 && mgx::aligned16(dy) && mgx::aligned16(dx) && avg_tr > 0) {
     const int C4 = g.C / 4;
-    const int64_t blocks = int64_t(g.B) * ((C4 + 7) / 8) * ((g.H + mgx::conv::kAvgTR - 1) / mgx::conv::kAvgTR);
-    const size_t smem = size_t(mgx::conv::kAvgTR + 2) * (g.W + 2) * mgx::conv::kAvgVS * 16;
+    const int64_t blocks = int64_t(g.B) * ((C4 + 7) / 8) * ((g.H + avg_tr - 1) / avg_tr);
+    const size_t smem = size_t(avg_tr + 2) * (g.W + 2) * mgx::conv::kAvgVS * 16;
     mgx::conv::pool_avg3_tile_kernel<true><<<static_cast<unsigned>(blocks), 256, smem, st>>>(
-        reinterpret_cast<const float4*>(dy), reinterpret_cast<float4*>(dx), nullptr, g);
+        reinterpret_cast<const float4*>(dy), reinterpret_cast<float4*>(dx), nullptr, g, avg_tr);
     MGX_LAUNCHED();
     return MGX_OK;
   }
