@@ -159,7 +159,7 @@ int mgx_gemm_bf16_conv(int mode, const void* src, const int64_t* geom, const voi
  * the epilogue also writes, for every 32-row block b and column n of C, the
  * pair (mean, M2) of the block's valid rows as float2 colstats[b*N + n] --
  * the BatchNorm statistics of a convolution output without re-reading it.
- * mgx_bn_stats_from_tiles merges them (Chan's update, fp64, fixed order)
+ * mgx_bn_stats_from_tiles merges them (shifted fp64 sums, fixed order)
  * into stats = [mean | rstd] and updates the moving averages like
  * mgx_bn_stats. */
 int mgx_bn_stats_from_tiles(const void* part, int64_t M, int64_t C, float* stats,

@@ -729,47 +729,60 @@ __global__ void bn_stats_finalize_kernel(const double* __restrict__ ws, int nchu
 }
 
 // BatchNorm statistics from the GEMM epilogue's per-32-row (mean, M2)
-// pairs of the convolution output: a block per channel; thread t merges
-// row blocks t, t+256, ... (Chan's pairwise update, fp64), then a fixed
-// halving tree over the 256 partial results (deterministic).
-__global__ void bn_stats_from_tiles_kernel(const float2* __restrict__ part, int64_t M, int C,
-                                           float eps, float momentum, float* __restrict__ stats,
-                                           float* __restrict__ mmean, float* __restrict__ mvar) {
-  __shared__ double sn[256], smu[256], sm2[256];
+// pairs of the convolution output: a 1024-thread block per channel; thread
+// t sums tiles t, t + 1024, ... (loads batched 8 deep) as shifted sums
+// against tile 0's mean -- S1 = sum n_t (mean_t - s), S2 = sum [M2_t +
+// n_t (mean_t - s)^2] in fp64, no divisions -- then a fixed xor tree per warp
+// and the 32 warp sums in warp order (deterministic):
+//   mean = s + S1 / M,  var = S2 / M - (S1 / M)^2.
+__global__ void __launch_bounds__(1024)
+bn_stats_from_tiles_kernel(const float2* __restrict__ part, int64_t M, int C, float eps,
+                           float momentum, float* __restrict__ stats,
+                           float* __restrict__ mmean, float* __restrict__ mvar) {
+  __shared__ double ws1[32], ws2[32];
   const int c = blockIdx.x;
-  const int t = threadIdx.x;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int nb = static_cast<int>((M + 31) / 32);
-  double n = 0.0, mu = 0.0, m2 = 0.0;
-  for (int b = t; b < nb; b += blockDim.x) {
-    const float2 p = part[int64_t(b) * C + c];
-    const int64_t left = M - int64_t(b) * 32;
-    const double nb_ = double(left < 32 ? left : 32);
-    const double tot = n + nb_;
-    const double d = double(p.x) - mu;
-    mu += d * nb_ / tot;
-    m2 += double(p.y) + d * d * n * nb_ / tot;
-    n = tot;
-  }
-  sn[t] = n;
-  smu[t] = mu;
-  sm2[t] = m2;
-  __syncthreads();
-  for (int h = blockDim.x / 2; h > 0; h >>= 1) {
-    if (t < h) {
-      const double na = sn[t], nb_ = sn[t + h];
-      const double tot = na + nb_;
-      if (nb_ > 0.0) {
-        const double d = smu[t + h] - smu[t];
-        smu[t] = tot > 0.0 ? smu[t] + d * nb_ / tot : 0.0;
-        sm2[t] = sm2[t] + sm2[t + h] + (tot > 0.0 ? d * d * na * nb_ / tot : 0.0);
-        sn[t] = tot;
-      }
+  const double sh = double(part[c].x);
+  double s1 = 0.0, s2 = 0.0;
+  constexpr int B = 8;
+  for (int b0 = t; b0 < nb; b0 += 1024 * B) {
+    float2 p[B];
+#pragma unroll
+    for (int u = 0; u < B; ++u) {
+      const int b = b0 + 1024 * u;
+      p[u] = b < nb ? part[int64_t(b) * C + c] : make_float2(0.f, 0.f);
     }
-    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < B; ++u) {
+      const int b = b0 + 1024 * u;
+      if (b >= nb) continue;
+      const int64_t left = M - int64_t(b) * 32;
+      const double n = double(left < 32 ? left : 32);
+      const double d = double(p[u].x) - sh;
+      s1 += n * d;
+      s2 += double(p[u].y) + n * d * d;
+    }
   }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    s1 += __shfl_xor_sync(0xffffffffu, s1, off);
+    s2 += __shfl_xor_sync(0xffffffffu, s2, off);
+  }
+  if (lane == 0) {
+    ws1[warp] = s1;
+    ws2[warp] = s2;
+  }
+  __syncthreads();
   if (t == 0) {
-    const double mean = smu[0];
-    double var = sm2[0] / double(M);
+    double a1 = 0.0, a2 = 0.0;
+    for (int w = 0; w < 32; ++w) {
+      a1 += ws1[w];
+      a2 += ws2[w];
+    }
+    const double dm = a1 / double(M);
+    const double mean = sh + dm;
+    double var = a2 / double(M) - dm * dm;
     if (var < 0.0) var = 0.0;
     stats[c] = static_cast<float>(mean);
     stats[C + c] = static_cast<float>(1.0 / sqrt(var + double(eps)));
@@ -2023,7 +2036,7 @@ extern "C" int mgx_bn_stats_from_tiles(const void* part, int64_t M, int64_t C, f
                                        float* moving_mean, float* moving_var, float eps,
                                        float momentum, uintptr_t stream) {
   MGX_REQUIRE(part && stats && M > 0 && C > 0, "mgx_bn_stats_from_tiles: bad arguments");
-  mgx::conv::bn_stats_from_tiles_kernel<<<static_cast<unsigned>(C), 256, 0, mgx::as_stream(stream)>>>(
+  mgx::conv::bn_stats_from_tiles_kernel<<<static_cast<unsigned>(C), 1024, 0, mgx::as_stream(stream)>>>(
       static_cast<const float2*>(part), M, static_cast<int>(C), eps, momentum, stats, moving_mean,
       moving_var);
   MGX_LAUNCHED();
