@@ -1011,7 +1011,14 @@ static int gemm_impl(const void* A, int64_t lda, int a_mn, const void* B, int64_
   l.sc = Sched{static_cast<int>(m_tiles), static_cast<int>(n_tiles), splits, kps,
                static_cast<int>(nk), static_cast<int>(K)};
   const int64_t total = m_tiles * n_tiles * splits;
-  l.grid = static_cast<int>(total < mgx::kNumSMs ? total : mgx::kNumSMs);
+  // persistent CTAs: at most one per SM (env MGX_GEMM_MAX_CTAS caps it lower:
+  // concurrent branches of the graph share the GPU)
+  static const int64_t max_ctas = [] {
+    const char* v = getenv("MGX_GEMM_MAX_CTAS");
+    const int64_t c = v && *v ? atoi(v) : mgx::kNumSMs;
+    return c < 1 ? 1 : (c > mgx::kNumSMs ? int64_t(mgx::kNumSMs) : c);
+  }();
+  l.grid = static_cast<int>(total < max_ctas ? total : max_ctas);
   l.sstride = M * N;
   l.bias = splits == 1 ? bias : nullptr;
   l.act = splits == 1 ? act : 0;
