@@ -143,14 +143,19 @@ int mgx_gemm_bf16_tc_ex(const void* A, int64_t lda, int a_mn, const void* B, int
                         int64_t N, int64_t K, int act, int splits, float* workspace,
                         float* colstats, uintptr_t stream);
 /* Implicit-GEMM convolution contractions: one operand is gathered on the
- * fly from a compact bf16 NHWC tensor `src` (C % 8 == 0) by cp.async
- * producer warps inside the tcgen05 GEMM, never materialised:
+ * fly from a compact bf16 NHWC tensor `src` (C % 8 == 0) inside the tcgen05
+ * GEMM, never materialised -- by one TMA im2col load per k-block when
+ * C % 64 == 0 (mode 1), else by cp.async producer warps:
  *   gather(src)[m, k] = src[b, oh*sh-ph+i, ow*sw-pw+j, c],
  *   m = (b, oh, ow) output pixel, k = (i*kw + j)*C + c  (geom as below).
  * mode 1: C[M=pixels, N] = gather . op[N, K]^T      (op K-major, row stride
  *         ldop: convolution forward / stride-1 data gradient)
  * mode 2: C[M, N=kh*kw*C] = op[K=pixels, M]^T . gather  (op MN-major: the
- *         output gradient; weight gradient).  Split-K as mgx_gemm_bf16_tc_ex. */
+ *         output gradient; weight gradient)
+ * mode 3: data gradient of a stride-2 convolution whose FORWARD geometry is
+ *         geom: src = dY [B, Ho, Wo, F] read dilated by 2 with pad k-1-p,
+ *         op = the flipped weights [C, kh*kw*F], C[M=B*H*W, N=C].
+ * Split-K as mgx_gemm_bf16_tc_ex. */
 int mgx_gemm_bf16_conv(int mode, const void* src, const int64_t* geom, const void* op,
                        int64_t ldop, const float* bias, float* C, int64_t ldc, int64_t M,
                        int64_t N, int64_t K, int act, int splits, float* workspace,
