@@ -66,6 +66,70 @@ softmax_fwd_kernel(const float* __restrict__ x, float* __restrict__ p, int64_t B
   softmax_fwd_tile(blockIdx.x, x, p, Bn, C, leaves, nleaves);
 }
 
+// Wide rows (C >= 256: the 1000-class heads): a 256-thread block per row so
+// the elementwise exp and divide passes use the whole block (one group of 8
+// lanes per row left a batch of 64 on two SMs); the row maximum is order-
+// independent; the sum keeps the exact pairwise order above (one group of 8
+// lanes over the block's exponentials).  Bitwise the same result as
+// softmax_fwd_kernel.
+__global__ void __launch_bounds__(256)
+softmax_fwd_row_kernel(const float* __restrict__ x, float* __restrict__ p, int64_t C,
+                       const PwLeaf* __restrict__ leaves, int nleaves) {
+  __shared__ float red[8];
+  __shared__ float total;
+  const int64_t row = blockIdx.x;
+  const float* xr = x + row * C;
+  float* pr = p + row * C;
+  float mx = -INFINITY;
+  for (int64_t c = threadIdx.x; c < C; c += blockDim.x) mx = max_nan(mx, xr[c]);
+#pragma unroll
+  for (int mask = 1; mask < 32; mask <<= 1) mx = max_nan(mx, __shfl_xor_sync(0xffffffffu, mx, mask));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  mx = red[0];
+  for (int w = 1; w < 8; ++w) mx = max_nan(mx, red[w]);
+  for (int64_t c = threadIdx.x; c < C; c += blockDim.x) pr[c] = exp_rn(fsub(xr[c], mx));
+  __syncthreads();
+  if (threadIdx.x < 8) {
+    const int lane8 = threadIdx.x;
+    float stk[32];
+    int sp = 0;
+    float res = 0.0f;
+    for (int l = 0; l < nleaves; ++l) {
+      const PwLeaf lf = leaves[l];
+      const int nb = lf.len >> 3, tail = lf.len & 7;
+      float acc;
+      if (nb > 0) {
+        int64_t c = lf.start + lane8;
+        acc = pr[c];
+        for (int bb = 1; bb < nb; ++bb) {
+          c += 8;
+          acc = fadd(acc, pr[c]);
+        }
+#pragma unroll
+        for (int mask = 1; mask < 8; mask <<= 1) acc = fadd(acc, __shfl_xor_sync(0xffu, acc, mask));
+      } else {
+        acc = 0.0f;
+      }
+      for (int t = 0; t < tail; ++t) acc = fadd(acc, pr[lf.start + 8 * nb + t]);
+      if (nleaves == 1) {
+        res = acc;
+      } else {
+        stk[sp++] = acc;
+        for (int q = 0; q < lf.merges; ++q) {
+          --sp;
+          stk[sp - 1] = fadd(stk[sp - 1], stk[sp]);
+        }
+      }
+    }
+    if (nleaves > 1) res = stk[0];
+    if (lane8 == 0) total = res;
+  }
+  __syncthreads();
+  const float res = total;
+  for (int64_t c = threadIdx.x; c < C; c += blockDim.x) pr[c] = fdiv(pr[c], res);
+}
+
 }  // namespace
 
 int launch_softmax_forward(const float* x, float* p, int64_t Bn, int64_t C, cudaStream_t st) {
@@ -73,6 +137,11 @@ int launch_softmax_forward(const float* x, float* p, int64_t Bn, int64_t C, cuda
   int nleaves = 0, depth = 0;
   MGX_TRY(pw_leaf_table(C, &leaves, &nleaves, &depth));
   MGX_REQUIRE(depth <= 32, "softmax: %lld classes too deep", static_cast<long long>(C));
+  if (C >= 256 && Bn < (int64_t(1) << 31)) {
+    softmax_fwd_row_kernel<<<static_cast<unsigned>(Bn), 256, 0, st>>>(x, p, C, leaves, nleaves);
+    MGX_LAUNCHED();
+    return MGX_OK;
+  }
   const unsigned blocks = static_cast<unsigned>(ceil_div(Bn, 32));
   softmax_fwd_kernel<<<blocks, 256, 0, st>>>(x, p, Bn, C, leaves,
                                              nleaves);
