@@ -323,9 +323,17 @@ prep_batch_kernel(const mgx_prep_job* __restrict__ jobs, int njobs, int64_t unit
       // cast rows: dst[r, k] (rows x ldo) = src[r * ldi + k] for r < R, k < C, else 0
       const int64_t R = jb.a, C = jb.b, ldi = jb.c, ldo = jb.e;
       const int64_t r = e0 / ldo, k0 = e0 - r * ldo;
+      const float* sp = jb.src + r * ldi + k0;
+      if (r < R && k0 + 8 <= C && (reinterpret_cast<uintptr_t>(sp) & 15) == 0) {
+        const float4 a = __ldg(reinterpret_cast<const float4*>(sp));
+        const float4 c = __ldg(reinterpret_cast<const float4*>(sp) + 1);
+        v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+        v[4] = c.x; v[5] = c.y; v[6] = c.z; v[7] = c.w;
+      } else {
 #pragma unroll
-      for (int t = 0; t < 8; ++t)
-        v[t] = r < R && k0 + t < C ? __ldg(jb.src + r * ldi + k0 + t) : 0.0f;
+        for (int t = 0; t < 8; ++t)
+          v[t] = r < R && k0 + t < C ? __ldg(jb.src + r * ldi + k0 + t) : 0.0f;
+      }
     } else {
       // weight flip: dst[c, (i*kw + j)*F + f] (row stride ld) = w[f, kh-1-i, kw-1-j, c]
       const int F = static_cast<int>(jb.a), kh = static_cast<int>(jb.b);
