@@ -37,16 +37,32 @@ def main():
         sums = torch.empty(2 * c, device="cuda")
         dx16 = torch.empty(m, c, dtype=torch.bfloat16, device="cuda")
         ds = torch.empty(c, device="cuda")
-        for _ in range(3):
+
+        def fwd():
             L.call("mgx_bn_act_pool_fwd", x.data_ptr(), st.data_ptr(), None, beta.data_ptr(), 1,
                    gp, 0, None, y16.data_ptr(), arg.data_ptr(), 0)
+
+        def red():
             L.call("mgx_bn_bwd_reduce_pooled", dyp.data_ptr(), arg.data_ptr(), gp, 0, x.data_ptr(),
                    st.data_ptr(), m, c, ws.data_ptr(), sums.data_ptr(), None, None, 1, None,
                    beta.data_ptr(), 0)
+
+        def dxp():
             L.call("mgx_bn_bwd_dx_pooled", dyp.data_ptr(), arg.data_ptr(), gp, 0, x.data_ptr(),
                    st.data_ptr(), sums.data_ptr(), None, m, c, beta.data_ptr(), ds.data_ptr(),
                    ws.data_ptr(), None, dx16.data_ptr(), 0)
-        torch.cuda.synchronize()
+        for name, fn in (("bn_act_pool_fwd", fwd), ("bn_bwd_reduce_pooled", red),
+                         ("bn_bwd_dx_pooled", dxp)):
+            for _ in range(3):
+                fn()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(10):
+                fn()
+            e1.record()
+            torch.cuda.synchronize()
+            print(f"{name:22s} {(b, h, w, c)}: {e0.elapsed_time(e1) * 100:7.1f} us")
     print("ok")
 
 
