@@ -375,6 +375,13 @@ class _EagerCtx(LowerCtx):
     def persistent(self, nbytes: int) -> int:
         return self._alloc(nbytes)
 
+    def prep(self, key, nbytes: int, instrs, src_range) -> int:
+        """Eager: the preparation runs right away on the current stream."""
+        ptr = self._alloc(nbytes)
+        dict.__setitem__(self.memo, key, ptr)
+        run_instrs(instrs(ptr), _current_stream())
+        return ptr
+
 
 _CTX: List[LowerCtx] = []
 

@@ -598,3 +598,26 @@ def test_sum_n_and_concat_kernels(cuda):
     torch.cuda.synchronize()
     assert torch.equal(cat, torch.cat(ins, dim=1))
     assert torch.equal(c16, cat.to(torch.bfloat16))
+
+
+@pytest.mark.parametrize("case", [(2, 15, 15, 3, 8, (7, 7), (2, 2), (3, 3)),
+                                  (2, 9, 7, 8, 16, (3, 3), (1, 1), (1, 1))])
+def test_conv_eager_forward(cuda, engine, case):
+    """Plugin-style eager call of the Convolution operator (no executor):
+    its preparation work (weight casts, the stem's column matrix) runs
+    right away on the current stream."""
+    torch = cuda
+    from paper_1512_01274_b200 import ops
+    b, h, wd, c, f, k, s, p = case
+    x, wt, bias = _conv_case(torch, case, 3 + sum(case[:5]))
+    xd, wd_, bd = (t.float().cuda() for t in (x, wt, bias))
+    ho, wo = (h + 2 * p[0] - k[0]) // s[0] + 1, (wd + 2 * p[1] - k[1]) // s[1] + 1
+    y = torch.full((b, ho, wo, f), float("nan"), device="cuda")
+    ops.get_op("Convolution").forward([xd, wd_, bd], y, {"kernel": k, "num_filter": f,
+                                                         "stride": s, "pad": p})
+    torch.cuda.synchronize()
+    r16 = lambda t: t.float().to(torch.bfloat16).double()  # noqa: E731
+    ref = oc.conv2d_nhwc(r16(x), r16(wt), bias, s, p)
+    kk = k[0] * k[1] * c
+    torch.testing.assert_close(y.double().cpu(), ref, rtol=1e-4,
+                               atol=1e-4 * max(1.0, (kk / 64) ** 0.5) * 8)
