@@ -1810,7 +1810,7 @@ extern "C" int mgx_pool_forward(const float* x, float* y, const int64_t* geom, i
     __nv_bfloat16* h16 = static_cast<__nv_bfloat16*>(y16);
     const int sq = pool_square(g) * 2 + type;
 #define MGX_POOL_FWD(K_, S_, T_) \
-  mgx::conv::pool_fwd_vec_kernel<K_, S_, T_><<<grid, 256, 0, st>>>(x, y, arg, g, h16)
+  mgx::conv::pool_fwd_vec_kernel<K_, S_, T_, false, (K_ > 0 ? 4 : 1)><<<grid, 256, 0, st>>>(x, y, arg, g, h16)
     switch (sq) {
       case 62: MGX_POOL_FWD(3, 1, 0); break;
       case 63: MGX_POOL_FWD(3, 1, 1); break;
