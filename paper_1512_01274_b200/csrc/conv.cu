@@ -1500,14 +1500,27 @@ __global__ void concat_kernel(CatSrcs in, float* __restrict__ out, int64_t rows,
   }
   const int cc = col - base, ck = in.c[k];
   const float* src = in.p[k];
-  for (int64_t r = ri.r; r < rows; r += ri.rstep) {
-    const float4 v = __ldg(reinterpret_cast<const float4*>(src + r * ck + cc));
-    *reinterpret_cast<float4*>(out + r * ctot + col) = v;
-    if (out16) {
-      uint2 h;
-      h.x = pack_bf16(v.x, v.y);
-      h.y = pack_bf16(v.z, v.w);
-      *reinterpret_cast<uint2*>(out16 + r * ctot + col) = h;
+  // four rows' loads in flight per thread before their stores (a pure copy:
+  // the per-row loop otherwise keeps one 16-byte load outstanding)
+  constexpr int U = 4;
+  for (int64_t r0 = ri.r; r0 < rows; r0 += int64_t(U) * ri.rstep) {
+    float4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t r = r0 + int64_t(u) * ri.rstep;
+      if (r < rows) v[u] = __ldg(reinterpret_cast<const float4*>(src + r * ck + cc));
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t r = r0 + int64_t(u) * ri.rstep;
+      if (r >= rows) break;
+      *reinterpret_cast<float4*>(out + r * ctot + col) = v[u];
+      if (out16) {
+        uint2 h;
+        h.x = pack_bf16(v[u].x, v[u].y);
+        h.y = pack_bf16(v[u].z, v[u].w);
+        *reinterpret_cast<uint2*>(out16 + r * ctot + col) = h;
+      }
     }
   }
 }
