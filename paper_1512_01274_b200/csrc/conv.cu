@@ -1468,13 +1468,22 @@ struct SumSrcs {
 __global__ void sum_n_kernel(SumSrcs src, float* __restrict__ out, int64_t n4) {
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += stride) {
-    float4 a = __ldg(reinterpret_cast<const float4*>(src.p[0]) + i);
-    for (int k = 1; k < src.n; ++k) {
-      const float4 b = __ldg(reinterpret_cast<const float4*>(src.p[k]) + i);
-      a.x = fadd(a.x, b.x);
-      a.y = fadd(a.y, b.y);
-      a.z = fadd(a.z, b.z);
-      a.w = fadd(a.w, b.w);
+    // every source's load issued before the first add (a runtime-count loop
+    // kept one 16-byte load outstanding); the sum stays the left fold
+    // ((p0 + p1) + p2) + ...
+    float4 b[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k)
+      if (k < src.n) b[k] = __ldg(reinterpret_cast<const float4*>(src.p[k]) + i);
+    float4 a = b[0];
+#pragma unroll
+    for (int k = 1; k < 6; ++k) {
+      if (k < src.n) {
+        a.x = fadd(a.x, b[k].x);
+        a.y = fadd(a.y, b[k].y);
+        a.z = fadd(a.z, b[k].z);
+        a.w = fadd(a.w, b[k].w);
+      }
     }
     reinterpret_cast<float4*>(out)[i] = a;
   }
