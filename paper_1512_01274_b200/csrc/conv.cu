@@ -2109,7 +2109,7 @@ extern "C" int mgx_concat(const float* const* srcs, const int64_t* channels, int
   }
   MGX_REQUIRE(mgx::aligned16(out) && (!out16 || mgx::aligned16(out16)), "mgx_concat: unaligned output");
   if (rows == 0) return MGX_OK;
-  mgx::conv::concat_kernel<<<mgx::rows_grid(rows, ctot / 4), mgx::rows_block(ctot / 4), 0,
+  mgx::conv::concat_kernel<<<mgx::rows_grid(rows, ctot / 4, 4), mgx::rows_block(ctot / 4), 0,
                              mgx::as_stream(stream)>>>(in, out, rows, ctot,
                                                        static_cast<__nv_bfloat16*>(out16));
   MGX_LAUNCHED();
