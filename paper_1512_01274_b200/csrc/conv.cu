@@ -1544,14 +1544,25 @@ __global__ void chan_copy_kernel(const float* __restrict__ src, int64_t lds, int
     const RowsIdx ri(static_cast<int>(cols / 4));
     if (!ri.active) return;
     const int64_t c = int64_t(ri.v) * 4;
-    for (int64_t r = ri.r; r < rows; r += ri.rstep) {
-      const float4 v = __ldg(reinterpret_cast<const float4*>(src + r * lds + soff + c));
-      *reinterpret_cast<float4*>(dst + r * ldd + doff + c) = v;
-      if (dst16) {
-        uint2 h;
-        h.x = pack_bf16(v.x, v.y);
-        h.y = pack_bf16(v.z, v.w);
-        *reinterpret_cast<uint2*>(dst16 + r * ldd + doff + c) = h;
+    constexpr int U = 4;  // rows' loads in flight per thread (as concat_kernel)
+    for (int64_t r0 = ri.r; r0 < rows; r0 += int64_t(U) * ri.rstep) {
+      float4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t r = r0 + int64_t(u) * ri.rstep;
+        if (r < rows) v[u] = __ldg(reinterpret_cast<const float4*>(src + r * lds + soff + c));
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t r = r0 + int64_t(u) * ri.rstep;
+        if (r >= rows) break;
+        *reinterpret_cast<float4*>(dst + r * ldd + doff + c) = v[u];
+        if (dst16) {
+          uint2 h;
+          h.x = pack_bf16(v[u].x, v[u].y);
+          h.y = pack_bf16(v[u].z, v[u].w);
+          *reinterpret_cast<uint2*>(dst16 + r * ldd + doff + c) = h;
+        }
       }
     }
   } else {
@@ -2034,7 +2045,7 @@ extern "C" int mgx_chan_copy(const float* src, int64_t lds, int64_t soff, float*
               "mgx_chan_copy: a bf16 copy needs 4-aligned columns");
   if (rows == 0 || cols == 0) return MGX_OK;
   if (((cols | lds | soff | ldd | doff) & 3) == 0)
-    mgx::conv::chan_copy_kernel<<<mgx::rows_grid(rows, cols / 4),
+    mgx::conv::chan_copy_kernel<<<mgx::rows_grid(rows, cols / 4, 4),
                                   mgx::rows_block(cols / 4), 0,
                                   mgx::as_stream(stream)>>>(src, lds, soff, dst, ldd, doff, rows, cols,
                                                             static_cast<__nv_bfloat16*>(dst16));
