@@ -1511,7 +1511,7 @@ __global__ void concat_kernel(CatSrcs in, float* __restrict__ out, int64_t rows,
   const float* src = in.p[k];
   // four rows' loads in flight per thread before their stores (a pure copy:
   // the per-row loop otherwise keeps one 16-byte load outstanding)
-  constexpr int U = 4;
+  constexpr int U = 8;
   for (int64_t r0 = ri.r; r0 < rows; r0 += int64_t(U) * ri.rstep) {
     float4 v[U];
 #pragma unroll
@@ -2120,7 +2120,7 @@ extern "C" int mgx_concat(const float* const* srcs, const int64_t* channels, int
   }
   MGX_REQUIRE(mgx::aligned16(out) && (!out16 || mgx::aligned16(out16)), "mgx_concat: unaligned output");
   if (rows == 0) return MGX_OK;
-  mgx::conv::concat_kernel<<<mgx::rows_grid(rows, ctot / 4, 4), mgx::rows_block(ctot / 4), 0,
+  mgx::conv::concat_kernel<<<mgx::rows_grid(rows, ctot / 4, 8), mgx::rows_block(ctot / 4), 0,
                              mgx::as_stream(stream)>>>(in, out, rows, ctot,
                                                        static_cast<__nv_bfloat16*>(out16));
   MGX_LAUNCHED();
