@@ -316,6 +316,42 @@ int mgx_plan_memory(int32_t n, const uint8_t* is_var, const int64_t* nbytes,
  * (the order planner.py:298 frees inputs in); exposed for testing. */
 int mgx_py_set_order(const int64_t* keys, int32_t n, int64_t* out, int32_t* n_out);
 
+/* ------------------------------------------------------------ graph builder
+ * Reverse-mode gradient structure (replaces symbol.build_gradient,
+ * symbol.py:227-298) over the flat form of a forward graph in topo order.
+ *   in_ptr/in_idx   CSR of each node's input source indices; the (node, slot)
+ *                   pair p = in_ptr[i] + k also indexes role_ptr
+ *   role_ptr/role_code  per (node, slot): the values the slot's Backward
+ *                   reads: MGX_ROLE_OG, MGX_ROLE_OUT or an input position j
+ *   seed_node       nodes seeded by a head-gradient variable (endpoint n + s)
+ *   wrt_node        the requested argument nodes
+ * Records are emitted in node-creation order (the host names them from its
+ * counters): kind MGX_GREC_ADD (a, b = endpoints), MGX_GREC_BACKWARD (a =
+ * node, b = slot, inputs in rec_in_ptr/rec_in_idx), MGX_GREC_ZEROS (a = var).
+ * Endpoint codes: < n original node, < n + nseed head variable, else record
+ * (code - n - nseed); -1 = none (a loss head's output gradient).  wrt_out[j]
+ * is the endpoint of argument j's gradient.  A node that needs a gradient but
+ * has none sets *bad_node and returns MGX_BAD_ARGUMENT. */
+#define MGX_ROLE_OG (-1)
+#define MGX_ROLE_OUT (-2)
+#define MGX_GREC_ADD 0
+#define MGX_GREC_BACKWARD 1
+#define MGX_GREC_ZEROS 2
+int mgx_grad_build(int32_t n, const uint8_t* is_var, const uint8_t* is_loss,
+                   const uint8_t* differentiable, const int32_t* in_ptr, const int32_t* in_idx,
+                   int32_t nseed, const int32_t* seed_node, const int32_t* role_ptr,
+                   const int32_t* role_code, int32_t nwrt, const int32_t* wrt_node, int32_t cap,
+                   int32_t in_cap, int32_t* rec_kind, int64_t* rec_a, int64_t* rec_b,
+                   int32_t* rec_in_ptr, int64_t* rec_in_idx, int64_t* wrt_out, int32_t* n_rec,
+                   int32_t* bad_node);
+/* Launch order of a bound graph (executor.py:143-185): min-heap over
+ * (phase, topo index) on the graph's operator edges plus the planner's extra
+ * edges (pairs).  Writes every operator node once; non-acyclic input
+ * returns MGX_BAD_ARGUMENT. */
+int mgx_push_order(int32_t n, const uint8_t* is_var, const int32_t* phase, const int32_t* in_ptr,
+                   const int32_t* in_idx, int32_t nextra, const int32_t* extra, int32_t* order,
+                   int32_t* n_order);
+
 /* ------------------------------------------------------ executor program
  * The bound graph's push lists (executor.py:143-185) compiled into a native
  * instruction list; forward()/backward() (executor.py:198-215) replay a
@@ -400,22 +436,9 @@ typedef struct mgx_instr {
 int mgx_instr_run(const mgx_instr* instrs, int32_t count, uintptr_t stream);
 int mgx_prog_create(const mgx_instr* instrs, int32_t count, uint64_t* out);
 /* Launch instructions [begin, end) on stream.  mode 0: one kernel per
- * instruction; 1: those kernels captured once into a CUDA graph and
- * replayed; 2: ONE cooperative program kernel that runs the range as
- * dependency levels separated by grid barriers; 3: mode 2 inside a graph. */
+ * instruction; 1: those kernels captured once into a CUDA graph (with the
+ * multi-lane schedule's side streams) and replayed. */
 int mgx_prog_run(uint64_t prog, int32_t begin, int32_t end, uintptr_t stream, int32_t mode);
-/* Dependency levels the program kernel uses for [begin, end): level count,
- * grid size, and (optional, capacity end-begin) the level of each instruction. */
-int mgx_prog_levels(uint64_t prog, int32_t begin, int32_t end, int32_t* nlevels,
-                    int32_t* grid, int32_t* level_of);
-/* Non-zero if a program kernel's grid barrier timed out since the last
- * call (its blocks could not all be resident); clears the flag. */
-int mgx_prog_error(uint32_t* out);
-/* Diagnostics: one instrumented program-kernel launch of [begin, end);
- * ns_out[l] = ns from the first block's start until the last block finished
- * level l (capacity = level count). */
-int mgx_prog_time_levels(uint64_t prog, int32_t begin, int32_t end, uintptr_t stream,
-                         double* ns_out);
 /* Per-instruction device time of one eager run of [begin,end) (profiling). */
 int mgx_prog_profile(uint64_t prog, int32_t begin, int32_t end, uintptr_t stream, float* ms_out);
 /* Multi-lane schedule (the dependency engine of engine.py:94-196 as CUDA

@@ -106,3 +106,129 @@ def plan(is_var: Sequence[bool], nbytes: Sequence[int], dedicated: Sequence[bool
                 free.setdefault(nbytes[u], []).append((slot_of[u], u))
     total = sum(b for s, b in slot_bytes.items() if s not in ded_slots)
     return slot_of, slot_bytes, ded_slots, sorted(edges), total
+
+
+# ------------------------------------------------------------ plan checker
+#
+# Restates the reference's plan replay checker (planner.py:378-474): a plan
+# is valid if, for every topological order of the operator nodes under the
+# graph edges plus the plan's extra edges, no internal slot is overwritten
+# while the value in it still has consumers to run.  Small graphs are checked
+# over all orders (capped), larger ones over random orders.
+
+def _op_successors(fg, extra_edges):
+    ops_ = [i for i in range(fg.n) if not fg.is_var[i]]
+    is_op = set(ops_)
+    succ = {i: [] for i in ops_}
+    indeg = {i: 0 for i in ops_}
+    edges = [(u, v) for v in ops_ for u in fg.inputs[v] if u in is_op]
+    edges += [(a, b) for a, b in extra_edges if a in is_op and b in is_op]
+    for a, b in edges:
+        succ[a].append(b)
+        indeg[b] += 1
+    return ops_, succ, indeg
+
+
+def _kahn_ok(ops_, succ, indeg) -> bool:
+    left = dict(indeg)
+    ready = [i for i in ops_ if left[i] == 0]
+    count = 0
+    while ready:
+        x = ready.pop()
+        count += 1
+        for y in succ[x]:
+            left[y] -= 1
+            if left[y] == 0:
+                ready.append(y)
+    return count == len(ops_)
+
+
+def _all_orders(ops_, succ, indeg, cap):
+    """Every topological order (lexicographic over ready sets), at most cap."""
+    left = dict(indeg)
+    order: List[int] = []
+    produced = [0]
+
+    def rec(ready):
+        if produced[0] >= cap:
+            return
+        if len(order) == len(ops_):
+            produced[0] += 1
+            yield list(order)
+            return
+        for r in sorted(ready):
+            freed = []
+            for c in succ[r]:
+                left[c] -= 1
+                if left[c] == 0:
+                    freed.append(c)
+            order.append(r)
+            yield from rec([x for x in ready if x != r] + freed)
+            order.pop()
+            for c in succ[r]:
+                left[c] += 1
+
+    yield from rec([i for i in ops_ if left[i] == 0])
+
+
+def _random_orders(ops_, succ, indeg, samples, seed):
+    import random
+    rng = random.Random(seed)
+    for _ in range(samples):
+        left = dict(indeg)
+        ready = [i for i in ops_ if left[i] == 0]
+        order = []
+        while ready:
+            x = ready.pop(rng.randrange(len(ready)))
+            order.append(x)
+            for y in succ[x]:
+                left[y] -= 1
+                if left[y] == 0:
+                    ready.append(y)
+        yield order
+
+
+def _replay(fg, slot_of, order):
+    owner: Dict[int, List[int]] = {}   # slot -> [node holding it, consumers left]
+    for v in order:
+        for u in fg.inputs[v]:
+            if fg.dedicated[u]:
+                continue
+            held = owner.get(slot_of[u])
+            if held is None or held[0] != u:
+                who = fg.names[held[0]] if held else "<gone>"
+                return (f"value of {fg.names[u]} overwritten by {who} before its consumer "
+                        f"{fg.names[v]} ran")
+            held[1] -= 1
+        if fg.dedicated[v]:
+            continue
+        held = owner.get(slot_of[v])
+        if held is not None and held[0] != v and held[1] > 0:
+            return f"slot collision: {fg.names[v]} overwrites live value of {fg.names[held[0]]}"
+        owner[slot_of[v]] = [v, len(fg.consumers[v])]
+    return None
+
+
+def validate_plan(g, plan, given_shapes, etype="float32", outputs=None, exhaustive_nodes=10,
+                  samples=10000, order_cap=300000, seed=0) -> List[str]:
+    """[] when ``plan`` is safe for every admissible execution order, else
+    the first violation found."""
+    from paper_1512_01274_b200.planner import FlatGraph
+    fg = FlatGraph.of(g, given_shapes, etype, outputs)
+    ops_, succ, indeg = _op_successors(fg, plan.extra_dep_edges)
+    if not _kahn_ok(ops_, succ, indeg):
+        return ["cycle in graph plus extra_dep_edges"]
+    sources = []
+    if len(ops_) <= exhaustive_nodes:
+        sources.append(_all_orders(ops_, succ, indeg, order_cap))
+    sources.append(_random_orders(ops_, succ, indeg, samples, seed))
+    for i, orders in enumerate(sources):
+        seen = 0
+        for order in orders:
+            seen += 1
+            msg = _replay(fg, plan.slot_of, order)
+            if msg:
+                return [msg]
+        if i == 0 and seen < order_cap:
+            return []  # every order enumerated
+    return []

@@ -32,7 +32,6 @@ def __getattr__(name):
         return importlib.import_module(f".{lazy[name]}", __name__)
     attrs = {
         "plan_memory": ("planner", "plan_memory"), "prune": ("planner", "prune"),
-        "fuse": ("planner", "fuse"), "validate_plan": ("planner", "validate_plan"),
         "Engine": ("engine", "Engine"), "Tensor": ("tensor", "Tensor"),
         "Executor": ("executor", "Executor"), "bind": ("executor", "bind"),
         "KVStore": ("kvstore", "KVStore"), "SGDConfig": ("optim", "SGDConfig"),

@@ -126,18 +126,19 @@ _SIGNATURES = {
                          ctypes.POINTER(c_i32), ctypes.POINTER(c_i64),
                          ctypes.POINTER(c_i64)], ctypes.c_int),
     "mgx_py_set_order": ([c_vp, c_i32, c_vp, ctypes.POINTER(c_i32)], ctypes.c_int),
+    "mgx_grad_build": ([c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_vp, c_i32, c_vp,
+                        c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, ctypes.POINTER(c_i32),
+                        ctypes.POINTER(c_i32)], ctypes.c_int),
+    "mgx_push_order": ([c_i32, c_vp, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, ctypes.POINTER(c_i32)],
+                       ctypes.c_int),
     "mgx_instr_run": ([ctypes.POINTER(Instr), c_i32, c_uptr], ctypes.c_int),
     "mgx_prog_create": ([ctypes.POINTER(Instr), c_i32, ctypes.POINTER(c_u64)], ctypes.c_int),
     "mgx_prog_run": ([c_u64, c_i32, c_i32, c_uptr, c_i32], ctypes.c_int),
-    "mgx_prog_levels": ([c_u64, c_i32, c_i32, ctypes.POINTER(c_i32), ctypes.POINTER(c_i32),
-                         c_vp], ctypes.c_int),
     "mgx_prog_profile": ([c_u64, c_i32, c_i32, c_uptr, ctypes.POINTER(c_f32)], ctypes.c_int),
     "mgx_prog_destroy": ([c_u64], ctypes.c_int),
     "mgx_prog_set_schedule": ([c_u64, c_i32, c_vp, c_vp, c_vp], ctypes.c_int),
     "mgx_prog_kernel_count": ([c_u64, c_i32, c_i32, c_uptr, ctypes.POINTER(c_i64)], ctypes.c_int),
     "mgx_kv_round": ([ctypes.POINTER(KvRoundArgs), c_uptr], ctypes.c_int),
-    "mgx_prog_error": ([ctypes.POINTER(c_u32)], ctypes.c_int),
-    "mgx_prog_time_levels": ([c_u64, c_i32, c_i32, c_uptr, c_vp], ctypes.c_int),
     "mgx_gemm_bf16_tc_ex": ([c_vp, c_i64, ctypes.c_int, c_vp, c_i64, ctypes.c_int, c_vp, c_vp,
                              c_i64, c_i64, c_i64, c_i64, ctypes.c_int, ctypes.c_int, c_vp, c_vp,
                              c_uptr], ctypes.c_int),
@@ -224,6 +225,12 @@ def check(status: int, what: str = "") -> None:
     if status == BAD_ARGUMENT:
         raise ArgumentError(f"{where}{msg}")
     raise NativeError(f"{where}status {status}: {msg}")
+
+
+def np_ptr(a) -> ctypes.c_void_p:
+    """Host pointer of a contiguous numpy array (index arrays for the native
+    graph builder and planner)."""
+    return a.ctypes.data_as(ctypes.c_void_p)
 
 
 def call(name: str, *args) -> None:

@@ -19,7 +19,6 @@
 #include <vector>
 
 #include "common.cuh"
-#include "fused.cuh"
 
 namespace mgx {
 
@@ -190,8 +189,6 @@ namespace mgx {
 struct Program {
   std::vector<mgx_instr> instrs;
   std::map<std::pair<int32_t, int32_t>, cudaGraphExec_t> graphs;   // mode 1
-  std::map<std::pair<int32_t, int32_t>, cudaGraphExec_t> fgraphs;  // mode 3
-  std::map<std::pair<int32_t, int32_t>, FusedRange> fused;         // modes 2, 3
   std::mutex mu;
   // multi-lane schedule (mgx_prog_set_schedule): lane of every instruction,
   // cross-lane dependencies (CSR), one side stream per extra lane, one
@@ -203,21 +200,6 @@ struct Program {
   std::vector<cudaEvent_t> join;    // per lane: range start / end joins
 };
 
-static int get_fused(Program* p, int32_t begin, int32_t end, FusedRange** out) {
-  auto key = std::make_pair(begin, end);
-  auto it = p->fused.find(key);
-  if (it == p->fused.end()) {
-    FusedRange f;
-    int rc = build_fused(p->instrs.data() + begin, end - begin, &f);
-    if (rc != MGX_OK) {
-      free_fused(f);
-      return rc;
-    }
-    it = p->fused.emplace(key, f).first;
-  }
-  *out = &it->second;
-  return MGX_OK;
-}
 
 static std::mutex g_prog_mu;
 static std::map<uint64_t, Program*> g_progs;
@@ -447,8 +429,8 @@ extern "C" int mgx_prog_create(const mgx_instr* instrs, int32_t count, uint64_t*
 
 extern "C" int mgx_prog_run(uint64_t prog, int32_t begin, int32_t end, uintptr_t stream,
                             int32_t mode) {
-  // mode 0: eager launches; 1: captured CUDA graph of the per-instruction
-  // kernels; 2: one cooperative program kernel; 3: that kernel in a graph
+  // mode 0: eager launches; 1: the range captured once as a CUDA graph
+  // (side lanes forked and joined inside it) and replayed
   mgx::Program* p = mgx::find_prog(prog);
   if (!p) {
     mgx::set_error("mgx_prog_run: unknown program handle %llu", (unsigned long long)prog);
@@ -456,25 +438,17 @@ extern "C" int mgx_prog_run(uint64_t prog, int32_t begin, int32_t end, uintptr_t
   }
   MGX_REQUIRE(0 <= begin && begin <= end && end <= static_cast<int32_t>(p->instrs.size()),
               "mgx_prog_run: bad range [%d, %d)", begin, end);
-  MGX_REQUIRE(mode >= 0 && mode <= 3, "mgx_prog_run: unknown mode %d", mode);
+  MGX_REQUIRE(mode == 0 || mode == 1, "mgx_prog_run: unknown mode %d", mode);
   if (begin == end) return MGX_OK;
   cudaStream_t st = as_stream(stream);
-  if (mode == 0 || (stream == 0 && mode == 1)) return mgx::run_range(p, begin, end, st);
+  if (mode == 0 || stream == 0) return mgx::run_range(p, begin, end, st);
   std::lock_guard<std::mutex> lock(p->mu);
   auto key = std::make_pair(begin, end);
-  if (mode == 2 || (mode == 3 && stream == 0)) {
-    mgx::FusedRange* f = nullptr;
-    MGX_TRY(mgx::get_fused(p, begin, end, &f));
-    return mgx::launch_fused(*f, st);
-  }
-  auto& cache = mode == 1 ? p->graphs : p->fgraphs;
-  auto it = cache.find(key);
-  if (it == cache.end()) {
-    mgx::FusedRange* f = nullptr;
-    if (mode == 3) MGX_TRY(mgx::get_fused(p, begin, end, &f));
+  auto it = p->graphs.find(key);
+  if (it == p->graphs.end()) {
     cudaGraph_t graph;
     MGX_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-    int rc = mode == 1 ? mgx::run_range(p, begin, end, st) : mgx::launch_fused(*f, st);
+    int rc = mgx::run_range(p, begin, end, st);
     cudaError_t ce = cudaStreamEndCapture(st, &graph);
     if (rc != MGX_OK) {
       if (ce == cudaSuccess) cudaGraphDestroy(graph);
@@ -485,53 +459,9 @@ extern "C" int mgx_prog_run(uint64_t prog, int32_t begin, int32_t end, uintptr_t
     cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
     cudaGraphDestroy(graph);
     MGX_CUDA(ie);
-    it = cache.emplace(key, exec).first;
+    it = p->graphs.emplace(key, exec).first;
   }
   MGX_CUDA(cudaGraphLaunch(it->second, st));
-  return MGX_OK;
-}
-
-extern "C" int mgx_prog_time_levels(uint64_t prog, int32_t begin, int32_t end, uintptr_t stream,
-                                    double* ns_out) {
-  mgx::Program* p = mgx::find_prog(prog);
-  if (!p) {
-    mgx::set_error("mgx_prog_time_levels: unknown program handle");
-    return MGX_BAD_HANDLE;
-  }
-  MGX_REQUIRE(ns_out && stream && 0 <= begin && begin <= end &&
-                  end <= static_cast<int32_t>(p->instrs.size()),
-              "mgx_prog_time_levels: bad arguments");
-  std::lock_guard<std::mutex> lock(p->mu);
-  mgx::FusedRange* f = nullptr;
-  MGX_TRY(mgx::get_fused(p, begin, end, &f));
-  return mgx::time_fused(*f, as_stream(stream), ns_out);
-}
-
-extern "C" int mgx_prog_error(uint32_t* out) {
-  MGX_REQUIRE(out, "mgx_prog_error: null out");
-  uint32_t* w = mgx::program_error_word();
-  *out = w ? *reinterpret_cast<volatile uint32_t*>(w) : 0;
-  if (w) *w = 0;
-  return MGX_OK;
-}
-
-extern "C" int mgx_prog_levels(uint64_t prog, int32_t begin, int32_t end, int32_t* nlevels,
-                               int32_t* grid, int32_t* level_of) {
-  mgx::Program* p = mgx::find_prog(prog);
-  if (!p) {
-    mgx::set_error("mgx_prog_levels: unknown program handle");
-    return MGX_BAD_HANDLE;
-  }
-  MGX_REQUIRE(nlevels && grid && 0 <= begin && begin <= end &&
-                  end <= static_cast<int32_t>(p->instrs.size()),
-              "mgx_prog_levels: bad arguments");
-  std::lock_guard<std::mutex> lock(p->mu);
-  mgx::FusedRange* f = nullptr;
-  MGX_TRY(mgx::get_fused(p, begin, end, &f));
-  *nlevels = f->nlevels;
-  *grid = f->grid;
-  if (level_of)
-    for (size_t i = 0; i < f->level_of.size(); ++i) level_of[i] = f->level_of[i];
   return MGX_OK;
 }
 
@@ -586,7 +516,7 @@ extern "C" int mgx_prog_set_schedule(uint64_t prog, int32_t nlanes, const int32_
   MGX_REQUIRE(nlanes >= 1 && nlanes <= 16 && (nlanes == 1 || (lane && dep_ptr)),
               "mgx_prog_set_schedule: bad arguments");
   std::lock_guard<std::mutex> lock(p->mu);
-  MGX_REQUIRE(p->graphs.empty() && p->fgraphs.empty(),
+  MGX_REQUIRE(p->graphs.empty(),
               "mgx_prog_set_schedule: program already captured");
   if (nlanes == 1) {
     p->nlanes = 1;
@@ -664,14 +594,12 @@ extern "C" int mgx_prog_destroy(uint64_t prog) {
     mgx::g_progs.erase(it);
   }
   for (auto& kv : p->graphs) cudaGraphExecDestroy(kv.second);
-  for (auto& kv : p->fgraphs) cudaGraphExecDestroy(kv.second);
   for (auto e : p->ev)
     if (e) cudaEventDestroy(e);
   for (auto e : p->join)
     if (e) cudaEventDestroy(e);
   for (auto st : p->side)
     if (st) cudaStreamDestroy(st);
-  for (auto& kv : p->fused) mgx::free_fused(kv.second);
   delete p;
   return MGX_OK;
 }

@@ -240,6 +240,7 @@ class KVStore:
         self._sgd = None                      # (eta, momentum, wd, scale)
         self._epoch = 0
         self._err = None
+        self._failed = ""
         self._closed = False
         self._grid_cap = None
 
@@ -467,6 +468,9 @@ class KVStore:
             L.call("mgx_host_alloc", 64, ctypes.byref(p))
             ctypes.memset(p.value, 0, 64)
             self._err = p.value
+            # every engine sync point (wait_for / wait_all / to_numpy) raises
+            # once a device barrier has timed out
+            self.engine.add_check(self._check_error)
         if self.distributed:
             self._materialize_distributed(ar, alloc, nbytes)
         else:
@@ -587,6 +591,8 @@ class KVStore:
         return max(1, min(self._grid_cap, want))
 
     def _launch_locked(self, keys: List[int], single_worker: Optional[int] = None) -> None:
+        if self._failed:
+            raise KVStoreError(f"store failed earlier: {self._failed}")
         ar = self._arenas[self._keys[keys[0]].arena]
         updater = self._native
         custom = updater == L.KV_AGG
@@ -718,5 +724,11 @@ class KVStore:
                                k.numel, self.engine.stream_handle)
 
     def _check_error(self) -> None:
+        if self._failed:
+            raise KVStoreError(self._failed)
         if self._err is not None and ctypes.c_uint32.from_address(self._err).value:
-            raise KVStoreError("a peer did not reach the device barrier within 30 s")
+            # the timed-out blocks skipped their reduce and closing barrier:
+            # replicas and barrier epochs are no longer consistent
+            self._failed = ("a peer did not reach the device barrier within the kernel's 30 s "
+                            "limit; replicas may have diverged, the store refuses further rounds")
+            raise KVStoreError(self._failed)

@@ -365,8 +365,13 @@ class _EagerCtx(LowerCtx):
     def _alloc(self, nbytes: int) -> int:
         import torch
         t = torch.empty(self._al(nbytes), dtype=torch.uint8, device=f"cuda:{self.device}")
-        _EagerCtx._keep.append(t)
-        del _EagerCtx._keep[:-256]
+        keep = _EagerCtx._keep
+        if len(keep) >= 512:
+            # the oldest allocations may still be read by queued kernels:
+            # drain the device before handing them back to the allocator
+            torch.cuda.synchronize(self.device)
+            del keep[:-256]
+        keep.append(t)
         return t.data_ptr()
 
     def scratch(self, nbytes: int) -> int:
@@ -823,50 +828,6 @@ register(OperatorDef(
     infer_shape=_scalar_infer, forward=_native_forward(_zeros_lower_fwd),
     backward=_native_backward("ZerosLike"), backward_uses=lambda slot, nin: (("in0",), "in0"),
     lower_forward=_zeros_lower_fwd, lower_backward=_zeros_lower_bwd,
-))
-
-
-# -------------------------------------------------------- FusedElementwise
-# Only produced by planner.fuse (never by bind); steps evaluated as a chain
-# of the same elementwise kernels, so results equal the unfused graph.
-
-FUSABLE = {"ElementwiseAdd", "ElementwiseMul", "ScalarAdd", "ScalarMul"}
-_BIN_CODE = {"ElementwiseAdd": 0, "ElementwiseMul": 2}
-_SCALAR_CODE = {"ScalarAdd": 0, "ScalarMul": 1}
-
-
-def _fused_infer(shapes, attrs):
-    return _same_shape_infer(shapes, attrs)
-
-
-def _fused_lower_fwd(ins, out, attrs):
-    code = []
-    cur = None
-    for step in attrs["steps"]:
-        op = step["op"]
-        if cur is None:
-            if op in _BIN_CODE:
-                a, b = step["args"]
-                code.append(instr(L.OP_EW, [ins[a].ptr, ins[b].ptr, out.ptr],
-                                  [out.size, _BIN_CODE[op]]))
-            else:
-                code.append(instr(L.OP_SCALAR, [ins[step["args"][0]].ptr, out.ptr],
-                                  [out.size, _SCALAR_CODE[op]], [step["scalar"]]))
-            cur = out
-        elif op in _BIN_CODE:
-            code.append(instr(L.OP_EW, [out.ptr, ins[step["other"]].ptr, out.ptr],
-                              [out.size, _BIN_CODE[op]]))
-        else:
-            code.append(instr(L.OP_SCALAR, [out.ptr, out.ptr], [out.size, _SCALAR_CODE[op]],
-                              [step["scalar"]]))
-    return code
-
-
-register(OperatorDef(
-    name="FusedElementwise", prefix="fused", input_names=(),
-    attr_schema={"steps": (list, True)}, infer_shape=_fused_infer,
-    forward=_native_forward(_fused_lower_fwd), backward=None, variadic=True,
-    lower_forward=_fused_lower_fwd,
 ))
 
 

@@ -94,8 +94,8 @@ def test_kv_rounds(kv_golden, machines, workers):
 
 def _flat_view(text, given):
     from paper_1512_01274_b200 import symbol
-    from paper_1512_01274_b200.planner import _View
-    return _View(symbol.load(text), given, "float32")
+    from paper_1512_01274_b200.planner import FlatGraph
+    return FlatGraph.of(symbol.load(text), given, "float32")
 
 
 def test_plan_oracle_matches_reference_plans(plans_golden):

@@ -159,39 +159,3 @@ def test_whole_step_graph_capture_matches_eager(engine):
         assert np.array_equal(outs[0][n], outs[1][n]), n
 
 
-def test_program_kernel_levels_and_bits(engine):
-    """One cooperative program kernel per pass (dependency levels + grid
-    barriers) gives the same bits as one kernel per instruction."""
-    from paper_1512_01274_b200 import symbol
-    from paper_1512_01274_b200 import tensor as tmod
-    from paper_1512_01274_b200.executor import bind
-    from paper_1512_01274_b200.train import init_params, mlp, param_names
-    feats, labels = ostep.cfg1_data(100)
-    results = []
-    for fused_kernel in (True, False):
-        for use_graph in (True, False):
-            symbol.reset_names()
-            g = mlp([128, 64], 10)
-            shapes, _ = symbol.infer_shape(g, {"data": (100, 784), "label": (100,)})
-            p0 = init_params(g, shapes, 0)
-            names = param_names(g)
-            args = {"data": tmod.from_host((100, 784), "float32", feats, engine=engine),
-                    "label": tmod.from_host((100,), "float32", labels, engine=engine)}
-            for n in names:
-                args[n] = tmod.from_host(shapes[n], "float32", p0[n], engine=engine)
-            grads = {n: tmod.zeros(shapes[n], engine=engine) for n in names}
-            ex = bind(g, args, {n: "write" for n in names}, grads, engine=engine,
-                      fused_kernel=fused_kernel, use_graph=use_graph)
-            if fused_kernel and use_graph:
-                nf, _grid, _ = ex.levels("forward")
-                nb, _grid, lv = ex.levels("backward")
-                assert (nf, nb) == (4, 4), (nf, nb, lv)
-            for _ in range(3):
-                ex.forward()
-                ex.backward()
-            engine.wait_all()
-            assert ex.uses_program_kernel == fused_kernel, getattr(ex, "fused_fallback_reason", "")
-            results.append([tmod.to_numpy(ex.outputs[0])] + [tmod.to_numpy(grads[n]) for n in names])
-    for other in results[1:]:
-        for a, b in zip(results[0], other):
-            assert np.array_equal(a, b)
