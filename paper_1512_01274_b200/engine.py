@@ -79,6 +79,7 @@ class Engine:
         self._ids = itertools.count(1)
         self._lock = threading.Lock()
         self._executed = 0
+        self._since_sync = 0
         self._closed = False
         self._checks: List[Callable[[], None]] = []
 
@@ -140,6 +141,7 @@ class Engine:
                     t._poison = exc
         with self._lock:
             self._executed += 1
+            self._since_sync += 1
 
     def push_delete(self, tag: ResourceTag,
                     on_delete: Optional[Callable[[], None]] = None) -> None:
@@ -164,6 +166,8 @@ class Engine:
 
     def synchronize(self) -> None:
         L.call("mgx_stream_sync", self.stream_handle)
+        with self._lock:
+            self._since_sync = 0
 
     def wait_for(self, tag: ResourceTag) -> None:
         """Synchronisation point: all enqueued work done; re-raise the tag's
@@ -194,7 +198,12 @@ class Engine:
 
     @property
     def pending(self) -> int:
-        return 0
+        """Closures pushed since the stream was last seen idle whose device
+        work may still be in flight (0 once the stream has drained)."""
+        with self._lock:
+            if self._since_sync and self.stream.query():
+                self._since_sync = 0
+            return self._since_sync
 
     @property
     def executed(self) -> int:

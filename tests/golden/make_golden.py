@@ -10,6 +10,10 @@ reference OUTPUTS are stored:
   kv_golden.npz     KVStore rounds (SGD and add updaters, W=2/4/8, M=2xW=2)
   plans_golden.json memory plans: config-1 MLP, 8x64 MLP, 200 random DAGs
   train_golden.npz  train_distributed / train_local weights on config-1 data
+  blobs130.rec(+.idx), data_golden.npz
+                    a record file packed by the reference's recordio.pack and
+                    the batches its BatchIterator yields (seeds 0/1, two
+                    epochs, shuffle on/off, affine)
 """
 
 from __future__ import annotations
@@ -215,7 +219,29 @@ def make_train():
     np.savez_compressed(os.path.join(HERE, "train_golden.npz"), **out)
 
 
+def make_data():
+    from minigraph.dataiter import BatchIterator
+    from minigraph.datasets import pack_blobs
+    path = os.path.join(HERE, "blobs130.rec")
+    pack_blobs(path, 130, classes=3, dim=4, seed=0)
+    out = {}
+    for tag, kw in (("s0", dict(seed=0)), ("s1", dict(seed=1)), ("noshuf", dict(shuffle=False)),
+                    ("affine", dict(seed=0, affine=(np.array([1.0, -1.0, 0.5, 0.0], F32),
+                                                    np.array([0.5, 2.0, 1.0, 3.0], F32))))):
+        with BatchIterator(path, 16, prefetch=2, **kw) as it:
+            for epoch in range(2):
+                for b, (f, l) in enumerate(it):
+                    out[f"{tag}_e{epoch}_b{b}_x"] = f
+                    out[f"{tag}_e{epoch}_b{b}_y"] = l
+                it.reset()
+    np.savez_compressed(os.path.join(HERE, "data_golden.npz"), **out)
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["data"]:
+        make_data()
+        sys.exit(0)
+    make_data()
     make_ops()
     make_kv()
     make_plans()
