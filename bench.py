@@ -229,7 +229,7 @@ def cpu_sample(name: str, seconds: float = None, steps: int = None, nworkers: in
     from paper_1512_01274_b200 import symbol
     from paper_1512_01274_b200.train import init_aux, init_params, param_names
     g = build_graph(name)
-    sample = 8 if name == "lenet" else 2
+    sample = CONFIGS[name]["batch"]  # the full per-GPU batch of the config
     given = {"data": (sample,) + CONFIGS[name]["image"], "label": (sample,)}
     shapes, _ = symbol.infer_shape(g, given)
     x, y = synthetic(name, sample, 0)
@@ -237,37 +237,140 @@ def cpu_sample(name: str, seconds: float = None, steps: int = None, nworkers: in
     names = param_names(g)
     done, t0 = 0, time.perf_counter()
     while True:
-        oc.run_graph(g, vals, wrt=names)
+        oc.run_graph(g, vals, wrt=names, dtype="float32")
         done += 1
         el = time.perf_counter() - t0
         if (steps is not None and done >= steps) or (steps is None and el >= seconds and done >= 1):
             return (done * sample / el, done, el, torch.get_num_threads(),
-                    f"{done} forward+backward passes of {sample} images, oracle/convnet.py float64 "
-                    "torch-CPU restatement (the reference has no conv operators)")
+                    f"{done} forward+backward passes of the full {sample}-image batch, "
+                    "oracle/convnet.py restatement in fp32 torch-CPU (the reference has no "
+                    "convolution operators, so no reference CPU number exists for this config)")
+
+
+def host_cpu() -> dict:
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
+
+
+def reference_own(seconds: float = 20.0) -> dict:
+    """The reference's OWN CPU implementation (minigraph from baseline/_ref,
+    installed offline from /root/reference), timed on this host: config 1
+    train_distributed (W=2, batch 100, engine threads 2W+6 as train.py:181)
+    and config 2 KVStore(1, W) push -> pull -> wait rounds with the SGD
+    updater (kvstore.py:190-241), bounded to ~``seconds`` in total."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "minigraph")):
+        return {"unavailable": "baseline/_ref not installed"}
+    sys.path.insert(0, ref)
+    try:
+        import tempfile
+        from minigraph import symbol as rsym
+        from minigraph.kvstore import KVStore as RKV
+        from minigraph.optim import SGDConfig as RCfg, make_sgd_updater as rmk
+        from minigraph.recordio import Example, pack
+        from minigraph import tensor as rt
+        from minigraph.train import mlp as rmlp, train_distributed as rtd
+        from oracle import step as ostep
+        out = {"source": "baseline/_ref (reference minigraph, unmodified)", **host_cpu()}
+        feats, labels = ostep.cfg1_data(2000)
+        with tempfile.TemporaryDirectory() as tmp:
+            path = os.path.join(tmp, "cfg1.rec")
+            pack((Example(int(l), f) for f, l in zip(feats, labels)), path)
+            rsym.reset_names()
+            t0 = time.perf_counter()
+            rtd(rmlp([128, 64], 10), path, RCfg(ETA, MOM, WD), epochs=1, batch=100, machines=1,
+                workers=2)
+            el = time.perf_counter() - t0
+        out["config1"] = {"value": 2000 / el, "unit": "images/s",
+                          "sample": "1 epoch of 2000 synthetic MNIST-shaped images, batch 100, "
+                                    "W=2 (train_distributed incl. its per-epoch setup)"}
+        kv = []
+        budget = time.perf_counter() + seconds
+        for nbytes in (1 << 10, 1 << 14, 1 << 18, 1 << 22, 1 << 24, 1 << 26):
+            n = nbytes // 4
+            for w_ in (2, 4, 8):
+                if time.perf_counter() > budget:
+                    break
+                with RKV(1, w_) as store:
+                    store.init(0, np.zeros(n, np.float32))
+                    store.set_updater(rmk(RCfg(ETA, MOM, WD), scale=w_))
+                    grads = [rt.from_host((n,), "float32", np.ones(n, np.float32))
+                             for _ in range(w_)]
+                    outs = [rt.zeros((n,)) for _ in range(w_)]
+                    rounds = 0
+                    t0 = time.perf_counter()
+                    while rounds < 3 or (time.perf_counter() - t0 < 0.5 and rounds < 50):
+                        for w in range(w_):
+                            store.push(0, grads[w], w)
+                        for w in range(w_):
+                            store.pull(0, outs[w], w)
+                        for o in outs:
+                            o.engine.wait_for(o.tag)
+                        rounds += 1
+                    ms = (time.perf_counter() - t0) * 1e3 / rounds
+                kv.append({"key_bytes": nbytes, "workers": w_, "ms_per_round": ms,
+                           "algbw_GBps": nbytes / (ms * 1e-3) / 1e9})
+        out["kvstore"] = kv
+        return out
+    except Exception as exc:  # noqa: BLE001 - report, never fail the arm
+        return {"unavailable": f"{type(exc).__name__}: {exc}"}
+    finally:
+        sys.path.remove(ref)
 
 
 def run_reference(args, world, rank):
+    """CPU arm.  Headline conv nets: the oracle's fp32 torch-CPU restatement
+    of the same step on the full per-GPU batch (no reference conv ops exist;
+    kind "port").  Config 1 (--config mlp): the reference's own
+    train_distributed from baseline/_ref when installed (kind "reference"),
+    else the bitwise numpy restatement.  Plus the reference's own config-1
+    and KVStore timings (``reference_own``)."""
     if rank != 0:
         return
     n = args.gpus
     name = args.config
-    for _ in range(args.warmup):
-        cpu_sample(name, steps=1, nworkers=n)
-    value, steps, el, cores, sample = cpu_sample(name, steps=args.steps, nworkers=n)
+    kind = "port"
+    if name == "mlp" and os.path.isdir(os.path.join(ROOT, "baseline", "_ref", "minigraph")):
+        own = reference_own(seconds=5.0)
+        value = own.get("config1", {}).get("value")
+        kind = "reference" if value else "port"
+    if kind == "port":
+        for _ in range(args.warmup if name == "mlp" else min(args.warmup, 1)):
+            cpu_sample(name, steps=1, nworkers=n)
+        value, steps, el, cores, sample = cpu_sample(
+            name, steps=args.steps if name == "mlp" else max(1, min(args.steps, 3)), nworkers=n)
+        ms = 1e3 * el / steps
+    else:
+        cores, steps = 2 * 2 + 6, 1
+        sample = own["config1"]["sample"]
+        ms = 1e3 * CONFIGS["mlp"]["batch"] * 2 / value
     cfg = CONFIGS[name]
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": n,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32"
-        if name == "mlp" else "fp64",
-        "data": "synthetic", "config": {"workload": cfg["workload"],
-                                        "global_batch": cfg["batch"] * n,
-                                        "per_gpu_batch": cfg["batch"], "parallelism": f"dp{n}"},
-        "cpu_baseline": {"value": value, "unit": "images/s", "cores": cores, "kind": "port",
-                         "sample": sample},
+        "steps": steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "fp32", "data": "synthetic",
+        "config": {"workload": cfg["workload"] + (
+            " -- CPU arm: fp32 torch-CPU restatement of the same step on the host cores (the "
+            "reference has no conv operators)" if name != "mlp" else ""),
+            "global_batch": cfg["batch"] * n, "per_gpu_batch": cfg["batch"],
+            "parallelism": f"dp{n}", "same_config": name == "mlp",
+            "same_precision": name == "mlp"},
+        "cpu_baseline": {"value": value, "unit": "images/s", "cores": cores, "kind": kind,
+                         "sample": sample, **host_cpu()},
         "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
+    if not args.no_extra:
+        line["reference_own"] = reference_own(seconds=args.cpu_seconds)
     print(json.dumps(line), flush=True)
 
 
@@ -290,7 +393,10 @@ def kernel_family(op: int) -> str:
             L.OP_CHAN_COPY: "concat_copy", L.OP_COLSUM: "colsum", L.OP_ACT_FWD: "act_fwd",
             L.OP_ACT_BWD: "act_bwd", L.OP_GEMM_PW: "gemm_pairwise", L.OP_GEMM_SEQ: "gemm_sequential",
             L.OP_DW_DB: "fc_dw_db", L.OP_SOFTMAX_FWD: "softmax_fwd", L.OP_SOFTMAX_BWD: "softmax_bwd",
-            L.OP_COPY: "copy", L.OP_FILL: "fill", L.OP_EW: "elementwise", L.OP_AXPY: "axpy"})
+            L.OP_COPY: "copy", L.OP_FILL: "fill", L.OP_EW: "elementwise", L.OP_AXPY: "axpy",
+            L.OP_SCALAR: "scalar", L.OP_BN_ACT_POOL: "bn_act_pool (stem fwd)",
+            L.OP_BN_BWD_REDUCE_POOL: "bn_bwd_reduce_pool (stem)",
+            L.OP_BN_BWD_DX_POOL: "bn_bwd_dx_pool (stem)", L.OP_PREP_BATCH: "prep_batch (weight casts)"})
     return KERNEL_OF.get(op, f"op{op}")
 
 
@@ -441,7 +547,9 @@ def run_config(name, args, world, rank, local, eng, steps, warmup, with_e2e=True
 
 
 def kv_launches(kv) -> int:
-    return 1
+    """Kernels the store launched for ONE step's round (counted by the store
+    around the step's flush)."""
+    return kv.launches_per_flush
 
 
 def kv_round_ms(step, kv, eng, steps):
@@ -514,14 +622,14 @@ def kv_sweep(args, eng, world, rank, distributed):
     from paper_1512_01274_b200.optim import SGDConfig, make_sgd_updater
     out = []
     hbm = peaks()[0]
-    for mb in args.kv_mb:
-        n = (mb << 20) // 4
+    for nbytes in args.kv_bytes:
+        n = nbytes // 4
         kv = KVStore(1, world, engine=eng, distributed=distributed)
         kv.init(0, np.zeros(n, np.float32))
         kv.set_updater(make_sgd_updater(SGDConfig(ETA, MOM, WD), scale=world))
         w = kv.local_workers[0]
         gt, wt = kv.grad_tensor(0, w), kv.weight_tensor(0, w)
-        rounds = max(3, min(args.steps, 20))
+        rounds = max(3, min(args.steps, 20)) if n >= (1 << 24) else 50
         for _ in range(3):
             kv.push(0, gt, w)
             kv.pull(0, wt, w)
@@ -610,7 +718,9 @@ def main():
     ap.add_argument("--config", choices=tuple(CONFIGS), default="inception_bn")
     ap.add_argument("--no-extra", action="store_true",
                     help="skip the secondary configurations")
-    ap.add_argument("--kv-mb", type=int, nargs="*", default=[64, 256])
+    ap.add_argument("--kv-bytes", type=int, nargs="*",
+                    default=[1 << e for e in range(10, 31, 2)],
+                    help="config-2 KVStore sweep key sizes (default 1 KB ... 1 GB, x4)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     args = ap.parse_args()
     world, rank, local = dist_env()

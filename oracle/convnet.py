@@ -133,7 +133,7 @@ class _Bf16FC:
 
 
 def run_graph(g, values: Dict[str, np.ndarray], wrt=(), bf16_operands: bool = False,
-              bf16_fc: bool = False
+              bf16_fc: bool = False, dtype: str = "float64"
               ) -> Tuple[Dict[str, np.ndarray], Dict[str, np.ndarray], Dict[str, np.ndarray]]:
     """Forward (and, for a SoftmaxOutput head, backward) of ``g`` in float64.
 
@@ -141,13 +141,16 @@ def run_graph(g, values: Dict[str, np.ndarray], wrt=(), bf16_operands: bool = Fa
     BatchNorm moving statistics by name).  ``bf16_operands`` rounds every
     operand of the Convolution contractions (forward, data and weight
     gradients) to bf16 like the device does; ``bf16_fc`` does the same for
-    FullyConnected (the device's dense="bf16" mode)."""
+    FullyConnected (the device's dense="bf16" mode).  ``dtype="float32"``
+    runs the same restatement in fp32 (bench.py's CPU baseline timing only;
+    parity uses float64)."""
     torch = _torch()
+    tdt = getattr(torch, dtype)
     env = {}
     leaves = {}
     aux_out = {}
     for name, v in values.items():
-        t = torch.tensor(np.asarray(v), dtype=torch.float64)
+        t = torch.tensor(np.asarray(v), dtype=tdt)
         if name in wrt:
             t.requires_grad_(True)
         leaves[name] = t

@@ -20,6 +20,8 @@ forward and the sibling backward nodes through the lowering context memo.
 
 from __future__ import annotations
 
+import os
+
 from math import prod
 from typing import Optional
 
@@ -313,7 +315,8 @@ def _conv_lower_bwd(slot, env, out, attrs):
         code.append(_gemm(dcolt, ldkf, False, wfl, ldkf, False, out.ptr, c, b * h * wd, c, kf,
                           splits=sp, ws=ws))
         return code
-    if s == (2, 2) and p[0] < k[0] and p[1] < k[1] and f % 8 == 0:
+    if (s == (2, 2) and p[0] < k[0] and p[1] < k[1] and f % 8 == 0
+            and os.environ.get("MGX_S2_DX", "col2im") == "mode3"):
         # stride 2: dX = the stride-1 transposed convolution of dY read
         # dilated by 2 (gather mode 3) with the flipped weights -- no column
         # matrix, no col2im

@@ -273,6 +273,83 @@ __global__ void col2im_kernel(const float* __restrict__ dcol, int64_t ldk, float
   }
 }
 
+// The same gather, four channels per thread (C % 4 == 0, ldk % 4 == 0,
+// 16-byte aligned): consecutive threads read consecutive 16-byte chunks of
+// a dcol row and write consecutive chunks of dx (coalesced); the taps of a
+// compile-time kernel/stride are unrolled so every covering window's load
+// is issued before the first add (sums still in ascending tap order).
+template <int KH, int KW, int SH, int SW>
+__global__ void __launch_bounds__(256)
+col2im_vec4_kernel(const float4* __restrict__ dcol, int64_t ldk4, float4* __restrict__ dx,
+                   Geom g) {
+  const int c4n = g.C >> 2;
+  const int kh = KH ? KH : g.kh, kw = KW ? KW : g.kw;
+  const int sh = SH ? SH : g.sh, sw = SW ? SW : g.sw;
+  const int64_t total = int64_t(g.B) * g.H * g.W * c4n;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < total; idx += stride) {
+    const int c4 = static_cast<int>(idx % c4n);
+    const int64_t pix = idx / c4n;
+    const int w = static_cast<int>(pix % g.W);
+    const int64_t bh = pix / g.W;
+    const int h = static_cast<int>(bh % g.H);
+    const int b = static_cast<int>(bh / g.H);
+    constexpr int kMax = (KH ? KH : 1) * (KW ? KW : 1);
+    if (KH && KW) {
+      float4 v[kMax];
+      bool ok[kMax];
+#pragma unroll
+      for (int i = 0; i < KH; ++i) {
+#pragma unroll
+        for (int j = 0; j < KW; ++j) {
+          const int hn = h + g.ph - i, wn = w + g.pw - j;
+          const int oh = hn / SH, ow = wn / SW;
+          const bool valid = hn >= 0 && wn >= 0 && hn - oh * SH == 0 && wn - ow * SW == 0 &&
+                             oh < g.Ho && ow < g.Wo;
+          ok[i * KW + j] = valid;
+          v[i * KW + j] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (valid) {
+            const int64_t m = (int64_t(b) * g.Ho + oh) * g.Wo + ow;
+            v[i * KW + j] = __ldg(dcol + m * ldk4 + (i * KW + j) * c4n + c4);
+          }
+        }
+      }
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int t = 0; t < kMax; ++t) {
+        if (ok[t]) {
+          acc.x = fadd(acc.x, v[t].x);
+          acc.y = fadd(acc.y, v[t].y);
+          acc.z = fadd(acc.z, v[t].z);
+          acc.w = fadd(acc.w, v[t].w);
+        }
+      }
+      dx[idx] = acc;
+    } else {
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int i = 0; i < kh; ++i) {
+        const int hn = h + g.ph - i;
+        if (hn < 0 || hn % sh) continue;
+        const int oh = hn / sh;
+        if (oh >= g.Ho) continue;
+        for (int j = 0; j < kw; ++j) {
+          const int wn = w + g.pw - j;
+          if (wn < 0 || wn % sw) continue;
+          const int ow = wn / sw;
+          if (ow >= g.Wo) continue;
+          const int64_t m = (int64_t(b) * g.Ho + oh) * g.Wo + ow;
+          const float4 t = __ldg(dcol + m * ldk4 + (i * kw + j) * c4n + c4);
+          acc.x = fadd(acc.x, t.x);
+          acc.y = fadd(acc.y, t.y);
+          acc.z = fadd(acc.z, t.z);
+          acc.w = fadd(acc.w, t.w);
+        }
+      }
+      dx[idx] = acc;
+    }
+  }
+}
+
 // wf[c, (i*kw + j)*F + f] (bf16, row stride ld, zero beyond kh*kw*F) =
 // w[f, kh-1-i, kw-1-j, c]: the weight of the transposed convolution that
 // computes a stride-1 data gradient as im2col(dY) . wf^T.
@@ -1676,7 +1753,21 @@ extern "C" int mgx_col2im(const float* dcol, int64_t ldk, float* dx, const int64
   Geom g = mgx::conv::decode(geom);
   MGX_REQUIRE(g.Ho > 0 && g.Wo > 0 && ldk >= int64_t(g.kh) * g.kw * g.C, "mgx_col2im: bad geometry");
   const int64_t n = int64_t(g.B) * g.H * g.W * g.C;
-  mgx::conv::col2im_kernel<<<grid_for(n), 256, 0, mgx::as_stream(stream)>>>(dcol, ldk, dx, g);
+  cudaStream_t st = mgx::as_stream(stream);
+  if (g.C % 4 == 0 && ldk % 4 == 0 && mgx::aligned16(dcol) && mgx::aligned16(dx)) {
+    const auto* d4 = reinterpret_cast<const float4*>(dcol);
+    auto* x4 = reinterpret_cast<float4*>(dx);
+    const unsigned grid = grid_for(n / 4, 256, int64_t(mgx::kNumSMs) * 8);
+    if (g.kh == 3 && g.kw == 3 && g.sh == 2 && g.sw == 2)
+      mgx::conv::col2im_vec4_kernel<3, 3, 2, 2><<<grid, 256, 0, st>>>(d4, ldk / 4, x4, g);
+    else if (g.kh == 3 && g.kw == 3 && g.sh == 1 && g.sw == 1)
+      mgx::conv::col2im_vec4_kernel<3, 3, 1, 1><<<grid, 256, 0, st>>>(d4, ldk / 4, x4, g);
+    else
+      mgx::conv::col2im_vec4_kernel<0, 0, 0, 0><<<grid, 256, 0, st>>>(d4, ldk / 4, x4, g);
+    MGX_LAUNCHED();
+    return MGX_OK;
+  }
+  mgx::conv::col2im_kernel<<<grid_for(n), 256, 0, st>>>(dcol, ldk, dx, g);
   MGX_LAUNCHED();
   return MGX_OK;
 }

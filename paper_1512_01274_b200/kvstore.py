@@ -241,6 +241,8 @@ class KVStore:
         self._epoch = 0
         self._err = None
         self._failed = ""
+        self._launch_count = 0          # kernels launched by rounds so far
+        self.launches_per_flush = 0     # ... by the latest flush
         self._closed = False
         self._grid_cap = None
 
@@ -555,12 +557,14 @@ class KVStore:
         if not self._pending:
             return
         pending, self._pending = self._pending, []
+        before = self._launch_count
         by_arena: Dict[int, List[int]] = {}
         for key in pending:
             by_arena.setdefault(self._keys[key].arena, []).append(key)
         for aid in sorted(by_arena):
             self._launch_locked(by_arena[aid])
         self._stats["flushes"] += 1
+        self.launches_per_flush = self._launch_count - before
         for key in pending:
             self._stats["level1_aggregates"] += self.machines
             self._stats["level2_messages"] += self.machines
@@ -697,6 +701,7 @@ class KVStore:
         # an eventual-mode push reduces one source; the kernel stores into
         # that many replicas, the rest are refreshed by a copy below
         broadcast_rest = nw == 1 and len(weights) > 1
+        self._launch_count += 1 + (len(segs) * (len(weights) - 1) if broadcast_rest else 0)
         self.engine.activate()
         L.call("mgx_kv_round", ctypes.byref(a), self.engine.stream_handle)
         self._stats["launches"] += 1
