@@ -427,6 +427,10 @@ typedef struct mgx_instr {
 #define MGX_OP_BN_BWD_DX_POOL 34 /* ptr0=dy_pool ptr1=x ptr2=stats ptr3=sums        */
                               /* ptr4=gamma ptr5=argmax dims=M,C,relu_beta*,dsum*, */
                               /* ws*,dx16*,geom packed (bf16 dx only)              */
+#define MGX_OP_KV_ROUND 36    /* ptr0=host mgx_kv_round_args (kept alive by the     */
+                              /* caller): one fused reduce+update+broadcast round   */
+                              /* of a KVStore bucket inside the backward program,   */
+                              /* so it overlaps the rest of the backward            */
 #define MGX_OP_GEMM_CONV 27   /* ptr0=src(bf16 NHWC) ptr1=op ptr2=bias ptr3=C      */
                               /* ptr4=workspace ptr5=colstats dims=M,N,K,ldop,ldc, */
                               /* mode|splits<<8, B<<48|H<<32|W<<16|C,              */

@@ -6,8 +6,9 @@ here independently of the product so tests can check it bit-exactly:
 
   * keys are laid out in init order, each padded to a multiple of 64
     elements;
-  * consecutive keys form a bucket until the bucket holds >= bucket_bytes,
-    and a key of >= bucket_bytes starts its own bucket;
+  * walking the keys in push order (last key first), consecutive keys form
+    a bucket until it holds >= bucket_bytes, and a key of >= bucket_bytes
+    starts its own bucket;
   * a bucket of L elements is split among N owners at
     floor((r*L/N) / 32) * 32, the last owner ending at L.
 
@@ -26,18 +27,26 @@ from . import numerics as nm
 
 
 def arena_layout(numels: List[int], bucket_bytes: int):
-    offsets, buckets, owner_bucket = [], [], []
-    cur_start, pos = 0, 0
+    """Offsets in init order; buckets packed from the LAST key backwards
+    (push order) and listed in arena order; bucket index of every key."""
+    offsets = []
+    pos = 0
     for n in numels:
-        starts_new = pos != cur_start and (4 * (pos - cur_start) >= bucket_bytes
-                                           or 4 * n >= bucket_bytes)
-        if starts_new:
-            buckets.append((cur_start, pos))
-            cur_start = pos
         offsets.append(pos)
-        owner_bucket.append(len(buckets))
         pos += ((n + 63) // 64) * 64
-    buckets.append((cur_start, pos))
+    rev = []
+    end, start = pos, pos
+    for n, off in zip(reversed(numels), reversed(offsets)):
+        if end != start and (4 * (end - start) >= bucket_bytes or 4 * n >= bucket_bytes):
+            rev.append((start, end))
+            end = start
+        start = off
+    if end != start or not rev:
+        rev.append((start, end))
+    buckets = list(reversed(rev))
+    owner_bucket = [next(b for b, (lo, hi) in enumerate(buckets) if lo <= off < hi)
+                    if any(lo <= off < hi for lo, hi in buckets) else len(buckets) - 1
+                    for off in offsets]
     return offsets, buckets, owner_bucket
 
 

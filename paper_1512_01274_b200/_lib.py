@@ -34,6 +34,7 @@ OP_WFLIP, OP_GEMM_CONV, OP_SUM_N, OP_CONCAT = 26, 27, 28, 29
 OP_BN_FWD_FUSED, OP_BN_BWD_FUSED = 30, 31
 OP_BN_ACT_POOL, OP_BN_BWD_REDUCE_POOL, OP_BN_BWD_DX_POOL = 32, 33, 34
 OP_PREP_BATCH = 35
+OP_KV_ROUND = 36
 
 KV_ADD, KV_SGD, KV_AGG = 0, 1, 2
 KV_MAX_SEGS = 256

@@ -237,6 +237,8 @@ static int run_instr(const mgx_instr& in, cudaStream_t st) {
     case MGX_OP_SOFTMAX_FWD: return mgx_softmax_forward(p0, p1, d[0], d[1], s);
     case MGX_OP_SOFTMAX_BWD: return mgx_softmax_backward(p0, p1, p2, d[0], d[1], s);
     case MGX_OP_AXPY: return mgx_axpy(in.fattr[0], p0, p1, d[0], s);
+    case MGX_OP_KV_ROUND:
+      return mgx_kv_round(static_cast<const mgx_kv_round_args*>(in.ptr[0]), s);
     case MGX_OP_CAST_BF16:
       return mgx_cast_bf16_2d(p0, d[0], d[1], d[2], in.ptr[1], d[3], d[4], static_cast<int>(d[5]), s);
     case MGX_OP_GEMM_TC:

@@ -16,8 +16,9 @@ every sharding, so the placement rule below is a free choice:
 
 * keys are laid out in init order in a flat arena, each key starting on a
   256-byte boundary and padded to 64 elements (padding stays zero);
-* consecutive keys are grouped into buckets of at least ``bucket_bytes``
-  (4 MB default; a key of that size or more is a bucket of its own);
+* consecutive keys are grouped, in push order (the reverse of init order),
+  into buckets of at least ``bucket_bytes`` (4 MB default; a key of that
+  size or more is a bucket of its own);
 * each bucket range of L elements is split into ``M*W`` contiguous owner
   shards: owner r gets [floor32(r*L/N), floor32((r+1)*L/N)), the last owner
   ending at L (``shard_ranges``); the owner keeps the momentum state for
@@ -80,20 +81,34 @@ def shard_ranges(length: int, owners: int) -> List[Tuple[int, int]]:
 
 def plan_buckets(numels: List[int], bucket_bytes: int = DEFAULT_BUCKET_BYTES
                  ) -> Tuple[List[int], List[Tuple[int, int]], List[int]]:
-    """Arena layout for keys in init order: (key offsets, bucket ranges,
-    bucket of each key).  Offsets/lengths in elements."""
-    offs, key_bucket, buckets = [], [], []
-    pos = 0
-    start = 0
+    """Arena layout for keys in init order: (key offsets, bucket ranges in
+    arena order, bucket of each key).  Offsets/lengths in elements.
+
+    Buckets are packed in PUSH order -- gradient-ready order, the reverse of
+    init order for a feed-forward net: walking the keys from
+    the last, consecutive keys join the open bucket until it holds
+    ``bucket_bytes``; a key of ``bucket_bytes`` or more closes it and starts
+    its own.  Each bucket is still a contiguous arena range, so its round is
+    one launch that can start as soon as its last gradient is produced."""
+    offs, pos = [], 0
     for n in numels:
-        if pos > start and ((pos - start) * 4 >= bucket_bytes or n * 4 >= bucket_bytes):
-            buckets.append((start, pos))
-            start = pos
         offs.append(pos)
-        key_bucket.append(len(buckets))
         pos += padded(n)
-    if pos > start or not buckets:
-        buckets.append((start, pos))
+    spans: List[Tuple[int, int]] = []
+    hi = lo = pos
+    for i in range(len(numels) - 1, -1, -1):
+        if hi > lo and ((hi - lo) * 4 >= bucket_bytes or numels[i] * 4 >= bucket_bytes):
+            spans.append((lo, hi))
+            hi = lo
+        lo = offs[i]
+    if hi > lo or not spans:
+        spans.append((lo, hi))
+    buckets = spans[::-1]
+    key_bucket, b = [], 0
+    for off in offs:
+        while buckets[b][1] <= off and b + 1 < len(buckets):
+            b += 1
+        key_bucket.append(b)
     return offs, buckets, key_bucket
 
 
@@ -241,6 +256,7 @@ class KVStore:
         self._epoch = 0
         self._err = None
         self._failed = ""
+        self._embedded: List = []       # round args placed inside executors
         self._launch_count = 0          # kernels launched by rounds so far
         self.launches_per_flush = 0     # ... by the latest flush
         self._closed = False
@@ -285,8 +301,13 @@ class KVStore:
             elif fn is add_updater:
                 self._native = L.KV_ADD
             else:
+                if self._embedded:
+                    raise KVStoreError("a plugin updater cannot run inside a bound step's "
+                                       "backward (embedded rounds); set it before binding")
                 self._native = L.KV_AGG
             self._updater = fn
+            for a in self._embedded:
+                self._set_updater_fields(a)
 
     def push(self, key: int, value: Tensor, worker: int) -> None:
         """Join this worker's next round for ``key`` (kvstore.py:190-211)."""
@@ -375,7 +396,12 @@ class KVStore:
             for p in ar.owned_local:
                 L.lib().mgx_free(p)
         if self._err is not None:
+            try:
+                self.engine._checks.remove(self._check_error)
+            except ValueError:
+                pass
             L.lib().mgx_host_free(self._err)
+            self._err = None
         self._arenas = []
         self._closed = True
 
@@ -654,6 +680,26 @@ class KVStore:
 
     def _launch_one(self, ar, segs, machines, workers, grads, weights, updater, total,
                     barrier: bool, scatter=None) -> None:
+        a, _keep = self._round_args(ar, segs, machines, workers, grads, weights, updater, total,
+                                    barrier, scatter)
+        nw = machines * workers
+        # an eventual-mode push reduces one source; the kernel stores into
+        # that many replicas, the rest are refreshed by a copy below
+        broadcast_rest = nw == 1 and len(weights) > 1
+        self._launch_count += 1 + (len(segs) * (len(weights) - 1) if broadcast_rest else 0)
+        self.engine.activate()
+        L.call("mgx_kv_round", ctypes.byref(a), self.engine.stream_handle)
+        self._stats["launches"] += 1
+        if broadcast_rest and updater != L.KV_AGG:
+            for off, ln, _ in segs:
+                for w in weights[1:]:
+                    L.call("mgx_copy", weights[0] + 4 * off, w + 4 * off, ln,
+                           self.engine.stream_handle)
+
+    def _round_args(self, ar, segs, machines, workers, grads, weights, updater, total,
+                    barrier: bool, scatter=None):
+        """mgx_kv_round_args for one launch, plus the host arrays it points
+        to (the caller keeps them alive as long as the args are used)."""
         nw = machines * workers
         a = L.KvRoundArgs()
         seg_arr = (L.KvSeg * max(len(segs), 1))()
@@ -670,9 +716,7 @@ class KVStore:
         a.velocity = ar.velocity
         a.agg_out = ar.agg or None
         a.updater = updater
-        if self._sgd is not None:
-            eta, mom, wd, rescale = self._sgd
-            a.rescale, a.neg_eta, a.momentum, a.weight_decay = rescale, -eta, mom, wd
+        self._set_updater_fields(a, updater)
         f_arr = None
         if barrier:
             self._epoch += 1
@@ -698,18 +742,88 @@ class KVStore:
             a.nscatter = len(scatter)
             a.stage = ctypes.cast(st_arr, ctypes.POINTER(ctypes.c_void_p))
             a.stage_slot = ar.stage_slot
-        # an eventual-mode push reduces one source; the kernel stores into
-        # that many replicas, the rest are refreshed by a copy below
-        broadcast_rest = nw == 1 and len(weights) > 1
-        self._launch_count += 1 + (len(segs) * (len(weights) - 1) if broadcast_rest else 0)
-        self.engine.activate()
-        L.call("mgx_kv_round", ctypes.byref(a), self.engine.stream_handle)
-        self._stats["launches"] += 1
-        if broadcast_rest and updater != L.KV_AGG:
-            for off, ln, _ in segs:
-                for w in weights[1:]:
-                    L.call("mgx_copy", weights[0] + 4 * off, w + 4 * off, ln,
-                           self.engine.stream_handle)
+        keep = [seg_arr, g_arr, w_arr, f_arr]
+        if scatter:
+            keep += [sc_arr, own_arr, st_arr]
+        return a, keep
+
+    def _set_updater_fields(self, a, updater: Optional[int] = None) -> None:
+        a.updater = self._native if updater is None else updater
+        if self._sgd is not None:
+            eta, mom, wd, rescale = self._sgd
+            a.rescale, a.neg_eta, a.momentum, a.weight_decay = rescale, -eta, mom, wd
+
+    # ------------------------------------------- rounds inside the backward
+
+    def embedded_rounds(self, worker: int) -> List[dict]:
+        """Per-bucket round launches for a step in which ``worker`` (this
+        process's only worker) pushes every key, in push order (last bucket
+        first), for the executor to place INSIDE its backward program: each
+        round then starts as soon as its bucket's last gradient is written
+        and overlaps the rest of the backward (the
+        reference pushes after the backward, kvstore.py:116-120,
+        train.py:210-223).  Each dict: ``args`` (mgx_kv_round_args, kept
+        alive with ``keep``), ``reads`` (this worker's gradient ranges of the
+        bucket's keys), ``writes`` (its weight ranges), ``keys``.  Only for
+        the fused native updaters in sequential mode with one local worker;
+        returns [] otherwise (the step then flushes after the backward)."""
+        if (self.mode != "sequential" or self._native == L.KV_AGG
+                or self.local_workers != [worker] or not self._order):
+            return []
+        rounds = []
+        with self._lock:
+            for key in self._order:
+                self._materialize_locked(self._keys[key])
+            for aid, ar in enumerate(self._arenas):
+                by_bucket: Dict[int, List[int]] = {}
+                for kk in ar.keys:
+                    by_bucket.setdefault(self._keys[kk].bucket, []).append(kk)
+                for b in sorted(by_bucket, reverse=True):
+                    keys = by_bucket[b]
+                    rounds += self._bucket_rounds(ar, keys, worker)
+        return rounds
+
+    def _bucket_rounds(self, ar: _Arena, keys: List[int], worker: int) -> List[dict]:
+        owners = self.local_workers if self.distributed else list(range(self.nw))
+        segs = self._segments(ar, keys, owners)
+        total = sum(padded(self._keys[kk].numel) for kk in keys)
+        barrier = self.distributed
+        nchunks = -(-max(len(segs), 1) // L.KV_MAX_SEGS)
+        if barrier:
+            spans = [(self._keys[kk].off, padded(self._keys[kk].numel), self._keys[kk].bucket)
+                     for kk in keys]
+            counts = [len(owner_segments(spans, ar.buckets, self.nw, r)) for r in range(self.nw)]
+            nchunks = launches_for(counts, L.KV_MAX_SEGS)
+        slot = self._slot(worker)
+        reads = [(ar.grads[slot] + 4 * self._keys[kk].off,
+                  ar.grads[slot] + 4 * (self._keys[kk].off + self._keys[kk].numel)) for kk in keys]
+        writes = [(ar.weights[slot] + 4 * self._keys[kk].off,
+                   ar.weights[slot] + 4 * (self._keys[kk].off + self._keys[kk].numel))
+                  for kk in keys]
+        out = []
+        for c in range(nchunks):
+            chunk = segs[c * L.KV_MAX_SEGS: (c + 1) * L.KV_MAX_SEGS]
+            a, keep = self._round_args(ar, chunk, self.machines, self.workers, ar.grads,
+                                       ar.weights, self._native, total, barrier)
+            out.append({"args": a, "keep": keep, "reads": reads, "writes": writes,
+                        "keys": list(keys), "bytes": 4 * total})
+            # set_updater refreshes these in place (the program captures the
+            # struct's values at launch / graph-capture time)
+            self._embedded.append(a)
+        return out
+
+    def note_embedded_round(self, worker: int) -> None:
+        """Book-keeping for a step whose rounds ran inside the executor's
+        backward: every key's round counter advances as if pushed and
+        reduced (pulls and round_barrier stay consistent)."""
+        with self._lock:
+            for key in self._order:
+                self._rounds[(worker, key)] = self._rounds.get((worker, key), 0) + 1
+            self._stats["pushes"] += len(self._order)
+            self._stats["level1_aggregates"] += self.machines * len(self._order)
+            self._stats["level2_messages"] += self.machines * len(self._order)
+            self._stats["level2_updates"] += len(self._order)
+            self._cv.notify_all()
 
     def _run_custom_updater(self, ar: _Arena, keys: List[int]) -> None:
         import torch

@@ -132,12 +132,29 @@ class DataParallelStep:
     Binds one executor per local worker (all workers in a single-process
     store, the rank's own worker in a distributed one) against the store's
     replicas and gradient buffers.
+
+    Push/backward overlap (``overlap=True``): when this
+    process drives exactly one worker (one rank per GPU, or a 1-worker
+    store) and the updater is a fused native one, the store's per-bucket
+    rounds are placed INSIDE the executor's backward program on their own
+    stream: bucket b's fused reduce + update + broadcast starts as soon as
+    its last gradient is written and overlaps the rest of the backward
+    (buckets are packed in push order, KVStore.plan_buckets).  Otherwise --
+    several workers in one process, a plugin updater -- every key is pushed
+    after the backward and reduced in one flush (the reference's order,
+    kvstore.py:116-120, train.py:210-223).  Executors bind lazily, at the
+    first step / capture / ``execs`` access, so ``set_updater`` may come
+    after construction.
     """
 
     def __init__(self, g: SymbolGraph, kv: KVStore, shard_shapes: Dict[str, tuple],
                  params0: Dict[str, np.ndarray], strategy: str = "both",
-                 engine: Optional[Engine] = None, use_graph: bool = True, dense: str = "fp32"):
+                 engine: Optional[Engine] = None, use_graph: bool = True, dense: str = "fp32",
+                 overlap: Optional[bool] = None):
         _check_graph(g)
+        if overlap is None:  # env MGX_OVERLAP=0 turns it off (A/B measurements)
+            import os
+            overlap = os.environ.get("MGX_OVERLAP", "1") != "0"
         self.g, self.kv = g, kv
         # the step pushes every key back to back after the backward: reduce
         # them in one flush (the next pull, capture() or round_barrier)
@@ -145,6 +162,7 @@ class DataParallelStep:
         self.engine = engine or kv.engine
         self.names = param_names(g)
         self.aux = aux_names(g)
+        self._shard_shapes = dict(shard_shapes)
         arg_shapes, _ = infer_shape(g, shard_shapes)
         aux0 = init_aux(g, arg_shapes)
         for i, n in enumerate(self.names):
@@ -152,7 +170,7 @@ class DataParallelStep:
         self.workers = list(kv.local_workers)
         self.args: Dict[int, Dict[str, tmod.Tensor]] = {}
         self.grads: Dict[int, Dict[str, tmod.Tensor]] = {}
-        self.execs = {}
+        self._execs: Dict[int, object] = {}
         for w in self.workers:
             args = {"data": tmod.zeros(shard_shapes["data"], engine=self.engine),
                     "label": tmod.zeros(shard_shapes["label"], engine=self.engine)}
@@ -163,11 +181,32 @@ class DataParallelStep:
             for n in self.aux:
                 args[n] = tmod.from_host(arg_shapes[n], "float32", aux0[n], engine=self.engine)
             self.args[w], self.grads[w] = args, grads
-            self.execs[w] = bind(g, args, {n: "write" for n in self.names}, grads,
-                                 strategy=strategy, engine=self.engine, use_graph=use_graph,
-                                 dense=dense)
-        self.plan_bytes = self.execs[self.workers[0]].plan.total_internal_bytes
+        self._bind_opts = dict(strategy=strategy, use_graph=use_graph, dense=dense)
+        self._overlap = overlap
+        self.embedded = False
         self._graph_exec = None
+
+    def _ensure_bound(self) -> None:
+        if self._execs:
+            return
+        kv = self.kv
+        embed = (self._overlap and len(self.workers) == 1 and kv.mode == "sequential"
+                 and kv._native != L.KV_AGG)
+        for w in self.workers:
+            rounds = kv.embedded_rounds(w) if embed else []
+            self._execs[w] = bind(self.g, self.args[w], {n: "write" for n in self.names},
+                                  self.grads[w], engine=self.engine, rounds=rounds,
+                                  **self._bind_opts)
+            self.embedded = bool(rounds)
+
+    @property
+    def execs(self) -> Dict[int, object]:
+        self._ensure_bound()
+        return self._execs
+
+    @property
+    def plan_bytes(self) -> int:
+        return self.execs[self.workers[0]].plan.total_internal_bytes
 
     # host-staged step (the reference's per-step sequence)
     def load(self, w: int, feats, labels) -> None:
@@ -225,13 +264,21 @@ class DataParallelStep:
                 kv.pull(i, self.args[w][n], w)
         ex.forward()
         ex.backward()
+        self._push(w)
+
+    def _push(self, w: int) -> None:
+        if self.embedded:
+            # the rounds ran inside the backward program
+            self.kv.note_embedded_round(w)
+            return
         for i, n in enumerate(self.names):
-            kv.push(i, self.grads[w][n], w)
+            self.kv.push(i, self.grads[w][n], w)
 
     def step(self, shards: Optional[Dict[int, Tuple[np.ndarray, np.ndarray]]] = None,
              staged: bool = False) -> None:
         """pull -> (load) -> forward -> backward -> push, for every local
         worker.  staged=True takes the batch started by ``stage``."""
+        self._ensure_bound()
         for w in self.workers:
             for i, n in enumerate(self.names):
                 self.kv.pull(i, self.args[w][n], w)
@@ -239,12 +286,12 @@ class DataParallelStep:
                 self.load(w, *shards[w])
             elif staged:
                 self._consume_stage(w)
-            ex = self.execs[w]
+            ex = self._execs[w]
             ex.forward()
             ex.backward()
-            for i, n in enumerate(self.names):
-                self.kv.push(i, self.grads[w][n], w)
+            self._push(w)
         # one fused reduce + update + broadcast round for all the step's keys
+        # (nothing pending when the rounds ran inside the backward)
         with self.kv._lock:
             self.kv._flush_locked()
 
@@ -257,6 +304,7 @@ class DataParallelStep:
         """Capture one device-resident step (all workers) as a CUDA graph.
         Executors run eagerly inside the capture; the store's launches use a
         device-side barrier epoch, so replays stay correct."""
+        self._ensure_bound()
         for ex in self.execs.values():
             ex._use_graph = False
         self.engine.activate()

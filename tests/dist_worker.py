@@ -99,7 +99,9 @@ def check_capture(eng, world, rank, failures):
 def check_convnet(eng, world, rank, failures):
     """LeNet (bf16 tensor-core convs, config 3) trained 3 steps with one
     rank per GPU == the same step with all `world` workers in one process
-    (bitwise: identical kernels, identical tree order in the store)."""
+    (bitwise: identical kernels, identical tree order in the store).  The
+    distributed runs cover the store's rounds inside the backward program
+    (push/backward overlap, eager and captured) and after it."""
     from paper_1512_01274_b200 import nets, symbol
     from paper_1512_01274_b200 import tensor as tmod
     from paper_1512_01274_b200.kvstore import KVStore
@@ -110,24 +112,39 @@ def check_convnet(eng, world, rank, failures):
     ls = rs.randint(0, 10, (3, 16 * world)).astype(F32)
     given = {"data": (16, 28, 28, 1), "label": (16,)}
     results = []
-    for distributed in (True, False):
+    variants = ((True, True, False), (False, True, False), (True, False, False),
+                (True, True, True))
+    for distributed, overlap, captured in variants:
         symbol.reset_names()
         g = nets.lenet(10)
         shapes, _ = symbol.infer_shape(g, given)
-        kv = KVStore(1, world, engine=eng, distributed=distributed)
-        st = DataParallelStep(g, kv, given, init_params(g, shapes, 0), engine=eng, dense="bf16")
+        # small buckets so the step has several rounds inside the backward
+        kv = KVStore(1, world, engine=eng, distributed=distributed, bucket_bytes=1 << 16)
+        st = DataParallelStep(g, kv, given, init_params(g, shapes, 0), engine=eng, dense="bf16",
+                              overlap=overlap)
         kv.set_updater(make_sgd_updater(SGDConfig(0.05, 0.9, 1e-4), scale=world))
         for s in range(3):
-            st.step({w: (xs[s, 16 * w:16 * (w + 1)], ls[s, 16 * w:16 * (w + 1)])
-                     for w in st.workers})
+            shard = {w: (xs[s, 16 * w:16 * (w + 1)], ls[s, 16 * w:16 * (w + 1)])
+                     for w in st.workers}
+            if captured and s > 0:
+                for w in st.workers:
+                    st.load(w, *shard[w])
+                if s == 1:
+                    st.capture()
+                st.replay()
+            else:
+                st.step(shard)
         kv.round_barrier()
+        if distributed and overlap and not st.embedded:
+            failures.append("distributed 1-worker step did not embed its rounds")
         w0 = st.workers[0]
         results.append({n: tmod.to_numpy(st.args[w0][n]) for n in st.names})
         kv.close()
-    for n in results[0]:
-        if not np.array_equal(results[0][n], results[1][n]):
-            failures.append(f"convnet {n}: distributed != single-process "
-                            f"(max diff {np.abs(results[0][n] - results[1][n]).max()})")
+    for v, other in zip(variants[1:], results[1:]):
+        for n in results[0]:
+            if not np.array_equal(results[0][n], other[n]):
+                failures.append(f"convnet {n}: variant {v} != distributed overlapped "
+                                f"(max diff {np.abs(results[0][n] - other[n]).max()})")
 
 
 def main():

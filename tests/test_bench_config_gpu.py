@@ -74,6 +74,7 @@ def _make_step(engine, lanes=None, monkeypatch=None):
     kv = KVStore(1, 1, engine=engine)
     step = DataParallelStep(g, kv, given, p0, engine=engine, dense="bf16")
     kv.set_updater(make_sgd_updater(SGDConfig(ETA, MOM, WD), scale=1))
+    step.execs  # bind now (MGX_LANES is read at bind time)
     if lanes is not None:
         monkeypatch.delenv("MGX_LANES")
     x, y = _synthetic()
