@@ -257,6 +257,11 @@ class KVStore:
         self._err = None
         self._failed = ""
         self._embedded: List = []       # round args placed inside executors
+        # blocks per round when it runs inside the backward (fewer SMs taken
+        # from the overlapped compute; env MGX_KV_OVERLAP_BLOCKS, 0 = all;
+        # 32 measured best at N=2: AlexNet 2.588 -> 2.464 ms, Inception-BN
+        # 5.887 -> 5.794 ms vs every SM, profiles/r02_overlap_sweep_n2.txt)
+        self.overlap_blocks = int(_os.environ.get("MGX_KV_OVERLAP_BLOCKS", "32"))
         self._launch_count = 0          # kernels launched by rounds so far
         self.launches_per_flush = 0     # ... by the latest flush
         self._closed = False
@@ -697,7 +702,7 @@ class KVStore:
                            self.engine.stream_handle)
 
     def _round_args(self, ar, segs, machines, workers, grads, weights, updater, total,
-                    barrier: bool, scatter=None):
+                    barrier: bool, scatter=None, grid_cap: Optional[int] = None):
         """mgx_kv_round_args for one launch, plus the host arrays it points
         to (the caller keeps them alive as long as the args are used)."""
         nw = machines * workers
@@ -726,6 +731,8 @@ class KVStore:
             a.epoch_ctr = ar.epoch_ctr
             a.error_word = self._err
             a.grid = self._grid_locked(total)
+            if grid_cap:
+                a.grid = max(1, min(a.grid, grid_cap))
         else:
             a.flags = None
             a.grid = 0
@@ -804,7 +811,8 @@ class KVStore:
         for c in range(nchunks):
             chunk = segs[c * L.KV_MAX_SEGS: (c + 1) * L.KV_MAX_SEGS]
             a, keep = self._round_args(ar, chunk, self.machines, self.workers, ar.grads,
-                                       ar.weights, self._native, total, barrier)
+                                       ar.weights, self._native, total, barrier,
+                                       grid_cap=self.overlap_blocks)
             out.append({"args": a, "keep": keep, "reads": reads, "writes": writes,
                         "keys": list(keys), "bytes": 4 * total})
             # set_updater refreshes these in place (the program captures the
