@@ -458,6 +458,13 @@ int mgx_prog_set_schedule(uint64_t prog, int32_t nlanes, const int32_t* lane,
 int mgx_prog_kernel_count(uint64_t prog, int32_t begin, int32_t end, uintptr_t stream,
                           int64_t* out);
 int mgx_prog_destroy(uint64_t prog);
+/* Whole-step graphs: capture what this thread enqueues on `stream` between
+ * begin and end (both passes, their lanes, the store's rounds) into one
+ * graph instantiated with per-node priorities; launch / destroy by handle. */
+int mgx_capture_begin(uintptr_t stream);
+int mgx_capture_end(uintptr_t stream, uint64_t* out);
+int mgx_graph_launch(uint64_t graph, uintptr_t stream);
+int mgx_graph_destroy(uint64_t graph);
 
 /* ------------------------------------------------------------- KVStore
  * Device KVStore (kvstore.py:84-409): push -> level-1 tree aggregate over the

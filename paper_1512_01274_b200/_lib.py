@@ -137,6 +137,10 @@ _SIGNATURES = {
     "mgx_prog_run": ([c_u64, c_i32, c_i32, c_uptr, c_i32], ctypes.c_int),
     "mgx_prog_profile": ([c_u64, c_i32, c_i32, c_uptr, ctypes.POINTER(c_f32)], ctypes.c_int),
     "mgx_prog_destroy": ([c_u64], ctypes.c_int),
+    "mgx_capture_begin": ([c_uptr], ctypes.c_int),
+    "mgx_capture_end": ([c_uptr, ctypes.POINTER(c_u64)], ctypes.c_int),
+    "mgx_graph_launch": ([c_u64, c_uptr], ctypes.c_int),
+    "mgx_graph_destroy": ([c_u64], ctypes.c_int),
     "mgx_prog_set_schedule": ([c_u64, c_i32, c_vp, c_vp, c_vp], ctypes.c_int),
     "mgx_prog_kernel_count": ([c_u64, c_i32, c_i32, c_uptr, ctypes.POINTER(c_i64)], ctypes.c_int),
     "mgx_kv_round": ([ctypes.POINTER(KvRoundArgs), c_uptr], ctypes.c_int),

@@ -458,7 +458,8 @@ extern "C" int mgx_prog_run(uint64_t prog, int32_t begin, int32_t end, uintptr_t
     }
     MGX_CUDA(ce);
     cudaGraphExec_t exec;
-    cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+    cudaError_t ie =
+        cudaGraphInstantiateWithFlags(&exec, graph, cudaGraphInstantiateFlagUseNodePriority);
     cudaGraphDestroy(graph);
     MGX_CUDA(ie);
     it = p->graphs.emplace(key, exec).first;
@@ -509,6 +510,8 @@ extern "C" int mgx_prog_profile(uint64_t prog, int32_t begin, int32_t end, uintp
 
 extern "C" int mgx_prog_set_schedule(uint64_t prog, int32_t nlanes, const int32_t* lane,
                                      const int32_t* dep_ptr, const int32_t* dep_idx) {
+  const char* cl = getenv("MGX_CRIT_LANE");
+  const bool crit_lane = !cl || cl[0] != '0';
   mgx::Program* p = mgx::find_prog(prog);
   if (!p) {
     mgx::set_error("mgx_prog_set_schedule: unknown program handle");
@@ -520,6 +523,16 @@ extern "C" int mgx_prog_set_schedule(uint64_t prog, int32_t nlanes, const int32_
   std::lock_guard<std::mutex> lock(p->mu);
   MGX_REQUIRE(p->graphs.empty(),
               "mgx_prog_set_schedule: program already captured");
+  // a re-schedule (profile-guided) replaces the previous lanes' resources
+  for (auto e : p->ev)
+    if (e) cudaEventDestroy(e);
+  for (auto e : p->join)
+    if (e) cudaEventDestroy(e);
+  for (auto st : p->side)
+    if (st) cudaStreamDestroy(st);
+  p->ev.clear();
+  p->join.clear();
+  p->side.clear();
   if (nlanes == 1) {
     p->nlanes = 1;
     return MGX_OK;
@@ -541,8 +554,16 @@ extern "C" int mgx_prog_set_schedule(uint64_t prog, int32_t nlanes, const int32_
   }
   p->side.assign(nlanes, nullptr);
   p->join.assign(nlanes, nullptr);
+  // lane 1 carries the modelled critical path (Executor._schedule): its
+  // stream has the device's greatest priority, so when SMs free up its
+  // kernels are placed before the off-path lanes' (graphs keep the
+  // per-node priority: instantiated with UseNodePriority)
+  int lo_prio = 0, hi_prio = 0;
+  MGX_CUDA(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
   for (int l = 0; l < nlanes; ++l) {
-    if (l > 0) MGX_CUDA(cudaStreamCreateWithFlags(&p->side[l], cudaStreamNonBlocking));
+    if (l > 0)
+      MGX_CUDA(cudaStreamCreateWithPriority(&p->side[l], cudaStreamNonBlocking,
+                                            (l == 1 && crit_lane) ? hi_prio : lo_prio));
     MGX_CUDA(cudaEventCreateWithFlags(&p->join[l], cudaEventDisableTiming));
   }
   p->nlanes = nlanes;
@@ -603,5 +624,64 @@ extern "C" int mgx_prog_destroy(uint64_t prog) {
   for (auto st : p->side)
     if (st) cudaStreamDestroy(st);
   delete p;
+  return MGX_OK;
+}
+
+// ---------------------------------------------------- whole-step graphs
+// Capture everything a thread enqueues on `stream` (a data-parallel step:
+// both passes' lanes and the store's rounds) into one graph, instantiated
+// with per-node priorities (the critical lane's kernels keep theirs).
+
+namespace mgx {
+static std::mutex g_graph_mu;
+static std::map<uint64_t, cudaGraphExec_t> g_graphs;
+static uint64_t g_next_graph = 1;
+}  // namespace mgx
+
+extern "C" int mgx_capture_begin(uintptr_t stream) {
+  MGX_REQUIRE(stream != 0, "mgx_capture_begin: needs a non-default stream");
+  MGX_CUDA(cudaStreamBeginCapture(as_stream(stream), cudaStreamCaptureModeThreadLocal));
+  return MGX_OK;
+}
+
+extern "C" int mgx_capture_end(uintptr_t stream, uint64_t* out) {
+  MGX_REQUIRE(out && stream != 0, "mgx_capture_end: bad arguments");
+  cudaGraph_t graph = nullptr;
+  MGX_CUDA(cudaStreamEndCapture(as_stream(stream), &graph));
+  cudaGraphExec_t exec = nullptr;
+  cudaError_t ie =
+      cudaGraphInstantiateWithFlags(&exec, graph, cudaGraphInstantiateFlagUseNodePriority);
+  cudaGraphDestroy(graph);
+  MGX_CUDA(ie);
+  std::lock_guard<std::mutex> lock(mgx::g_graph_mu);
+  *out = mgx::g_next_graph++;
+  mgx::g_graphs[*out] = exec;
+  return MGX_OK;
+}
+
+extern "C" int mgx_graph_launch(uint64_t graph, uintptr_t stream) {
+  cudaGraphExec_t exec = nullptr;
+  {
+    std::lock_guard<std::mutex> lock(mgx::g_graph_mu);
+    auto it = mgx::g_graphs.find(graph);
+    if (it == mgx::g_graphs.end()) {
+      mgx::set_error("mgx_graph_launch: unknown graph handle");
+      return MGX_BAD_HANDLE;
+    }
+    exec = it->second;
+  }
+  MGX_CUDA(cudaGraphLaunch(exec, as_stream(stream)));
+  return MGX_OK;
+}
+
+extern "C" int mgx_graph_destroy(uint64_t graph) {
+  std::lock_guard<std::mutex> lock(mgx::g_graph_mu);
+  auto it = mgx::g_graphs.find(graph);
+  if (it == mgx::g_graphs.end()) {
+    mgx::set_error("mgx_graph_destroy: unknown graph handle");
+    return MGX_BAD_HANDLE;
+  }
+  cudaGraphExecDestroy(it->second);
+  mgx::g_graphs.erase(it);
   return MGX_OK;
 }

@@ -20,6 +20,7 @@ step (forward, backward, store round) into a single CUDA graph.
 from __future__ import annotations
 
 import ctypes
+import os
 import time
 from dataclasses import dataclass, field
 from typing import Dict, List, Optional, Sequence, Tuple
@@ -198,6 +199,10 @@ class DataParallelStep:
                                   self.grads[w], engine=self.engine, rounds=rounds,
                                   **self._bind_opts)
             self.embedded = bool(rounds)
+            if os.environ.get("MGX_PGO", "1") == "1":
+                # schedule the lanes on measured instruction times
+                self._execs[w].reschedule_from_profile(
+                    keep=[self.args[w][n] for n in self.aux])
 
     @property
     def execs(self) -> Dict[int, object]:
@@ -301,29 +306,43 @@ class DataParallelStep:
     # ---------------------------------------------------- whole-step graph
 
     def capture(self) -> None:
-        """Capture one device-resident step (all workers) as a CUDA graph.
-        Executors run eagerly inside the capture; the store's launches use a
-        device-side barrier epoch, so replays stay correct."""
+        """Capture one device-resident step (all workers) as a CUDA graph,
+        instantiated natively with per-node priorities (the critical lane's
+        kernels keep their stream priority).  Executors run eagerly inside
+        the capture; the store's launches use a device-side barrier epoch,
+        so replays stay correct."""
         self._ensure_bound()
         for ex in self.execs.values():
             ex._use_graph = False
         self.engine.activate()
         self.engine.synchronize()
-        import torch
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=self.engine.stream, capture_error_mode="thread_local"):
+        st = self.engine.stream_handle
+        L.call("mgx_capture_begin", st)
+        try:
             self.step()
             with self.kv._lock:
                 self.kv._flush_locked()
-        self._graph_exec = g
+        finally:
+            h = ctypes.c_uint64()
+            rc = L.lib().mgx_capture_end(st, ctypes.byref(h))
+        L.check(rc, "mgx_capture_end")
+        if self._graph_exec is not None:
+            L.lib().mgx_graph_destroy(self._graph_exec)
+        self._graph_exec = h.value
 
     def replay(self) -> None:
         if self._graph_exec is None:
             raise ArgumentError("capture() first")
-        import torch
-        # CUDAGraph.replay launches on torch's current stream: make it ours
-        with torch.cuda.stream(self.engine.stream):
-            self._graph_exec.replay()
+        self.engine.activate()
+        L.call("mgx_graph_launch", self._graph_exec, self.engine.stream_handle)
+
+    def __del__(self):
+        g = getattr(self, "_graph_exec", None)
+        if g:
+            try:
+                L.lib().mgx_graph_destroy(g)
+            except Exception:  # noqa: BLE001 - interpreter shutdown
+                pass
 
 
 # ----------------------------------------------------------------- drivers

@@ -36,7 +36,33 @@ def main():
     scratch = torch.empty(n, dtype=torch.float32, device=f"cuda:{local}")
     st = eng.stream_handle
 
+    side = [torch.cuda.Stream(device=f"cuda:{local}") for _ in range(2 * world)]
+
+    def run_ce(kind):
+        # copy engines: one cudaMemcpyAsync per peer, each on its own stream
+        # (forked from / joined back into the engine stream)
+        ev0 = torch.cuda.Event()
+        ev0.record(eng.stream)
+        for k in range(1, world):
+            peer = (rank + k) % world
+            for j, what in enumerate(("read", "write")):
+                if kind not in ("ce_" + what, "ce_mixed"):
+                    continue
+                s_ = side[2 * k + j]
+                s_.wait_event(ev0)
+                if what == "read":
+                    L.call("mgx_memcpy_async", scratch.data_ptr() + 4 * k * part,
+                           ar.grads[peer] + 4 * rank * part, 4 * part, s_.cuda_stream)
+                else:
+                    L.call("mgx_memcpy_async", ar.weights[peer] + 4 * rank * part,
+                           scratch.data_ptr() + 4 * k * part, 4 * part, s_.cuda_stream)
+                e = torch.cuda.Event()
+                e.record(s_)
+                eng.stream.wait_event(e)
+
     def run(kind):
+        if kind.startswith("ce_"):
+            return run_ce(kind)
         for k in range(1, world):
             peer = (rank + k) % world
             if kind in ("read", "mixed"):
@@ -47,7 +73,7 @@ def main():
                        ar.weights[peer] + 4 * rank * part, part, st)
 
     out = {"n": world, "key_mb": mb}
-    for kind in ("read", "write", "mixed"):
+    for kind in ("read", "write", "mixed", "ce_read", "ce_write", "ce_mixed"):
         for _ in range(2):
             run(kind)
         torch.cuda.synchronize()
@@ -62,7 +88,9 @@ def main():
         t = torch.tensor([a.elapsed_time(b) / reps], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         # per direction per rank: (N-1)/N*S each way; mixed carries both
-        bytes_dir = (world - 1) * part * 4 * (2 if kind == "mixed" else 1)
+        bytes_dir = (world - 1) * part * 4
+        if kind in ("mixed",):
+            bytes_dir *= 2  # one stream carries both directions' bytes in sequence
         out[kind + "_GBps_per_dir"] = bytes_dir / (float(t.item()) * 1e-3) / 1e9
     dist.barrier()
     kv.close()
