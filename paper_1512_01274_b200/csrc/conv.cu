@@ -1035,13 +1035,24 @@ bn_pool_dx_k3s2_kernel(PoolGrad pg, const float* __restrict__ x, const float* __
         d[wi] = ok ? __ldg(pg.dy + o) : make_float4(0.f, 0.f, 0.f, 0.f);
         am[wi] = ok ? __ldg(pg.arg + o) : make_uchar4(255, 255, 255, 255);
       }
+      // the block's 4 pixels of x, loaded together with the windows' loads
+      float4 xq[4];
+      bool pin[4];
+#pragma unroll
+      for (int pi = 0; pi < 4; ++pi) {
+        const int h = 2 * ba + (pi >> 1), w = 2 * bb + (pi & 1);
+        pin[pi] = h < g.H && w < g.W;
+        const int64_t i = ((int64_t(b) * g.H + h) * g.W + w) * C4 + c4;
+        xq[pi] = pin[pi] ? __ldg(reinterpret_cast<const float4*>(x) + i)
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
 #pragma unroll
       for (int pi = 0; pi < 4; ++pi) {
         const int dh = pi >> 1, dw = pi & 1;
         const int h = 2 * ba + dh, w = 2 * bb + dw;
-        if (h >= g.H || w >= g.W) continue;
+        if (!pin[pi]) continue;
         const int64_t i = ((int64_t(b) * g.H + h) * g.W + w) * C4 + c4;
-        const float4 xv = __ldg(reinterpret_cast<const float4*>(x) + i);
+        const float4 xv = xq[pi];
         const float* px = &xv.x;
         float og[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -1389,6 +1400,87 @@ pool_fwd_vec_kernel(const float* __restrict__ x, float* __restrict__ y,
       h.x = pack_bf16(o.x, o.y);
       h.y = pack_bf16(o.z, o.w);
       reinterpret_cast<uint2*>(y16)[idx] = h;
+    }
+  }
+}
+
+// The stem's BatchNorm + ReLU + 3x3 / stride-2 / pad-0 max pooling, two
+// horizontally adjacent outputs per thread: their windows share a column,
+// so 15 loads and 15 BatchNorm transforms serve 18 taps (vs 18 of each),
+// 32-bit indexing throughout.  Same arithmetic and tap order as
+// pool_fwd_vec_kernel<3, 2, 0, true> (bitwise).
+__global__ void __launch_bounds__(256, 2)
+bn_relu_maxpool3s2_kernel(const float4* __restrict__ x, float4* __restrict__ y,
+                          uchar4* __restrict__ arg, Geom g, uint2* __restrict__ y16, BnAct bn) {
+  const int C4 = g.C >> 2;
+  const int wp = (g.Wo + 1) >> 1;  // output pairs per row
+  const int total = g.B * g.Ho * wp * C4;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += gridDim.x * blockDim.x) {
+    const int c4 = idx % C4;
+    const int pp = idx / C4;
+    const int owp = pp % wp;
+    const int bo = pp / wp;
+    const int oh = bo % g.Ho, b = bo / g.Ho;
+    const int hs = oh * 2, ws = owp * 4;
+    const float4 mu4 = __ldg(reinterpret_cast<const float4*>(bn.stats) + c4);
+    const float4 rs4 = __ldg(reinterpret_cast<const float4*>(bn.stats + g.C) + c4);
+    const float4 gm4 = bn.gamma ? __ldg(reinterpret_cast<const float4*>(bn.gamma) + c4)
+                                : make_float4(1.f, 1.f, 1.f, 1.f);
+    const float4 bt4 = __ldg(reinterpret_cast<const float4*>(bn.beta) + c4);
+    const float4* xb = x + (b * g.H + hs) * g.W * C4 + c4;
+    float4 v[3][5];
+    bool okc[5];
+#pragma unroll
+    for (int j = 0; j < 5; ++j) okc[j] = ws + j < g.W;
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 5; ++j)
+        v[i][j] = okc[j] ? __ldg(xb + (i * g.W + ws + j) * C4) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 5; ++j) {
+        float* pv = &v[i][j].x;
+        const float* pm = &mu4.x;
+        const float* pr = &rs4.x;
+        const float* pg = &gm4.x;
+        const float* pb = &bt4.x;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float t = (pv[q] - pm[q]) * pr[q] * pg[q] + pb[q];
+          pv[q] = bn.act == MGX_ACT_RELU ? relu(t) : act_forward(bn.act, t);
+        }
+      }
+#pragma unroll
+    for (int o = 0; o < 2; ++o) {
+      const int ow = owp * 2 + o;
+      if (ow >= g.Wo) break;
+      float acc[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+      int ai[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          const float* pv = &v[i][2 * o + j].x;
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (pv[q] > acc[q]) {
+              acc[q] = pv[q];
+              ai[q] = i * 3 + j;
+            }
+        }
+      const int oi = ((b * g.Ho + oh) * g.Wo + ow) * C4 + c4;
+      const float4 r = make_float4(acc[0], acc[1], acc[2], acc[3]);
+      if (y) y[oi] = r;
+      arg[oi] = make_uchar4(ai[0], ai[1], ai[2], ai[3]);
+      if (y16) {
+        uint2 h;
+        h.x = pack_bf16(r.x, r.y);
+        h.y = pack_bf16(r.z, r.w);
+        y16[oi] = h;
+      }
     }
   }
 }
@@ -2016,7 +2108,17 @@ extern "C" int mgx_bn_act_pool_fwd(const float* x, const float* stats, const flo
   uint8_t* arg = static_cast<uint8_t*>(argmax);
   __nv_bfloat16* h16 = static_cast<__nv_bfloat16*>(y16);
   // 3 resident CTAs per SM (<= 85 registers): latency-bound gather, +20% over 2
-  if (pool_square(g) == 32)
+  static const bool pair = [] {
+    const char* v = getenv("MGX_STEM_POOL_PAIR");
+    return !(v && *v == '0');
+  }();
+  if (pair && pool_square(g) == 32 && g.ph == 0 && g.pw == 0 &&
+      int64_t(g.B) * g.H * g.W * g.C < (int64_t(1) << 31)) {
+    const unsigned gp = grid_for(int64_t(g.B) * g.Ho * ((g.Wo + 1) / 2) * (g.C / 4));
+    mgx::conv::bn_relu_maxpool3s2_kernel<<<gp, 256, 0, st>>>(
+        reinterpret_cast<const float4*>(x), reinterpret_cast<float4*>(y),
+        reinterpret_cast<uchar4*>(arg), g, reinterpret_cast<uint2*>(h16), bn);
+  } else if (pool_square(g) == 32)
     mgx::conv::pool_fwd_vec_kernel<3, 2, 0, true, 3><<<grid, 256, 0, st>>>(x, y, arg, g, h16, bn);
   else
     mgx::conv::pool_fwd_vec_kernel<0, 0, 0, true><<<grid, 256, 0, st>>>(x, y, arg, g, h16, bn);
@@ -2098,7 +2200,11 @@ extern "C" int mgx_bn_bwd_dx_pooled(const float* dy_pool, const void* argmax, co
   const mgx::conv::ReluMask rm{relu_beta ? gamma : nullptr, relu_beta};
   __nv_bfloat16* h16 = static_cast<__nv_bfloat16*>(dx16);
   double* wsd = static_cast<double*>(ws);
-  if (pk == 32 && pg.g.ph == 0 && pg.g.pw == 0 && dx == nullptr && dx16 != nullptr) {
+  static const bool block_dx = [] {
+    const char* v = getenv("MGX_STEM_DX_BLOCK");
+    return !(v && *v == '0');
+  }();
+  if (block_dx && pk == 32 && pg.g.ph == 0 && pg.g.pw == 0 && dx == nullptr && dx16 != nullptr) {
     // 2x2 pixel blocks: 4 windows cover a block
     const int Hb = (pg.g.H + 1) / 2, Wb = (pg.g.W + 1) / 2;
     const int64_t Mb = int64_t(pg.g.B) * Hb * Wb;
