@@ -228,6 +228,21 @@ constexpr int threads_for() {
   return gathered<GM>() ? kThreads + kGatherThreads : kThreads;
 }
 
+// in-place warp reduce-scatter of 32 per-lane values: afterwards a[0] in
+// lane l holds the sum over all lanes of their a[l] (butterfly halving)
+__device__ __forceinline__ void warp_reduce_scatter32(float (&a)[32], int lane) {
+#pragma unroll
+  for (int w = 16; w >= 1; w >>= 1) {
+    const bool up = (lane & w) != 0;
+#pragma unroll
+    for (int i = 0; i < w; ++i) {
+      const float send = up ? a[i] : a[i + w];
+      const float keep = up ? a[i + w] : a[i];
+      a[i] = fadd(keep, __shfl_xor_sync(0xffffffffu, send, w));
+    }
+  }
+}
+
 // ACTK: 0 no activation, 1 relu, 2 any (runtime code; cold path)
 template <bool A_MN, bool B_MN, int BN, int ACTK, int GM>
 __global__ void __launch_bounds__(threads_for<GM>(), 1)
@@ -580,24 +595,28 @@ tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           }
           if (colstats) {
-            // per-column (mean, M2) of this warp's valid rows, read back
-            // column-wise from the staged box (one row per step: conflict
-            // free): the BatchNorm statistics of the convolution output,
-            // merged later in a fixed order (bn_stats_from_tiles)
+            // per-column (mean, M2) of this warp's valid rows (lane = row):
+            // values shifted by the block's first row, then two warp
+            // reduce-scatter butterflies leave column c0 + lane's sums in
+            // lane `lane` (fixed tree order: deterministic) -- the
+            // BatchNorm statistics of the convolution output, merged later
+            // in a fixed order (bn_stats_from_tiles)
             const int nrows = min(32, M - row0);
             const int col = n0 + c0 + lane;
-            // one pass of sums shifted by the block's first value (no
-            // cancellation), converted to (mean, M2) of the block
-            const uint8_t* cp = buf + ((lane & 3) << 2);
-            const float x0 = *reinterpret_cast<const float*>(cp + ((lane >> 2) << 4));
-            float s1 = 0.0f, s2 = 0.0f;
-#pragma unroll 8
-            for (int r = 1; r < nrows; ++r) {
-              const float d =
-                  *reinterpret_cast<const float*>(cp + r * 128 + (((lane >> 2) ^ (r & 7)) << 4)) - x0;
-              s1 += d;
-              s2 += d * d;
+            const bool valid = lane < nrows;
+            float x0 = 0.0f;
+            float sq[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const float t = __shfl_sync(0xffffffffu, v[j], 0);
+              if (lane == j) x0 = t;
+              const float d = valid ? v[j] - t : 0.0f;
+              v[j] = d;
+              sq[j] = d * d;
             }
+            warp_reduce_scatter32(v, lane);
+            warp_reduce_scatter32(sq, lane);
+            const float s1 = v[0], s2 = sq[0];
             const float inv = 1.0f / float(nrows);
             const float dm = s1 * inv;
             const float m2 = fmaxf(s2 - s1 * dm, 0.0f);
