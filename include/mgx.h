@@ -194,6 +194,16 @@ int mgx_bn_stats(const float* x, int64_t M, int64_t C, void* ws, float* stats, f
                  float* moving_var, float eps, float momentum, int use_global, uintptr_t stream);
 /* y = act((x - mean) * rstd * gamma + beta); gamma NULL = fix_gamma (1).
  * y16 (C % 4 == 0): also a bf16 copy; y may then be NULL (copy only). */
+/* As mgx_bn_apply / mgx_bn_fwd_fused with an output row stride `ldo`
+ * (elements, 0 = C): y / y16 may be channel slices of a wider tensor (a
+ * Concat output written in place by its producers). */
+int mgx_bn_apply_ld(const float* x, const float* stats, const float* gamma, const float* beta,
+                    float* y, int64_t M, int64_t C, int act, void* y16, int64_t ldo,
+                    uintptr_t stream);
+int mgx_bn_fwd_fused_ld(const float* x, int64_t M, int64_t C, float* stats, float* moving_mean,
+                        float* moving_var, float eps, float momentum, const float* gamma,
+                        const float* beta, float* y, void* y16, int act, int64_t ldo,
+                        uintptr_t stream);
 int mgx_bn_apply(const float* x, const float* stats, const float* gamma, const float* beta,
                  float* y, int64_t M, int64_t C, int act, void* y16, uintptr_t stream);
 /* sums = [sum dy | sum dy*xhat] per channel; also written to dbeta and

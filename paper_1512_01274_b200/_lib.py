@@ -158,6 +158,10 @@ _SIGNATURES = {
     "mgx_reduce_workspace_bytes": ([c_i64, c_i64, ctypes.POINTER(c_i64)], ctypes.c_int),
     "mgx_bn_stats": ([c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_f32, c_f32, ctypes.c_int,
                       c_uptr], ctypes.c_int),
+    "mgx_bn_apply_ld": ([c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, ctypes.c_int, c_vp, c_i64,
+                         c_uptr], ctypes.c_int),
+    "mgx_bn_fwd_fused_ld": ([c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_f32, c_f32, c_vp, c_vp, c_vp,
+                             c_vp, ctypes.c_int, c_i64, c_uptr], ctypes.c_int),
     "mgx_bn_apply": ([c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, ctypes.c_int, c_vp, c_uptr],
                      ctypes.c_int),
     "mgx_bn_bwd_reduce": ([c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, ctypes.c_int,

@@ -425,7 +425,7 @@ def _bn_stats(x: View, attrs, ctx, code: list, update: bool, mm=None, mv=None,
 
 
 def bn_forward_instrs(ins, out: View, attrs, act: int = 0, tiles: Optional[int] = None,
-                      xnode=None, y_fp32: bool = True) -> list:
+                      xnode=None, y_fp32: bool = True, cat: Optional[tuple] = None) -> list:
     """BatchNorm (+ activation) forward: statistics, then one apply pass
     writing the fp32 output and, when a convolution consumes it, its bf16
     copy; ``y_fp32=False`` (the executor proved every consumer reads the
@@ -437,6 +437,10 @@ def bn_forward_instrs(ins, out: View, attrs, act: int = 0, tiles: Optional[int] 
     gamma = None if attrs.get("fix_gamma", True) else ins[1].ptr
     y16 = ctx.shadow_out(out.size) if c % 8 == 0 else None
     yp = out.ptr if (y_fp32 or y16 is None) else None
+    ldo = 0
+    if cat is not None:
+        # the output is a channel slice of a Concat written in place
+        yp, y16, ldo = cat
     eps = float(attrs.get("eps", 1e-3))
     key = ("bnstats", id(xnode if xnode is not None else ctx.input_node("in0")), x.ptr, eps)
     if tiles is None and key not in ctx.memo and _bn_train_fused(attrs, ctx, m, c):
@@ -444,12 +448,12 @@ def bn_forward_instrs(ins, out: View, attrs, act: int = 0, tiles: Optional[int] 
         st = ctx.persistent(8 * c)
         ctx.memo[key] = st
         code.append(instr(L.OP_BN_FWD_FUSED, [x.ptr, st, gamma, ins[2].ptr, yp, y16],
-                          [m, c, ins[3].ptr if ins[3] else 0, ins[4].ptr if ins[4] else 0],
+                          [m, c, ins[3].ptr if ins[3] else 0, ins[4].ptr if ins[4] else 0, ldo],
                           [eps, float(attrs.get("momentum", 0.9))], act=act))
         return code
     st = _bn_stats(x, attrs, ctx, code, update=True, mm=ins[3], mv=ins[4], xnode=xnode,
                    tiles=tiles)
-    code.append(instr(L.OP_BN_APPLY, [x.ptr, st, gamma, ins[2].ptr, yp, y16], [m, c], act=act))
+    code.append(instr(L.OP_BN_APPLY, [x.ptr, st, gamma, ins[2].ptr, yp, y16], [m, c, ldo], act=act))
     return code
 
 
@@ -579,7 +583,7 @@ AUX_SUFFIXES = ("_moving_mean", "_moving_var")
 
 
 def conv_bn_instrs(cins, cout: View, cattrs, bins, bout: View, battrs, act: int, conv_node,
-                   y_fp32: bool = True):
+                   y_fp32: bool = True, cat: Optional[tuple] = None):
     """Convolution -> BatchNorm (-> activation) forward: the GEMM epilogue
     produces the BatchNorm statistics of its output (per 32-row (mean, M2)
     pairs), so the BatchNorm never re-reads the convolution output for its
@@ -591,11 +595,11 @@ def conv_bn_instrs(cins, cout: View, cattrs, bins, bout: View, battrs, act: int,
         # on-chip pass: no epilogue statistics needed
         code = conv_forward_instrs(cins, cout, cattrs)
         return code + bn_forward_instrs(bins, bout, battrs, act=act, xnode=conv_node,
-                                        y_fp32=y_fp32)
+                                        y_fp32=y_fp32, cat=cat)
     tiles = ctx.scratch(8 * (-(-m // 32)) * f)
     code = conv_forward_instrs(cins, cout, cattrs, colstats=tiles)
     code += bn_forward_instrs(bins, bout, battrs, act=act, tiles=tiles, xnode=conv_node,
-                              y_fp32=y_fp32)
+                              y_fp32=y_fp32, cat=cat)
     return code
 
 

@@ -211,7 +211,7 @@ bn_fwd_fused_kernel(const float* __restrict__ x, int M, int C, int rows_cta, flo
                     float momentum, float* __restrict__ stats, float* __restrict__ mmean,
                     float* __restrict__ mvar, const float* __restrict__ gamma,
                     const float* __restrict__ beta, float* __restrict__ y,
-                    __nv_bfloat16* __restrict__ y16, int act) {
+                    __nv_bfloat16* __restrict__ y16, int act, int ldo4) {
   constexpr int RP = kThreads / W;  // rows per pass
   constexpr int NC = 4 * W;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -286,7 +286,9 @@ bn_fwd_fused_kernel(const float* __restrict__ x, int M, int C, int rows_cta, flo
       const float t = (pv[q] - mu[q]) * rs[q] * gm[q] + bt[q];
       pv[q] = act == MGX_ACT_RELU ? relu(t) : act_forward(act, t);
     }
-    const int i = r * C4 + s.c4;
+    // outputs may be channel slices of a wider tensor (a Concat written in
+    // place): row stride ldo4 float4 / uint2 vectors
+    const int i = r * ldo4 + s.c4;
     if (y) reinterpret_cast<float4*>(y)[i] = v;
     if (y16) {
       uint2 h;
@@ -511,7 +513,7 @@ int Launcher<Params...>::run(const Cfg& cfg, int64_t C, cudaStream_t st, Args...
 template <int W, typename... Args>
 int launch_fwd(const Cfg& cfg, int64_t C, cudaStream_t st, Args... args) {
   return Launcher<const float*, int, int, int, float, float, float*, float*, float*,
-                  const float*, const float*, float*, __nv_bfloat16*,
+                  const float*, const float*, float*, __nv_bfloat16*, int,
                   int>::template run<bn_fwd_fused_kernel<W>>(cfg, C, st, args...);
 }
 
@@ -534,31 +536,42 @@ extern "C" int mgx_bn_fused_ok(int64_t M, int64_t C, int backward, int* ok) {
   return MGX_OK;
 }
 
-extern "C" int mgx_bn_fwd_fused(const float* x, int64_t M, int64_t C, float* stats,
-                                float* moving_mean, float* moving_var, float eps, float momentum,
-                                const float* gamma, const float* beta, float* y, void* y16,
-                                int act, uintptr_t stream) {
+extern "C" int mgx_bn_fwd_fused_ld(const float* x, int64_t M, int64_t C, float* stats,
+                                   float* moving_mean, float* moving_var, float eps,
+                                   float momentum, const float* gamma, const float* beta, float* y,
+                                   void* y16, int act, int64_t ldo, uintptr_t stream) {
   MGX_REQUIRE(x && stats && beta && (y || y16) && M > 0 && C > 0 && C <= 65536,
               "mgx_bn_fwd_fused: bad arguments");
   MGX_REQUIRE(mgx::aligned16(x) && (!y || mgx::aligned16(y)) && (!y16 || mgx::aligned16(y16)),
               "mgx_bn_fwd_fused: unaligned tensors");
+  if (ldo == 0) ldo = C;
+  MGX_REQUIRE(ldo >= C && ldo % 4 == 0 && ldo < 65536 * 4, "mgx_bn_fwd_fused: bad output stride");
   const Cfg cfg = mgx::bnf::pick(M, C, 1);
   MGX_REQUIRE(cfg.W != 0, "mgx_bn_fwd_fused: shape (%lld, %lld) does not fit a cluster",
               static_cast<long long>(M), static_cast<long long>(C));
   cudaStream_t st = mgx::as_stream(stream);
   const int Ci = static_cast<int>(C);
+  const int ld4 = static_cast<int>(ldo / 4);
   __nv_bfloat16* h = static_cast<__nv_bfloat16*>(y16);
   switch (cfg.W) {
     case 8:
-      return mgx::bnf::launch_fwd<8>(cfg, C, st, x, M, Ci, cfg.rows_cta,
-                              eps, momentum, stats, moving_mean, moving_var, gamma, beta, y, h, act);
+      return mgx::bnf::launch_fwd<8>(cfg, C, st, x, M, Ci, cfg.rows_cta, eps, momentum, stats,
+                                     moving_mean, moving_var, gamma, beta, y, h, act, ld4);
     case 4:
-      return mgx::bnf::launch_fwd<4>(cfg, C, st, x, M, Ci, cfg.rows_cta,
-                              eps, momentum, stats, moving_mean, moving_var, gamma, beta, y, h, act);
+      return mgx::bnf::launch_fwd<4>(cfg, C, st, x, M, Ci, cfg.rows_cta, eps, momentum, stats,
+                                     moving_mean, moving_var, gamma, beta, y, h, act, ld4);
     default:
-      return mgx::bnf::launch_fwd<2>(cfg, C, st, x, M, Ci, cfg.rows_cta,
-                              eps, momentum, stats, moving_mean, moving_var, gamma, beta, y, h, act);
+      return mgx::bnf::launch_fwd<2>(cfg, C, st, x, M, Ci, cfg.rows_cta, eps, momentum, stats,
+                                     moving_mean, moving_var, gamma, beta, y, h, act, ld4);
   }
+}
+
+extern "C" int mgx_bn_fwd_fused(const float* x, int64_t M, int64_t C, float* stats,
+                                float* moving_mean, float* moving_var, float eps, float momentum,
+                                const float* gamma, const float* beta, float* y, void* y16,
+                                int act, uintptr_t stream) {
+  return mgx_bn_fwd_fused_ld(x, M, C, stats, moving_mean, moving_var, eps, momentum, gamma, beta,
+                             y, y16, act, C, stream);
 }
 
 extern "C" int mgx_bn_bwd_fused(const float* dy, int64_t ldd, const float* x, const float* stats,

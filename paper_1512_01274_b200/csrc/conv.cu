@@ -1118,7 +1118,7 @@ __global__ void colsum_finalize_kernel(const double* __restrict__ ws, int nchunk
 __global__ void bn_apply_kernel(const float* __restrict__ x, const float* __restrict__ stats,
                                 const float* __restrict__ gamma, const float* __restrict__ beta,
                                 float* __restrict__ y, int64_t M, int C, int act,
-                                __nv_bfloat16* __restrict__ y16) {
+                                __nv_bfloat16* __restrict__ y16, int64_t ldo4) {
   const int64_t total = M * C;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   if ((C & 3) == 0) {
@@ -1137,7 +1137,9 @@ __global__ void bn_apply_kernel(const float* __restrict__ x, const float* __rest
       gm[u] = g;
       bt[u] = __ldg(beta + cc);
     }
-    auto one = [&](float4 v, int64_t i) {
+    // outputs may be channel slices of a wider tensor (row stride ldo4)
+    auto one = [&](float4 v, int64_t row) {
+      const int64_t i = row * ldo4 + c4;
       float* pv = &v.x;
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
@@ -1159,9 +1161,9 @@ __global__ void bn_apply_kernel(const float* __restrict__ x, const float* __rest
 #pragma unroll
       for (int u = 0; u < U; ++u) v[u] = __ldg(reinterpret_cast<const float4*>(x) + (r + u * int64_t(ri.rstep)) * C4 + c4);
 #pragma unroll
-      for (int u = 0; u < U; ++u) one(v[u], (r + u * int64_t(ri.rstep)) * C4 + c4);
+      for (int u = 0; u < U; ++u) one(v[u], r + u * int64_t(ri.rstep));
     }
-    for (; r < M; r += ri.rstep) one(__ldg(reinterpret_cast<const float4*>(x) + r * C4 + c4), r * C4 + c4);
+    for (; r < M; r += ri.rstep) one(__ldg(reinterpret_cast<const float4*>(x) + r * C4 + c4), r);
   } else {
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
       const int c = static_cast<int>(i % C);
@@ -1883,9 +1885,11 @@ extern "C" int mgx_bn_stats(const float* x, int64_t M, int64_t C, void* ws, floa
   return MGX_OK;
 }
 
-extern "C" int mgx_bn_apply(const float* x, const float* stats, const float* gamma,
-                            const float* beta, float* y, int64_t M, int64_t C, int act, void* y16,
-                            uintptr_t stream) {
+extern "C" int mgx_bn_apply_ld(const float* x, const float* stats, const float* gamma,
+                               const float* beta, float* y, int64_t M, int64_t C, int act,
+                               void* y16, int64_t ldo, uintptr_t stream) {
+  if (ldo == 0) ldo = C;
+  MGX_REQUIRE(ldo == C || (ldo > C && ldo % 4 == 0 && C % 4 == 0), "mgx_bn_apply: bad output stride");
   MGX_REQUIRE(x && stats && beta && (y || y16) && M > 0 && C > 0, "mgx_bn_apply: bad arguments");
   MGX_REQUIRE(!y16 || (C % 4 == 0 && mgx::aligned16(y16)), "mgx_bn_apply: bf16 copy needs C %% 4 == 0");
   if ((C & 3) == 0) {
@@ -1894,13 +1898,19 @@ extern "C" int mgx_bn_apply(const float* x, const float* stats, const float* gam
                                  mgx::rows_block(C / 4), 0,
                                  mgx::as_stream(stream)>>>(x, stats, gamma, beta, y, M,
                                                            static_cast<int>(C), act,
-                                                           static_cast<__nv_bfloat16*>(y16));
+                                                           static_cast<__nv_bfloat16*>(y16), ldo / 4);
   } else {
     mgx::conv::bn_apply_kernel<<<grid_for(M * C), 256, 0, mgx::as_stream(stream)>>>(
-        x, stats, gamma, beta, y, M, static_cast<int>(C), act, nullptr);
+        x, stats, gamma, beta, y, M, static_cast<int>(C), act, nullptr, int64_t(0));
   }
   MGX_LAUNCHED();
   return MGX_OK;
+}
+
+extern "C" int mgx_bn_apply(const float* x, const float* stats, const float* gamma,
+                            const float* beta, float* y, int64_t M, int64_t C, int act, void* y16,
+                            uintptr_t stream) {
+  return mgx_bn_apply_ld(x, stats, gamma, beta, y, M, C, act, y16, C, stream);
 }
 
 extern "C" int mgx_bn_bwd_reduce(const float* dy, const float* x, const float* stats, int64_t M,

@@ -253,8 +253,8 @@ static int run_instr(const mgx_instr& in, cudaStream_t st) {
       return mgx_bn_stats(p0, d[0], d[1], in.ptr[1], p2, p3, static_cast<float*>(in.ptr[4]),
                           in.fattr[0], in.fattr[1], static_cast<int>(d[2]), s);
     case MGX_OP_BN_APPLY:
-      return mgx_bn_apply(p0, p1, p2, p3, static_cast<float*>(in.ptr[4]), d[0], d[1], in.act,
-                          in.ptr[5], s);
+      return mgx_bn_apply_ld(p0, p1, p2, p3, static_cast<float*>(in.ptr[4]), d[0], d[1], in.act,
+                             in.ptr[5], d[2], s);
     case MGX_OP_BN_BWD_REDUCE:
       return mgx_bn_bwd_reduce(p0, p1, p2, d[0], d[1], in.ptr[3], static_cast<float*>(in.ptr[4]),
                                reinterpret_cast<float*>(d[2]), reinterpret_cast<float*>(d[3]),
@@ -331,9 +331,9 @@ static int run_instr(const mgx_instr& in, cudaStream_t st) {
                         in.ptr[5], d[0], s);
     }
     case MGX_OP_BN_FWD_FUSED:
-      return mgx_bn_fwd_fused(p0, d[0], d[1], p1, reinterpret_cast<float*>(d[2]),
-                              reinterpret_cast<float*>(d[3]), in.fattr[0], in.fattr[1], p2, p3,
-                              static_cast<float*>(in.ptr[4]), in.ptr[5], in.act, s);
+      return mgx_bn_fwd_fused_ld(p0, d[0], d[1], p1, reinterpret_cast<float*>(d[2]),
+                                 reinterpret_cast<float*>(d[3]), in.fattr[0], in.fattr[1], p2, p3,
+                                 static_cast<float*>(in.ptr[4]), in.ptr[5], in.act, d[4], s);
     case MGX_OP_BN_BWD_FUSED:
       return mgx_bn_bwd_fused(p0, (d[6] >> 8) ? (d[6] >> 8) : d[1], p1, p2, p3, d[0], d[1],
                               reinterpret_cast<const float*>(d[2]),
