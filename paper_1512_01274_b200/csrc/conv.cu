@@ -1583,13 +1583,19 @@ pool_avg3_tile_kernel(const float4* __restrict__ src, float4* __restrict__ dst,
   const int WP = g.W + 2;
   const int rows = min(kAvgTR, g.H - h0);
   const int nload = (rows + 2) * WP * kAvgVS;
+  // the whole strip in flight at once: 16-byte cp.async copies straight
+  // into shared memory, zero-filled outside the map (the padding taps)
   for (int e = threadIdx.x; e < nload; e += blockDim.x) {
     const int v = e % kAvgVS, cw = (e / kAvgVS) % WP, rr = e / (kAvgVS * WP);
     const int h = h0 - 1 + rr, w = cw - 1, c4 = v0 + v;
-    avg_tile[e] = (h >= 0 && h < g.H && w >= 0 && w < g.W && c4 < C4)
-                  ? __ldg(src + ((int64_t(b) * g.H + h) * g.W + w) * C4 + c4)
-                  : make_float4(0.f, 0.f, 0.f, 0.f);
+    const bool ok = h >= 0 && h < g.H && w >= 0 && w < g.W && c4 < C4;
+    const float4* sp = ok ? src + ((int64_t(b) * g.H + h) * g.W + w) * C4 + c4 : src;
+    const uint32_t dst_s = static_cast<uint32_t>(__cvta_generic_to_shared(avg_tile + e));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst_s), "l"(sp),
+                 "r"(ok ? 16 : 0)
+                 : "memory");
   }
+  asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
   const float inv = __frcp_rn(9.0f);
   const int nout = rows * g.W * kAvgVS;
