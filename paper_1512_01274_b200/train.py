@@ -285,8 +285,12 @@ class DataParallelStep:
         worker.  staged=True takes the batch started by ``stage``."""
         self._ensure_bound()
         for w in self.workers:
-            for i, n in enumerate(self.names):
-                self.kv.pull(i, self.args[w][n], w)
+            if not self.embedded:
+                for i, n in enumerate(self.names):
+                    self.kv.pull(i, self.args[w][n], w)
+            # (rounds inside the backward: the executor's arguments ARE the
+            # replicas the previous step's rounds wrote, in stream order --
+            # the per-key pulls would be no-ops)
             if shards is not None:
                 self.load(w, *shards[w])
             elif staged:
