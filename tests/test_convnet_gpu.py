@@ -224,3 +224,54 @@ def test_inception_bn_full_size_runs(engine):
             sgd_step(args[n], grads[n], vel[n], vel[n], SGDConfig(0.01, 0.9, 1e-4))
     assert np.all(np.isfinite(losses))
     assert losses[-1] < losses[0]
+
+
+def _train_steps(engine, monkeypatch, env, overlap, steps=2):
+    """Two LeNet-less mini-Inception data-parallel steps (1 worker, bf16
+    mode) under the given environment; returns weights, BatchNorm state and
+    outputs."""
+    from paper_1512_01274_b200 import tensor as tmod
+    from paper_1512_01274_b200.kvstore import KVStore
+    from paper_1512_01274_b200.optim import SGDConfig, make_sgd_updater
+    from paper_1512_01274_b200.train import DataParallelStep, init_params
+    from paper_1512_01274_b200 import symbol
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    symbol.reset_names()
+    g = mini_inception()
+    given = {"data": (8, 32, 32, 3), "label": (8,)}
+    shapes, _ = symbol.infer_shape(g, given)
+    kv = KVStore(1, 1, engine=engine, bucket_bytes=1 << 12)
+    st = DataParallelStep(g, kv, given, init_params(g, shapes, 5), engine=engine, dense="bf16",
+                          overlap=overlap)
+    kv.set_updater(make_sgd_updater(SGDConfig(0.05, 0.9, 1e-4), scale=1))
+    st.execs  # bind under env
+    for k in env:
+        monkeypatch.delenv(k)
+    rs = np.random.RandomState(3)
+    for _ in range(steps):
+        st.step({0: (rs.randn(8, 32, 32, 3).astype(np.float32),
+                     rs.randint(0, 10, 8).astype(np.float32))})
+    kv.round_barrier()
+    out = {n: tmod.to_numpy(st.args[0][n]) for n in st.names + st.aux}
+    out["__softmax"] = st.outputs(0)
+    embedded, cats = st.embedded, len(st.execs[0]._cat_concats)
+    kv.close()
+    return out, embedded, cats
+
+
+def test_concat_in_place_and_embedded_rounds_are_bitwise_neutral(engine, monkeypatch):
+    """The round-2 data-movement changes do not change a bit: Concats
+    written in place by their branches' BatchNorms vs copied, and the
+    store's rounds inside the backward program (per bucket, own lane) vs one
+    flush after it."""
+    base, emb, cats = _train_steps(engine, monkeypatch, {}, overlap=True)
+    assert emb and cats == 3
+    no_cat, _e, cats0 = _train_steps(engine, monkeypatch, {"MGX_CONCAT_INPLACE": "0"},
+                                     overlap=True)
+    assert cats0 == 0
+    flush, emb1, _c = _train_steps(engine, monkeypatch, {}, overlap=False)
+    assert not emb1
+    for other in (no_cat, flush):
+        for k in base:
+            np.testing.assert_array_equal(other[k], base[k], err_msg=k)
