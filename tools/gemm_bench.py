@@ -16,6 +16,8 @@ SHAPES = [  # (M, N, K, a_mn, b_mn, splits)
     (193600, 192, 576, 0, 0, 1),    # conv_2 forward
     (46656, 96, 864, 0, 0, 1),      # 3x3 forward
     (192, 576, 193600, 1, 1, 0),    # wgrad split-K
+    (12544, 192, 1728, 0, 0, 1),    # 14x14 3x3 forward (one tile per CTA)
+    (3136, 224, 2016, 0, 0, 0),     # 7x7 3x3 forward (split-K)
     (8192, 8192, 8192, 0, 0, 1),    # big square
 ]
 
@@ -49,8 +51,25 @@ def main():
             tot += e0.elapsed_time(e1)
         ms = tot / reps
         byt = 2 * (m * k + n * k) + 4 * m * n
+        # cuBLAS (torch.matmul, bf16 in / bf16 out) on the same shape, for context
+        ta = torch.randn(m, k, device="cuda", dtype=torch.bfloat16)
+        tb = torch.randn(k, n, device="cuda", dtype=torch.bfloat16)
+        for _ in range(3):
+            torch.matmul(ta, tb)
+        torch.cuda.synchronize()
+        cb = 0.0
+        for _ in range(reps):
+            flush.fill_(1.0)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch.matmul(ta, tb)
+            e1.record()
+            torch.cuda.synchronize()
+            cb += e0.elapsed_time(e1)
+        cb /= reps
         print(f"M={m:7d} N={n:5d} K={k:7d} amn={amn} bmn={bmn}: {ms * 1e3:9.1f} us "
-              f"{2 * m * n * k / ms / 1e9:8.1f} TF/s  {byt / ms / 1e6:8.1f} GB/s", flush=True)
+              f"{2 * m * n * k / ms / 1e9:8.1f} TF/s  {byt / ms / 1e6:8.1f} GB/s   "
+              f"| cuBLAS {cb * 1e3:8.1f} us {2 * m * n * k / cb / 1e9:8.1f} TF/s", flush=True)
     # write-bandwidth reference: fill of the largest output
     c = torch.empty(193600 * 576, device="cuda")
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
