@@ -40,7 +40,8 @@ def main():
     for n in aux_names(g):
         args[n] = tmod.from_host(shapes[n], "float32", a0[n], engine=eng)
     grads = {n: tmod.zeros(shapes[n], engine=eng) for n in names}
-    ex = bind(g, args, {n: "write" for n in names}, grads, engine=eng, dense=cfg["dense"])
+    ex = bind(g, args, {n: "write" for n in names}, grads, engine=eng, dense=cfg["dense"],
+              strategy=cfg.get("strategy", "both"))
     for _ in range(3):
         ex.forward()
         ex.backward()
