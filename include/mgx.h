@@ -224,11 +224,13 @@ int mgx_bn_bwd_reduce(const float* dy, const float* x, const float* stats, int64
 int mgx_bn_bwd_dx(const float* dy, const float* x, const float* stats, const float* sums,
                   const float* gamma, float* dx, int64_t M, int64_t C, const float* relu_gamma,
                   const float* relu_beta, float* dsum, void* ws, void* dx16, uintptr_t stream);
-/* Cluster-fused BatchNorm (training) for layers whose rows fit on-chip
+/* Cluster-fused BatchNorm (training) for layers of up to 65536 rows
  * (bn_fused.cu): a thread-block cluster owns a channel slice and all rows,
- * stages them in shared memory once, reduces over DSMEM in a fixed order.
- * mgx_bn_fused_ok: *ok = 1 when (M, C) has such a launch shape (C % 8 == 0,
- * tile fits); the fused entry points reject other shapes.
+ * stages them in shared memory once (or, from 32768 rows, streams them
+ * twice through L2), reduces over DSMEM in a fixed order.
+ * mgx_bn_fused_ok: *ok = 1 (staged) or 2 (streamed) when (M, C) has such a
+ * launch shape (C % 8 == 0), else 0; the fused entry points reject other
+ * shapes.
  * fwd: stats [mean | rstd] + moving averages + y = act(bn(x)) -> y (fp32,
  * optional) / y16 (bf16, optional) in one kernel.
  * bwd: dy' = dy masked by the fused ReLU (relu_beta non-NULL: mask

@@ -383,16 +383,23 @@ def _bn_infer(shapes, attrs):
 _FUSED_OK = {}
 
 
-def bn_fused_ok(m: int, c: int, backward: bool) -> bool:
-    """Whether the cluster-fused BatchNorm kernels (bn_fused.cu) take this
-    (rows, channels) shape: one launch per pass instead of 2-4."""
+def bn_fused_kind(m: int, c: int, backward: bool) -> int:
+    """How the cluster-fused BatchNorm kernels (bn_fused.cu) take this
+    (rows, channels) shape: 0 not at all, 1 rows staged on-chip, 2 rows
+    streamed twice through L2."""
     key = (m, c, bool(backward))
     if key not in _FUSED_OK:
         import ctypes
         ok = ctypes.c_int(0)
         L.call("mgx_bn_fused_ok", m, c, 1 if backward else 0, ctypes.byref(ok))
-        _FUSED_OK[key] = bool(ok.value)
+        _FUSED_OK[key] = int(ok.value)
     return _FUSED_OK[key]
+
+
+def bn_fused_ok(m: int, c: int, backward: bool) -> bool:
+    """Whether the cluster-fused BatchNorm kernels take this shape: one
+    launch per pass instead of 2-4."""
+    return bn_fused_kind(m, c, backward) != 0
 
 
 def _bn_train_fused(attrs, ctx, m, c) -> bool:

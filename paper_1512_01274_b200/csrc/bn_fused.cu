@@ -38,6 +38,13 @@ namespace bnf {
 constexpr int kThreads = 512;
 constexpr int kStages = 4;  // cp.async commit groups per tile (load/compute overlap)
 constexpr int kWarps = kThreads / 32;
+constexpr int kU = 4;  // streaming variant: rows in flight per thread
+
+// Streaming variant (layers whose rows do not fit on-chip): the first pass
+// reads with the default policy (the lines stay in L2), the second pass is
+// the last use of them.
+__device__ __forceinline__ float4 ld_keep(const float4* p) { return __ldg(p); }
+__device__ __forceinline__ float4 ld_last(const float4* p) { return __ldcs(p); }
 
 __device__ __forceinline__ uint32_t pack2(float a, float b) {
   __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
@@ -205,7 +212,7 @@ __device__ __forceinline__ void stage_in(const Slice& s, const float4* const (&s
 
 // Forward: statistics (training, shifted sums against row 0), moving
 // averages, apply (+act) -> y (fp32, optional) and y16 (bf16, optional).
-template <int W>
+template <int W, bool STREAM>
 __global__ void __launch_bounds__(kThreads)
 bn_fwd_fused_kernel(const float* __restrict__ x, int M, int C, int rows_cta, float eps,
                     float momentum, float* __restrict__ stats, float* __restrict__ mmean,
@@ -230,7 +237,7 @@ bn_fwd_fused_kernel(const float* __restrict__ x, int M, int C, int rows_cta, flo
   const Slice s = slice_of<W>(cl, M, rows_cta);
   const int C4 = C >> 2;
   const float4* x4 = reinterpret_cast<const float4*>(x);
-  {
+  if (!STREAM) {
     const float4* src[1] = {x4};
     float4* dst[1] = {tile};
     const int ld4[1] = {C4};
@@ -239,18 +246,34 @@ bn_fwd_fused_kernel(const float* __restrict__ x, int M, int C, int rows_cta, flo
   const float4 shv = __ldg(x4 + s.c4);  // row 0: the shift of the sums
   const float sh[4] = {shv.x, shv.y, shv.z, shv.w};
   float s0[4] = {0.f, 0.f, 0.f, 0.f}, s1[4] = {0.f, 0.f, 0.f, 0.f};
-  for (int st = 0; st < kStages; ++st) {
-    wait_stage(kStages - 1 - st);
-    for (int k = st * s.per; k < (st + 1) * s.per; ++k) {
-      const int lr = s.rin + k * RP;
-      if (s.r0 + lr >= s.r1) break;
-      const float4 v = tile[lr * W + s.v];
-      const float* pv = &v.x;
+  auto acc_stats = [&](const float4& v) {
+    const float* pv = &v.x;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const float d = pv[q] - sh[q];
-        s0[q] += d;
-        s1[q] += d * d;
+    for (int q = 0; q < 4; ++q) {
+      const float d = pv[q] - sh[q];
+      s0[q] += d;
+      s1[q] += d * d;
+    }
+  };
+  if (STREAM) {
+    // rows straight from global memory, kU loads in flight per thread (the
+    // same per-thread row order as the staged path)
+    for (int r = s.r0 + s.rin; r < s.r1; r += kU * RP) {
+      float4 v[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+        if (r + u * RP < s.r1) v[u] = ld_keep(x4 + int64_t(r + u * RP) * C4 + s.c4);
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+        if (r + u * RP < s.r1) acc_stats(v[u]);
+    }
+  } else {
+    for (int st = 0; st < kStages; ++st) {
+      wait_stage(kStages - 1 - st);
+      for (int k = st * s.per; k < (st + 1) * s.per; ++k) {
+        const int lr = s.rin + k * RP;
+        if (s.r0 + lr >= s.r1) break;
+        acc_stats(tile[lr * W + s.v]);
       }
     }
   }
@@ -278,8 +301,7 @@ bn_fwd_fused_kernel(const float* __restrict__ x, int M, int C, int rows_cta, flo
       if (mvar) mvar[c] = static_cast<float>(double(mvar[c]) * momentum + var * (1.0 - momentum));
     }
   }
-  for (int r = s.r0 + s.rin; r < s.r1; r += RP) {
-    float4 v = tile[(r - s.r0) * W + s.v];
+  auto apply = [&](float4 v, int r) {
     float* pv = &v.x;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -288,7 +310,7 @@ bn_fwd_fused_kernel(const float* __restrict__ x, int M, int C, int rows_cta, flo
     }
     // outputs may be channel slices of a wider tensor (a Concat written in
     // place): row stride ldo4 float4 / uint2 vectors
-    const int i = r * ldo4 + s.c4;
+    const int64_t i = int64_t(r) * ldo4 + s.c4;
     if (y) reinterpret_cast<float4*>(y)[i] = v;
     if (y16) {
       uint2 h;
@@ -296,6 +318,20 @@ bn_fwd_fused_kernel(const float* __restrict__ x, int M, int C, int rows_cta, flo
       h.y = pack2(v.z, v.w);
       reinterpret_cast<uint2*>(y16)[i] = h;
     }
+  };
+  if (STREAM) {
+    // second read of the rows: L2 hits (this CTA read them moments ago)
+    for (int r = s.r0 + s.rin; r < s.r1; r += kU * RP) {
+      float4 v[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+        if (r + u * RP < s.r1) v[u] = ld_last(x4 + int64_t(r + u * RP) * C4 + s.c4);
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+        if (r + u * RP < s.r1) apply(v[u], r + u * RP);
+    }
+  } else {
+    for (int r = s.r0 + s.rin; r < s.r1; r += RP) apply(tile[(r - s.r0) * W + s.v], r);
   }
   cluster_wait();  // no CTA leaves while a peer's pushes may be in flight
 }
@@ -304,7 +340,7 @@ bn_fwd_fused_kernel(const float* __restrict__ x, int M, int C, int rows_cta, flo
 // mask), dbeta/dgamma/sums, then dx = gamma * rstd * (dy' - (s1 + xhat s2)/M)
 // -> dx (fp32, optional) / dx16 (bf16, optional), and dsum = sum dx
 // (the bias gradient of the convolution feeding the BatchNorm, optional).
-template <int W>
+template <int W, bool STREAM>
 __global__ void __launch_bounds__(kThreads)
 bn_bwd_fused_kernel(const float* __restrict__ dy, int ldd, const float* __restrict__ x,
                     const float* __restrict__ stats, const float* __restrict__ gamma, int M,
@@ -331,10 +367,13 @@ bn_bwd_fused_kernel(const float* __restrict__ dy, int ldd, const float* __restri
   cluster_arrive_relaxed();
   const Slice s = slice_of<W>(cl, M, rows_cta);
   const int C4 = C >> 2;
-  {
-    const float4* src[2] = {reinterpret_cast<const float4*>(dy), reinterpret_cast<const float4*>(x)};
+  const float4* dy4 = reinterpret_cast<const float4*>(dy);
+  const float4* x4 = reinterpret_cast<const float4*>(x);
+  const int ldd4 = ldd >> 2;
+  if (!STREAM) {
+    const float4* src[2] = {dy4, x4};
     float4* dst[2] = {tdy, tx};
-    const int ld4[2] = {ldd >> 2, C4};
+    const int ld4[2] = {ldd4, C4};
     stage_in<W, 2>(s, src, dst, ld4);
   }
   const bool relu = relu_beta != nullptr;
@@ -349,21 +388,39 @@ bn_bwd_fused_kernel(const float* __restrict__ dy, int ldd, const float* __restri
     bt[q] = relu ? __ldg(relu_beta + c) : 0.0f;
   }
   float a0[4] = {0.f, 0.f, 0.f, 0.f}, a1[4] = {0.f, 0.f, 0.f, 0.f};
-  for (int st = 0; st < kStages; ++st) {
-    wait_stage(kStages - 1 - st);
-    for (int k = st * s.per; k < (st + 1) * s.per; ++k) {
-      const int lr = s.rin + k * RP;
-      if (s.r0 + lr >= s.r1) break;
-      const int l = lr * W + s.v;
-      const float4 d = tdy[l], xv = tx[l];
-      const float* pd = &d.x;
-      const float* px = &xv.x;
+  auto acc_sums = [&](const float4& d, const float4& xv) {
+    const float* pd = &d.x;
+    const float* px = &xv.x;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        float dq = pd[q];
-        if (relu && !((px[q] - mu[q]) * rs[q] * gm[q] + bt[q] > 0.0f)) dq = 0.0f;
-        a0[q] += dq;
-        a1[q] += dq * ((px[q] - mu[q]) * rs[q]);
+    for (int q = 0; q < 4; ++q) {
+      float dq = pd[q];
+      if (relu && !((px[q] - mu[q]) * rs[q] * gm[q] + bt[q] > 0.0f)) dq = 0.0f;
+      a0[q] += dq;
+      a1[q] += dq * ((px[q] - mu[q]) * rs[q]);
+    }
+  };
+  if (STREAM) {
+    for (int r = s.r0 + s.rin; r < s.r1; r += kU * RP) {
+      float4 d[kU], xv[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        if (r + u * RP < s.r1) {
+          d[u] = ld_keep(dy4 + int64_t(r + u * RP) * ldd4 + s.c4);
+          xv[u] = ld_keep(x4 + int64_t(r + u * RP) * C4 + s.c4);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+        if (r + u * RP < s.r1) acc_sums(d[u], xv[u]);
+    }
+  } else {
+    for (int st = 0; st < kStages; ++st) {
+      wait_stage(kStages - 1 - st);
+      for (int k = st * s.per; k < (st + 1) * s.per; ++k) {
+        const int lr = s.rin + k * RP;
+        if (s.r0 + lr >= s.r1) break;
+        const int l = lr * W + s.v;
+        acc_sums(tdy[l], tx[l]);
       }
     }
   }
@@ -388,9 +445,7 @@ bn_bwd_fused_kernel(const float* __restrict__ dy, int ldd, const float* __restri
   }
   const float invm = static_cast<float>(1.0 / double(M));
   float ds[4] = {0.f, 0.f, 0.f, 0.f};
-  for (int r = s.r0 + s.rin; r < s.r1; r += RP) {
-    const int l = (r - s.r0) * W + s.v;
-    const float4 d = tdy[l], xv = tx[l];
+  auto dx_row = [&](const float4& d, const float4& xv, int r) {
     const float* pd = &d.x;
     const float* px = &xv.x;
     float4 o;
@@ -403,13 +458,33 @@ bn_bwd_fused_kernel(const float* __restrict__ dy, int ldd, const float* __restri
       po[q] = g[q] * rs[q] * (dq - (s1[q] + xhat * s2[q]) * invm);
       ds[q] += po[q];
     }
-    const int i = r * C4 + s.c4;
+    const int64_t i = int64_t(r) * C4 + s.c4;
     if (dx) reinterpret_cast<float4*>(dx)[i] = o;
     if (dx16) {
       uint2 h;
       h.x = pack2(o.x, o.y);
       h.y = pack2(o.z, o.w);
       reinterpret_cast<uint2*>(dx16)[i] = h;
+    }
+  };
+  if (STREAM) {
+    for (int r = s.r0 + s.rin; r < s.r1; r += kU * RP) {
+      float4 d[kU], xv[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        if (r + u * RP < s.r1) {
+          d[u] = ld_last(dy4 + int64_t(r + u * RP) * ldd4 + s.c4);
+          xv[u] = ld_last(x4 + int64_t(r + u * RP) * C4 + s.c4);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u)
+        if (r + u * RP < s.r1) dx_row(d[u], xv[u], r + u * RP);
+    }
+  } else {
+    for (int r = s.r0 + s.rin; r < s.r1; r += RP) {
+      const int l = (r - s.r0) * W + s.v;
+      dx_row(tdy[l], tx[l], r);
     }
   }
   if (dsum) {
@@ -430,6 +505,7 @@ struct Cfg {
   int W = 0, CS = 0;
   int rows_cta = 0;
   size_t smem = 0;
+  bool stream = false;  // rows read from global memory twice, not staged
 };
 
 inline size_t smem_bytes(int W, int CS, int rows_cta, int tensors) {
@@ -447,7 +523,43 @@ inline int env_int(const char* name, int dflt) {
   return v && *v ? atoi(v) : dflt;
 }
 
+// Streaming shape: slices of W vectors (env MGX_BNS_W, default 4: 64-byte
+// fp32 rows), clusters of 16 when fewer than 128 CTAs would run with 8.
+// Rows MGX_BNS_MINM..MGX_BNS_MAXM (default 32768..65536: the 27x27 layers
+// at batch 64) stream; larger layers keep the unfused multi-CTA passes
+// (tools/kbench.py bn / bnf: at 46656 rows x 64 channels the stream runs
+// 14.6 / 18.9 us forward / backward against 16.3 staged and 22.3 unfused;
+// at 193600 rows it loses to the unfused passes).
+inline Cfg pick_stream(int64_t M, int64_t C, int tensors) {
+  static const int sw = env_int("MGX_BNS_W", 4);
+  static const int max_m = env_int("MGX_BNS_MAXM", 65536);
+  Cfg c;
+  if (C % 8 != 0 || M < 1 || M > max_m) return c;
+  const int64_t C4 = C / 4;
+  const int W = (sw == 4 || sw == 8) && C4 % sw == 0 ? sw : 2;
+  const int64_t groups = C4 / W;
+  static const int cs_env = env_int("MGX_BNS_CS", 0);
+  const int CS = cs_env == 8 || cs_env == 16 ? cs_env : (groups * 8 >= 128 ? 8 : 16);
+  return Cfg{W, CS, static_cast<int>(ceil_div(M, CS)), smem_bytes(W, CS, 0, tensors), true};
+}
+
+inline Cfg pick_staged(int64_t M, int64_t C, int tensors);
+
+// env MGX_BNF_STREAM: 0 never stream, 1 stream from MGX_BNS_MINM rows or
+// when the staged tile does not fit (default), 2 always stream
 inline Cfg pick(int64_t M, int64_t C, int tensors) {
+  static const int mode = env_int("MGX_BNF_STREAM", 1);
+  static const int min_m = env_int("MGX_BNS_MINM", 32768);
+  if (mode == 2 || (mode == 1 && M >= min_m)) {
+    const Cfg c = pick_stream(M, C, tensors);
+    if (c.W != 0 || mode == 2) return c;
+  }
+  const Cfg c = pick_staged(M, C, tensors);
+  if (c.W != 0 || mode == 0) return c;
+  return pick_stream(M, C, tensors);
+}
+
+inline Cfg pick_staged(int64_t M, int64_t C, int tensors) {
   // tuning knobs (read once): narrowest slice, CTA target, smem per CTA
   // defaults measured on Inception-BN (bench sweep): slices of >= 4 vectors
   // (full 32-byte sectors for the bf16 writes), >= 64 CTAs, up to 200 KB
@@ -512,17 +624,19 @@ int Launcher<Params...>::run(const Cfg& cfg, int64_t C, cudaStream_t st, Args...
 
 template <int W, typename... Args>
 int launch_fwd(const Cfg& cfg, int64_t C, cudaStream_t st, Args... args) {
-  return Launcher<const float*, int, int, int, float, float, float*, float*, float*,
-                  const float*, const float*, float*, __nv_bfloat16*, int,
-                  int>::template run<bn_fwd_fused_kernel<W>>(cfg, C, st, args...);
+  using L = Launcher<const float*, int, int, int, float, float, float*, float*, float*,
+                     const float*, const float*, float*, __nv_bfloat16*, int, int>;
+  return cfg.stream ? L::template run<bn_fwd_fused_kernel<W, true>>(cfg, C, st, args...)
+                    : L::template run<bn_fwd_fused_kernel<W, false>>(cfg, C, st, args...);
 }
 
 template <int W, typename... Args>
 int launch_bwd(const Cfg& cfg, int64_t C, cudaStream_t st, Args... args) {
-  return Launcher<const float*, int, const float*, const float*, const float*, int, int, int,
-                  const float*, const float*, float*, float*, int, float*, float*,
-                  __nv_bfloat16*, float*>::template run<bn_bwd_fused_kernel<W>>(cfg, C, st,
-                                                                                  args...);
+  using L = Launcher<const float*, int, const float*, const float*, const float*, int, int, int,
+                     const float*, const float*, float*, float*, int, float*, float*,
+                     __nv_bfloat16*, float*>;
+  return cfg.stream ? L::template run<bn_bwd_fused_kernel<W, true>>(cfg, C, st, args...)
+                    : L::template run<bn_bwd_fused_kernel<W, false>>(cfg, C, st, args...);
 }
 
 }  // namespace bnf
@@ -532,7 +646,8 @@ using mgx::bnf::Cfg;
 
 extern "C" int mgx_bn_fused_ok(int64_t M, int64_t C, int backward, int* ok) {
   MGX_REQUIRE(ok && M > 0 && C > 0, "mgx_bn_fused_ok: bad arguments");
-  *ok = mgx::bnf::pick(M, C, backward ? 2 : 1).W != 0;
+  const Cfg c = mgx::bnf::pick(M, C, backward ? 2 : 1);
+  *ok = c.W == 0 ? 0 : (c.stream ? 2 : 1);
   return MGX_OK;
 }
 

@@ -328,11 +328,16 @@ def test_batchnorm_backward_with_fused_relu(cuda, m, c, fix_gamma):
 
 
 @pytest.mark.parametrize("m,c", [(12544, 96), (3136, 1024), (23328, 64), (1001, 48), (97, 16),
-                                 (12544, 576)])
+                                 (12544, 576),
+                                 # streaming variant (rows read twice from
+                                 # global memory): 4- and 2-vector slices,
+                                 # clusters of 16 and 8, ragged row split
+                                 (46656, 64), (46656, 96), (40001, 136), (32768, 32)])
 @pytest.mark.parametrize("fix_gamma,relu", [(True, True), (False, False), (False, True)])
 def test_batchnorm_cluster_fused(cuda, m, c, fix_gamma, relu):
     """The cluster-fused BatchNorm passes (one kernel per pass, rows staged
-    on-chip, DSMEM reduction) against the float64 oracle, and against the
+    on-chip or -- from 32768 rows -- streamed twice through L2, DSMEM
+    reduction) against the float64 oracle, and against the
     unfused statistics kernel for the values the backward consumes."""
     torch = cuda
     from paper_1512_01274_b200 import _lib as L

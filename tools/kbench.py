@@ -78,7 +78,8 @@ def bench_pool(torch, L):
         print(f"pool_bwd {kind} {shape} k{k}s{s}: {us_b:8.1f} us  {bb / us_b / 1e3:7.0f} GB/s")
 
 
-BNS = [(802816, 64), (193600, 192), (46656, 256), (12544, 576), (3136, 1024)]
+BNS = [(802816, 64), (193600, 192), (193600, 64), (46656, 32), (46656, 64), (46656, 96),
+       (46656, 256), (12544, 576), (3136, 1024)]
 
 
 def bench_bn(torch, L):
@@ -120,7 +121,8 @@ def bench_bn(torch, L):
             print(f"{name:14s} ({m}, {c}): {us:8.1f} us  {nb / us / 1e3:7.0f} GB/s")
 
 
-BNF = [(12544, 160), (12544, 576), (46656, 64), (46656, 256), (3136, 352), (3136, 1024)]
+BNF = [(12544, 160), (12544, 576), (193600, 64), (46656, 32), (46656, 64), (46656, 96),
+       (46656, 256), (3136, 352), (3136, 1024)]
 
 
 def bench_bn_fused(torch, L):
