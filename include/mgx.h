@@ -160,19 +160,6 @@ int mgx_gemm_bf16_conv(int mode, const void* src, const int64_t* geom, const voi
                        int64_t ldop, const float* bias, float* C, int64_t ldc, int64_t M,
                        int64_t N, int64_t K, int act, int splits, float* workspace,
                        float* colstats, uintptr_t stream);
-/* The same two GEMMs with an accumulator: C = acc + act(result (+bias)),
- * acc [M, N] with C's row pitch ldc (NULL: none; may be C itself) -- an
- * ElementwiseAdd fused into the producer of one of its operands (the
- * executor's gradient fan-in sums: replaces reference symbol.py:254-258's
- * ElementwiseAdd nodes bitwise, fp32 a + b).  Excludes colstats. */
-int mgx_gemm_bf16_tc_acc(const void* A, int64_t lda, int a_mn, const void* B, int64_t ldb,
-                         int b_mn, const float* bias, float* C, int64_t ldc, int64_t M,
-                         int64_t N, int64_t K, int act, int splits, float* workspace,
-                         float* colstats, const float* acc, uintptr_t stream);
-int mgx_gemm_bf16_conv_acc(int mode, const void* src, const int64_t* geom, const void* op,
-                           int64_t ldop, const float* bias, float* C, int64_t ldc, int64_t M,
-                           int64_t N, int64_t K, int act, int splits, float* workspace,
-                           float* colstats, const float* acc, uintptr_t stream);
 /* colstats (optional, both GEMM entry points, one split, C pitch % 4 == 0):
  * the epilogue also writes, for every 32-row block b and column n of C, the
  * pair (mean, M2) of the block's valid rows as float2 colstats[b*N + n] --

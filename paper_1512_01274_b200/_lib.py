@@ -147,12 +147,6 @@ _SIGNATURES = {
     "mgx_gemm_bf16_tc_ex": ([c_vp, c_i64, ctypes.c_int, c_vp, c_i64, ctypes.c_int, c_vp, c_vp,
                              c_i64, c_i64, c_i64, c_i64, ctypes.c_int, ctypes.c_int, c_vp, c_vp,
                              c_uptr], ctypes.c_int),
-    "mgx_gemm_bf16_tc_acc": ([c_vp, c_i64, ctypes.c_int, c_vp, c_i64, ctypes.c_int, c_vp, c_vp,
-                              c_i64, c_i64, c_i64, c_i64, ctypes.c_int, ctypes.c_int, c_vp, c_vp,
-                              c_vp, c_uptr], ctypes.c_int),
-    "mgx_gemm_bf16_conv_acc": ([ctypes.c_int, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_i64,
-                                c_i64, c_i64, ctypes.c_int, ctypes.c_int, c_vp, c_vp, c_vp, c_uptr],
-                               ctypes.c_int),
     "mgx_gemm_bf16_conv": ([ctypes.c_int, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_i64, c_i64,
                             c_i64, ctypes.c_int, ctypes.c_int, c_vp, c_vp, c_uptr], ctypes.c_int),
     "mgx_bn_stats_from_tiles": ([c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_f32, c_f32, c_uptr],

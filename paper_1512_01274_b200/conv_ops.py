@@ -197,25 +197,6 @@ def _gemm_conv(mode: int, src: int, shape, k, s, p, op: int, ldop: int, out: int
                  [m, n, kdim, ldop, ldc, mode | (splits << 8), g1, g2], act=act)
 
 
-def dx_acc_ok(attrs) -> bool:
-    """Can this convolution's data gradient take an accumulator
-    (``ctx.dx_acc``)?  The 1x1 stride-1 ones (one plain GEMM)."""
-    k, s, p = _conv_params(attrs)
-    return _pointwise(k, s, p)
-
-
-def _with_acc(g: L.Instr, acc: Optional[int]) -> L.Instr:
-    """Mark a tensor-core GEMM instruction as accumulating: C = acc + result
-    (ptr 5 = acc; OP_GEMM_TC_EX dims[6] bit 2, OP_GEMM_CONV dims[5] bit 32)."""
-    if acc:
-        if g.op == L.OP_GEMM_TC_EX:
-            g.dims[6] |= 4
-        else:
-            g.dims[5] |= 1 << 32
-        g.ptr[5] = acc
-    return g
-
-
 def _conv_lower_fwd(ins, out, attrs):
     return conv_forward_instrs(ins, out, attrs)
 
@@ -305,16 +286,13 @@ def _conv_lower_bwd(slot, env, out, attrs):
         code.append(_gemm(dyb, ldf, True, col, ldk, True, out.ptr, kk, f, kk, m,
                           splits=0 if ws else 1, ws=ws))
         return code
-    # dX (ctx.dx_acc: out = acc + dX, the executor's fused fan-in add)
-    acc = ctx.dx_acc
+    # dX
     dyb, ldf = _conv_dy(og, f, ctx, code)
     wb, ldk = _weights_bf16(w, ctx, code)
     if k == (1, 1) and s == (1, 1) and p == (0, 0):
         sp, ws = _auto_split(m, c, f, ctx)
-        code.append(_with_acc(_gemm(dyb, ldf, False, wb, ldk, True, out.ptr, c, m, c, f,
-                                    splits=sp, ws=ws), acc))
+        code.append(_gemm(dyb, ldf, False, wb, ldk, True, out.ptr, c, m, c, f, splits=sp, ws=ws))
         return code
-    assert acc is None, "an accumulating data gradient needs a 1x1 stride-1 convolution"
     if s == (1, 1) and p[0] < k[0] and p[1] < k[1]:
         # stride 1: dX = conv(dY, flipped W, pad k-1-p): implicit GEMM over
         # dY's bf16 copy when F % 8 == 0, else explicit im2col(dY)

@@ -280,14 +280,9 @@ static int run_instr(const mgx_instr& in, cudaStream_t st) {
                                a & 0xFFFF, (((w >> 40) & 0xFF) << 16) | ((w >> 32) & 0xFF),
                                (((w >> 24) & 0xFF) << 16) | ((w >> 16) & 0xFF),
                                (((w >> 8) & 0xFF) << 16) | (w & 0xFF)};
-      // d[5] bit 32: ptr5 is an accumulator (C = acc + result), else colstats
-      const bool acc = (d[5] >> 32) & 1;
-      return mgx_gemm_bf16_conv_acc(static_cast<int>(d[5] & 0xFF), in.ptr[0], geom, in.ptr[1],
-                                    d[3], p2, p3, d[4], d[0], d[1], d[2], in.act,
-                                    static_cast<int>((d[5] >> 8) & 0xFFFFFF),
-                                    static_cast<float*>(in.ptr[4]),
-                                    acc ? nullptr : static_cast<float*>(in.ptr[5]),
-                                    acc ? static_cast<const float*>(in.ptr[5]) : nullptr, s);
+      return mgx_gemm_bf16_conv(static_cast<int>(d[5] & 0xFF), in.ptr[0], geom, in.ptr[1], d[3],
+                                p2, p3, d[4], d[0], d[1], d[2], in.act, static_cast<int>(d[5] >> 8),
+                                static_cast<float*>(in.ptr[4]), static_cast<float*>(in.ptr[5]), s);
     }
     case MGX_OP_BN_ACT_POOL: {
       // dims 0..6: pool geometry (input B, H, W, C; k, s, p), bit 40 of
@@ -348,17 +343,11 @@ static int run_instr(const mgx_instr& in, cudaStream_t st) {
                               reinterpret_cast<float*>(d[7]), s);
     case MGX_OP_WFLIP: return mgx_weight_flip_bf16(p0, d[0], d[1], d[2], d[3], in.ptr[1], d[4], s);
     case MGX_OP_COLSUM: return mgx_colsum(p0, d[0], d[1], in.ptr[1], p2, s);
-    case MGX_OP_GEMM_TC_EX: {
-      // d[6]: bit 0 A MN-major, bit 1 B MN-major, bit 2 ptr5 is an
-      // accumulator (C = acc + result), else colstats
-      const bool acc = (d[6] >> 2) & 1;
-      return mgx_gemm_bf16_tc_acc(in.ptr[0], d[3], static_cast<int>(d[6] & 1), in.ptr[1], d[4],
-                                  static_cast<int>((d[6] >> 1) & 1), p2, p3, d[5], d[0], d[1],
-                                  d[2], in.act, static_cast<int>(d[7]),
-                                  static_cast<float*>(in.ptr[4]),
-                                  acc ? nullptr : static_cast<float*>(in.ptr[5]),
-                                  acc ? static_cast<const float*>(in.ptr[5]) : nullptr, s);
-    }
+    case MGX_OP_GEMM_TC_EX:
+      return mgx_gemm_bf16_tc_ex(in.ptr[0], d[3], static_cast<int>(d[6] & 1), in.ptr[1], d[4],
+                                 static_cast<int>((d[6] >> 1) & 1), p2, p3, d[5], d[0], d[1], d[2],
+                                 in.act, static_cast<int>(d[7]), static_cast<float*>(in.ptr[4]),
+                                 static_cast<float*>(in.ptr[5]), s);
     default:
       set_error("program: unknown opcode %d", in.op);
       return MGX_BAD_ARGUMENT;

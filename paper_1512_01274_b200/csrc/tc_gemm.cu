@@ -251,7 +251,7 @@ tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
                     const __grid_constant__ CUtensorMap map_c, const float* __restrict__ bias,
                     float* __restrict__ C, int ldc, int M, int N, int act, Sched sc,
                     int64_t split_stride, int use_tma_store, const __grid_constant__ Gather ga,
-                    float2* __restrict__ colstats, const float* accum) {
+                    float2* __restrict__ colstats) {
   using G = Cfg<BN>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -577,30 +577,6 @@ tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = act_forward(act, v[j]);
         }
-        if (accum != nullptr) {
-          // C = accum + result (an ElementwiseAdd fused into the producer of
-          // its second operand; acc may alias C: each element is read by
-          // the thread that writes it, before the write)
-          const int row = row0 + lane;
-          const int nb = n0 + c0;
-          if (row < M) {
-            const float* arow = accum + int64_t(row) * ldc + nb;
-            if (nb + 32 <= N && ((ldc | nb) & 3) == 0) {
-#pragma unroll
-              for (int j = 0; j < 8; ++j) {
-                const float4 a4 = __ldcg(reinterpret_cast<const float4*>(arow) + j);
-                v[4 * j] = fadd(a4.x, v[4 * j]);
-                v[4 * j + 1] = fadd(a4.y, v[4 * j + 1]);
-                v[4 * j + 2] = fadd(a4.z, v[4 * j + 2]);
-                v[4 * j + 3] = fadd(a4.w, v[4 * j + 3]);
-              }
-            } else {
-#pragma unroll
-              for (int j = 0; j < 32; ++j)
-                if (nb + j < N) v[j] = fadd(__ldcg(arow + j), v[j]);
-            }
-          }
-        }
         if (use_tma_store) {
           if (row0 >= M) continue;  // warp-uniform: nothing of this box is in C
           uint8_t* buf = cbuf + nbuf * kStageCBytes;
@@ -674,9 +650,8 @@ tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
 // Split-K epilogue: C[m, n] = act(sum_z ws[z][m, n] (+ bias[n])), partial
 // tiles summed in ascending split order (deterministic).
 __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, int64_t split_stride,
-                                     const float* __restrict__ bias, float* C,
-                                     int64_t ldc, int64_t M, int64_t N, int act,
-                                     const float* acc) {
+                                     const float* __restrict__ bias, float* __restrict__ C,
+                                     int64_t ldc, int64_t M, int64_t N, int act) {
   const int64_t total = M * N;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += stride) {
@@ -685,9 +660,7 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, i
     float v = ws[o];
     for (int z = 1; z < splits; ++z) v = fadd(v, ws[z * split_stride + o]);
     if (bias) v = fadd(v, __ldg(bias + n));
-    v = act_forward(act, v);
-    if (acc) v = fadd(acc[m * ldc + n], v);
-    C[m * ldc + n] = v;
+    C[m * ldc + n] = act_forward(act, v);
   }
 }
 
@@ -699,8 +672,8 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, i
 // block, so a tall split count over a small output is not a serial chain.
 __global__ void __launch_bounds__(256)
 splitk_reduce4_kernel(const float4* __restrict__ ws, int splits, int64_t split_stride4,
-                      const float* __restrict__ bias, float4* C, int64_t ldc4,
-                      int64_t M, int64_t N4, int act, int SL, const float4* accum) {
+                      const float* __restrict__ bias, float4* __restrict__ C, int64_t ldc4,
+                      int64_t M, int64_t N4, int act, int SL) {
   __shared__ float4 part[256];
   const int VB = blockDim.x / SL;
   const int lane = threadIdx.x / VB, v = threadIdx.x - (threadIdx.x / VB) * VB;
@@ -754,13 +727,6 @@ splitk_reduce4_kernel(const float4* __restrict__ ws, int splits, int64_t split_s
       t.y = act_forward(act, t.y);
       t.z = act_forward(act, t.z);
       t.w = act_forward(act, t.w);
-      if (accum) {
-        const float4 a = accum[m * ldc4 + n4];
-        t.x = fadd(a.x, t.x);
-        t.y = fadd(a.y, t.y);
-        t.z = fadd(a.z, t.z);
-        t.w = fadd(a.w, t.w);
-      }
       C[m * ldc4 + n4] = t;
     }
     __syncthreads();
@@ -919,7 +885,7 @@ template <bool A_MN, bool B_MN, int BN, int ACTK, int GM>
 static int launch_act(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
                       int grid, const float* bias, float* C, int ldc, int M, int N, int act,
                       const Sched& sc, int64_t split_stride, int tma_store, const Gather& ga,
-                      float2* colstats, const float* acc, cudaStream_t st) {
+                      float2* colstats, cudaStream_t st) {
   using G = Cfg<BN>;
   static bool configured = false;
   if (!configured) {
@@ -928,7 +894,7 @@ static int launch_act(const CUtensorMap& ma, const CUtensorMap& mb, const CUtens
     configured = true;
   }
   tc_gemm_bf16_kernel<A_MN, B_MN, BN, ACTK, GM><<<grid, threads_for<GM>(), G::kSmemBytes, st>>>(
-      ma, mb, mc, bias, C, ldc, M, N, act, sc, split_stride, tma_store, ga, colstats, acc);
+      ma, mb, mc, bias, C, ldc, M, N, act, sc, split_stride, tma_store, ga, colstats);
   MGX_LAUNCHED();
   return MGX_OK;
 }
@@ -944,19 +910,18 @@ struct Launch {
   int tma;
   Gather ga;
   float2* colstats;
-  const float* acc;
 };
 
 template <bool A_MN, bool B_MN, int BN, int GM>
 static int launch_acts(const Launch& l, cudaStream_t st) {
   if (l.act == MGX_ACT_NONE)
     return launch_act<A_MN, B_MN, BN, 0, GM>(l.ma, l.mb, l.mc, l.grid, l.bias, l.C, l.ldc, l.M, l.N,
-                                             l.act, l.sc, l.sstride, l.tma, l.ga, l.colstats, l.acc, st);
+                                             l.act, l.sc, l.sstride, l.tma, l.ga, l.colstats, st);
   if (l.act == MGX_ACT_RELU)
     return launch_act<A_MN, B_MN, BN, 1, GM>(l.ma, l.mb, l.mc, l.grid, l.bias, l.C, l.ldc, l.M, l.N,
-                                             l.act, l.sc, l.sstride, l.tma, l.ga, l.colstats, l.acc, st);
+                                             l.act, l.sc, l.sstride, l.tma, l.ga, l.colstats, st);
   return launch_act<A_MN, B_MN, BN, 2, GM>(l.ma, l.mb, l.mc, l.grid, l.bias, l.C, l.ldc, l.M, l.N,
-                                           l.act, l.sc, l.sstride, l.tma, l.ga, l.colstats, l.acc, st);
+                                           l.act, l.sc, l.sstride, l.tma, l.ga, l.colstats, st);
 }
 
 template <int BN>
@@ -1024,7 +989,7 @@ namespace tc {
 static int gemm_impl(const void* A, int64_t lda, int a_mn, const void* B, int64_t ldb, int b_mn,
                      const float* bias, float* C, int64_t ldc, int64_t M, int64_t N, int64_t K,
                      int act, int splits, float* workspace, int gm, const Gather& ga,
-                     float* colstats, const float* acc, cudaStream_t st) {
+                     float* colstats, cudaStream_t st) {
   MGX_REQUIRE(C && M > 0 && N > 0 && K > 0, "mgx_gemm_bf16_tc: bad arguments");
   const bool a_impl = gm == 1 || gm == 3;  // A gathered / by TMA im2col
   MGX_REQUIRE((a_impl || A) && (gm == 2 || B), "mgx_gemm_bf16_tc: missing operand");
@@ -1082,7 +1047,6 @@ static int gemm_impl(const void* A, int64_t lda, int a_mn, const void* B, int64_
   l.N = static_cast<int>(N);
   l.ga = ga;
   l.colstats = reinterpret_cast<float2*>(colstats);
-  l.acc = splits == 1 ? acc : nullptr;  // split-K: added by the reduce pass
   MGX_REQUIRE(!colstats || (splits == 1 && l.tma && mgx::aligned16(colstats)),
               "mgx_gemm_bf16_tc: column statistics need one split and a 16-byte aligned C pitch");
   int rc = bn == 64    ? launch_bn<64>(a_mn, b_mn, gm, l, st)
@@ -1091,8 +1055,7 @@ static int gemm_impl(const void* A, int64_t lda, int a_mn, const void* B, int64_
                        : launch_bn<256>(a_mn, b_mn, gm, l, st);
   if (rc != MGX_OK || splits == 1) return rc;
   if (N % 4 == 0 && ldc % 4 == 0 && l.sstride % 4 == 0 && mgx::aligned16(C) &&
-      mgx::aligned16(workspace) && (!bias || mgx::aligned16(bias)) &&
-      (!acc || mgx::aligned16(acc))) {
+      mgx::aligned16(workspace) && (!bias || mgx::aligned16(bias))) {
     // split lanes: enough to put ~4 split loads per thread in flight
     int SL = 1;
     while (SL < 32 && SL * 4 < splits) SL *= 2;
@@ -1101,16 +1064,14 @@ static int gemm_impl(const void* A, int64_t lda, int a_mn, const void* B, int64_
     if (blocks > 148 * 8) blocks = 148 * 8;
     splitk_reduce4_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(
         reinterpret_cast<const float4*>(workspace), splits, l.sstride / 4, bias,
-        reinterpret_cast<float4*>(C), ldc / 4, M, N / 4, act, SL,
-        reinterpret_cast<const float4*>(acc));
+        reinterpret_cast<float4*>(C), ldc / 4, M, N / 4, act, SL);
     MGX_LAUNCHED();
     return MGX_OK;
   }
   int64_t blocks = mgx::ceil_div(M * N, 256);
   if (blocks > 148 * 8) blocks = 148 * 8;
   splitk_reduce_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(workspace, splits, l.sstride,
-                                                                      bias, C, ldc, M, N, act,
-                                                                      acc);
+                                                                      bias, C, ldc, M, N, act);
   MGX_LAUNCHED();
   return MGX_OK;
 }
@@ -1118,41 +1079,21 @@ static int gemm_impl(const void* A, int64_t lda, int a_mn, const void* B, int64_
 }  // namespace tc
 }  // namespace mgx
 
-extern "C" int mgx_gemm_bf16_tc_acc(const void* A, int64_t lda, int a_mn, const void* B,
-                                    int64_t ldb, int b_mn, const float* bias, float* C,
-                                    int64_t ldc, int64_t M, int64_t N, int64_t K, int act,
-                                    int splits, float* workspace, float* colstats,
-                                    const float* acc, uintptr_t stream) {
-  mgx::tc::Gather none;
-  std::memset(&none, 0, sizeof(none));
-  MGX_REQUIRE(!acc || !colstats, "mgx_gemm_bf16_tc_acc: acc and column statistics exclude each other");
-  return mgx::tc::gemm_impl(A, lda, a_mn, B, ldb, b_mn, bias, C, ldc, M, N, K, act, splits,
-                            workspace, 0, none, colstats, acc, mgx::as_stream(stream));
-}
-
 extern "C" int mgx_gemm_bf16_tc_ex(const void* A, int64_t lda, int a_mn, const void* B,
                                    int64_t ldb, int b_mn, const float* bias, float* C, int64_t ldc,
                                    int64_t M, int64_t N, int64_t K, int act, int splits,
                                    float* workspace, float* colstats, uintptr_t stream) {
-  return mgx_gemm_bf16_tc_acc(A, lda, a_mn, B, ldb, b_mn, bias, C, ldc, M, N, K, act, splits,
-                              workspace, colstats, nullptr, stream);
+  mgx::tc::Gather none;
+  std::memset(&none, 0, sizeof(none));
+  return mgx::tc::gemm_impl(A, lda, a_mn, B, ldb, b_mn, bias, C, ldc, M, N, K, act, splits,
+                            workspace, 0, none, colstats, mgx::as_stream(stream));
 }
 
 extern "C" int mgx_gemm_bf16_conv(int mode, const void* src, const int64_t* geom, const void* op,
                                   int64_t ldop, const float* bias, float* C, int64_t ldc,
                                   int64_t M, int64_t N, int64_t K, int act, int splits,
                                   float* workspace, float* colstats, uintptr_t stream) {
-  return mgx_gemm_bf16_conv_acc(mode, src, geom, op, ldop, bias, C, ldc, M, N, K, act, splits,
-                                workspace, colstats, nullptr, stream);
-}
-
-extern "C" int mgx_gemm_bf16_conv_acc(int mode, const void* src, const int64_t* geom,
-                                      const void* op, int64_t ldop, const float* bias, float* C,
-                                      int64_t ldc, int64_t M, int64_t N, int64_t K, int act,
-                                      int splits, float* workspace, float* colstats,
-                                      const float* acc, uintptr_t stream) {
   using namespace mgx::tc;
-  MGX_REQUIRE(!acc || !colstats, "mgx_gemm_bf16_conv_acc: acc and column statistics exclude each other");
   MGX_REQUIRE(src && geom && op && (mode >= 1 && mode <= 3), "mgx_gemm_bf16_conv: bad arguments");
   MGX_REQUIRE(mgx::aligned16(src), "mgx_gemm_bf16_conv: source not 16-byte aligned");
   Gather ga;
@@ -1195,7 +1136,7 @@ extern "C" int mgx_gemm_bf16_conv_acc(int mode, const void* src, const int64_t* 
     ga.mul_c = fastdiv_mul(F);
     ga.mul_kw = fastdiv_mul(ga.kw);
     return gemm_impl(nullptr, 0, 0, op, ldop, 0, bias, C, ldc, M, N, K, act, splits, workspace, 1,
-                     ga, colstats, acc, mgx::as_stream(stream));
+                     ga, colstats, mgx::as_stream(stream));
   }
   MGX_REQUIRE(ga.C % 8 == 0 && ga.C > 0 && ga.Ho > 0 && ga.Wo > 0 && ga.B > 0,
               "mgx_gemm_bf16_conv: the gathered tensor needs C %% 8 == 0");
@@ -1218,12 +1159,12 @@ extern "C" int mgx_gemm_bf16_conv_acc(int mode, const void* src, const int64_t* 
                          ga.kh - 1 - ga.ph <= 128 && ga.kw - 1 - ga.pw <= 128 && ga.sh <= 8 &&
                          ga.sw <= 8;
     return gemm_impl(nullptr, 0, 0, op, ldop, 0, bias, C, ldc, M, N, K, act, splits, workspace,
-                     use_tma ? 3 : 1, ga, colstats, acc, mgx::as_stream(stream));
+                     use_tma ? 3 : 1, ga, colstats, mgx::as_stream(stream));
   }
   // C[M, kconv] = op[pixels, M]^T (MN-major) . gather(src)[pixels, kconv]
   MGX_REQUIRE(K == pixels && N == kconv, "mgx_gemm_bf16_conv: N/K do not match the geometry");
   return gemm_impl(op, ldop, 1, nullptr, 0, 1, bias, C, ldc, M, N, K, act, splits, workspace, 2,
-                   ga, colstats, acc, mgx::as_stream(stream));
+                   ga, colstats, mgx::as_stream(stream));
 }
 
 extern "C" int mgx_gemm_bf16_tc(const void* A, int64_t lda, const void* B, int64_t ldb,

@@ -135,10 +135,9 @@ def instr_cost(ins: L.Instr) -> tuple:
     if op == L.OP_GEMM_TC:
         m, n, k = d[0], d[1], d[2]
         return 2 * (m * k + n * k) + 4 * m * n + (4 * n if has[2] else 0), 2 * m * n * k
-    if op == L.OP_GEMM_TC_EX:  # (+ the accumulator read when dims[6] bit 2)
+    if op == L.OP_GEMM_TC_EX:
         m, n, k = d[0], d[1], d[2]
-        return (2 * (m * k + n * k) + 4 * m * n + (4 * n if has[2] else 0)
-                + (4 * m * n if (d[6] >> 2) & 1 else 0)), 2 * m * n * k
+        return 2 * (m * k + n * k) + 4 * m * n + (4 * n if has[2] else 0), 2 * m * n * k
     if op == L.OP_GEMM_CONV:  # implicit GEMM: the gathered source counted once
         m, n, k = d[0], d[1], d[2]
         a, w = d[6], d[7]
@@ -148,8 +147,7 @@ def instr_cost(ins: L.Instr) -> tuple:
         # mode 3 (stride-2 data gradient over the dilated dY): 3 of 4 taps
         # multiply inserted zeros -- the algorithmic work is a quarter
         flops = 2 * m * n * k // (4 if mode == 3 else 1)
-        return (src + opb + 4 * m * n + (4 * n if has[2] else 0)
-                + (4 * m * n if (d[5] >> 32) & 1 else 0)), flops
+        return src + opb + 4 * m * n + (4 * n if has[2] else 0), flops
     if op == L.OP_IM2COL:  # reads the input once, writes the bf16 col matrix
         b, h, w, c = d[0], d[1], d[2], d[3]
         kh, kw, sh, sw, ph, pw = d[4] >> 16, d[4] & 0xFFFF, d[5] >> 16, d[5] & 0xFFFF, d[6] >> 16, d[6] & 0xFFFF
@@ -252,9 +250,6 @@ class LowerCtx:
         self.want_shadow: set = set()
         self.out_node = None
         self.pre: list = []
-        # a convolution data gradient lowered with an accumulator (C = acc +
-        # dX: an ElementwiseAdd fused into it by the executor), or None
-        self.dx_acc: Optional[int] = None
 
     def begin_op(self, node) -> None:
         self.node = node

@@ -63,34 +63,6 @@ def test_gemm_operand_majors(cuda, a_mn, b_mn, m, n, k):
     torch.testing.assert_close(c.double(), ref, rtol=1e-4, atol=1e-3 * max(1.0, (k / 64) ** 0.5))
 
 
-@pytest.mark.parametrize("m,n,k,splits", [(300, 96, 64, 1), (4096, 256, 192, 1),
-                                          (1000, 72, 640, 0), (3136, 192, 1024, 0),
-                                          (130, 36, 64, 1)])
-@pytest.mark.parametrize("inplace", [False, True])
-def test_gemm_accumulator_epilogue(cuda, m, n, k, splits, inplace):
-    """C = acc + A.B^T (the executor's gradient fan-in add fused into a
-    data-gradient GEMM): bitwise equal to the GEMM alone followed by an fp32
-    add, with and without split-K, and with acc aliasing C (in place)."""
-    torch = cuda
-    from paper_1512_01274_b200 import _lib as L
-    g = torch.Generator(device="cuda").manual_seed(m + n + k)
-    pad = lambda v: -(-v // 8) * 8  # noqa: E731
-    a = torch.zeros(m, pad(k), dtype=torch.bfloat16, device="cuda")
-    a[:, :k] = torch.randn(m, k, device="cuda", generator=g).to(torch.bfloat16)
-    b = torch.randn(k, pad(n), device="cuda", generator=g).to(torch.bfloat16)  # MN-major
-    acc = torch.randn(m, n, device="cuda", generator=g)
-    ws = torch.empty(64 * m * n + 1, device="cuda")
-    plain = torch.full((m, n), float("nan"), device="cuda")
-    L.call("mgx_gemm_bf16_tc_ex", a.data_ptr(), pad(k), 0, b.data_ptr(), pad(n), 1, None,
-           plain.data_ptr(), n, m, n, k, 0, splits, ws.data_ptr(), None, 0)
-    out = acc.clone() if inplace else torch.full((m, n), float("nan"), device="cuda")
-    L.call("mgx_gemm_bf16_tc_acc", a.data_ptr(), pad(k), 0, b.data_ptr(), pad(n), 1, None,
-           out.data_ptr(), n, m, n, k, 0, splits, ws.data_ptr(), None,
-           (out if inplace else acc).data_ptr(), 0)
-    torch.cuda.synchronize()
-    assert torch.equal(out, acc + plain)
-
-
 CONV_CASES = [
     # (B, H, W, C, F, k, s, p)
     (2, 8, 8, 16, 24, (1, 1), (1, 1), (0, 0)),
@@ -372,7 +344,7 @@ def test_batchnorm_cluster_fused(cuda, m, c, fix_gamma, relu):
     import ctypes
     ok = ctypes.c_int()
     L.call("mgx_bn_fused_ok", m, c, 1, ctypes.byref(ok))
-    assert ok.value == 1
+    assert ok.value == (2 if m >= 32768 else 1)  # 2: the streaming variant
     L.call("mgx_bn_fused_ok", m, 12, 1, ctypes.byref(ok))
     assert ok.value == 0  # C % 8 != 0: the unfused kernels
     g = torch.Generator().manual_seed(m + 3 * c)
