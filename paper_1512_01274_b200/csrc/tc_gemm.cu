@@ -43,7 +43,7 @@ namespace tc {
 
 constexpr int BM = 128, BK = 64, UMMA_K = 16;
 constexpr int kThreads = 192;
-constexpr int kEpiWarps = 4;
+constexpr int kStageBoxes = 8;  // epilogue staging boxes: 2 per warp (4 warps) or 1 (8)
 constexpr int kMnChunkBytes = BK * 128;  // one MN-major TMA box: 64 K rows x 128 B
 constexpr int kStageCBytes = 32 * 32 * 4;  // one epilogue staging box (32 x 32 fp32)
 
@@ -58,7 +58,7 @@ struct Cfg {
   // double-buffered accumulator, rounded up to a power of two columns
   static constexpr int kTmemCols = 2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512);
   static constexpr int kSmemBytes =
-      1024 + kStages * kStageBytes + kEpiWarps * 2 * kStageCBytes + 256;
+      1024 + kStages * kStageBytes + kStageBoxes * kStageCBytes + 256;
 };
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
@@ -223,9 +223,12 @@ template <int GM>
 constexpr bool gathered() {
   return GM == 1 || GM == 2;
 }
-template <int GM>
+// block: TMA producer warp, MMA warp, EPI epilogue warps (4, or 8 with the
+// columns of a tile split between two warps per TMEM lane quadrant), then
+// the gather warps of the implicit modes (EPI 4 there)
+template <int GM, int EPI>
 constexpr int threads_for() {
-  return gathered<GM>() ? kThreads + kGatherThreads : kThreads;
+  return 64 + 32 * EPI + (gathered<GM>() ? kGatherThreads : 0);
 }
 
 // in-place warp reduce-scatter of 32 per-lane values: afterwards a[0] in
@@ -244,8 +247,8 @@ __device__ __forceinline__ void warp_reduce_scatter32(float (&a)[32], int lane) 
 }
 
 // ACTK: 0 no activation, 1 relu, 2 any (runtime code; cold path)
-template <bool A_MN, bool B_MN, int BN, int ACTK, int GM>
-__global__ void __launch_bounds__(threads_for<GM>(), 1)
+template <bool A_MN, bool B_MN, int BN, int ACTK, int GM, int EPI>
+__global__ void __launch_bounds__(threads_for<GM, EPI>(), 1)
 tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
                     const __grid_constant__ CUtensorMap map_b,
                     const __grid_constant__ CUtensorMap map_c, const float* __restrict__ bias,
@@ -253,10 +256,11 @@ tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
                     int64_t split_stride, int use_tma_store, const __grid_constant__ Gather ga,
                     float2* __restrict__ colstats) {
   using G = Cfg<BN>;
+  static_assert(EPI == 4 || (EPI == 8 && !gathered<GM>()), "8 epilogue warps: TMA-fed modes only");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* stage_c = smem + G::kStages * G::kStageBytes;  // [4 warps][2 bufs][4 KB]
-  uint64_t* full = reinterpret_cast<uint64_t*>(stage_c + kEpiWarps * 2 * kStageCBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(stage_c + kStageBoxes * kStageCBytes);
   uint64_t* empty = full + G::kStages;
   uint64_t* tfull = empty + G::kStages;   // [2]
   uint64_t* tempty = tfull + 2;           // [2]
@@ -275,7 +279,7 @@ tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], kEpiWarps);
+      mbar_init(&tempty[a], EPI);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -376,11 +380,11 @@ tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
         umma_commit(&tfull[acc]);
       }
     }
-  } else if (gathered<GM>() && warp >= 6) {
+  } else if (gathered<GM>() && warp >= 2 + EPI) {
     // ---------------- gather producers (implicit GEMM): cp.async 16-byte
     // chunks straight into the 128B-swizzled operand tile, zero-filled
     // outside the input; the mbarrier arrival fires when they land
-    const int g = threadIdx.x - kThreads;
+    const int g = threadIdx.x - (64 + 32 * EPI);
     int it = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
       int m0, nt, z, kb0, nkb;
@@ -514,10 +518,14 @@ tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
   } else if (warp >= 2) {
-    // ---------------- epilogue warps: TMEM lanes 32*(warp%4) .. +31
+    // ---------------- epilogue warps: TMEM lanes 32*(warp%4) .. +31; with
+    // 8 warps, warp ew takes the 32-column chunks h, h+2, ... (h = ew / 4)
+    // and stages through one 4 KB box instead of two
+    constexpr int NB = 8 / EPI;           // staging boxes per warp
+    constexpr int CSTEP = 32 * (EPI / 4);  // column step between a warp's chunks
     const int ew = warp - 2;
     const int lane_base = (warp & 3) * 32;
-    uint8_t* cbuf = stage_c + ew * 2 * kStageCBytes;
+    uint8_t* cbuf = stage_c + ew * NB * kStageCBytes;
     int local = 0, nbuf = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++local) {
       int m0, nt, z, kb0, nkb;
@@ -529,7 +537,7 @@ tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
       mbar_wait_sleep(&tfull[acc], aph);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int row0 = m0 + lane_base;
-      for (int c0 = 0; c0 < BN; c0 += 32) {
+      for (int c0 = 32 * (ew / 4); c0 < BN; c0 += CSTEP) {
         uint32_t r[32];
         const uint32_t taddr = tmem + (uint32_t(lane_base) << 16) + uint32_t(acc * BN + c0);
         asm volatile(
@@ -543,7 +551,7 @@ tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
               "=r"(r[31])
             : "r"(taddr));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (c0 + 32 >= BN) {
+        if (c0 + CSTEP >= BN) {
           // all of this accumulator is in registers: hand TMEM back early
           asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
           __syncwarp();
@@ -580,8 +588,13 @@ tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
         if (use_tma_store) {
           if (row0 >= M) continue;  // warp-uniform: nothing of this box is in C
           uint8_t* buf = cbuf + nbuf * kStageCBytes;
-          // the store that last read this buffer (two chunks ago) is done
-          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          // the store that last read this buffer (NB chunks ago) is done
+          if (lane == 0) {
+            if (NB == 2)
+              asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            else
+              asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          }
           __syncwarp();
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
@@ -622,7 +635,7 @@ tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
             const float m2 = fmaxf(s2 - s1 * dm, 0.0f);
             if (col < N) colstats[int64_t(row0 >> 5) * N + col] = make_float2(x0 + dm, m2);
           }
-          nbuf ^= 1;
+          if (NB == 2) nbuf ^= 1;
         } else {
           const int row = row0 + lane;
           if (row < M) {
@@ -881,22 +894,43 @@ static int make_map(CUtensorMap* map, const void* base, int64_t rows, int64_t K,
   return encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, base, rows, K, ld * 2, 64, BK);
 }
 
-template <bool A_MN, bool B_MN, int BN, int ACTK, int GM>
-static int launch_act(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
+template <bool A_MN, bool B_MN, int BN, int ACTK, int GM, int EPI>
+static int launch_epi(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
                       int grid, const float* bias, float* C, int ldc, int M, int N, int act,
                       const Sched& sc, int64_t split_stride, int tma_store, const Gather& ga,
                       float2* colstats, cudaStream_t st) {
   using G = Cfg<BN>;
   static bool configured = false;
   if (!configured) {
-    MGX_CUDA(cudaFuncSetAttribute(tc_gemm_bf16_kernel<A_MN, B_MN, BN, ACTK, GM>,
+    MGX_CUDA(cudaFuncSetAttribute(tc_gemm_bf16_kernel<A_MN, B_MN, BN, ACTK, GM, EPI>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, G::kSmemBytes));
     configured = true;
   }
-  tc_gemm_bf16_kernel<A_MN, B_MN, BN, ACTK, GM><<<grid, threads_for<GM>(), G::kSmemBytes, st>>>(
-      ma, mb, mc, bias, C, ldc, M, N, act, sc, split_stride, tma_store, ga, colstats);
+  tc_gemm_bf16_kernel<A_MN, B_MN, BN, ACTK, GM, EPI>
+      <<<grid, threads_for<GM, EPI>(), G::kSmemBytes, st>>>(
+          ma, mb, mc, bias, C, ldc, M, N, act, sc, split_stride, tma_store, ga, colstats);
   MGX_LAUNCHED();
   return MGX_OK;
+}
+
+// 8 epilogue warps for the TMA-fed modes (env MGX_GEMM_EPI=4: four)
+template <bool A_MN, bool B_MN, int BN, int ACTK, int GM>
+static int launch_act(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
+                      int grid, const float* bias, float* C, int ldc, int M, int N, int act,
+                      const Sched& sc, int64_t split_stride, int tma_store, const Gather& ga,
+                      float2* colstats, cudaStream_t st) {
+  static const bool epi8 = [] {
+    const char* v = getenv("MGX_GEMM_EPI");
+    return !(v && atoi(v) == 4);
+  }();
+  if constexpr (!gathered<GM>()) {
+    if (epi8)
+      return launch_epi<A_MN, B_MN, BN, ACTK, GM, 8>(ma, mb, mc, grid, bias, C, ldc, M, N, act,
+                                                     sc, split_stride, tma_store, ga, colstats,
+                                                     st);
+  }
+  return launch_epi<A_MN, B_MN, BN, ACTK, GM, 4>(ma, mb, mc, grid, bias, C, ldc, M, N, act, sc,
+                                                 split_stride, tma_store, ga, colstats, st);
 }
 
 struct Launch {
