@@ -87,6 +87,12 @@ __device__ __forceinline__ float act_backward(int act, float y, float og) {
 
 constexpr int kNumSMs = 148;
 
+// CTA cap for the tensor-core GEMMs launched by this host thread (0: none):
+// the multi-lane program runner sets it for the instructions OFF the
+// critical lane, so their persistent grids leave SMs to the critical path
+// (tc_gemm.cu; runtime.cu run_range).
+void set_gemm_cta_cap(int cap);
+
 // One leaf of numpy's pairwise-summation split tree over n elements
 // (see dense.cu); `merges` = number of stack merges after this leaf.
 struct PwLeaf {

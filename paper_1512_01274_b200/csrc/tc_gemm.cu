@@ -974,6 +974,10 @@ static int launch_bn(int a_mn, int b_mn, int gm, const Launch& l, cudaStream_t s
 // GEMM need not own the whole GPU), each split at least `min_kb` k-blocks
 // (env MGX_SPLIT_MINK, default 16: short splits are all prologue, epilogue
 // and workspace traffic) -- both measured best on Inception-BN
+static thread_local int t_cta_cap = 0;
+
+// (the split count never depends on t_cta_cap: results are the same on
+// every lane schedule, bitwise)
 static int auto_splits(int64_t tiles, int64_t nk) {
   static const int64_t target = [] {
     const char* v = getenv("MGX_SPLIT_TARGET");
@@ -1071,7 +1075,8 @@ static int gemm_impl(const void* A, int64_t lda, int a_mn, const void* B, int64_
     const int64_t c = v && *v ? atoi(v) : mgx::kNumSMs;
     return c < 1 ? 1 : (c > mgx::kNumSMs ? int64_t(mgx::kNumSMs) : c);
   }();
-  l.grid = static_cast<int>(total < max_ctas ? total : max_ctas);
+  const int64_t cap = t_cta_cap > 0 && t_cta_cap < max_ctas ? t_cta_cap : max_ctas;
+  l.grid = static_cast<int>(total < cap ? total : cap);
   l.sstride = M * N;
   l.bias = splits == 1 ? bias : nullptr;
   l.act = splits == 1 ? act : 0;
@@ -1111,6 +1116,9 @@ static int gemm_impl(const void* A, int64_t lda, int a_mn, const void* B, int64_
 }
 
 }  // namespace tc
+
+void set_gemm_cta_cap(int cap) { tc::t_cta_cap = cap < 0 ? 0 : cap; }
+
 }  // namespace mgx
 
 extern "C" int mgx_gemm_bf16_tc_ex(const void* A, int64_t lda, int a_mn, const void* B,
