@@ -51,9 +51,12 @@ CONFIGS = {
                     workload="config-4 AlexNet-style (5 conv, fc6 4096x9216, fc7, fc8; 62M params), "
                              "synthetic 224x224x3, batch 128 per GPU, kvstore device"),
     # strategy "inplace": no co-shared slots between independent branches
-    # (their reuse adds write-after-read edges across lanes: 5.24 -> 5.19 ms)
+    # (their reuse adds write-after-read edges across lanes: 5.24 -> 5.19 ms);
+    # split_target 32: split-K sized for ~32 CTAs per GEMM, the inception
+    # branches run side by side (4.83 -> 4.67 ms; a chain like AlexNet keeps
+    # the default 128)
     "inception_bn": dict(batch=64, image=(224, 224, 3), classes=1000, dense="bf16", dtype="bf16",
-                         strategy="inplace",
+                         strategy="inplace", split_target=32,
                          workload="config-5 Inception-BN (MXNet symbol, 69 conv+BN+ReLU, 10 "
                                   "inception concats), synthetic 224x224x3, batch 64 per GPU, bf16 "
                                   "tensor-core convs, momentum SGD, kvstore device"),
@@ -422,7 +425,8 @@ def run_config(name, args, world, rank, local, eng, steps, warmup, with_e2e=True
     given = {"data": (per,) + cfg["image"], "label": (per,)}
     shapes, _ = symbol.infer_shape(g, given)
     step = DataParallelStep(g, kv, given, init_params(g, shapes, 0), engine=eng,
-                            dense=cfg["dense"], strategy=cfg.get("strategy", "both"))
+                            dense=cfg["dense"], strategy=cfg.get("strategy", "both"),
+                            split_target=cfg.get("split_target", 0))
     kv.set_updater(make_sgd_updater(SGDConfig(ETA, MOM, WD), scale=world))
     w = step.workers[0]
     feats, labels = synthetic(name, per * world, 0)

@@ -172,6 +172,10 @@ int mgx_bn_stats_from_tiles(const void* part, int64_t M, int64_t C, float* stats
                             uintptr_t stream);
 /* Workspace (floats) the auto split-K choice needs for an M x N x K GEMM. */
 int mgx_gemm_splitk_workspace(int64_t M, int64_t N, int64_t K, int64_t* out_floats);
+/* The split-K plan for about `target` CTAs (0: the default): split count
+ * (1 = none; at most 128 k-blocks per split) and its workspace floats. */
+int mgx_gemm_split_plan(int64_t M, int64_t N, int64_t K, int32_t target, int32_t* splits,
+                        int64_t* out_floats);
 
 /* ------------------------------------------------ convolution-net kernels
  * geom = int64[7] {B, H, W, C, kh<<16|kw, sh<<16|sw, ph<<16|pw}. */

@@ -152,6 +152,8 @@ _SIGNATURES = {
     "mgx_bn_stats_from_tiles": ([c_vp, c_i64, c_i64, c_vp, c_vp, c_vp, c_f32, c_f32, c_uptr],
                                 ctypes.c_int),
     "mgx_gemm_splitk_workspace": ([c_i64, c_i64, c_i64, ctypes.POINTER(c_i64)], ctypes.c_int),
+    "mgx_gemm_split_plan": ([c_i64, c_i64, c_i64, c_i32, ctypes.POINTER(c_i32),
+                             ctypes.POINTER(c_i64)], ctypes.c_int),
     "mgx_im2col_bf16": ([c_vp, c_vp, c_vp, c_i64, c_uptr], ctypes.c_int),
     "mgx_col2im": ([c_vp, c_i64, c_vp, c_vp, c_uptr], ctypes.c_int),
     "mgx_weight_flip_bf16": ([c_vp, c_i64, c_i64, c_i64, c_i64, c_vp, c_i64, c_uptr], ctypes.c_int),

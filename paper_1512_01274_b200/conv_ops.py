@@ -109,21 +109,22 @@ def _gemm(a: int, lda: int, a_mn: bool, b: int, ldb: int, b_mn: bool, c: int, ld
                  act=act)
 
 
-def _splitk_ws(m: int, n: int, k: int) -> int:
-    import ctypes
-    out = ctypes.c_int64()
-    L.call("mgx_gemm_splitk_workspace", m, n, k, ctypes.byref(out))
-    return out.value
-
-
 def _auto_split(m: int, n: int, k: int, ctx):
-    """(splits, workspace) for a GEMM with fewer output tiles than SMs:
-    split-K over the K loop (deterministic in-order reduce) so every SM
-    works; (1, None) when the tiles already fill the GPU."""
-    nws = _splitk_ws(m, n, k)
-    if not nws:
+    """(splits, workspace) for a GEMM with fewer output tiles than the
+    bind's CTA target (``ctx.split_target``, 0: the library default):
+    split-K over the K loop (deterministic in-order reduce); (1, None) when
+    the tiles already suffice.  The count is fixed here, at lowering."""
+    return split_plan(m, n, k, ctx)
+
+
+def split_plan(m: int, n: int, k: int, ctx):
+    import ctypes
+    sp, nws = ctypes.c_int32(), ctypes.c_int64()
+    L.call("mgx_gemm_split_plan", m, n, k, int(getattr(ctx, "split_target", 0) or 0),
+           ctypes.byref(sp), ctypes.byref(nws))
+    if sp.value <= 1:
         return 1, None
-    return 0, ctx.scratch(4 * nws)
+    return sp.value, ctx.scratch(4 * nws.value)
 
 
 def _weights_bf16(w: View, ctx, code: list):
@@ -271,20 +272,19 @@ def _conv_lower_bwd(slot, env, out, attrs):
     if slot == 1:
         # dW[f, kk] = sum_m dY[m, f] col[m, kk]: both operands MN-major, split-K
         dyb, ldf = _conv_dy(og, f, ctx, code)
-        nws = _splitk_ws(f, kk, m)
-        ws = ctx.scratch(4 * nws) if nws else None
+        sp, ws = _auto_split(f, kk, m, ctx)
         if implicit:
             sh = _shadow(x, ctx.input_node("in0"), ctx, code)
             if _pointwise(k, s, p):  # dW = dY^T x over the bf16 copies, both by TMA
                 code.append(_gemm(dyb, ldf, True, sh, c, True, out.ptr, kk, f, kk, m,
-                                  splits=0 if ws else 1, ws=ws))
+                                  splits=sp, ws=ws))
                 return code
             code.append(_gemm_conv(2, sh, x.shape, k, s, p, dyb, ldf, out.ptr, kk, f, kk, m,
-                                   splits=0 if ws else 1, ws=ws))
+                                   splits=sp, ws=ws))
             return code
         col, _wb, (m, kk, ldk, *_r) = _conv_operands(x, w, attrs, ctx, code)
         code.append(_gemm(dyb, ldf, True, col, ldk, True, out.ptr, kk, f, kk, m,
-                          splits=0 if ws else 1, ws=ws))
+                          splits=sp, ws=ws))
         return code
     # dX
     dyb, ldf = _conv_dy(og, f, ctx, code)

@@ -969,17 +969,22 @@ static int launch_bn(int a_mn, int b_mn, int gm, const Launch& l, cudaStream_t s
   return launch_acts<true, true, BN, 0>(l, st);
 }
 
-// split-K count: fill about `target` CTAs (env MGX_SPLIT_TARGET, default
-// 128 of the 148 SMs: the graph runs independent branches concurrently, so a
-// GEMM need not own the whole GPU), each split at least `min_kb` k-blocks
-// (env MGX_SPLIT_MINK, default 16: short splits are all prologue, epilogue
-// and workspace traffic) -- both measured best on Inception-BN
 static thread_local int t_cta_cap = 0;
 
-// (the split count never depends on t_cta_cap: results are the same on
-// every lane schedule, bitwise)
-static int auto_splits(int64_t tiles, int64_t nk) {
-  static const int64_t target = [] {
+// split-K count: about `target` CTAs per GEMM (0: env MGX_SPLIT_TARGET,
+// default 128 -- a GEMM alone on the GPU fills it; the executor passes a
+// lower per-network target when independent branches run side by side:
+// Inception-BN A/B 128 -> 4.83, 64 -> 4.76, 32 -> 4.67, 16 -> 4.79
+// ms/step), each split at least `min_kb` k-blocks (env MGX_SPLIT_MINK,
+// default 16: short splits are all prologue, epilogue and workspace
+// traffic), and -- for accuracy -- at most kMaxKbPerSplit k-blocks per
+// split (fp32 accumulation runs of <= 8192 products, like the default
+// target gives the long-K weight gradients).  Never depends on t_cta_cap:
+// results are the same on every lane schedule, bitwise.
+constexpr int64_t kMaxKbPerSplit = 128;
+
+static int auto_splits(int64_t tiles, int64_t nk, int64_t target = 0) {
+  static const int64_t target_env = [] {
     const char* v = getenv("MGX_SPLIT_TARGET");
     return int64_t(v && *v ? atoi(v) : 128);
   }();
@@ -987,9 +992,14 @@ static int auto_splits(int64_t tiles, int64_t nk) {
     const char* v = getenv("MGX_SPLIT_MINK");
     return int64_t(v && *v ? atoi(v) : 16);
   }();
-  if (tiles >= target) return 1;
-  int64_t want = target / tiles, most = nk / min_kb;
-  int64_t s = want < most ? want : most;
+  if (target <= 0) target = target_env;
+  int64_t s = 1;
+  if (tiles < target) {
+    const int64_t want = target / tiles, most = nk / min_kb;
+    s = want < most ? want : most;
+  }
+  const int64_t floor_s = ceil_div(nk, kMaxKbPerSplit);
+  if (s < floor_s) s = floor_s;
   return static_cast<int>(s < 1 ? 1 : s);
 }
 
@@ -1216,18 +1226,26 @@ extern "C" int mgx_gemm_bf16_tc(const void* A, int64_t lda, const void* B, int64
                              stream);
 }
 
-extern "C" int mgx_gemm_splitk_workspace(int64_t M, int64_t N, int64_t K, int64_t* out_floats) {
+extern "C" int mgx_gemm_split_plan(int64_t M, int64_t N, int64_t K, int32_t target,
+                                   int32_t* splits_out, int64_t* out_floats) {
   using namespace mgx::tc;
-  MGX_REQUIRE(out_floats && M > 0 && N > 0 && K > 0, "mgx_gemm_splitk_workspace: bad arguments");
+  MGX_REQUIRE(splits_out && out_floats && M > 0 && N > 0 && K > 0,
+              "mgx_gemm_split_plan: bad arguments");
   const int64_t tiles = mgx::ceil_div(N, pick_bn(M, N)) * mgx::ceil_div(M, BM);
   const int64_t nk = mgx::ceil_div(K, BK);
-  int64_t splits = auto_splits(tiles, nk);
+  int64_t splits = auto_splits(tiles, nk, target);
   if (splits > 1) {
     const int64_t kps = mgx::ceil_div(nk, splits);
     splits = mgx::ceil_div(nk, kps);
   }
+  *splits_out = static_cast<int32_t>(splits);
   *out_floats = splits > 1 ? splits * M * N : 0;
   return MGX_OK;
+}
+
+extern "C" int mgx_gemm_splitk_workspace(int64_t M, int64_t N, int64_t K, int64_t* out_floats) {
+  int32_t splits = 1;
+  return mgx_gemm_split_plan(M, N, K, 0, &splits, out_floats);
 }
 
 extern "C" int mgx_cast_bf16_2d(const float* x, int64_t R, int64_t C, int64_t ldi, void* y,

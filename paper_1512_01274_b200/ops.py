@@ -250,6 +250,8 @@ class LowerCtx:
         self.want_shadow: set = set()
         self.out_node = None
         self.pre: list = []
+        # split-K CTA target of this bind's GEMMs (0: the library default)
+        self.split_target = 0
 
     def begin_op(self, node) -> None:
         self.node = node
@@ -554,12 +556,10 @@ def fc_dw_tc(og: View, x: View, dw: View, alloc=None) -> list:
     code = []
     ogb, ldo = _bf16_copy("fcog", "og", og, bsz, h, code)
     xb, ldx = _bf16_copy("fcx", "in0", x, bsz, f, code)
-    import ctypes
-    nws = ctypes.c_int64()
-    L.call("mgx_gemm_splitk_workspace", h, f, bsz, ctypes.byref(nws))
-    ws = current_ctx().scratch(4 * nws.value) if nws.value else None
+    from .conv_ops import split_plan
+    sp, ws = split_plan(h, f, bsz, current_ctx())
     code.append(_gemm_ex(ogb, ldo, True, xb, ldx, True, dw.ptr, f, h, f, bsz,
-                         splits=0 if ws else 1, ws=ws))
+                         splits=sp, ws=ws))
     return code
 
 

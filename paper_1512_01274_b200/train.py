@@ -151,7 +151,7 @@ class DataParallelStep:
     def __init__(self, g: SymbolGraph, kv: KVStore, shard_shapes: Dict[str, tuple],
                  params0: Dict[str, np.ndarray], strategy: str = "both",
                  engine: Optional[Engine] = None, use_graph: bool = True, dense: str = "fp32",
-                 overlap: Optional[bool] = None):
+                 overlap: Optional[bool] = None, split_target: int = 0):
         _check_graph(g)
         if overlap is None:  # env MGX_OVERLAP=0 turns it off (A/B measurements)
             import os
@@ -182,7 +182,8 @@ class DataParallelStep:
             for n in self.aux:
                 args[n] = tmod.from_host(arg_shapes[n], "float32", aux0[n], engine=self.engine)
             self.args[w], self.grads[w] = args, grads
-        self._bind_opts = dict(strategy=strategy, use_graph=use_graph, dense=dense)
+        self._bind_opts = dict(strategy=strategy, use_graph=use_graph, dense=dense,
+                               split_target=split_target)
         self._overlap = overlap
         self.embedded = False
         self._graph_exec = None

@@ -2,7 +2,7 @@
 
 bench.py (default ``--config inception_bn``) builds ``nets.inception_bn(1000)``
 at 224x224x3, batch 64 per GPU, ``dense="bf16"``, memory plan strategy
-"inplace", the default 6-lane schedule, wraps it in ``DataParallelStep`` over a device ``KVStore`` with the
+"inplace", split-K target 32, the default 6-lane schedule, wraps it in ``DataParallelStep`` over a device ``KVStore`` with the
 fused SGD updater (lr 0.05, momentum 0.9, wd 1e-4) and replays the whole step
 (forward, backward, KV round) from one CUDA graph.  These tests bind exactly
 that -- same graph, batch, dense mode, lanes, synthetic data and seeds -- so
@@ -49,6 +49,7 @@ PER = 64
 IMAGE = (224, 224, 3)
 CLASSES = 1000
 STRATEGY = "inplace"  # bench.CONFIGS["inception_bn"]["strategy"]
+SPLIT_TARGET = 32  # bench.CONFIGS["inception_bn"]["split_target"]
 ETA, MOM, WD = 0.05, 0.9, 1e-4
 
 
@@ -74,7 +75,7 @@ def _make_step(engine, lanes=None, monkeypatch=None):
     p0 = init_params(g, shapes, 0)
     kv = KVStore(1, 1, engine=engine)
     step = DataParallelStep(g, kv, given, p0, engine=engine, dense="bf16",
-                            strategy=STRATEGY)
+                            strategy=STRATEGY, split_target=SPLIT_TARGET)
     kv.set_updater(make_sgd_updater(SGDConfig(ETA, MOM, WD), scale=1))
     step.execs  # bind now (MGX_LANES is read at bind time)
     if lanes is not None:
