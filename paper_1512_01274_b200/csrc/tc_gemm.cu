@@ -219,6 +219,8 @@ __device__ __forceinline__ void cp_async16_zfill(uint32_t dst, const void* src, 
 // GM: 0 plain (both operands by TMA); 1 A gathered (K-major: forward /
 // data gradient of a convolution); 2 B gathered (MN-major: weight gradient)
 // GM 3: A (K-major) loaded by TMA in im2col mode -- no gather warps
+// GM 4: B (MN-major: weight gradient) loaded by TMA in im2col mode, one
+// 64-pixel x 64-channel box per 64 columns (tap, channel block)
 template <int GM>
 constexpr bool gathered() {
   return GM == 1 || GM == 2;
@@ -322,6 +324,31 @@ tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
           mbar_wait_sleep(&empty[s], ph ^ 1);
           uint8_t* sa = smem + s * G::kStageBytes;
           mbar_expect_tx(&full[s], GM == 1 ? G::kBBytes : GM == 2 ? G::kABytes : G::kStageBytes);
+          if (GM == 4) {
+            // B = im2col(x)[pixels (K), (tap, c) (N)]: the 64 pixels of this
+            // k-block -> their first output position; per 64-column chunk
+            // its (tap, channel block), clamped to the last chunk past N
+            // (columns never stored)
+            const int p0 = (kb0 + kb) * BK;
+            const int hw = ga.Ho * ga.Wo;
+            const int pn = p0 / hw, prem = p0 - pn * hw;
+            const int poh = prem / ga.Wo, pow_ = prem - (prem / ga.Wo) * ga.Wo;
+            const int piw = pow_ * ga.sw - ga.pw, pih = poh * ga.sh - ga.ph;
+#pragma unroll
+            for (int c = 0; c < BN / 64; ++c) {
+              const int col = min(n0 + c * 64, N - 64);
+              const int ctap = col / ga.C, ccb = col - ctap * ga.C;
+              const int ci = ctap / ga.kw, cj = ctap - ci * ga.kw;
+              asm volatile(
+                  "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::"
+                  "bytes [%0], [%1, {%2, %3, %4, %5}], [%6], {%7, %8};" ::"r"(
+                      smem_u32(sa + G::kABytes + c * kMnChunkBytes)),
+                  "l"(reinterpret_cast<uint64_t>(&map_b)), "r"(ccb), "r"(piw), "r"(pih), "r"(pn),
+                  "r"(smem_u32(&full[s])), "h"(static_cast<uint16_t>(cj)),
+                  "h"(static_cast<uint16_t>(ci))
+                  : "memory");
+            }
+          }
           if (GM == 3) {
             const int ti = tap / ga.kw, tj = tap - (tap / ga.kw) * ga.kw;
             asm volatile(
@@ -339,7 +366,7 @@ tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
           } else if (GM != 1) {
             load_operand<A_MN, BM>(sa, &map_a, &full[s], (kb0 + kb) * BK, m0);
           }
-          if (GM != 2)
+          if (GM != 2 && GM != 4)
             load_operand<B_MN, BN>(sa + G::kABytes, &map_b, &full[s], (kb0 + kb) * BK, n0);
         }
       }
@@ -823,7 +850,7 @@ static std::once_flag g_im2col_once;
 // convolution: each load gives 128 consecutive output pixels x 64 channels
 // of one filter tap (offsets in the instruction), zero in the padding
 static int encode_im2col(CUtensorMap* map, const void* src, int B, int H, int W, int C, int kh,
-                         int kw, int sh, int sw, int ph, int pw) {
+                         int kw, int sh, int sw, int ph, int pw, int pixels = BM) {
   std::call_once(g_im2col_once, [] {
     cudaDriverEntryPointQueryResult q;
     void* fn = nullptr;
@@ -842,7 +869,7 @@ static int encode_im2col(CUtensorMap* map, const void* src, int B, int H, int W,
   int upper[2] = {pw - (kw - 1), ph - (kh - 1)};
   cuuint32_t estr[4] = {1, cuuint32_t(sw), cuuint32_t(sh), 1};
   CUresult r = g_encode_im2col(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(src),
-                               dims, strides, lower, upper, BK, BM, estr,
+                               dims, strides, lower, upper, BK, pixels, estr,
                                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -963,6 +990,7 @@ static int launch_bn(int a_mn, int b_mn, int gm, const Launch& l, cudaStream_t s
   if (gm == 1) return launch_acts<false, false, BN, 1>(l, st);  // implicit A, B K-major
   if (gm == 3) return launch_acts<false, false, BN, 3>(l, st);  // A by TMA im2col, B K-major
   if (gm == 2) return launch_acts<true, true, BN, 2>(l, st);    // A MN-major, implicit B
+  if (gm == 4) return launch_acts<true, true, BN, 4>(l, st);    // A MN-major, B by TMA im2col
   if (!a_mn && !b_mn) return launch_acts<false, false, BN, 0>(l, st);
   if (!a_mn && b_mn) return launch_acts<false, true, BN, 0>(l, st);
   if (a_mn && !b_mn) return launch_acts<true, false, BN, 0>(l, st);
@@ -1040,12 +1068,13 @@ static int gemm_impl(const void* A, int64_t lda, int a_mn, const void* B, int64_
                      float* colstats, cudaStream_t st) {
   MGX_REQUIRE(C && M > 0 && N > 0 && K > 0, "mgx_gemm_bf16_tc: bad arguments");
   const bool a_impl = gm == 1 || gm == 3;  // A gathered / by TMA im2col
-  MGX_REQUIRE((a_impl || A) && (gm == 2 || B), "mgx_gemm_bf16_tc: missing operand");
-  MGX_REQUIRE((a_impl || lda % 8 == 0) && (gm == 2 || ldb % 8 == 0),
+  const bool b_impl = gm == 2 || gm == 4;  // B gathered / by TMA im2col
+  MGX_REQUIRE((a_impl || A) && (b_impl || B), "mgx_gemm_bf16_tc: missing operand");
+  MGX_REQUIRE((a_impl || lda % 8 == 0) && (b_impl || ldb % 8 == 0),
               "mgx_gemm_bf16_tc: leading dimensions must be multiples of 8");
-  MGX_REQUIRE((a_impl || lda >= (a_mn ? M : K)) && (gm == 2 || ldb >= (b_mn ? N : K)),
+  MGX_REQUIRE((a_impl || lda >= (a_mn ? M : K)) && (b_impl || ldb >= (b_mn ? N : K)),
               "mgx_gemm_bf16_tc: leading dimension smaller than the operand row");
-  MGX_REQUIRE((a_impl || mgx::aligned16(A)) && (gm == 2 || mgx::aligned16(B)),
+  MGX_REQUIRE((a_impl || mgx::aligned16(A)) && (b_impl || mgx::aligned16(B)),
               "mgx_gemm_bf16_tc: operands not 16-byte aligned");
   MGX_REQUIRE(M < (1ll << 31) && N < (1ll << 31) && K < (1ll << 31) && ldc < (1ll << 31),
               "mgx_gemm_bf16_tc: dimensions exceed 2^31");
@@ -1066,7 +1095,11 @@ static int gemm_impl(const void* A, int64_t lda, int a_mn, const void* B, int64_
                           ga.ph, ga.pw));
   else if (gm != 1)
     MGX_TRY(make_map(&l.ma, A, M, K, lda, a_mn != 0, BM));
-  if (gm != 2) MGX_TRY(make_map(&l.mb, B, N, K, ldb, b_mn != 0, bn));
+  if (gm == 4)
+    MGX_TRY(encode_im2col(&l.mb, ga.src, ga.B, ga.H, ga.W, ga.C, ga.kh, ga.kw, ga.sh, ga.sw,
+                          ga.ph, ga.pw, BK));
+  else if (gm != 2)
+    MGX_TRY(make_map(&l.mb, B, N, K, ldb, b_mn != 0, bn));
   float* out = splits == 1 ? C : workspace;
   const int64_t oldc = splits == 1 ? ldc : N;
   // TMA store needs a 16-byte row pitch and base; the map spans all splits
@@ -1213,10 +1246,19 @@ extern "C" int mgx_gemm_bf16_conv(int mode, const void* src, const int64_t* geom
     return gemm_impl(nullptr, 0, 0, op, ldop, 0, bias, C, ldc, M, N, K, act, splits, workspace,
                      use_tma ? 3 : 1, ga, colstats, mgx::as_stream(stream));
   }
-  // C[M, kconv] = op[pixels, M]^T (MN-major) . gather(src)[pixels, kconv]
+  // C[M, kconv] = op[pixels, M]^T (MN-major) . gather(src)[pixels, kconv];
+  // whole 64-channel blocks per tap: B by TMA im2col boxes of 64 pixels x 64
+  // channels (MN-major chunks) instead of the gather warps
   MGX_REQUIRE(K == pixels && N == kconv, "mgx_gemm_bf16_conv: N/K do not match the geometry");
-  return gemm_impl(op, ldop, 1, nullptr, 0, 1, bias, C, ldc, M, N, K, act, splits, workspace, 2,
-                   ga, colstats, mgx::as_stream(stream));
+  static const bool tma_dw = [] {
+    const char* v = getenv("MGX_TMA_IM2COL_DW");
+    return !(v && *v == '0');
+  }();
+  const bool use_tma = tma_dw && ga.C % BK == 0 && ga.ph <= 127 && ga.pw <= 127 &&
+                       ga.kh - 1 - ga.ph <= 128 && ga.kw - 1 - ga.pw <= 128 && ga.sh <= 8 &&
+                       ga.sw <= 8 && N >= 64;
+  return gemm_impl(op, ldop, 1, nullptr, 0, 1, bias, C, ldc, M, N, K, act, splits, workspace,
+                   use_tma ? 4 : 2, ga, colstats, mgx::as_stream(stream));
 }
 
 extern "C" int mgx_gemm_bf16_tc(const void* A, int64_t lda, const void* B, int64_t ldb,

@@ -76,6 +76,11 @@ CONV_CASES = [
     (2, 14, 14, 16, 24, (3, 3), (2, 2), (1, 1)),
     (2, 27, 27, 32, 16, (3, 3), (2, 2), (0, 0)),
     (2, 10, 11, 8, 16, (3, 3), (2, 2), (1, 1)),
+    # C % 64 == 0: forward A and weight-gradient B by TMA im2col (ragged
+    # pixel counts: the last 64-pixel k-block is partial)
+    (2, 9, 9, 64, 24, (3, 3), (1, 1), (1, 1)),
+    (2, 14, 13, 128, 80, (3, 3), (2, 2), (1, 1)),
+    (1, 7, 7, 64, 64, (1, 7), (1, 1), (0, 3)),
 ]
 
 
