@@ -402,7 +402,8 @@ def kernel_family(op: int) -> str:
             L.OP_COPY: "copy", L.OP_FILL: "fill", L.OP_EW: "elementwise", L.OP_AXPY: "axpy",
             L.OP_SCALAR: "scalar", L.OP_BN_ACT_POOL: "bn_act_pool (stem fwd)",
             L.OP_BN_BWD_REDUCE_POOL: "bn_bwd_reduce_pool (stem)",
-            L.OP_BN_BWD_DX_POOL: "bn_bwd_dx_pool (stem)", L.OP_PREP_BATCH: "prep_batch (weight casts)"})
+            L.OP_BN_BWD_DX_POOL: "bn_bwd_dx_pool (stem)", L.OP_PREP_BATCH: "prep_batch (weight casts)",
+            L.OP_KV_ROUND: "kv_round (fused reduce+SGD+broadcast)"})
     return KERNEL_OF.get(op, f"op{op}")
 
 

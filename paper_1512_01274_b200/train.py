@@ -196,9 +196,12 @@ class DataParallelStep:
                  and kv._native != L.KV_AGG)
         for w in self.workers:
             rounds = kv.embedded_rounds(w) if embed else []
+            # rounds that exchange over NVLink (several workers): issue the
+            # weight gradients early so the rounds overlap the backward
+            cross = bool(rounds) and kv.machines * kv.workers > 1
             self._execs[w] = bind(self.g, self.args[w], {n: "write" for n in self.names},
                                   self.grads[w], engine=self.engine, rounds=rounds,
-                                  **self._bind_opts)
+                                  hoist_wgrad=cross, **self._bind_opts)
             self.embedded = bool(rounds)
             if os.environ.get("MGX_PGO", "1") == "1":
                 # schedule the lanes on measured instruction times
