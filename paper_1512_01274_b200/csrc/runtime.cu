@@ -573,14 +573,9 @@ extern "C" int mgx_prog_set_schedule(uint64_t prog, int32_t nlanes, const int32_
   int lo_prio = 0, hi_prio = 0;
   MGX_CUDA(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
   for (int l = 0; l < nlanes; ++l) {
-    static const bool kv_prio = [] {
-      const char* v = getenv("MGX_KV_LANE_PRIO");
-      return v && *v == '1';
-    }();
-    const bool hi = (l == 1 && crit_lane) || (kv_prio && l == nlanes - 1 && nlanes > 2);
     if (l > 0)
       MGX_CUDA(cudaStreamCreateWithPriority(&p->side[l], cudaStreamNonBlocking,
-                                            hi ? hi_prio : lo_prio));
+                                            (l == 1 && crit_lane) ? hi_prio : lo_prio));
     MGX_CUDA(cudaEventCreateWithFlags(&p->join[l], cudaEventDisableTiming));
   }
   p->nlanes = nlanes;
