@@ -38,7 +38,8 @@ def main():
         args[n] = tmod.from_host(shapes[n], "float32", a0[n], engine=eng)
     grads = {n: tmod.zeros(shapes[n], engine=eng) for n in names}
     ex = bind(g, args, {n: "write" for n in names}, grads, engine=eng, dense=cfg["dense"],
-              use_graph=False)
+              use_graph=False, strategy=cfg.get("strategy", "both"),
+              split_target=cfg.get("split_target", 0))
     for _ in range(2):
         ex.forward()
         ex.backward()

@@ -85,7 +85,7 @@ def launches(raw, out):
         f[1] += us
     tot = sum(v[1] for v in per.values())
     with open(out, "w") as fh:
-        fh.write("# ncu launch list of `python bench.py --no-extra --steps 3 --warmup 3` "
+        fh.write("# ncu launch list of `python bench.py --no-extra --steps 2 --warmup 3 --kv-bytes 1048576` (tools/ncu_round.sh) "
                  "(Inception-BN, 1 B200)\n# gpu__time_duration.sum, --clock-control none; "
                  "cold-cache serialised launches: compare shares\n")
         fh.write(f"# total kernel time {tot / 1e3:.3f} ms over {sum(v[0] for v in per.values())}"
