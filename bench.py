@@ -47,7 +47,10 @@ CONFIGS = {
     "lenet": dict(batch=128, image=(28, 28, 1), classes=10, dense="bf16", dtype="bf16",
                   workload="config-3 LeNet (conv5x5x20-tanh-pool, conv5x5x50-tanh-pool, fc500, "
                            "fc10), synthetic 28x28x1, batch 128 per GPU, kvstore device"),
+    # hoist_wgrad: weight gradients issued as soon as their inputs exist
+    # (the chain's dW GEMMs overlap the dX chain: 2.42 -> 2.27 ms)
     "alexnet": dict(batch=128, image=(224, 224, 3), classes=1000, dense="bf16", dtype="bf16",
+                    hoist_wgrad=True,
                     workload="config-4 AlexNet-style (5 conv, fc6 4096x9216, fc7, fc8; 62M params), "
                              "synthetic 224x224x3, batch 128 per GPU, kvstore device"),
     # strategy "inplace": no co-shared slots between independent branches
@@ -427,7 +430,8 @@ def run_config(name, args, world, rank, local, eng, steps, warmup, with_e2e=True
     shapes, _ = symbol.infer_shape(g, given)
     step = DataParallelStep(g, kv, given, init_params(g, shapes, 0), engine=eng,
                             dense=cfg["dense"], strategy=cfg.get("strategy", "both"),
-                            split_target=cfg.get("split_target", 0))
+                            split_target=cfg.get("split_target", 0),
+                            hoist_wgrad=cfg.get("hoist_wgrad"))
     kv.set_updater(make_sgd_updater(SGDConfig(ETA, MOM, WD), scale=world))
     w = step.workers[0]
     feats, labels = synthetic(name, per * world, 0)

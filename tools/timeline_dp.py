@@ -42,7 +42,8 @@ def main():
     shapes, _ = symbol.infer_shape(g, given)
     step = DataParallelStep(g, kv, given, init_params(g, shapes, 0), engine=eng,
                             dense=cfg["dense"], strategy=cfg.get("strategy", "both"),
-                            split_target=cfg.get("split_target", 0))
+                            split_target=cfg.get("split_target", 0),
+                            hoist_wgrad=cfg.get("hoist_wgrad"))
     kv.set_updater(make_sgd_updater(SGDConfig(0.05, 0.9, 1e-4), scale=world))
     x, y = bench.synthetic(name, per, rank)
     step.load(step.workers[0], x, y)
