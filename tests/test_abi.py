@@ -60,3 +60,29 @@ def test_planner_core_runs_without_gpu():
                                  ctypes.byref(tot), ctypes.byref(vis))
     assert st == L.OK
     assert ns.value == 3 and tot.value == 16 and list(slot_of) == [0, 1, 2]
+
+
+def test_split_plan_without_gpu():
+    """mgx_gemm_split_plan: about `target` CTAs per GEMM, at least 16 and at
+    most 128 k-blocks per split (the fp32 accumulation-run bound), the
+    default target (0) = 128; the count never depends on anything but
+    (M, N, K, target) -- the lowering fixes it (tc_gemm.cu auto_splits)."""
+    def plan(m, n, k, target):
+        sp, ws = ctypes.c_int32(), ctypes.c_int64()
+        assert L.lib().mgx_gemm_split_plan(m, n, k, target, ctypes.byref(sp),
+                                           ctypes.byref(ws)) == L.OK
+        return sp.value, ws.value
+    # many tiles: no split
+    assert plan(50176, 256, 1152, 32) == (1, 0)
+    # the 14x14 weight gradient [192, 1728, 12544]: 2 x 9 tiles, 196 k-blocks
+    s32, ws32 = plan(192, 1728, 12544, 32)
+    s128, _ = plan(192, 1728, 12544, 0)
+    assert s32 < s128 and ws32 == s32 * 192 * 1728
+    nk = -(-12544 // 64)
+    for s in (s32, s128):
+        assert -(-nk // s) <= 128 and -(-nk // s) >= 16
+    # the stem weight gradient [64, 147, 802816]: one tile, 12544 k-blocks --
+    # the accumulation bound wins over any target
+    s, _ = plan(64, 147, 802816, 32)
+    assert -(-12544 // s) <= 128
+    assert L.lib().mgx_gemm_split_plan(0, 1, 1, 0, None, None) == L.BAD_ARGUMENT

@@ -63,3 +63,42 @@ def test_conv_attribute_errors():
     with pytest.raises(InferenceError):
         symbol.infer_shape(symbol.apply("Concat", {"dim": 1}, [data, data]),
                            {"data": (1, 4, 4, 2)})
+
+
+def test_weight_gradient_hoisting_keeps_a_topological_order():
+    """executor._hoist_weight_grads (DataParallelStep's hoist_wgrad): every
+    weight / bias gradient moves up to one node after its last input, the
+    result is still a topological order of the combined graph, and nothing
+    else changes order."""
+    from paper_1512_01274_b200.executor import (_gradient_request, _hoist_weight_grads,
+                                                launch_order, prune)
+    symbol.reset_names()
+    g = nets.inception_bn(1000)
+    given = {"data": (8, 224, 224, 3), "label": (8,)}
+    shapes, _ = symbol.infer_shape(g, given)
+    fg = prune(g, None)
+    names = param_names(fg)
+    wrt, grad_eps, head_pairs, combined = _gradient_request(fg, {n: "write" for n in names})
+    fnamed = symbol.infer_shape(fg, given)[1]
+    given2 = {a: shapes[a] for a in fg.list_arguments()}
+    given2.update((hv.name, fnamed[nd.name]) for hv, (nd, _s) in head_pairs)
+    topo = combined.topo_nodes()
+    index = {id(nd): i for i, nd in enumerate(topo)}
+    fids = {id(nd) for nd in fg.topo_nodes()}
+    phase = [int(nd.op is not None and id(nd) not in fids) for nd in topo]
+    plan = plan_memory(combined, given2, "inplace", phases=phase)
+    order = launch_order(topo, index, phase, plan.extra_dep_edges)
+    new = _hoist_weight_grads(order, topo, index, phase)
+    assert sorted(new) == sorted(order)
+    pos = {n: q for q, n in enumerate(new)}
+    for i in new:
+        for src, _ in topo[i].inputs:
+            if src.op is not None:
+                assert pos[index[id(src)]] < pos[i], (topo[i].name, src.name)
+    wg = [i for i in order if topo[i].op == "Backward"
+          and topo[i].attrs["of"] in ("Convolution", "FullyConnected")
+          and topo[i].attrs["slot"] in (1, 2)]
+    old = {n: q for q, n in enumerate(order)}
+    assert sum(pos[i] < old[i] for i in wg) > len(wg) // 2  # most move up
+    rest = [i for i in new if i not in set(wg)]
+    assert rest == [i for i in order if i not in set(wg)]
