@@ -698,6 +698,11 @@ def run_ours(args, world, rank, local):
     if rank == 0:
         cfg = CONFIGS[name]
         tensor_tflops = (flops_img * head["value"] / world / 1e12) if flops_img else None
+        if roof and tensor_tflops and roof.get("bound") == "tensor":
+            # the family's rate from isolated per-launch times understates a
+            # step whose GEMMs run side by side: also the step-level rate
+            roof = dict(roof, step_achieved=tensor_tflops,
+                        step_frac=tensor_tflops / roof["peak"])
         line = {
             "metric": METRIC, "value": head["value"], "unit": "images/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": head["ms_per_step"],
