@@ -219,6 +219,10 @@ __device__ __forceinline__ void cp_async16_zfill(uint32_t dst, const void* src, 
 // GM: 0 plain (both operands by TMA); 1 A gathered (K-major: forward /
 // data gradient of a convolution); 2 B gathered (MN-major: weight gradient)
 // GM 3: A (K-major) loaded by TMA in im2col mode -- no gather warps
+// GM 6: the weight gradient transposed (D[kconv, F] = im2col(x)^T . dY, its
+// tiles stored transposed into C[F, kconv]): A (MN-major) by TMA im2col,
+// B = dY (MN-major) by TMA -- for few filters F (the 128-row M tile would
+// be mostly padding in GM 4's orientation)
 // GM 4: B (MN-major: weight gradient) loaded by TMA in im2col mode, one
 // 64-pixel x 64-channel box per 64 columns (tap, channel block)
 template <int GM>
@@ -324,6 +328,28 @@ tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
           mbar_wait_sleep(&empty[s], ph ^ 1);
           uint8_t* sa = smem + s * G::kStageBytes;
           mbar_expect_tx(&full[s], GM == 1 ? G::kBBytes : GM == 2 ? G::kABytes : G::kStageBytes);
+          if (GM == 6) {
+            // A = im2col(x)[pixels (K), (tap, c) (M)], as GM 4's B
+            const int p0 = (kb0 + kb) * BK;
+            const int hw = ga.Ho * ga.Wo;
+            const int pn = p0 / hw, prem = p0 - pn * hw;
+            const int poh = prem / ga.Wo, pow_ = prem - (prem / ga.Wo) * ga.Wo;
+            const int piw = pow_ * ga.sw - ga.pw, pih = poh * ga.sh - ga.ph;
+#pragma unroll
+            for (int c = 0; c < BM / 64; ++c) {
+              const int col = min(m0 + c * 64, M - 64);
+              const int ctap = col / ga.C, ccb = col - ctap * ga.C;
+              const int ci = ctap / ga.kw, cj = ctap - ci * ga.kw;
+              asm volatile(
+                  "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::"
+                  "bytes [%0], [%1, {%2, %3, %4, %5}], [%6], {%7, %8};" ::"r"(
+                      smem_u32(sa + c * kMnChunkBytes)),
+                  "l"(reinterpret_cast<uint64_t>(&map_a)), "r"(ccb), "r"(piw), "r"(pih), "r"(pn),
+                  "r"(smem_u32(&full[s])), "h"(static_cast<uint16_t>(cj)),
+                  "h"(static_cast<uint16_t>(ci))
+                  : "memory");
+            }
+          }
           if (GM == 4) {
             // B = im2col(x)[pixels (K), (tap, c) (N)]: the 64 pixels of this
             // k-block -> their first output position; per 64-column chunk
@@ -363,7 +389,7 @@ tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
               cb = 0;
               ++tap;
             }
-          } else if (GM != 1) {
+          } else if (GM != 1 && GM != 6) {
             load_operand<A_MN, BM>(sa, &map_a, &full[s], (kb0 + kb) * BK, m0);
           }
           if (GM != 2 && GM != 4)
@@ -614,6 +640,9 @@ tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
         }
         if (use_tma_store) {
           if (row0 >= M) continue;  // warp-uniform: nothing of this box is in C
+          // transposed: this chunk's columns are rows of C; past N they would
+          // land in the next split's rows of the workspace (N % 32 == 0)
+          if (GM == 6 && n0 + c0 >= N) continue;
           uint8_t* buf = cbuf + nbuf * kStageCBytes;
           // the store that last read this buffer (NB chunks ago) is done
           if (lane == 0) {
@@ -623,15 +652,27 @@ tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
               asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
           }
           __syncwarp();
+          if (GM == 6) {
+            // transposed box: row j = column n0 + c0 + j of D, element lane
+            // = row row0 + lane (128-byte swizzle: 16-byte chunk ^ row & 7)
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            float4 q = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-            *reinterpret_cast<float4*>(buf + lane * 128 + ((j ^ (lane & 7)) << 4)) = q;
+            for (int j = 0; j < 32; ++j)
+              *reinterpret_cast<float*>(buf + j * 128 + ((((lane >> 2) ^ (j & 7)) << 4) |
+                                                         ((lane & 3) << 2))) = v[j];
+          } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              float4 q = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+              *reinterpret_cast<float4*>(buf + lane * 128 + ((j ^ (lane & 7)) << 4)) = q;
+            }
           }
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
           if (lane == 0) {
-            tma_store_2d(&map_c, buf, n0 + c0, int(int64_t(z) * M) + row0);
+            if (GM == 6)
+              tma_store_2d(&map_c, buf, row0, int(int64_t(z) * N) + n0 + c0);
+            else
+              tma_store_2d(&map_c, buf, n0 + c0, int(int64_t(z) * M) + row0);
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           }
           if (colstats) {
@@ -991,6 +1032,7 @@ static int launch_bn(int a_mn, int b_mn, int gm, const Launch& l, cudaStream_t s
   if (gm == 3) return launch_acts<false, false, BN, 3>(l, st);  // A by TMA im2col, B K-major
   if (gm == 2) return launch_acts<true, true, BN, 2>(l, st);    // A MN-major, implicit B
   if (gm == 4) return launch_acts<true, true, BN, 4>(l, st);    // A MN-major, B by TMA im2col
+  if (gm == 6) return launch_acts<true, true, BN, 6>(l, st);    // transposed weight gradient
   if (!a_mn && !b_mn) return launch_acts<false, false, BN, 0>(l, st);
   if (!a_mn && b_mn) return launch_acts<false, true, BN, 0>(l, st);
   if (a_mn && !b_mn) return launch_acts<true, false, BN, 0>(l, st);
@@ -1067,7 +1109,8 @@ static int gemm_impl(const void* A, int64_t lda, int a_mn, const void* B, int64_
                      int act, int splits, float* workspace, int gm, const Gather& ga,
                      float* colstats, cudaStream_t st) {
   MGX_REQUIRE(C && M > 0 && N > 0 && K > 0, "mgx_gemm_bf16_tc: bad arguments");
-  const bool a_impl = gm == 1 || gm == 3;  // A gathered / by TMA im2col
+  const bool a_impl = gm == 1 || gm == 3 || gm == 6;  // A gathered / by TMA im2col
+  const bool trans = gm == 6;  // D = C^T: C[N, ldc] holds the transposed tiles
   const bool b_impl = gm == 2 || gm == 4;  // B gathered / by TMA im2col
   MGX_REQUIRE((a_impl || A) && (b_impl || B), "mgx_gemm_bf16_tc: missing operand");
   MGX_REQUIRE((a_impl || lda % 8 == 0) && (b_impl || ldb % 8 == 0),
@@ -1093,6 +1136,9 @@ static int gemm_impl(const void* A, int64_t lda, int a_mn, const void* B, int64_
   if (gm == 3)
     MGX_TRY(encode_im2col(&l.ma, ga.src, ga.B, ga.H, ga.W, ga.C, ga.kh, ga.kw, ga.sh, ga.sw,
                           ga.ph, ga.pw));
+  else if (gm == 6)
+    MGX_TRY(encode_im2col(&l.ma, ga.src, ga.B, ga.H, ga.W, ga.C, ga.kh, ga.kw, ga.sh, ga.sw,
+                          ga.ph, ga.pw, BK));
   else if (gm != 1)
     MGX_TRY(make_map(&l.ma, A, M, K, lda, a_mn != 0, BM));
   if (gm == 4)
@@ -1101,13 +1147,16 @@ static int gemm_impl(const void* A, int64_t lda, int a_mn, const void* B, int64_
   else if (gm != 2)
     MGX_TRY(make_map(&l.mb, B, N, K, ldb, b_mn != 0, bn));
   float* out = splits == 1 ? C : workspace;
-  const int64_t oldc = splits == 1 ? ldc : N;
+  // the stored matrix: M x N, or N x M for the transposed weight gradient
+  const int64_t orows = trans ? N : M, ocols = trans ? M : N;
+  const int64_t oldc = splits == 1 ? ldc : ocols;
   // TMA store needs a 16-byte row pitch and base; the map spans all splits
   // (partial 32-row boxes of a split would spill into the next split's rows)
-  l.tma = (oldc % 4 == 0) && mgx::aligned16(out) && (splits == 1 || M % 32 == 0);
+  l.tma = (oldc % 4 == 0) && mgx::aligned16(out) && (splits == 1 || orows % 32 == 0);
+  MGX_REQUIRE(l.tma || !trans, "mgx_gemm_bf16_tc: the transposed form needs a TMA store");
   if (l.tma)
-    MGX_TRY(mgx::tc::encode(&l.mc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, out, N, int64_t(splits) * M,
-                            oldc * 4, 32, 32));
+    MGX_TRY(mgx::tc::encode(&l.mc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, out, ocols,
+                            int64_t(splits) * orows, oldc * 4, 32, 32));
   l.sc = Sched{static_cast<int>(m_tiles), static_cast<int>(n_tiles), splits, kps,
                static_cast<int>(nk), static_cast<int>(K)};
   const int64_t total = m_tiles * n_tiles * splits;
@@ -1136,7 +1185,8 @@ static int gemm_impl(const void* A, int64_t lda, int a_mn, const void* B, int64_
            : bn == 192 ? launch_bn<192>(a_mn, b_mn, gm, l, st)
                        : launch_bn<256>(a_mn, b_mn, gm, l, st);
   if (rc != MGX_OK || splits == 1) return rc;
-  if (N % 4 == 0 && ldc % 4 == 0 && l.sstride % 4 == 0 && mgx::aligned16(C) &&
+  MGX_REQUIRE(!trans || !bias, "mgx_gemm_bf16_tc: the transposed form takes no bias");
+  if (ocols % 4 == 0 && ldc % 4 == 0 && l.sstride % 4 == 0 && mgx::aligned16(C) &&
       mgx::aligned16(workspace) && (!bias || mgx::aligned16(bias))) {
     // split lanes: enough to put ~4 split loads per thread in flight
     int SL = 1;
@@ -1146,14 +1196,15 @@ static int gemm_impl(const void* A, int64_t lda, int a_mn, const void* B, int64_
     if (blocks > 148 * 8) blocks = 148 * 8;
     splitk_reduce4_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(
         reinterpret_cast<const float4*>(workspace), splits, l.sstride / 4, bias,
-        reinterpret_cast<float4*>(C), ldc / 4, M, N / 4, act, SL);
+        reinterpret_cast<float4*>(C), ldc / 4, orows, ocols / 4, act, SL);
     MGX_LAUNCHED();
     return MGX_OK;
   }
   int64_t blocks = mgx::ceil_div(M * N, 256);
   if (blocks > 148 * 8) blocks = 148 * 8;
   splitk_reduce_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(workspace, splits, l.sstride,
-                                                                      bias, C, ldc, M, N, act);
+                                                                      bias, C, ldc, orows, ocols,
+                                                                      act);
   MGX_LAUNCHED();
   return MGX_OK;
 }
@@ -1257,6 +1308,24 @@ extern "C" int mgx_gemm_bf16_conv(int mode, const void* src, const int64_t* geom
   const bool use_tma = tma_dw && ga.C % BK == 0 && ga.ph <= 127 && ga.pw <= 127 &&
                        ga.kh - 1 - ga.ph <= 128 && ga.kw - 1 - ga.pw <= 128 && ga.sh <= 8 &&
                        ga.sw <= 8 && N >= 64;
+  // few filters: the transposed product D[kconv, F] fills the 128-row M
+  // tiles better (e.g. F = 160: 62 % of the M tile used, transposed 83 %);
+  // its tiles are stored transposed (GEMM mode 6; env MGX_DW_SWAP=0: off)
+  static const bool dw_swap = [] {
+    const char* v = getenv("MGX_DW_SWAP");
+    return !(v && *v == '0');
+  }();
+  if (use_tma && dw_swap && !bias && !colstats && M % 32 == 0 && N % 4 == 0 && ldc % 4 == 0 &&
+      mgx::aligned16(C) && (!workspace || mgx::aligned16(workspace))) {
+    auto fill = [](int64_t m, int64_t n) {
+      const int64_t bn = pick_bn(m, n);
+      return double(m) / double(mgx::ceil_div(m, int64_t(BM)) * BM) * double(n) /
+             double(mgx::ceil_div(n, bn) * bn);
+    };
+    if (fill(N, M) > 1.1 * fill(M, N))
+      return gemm_impl(nullptr, 0, 1, op, ldop, 1, nullptr, C, ldc, N, M, K, act, splits,
+                       workspace, 6, ga, nullptr, mgx::as_stream(stream));
+  }
   return gemm_impl(op, ldop, 1, nullptr, 0, 1, bias, C, ldc, M, N, K, act, splits, workspace,
                    use_tma ? 4 : 2, ga, colstats, mgx::as_stream(stream));
 }

@@ -81,6 +81,8 @@ CONV_CASES = [
     (2, 9, 9, 64, 24, (3, 3), (1, 1), (1, 1)),
     (2, 14, 13, 128, 80, (3, 3), (2, 2), (1, 1)),
     (1, 7, 7, 64, 64, (1, 7), (1, 1), (0, 3)),
+    # few filters: the weight gradient computed transposed (GEMM mode 6)
+    (2, 10, 10, 64, 160, (3, 3), (1, 1), (1, 1)),
 ]
 
 
