@@ -223,11 +223,13 @@ __device__ __forceinline__ void cp_async16_zfill(uint32_t dst, const void* src, 
 // tiles stored transposed into C[F, kconv]): A (MN-major) by TMA im2col,
 // B = dY (MN-major) by TMA -- for few filters F (the 128-row M tile would
 // be mostly padding in GM 4's orientation)
+// GM 7: GM 6 with the im2col operand gathered by the cp.async warps (C %
+// 64 != 0)
 // GM 4: B (MN-major: weight gradient) loaded by TMA in im2col mode, one
 // 64-pixel x 64-channel box per 64 columns (tap, channel block)
 template <int GM>
 constexpr bool gathered() {
-  return GM == 1 || GM == 2;
+  return GM == 1 || GM == 2 || GM == 7;
 }
 // block: TMA producer warp, MMA warp, EPI epilogue warps (4, or 8 with the
 // columns of a tile split between two warps per TMEM lane quadrant), then
@@ -327,7 +329,9 @@ tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
           const uint32_t ph = (it / G::kStages) & 1;
           mbar_wait_sleep(&empty[s], ph ^ 1);
           uint8_t* sa = smem + s * G::kStageBytes;
-          mbar_expect_tx(&full[s], GM == 1 ? G::kBBytes : GM == 2 ? G::kABytes : G::kStageBytes);
+          mbar_expect_tx(&full[s], (GM == 1 || GM == 7) ? G::kBBytes
+                                   : GM == 2              ? G::kABytes
+                                                          : G::kStageBytes);
           if (GM == 6) {
             // A = im2col(x)[pixels (K), (tap, c) (M)], as GM 4's B
             const int p0 = (kb0 + kb) * BK;
@@ -389,7 +393,7 @@ tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
               cb = 0;
               ++tap;
             }
-          } else if (GM != 1 && GM != 6) {
+          } else if (GM != 1 && GM != 6 && GM != 7) {
             load_operand<A_MN, BM>(sa, &map_a, &full[s], (kb0 + kb) * BK, m0);
           }
           if (GM != 2 && GM != 4)
@@ -525,14 +529,16 @@ tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
         // B tile (MN-major): 64 K rows (pixels) x BN columns in 64-column
         // groups of 128-byte rows; lanes cover the 8 chunks of a row; thread
         // (q = g & 7, r0 = g >> 3) owns rows r0 + 16*i (i < 4) of every group
+        // (GM 7: the A tile, BM columns from m0)
         const int q = g & 7, r0 = g >> 3;
-        constexpr int NG = BN / 64;
+        constexpr int NG = (GM == 7 ? BM : BN) / 64;
+        const int col0 = GM == 7 ? m0 : n0, ncol = GM == 7 ? M : N;
         int gi[NG], gj[NG], gc[NG];
 #pragma unroll
         for (int cg = 0; cg < NG; ++cg) {
-          const int n = n0 + cg * 64 + q * 8;
+          const int n = col0 + cg * 64 + q * 8;
           const int tap = n / ga.C;
-          gc[cg] = n < N ? n - tap * ga.C : -1;
+          gc[cg] = n < ncol ? n - tap * ga.C : -1;
           gi[cg] = tap / ga.kw;
           gj[cg] = tap - gi[cg] * ga.kw;
         }
@@ -541,7 +547,8 @@ tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
           const int s = it % G::kStages;
           const uint32_t ph = (it / G::kStages) & 1;
           mbar_wait_sleep(&empty[s], ph ^ 1);
-          const uint32_t tile = smem_u32(smem + s * G::kStageBytes + G::kABytes);
+          const uint32_t tile =
+              smem_u32(smem + s * G::kStageBytes + (GM == 7 ? 0 : G::kABytes));
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             const int kr = r0 + 16 * i;
@@ -642,7 +649,7 @@ tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
           if (row0 >= M) continue;  // warp-uniform: nothing of this box is in C
           // transposed: this chunk's columns are rows of C; past N they would
           // land in the next split's rows of the workspace (N % 32 == 0)
-          if (GM == 6 && n0 + c0 >= N) continue;
+          if ((GM == 6 || GM == 7) && n0 + c0 >= N) continue;
           uint8_t* buf = cbuf + nbuf * kStageCBytes;
           // the store that last read this buffer (NB chunks ago) is done
           if (lane == 0) {
@@ -652,7 +659,7 @@ tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
               asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
           }
           __syncwarp();
-          if (GM == 6) {
+          if (GM == 6 || GM == 7) {
             // transposed box: row j = column n0 + c0 + j of D, element lane
             // = row row0 + lane (128-byte swizzle: 16-byte chunk ^ row & 7)
 #pragma unroll
@@ -669,7 +676,7 @@ tc_gemm_bf16_kernel(const __grid_constant__ CUtensorMap map_a,
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncwarp();
           if (lane == 0) {
-            if (GM == 6)
+            if (GM == 6 || GM == 7)
               tma_store_2d(&map_c, buf, row0, int(int64_t(z) * N) + n0 + c0);
             else
               tma_store_2d(&map_c, buf, n0 + c0, int(int64_t(z) * M) + row0);
@@ -1033,6 +1040,7 @@ static int launch_bn(int a_mn, int b_mn, int gm, const Launch& l, cudaStream_t s
   if (gm == 2) return launch_acts<true, true, BN, 2>(l, st);    // A MN-major, implicit B
   if (gm == 4) return launch_acts<true, true, BN, 4>(l, st);    // A MN-major, B by TMA im2col
   if (gm == 6) return launch_acts<true, true, BN, 6>(l, st);    // transposed weight gradient
+  if (gm == 7) return launch_acts<true, true, BN, 7>(l, st);    // ... its A gathered
   if (!a_mn && !b_mn) return launch_acts<false, false, BN, 0>(l, st);
   if (!a_mn && b_mn) return launch_acts<false, true, BN, 0>(l, st);
   if (a_mn && !b_mn) return launch_acts<true, false, BN, 0>(l, st);
@@ -1109,8 +1117,8 @@ static int gemm_impl(const void* A, int64_t lda, int a_mn, const void* B, int64_
                      int act, int splits, float* workspace, int gm, const Gather& ga,
                      float* colstats, cudaStream_t st) {
   MGX_REQUIRE(C && M > 0 && N > 0 && K > 0, "mgx_gemm_bf16_tc: bad arguments");
-  const bool a_impl = gm == 1 || gm == 3 || gm == 6;  // A gathered / by TMA im2col
-  const bool trans = gm == 6;  // D = C^T: C[N, ldc] holds the transposed tiles
+  const bool a_impl = gm == 1 || gm == 3 || gm == 6 || gm == 7;  // A gathered / TMA im2col
+  const bool trans = gm == 6 || gm == 7;  // D = C^T: C[N, ldc] holds the transposed tiles
   const bool b_impl = gm == 2 || gm == 4;  // B gathered / by TMA im2col
   MGX_REQUIRE((a_impl || A) && (b_impl || B), "mgx_gemm_bf16_tc: missing operand");
   MGX_REQUIRE((a_impl || lda % 8 == 0) && (b_impl || ldb % 8 == 0),
@@ -1139,7 +1147,7 @@ static int gemm_impl(const void* A, int64_t lda, int a_mn, const void* B, int64_
   else if (gm == 6)
     MGX_TRY(encode_im2col(&l.ma, ga.src, ga.B, ga.H, ga.W, ga.C, ga.kh, ga.kw, ga.sh, ga.sw,
                           ga.ph, ga.pw, BK));
-  else if (gm != 1)
+  else if (gm != 1 && gm != 7)
     MGX_TRY(make_map(&l.ma, A, M, K, lda, a_mn != 0, BM));
   if (gm == 4)
     MGX_TRY(encode_im2col(&l.mb, ga.src, ga.B, ga.H, ga.W, ga.C, ga.kh, ga.kw, ga.sh, ga.sw,
@@ -1315,7 +1323,7 @@ extern "C" int mgx_gemm_bf16_conv(int mode, const void* src, const int64_t* geom
     const char* v = getenv("MGX_DW_SWAP");
     return !(v && *v == '0');
   }();
-  if (use_tma && dw_swap && !bias && !colstats && M % 32 == 0 && N % 4 == 0 && ldc % 4 == 0 &&
+  if (dw_swap && !bias && !colstats && M % 32 == 0 && N % 4 == 0 && N >= 64 && ldc % 4 == 0 &&
       mgx::aligned16(C) && (!workspace || mgx::aligned16(workspace))) {
     auto fill = [](int64_t m, int64_t n) {
       const int64_t bn = pick_bn(m, n);
@@ -1324,7 +1332,7 @@ extern "C" int mgx_gemm_bf16_conv(int mode, const void* src, const int64_t* geom
     };
     if (fill(N, M) > 1.1 * fill(M, N))
       return gemm_impl(nullptr, 0, 1, op, ldop, 1, nullptr, C, ldc, N, M, K, act, splits,
-                       workspace, 6, ga, nullptr, mgx::as_stream(stream));
+                       workspace, use_tma ? 6 : 7, ga, nullptr, mgx::as_stream(stream));
   }
   return gemm_impl(op, ldop, 1, nullptr, 0, 1, bias, C, ldc, M, N, K, act, splits, workspace,
                    use_tma ? 4 : 2, ga, colstats, mgx::as_stream(stream));

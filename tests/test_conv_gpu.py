@@ -83,6 +83,7 @@ CONV_CASES = [
     (1, 7, 7, 64, 64, (1, 7), (1, 1), (0, 3)),
     # few filters: the weight gradient computed transposed (GEMM mode 6)
     (2, 10, 10, 64, 160, (3, 3), (1, 1), (1, 1)),
+    (2, 10, 10, 32, 160, (3, 3), (1, 1), (1, 1)),  # ... its A operand gathered (mode 7)
 ]
 
 
