@@ -18,6 +18,7 @@
 // (row chunks -> fixed-order merge), so results are run-to-run
 // deterministic.
 
+#include <cooperative_groups.h>
 #include <cuda_bf16.h>
 
 #include "common.cuh"
@@ -874,6 +875,79 @@ bn_stats_from_tiles_kernel(const float2* __restrict__ part, int64_t M, int C, fl
     if (mmean) mmean[c] = static_cast<float>(double(mmean[c]) * momentum + mean * (1.0 - momentum));
     if (mvar) mvar[c] = static_cast<float>(double(mvar[c]) * momentum + var * (1.0 - momentum));
   }
+}
+
+// The same statistics with coalesced reads over more SMs: a cluster of CS
+// CTAs per 32-channel group, the row blocks split contiguously over the
+// cluster's CTAs; in a CTA lane = channel (each warp load is 256 contiguous
+// bytes of one row block) and warp w takes blocks w, w + 32, ... in order;
+// warp sums merged in warp order, then the CS CTA sums in rank order over
+// distributed shared memory by rank 0 (deterministic).  The per-block
+// terms are bn_stats_from_tiles_kernel's (shift = tile 0's mean).
+template <int CS>
+__global__ void __launch_bounds__(1024)
+bn_stats_tiles_cluster_kernel(const float2* __restrict__ part, int64_t M, int C, float eps,
+                              float momentum, float* __restrict__ stats,
+                              float* __restrict__ mmean, float* __restrict__ mvar) {
+  namespace cg = cooperative_groups;
+  __shared__ double red[2][32][33];
+  __shared__ double tot[2][32];
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = static_cast<int>(cl.block_rank());
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = blockIdx.y * 32 + lane;
+  const bool cv = c < C;
+  const int64_t nb = (M + 31) / 32;
+  const double sh = cv ? double(part[c].x) : 0.0;
+  const int64_t per = (nb + CS - 1) / CS;
+  const int64_t b_lo = rank * per, b_hi = b_lo + per < nb ? b_lo + per : nb;
+  double s1 = 0.0, s2 = 0.0;
+  constexpr int U = 8;
+  for (int64_t b0 = b_lo + warp; b0 < b_hi; b0 += 32 * U) {
+    float2 p[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t b = b0 + 32 * u;
+      p[u] = (cv && b < b_hi) ? part[b * C + c] : make_float2(0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t b = b0 + 32 * u;
+      if (!cv || b >= b_hi) continue;
+      const int64_t left = M - b * 32;
+      const double n = double(left < 32 ? left : 32);
+      const double d = double(p[u].x) - sh;
+      s1 += n * d;
+      s2 += double(p[u].y) + n * d * d;
+    }
+  }
+  red[0][warp][lane] = s1;
+  red[1][warp][lane] = s2;
+  __syncthreads();
+  if (threadIdx.x < 64) {
+    const int k = threadIdx.x >> 5, ch = threadIdx.x & 31;
+    double a = 0.0;
+    for (int w = 0; w < 32; ++w) a += red[k][w][ch];
+    tot[k][ch] = a;
+  }
+  cl.sync();
+  if (rank == 0 && threadIdx.x < 32 && cv) {
+    double a1 = 0.0, a2 = 0.0;
+    for (int r = 0; r < CS; ++r) {
+      const double* t = cl.map_shared_rank(&tot[0][0], r);
+      a1 += t[lane];
+      a2 += t[32 + lane];
+    }
+    const double dm = a1 / double(M);
+    const double mean = sh + dm;
+    double var = a2 / double(M) - dm * dm;
+    if (var < 0.0) var = 0.0;
+    stats[c] = static_cast<float>(mean);
+    stats[C + c] = static_cast<float>(1.0 / sqrt(var + double(eps)));
+    if (mmean) mmean[c] = static_cast<float>(double(mmean[c]) * momentum + mean * (1.0 - momentum));
+    if (mvar) mvar[c] = static_cast<float>(double(mvar[c]) * momentum + var * (1.0 - momentum));
+  }
+  cl.sync();  // peers' tot stays alive until rank 0 has read it
 }
 
 // ---- stem fusion, backward reductions over the pooling WINDOWS: only the
@@ -2293,6 +2367,37 @@ extern "C" int mgx_bn_stats_from_tiles(const void* part, int64_t M, int64_t C, f
                                        float* moving_mean, float* moving_var, float eps,
                                        float momentum, uintptr_t stream) {
   MGX_REQUIRE(part && stats && M > 0 && C > 0, "mgx_bn_stats_from_tiles: bad arguments");
+  // many row blocks (the stem's 112x112 / 56x56 maps): the cluster kernel
+  // (coalesced 32-channel rows over 16 CTAs per channel group); else one
+  // block per channel (env MGX_BN_STATS_CLUSTER=0: always the latter)
+  static const bool cluster = [] {
+    const char* v = getenv("MGX_BN_STATS_CLUSTER");
+    return !(v && *v == '0');
+  }();
+  if (cluster && M >= (int64_t(1) << 16)) {
+    constexpr int CS = 16;
+    static bool attrs = false;
+    if (!attrs) {
+      MGX_CUDA(cudaFuncSetAttribute(mgx::conv::bn_stats_tiles_cluster_kernel<CS>,
+                                    cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      attrs = true;
+    }
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(CS, static_cast<unsigned>(mgx::ceil_div(C, int64_t(32))), 1);
+    lc.blockDim = dim3(1024, 1, 1);
+    lc.stream = mgx::as_stream(stream);
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CS;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    MGX_CUDA(cudaLaunchKernelEx(&lc, mgx::conv::bn_stats_tiles_cluster_kernel<CS>,
+                                static_cast<const float2*>(part), M, static_cast<int>(C), eps,
+                                momentum, stats, moving_mean, moving_var));
+    return MGX_OK;
+  }
   mgx::conv::bn_stats_from_tiles_kernel<<<static_cast<unsigned>(C), 1024, 0, mgx::as_stream(stream)>>>(
       static_cast<const float2*>(part), M, static_cast<int>(C), eps, momentum, stats, moving_mean,
       moving_var);

@@ -634,3 +634,36 @@ def test_conv_eager_forward(cuda, engine, case):
     kk = k[0] * k[1] * c
     torch.testing.assert_close(y.double().cpu(), ref, rtol=1e-4,
                                atol=1e-4 * max(1.0, (kk / 64) ** 0.5) * 8)
+
+
+@pytest.mark.parametrize("m,c", [(65536 + 7, 40), (200704, 64), (1000, 24)])
+def test_bn_stats_from_tiles(cuda, m, c):
+    """BatchNorm statistics merged from per-32-row (mean, M2) pairs -- the
+    cluster kernel from 65536 rows (coalesced 32-channel rows, 16 CTAs per
+    channel group; ragged channel groups and row blocks), the per-channel
+    block below -- against float64 over the rows, moving averages too."""
+    torch = cuda
+    from paper_1512_01274_b200 import _lib as L
+    g = torch.Generator().manual_seed(m + c)
+    x = (torch.randn(m, c, generator=g, dtype=torch.float64) * 3 + 1.5)
+    nb = -(-m // 32)
+    pad = torch.zeros(nb * 32, c, dtype=torch.float64)
+    pad[:m] = x
+    blocks = pad.reshape(nb, 32, c)
+    cnt = torch.full((nb, 1), 32.0, dtype=torch.float64)
+    cnt[-1] = m - (nb - 1) * 32
+    mean_b = blocks.sum(1) / cnt
+    dev = blocks - mean_b[:, None, :]
+    mask = (torch.arange(32)[None, :, None] < cnt[:, :, None])
+    m2_b = (dev * dev * mask).sum(1)
+    part = torch.stack([mean_b, m2_b], dim=-1).float().cuda().contiguous()
+    st = torch.empty(2 * c, device="cuda")
+    mm, mv = torch.zeros(c, device="cuda"), torch.ones(c, device="cuda")
+    L.call("mgx_bn_stats_from_tiles", part.data_ptr(), m, c, st.data_ptr(), mm.data_ptr(),
+           mv.data_ptr(), 1e-3, 0.9, 0)
+    torch.cuda.synchronize()
+    mean, var = x.mean(0), x.var(0, unbiased=False)
+    np.testing.assert_allclose(st[:c].cpu().numpy(), mean.numpy(), rtol=1e-5, atol=1e-6)
+    np.testing.assert_allclose(st[c:].cpu().numpy(), (1 / (var + 1e-3).sqrt()).numpy(),
+                               rtol=1e-5)
+    np.testing.assert_allclose(mv.cpu().numpy(), (0.9 + 0.1 * var).numpy(), rtol=1e-5)
