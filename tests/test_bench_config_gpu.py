@@ -34,7 +34,7 @@ biases in front of a BatchNorm have an exactly-zero gradient; the device's
 fp32 noise there is bounded absolutely (<= 1e-6).  Post-step weights are
 checked bitwise against the a10 SGD sequence applied to the device's own
 gradient (the KV round's arithmetic), and bitwise: captured replay == eager,
-6 lanes == 1 lane, at full size.
+8 lanes (the default) == 1 lane, at full size.
 """
 
 import numpy as np
@@ -168,7 +168,7 @@ def test_bench_config_step_matches_oracle(engine, oracle_step):
 
 
 def test_bench_config_replay_and_lanes_bitwise(engine, monkeypatch):
-    """Two steps three ways at full size: eager (6 lanes), eager + the
+    """Two steps three ways at full size: eager (the default lanes), eager + the
     captured whole-step graph replay (what bench.py times), and eager with
     one lane.  Weights, momentum-carrying second-step weights, gradients,
     BatchNorm statistics and softmax outputs are bitwise identical."""
