@@ -55,11 +55,11 @@ CONFIGS = {
                              "synthetic 224x224x3, batch 128 per GPU, kvstore device"),
     # strategy "inplace": no co-shared slots between independent branches
     # (their reuse adds write-after-read edges across lanes: 5.24 -> 5.19 ms);
-    # split_target 32: split-K sized for ~32 CTAs per GEMM, the inception
-    # branches run side by side (4.83 -> 4.67 ms; a chain like AlexNet keeps
-    # the default 128)
+    # split_target 20: split-K sized for ~20 CTAs per GEMM, the inception
+    # branches run side by side (128 -> 32: 4.83 -> 4.67 ms; with 8 lanes
+    # 32 -> 20: 4.60 -> 4.51 ms; a chain like AlexNet keeps the default 128)
     "inception_bn": dict(batch=64, image=(224, 224, 3), classes=1000, dense="bf16", dtype="bf16",
-                         strategy="inplace", split_target=32,
+                         strategy="inplace", split_target=20,
                          workload="config-5 Inception-BN (MXNet symbol, 69 conv+BN+ReLU, 10 "
                                   "inception concats), synthetic 224x224x3, batch 64 per GPU, bf16 "
                                   "tensor-core convs, momentum SGD, kvstore device"),

@@ -2,7 +2,7 @@
 
 bench.py (default ``--config inception_bn``) builds ``nets.inception_bn(1000)``
 at 224x224x3, batch 64 per GPU, ``dense="bf16"``, memory plan strategy
-"inplace", split-K target 32, the default 6-lane schedule, wraps it in ``DataParallelStep`` over a device ``KVStore`` with the
+"inplace", split-K target 20, the default 6-lane schedule, wraps it in ``DataParallelStep`` over a device ``KVStore`` with the
 fused SGD updater (lr 0.05, momentum 0.9, wd 1e-4) and replays the whole step
 (forward, backward, KV round) from one CUDA graph.  These tests bind exactly
 that -- same graph, batch, dense mode, lanes, synthetic data and seeds -- so
@@ -49,7 +49,7 @@ PER = 64
 IMAGE = (224, 224, 3)
 CLASSES = 1000
 STRATEGY = "inplace"  # bench.CONFIGS["inception_bn"]["strategy"]
-SPLIT_TARGET = 32  # bench.CONFIGS["inception_bn"]["split_target"]
+SPLIT_TARGET = 20  # bench.CONFIGS["inception_bn"]["split_target"]
 ETA, MOM, WD = 0.05, 0.9, 1e-4
 
 

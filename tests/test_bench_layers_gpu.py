@@ -75,7 +75,7 @@ def test_bench_conv_geometry(engine, geom):
     grads = {n: tmod.zeros(tuple(shapes[n]), engine=engine) for n in ("data", "conv_weight", "conv_bias")}
     torch.cuda.synchronize()
     ex = bind(net, args, {n: "write" for n in grads}, grads, engine=engine, dense="bf16",
-              split_target=32)  # bench.CONFIGS["inception_bn"]["split_target"]
+              split_target=20)  # bench.CONFIGS["inception_bn"]["split_target"]
     ex.forward()
     ex.backward()
     engine.wait_all()
