@@ -344,6 +344,9 @@ def run_reference(args, world, rank):
     and KVStore timings (``reference_own``)."""
     if rank != 0:
         return
+    import torch
+    # torchrun sets OMP_NUM_THREADS=1 per rank: the CPU arm uses every host core
+    torch.set_num_threads(os.cpu_count() or 1)
     n = args.gpus
     name = args.config
     kind = "port"
